@@ -1,0 +1,266 @@
+/*
+ * mpg.h — C ABI of the B200-native shifted-solve engine (libmpg.so).
+ *
+ * Drop-in boundary for the reference `morprec` solve path
+ * (/root/reference/proj/include/morprec). Every entry point below names the
+ * reference interface it replaces. Plain pointers and sizes only; no torch or
+ * Eigen types. Vector arguments documented as "any memory" may point to host
+ * (pageable or pinned) or device memory of the handle's device: the library
+ * resolves them through unified addressing and copies as needed.
+ *
+ * Threading: handles are immutable after creation (as SparseMatrix and
+ * PrecondChain are, proj/include/morprec/sparse.hpp:29-32, chain.hpp:50-54)
+ * and may be shared between host threads; each call is synchronous with
+ * respect to the host and runs on the library's stream for the handle's
+ * device (mpg_stream()).
+ *
+ * Errors: every int-returning call returns MPG_OK or one of the codes below;
+ * mpg_last_error() gives the thread's last message. The reference raises
+ * std::invalid_argument / ConfigError / SolverError
+ * (proj/include/morprec/errors.hpp:12-28); GMRES non-convergence and
+ * breakdown are report flags, not errors (proj/include/morprec/gmres.hpp:41-48).
+ */
+#ifndef MPG_H_
+#define MPG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPG_OK 0
+#define MPG_ERR_INVALID 1 /* std::invalid_argument */
+#define MPG_ERR_CONFIG 2  /* morprec::ConfigError  (CLI exit 2) */
+#define MPG_ERR_SOLVER 3  /* morprec::SolverError  (CLI exit 3) */
+#define MPG_ERR_LOGIC 4   /* std::logic_error, other */
+#define MPG_ERR_CUDA 5    /* CUDA runtime failure / no device */
+#define MPG_ERR_NOMEM 6   /* device allocation failed */
+
+/* PrecondMode (proj/include/morprec/chain.hpp:21) + one extension. */
+#define MPG_PRECOND_NONE 0
+#define MPG_PRECOND_FRESH 1
+#define MPG_PRECOND_REUSE_CHAIN 2
+#define MPG_PRECOND_REUSE_FROZEN 3 /* build once at the first shift, apply unchanged afterwards */
+
+/* PrecondKind (proj/include/morprec/report.hpp:14-20). */
+#define MPG_KIND_NONE 0
+#define MPG_KIND_FRESH 1
+#define MPG_KIND_HORIZONTAL 2
+#define MPG_KIND_VERTICAL 3
+#define MPG_KIND_REUSED_SAME_MATRIX 4
+
+typedef struct mpg_csr mpg_csr;     /* device CSR matrix (int32 indices, fp64 values) */
+typedef struct mpg_op mpg_op;       /* shifted operator family sigma*E - A on one device */
+typedef struct mpg_chain mpg_chain; /* immutable preconditioner chain P, Q_1..Q_L */
+
+/* SpaiConfig (proj/include/morprec/spai.hpp:25-33); pattern_kind 0 = Diagonal,
+ * 1 = PatternOfA (default). */
+typedef struct {
+  int pattern_kind, power;
+  double fill_tol;
+  int max_fill_per_col, max_pattern_sweeps, threads;
+} mpg_spai_cfg;
+
+/* GmresConfig (proj/include/morprec/gmres.hpp:20-24). */
+typedef struct {
+  double rel_tol;
+  int max_iter, record_history;
+} mpg_gmres_cfg;
+
+/* GmresReport (proj/include/morprec/gmres.hpp:26-34); the residual history,
+ * when recorded, is returned through a separate array. */
+typedef struct {
+  int iterations, converged, breakdown, history_len;
+  double rhs_norm, final_residual, solve_seconds;
+} mpg_gmres_report;
+
+/* BirkaConfig (proj/include/morprec/birka.hpp:49-61) for N = 0; decoupled = 1
+ * solves one GMRES per shift unit (the GPU path always does). */
+typedef struct {
+  int r;
+  double tol;
+  int max_sweeps;
+  int decoupled;
+  unsigned long long seed;
+  mpg_gmres_cfg gmres;
+  mpg_spai_cfg spai;
+  int max_chain_len;
+  long long explicit_nnz_cap, standard_residual_max_dim;
+} mpg_irka_cfg;
+
+/* ReportRow (proj/include/morprec/report.hpp:28-40). */
+typedef struct {
+  int sweep, point, kind, solves;
+  long long iterations;
+  double build_seconds, gmres_seconds, min_residual, matrix_change, standard_residual;
+} mpg_report_row;
+
+/* Per-solve record of the multi-shift batch (one row per solve). */
+typedef struct {
+  double sigma_re, sigma_im;
+  int transpose, chain_length;
+  mpg_gmres_report report;
+} mpg_solve_record;
+
+/* ---- errors, devices, streams ------------------------------------------- */
+const char* mpg_last_error(void);
+int mpg_device_count(int* count);
+/* The library stream used for `device` (a cudaStream_t), for event timing. */
+int mpg_stream(int device, void** stream);
+int mpg_synchronize(int device);
+/* Kernels launched by this library since load (for gpu_launches accounting). */
+long long mpg_launch_count(void);
+/* cudaMemcpy with unified addressing (host or device pointers). */
+int mpg_copy(void* dst, const void* src, int64_t bytes);
+
+/* ---- matrices: SparseMatrix (proj/include/morprec/sparse.hpp:33-101) -----
+ * from_csr validates like SparseMatrix::from_csr (sparse.cpp:48-74):
+ * nondecreasing offsets, in-range and strictly increasing columns. */
+int mpg_csr_create(int device, int64_t nrows, int64_t ncols, const int64_t* rowptr, const int64_t* colind,
+                   const double* values, mpg_csr** out);
+void mpg_csr_destroy(mpg_csr* m);
+int mpg_csr_info(const mpg_csr* m, int64_t* nrows, int64_t* ncols, int64_t* nnz);
+/* Copies the CSR arrays back to host buffers (rowptr: nrows+1, colind/values: nnz). */
+int mpg_csr_download(const mpg_csr* m, int64_t* rowptr, int64_t* colind, double* values);
+/* y = A x / y = A^T x (SparseMatrix::multiply / multiply_transpose, sparse.cpp:236-269);
+ * x, y any memory. */
+int mpg_csr_multiply(const mpg_csr* m, const double* x, double* y);
+int mpg_csr_multiply_transpose(const mpg_csr* m, const double* x, double* y);
+/* SparseMatrix::transpose (sparse.cpp:289-299), built on the device. */
+int mpg_csr_transpose(const mpg_csr* m, mpg_csr** out);
+double mpg_csr_frobenius_norm(const mpg_csr* m);
+
+/* ---- shifted operator: replaces linear_combination(sigma*D, -K)
+ * (proj/src/qbihomm.cpp:164-171, sparse.cpp:156-202) and the N = 0
+ * KroneckerOperator::apply (proj/src/kron.cpp:34-64) — sigma*E - A is formed
+ * on the fly, never materialised. E == NULL means the identity (the
+ * reference's BIRKA case); diagonal E and E sharing A's pattern get fused
+ * fast paths. */
+int mpg_op_create(const mpg_csr* a, const mpg_csr* e, mpg_op** out);
+void mpg_op_destroy(mpg_op* op);
+int64_t mpg_op_dim(const mpg_op* op);
+/* Real shift (sigma_im == 0): y = (sigma E - A) x on n-vectors. Complex pair
+ * (sigma_im != 0): the real 2x2-block form of the reference's Kronecker
+ * operator on [x1; x2] (2n-vectors):
+ *   [ sigma_re E - A   sigma_im E      ] [x1]
+ *   [ -sigma_im E      sigma_re E - A  ] [x2]
+ * with sigma = -lambda for the block [[a, b], [-b, a]] (proj/src/birka.cpp:117).
+ * transpose != 0 uses A^T and E^T in the same form (the reference's test side,
+ * birka.cpp:198). x, y any memory. */
+int mpg_op_apply(const mpg_op* op, double sigma_re, double sigma_im, int transpose, const double* x, double* y);
+/* Explicit unit matrix of the operator above (input of the SPAI builds), the
+ * N = 0 block of assemble_explicit (proj/src/kron.cpp:72-131). */
+int mpg_op_explicit(const mpg_op* op, double sigma_re, double sigma_im, int transpose, mpg_csr** out);
+
+/* ---- preconditioner builds ------------------------------------------------
+ * spai_build (proj/src/spai.cpp:175-238): warp-per-column adaptive SPAI.
+ * column_residuals (nrows doubles, host) may be NULL. */
+int mpg_spai_build(const mpg_csr* a, const mpg_spai_cfg* cfg, mpg_csr** p, double* column_residuals,
+                   int64_t* fallback_count, double* build_seconds);
+/* spai_column_solve (proj/src/spai.cpp:158-173): fixed-pattern column solve. */
+int mpg_spai_column_solve(const mpg_csr* a, int64_t col, int64_t npattern, const int64_t* pattern, double* values,
+                          double* residual, int* rank_deficient);
+/* update_build (proj/src/chain.cpp:16-98): Q = argmin ||A_prev - A_new Q||_F. */
+int mpg_update_build(const mpg_csr* a_prev, const mpg_csr* a_new, const mpg_spai_cfg* cfg, mpg_csr** q,
+                     double* min_residual, double* matrix_change, int64_t* fallback_count, double* build_seconds);
+
+/* ---- chains: PrecondChain (proj/include/morprec/chain.hpp:55-77) ----------
+ * Immutable and reference counted; extend shares the prefix factors. */
+int mpg_chain_create(const mpg_csr* base, mpg_chain** out);
+int mpg_chain_extend(const mpg_chain* chain, const mpg_csr* q, mpg_chain** out);
+void mpg_chain_destroy(mpg_chain* chain);
+int mpg_chain_length(const mpg_chain* chain);
+/* Identity of factor i (0 = base): the same pointer for shared prefixes. */
+const void* mpg_chain_factor_id(const mpg_chain* chain, int i);
+/* out = Q_L(...Q_1(P in)) (chain.cpp:117-126); x, y any memory. */
+int mpg_chain_apply(const mpg_chain* chain, const double* x, double* y);
+/* ||I - A P||_F / sqrt(n) (chain.cpp:140-157), probing n columns. */
+int mpg_standard_residual(const mpg_csr* a, const mpg_chain* chain, double* out);
+
+/* ---- GMRES: gmres_right_preconditioned (proj/src/gmres.cpp:40-186) --------
+ * Full right-preconditioned GMRES, x0 = 0, with the reference's control flow
+ * (Gram-Schmidt + measured second pass at 1e-10, invariance at 1e-14, true
+ * residual recheck with the 0.25 back-off). chain == NULL is the identity.
+ * history (max_iter+1 doubles, host) may be NULL. b, x any memory. */
+int mpg_gmres_csr(const mpg_csr* m, const mpg_chain* chain, const double* b, double* x, const mpg_gmres_cfg* cfg,
+                  mpg_gmres_report* report, double* history);
+int mpg_gmres_shifted(const mpg_op* op, double sigma_re, double sigma_im, int transpose, const mpg_chain* chain,
+                      const double* b, double* x, const mpg_gmres_cfg* cfg, mpg_gmres_report* report,
+                      double* history);
+/* Multi-shift batch: nsolves independent solves advanced in lockstep on one
+ * device (shared launches, per-solve state). chains[i] may be NULL. */
+int mpg_gmres_batch(const mpg_op* op, int nsolves, const double* sigma_re, const double* sigma_im,
+                    const int* transpose, const mpg_chain* const* chains, const double* const* b, double* const* x,
+                    const mpg_gmres_cfg* cfg, mpg_gmres_report* reports);
+
+/* ---- IRKA: birka_reduce with N = 0 (proj/src/birka.cpp:139-310),
+ * generalised to E (E_r = W^T E V, A_r = W^T A V, K_r = E_r^{-1} A_r);
+ * one GMRES per shift unit, V/W by CholQR2 on the device.
+ * Inputs b (n x m) and c (n x q) column-major, any memory. init_shifts
+ * (r doubles) sets K_r = diag(-init_shifts) with fr/cr from the default-seed
+ * stream (birka.cpp:41-89); NULL uses the default seed entirely.
+ * Outputs (host, any may be NULL): kr, er, ar (r x r), fr (r x m), cr (r x q),
+ * lambda (r), v, w (n x r). */
+int mpg_irka_reduce(const mpg_op* op, const double* b, int m, const double* c, int q, const mpg_irka_cfg* cfg,
+                    int mode, const double* init_shifts, double* kr, double* fr, double* cr, double* er, double* ar,
+                    double* lam_re, double* lam_im, double* v, double* w, int* sweeps, int* converged,
+                    mpg_report_row* rows, int max_rows, int* nrows);
+
+/* Multi-GPU IRKA: this process (rank of world) solves its shard of the
+ * (unit, side) solves; `allgather` (provided by the caller, e.g. NCCL through
+ * torch.distributed) concatenates per-rank byte buffers; buffers are device
+ * pointers of this rank's device. */
+typedef int (*mpg_allgather_fn)(void* ctx, const void* send, void* recv, int64_t bytes_per_rank);
+int mpg_irka_reduce_sharded(const mpg_op* op, const double* b, int m, const double* c, int q,
+                            const mpg_irka_cfg* cfg, int mode, const double* init_shifts, int rank, int world,
+                            mpg_allgather_fn allgather, void* ctx, double* kr, double* fr, double* cr,
+                            double* lam_re, double* lam_im, int* sweeps, int* converged, mpg_report_row* rows,
+                            int max_rows, int* nrows);
+
+/* ---- shift sweep: run_spai_bench (proj/src/bench.cpp:159-249) for
+ * sigma_i E - A with a horizontal chain (fresh at i == 0 or when the chain
+ * would exceed max_chain_len). Non-convergence is recorded, not raised.
+ * x_out (n x npoints, any memory) may be NULL. */
+int mpg_spai_bench(const mpg_op* op, const double* b, int npoints, const double* points, const mpg_spai_cfg* spai,
+                   const mpg_gmres_cfg* gmres, int mode, int max_chain_len, double* x_out, mpg_report_row* rows,
+                   int max_rows, int* nrows, int* failed);
+
+/* ---- host-side synthetic inputs (gen/generators.cpp) ---------------------- */
+typedef struct {
+  int64_t nrows, ncols, nnz;
+  int64_t* rowptr;
+  int64_t* colind;
+  double* val;
+} mpg_host_csr;
+
+typedef struct {
+  int64_t n;
+  mpg_host_csr* a; /* A (n x n) */
+  mpg_host_csr* e; /* E as CSR, or NULL */
+  double* e_diag;  /* diagonal E, or NULL (both NULL: identity) */
+  int m, q, r;
+  double* b; /* n x m column-major */
+  double* c; /* n x q column-major */
+  double* shifts; /* r initial shifts */
+} mpg_host_system;
+
+const char* mpg_gen_last_error(void);
+void mpg_host_csr_free(mpg_host_csr* m);
+void mpg_host_system_free(mpg_host_system* s);
+int mpg_gen_random_dense(int64_t r, int64_t c, uint64_t seed, double* out);
+int mpg_gen_random_sparse(int64_t r, int64_t c, double density, uint64_t seed, double diag_shift, mpg_host_csr** out);
+int mpg_gen_from_triplets(int64_t nr, int64_t nc, int64_t nnz, const int64_t* ri, const int64_t* ci, const double* v,
+                          mpg_host_csr** out);
+int mpg_gen_bilinear_toy(int64_t n, int64_t m, uint64_t seed, mpg_host_csr** k_out, double* f, double* c);
+int mpg_gen_grid2d(int64_t N, uint64_t seed, mpg_host_system** out);
+int mpg_gen_convdiff3d(int64_t M, uint64_t seed, mpg_host_system** out);
+int mpg_gen_fem3d(int64_t N, uint64_t seed, int mimo, mpg_host_system** out);
+int mpg_gen_zipf(int64_t n, uint64_t seed, int64_t min_len, int64_t max_len, double expo, int nshifts,
+                 mpg_host_system** out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPG_H_ */

@@ -1,0 +1,345 @@
+// CPU ORACLE — test infrastructure only (see oracle.hpp).
+// Flat C entry points so tests/ and bench.py's CPU-baseline leg can drive
+// the restatement through ctypes. Status codes match include/mpg.h.
+#include <cstring>
+#include <string>
+
+#include "oracle.hpp"
+
+using namespace oracle;
+
+namespace {
+thread_local std::string g_err;
+
+struct orc_chain { PrecondChain chain; };
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const ConfigError& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const SolverError& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 4;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+typedef struct { int pattern_kind, power; double fill_tol; int max_fill_per_col, max_pattern_sweeps, threads; } orc_spai_cfg;
+typedef struct { double rel_tol; int max_iter, record_history; } orc_gmres_cfg;
+typedef struct {
+  int iterations, converged, breakdown, history_len;
+  double rhs_norm, final_residual, solve_seconds;
+} orc_gmres_report;
+typedef struct {
+  int r; double tol; int max_sweeps; int decoupled; unsigned long long seed;
+  orc_gmres_cfg gmres; orc_spai_cfg spai; int max_chain_len; long long explicit_nnz_cap, standard_residual_max_dim;
+} orc_irka_cfg;
+typedef struct {
+  int sweep, point, kind, solves; long long iterations;
+  double build_seconds, gmres_seconds, min_residual, matrix_change, standard_residual;
+} orc_report_row;
+
+static SpaiConfig to_spai(const orc_spai_cfg* c) {
+  SpaiConfig s;
+  if (c) {
+    s.pattern_kind = c->pattern_kind; s.power = c->power; s.fill_tol = c->fill_tol;
+    s.max_fill_per_col = c->max_fill_per_col; s.max_pattern_sweeps = c->max_pattern_sweeps; s.threads = c->threads;
+  }
+  return s;
+}
+static GmresConfig to_gmres(const orc_gmres_cfg* c) {
+  GmresConfig g;
+  if (c) { g.rel_tol = c->rel_tol; g.max_iter = c->max_iter; g.record_history = c->record_history != 0; }
+  return g;
+}
+static void fill_report(const GmresReport& r, orc_gmres_report* out, double* history) {
+  if (!out) return;
+  out->iterations = r.iterations; out->converged = r.converged; out->breakdown = r.breakdown;
+  out->rhs_norm = r.rhs_norm; out->final_residual = r.final_residual; out->solve_seconds = r.solve_seconds;
+  out->history_len = int(r.residual_history.size());
+  if (history) std::memcpy(history, r.residual_history.data(), r.residual_history.size() * sizeof(double));
+}
+static int copy_rows(const ReductionReport& rep, orc_report_row* rows, int max_rows, int* nrows) {
+  const int n = int(rep.rows.size());
+  if (nrows) *nrows = n;
+  for (int i = 0; i < n && i < max_rows && rows; ++i) {
+    const ReportRow& r = rep.rows[size_t(i)];
+    rows[i] = {r.sweep, r.point, int(r.kind), r.solves, (long long)r.gmres_iterations, r.precond_build_seconds,
+               r.gmres_seconds, r.min_residual, r.matrix_change, r.standard_residual};
+  }
+  return 0;
+}
+static Dense dense_from(const double* p, long long rows, long long cols) {
+  Dense d(rows, cols);
+  if (p) std::memcpy(d.a.data(), p, size_t(rows * cols) * sizeof(double));
+  return d;
+}
+
+const char* orc_last_error(void) { return g_err.c_str(); }
+
+int orc_csr_from_csr(long long nr, long long nc, const long long* rp, const long long* ci, const double* v, Csr** out) {
+  return guard([&] {
+    const size_t nnz = size_t(rp[nr]);
+    *out = new Csr(Csr::from_csr(nr, nc, std::vector<index_t>(rp, rp + nr + 1), std::vector<index_t>(ci, ci + nnz),
+                                 std::vector<double>(v, v + nnz)));
+  });
+}
+int orc_csr_from_triplets(long long nr, long long nc, long long nnz, const long long* ri, const long long* ci,
+                          const double* v, Csr** out) {
+  return guard([&] {
+    std::vector<Triplet> t(static_cast<size_t>(nnz));
+    for (long long k = 0; k < nnz; ++k) t[size_t(k)] = {ri[k], ci[k], v[k]};
+    *out = new Csr(Csr::from_triplets(nr, nc, std::move(t)));
+  });
+}
+void orc_csr_free(Csr* h) { delete h; }
+void orc_csr_info(const Csr* h, long long* nr, long long* nc, long long* nnz) {
+  *nr = h->nrows; *nc = h->ncols; *nnz = h->nnz();
+}
+void orc_csr_export(const Csr* h, long long* rp, long long* ci, double* v) {
+  std::memcpy(rp, h->rowptr.data(), h->rowptr.size() * sizeof(long long));
+  std::memcpy(ci, h->colind.data(), h->colind.size() * sizeof(long long));
+  std::memcpy(v, h->val.data(), h->val.size() * sizeof(double));
+}
+int orc_csr_multiply(const Csr* h, long long nx, const double* x, double* y) {
+  return guard([&] {
+    Vec in(x, x + nx), out;
+    h->multiply(in, out);
+    std::memcpy(y, out.data(), out.size() * sizeof(double));
+  });
+}
+int orc_csr_multiply_transpose(const Csr* h, long long nx, const double* x, double* y) {
+  return guard([&] {
+    Vec out = h->multiply_transpose(Vec(x, x + nx));
+    std::memcpy(y, out.data(), out.size() * sizeof(double));
+  });
+}
+int orc_csr_transpose(const Csr* h, Csr** out) {
+  return guard([&] { *out = new Csr(h->transpose()); });
+}
+int orc_csr_linear_combination(int nterms, const double* coeffs, const Csr* const* mats, Csr** out) {
+  return guard([&] {
+    std::vector<std::pair<double, const Csr*>> t;
+    for (int i = 0; i < nterms; ++i) t.push_back({coeffs[i], mats[i]});
+    *out = new Csr(Csr::linear_combination(t));
+  });
+}
+double orc_csr_frobenius_norm(const Csr* h) { return h->frobenius_norm(); }
+int orc_csr_extract(const Csr* h, long long np, const long long* pattern, long long* nrows_out, long long* row_map,
+                    double* block, long long cap_rows) {
+  return guard([&] {
+    auto sub = h->extract_column_submatrix(std::vector<index_t>(pattern, pattern + np));
+    *nrows_out = index_t(sub.row_map.size());
+    if (row_map && index_t(sub.row_map.size()) <= cap_rows) {
+      std::memcpy(row_map, sub.row_map.data(), sub.row_map.size() * sizeof(long long));
+      std::memcpy(block, sub.block.a.data(), sub.block.a.size() * sizeof(double));
+    }
+  });
+}
+
+int orc_spai_build(const Csr* a, const orc_spai_cfg* cfg, Csr** p, double* col_res, long long* fallback, double* secs) {
+  return guard([&] {
+    SpaiResult r = spai_build(*a, to_spai(cfg));
+    if (col_res) std::memcpy(col_res, r.column_residuals.data(), r.column_residuals.size() * sizeof(double));
+    if (fallback) *fallback = r.fallback_count;
+    if (secs) *secs = r.build_seconds;
+    *p = new Csr(std::move(r.p));
+  });
+}
+int orc_spai_column_solve(const Csr* a, long long col, long long np, const long long* pattern, double* values,
+                          double* residual, int* rank_def) {
+  return guard([&] {
+    SpaiColumn c = spai_column_solve(*a, col, std::vector<index_t>(pattern, pattern + np));
+    std::memcpy(values, c.values.data(), c.values.size() * sizeof(double));
+    *residual = c.residual;
+    *rank_def = c.rank_deficient;
+  });
+}
+int orc_update_build(const Csr* prev, const Csr* next, const orc_spai_cfg* cfg, Csr** q, double* min_res,
+                     double* change, long long* fallback, double* secs) {
+  return guard([&] {
+    UpdateFactor f = update_build(*prev, *next, to_spai(cfg));
+    *min_res = f.min_residual; *change = f.matrix_change;
+    if (fallback) *fallback = f.fallback_count;
+    if (secs) *secs = f.build_seconds;
+    *q = new Csr(std::move(f.q));
+  });
+}
+
+int orc_chain_create(const Csr* base, orc_chain** out) {
+  return guard([&] { *out = new orc_chain{PrecondChain(*base)}; });
+}
+int orc_chain_extend(const orc_chain* c, const Csr* q, orc_chain** out) {
+  return guard([&] {
+    auto f = std::make_shared<UpdateFactor>();
+    f->q = *q;
+    *out = new orc_chain{c->chain.extended(f)};
+  });
+}
+int orc_chain_length(const orc_chain* c) { return c->chain.length(); }
+void orc_chain_free(orc_chain* c) { delete c; }
+int orc_chain_apply(const orc_chain* c, long long n, const double* x, double* y) {
+  return guard([&] {
+    Vec out;
+    c->chain.apply(Vec(x, x + n), out);
+    std::memcpy(y, out.data(), out.size() * sizeof(double));
+  });
+}
+int orc_standard_residual(const Csr* a, const orc_chain* c, double* out) {
+  return guard([&] { *out = standard_residual(*a, c->chain); });
+}
+
+// GMRES with a plain CSR operator (matvec_operator) or the Kronecker / shifted
+// operator -(Lambda (x) E) - (I (x) A); chain null means identity.
+int orc_gmres_csr(const Csr* m, const orc_chain* c, long long n, const double* b, double* x, const orc_gmres_cfg* cfg,
+                  orc_gmres_report* rep, double* history) {
+  return guard([&] {
+    GmresResult r = gmres_right_preconditioned(matvec_operator(*m), c ? c->chain.as_operator() : identity_operator(),
+                                               Vec(b, b + n), to_gmres(cfg));
+    std::memcpy(x, r.x.data(), r.x.size() * sizeof(double));
+    fill_report(r.report, rep, history);
+  });
+}
+int orc_gmres_kron(const double* lambda, int r, const Csr* a, const Csr* e, const orc_chain* c, const double* b,
+                   double* x, const orc_gmres_cfg* cfg, orc_gmres_report* rep, double* history) {
+  return guard([&] {
+    KronOp op{dense_from(lambda, r, r), a, e};
+    const LinearOp aop = [&op](const Vec& in, Vec& out) { op.apply(in, out); };
+    const long long n = a->nrows * r;
+    GmresResult res = gmres_right_preconditioned(aop, c ? c->chain.as_operator() : identity_operator(),
+                                                 Vec(b, b + n), to_gmres(cfg));
+    std::memcpy(x, res.x.data(), res.x.size() * sizeof(double));
+    fill_report(res.report, rep, history);
+  });
+}
+int orc_kron_apply(const double* lambda, int r, const Csr* a, const Csr* e, const double* x, double* y) {
+  return guard([&] {
+    KronOp op{dense_from(lambda, r, r), a, e};
+    Vec out;
+    op.apply(Vec(x, x + a->nrows * r), out);
+    std::memcpy(y, out.data(), out.size() * sizeof(double));
+  });
+}
+int orc_kron_assemble(const double* lambda, int r, const Csr* a, const Csr* e, long long cap, Csr** out) {
+  return guard([&] {
+    KronOp op{dense_from(lambda, r, r), a, e};
+    *out = new Csr(assemble_explicit(op, cap));
+  });
+}
+
+int orc_real_spectrum(const double* m, int r, double* blocks, double* basis, double* basis_inv) {
+  RealSpectrum s;
+  if (!real_spectrum(dense_from(m, r, r), s)) return 3;
+  std::memcpy(blocks, s.blocks.a.data(), size_t(r * r) * sizeof(double));
+  std::memcpy(basis, s.basis.a.data(), size_t(r * r) * sizeof(double));
+  std::memcpy(basis_inv, s.basis_inv.a.data(), size_t(r * r) * sizeof(double));
+  return 0;
+}
+int orc_sorted_eigenvalues(const double* m, int r, double* re, double* im) {
+  return guard([&] {
+    auto l = sorted_eigenvalues(dense_from(m, r, r));
+    for (int i = 0; i < r; ++i) { re[i] = l[size_t(i)].re; im[i] = l[size_t(i)].im; }
+  });
+}
+int orc_colpiv_solve(const double* a, long long rows, long long cols, const double* b, double* x, long long* rank) {
+  return guard([&] {
+    ColPivQR qr(dense_from(a, rows, cols));
+    Vec s = qr.solve(Vec(b, b + rows));
+    std::memcpy(x, s.data(), s.size() * sizeof(double));
+    *rank = qr.rank();
+  });
+}
+int orc_thin_q(const double* a, long long rows, long long cols, double* q) {
+  return guard([&] {
+    Dense d = thin_q(dense_from(a, rows, cols));
+    std::memcpy(q, d.a.data(), d.a.size() * sizeof(double));
+  });
+}
+
+static LinearSystem make_sys(const Csr* a, const Csr* e, const double* b, int m, const double* c, int q) {
+  LinearSystem sys;
+  sys.a = *a;
+  if (e) sys.e = std::make_shared<Csr>(*e);
+  sys.b = dense_from(b, a->nrows, m);
+  sys.c = dense_from(c, a->nrows, q);
+  return sys;
+}
+
+int orc_irka_default_seed(const Csr* a, const Csr* e, const double* b, int m, const double* c, int q, int r,
+                          unsigned long long seed, double* kr, double* fr, double* cr) {
+  return guard([&] {
+    IrkaState s = irka_default_seed(make_sys(a, e, b, m, c, q), r, seed);
+    std::memcpy(kr, s.kr.a.data(), s.kr.a.size() * sizeof(double));
+    std::memcpy(fr, s.fr.a.data(), s.fr.a.size() * sizeof(double));
+    std::memcpy(cr, s.cr.a.data(), s.cr.a.size() * sizeof(double));
+  });
+}
+
+// Outputs: kr, er, ar (r x r), fr (r x m), cr (r x q), lambda (r), v, w (n x r);
+// any output pointer may be null.
+int orc_irka_reduce(const Csr* a, const Csr* e, const double* b, int m, const double* c, int q,
+                    const orc_irka_cfg* cfg, int mode, const double* init_kr, const double* init_fr,
+                    const double* init_cr, double* kr, double* fr, double* cr, double* er, double* ar,
+                    double* lam_re, double* lam_im, double* v, double* w, int* sweeps, int* converged,
+                    orc_report_row* rows, int max_rows, int* nrows) {
+  return guard([&] {
+    LinearSystem sys = make_sys(a, e, b, m, c, q);
+    IrkaConfig ic;
+    ic.r = cfg->r; ic.tol = cfg->tol; ic.max_sweeps = cfg->max_sweeps; ic.seed = cfg->seed;
+    ic.gmres = to_gmres(&cfg->gmres); ic.spai = to_spai(&cfg->spai); ic.max_chain_len = cfg->max_chain_len;
+    ic.explicit_nnz_cap = cfg->explicit_nnz_cap; ic.standard_residual_max_dim = cfg->standard_residual_max_dim;
+    ic.decoupled = cfg->decoupled != 0;
+    IrkaState init;
+    const IrkaState* initp = nullptr;
+    if (init_kr) {
+      init = irka_default_seed(sys, ic.r, ic.seed);  // keeps the fr/cr stream
+      init.kr = dense_from(init_kr, ic.r, ic.r);
+      if (init_fr) init.fr = dense_from(init_fr, ic.r, m);
+      if (init_cr) init.cr = dense_from(init_cr, ic.r, q);
+      initp = &init;
+    }
+    auto [s, rep] = irka_reduce(sys, ic, PrecondMode(mode), initp);
+    const size_t rr = size_t(s.kr.rows);
+    if (kr) std::memcpy(kr, s.kr.a.data(), rr * rr * sizeof(double));
+    if (er) std::memcpy(er, s.er.a.data(), rr * rr * sizeof(double));
+    if (ar) std::memcpy(ar, s.ar.a.data(), rr * rr * sizeof(double));
+    if (fr) std::memcpy(fr, s.fr.a.data(), s.fr.a.size() * sizeof(double));
+    if (cr) std::memcpy(cr, s.cr.a.data(), s.cr.a.size() * sizeof(double));
+    for (size_t i = 0; i < s.lambda.size(); ++i) {
+      if (lam_re) lam_re[i] = s.lambda[i].re;
+      if (lam_im) lam_im[i] = s.lambda[i].im;
+    }
+    if (v) std::memcpy(v, s.v.a.data(), s.v.a.size() * sizeof(double));
+    if (w) std::memcpy(w, s.w.a.data(), s.w.a.size() * sizeof(double));
+    *sweeps = s.sweeps;
+    *converged = rep.converged;
+    copy_rows(rep, rows, max_rows, nrows);
+  });
+}
+
+int orc_spai_bench(const Csr* a, const Csr* e, const double* b, int npoints, const double* points,
+                   const orc_spai_cfg* spai, const orc_gmres_cfg* gmres, int mode, int max_chain_len, double* x_out,
+                   orc_report_row* rows, int max_rows, int* nrows, int* failed) {
+  return guard([&] {
+    SweepResult r = run_spai_bench(*a, e, Vec(b, b + a->nrows), std::vector<double>(points, points + npoints),
+                                   to_spai(spai), to_gmres(gmres), PrecondMode(mode), max_chain_len, x_out != nullptr);
+    if (x_out)
+      for (size_t i = 0; i < r.x.size(); ++i) std::memcpy(x_out + i * size_t(a->nrows), r.x[i].data(), r.x[i].size() * sizeof(double));
+    copy_rows(r.report, rows, max_rows, nrows);
+    *failed = r.failed_solves;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,312 @@
+// CPU ORACLE — test infrastructure only (see oracle.hpp).
+// Restates proj/src/birka.cpp:41-310 for N = 0 (linear tangential IRKA),
+// generalised to a mass matrix E (the reference has E = I; with e == nullptr
+// this is the reference loop exactly), and proj/src/bench.cpp:159-249 (the
+// shift-sweep benchmark) for the first-order pencil sigma E - A.
+#include <algorithm>
+#include <cmath>
+#include <random>
+#include <string>
+
+#include "oracle.hpp"
+
+namespace oracle {
+
+namespace {
+std::string shortest(double v) {
+  char buf[64];
+  for (int p = 1; p <= 17; ++p) {
+    std::snprintf(buf, sizeof buf, "%.*g", p, v);
+    if (std::strtod(buf, nullptr) == v) break;
+  }
+  return buf;
+}
+
+Dense dense_of(const Csr& m, const Dense& x) { return m.multiply(x); }
+
+struct SidePrecond {
+  PrecondChain chain;
+  Csr prev_explicit;
+  bool degraded = false;
+  int shape = 0;  // decoupled mode: unit width of the slot that owns the chain
+};
+}  // namespace
+
+// proj/src/birka.cpp:41-89
+IrkaState irka_default_seed(const LinearSystem& sys, int r, std::uint64_t seed) {
+  const index_t n = sys.a.nrows;
+  if (r < 1) throw ConfigError("birka: reduced order must be at least 1");
+  if (index_t(r) > n) throw ConfigError("birka: reduced order exceeds the system dimension");
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unit(-1.0, 1.0);
+  Vec x(static_cast<size_t>(n));
+  for (index_t i = 0; i < n; ++i) x[size_t(i)] = unit(rng);
+  double radius = 0.0, xn = 0.0;
+  for (double v : x) xn += v * v;
+  xn = std::sqrt(xn);
+  if (xn > 0.0) {
+    for (double& v : x) v /= xn;
+    for (int it = 0; it < 20; ++it) {
+      const Vec y = sys.a.multiply(x);
+      double ny = 0.0;
+      for (double v : y) ny += v * v;
+      ny = std::sqrt(ny);
+      if (ny == 0.0) { radius = 0.0; break; }
+      radius = ny;
+      for (size_t i = 0; i < y.size(); ++i) x[i] = y[i] / ny;
+    }
+  }
+  if (!(radius > 0.0) || !std::isfinite(radius)) radius = 1.0;
+  IrkaState s;
+  s.kr = Dense(r, r);
+  for (int i = 0; i < r; ++i) {
+    const double t = r == 1 ? 1.0 : double(i) / (r - 1);
+    s.kr(i, i) = -radius * std::pow(10.0, -3.0 * (1.0 - t));
+  }
+  s.fr = Dense(r, sys.b.cols);
+  s.cr = Dense(r, sys.c.cols);
+  for (Dense* m : {&s.fr, &s.cr})
+    for (index_t j = 0; j < m->cols; ++j) {
+      double nn = 0.0;
+      for (int i = 0; i < r; ++i) { (*m)(i, j) = unit(rng); nn += (*m)(i, j) * (*m)(i, j); }
+      nn = std::sqrt(nn);
+      if (nn > 0.0)
+        for (int i = 0; i < r; ++i) (*m)(i, j) /= nn;
+    }
+  return s;
+}
+
+// proj/src/birka.cpp:139-310
+std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const IrkaConfig& cfg,
+                                                  PrecondMode mode, const IrkaState* init) {
+  const index_t n = sys.a.nrows;
+  if (sys.a.ncols != n) throw ConfigError("irka: A must be square");
+  if (sys.e && (sys.e->nrows != n || sys.e->ncols != n)) throw ConfigError("irka: E must be n x n");
+  if (sys.b.rows != n || sys.b.cols < 1) throw ConfigError("irka: B must have n rows and at least one column");
+  if (sys.c.rows != n || sys.c.cols < 1) throw ConfigError("irka: C must have n rows and at least one column");
+  if (cfg.max_sweeps < 1) throw ConfigError("birka: max_sweeps must be at least 1");
+  if (cfg.max_chain_len < 1) throw ConfigError("birka: max_chain_len must be at least 1");
+  IrkaState state = init ? *init : irka_default_seed(sys, cfg.r, cfg.seed);
+  const index_t r = state.kr.rows;
+  if (r < 1 || r > n) throw ConfigError("birka: reduced order must be in [1, n]");
+  if (state.fr.rows != r || state.fr.cols != sys.b.cols || state.cr.rows != r || state.cr.cols != sys.c.cols)
+    throw ConfigError("birka: initial state dimensions do not match the system");
+
+  const Csr at = sys.a.transpose();
+  std::shared_ptr<Csr> et;
+  if (sys.e) et = std::make_shared<Csr>(sys.e->transpose());
+
+  ReductionReport report;
+  report.reduced_order = int(r);
+  std::vector<SidePrecond> sides(2);
+  std::vector<std::vector<SidePrecond>> unit_sides(2, std::vector<SidePrecond>(static_cast<size_t>(r)));
+  std::mt19937_64 perturb_rng(cfg.seed ^ 0x9e3779b97f4a7c15ull);
+  std::vector<Complex> lambda_prev = sorted_eigenvalues(state.kr);
+  bool converged = false;
+  int sweeps_done = 0;
+
+  for (int z = 1; z <= cfg.max_sweeps && !converged; ++z) {
+    RealSpectrum spec;
+    if (!real_spectrum(state.kr, spec)) {  // :167-180
+      std::uniform_real_distribution<double> unit(-1.0, 1.0);
+      Dense nudged = state.kr;
+      const double scale = 1e-8 * std::max(1.0, state.kr.norm());
+      for (double& v : nudged.a) v += scale * unit(perturb_rng);
+      if (!real_spectrum(nudged, spec))
+        throw SolverError("birka: reduced state matrix is not diagonalizable (sweep " + std::to_string(z) +
+                          "), even after perturbation");
+      state.kr = nudged;
+      lambda_prev = sorted_eigenvalues(state.kr);
+    }
+    const Dense rinv_t = spec.basis_inv.transpose();
+    const Dense f2 = matmul(state.fr.transpose(), rinv_t);  // m x r, :182
+    const Dense c2 = matmul(state.cr.transpose(), spec.basis);  // q x r, :183
+    const KronOp ops[2] = {{spec.blocks, &sys.a, sys.e.get()}, {spec.blocks, &at, et.get()}};
+    const Dense rhs_mats[2] = {matmul(sys.b, f2), matmul(sys.c, c2)};  // :199
+
+    Dense bases[2];
+    for (int side = 0; side < 2; ++side) {
+      const Dense& rhs = rhs_mats[side];
+      double bn = 0.0;
+      for (double v : rhs.a) bn += v * v;
+      if (bn == 0.0)
+        throw SolverError(std::string("birka: zero right-hand side on the ") + (side == 0 ? "trial" : "test") +
+                          " side (sweep " + std::to_string(z) + "); input/output maps must be nonzero");
+      Dense xsol(n, r);
+      // Units: one joint n*r solve (reference), or one solve per real shift /
+      // conjugate-pair block (decoupled; same fixed point).
+      std::vector<std::pair<index_t, index_t>> units;  // (first column, width)
+      if (cfg.decoupled) {
+        for (index_t c = 0; c < r;) {
+          const index_t w = (c + 1 < r && spec.blocks(c, c + 1) != 0.0) ? 2 : 1;
+          units.push_back({c, w});
+          c += w;
+        }
+      } else {
+        units.push_back({0, r});
+      }
+      for (const auto& [c0, width] : units) {
+        ReportRow row;
+        row.sweep = z;
+        row.point = side + 1;
+        row.kind = PrecondKind::None;
+        Dense lam(width, width);
+        for (index_t i = 0; i < width; ++i)
+          for (index_t j = 0; j < width; ++j) lam(i, j) = spec.blocks(c0 + i, c0 + j);
+        const KronOp op{lam, ops[side].a, ops[side].e};
+        SidePrecond& sp = cfg.decoupled ? unit_sides[size_t(side)][size_t(c0)] : sides[size_t(side)];
+        if (cfg.decoupled && sp.shape != width) {  // slot changed shape: restart its chain
+          sp = SidePrecond{};
+          sp.shape = int(width);
+        }
+        LinearOp prec = identity_operator();
+        bool have_explicit = false;
+        Csr a_explicit;
+        if (mode != PrecondMode::None && !sp.degraded) {
+          try {
+            a_explicit = assemble_explicit(op, cfg.explicit_nnz_cap);
+            have_explicit = true;
+          } catch (const ConfigError& e) {
+            sp.degraded = true;
+            report.warnings.push_back(std::string(side == 0 ? "trial" : "test") +
+                                      " side continues unpreconditioned: " + e.what());
+          }
+        }
+        if (have_explicit) {
+          if (mode == PrecondMode::FreshSpai ||
+              (mode == PrecondMode::ReuseChain && (sp.chain.empty() || sp.chain.length() + 1 > cfg.max_chain_len))) {
+            SpaiResult built = spai_build(a_explicit, cfg.spai);
+            sp.chain = PrecondChain(std::move(built.p), built.build_seconds);
+            row.kind = PrecondKind::Fresh;
+            row.precond_build_seconds = built.build_seconds;
+          } else {
+            UpdateFactor f = update_build(sp.prev_explicit, a_explicit, cfg.spai);
+            row.kind = PrecondKind::Vertical;
+            row.precond_build_seconds = f.build_seconds;
+            row.min_residual = f.min_residual;
+            row.matrix_change = f.matrix_change;
+            sp.chain = sp.chain.extended(std::make_shared<const UpdateFactor>(std::move(f)));
+          }
+          if (mode == PrecondMode::ReuseChain) sp.prev_explicit = a_explicit;
+          prec = sp.chain.as_operator();
+          if (a_explicit.nrows <= cfg.standard_residual_max_dim)
+            row.standard_residual = standard_residual(a_explicit, sp.chain);
+        }
+        Vec b(static_cast<size_t>(n * width));
+        std::copy(rhs.col(c0), rhs.col(c0) + n * width, b.begin());
+        double ubn = 0.0;
+        for (double v : b) ubn += v * v;
+        Vec x(static_cast<size_t>(n * width), 0.0);
+        GmresResult res;
+        if (ubn > 0.0) {
+          const LinearOp a_op = [&op](const Vec& in, Vec& out) { op.apply(in, out); };
+          res = gmres_right_preconditioned(a_op, prec, b, cfg.gmres);
+          row.solves = 1;
+          row.gmres_iterations = res.report.iterations;
+          row.gmres_seconds = res.report.solve_seconds;
+          x = res.x;
+        }
+        report.rows.push_back(row);
+        if (ubn > 0.0 && !res.report.converged)
+          throw SolverError(std::string("birka: gmres did not converge on the ") + (side == 0 ? "trial" : "test") +
+                            " side (sweep " + std::to_string(z) + "; relative residual " +
+                            shortest(res.report.final_residual / std::max(res.report.rhs_norm, 1e-300)) + " after " +
+                            std::to_string(res.report.iterations) + " iterations)");
+        std::copy(x.begin(), x.end(), xsol.col(c0));
+      }
+      bases[side] = thin_q(xsol);  // :278
+    }
+    const Dense& v = bases[0];
+    const Dense& w = bases[1];
+    const Dense wt = w.transpose();
+    // E_r = W^T E V, A_r = W^T A V; reference (E = I): W^T V and W^T K V.
+    const Dense er = sys.e ? matmul(wt, dense_of(*sys.e, v)) : matmul(wt, v);
+    const Dense ar = matmul(wt, dense_of(sys.a, v));
+    FullPivLU lu(er);
+    if (!lu.invertible())
+      throw SolverError("birka: projection matrix (test basis^T trial basis) is singular at sweep " + std::to_string(z));
+    state.er = er;
+    state.ar = ar;
+    state.kr = lu.solve(ar);
+    state.fr = lu.solve(matmul(wt, sys.b));
+    state.cr = matmul(v.transpose(), sys.c);
+    state.v = v;
+    state.w = w;
+    sweeps_done = z;
+    const std::vector<Complex> lambda_new = sorted_eigenvalues(state.kr);
+    double num = 0.0, den = 0.0;
+    for (size_t i = 0; i < lambda_new.size(); ++i) {
+      const double dr = lambda_new[i].re - lambda_prev[i].re, di = lambda_new[i].im - lambda_prev[i].im;
+      num += dr * dr + di * di;
+      den += lambda_prev[i].re * lambda_prev[i].re + lambda_prev[i].im * lambda_prev[i].im;
+    }
+    if (std::sqrt(num) / std::max(std::sqrt(den), 1e-300) < cfg.tol) converged = true;
+    lambda_prev = lambda_new;
+  }
+  state.lambda = lambda_prev;
+  state.sweeps = sweeps_done;
+  report.converged = converged;
+  report.sweeps = sweeps_done;
+  if (!converged) report.warnings.push_back("fixed point left unconverged after " + std::to_string(sweeps_done) + " sweeps");
+  return {std::move(state), std::move(report)};
+}
+
+// proj/src/bench.cpp:159-249, with shifted_operator(s) = s E - A
+SweepResult run_spai_bench(const Csr& a, const Csr* e, const Vec& b, const std::vector<double>& points,
+                           const SpaiConfig& spai, const GmresConfig& gmres, PrecondMode mode, int max_chain_len,
+                           bool keep_solutions) {
+  if (points.empty()) throw ConfigError("spai-bench: at least one point is required");
+  for (double s : points)
+    if (!(s > 0.0) || !std::isfinite(s)) throw ConfigError("spai-bench: points must be positive and finite");
+  if (max_chain_len < 1) throw ConfigError("spai-bench: max_chain_len must be at least 1");
+  double bn = 0.0;
+  for (double v : b) bn += v * v;
+  if (bn == 0.0) throw ConfigError("spai-bench: the first input column must be nonzero");
+  const Csr ident = e ? Csr() : Csr::identity(a.nrows);
+  const Csr* emat = e ? e : &ident;
+  SweepResult result;
+  PrecondChain chain;
+  Csr prev;
+  for (size_t i = 0; i < points.size(); ++i) {
+    const Csr op = Csr::linear_combination({{points[i], emat}, {-1.0, &a}});
+    ReportRow row;
+    row.sweep = 1;
+    row.point = int(i) + 1;
+    LinearOp prec = identity_operator();
+    if (mode == PrecondMode::FreshSpai || (mode == PrecondMode::ReuseChain && (i == 0 || chain.length() + 1 > max_chain_len))) {
+      SpaiResult built = spai_build(op, spai);
+      chain = PrecondChain(std::move(built.p), built.build_seconds);
+      row.kind = PrecondKind::Fresh;
+      row.precond_build_seconds = built.build_seconds;
+      prec = chain.as_operator();
+    } else if (mode == PrecondMode::ReuseChain) {
+      UpdateFactor f = update_build(prev, op, spai);
+      row.kind = PrecondKind::Horizontal;
+      row.precond_build_seconds = f.build_seconds;
+      row.min_residual = f.min_residual;
+      row.matrix_change = f.matrix_change;
+      chain = chain.extended(std::make_shared<const UpdateFactor>(std::move(f)));
+      prec = chain.as_operator();
+    }
+    prev = op;
+    if (mode != PrecondMode::None && a.nrows <= 5000) row.standard_residual = standard_residual(op, chain);
+    GmresResult res = gmres_right_preconditioned(matvec_operator(op), prec, b, gmres);
+    row.solves = 1;
+    row.gmres_iterations = res.report.iterations;
+    row.gmres_seconds = res.report.solve_seconds;
+    result.report.rows.push_back(row);
+    if (!res.report.converged) {
+      ++result.failed_solves;
+      result.report.warnings.push_back("solve at point " + std::to_string(i + 1) + " (s = " + shortest(points[i]) +
+                                       ") did not converge: relative residual " +
+                                       shortest(res.report.final_residual / std::max(res.report.rhs_norm, 1e-300)) +
+                                       " after " + std::to_string(res.report.iterations) + " iterations");
+    }
+    if (keep_solutions) result.x.push_back(std::move(res.x));
+  }
+  result.report.converged = result.failed_solves == 0;
+  result.report.sweeps = 1;
+  return result;
+}
+
+}  // namespace oracle

@@ -1,0 +1,22 @@
+"""B200-native preconditioned shifted-solve engine for IRKA / moment matching
+(the hot path of arXiv 2003.12759, reference `morprec`, /root/reference/proj).
+
+The compute path is libmpg.so (hand-written sm_100a CUDA + C++ drivers behind
+the C ABI in include/mpg.h); this package is the Python mirror of the
+reference's API (morprec.py) and the synthetic-input generators (gen.py).
+"""
+from ._lib import ConfigError, CudaError, SolverError, lib  # noqa: F401  (fails loudly if libmpg.so is missing)
+from . import gen  # noqa: F401
+from .morprec import *  # noqa: F401,F403
+
+
+def device_count() -> int:
+    import ctypes
+    n = ctypes.c_int()
+    lib.mpg_device_count(ctypes.byref(n))
+    return n.value
+
+
+def launch_count() -> int:
+    """Kernels launched by libmpg.so in this process."""
+    return int(lib.mpg_launch_count())

@@ -1,0 +1,428 @@
+// extern "C" entry points of libmpg.so (include/mpg.h): thin wrappers that
+// translate the reference's exception classes into status codes.
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "irka.hpp"
+
+using namespace mpg;
+
+struct mpg_csr { CsrPtr p; };
+struct mpg_op { OpPtr p; };
+struct mpg_chain { ChainPtr p; };
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return MPG_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return MPG_ERR_INVALID;
+  } catch (const mpg::ConfigError& e) {
+    g_err = e.what();
+    return MPG_ERR_CONFIG;
+  } catch (const mpg::SolverError& e) {
+    g_err = e.what();
+    return MPG_ERR_SOLVER;
+  } catch (const mpg::CudaError& e) {
+    g_err = e.what();
+    return MPG_ERR_CUDA;
+  } catch (const std::bad_alloc&) {
+    g_err = "device or host allocation failed";
+    return MPG_ERR_NOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MPG_ERR_LOGIC;
+  }
+}
+
+SpaiOptions to_spai(const mpg_spai_cfg* c) {
+  SpaiOptions o;
+  if (c) {
+    o.pattern_kind = c->pattern_kind;
+    o.power = c->power;
+    o.fill_tol = c->fill_tol;
+    o.max_fill_per_col = c->max_fill_per_col;
+    o.max_pattern_sweeps = c->max_pattern_sweeps;
+  }
+  return o;
+}
+
+GmresOptions to_gmres(const mpg_gmres_cfg* c) {
+  GmresOptions o;
+  if (c) {
+    o.rel_tol = c->rel_tol;
+    o.max_iter = c->max_iter;
+    o.record_history = c->record_history != 0;
+  }
+  return o;
+}
+
+void fill(const GmresOutcome& o, mpg_gmres_report* r, double* history) {
+  if (r) {
+    r->iterations = o.iterations;
+    r->converged = o.converged;
+    r->breakdown = o.breakdown;
+    r->history_len = int(o.history.size());
+    r->rhs_norm = o.rhs_norm;
+    r->final_residual = o.final_residual;
+    r->solve_seconds = o.solve_seconds;
+  }
+  if (history && !o.history.empty()) std::memcpy(history, o.history.data(), o.history.size() * sizeof(double));
+}
+
+// A plain operator M x wrapped as the shifted family with sigma = 0, ca = +1.
+std::mutex g_plain_mu;
+OpPtr plain_op(const CsrPtr& m) {
+  std::scoped_lock l(g_plain_mu);
+  static std::map<const DevCsr*, std::weak_ptr<ShiftedOp>> cache;
+  auto it = cache.find(m.get());
+  if (it != cache.end())
+    if (auto sp = it->second.lock()) return sp;
+  if (m->nrows != m->ncols) throw std::invalid_argument("gmres: operator must be square");
+  OpPtr op = op_create(m, nullptr);
+  cache[m.get()] = op;
+  return op;
+}
+}  // namespace
+
+extern "C" {
+
+const char* mpg_last_error(void) { return g_err.c_str(); }
+
+int mpg_device_count(int* count) {
+  return guard([&] {
+    if (cudaGetDeviceCount(count) != cudaSuccess) {
+      cudaGetLastError();
+      *count = 0;
+    }
+  });
+}
+
+int mpg_stream(int device, void** stream) {
+  return guard([&] { *stream = ctx(device).stream; });
+}
+
+int mpg_synchronize(int device) {
+  return guard([&] {
+    DeviceGuard g(device);
+    MPG_CUDA(cudaStreamSynchronize(ctx(device).stream));
+  });
+}
+
+long long mpg_launch_count(void) { return g_launches.load(); }
+
+int mpg_copy(void* dst, const void* src, int64_t bytes) {
+  return guard([&] { MPG_CUDA(cudaMemcpy(dst, src, size_t(bytes), cudaMemcpyDefault)); });
+}
+
+// ---- matrices -------------------------------------------------------------------
+int mpg_csr_create(int device, int64_t nrows, int64_t ncols, const int64_t* rowptr, const int64_t* colind,
+                   const double* values, mpg_csr** out) {
+  return guard([&] { *out = new mpg_csr{csr_from_host(device, nrows, ncols, rowptr, colind, values)}; });
+}
+void mpg_csr_destroy(mpg_csr* m) { delete m; }
+int mpg_csr_info(const mpg_csr* m, int64_t* nr, int64_t* nc, int64_t* nnz) {
+  return guard([&] {
+    *nr = m->p->nrows;
+    *nc = m->p->ncols;
+    *nnz = m->p->nnz;
+  });
+}
+int mpg_csr_download(const mpg_csr* m, int64_t* rowptr, int64_t* colind, double* values) {
+  return guard([&] {
+    const DevCsr& d = *m->p;
+    auto& c = ctx(d.device);
+    DeviceGuard g(d.device);
+    std::vector<int> rp(size_t(d.nrows) + 1), ci(static_cast<size_t>(d.nnz));
+    MPG_CUDA(cudaMemcpyAsync(rp.data(), d.rowptr.get(), rp.size() * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (d.nnz) {
+      MPG_CUDA(cudaMemcpyAsync(ci.data(), d.colind.get(), ci.size() * 4, cudaMemcpyDeviceToHost, c.stream));
+      MPG_CUDA(cudaMemcpyAsync(values, d.val.get(), size_t(d.nnz) * 8, cudaMemcpyDefault, c.stream));
+    }
+    MPG_CUDA(cudaStreamSynchronize(c.stream));
+    for (size_t i = 0; i < rp.size(); ++i) rowptr[i] = rp[i];
+    for (size_t i = 0; i < ci.size(); ++i) colind[i] = ci[i];
+  });
+}
+
+static void spmv_any(const DevCsr& m, const double* x, double* y) {
+  auto& c = ctx(m.device);
+  DeviceGuard g(m.device);
+  DBuf<double> dx(m.device, size_t(m.ncols) + 1), dy(m.device, size_t(m.nrows) + 1);
+  copy_in(dx.get(), x, size_t(m.ncols), c.stream);
+  launch_spmv(m, dx.get(), dy.get(), 1.0, c.stream);
+  copy_out(y, dy.get(), size_t(m.nrows), c.stream);
+  MPG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+int mpg_csr_multiply(const mpg_csr* m, const double* x, double* y) {
+  return guard([&] { spmv_any(*m->p, x, y); });
+}
+int mpg_csr_multiply_transpose(const mpg_csr* m, const double* x, double* y) {
+  return guard([&] { spmv_any(*csr_transpose_cached(m->p), x, y); });
+}
+int mpg_csr_transpose(const mpg_csr* m, mpg_csr** out) {
+  return guard([&] { *out = new mpg_csr{csr_transpose(*m->p)}; });
+}
+double mpg_csr_frobenius_norm(const mpg_csr* m) {
+  double r = 0.0;
+  guard([&] {
+    const DevCsr& d = *m->p;
+    auto& c = ctx(d.device);
+    DeviceGuard g(d.device);
+    r = std::sqrt(device_norm2(d.device, d.val.get(), d.nnz, c.stream));
+  });
+  return r;
+}
+
+// ---- shifted operator -------------------------------------------------------------
+int mpg_op_create(const mpg_csr* a, const mpg_csr* e, mpg_op** out) {
+  return guard([&] { *out = new mpg_op{op_create(a->p, e ? e->p : nullptr)}; });
+}
+void mpg_op_destroy(mpg_op* op) { delete op; }
+int64_t mpg_op_dim(const mpg_op* op) { return op->p->n; }
+int mpg_op_apply(const mpg_op* op, double sre, double sim, int transpose, const double* x, double* y) {
+  return guard([&] {
+    const ShiftedOp& o = *op->p;
+    auto& c = ctx(o.device);
+    DeviceGuard g(o.device);
+    const int64_t len = sim != 0.0 ? 2 * o.n : o.n;
+    DBuf<double> dx(o.device, size_t(len) + 1), dy(o.device, size_t(len) + 1);
+    copy_in(dx.get(), x, size_t(len), c.stream);
+    launch_op(o, transpose != 0, sre, sim, -1.0, dx.get(), dy.get(), nullptr, 1.0, c.stream, nullptr);
+    copy_out(y, dy.get(), size_t(len), c.stream);
+    MPG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int mpg_op_explicit(const mpg_op* op, double sre, double sim, int transpose, mpg_csr** out) {
+  return guard([&] { *out = new mpg_csr{op_explicit(*op->p, sre, sim, transpose != 0)}; });
+}
+
+// ---- preconditioner builds ------------------------------------------------------------
+int mpg_spai_build(const mpg_csr* a, const mpg_spai_cfg* cfg, mpg_csr** p, double* column_residuals,
+                   int64_t* fallback_count, double* build_seconds) {
+  return guard([&] {
+    SpaiOutcome o = spai_or_update(a->p, nullptr, to_spai(cfg), column_residuals != nullptr);
+    if (column_residuals) std::memcpy(column_residuals, o.column_residuals.data(), o.column_residuals.size() * 8);
+    if (fallback_count) *fallback_count = o.fallback_count;
+    if (build_seconds) *build_seconds = o.build_seconds;
+    *p = new mpg_csr{o.p};
+  });
+}
+
+int mpg_update_build(const mpg_csr* a_prev, const mpg_csr* a_new, const mpg_spai_cfg* cfg, mpg_csr** q,
+                     double* min_residual, double* matrix_change, int64_t* fallback_count, double* build_seconds) {
+  return guard([&] {
+    SpaiOutcome o = spai_or_update(a_new->p, a_prev->p, to_spai(cfg), false);
+    if (min_residual) *min_residual = o.min_residual;
+    if (matrix_change) *matrix_change = o.matrix_change;
+    if (fallback_count) *fallback_count = o.fallback_count;
+    if (build_seconds) *build_seconds = o.build_seconds;
+    *q = new mpg_csr{o.p};
+  });
+}
+
+int mpg_spai_column_solve(const mpg_csr* a, int64_t col, int64_t npattern, const int64_t* pattern, double* values,
+                          double* residual, int* rank_deficient) {
+  // Fixed-pattern solve (spai.cpp:158-173) through the same warp kernel.
+  return guard([&] {
+    std::vector<double> v;
+    bool rd = false;
+    spai_column_solve_dev(a->p, col, std::vector<int64_t>(pattern, pattern + std::max<int64_t>(npattern, 0)), v,
+                          *residual, rd);
+    std::memcpy(values, v.data(), v.size() * 8);
+    *rank_deficient = rd;
+  });
+}
+
+// ---- chains ---------------------------------------------------------------------------------
+int mpg_chain_create(const mpg_csr* base, mpg_chain** out) {
+  return guard([&] {
+    if (base->p->nrows != base->p->ncols) throw std::invalid_argument("chain: base must be square");
+    auto c = std::make_shared<Chain>();
+    c->factors.push_back(base->p);
+    *out = new mpg_chain{c};
+  });
+}
+int mpg_chain_extend(const mpg_chain* chain, const mpg_csr* q, mpg_chain** out) {
+  return guard([&] {
+    if (!chain || !chain->p) throw std::logic_error("chain: cannot extend an empty chain");
+    if (!q) throw std::invalid_argument("chain: null update factor");
+    const int64_t d = chain->p->factors[0]->nrows;
+    if (q->p->nrows != d || q->p->ncols != d) throw std::invalid_argument("chain: factor dimension mismatch");
+    auto c = std::make_shared<Chain>(*chain->p);
+    c->factors.push_back(q->p);
+    *out = new mpg_chain{c};
+  });
+}
+void mpg_chain_destroy(mpg_chain* chain) { delete chain; }
+int mpg_chain_length(const mpg_chain* chain) { return chain->p->length(); }
+const void* mpg_chain_factor_id(const mpg_chain* chain, int i) {
+  if (i < 0 || i >= int(chain->p->factors.size())) return nullptr;
+  return chain->p->factors[size_t(i)].get();
+}
+int mpg_chain_apply(const mpg_chain* chain, const double* x, double* y) {
+  return guard([&] {
+    const Chain& ch = *chain->p;
+    const DevCsr& base = *ch.factors[0];
+    auto& c = ctx(base.device);
+    DeviceGuard g(base.device);
+    const size_t n = size_t(base.nrows);
+    DBuf<double> dx(base.device, n + 1), dy(base.device, n + 1), tmp(base.device, n + 1);
+    copy_in(dx.get(), x, n, c.stream);
+    launch_chain(ch, dx.get(), dy.get(), tmp.get(), c.stream);
+    copy_out(y, dy.get(), n, c.stream);
+    MPG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+}  // extern "C"
+
+namespace mpg {
+double std_residual_public(const CsrPtr& m, const ChainPtr& ch);
+}
+
+extern "C" {
+
+int mpg_standard_residual(const mpg_csr* a, const mpg_chain* chain, double* out) {
+  return guard([&] {
+    if (a->p->nrows != a->p->ncols || a->p->nrows != chain->p->factors[0]->nrows)
+      throw std::invalid_argument("standard_residual: dimension mismatch");
+    *out = std_residual_public(a->p, chain->p);
+  });
+}
+
+// ---- GMRES ------------------------------------------------------------------------------------
+int mpg_gmres_csr(const mpg_csr* m, const mpg_chain* chain, const double* b, double* x, const mpg_gmres_cfg* cfg,
+                  mpg_gmres_report* report, double* history) {
+  return guard([&] {
+    OpPtr op = plain_op(m->p);
+    std::vector<SolveSpec> specs(1);
+    specs[0].ca = 1.0;
+    specs[0].chain = chain ? chain->p : nullptr;
+    specs[0].b = b;
+    specs[0].x = x;
+    auto out = gmres_batch(*op, specs, to_gmres(cfg));
+    fill(out[0], report, history);
+  });
+}
+
+int mpg_gmres_shifted(const mpg_op* op, double sre, double sim, int transpose, const mpg_chain* chain, const double* b,
+                      double* x, const mpg_gmres_cfg* cfg, mpg_gmres_report* report, double* history) {
+  return guard([&] {
+    std::vector<SolveSpec> specs(1);
+    specs[0].sre = sre;
+    specs[0].sim = sim;
+    specs[0].transpose = transpose != 0;
+    specs[0].chain = chain ? chain->p : nullptr;
+    specs[0].b = b;
+    specs[0].x = x;
+    auto out = gmres_batch(*op->p, specs, to_gmres(cfg));
+    fill(out[0], report, history);
+  });
+}
+
+int mpg_gmres_batch(const mpg_op* op, int nsolves, const double* sre, const double* sim, const int* transpose,
+                    const mpg_chain* const* chains, const double* const* b, double* const* x,
+                    const mpg_gmres_cfg* cfg, mpg_gmres_report* reports) {
+  return guard([&] {
+    std::vector<SolveSpec> specs(size_t(std::max(nsolves, 0)));
+    for (int i = 0; i < nsolves; ++i) {
+      specs[size_t(i)].sre = sre[i];
+      specs[size_t(i)].sim = sim ? sim[i] : 0.0;
+      specs[size_t(i)].transpose = transpose ? transpose[i] != 0 : false;
+      specs[size_t(i)].chain = chains && chains[i] ? chains[i]->p : nullptr;
+      specs[size_t(i)].b = b[i];
+      specs[size_t(i)].x = x[i];
+    }
+    auto out = gmres_batch(*op->p, specs, to_gmres(cfg));
+    for (int i = 0; i < nsolves; ++i) fill(out[size_t(i)], reports ? reports + i : nullptr, nullptr);
+  });
+}
+
+// ---- IRKA / sweep -------------------------------------------------------------------------------
+static IrkaSettings to_irka(const mpg_irka_cfg* c, int mode, const double* init_shifts) {
+  IrkaSettings s;
+  s.r = c->r;
+  s.tol = c->tol;
+  s.max_sweeps = c->max_sweeps;
+  s.seed = c->seed;
+  s.gmres = to_gmres(&c->gmres);
+  s.spai = to_spai(&c->spai);
+  s.max_chain_len = c->max_chain_len;
+  s.standard_residual_max_dim = c->standard_residual_max_dim;
+  s.mode = mode;
+  if (init_shifts) s.init_shifts.assign(init_shifts, init_shifts + c->r);
+  return s;
+}
+
+static void copy_rows(const std::vector<mpg_report_row>& rows, mpg_report_row* out, int max_rows, int* nrows) {
+  if (nrows) *nrows = int(rows.size());
+  for (size_t i = 0; out && i < rows.size() && int(i) < max_rows; ++i) out[i] = rows[i];
+}
+
+int mpg_irka_reduce(const mpg_op* op, const double* b, int m, const double* c, int q, const mpg_irka_cfg* cfg,
+                    int mode, const double* init_shifts, double* kr, double* fr, double* cr, double* er, double* ar,
+                    double* lam_re, double* lam_im, double* v, double* w, int* sweeps, int* converged,
+                    mpg_report_row* rows, int max_rows, int* nrows) {
+  return guard([&] {
+    IrkaSettings s = to_irka(cfg, mode, init_shifts);
+    s.want_vw = v || w;
+    IrkaResult r = irka_run(*op->p, b, m, c, q, s, 0, 1, nullptr, nullptr);
+    if (kr) std::memcpy(kr, r.kr.a.data(), r.kr.a.size() * 8);
+    if (fr) std::memcpy(fr, r.fr.a.data(), r.fr.a.size() * 8);
+    if (cr) std::memcpy(cr, r.cr.a.data(), r.cr.a.size() * 8);
+    if (er) std::memcpy(er, r.er.a.data(), r.er.a.size() * 8);
+    if (ar) std::memcpy(ar, r.ar.a.data(), r.ar.a.size() * 8);
+    for (size_t i = 0; i < r.lambda.size(); ++i) {
+      if (lam_re) lam_re[i] = r.lambda[i].re;
+      if (lam_im) lam_im[i] = r.lambda[i].im;
+    }
+    if (v) std::memcpy(v, r.v.data(), r.v.size() * 8);
+    if (w) std::memcpy(w, r.w.data(), r.w.size() * 8);
+    if (sweeps) *sweeps = r.sweeps;
+    if (converged) *converged = r.converged;
+    copy_rows(r.rows, rows, max_rows, nrows);
+  });
+}
+
+int mpg_irka_reduce_sharded(const mpg_op* op, const double* b, int m, const double* c, int q,
+                            const mpg_irka_cfg* cfg, int mode, const double* init_shifts, int rank, int world,
+                            mpg_allgather_fn allgather, void* actx, double* kr, double* fr, double* cr,
+                            double* lam_re, double* lam_im, int* sweeps, int* converged, mpg_report_row* rows,
+                            int max_rows, int* nrows) {
+  return guard([&] {
+    IrkaSettings s = to_irka(cfg, mode, init_shifts);
+    IrkaResult r = irka_run(*op->p, b, m, c, q, s, rank, world, allgather, actx);
+    if (kr) std::memcpy(kr, r.kr.a.data(), r.kr.a.size() * 8);
+    if (fr) std::memcpy(fr, r.fr.a.data(), r.fr.a.size() * 8);
+    if (cr) std::memcpy(cr, r.cr.a.data(), r.cr.a.size() * 8);
+    for (size_t i = 0; i < r.lambda.size(); ++i) {
+      if (lam_re) lam_re[i] = r.lambda[i].re;
+      if (lam_im) lam_im[i] = r.lambda[i].im;
+    }
+    if (sweeps) *sweeps = r.sweeps;
+    if (converged) *converged = r.converged;
+    copy_rows(r.rows, rows, max_rows, nrows);
+  });
+}
+
+int mpg_spai_bench(const mpg_op* op, const double* b, int npoints, const double* points, const mpg_spai_cfg* spai,
+                   const mpg_gmres_cfg* gmres, int mode, int max_chain_len, double* x_out, mpg_report_row* rows,
+                   int max_rows, int* nrows, int* failed) {
+  return guard([&] {
+    SweepOutcome o = sweep_run(*op->p, b, std::vector<double>(points, points + std::max(npoints, 0)), to_spai(spai),
+                               to_gmres(gmres), mode, max_chain_len, x_out);
+    copy_rows(o.rows, rows, max_rows, nrows);
+    if (failed) *failed = o.failed;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,569 @@
+// IRKA driver (BIRKA with N = 0, proj/src/birka.cpp:139-310), generalised to
+// a mass matrix E, plus the shift-sweep benchmark (run_spai_bench,
+// proj/src/bench.cpp:159-249).
+//
+// Per sweep: real block spectrum of K_r on the host (r x r), right-hand
+// sides B f2 / C c2 on the device, one GMRES per shift unit and side (the
+// reference's joint n*r solve is block diagonal for N = 0, so the units are
+// independent), all advanced together by gmres_batch;
+// V, W by CholQR2 (K5: tall-skinny Gram + small triangular apply), the
+// projection E_r = W^T E V, A_r = W^T A V, K_r = E_r^{-1} A_r,
+// f_r = E_r^{-1} W^T B, c_r = V^T C; convergence on the sorted spectrum.
+// With E = I this is the reference's update (E_r = W^T V).
+//
+// Multi-GPU: (side, unit) solves are sharded by a static slot -> rank map so
+// each preconditioner chain stays on its rank; the only exchange is the
+// all-gather of the solved V/W columns (K6), after which every rank projects
+// redundantly.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <random>
+
+#include "host/small_dense.hpp"
+#include "irka.hpp"
+
+namespace mpg {
+namespace {
+
+using host::Mat;
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// part[blk][i + a*j] = sum over this block's rows of X[row, i] * Y[row, j]
+__global__ void __launch_bounds__(256) k_ts_gram(const double* __restrict__ X, int64_t ldx, int a,
+                                                 const double* __restrict__ Y, int64_t ldy, int b, int64_t n,
+                                                 double* __restrict__ part) {
+  extern __shared__ double sm[];
+  constexpr int CH = 64;
+  double* xs = sm;           // CH * a
+  double* ys = sm + CH * a;  // CH * b
+  const int npair = a * b;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t r0 = int64_t(blockIdx.x) * CH; r0 < n; r0 += int64_t(gridDim.x) * CH) {
+    const int rows = n - r0 < CH ? int(n - r0) : CH;
+    __syncthreads();
+    for (int t = threadIdx.x; t < CH * a; t += blockDim.x) {
+      const int i = t / CH, r = t % CH;
+      xs[t] = r < rows ? X[r0 + r + ldx * i] : 0.0;
+    }
+    for (int t = threadIdx.x; t < CH * b; t += blockDim.x) {
+      const int j = t / CH, r = t % CH;
+      ys[t] = r < rows ? Y[r0 + r + ldy * j] : 0.0;
+    }
+    __syncthreads();
+    for (int q = 0; q < 4; ++q) {
+      const int pidx = threadIdx.x + q * blockDim.x;
+      if (pidx >= npair) break;
+      const int i = pidx % a, j = pidx / a;
+      double s = acc[q];
+      for (int r = 0; r < CH; ++r) s = fma(xs[i * CH + r], ys[j * CH + r], s);
+      acc[q] = s;
+    }
+  }
+  for (int q = 0; q < 4; ++q) {
+    const int pidx = threadIdx.x + q * blockDim.x;
+    if (pidx < npair) part[size_t(blockIdx.x) * npair + pidx] = acc[q];
+  }
+}
+
+// Y[:, j] = sum_i X[:, i] M[i, j]   (M is a x b, column-major, in global memory)
+__global__ void __launch_bounds__(256) k_ts_apply(const double* __restrict__ X, int64_t ldx, int a,
+                                                  const double* __restrict__ M, int b, double* __restrict__ Y,
+                                                  int64_t ldy, int64_t n) {
+  extern __shared__ double ms[];
+  for (int t = threadIdx.x; t < a * b; t += blockDim.x) ms[t] = M[t];
+  __syncthreads();
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n; r += int64_t(gridDim.x) * blockDim.x) {
+    double xr[64];
+    for (int i = 0; i < a; ++i) xr[i] = X[r + ldx * i];
+    for (int j = 0; j < b; ++j) {
+      double s = 0.0;
+      for (int i = 0; i < a; ++i) s = fma(xr[i], ms[i + a * j], s);
+      Y[r + ldy * j] = s;
+    }
+  }
+}
+
+__global__ void k_fill_zero(double* p, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) p[i] = 0.0;
+}
+
+Mat ts_gram(int dev, const double* X, int64_t ldx, int a, const double* Y, int64_t ldy, int b, int64_t n) {
+  auto& c = ctx(dev);
+  const int blocks = std::max(1, std::min<int>(c.sm_count * 2, int((n + 63) / 64)));
+  DBuf<double> part(dev, size_t(blocks) * size_t(a) * size_t(b));
+  const size_t smem = size_t(64) * size_t(a + b) * sizeof(double);
+  if (a * b > 1024) throw std::invalid_argument("ts_gram: reduced order too large");
+  k_ts_gram<<<blocks, 256, smem, c.stream>>>(X, ldx, a, Y, ldy, b, n, part.get());
+  MPG_CHECK_LAUNCH();
+  count_launch();
+  std::vector<double> h(part.n);
+  MPG_CUDA(cudaMemcpyAsync(h.data(), part.get(), h.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  MPG_CUDA(cudaStreamSynchronize(c.stream));
+  Mat out(a, b);
+  for (int blk = 0; blk < blocks; ++blk)
+    for (int p = 0; p < a * b; ++p) out.a[size_t(p)] += h[size_t(blk) * size_t(a * b) + size_t(p)];
+  return out;
+}
+
+void ts_apply(int dev, const double* X, int64_t ldx, int a, const Mat& M, double* Y, int64_t ldy, int64_t n) {
+  auto& c = ctx(dev);
+  if (a > 64) throw std::invalid_argument("ts_apply: at most 64 columns");
+  DBuf<double> dm(dev, M.a.size());
+  MPG_CUDA(cudaMemcpyAsync(dm.get(), M.a.data(), M.a.size() * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  const int blocks = std::max(1, std::min<int>(c.sm_count * 8, int((n + 255) / 256)));
+  k_ts_apply<<<blocks, 256, M.a.size() * sizeof(double), c.stream>>>(X, ldx, a, dm.get(), M.cols, Y, ldy, n);
+  MPG_CHECK_LAUNCH();
+  count_launch();
+  MPG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+// CholQR2 in place on X (n x r, ld = n); returns false if X is rank deficient.
+bool cholqr2(int dev, double* X, int64_t n, int r) {
+  DBuf<double> tmp(dev, size_t(n) * size_t(r));
+  for (int pass = 0; pass < 2; ++pass) {
+    const Mat g = ts_gram(dev, X, n, r, X, n, r, n);
+    Mat R;
+    if (!host::cholesky_upper(g, R)) return false;
+    // reject a numerically rank-deficient block (Cholesky of the Gram squares kappa)
+    double dmax = 0.0, dmin = 1e300;
+    for (int i = 0; i < r; ++i) { dmax = std::max(dmax, R(i, i)); dmin = std::min(dmin, R(i, i)); }
+    if (pass == 0 && dmin < 1e-7 * dmax) return false;
+    ts_apply(dev, X, n, r, host::upper_inverse(R), tmp.get(), n, n);
+    MPG_CUDA(cudaMemcpyAsync(X, tmp.get(), size_t(n) * size_t(r) * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx(dev).stream));
+  }
+  MPG_CUDA(cudaStreamSynchronize(ctx(dev).stream));
+  return true;
+}
+
+void orthonormalize(int dev, double* X, int64_t n, int r) {
+  if (cholqr2(dev, X, n, r)) return;
+  // Host Householder fallback (thin_q, birka.cpp:125-128) for ill-conditioned blocks.
+  auto& c = ctx(dev);
+  Mat h(int(n), r);
+  MPG_CUDA(cudaMemcpyAsync(h.a.data(), X, h.a.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  MPG_CUDA(cudaStreamSynchronize(c.stream));
+  Mat q = host::householder_q(h);
+  MPG_CUDA(cudaMemcpyAsync(X, q.a.data(), q.a.size() * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  MPG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+double std_residual(const CsrPtr& m, const ChainPtr& ch) {
+  // ||I - M P||_F / sqrt(n) (chain.cpp:140-157)
+  const int dev = m->device;
+  auto& c = ctx(dev);
+  const int64_t n = m->nrows;
+  if (n == 0) return 0.0;
+  DBuf<double> e(dev, size_t(n)), pe(dev, size_t(n)), ape(dev, size_t(n)), tmp(dev, size_t(n));
+  double sq = 0.0;
+  MPG_CUDA(cudaMemsetAsync(e.get(), 0, size_t(n) * sizeof(double), c.stream));
+  const double one = 1.0, zero = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    MPG_CUDA(cudaMemcpyAsync(e.get() + j, &one, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    launch_chain(*ch, e.get(), pe.get(), tmp.get(), c.stream);
+    launch_spmv(*m, pe.get(), ape.get(), 1.0, c.stream);
+    double aj = 0.0;
+    MPG_CUDA(cudaMemcpyAsync(&aj, ape.get() + j, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    const double nrm = device_norm2(dev, ape.get(), n, c.stream);  // syncs
+    sq += nrm - aj * aj + (aj - 1.0) * (aj - 1.0);
+    MPG_CUDA(cudaMemcpyAsync(e.get() + j, &zero, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  }
+  return std::sqrt(std::max(sq, 0.0)) / std::sqrt(double(n));
+}
+
+}  // namespace
+
+double std_residual_public(const CsrPtr& m, const ChainPtr& ch) { return std_residual(m, ch); }
+
+namespace {
+
+struct SlotPrecond {
+  ChainPtr chain;
+  CsrPtr prev_explicit;
+  int width = 0;
+};
+
+}  // namespace
+
+IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const double* c_any, int q, const IrkaSettings& cfg,
+                    int rank, int world, mpg_allgather_fn allgather, void* agctx) {
+  const int dev = op.device;
+  auto& cx = ctx(dev);
+  DeviceGuard guard(dev);
+  cudaStream_t s = cx.stream;
+  const int64_t n = op.n;
+  const int r = cfg.r;
+  if (m < 1 || q < 1) throw ConfigError("irka: B and C need at least one column");
+  if (cfg.max_sweeps < 1) throw ConfigError("birka: max_sweeps must be at least 1");
+  if (cfg.max_chain_len < 1) throw ConfigError("birka: max_chain_len must be at least 1");
+  if (r < 1) throw ConfigError("birka: reduced order must be at least 1");
+  if (int64_t(r) > n) throw ConfigError("birka: reduced order exceeds the system dimension");
+  if (r > 64 || m > 64 || q > 64) throw ConfigError("irka: r, m, q are limited to 64 on the GPU path");
+  if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("irka: bad rank/world");
+
+  DBuf<double> B(dev, size_t(n) * m), C(dev, size_t(n) * q);
+  copy_in(B.get(), b_any, size_t(n) * m, s);
+  copy_in(C.get(), c_any, size_t(n) * q, s);
+
+  // ---- initial state (birka_default_seed, birka.cpp:41-89) ----
+  Mat kr(r, r), fr(r, m), cr(r, q);
+  {
+    std::mt19937_64 rng(cfg.seed);
+    std::uniform_real_distribution<double> unit(-1.0, 1.0);
+    std::vector<double> x(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) x[size_t(i)] = unit(rng);
+    if (cfg.init_shifts.empty()) {
+      double radius = 0.0, xn = 0.0;
+      for (double v : x) xn += v * v;
+      xn = std::sqrt(xn);
+      if (xn > 0.0) {
+        for (double& v : x) v /= xn;
+        DBuf<double> dx(dev, size_t(n)), dy(dev, size_t(n));
+        copy_in(dx.get(), x.data(), size_t(n), s);
+        for (int it = 0; it < 20; ++it) {
+          launch_spmv(*op.a, dx.get(), dy.get(), 1.0, s);
+          const double ny = std::sqrt(device_norm2(dev, dy.get(), n, s));
+          if (ny == 0.0) { radius = 0.0; break; }
+          radius = ny;
+          std::vector<double> hy(static_cast<size_t>(n));
+          MPG_CUDA(cudaMemcpyAsync(hy.data(), dy.get(), size_t(n) * 8, cudaMemcpyDeviceToHost, s));
+          MPG_CUDA(cudaStreamSynchronize(s));
+          for (double& v : hy) v /= ny;
+          copy_in(dx.get(), hy.data(), size_t(n), s);
+        }
+      }
+      if (!(radius > 0.0) || !std::isfinite(radius)) radius = 1.0;
+      for (int i = 0; i < r; ++i) {
+        const double t = r == 1 ? 1.0 : double(i) / (r - 1);
+        kr(i, i) = -radius * std::pow(10.0, -3.0 * (1.0 - t));
+      }
+    } else {
+      if (int(cfg.init_shifts.size()) != r) throw ConfigError("irka: init_shifts must have r entries");
+      for (int i = 0; i < r; ++i) kr(i, i) = -cfg.init_shifts[size_t(i)];
+    }
+    for (Mat* mm : {&fr, &cr})
+      for (int j = 0; j < mm->cols; ++j) {
+        double nn = 0.0;
+        for (int i = 0; i < r; ++i) { (*mm)(i, j) = unit(rng); nn += (*mm)(i, j) * (*mm)(i, j); }
+        nn = std::sqrt(nn);
+        if (nn > 0.0)
+          for (int i = 0; i < r; ++i) (*mm)(i, j) /= nn;
+      }
+  }
+
+  IrkaResult res;
+  res.reduced_order = r;
+  DBuf<double> X(dev, size_t(n) * r), Y(dev, size_t(n) * r), RHS(dev, size_t(n) * r * 2);
+  DBuf<double> AV(dev, size_t(n) * r), EV(dev, size_t(n) * r);
+  std::map<std::pair<int, int>, SlotPrecond> slots;   // (side, first column)
+  std::map<std::pair<int, int>, ChainPtr> frozen;      // (side, unit width) -> frozen base
+  std::mt19937_64 perturb_rng(cfg.seed ^ 0x9e3779b97f4a7c15ull);
+  std::vector<host::Eig> lambda_prev = host::sorted_eigenvalues(kr);
+  bool converged = false;
+  int sweeps_done = 0;
+  const GmresOptions gopt = cfg.gmres;
+
+  for (int z = 1; z <= cfg.max_sweeps && !converged; ++z) {
+    host::Spectrum spec;
+    if (!host::real_spectrum(kr, spec)) {  // birka.cpp:167-180
+      std::uniform_real_distribution<double> unit(-1.0, 1.0);
+      Mat nudged = kr;
+      const double scale = 1e-8 * std::max(1.0, host::fro(kr));
+      for (double& v : nudged.a) v += scale * unit(perturb_rng);
+      if (!host::real_spectrum(nudged, spec))
+        throw SolverError("birka: reduced state matrix is not diagonalizable (sweep " + std::to_string(z) +
+                          "), even after perturbation");
+      kr = nudged;
+      lambda_prev = host::sorted_eigenvalues(kr);
+    }
+    const Mat f2t = host::mul(host::transpose(spec.basis_inv), fr);  // (f2)^T = R^{-1} fr   (r x m)
+    const Mat c2t = host::mul(host::transpose(spec.basis), cr);      // (c2)^T = R^T cr      (r x q)
+    // right-hand sides: side 0 columns B f2 -> RHS[:, 0..r), side 1 C c2 -> RHS[:, r..2r)
+    ts_apply(dev, B.get(), n, m, host::transpose(f2t), RHS.get(), n, n);
+    ts_apply(dev, C.get(), n, q, host::transpose(c2t), RHS.get() + size_t(n) * r, n, n);
+    for (int side = 0; side < 2; ++side) {
+      const double bn = device_norm2(dev, RHS.get() + size_t(n) * r * side, n * r, s);
+      if (bn == 0.0)
+        throw SolverError(std::string("birka: zero right-hand side on the ") + (side == 0 ? "trial" : "test") +
+                          " side (sweep " + std::to_string(z) + "); input/output maps must be nonzero");
+    }
+    // ---- solve tasks for this rank ----
+    struct Task { int side, c0, w; double sre, sim; };
+    std::vector<Task> mine, all;
+    for (int side = 0; side < 2; ++side)
+      for (size_t u = 0; u < spec.unit_start.size(); ++u) {
+        const int c0 = spec.unit_start[u], w = spec.unit_width[u];
+        Task t{side, c0, w, -spec.blocks(c0, c0), w == 2 ? -spec.blocks(c0, c0 + 1) : 0.0};
+        all.push_back(t);
+        if ((side * r + c0) % world == rank) mine.push_back(t);
+      }
+    std::vector<SolveSpec> specs;
+    std::vector<mpg_report_row> rows;
+    DBuf<double> SOL(dev, size_t(n) * r * 2);
+    for (const Task& t : mine) {
+      mpg_report_row row{};
+      row.sweep = z;
+      row.point = t.side + 1;
+      row.kind = MPG_KIND_NONE;
+      row.min_residual = row.matrix_change = row.standard_residual = std::nan("");
+      ChainPtr chain;
+      if (cfg.mode != MPG_PRECOND_NONE) {
+        const auto key = std::make_pair(t.side, t.c0);
+        const bool tr = t.side == 1;
+        if (cfg.mode == MPG_PRECOND_REUSE_FROZEN) {
+          auto fk = std::make_pair(t.side, t.w);
+          auto it = frozen.find(fk);
+          if (it == frozen.end() && t.w == 2 && frozen.count({t.side, 1})) {
+            chain = frozen[{t.side, 1}];  // n x n base applied blockwise on the pair
+            row.kind = MPG_KIND_REUSED_SAME_MATRIX;
+          } else if (it == frozen.end()) {
+            CsrPtr M = op_explicit(op, t.sre, t.sim, tr);
+            SpaiOutcome so = spai_or_update(M, nullptr, cfg.spai, false);
+            auto ch = std::make_shared<Chain>();
+            ch->factors.push_back(so.p);
+            chain = ch;
+            frozen[fk] = chain;
+            row.kind = MPG_KIND_FRESH;
+            row.build_seconds = so.build_seconds;
+            if (M->nrows <= cfg.standard_residual_max_dim) row.standard_residual = std_residual(M, chain);
+          } else {
+            chain = it->second;
+            row.kind = MPG_KIND_REUSED_SAME_MATRIX;
+          }
+        } else {
+          CsrPtr M = op_explicit(op, t.sre, t.sim, tr);
+          SlotPrecond& sp = slots[key];
+          if (sp.width != t.w) sp = SlotPrecond{nullptr, nullptr, t.w};
+          if (cfg.mode == MPG_PRECOND_FRESH || !sp.chain || sp.chain->length() + 1 > cfg.max_chain_len) {
+            SpaiOutcome so = spai_or_update(M, nullptr, cfg.spai, false);
+            auto ch = std::make_shared<Chain>();
+            ch->factors.push_back(so.p);
+            sp.chain = ch;
+            row.kind = MPG_KIND_FRESH;
+            row.build_seconds = so.build_seconds;
+          } else {
+            SpaiOutcome so = spai_or_update(M, sp.prev_explicit, cfg.spai, false);
+            auto ch = std::make_shared<Chain>(*sp.chain);
+            ch->factors.push_back(so.p);
+            sp.chain = ch;
+            row.kind = MPG_KIND_VERTICAL;
+            row.build_seconds = so.build_seconds;
+            row.min_residual = so.min_residual;
+            row.matrix_change = so.matrix_change;
+          }
+          if (cfg.mode == MPG_PRECOND_REUSE_CHAIN) sp.prev_explicit = M;
+          chain = sp.chain;
+          if (M->nrows <= cfg.standard_residual_max_dim) row.standard_residual = std_residual(M, chain);
+        }
+      }
+      SolveSpec sp;
+      sp.sre = t.sre;
+      sp.sim = t.sim;
+      sp.transpose = t.side == 1;
+      sp.chain = chain;
+      sp.b = RHS.get() + size_t(n) * (size_t(r) * t.side + t.c0);
+      sp.x = SOL.get() + size_t(n) * (size_t(r) * t.side + t.c0);
+      specs.push_back(sp);
+      rows.push_back(row);
+    }
+    // batches bounded by device memory (each solve may grow to max_iter + 2 basis vectors)
+    size_t free_b = 0, total_b = 0;
+    MPG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    cudaMemPool_t pool;
+    MPG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t reserved = 0, used = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    const double avail = double(free_b) + double(reserved - used);
+    const double per_solve = 8.0 * double(2 * n + 64) * double(gopt.max_iter + 8) + 1e7;
+    const int per_batch = std::max(1, std::min<int>(32, int(0.85 * avail / per_solve)));
+    for (size_t b0 = 0; b0 < specs.size(); b0 += size_t(per_batch)) {
+      std::vector<SolveSpec> batch(specs.begin() + long(b0), specs.begin() + long(std::min(specs.size(), b0 + per_batch)));
+      std::vector<GmresOutcome> outc = gmres_batch(op, batch, gopt);
+      for (size_t i = 0; i < outc.size(); ++i) {
+        mpg_report_row& row = rows[b0 + i];
+        row.solves = 1;
+        row.iterations = outc[i].iterations;
+        row.gmres_seconds = outc[i].solve_seconds;
+        res.total_iterations += outc[i].iterations;
+        ++res.total_solves;
+        if (!outc[i].converged) {
+          res.rows.insert(res.rows.end(), rows.begin(), rows.end());
+          const Task& t = mine[b0 + i];
+          throw SolverError(std::string("birka: gmres did not converge on the ") + (t.side == 0 ? "trial" : "test") +
+                            " side (sweep " + std::to_string(z) + ", unit at column " + std::to_string(t.c0) +
+                            "; relative residual " +
+                            std::to_string(outc[i].final_residual / std::max(outc[i].rhs_norm, 1e-300)) + " after " +
+                            std::to_string(outc[i].iterations) + " iterations)");
+        }
+      }
+    }
+    res.rows.insert(res.rows.end(), rows.begin(), rows.end());
+    // ---- exchange (K6): all-gather the solved columns ----
+    if (world > 1) {
+      std::vector<int> owned_cnt(size_t(world), 0);
+      for (const Task& t : all) owned_cnt[size_t((t.side * r + t.c0) % world)] += t.w;
+      const int cmax = *std::max_element(owned_cnt.begin(), owned_cnt.end());
+      DBuf<double> send(dev, size_t(n) * std::max(cmax, 1)), recv(dev, size_t(n) * std::max(cmax, 1) * world);
+      int col = 0;
+      for (const Task& t : mine) {
+        MPG_CUDA(cudaMemcpyAsync(send.get() + size_t(n) * col, SOL.get() + size_t(n) * (size_t(r) * t.side + t.c0),
+                                 size_t(n) * t.w * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        col += t.w;
+      }
+      MPG_CUDA(cudaStreamSynchronize(s));
+      if (!allgather) throw std::invalid_argument("irka: world > 1 needs an allgather callback");
+      if (allgather(agctx, send.get(), recv.get(), int64_t(n) * std::max(cmax, 1) * 8) != 0)
+        throw CudaError("irka: allgather callback failed");
+      std::vector<int> cursor(size_t(world), 0);
+      for (const Task& t : all) {
+        const int owner = (t.side * r + t.c0) % world;
+        const double* src = recv.get() + size_t(n) * (size_t(owner) * std::max(cmax, 1) + cursor[size_t(owner)]);
+        MPG_CUDA(cudaMemcpyAsync(SOL.get() + size_t(n) * (size_t(r) * t.side + t.c0), src,
+                                 size_t(n) * t.w * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        cursor[size_t(owner)] += t.w;
+      }
+      MPG_CUDA(cudaStreamSynchronize(s));
+    }
+    MPG_CUDA(cudaMemcpyAsync(X.get(), SOL.get(), size_t(n) * r * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    MPG_CUDA(cudaMemcpyAsync(Y.get(), SOL.get() + size_t(n) * r, size_t(n) * r * sizeof(double),
+                             cudaMemcpyDeviceToDevice, s));
+    orthonormalize(dev, X.get(), n, r);
+    orthonormalize(dev, Y.get(), n, r);
+    // ---- projection (K5) ----
+    for (int j = 0; j < r; ++j) {
+      launch_spmv(*op.a, X.get() + size_t(n) * j, AV.get() + size_t(n) * j, 1.0, s);
+      if (op.e) launch_spmv(*op.e, X.get() + size_t(n) * j, EV.get() + size_t(n) * j, 1.0, s);
+    }
+    const double* ev = op.e ? EV.get() : X.get();
+    const Mat er = ts_gram(dev, Y.get(), n, r, ev, n, r, n);
+    const Mat ar = ts_gram(dev, Y.get(), n, r, AV.get(), n, r, n);
+    host::LU lu(er);
+    if (!lu.invertible())
+      throw SolverError("birka: projection matrix (test basis^T trial basis) is singular at sweep " + std::to_string(z));
+    kr = lu.solve(ar);
+    fr = lu.solve(ts_gram(dev, Y.get(), n, r, B.get(), n, m, n));
+    cr = ts_gram(dev, X.get(), n, r, C.get(), n, q, n);
+    res.er = er;
+    res.ar = ar;
+    sweeps_done = z;
+    const std::vector<host::Eig> lambda_new = host::sorted_eigenvalues(kr);
+    double num = 0.0, den = 0.0;
+    for (size_t i = 0; i < lambda_new.size(); ++i) {
+      const double dr = lambda_new[i].re - lambda_prev[i].re, di = lambda_new[i].im - lambda_prev[i].im;
+      num += dr * dr + di * di;
+      den += lambda_prev[i].re * lambda_prev[i].re + lambda_prev[i].im * lambda_prev[i].im;
+    }
+    if (std::sqrt(num) / std::max(std::sqrt(den), 1e-300) < cfg.tol) converged = true;
+    lambda_prev = lambda_new;
+  }
+  res.kr = kr;
+  res.fr = fr;
+  res.cr = cr;
+  res.lambda = lambda_prev;
+  res.sweeps = sweeps_done;
+  res.converged = converged;
+  if (cfg.want_vw) {
+    res.v.resize(size_t(n) * r);
+    res.w.resize(size_t(n) * r);
+    MPG_CUDA(cudaMemcpyAsync(res.v.data(), X.get(), res.v.size() * 8, cudaMemcpyDeviceToHost, s));
+    MPG_CUDA(cudaMemcpyAsync(res.w.data(), Y.get(), res.w.size() * 8, cudaMemcpyDeviceToHost, s));
+    MPG_CUDA(cudaStreamSynchronize(s));
+  }
+  return res;
+}
+
+SweepOutcome sweep_run(const ShiftedOp& op, const double* b_any, const std::vector<double>& points,
+                       const SpaiOptions& spai, const GmresOptions& gmres, int mode, int max_chain_len, double* x_out) {
+  if (points.empty()) throw ConfigError("spai-bench: at least one point is required");
+  for (double p : points)
+    if (!(p > 0.0) || !std::isfinite(p)) throw ConfigError("spai-bench: points must be positive and finite");
+  if (max_chain_len < 1) throw ConfigError("spai-bench: max_chain_len must be at least 1");
+  const int dev = op.device;
+  auto& cx = ctx(dev);
+  DeviceGuard guard(dev);
+  cudaStream_t s = cx.stream;
+  const int64_t n = op.n;
+  DBuf<double> b(dev, size_t(n));
+  copy_in(b.get(), b_any, size_t(n), s);
+  if (device_norm2(dev, b.get(), n, s) == 0.0) throw ConfigError("spai-bench: the first input column must be nonzero");
+  SweepOutcome out;
+  std::vector<ChainPtr> chains(points.size());
+  ChainPtr chain;
+  CsrPtr prev;
+  // preconditioners along the sweep (bench.cpp:189-216)
+  for (size_t i = 0; i < points.size(); ++i) {
+    mpg_report_row row{};
+    row.sweep = 1;
+    row.point = int(i) + 1;
+    row.kind = MPG_KIND_NONE;
+    row.min_residual = row.matrix_change = row.standard_residual = std::nan("");
+    if (mode != MPG_PRECOND_NONE) {
+      CsrPtr a = op_explicit(op, points[i], 0.0, false);
+      if (mode == MPG_PRECOND_FRESH || (mode == MPG_PRECOND_REUSE_CHAIN && (i == 0 || chain->length() + 1 > max_chain_len)) ||
+          (mode == MPG_PRECOND_REUSE_FROZEN && i == 0)) {
+        SpaiOutcome so = spai_or_update(a, nullptr, spai, false);
+        auto ch = std::make_shared<Chain>();
+        ch->factors.push_back(so.p);
+        chain = ch;
+        row.kind = MPG_KIND_FRESH;
+        row.build_seconds = so.build_seconds;
+      } else if (mode == MPG_PRECOND_REUSE_CHAIN) {
+        SpaiOutcome so = spai_or_update(a, prev, spai, false);
+        auto ch = std::make_shared<Chain>(*chain);
+        ch->factors.push_back(so.p);
+        chain = ch;
+        row.kind = MPG_KIND_HORIZONTAL;
+        row.build_seconds = so.build_seconds;
+        row.min_residual = so.min_residual;
+        row.matrix_change = so.matrix_change;
+      } else {
+        row.kind = MPG_KIND_REUSED_SAME_MATRIX;
+      }
+      prev = a;
+      chains[i] = chain;
+      if (n <= 5000) row.standard_residual = std_residual(a, chain);
+    }
+    out.rows.push_back(row);
+  }
+  // solves: independent once the chains exist, batched by memory
+  std::vector<SolveSpec> specs(points.size());
+  DBuf<double> xs(dev, x_out ? size_t(n) * points.size() : 0);
+  for (size_t i = 0; i < points.size(); ++i) {
+    specs[i].sre = points[i];
+    specs[i].chain = chains[i];
+    specs[i].b = b.get();
+    specs[i].x = x_out ? xs.get() + size_t(n) * i : nullptr;
+  }
+  size_t free_b = 0, total_b = 0;
+  MPG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const double per_solve = 8.0 * double(n + 64) * double(gmres.max_iter + 8) + 1e7;
+  const int per_batch = std::max(1, std::min<int>(32, int(0.7 * double(free_b) / per_solve)));
+  for (size_t b0 = 0; b0 < specs.size(); b0 += size_t(per_batch)) {
+    std::vector<SolveSpec> batch(specs.begin() + long(b0), specs.begin() + long(std::min(specs.size(), b0 + per_batch)));
+    std::vector<GmresOutcome> oc = gmres_batch(op, batch, gmres);
+    for (size_t i = 0; i < oc.size(); ++i) {
+      mpg_report_row& row = out.rows[b0 + i];
+      row.solves = 1;
+      row.iterations = oc[i].iterations;
+      row.gmres_seconds = oc[i].solve_seconds;
+      out.total_iterations += oc[i].iterations;
+      if (!oc[i].converged) ++out.failed;
+    }
+  }
+  if (x_out) {
+    copy_out(x_out, xs.get(), size_t(n) * points.size(), s);
+    MPG_CUDA(cudaStreamSynchronize(s));
+  }
+  return out;
+}
+
+}  // namespace mpg

@@ -1,0 +1,48 @@
+// IRKA and shift-sweep drivers (irka.cu).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "host/small_dense.hpp"
+#include "runtime.cuh"
+
+namespace mpg {
+
+struct IrkaSettings {
+  int r = 2;
+  double tol = 1e-4;
+  int max_sweeps = 50;
+  unsigned long long seed = 1;
+  GmresOptions gmres{1e-10, 1000, false};
+  SpaiOptions spai{};
+  int max_chain_len = 16;
+  long long standard_residual_max_dim = 5000;
+  int mode = MPG_PRECOND_REUSE_CHAIN;
+  std::vector<double> init_shifts;  // empty: default seed (power iteration)
+  bool want_vw = false;
+};
+
+struct IrkaResult {
+  host::Mat kr, fr, cr, er, ar;
+  std::vector<host::Eig> lambda;
+  std::vector<double> v, w;
+  int sweeps = 0, reduced_order = 0;
+  bool converged = false;
+  long long total_iterations = 0, total_solves = 0;
+  std::vector<mpg_report_row> rows;
+};
+
+IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const double* c_any, int q,
+                    const IrkaSettings& cfg, int rank, int world, mpg_allgather_fn allgather, void* agctx);
+
+struct SweepOutcome {
+  std::vector<mpg_report_row> rows;
+  int failed = 0;
+  long long total_iterations = 0;
+};
+SweepOutcome sweep_run(const ShiftedOp& op, const double* b_any, const std::vector<double>& points,
+                       const SpaiOptions& spai, const GmresOptions& gmres, int mode, int max_chain_len,
+                       double* x_out);
+
+}  // namespace mpg

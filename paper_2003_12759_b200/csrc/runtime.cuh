@@ -1,0 +1,196 @@
+// Device runtime shared by all translation units of libmpg.so.
+//
+// Data layout in HBM:
+//   * matrices: CSR with int32 row offsets and column indices, fp64 values;
+//     a matrix's transpose (the reference's CSC shadow, sparse.cpp:27-46) is
+//     a second CSR built on the device on first use;
+//   * E sharing A's pattern is stored as interleaved (a, e) double2 pairs so
+//     the fused shifted SpMV reads both with one 128-bit load per entry;
+//   * Krylov bases live in 64-vector panels, each vector padded to a multiple
+//     of 32 doubles (16-byte aligned double2 access).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mpg.h"
+
+namespace mpg {
+
+struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ConfigError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct SolverError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+#define MPG_CUDA(call)                                                                             \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      throw ::mpg::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_) + " at " __FILE__); \
+  } while (0)
+
+extern std::atomic<long long> g_launches;
+inline void count_launch(long long k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+#define MPG_CHECK_LAUNCH() MPG_CUDA(cudaGetLastError())
+
+// Per-device library context: one stream; allocations go through the
+// stream-ordered pool (cudaMallocAsync) which doubles as the caching allocator.
+struct DeviceCtx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+};
+DeviceCtx& ctx(int device);
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) { cudaGetDevice(&prev); MPG_CUDA(cudaSetDevice(dev)); }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+void* dmalloc(int device, size_t bytes);
+void dfree(int device, void* p);
+
+template <class T>
+struct DBuf {
+  int device = 0;
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(int dev, size_t count) : device(dev), p(count ? static_cast<T*>(dmalloc(dev, count * sizeof(T))) : nullptr), n(count) {}
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : device(o.device), p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { reset(); device = o.device; p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { reset(); }
+  void reset() { if (p) dfree(device, p); p = nullptr; n = 0; }
+  T* get() const { return p; }
+};
+
+// Kernel-side view of a CSR matrix.
+struct CsrView {
+  const int* rowptr;
+  const int* colind;
+  const double* val;
+  int nrows, ncols;
+};
+
+struct DevCsr {
+  int device = 0;
+  int64_t nrows = 0, ncols = 0, nnz = 0;
+  DBuf<int> rowptr, colind;
+  DBuf<double> val;
+  int max_row = 0;     // longest row
+  double mean_row = 0; // nnz / nrows
+  bool is_diag = false;
+  mutable std::mutex mu;
+  mutable std::shared_ptr<DevCsr> tcache;  // transpose, built on first use
+  CsrView view() const { return {rowptr.get(), colind.get(), val.get(), int(nrows), int(ncols)}; }
+};
+using CsrPtr = std::shared_ptr<DevCsr>;
+
+// Builders (spmv.cu).
+CsrPtr csr_from_host(int device, int64_t nr, int64_t nc, const int64_t* rp, const int64_t* ci, const double* v);
+CsrPtr csr_from_device_parts(int device, int64_t nr, int64_t nc, DBuf<int>&& rp, DBuf<int>&& ci, DBuf<double>&& v);
+CsrPtr csr_transpose(const DevCsr& a);           // deterministic counting-sort transpose
+CsrPtr csr_transpose_cached(const CsrPtr& a);
+void csr_finalize_stats(DevCsr& m);              // max_row / mean_row / is_diag (syncs)
+
+// Shifted operator family sigma E - A.
+enum EMode { E_IDENT = 0, E_DIAG = 1, E_SAMEPAT = 2, E_GENERAL = 3 };
+struct OpView {
+  CsrView a;
+  int emode;
+  const double* ediag;  // E_DIAG
+  const double2* ae;    // E_SAMEPAT: (a_k, e_k) along A's pattern
+  CsrView e;            // E_GENERAL
+};
+struct ShiftedOp {
+  int device = 0;
+  int64_t n = 0;
+  int emode = E_IDENT;
+  CsrPtr a, e, at, et;
+  DBuf<double> ediag;
+  DBuf<double2> ae, ae_t;
+  int vec_width = 32;  // sub-warp width for this operator's rows
+  OpView view(bool transpose) const;
+};
+using OpPtr = std::shared_ptr<ShiftedOp>;
+OpPtr op_create(const CsrPtr& a, const CsrPtr& e);
+
+// Explicit unit matrix sigma E - A (or its 2n pair form) on the device.
+CsrPtr op_explicit(const ShiftedOp& op, double sre, double sim, bool transpose);
+
+// Immutable chain (base + factors), factors shared between chains.
+struct Chain {
+  std::vector<CsrPtr> factors;  // [0] = base
+  int length() const { return int(factors.size()) - 1; }
+};
+using ChainPtr = std::shared_ptr<const Chain>;
+
+int choose_vec_width(double mean_row);
+
+// ---- launches (spmv.cu) ------------------------------------------------------
+// y = alpha * M x
+void launch_spmv(const DevCsr& m, const double* x, double* y, double alpha, cudaStream_t s);
+// y = scale * (sigma E - A) x   (pair form when sim != 0: x, y have 2n entries)
+// resid != null: y = resid - (sigma E - A) x
+void launch_op(const ShiftedOp& op, bool transpose, double sre, double sim, double ca, const double* x, double* y,
+               const double* resid, double scale, cudaStream_t s, double* tmp_general);
+// y = Q_L(...Q_1(P x)); tmp must hold n doubles.
+void launch_chain(const Chain& c, const double* x, double* y, double* tmp, cudaStream_t s);
+double device_norm2(int device, const double* x, int64_t n, cudaStream_t s);
+
+// Host <-> any memory helpers.
+bool is_device_ptr(const void* p);
+void copy_in(double* dst_dev, const double* src_any, size_t n, cudaStream_t s);
+void copy_out(double* dst_any, const double* src_dev, size_t n, cudaStream_t s);
+
+// ---- GMRES (gmres.cu) --------------------------------------------------------
+struct SolveSpec {
+  double sre = 0, sim = 0;
+  bool transpose = false;
+  double ca = -1.0;         // -1: sigma E - A;  +1 (with sigma = 0, E = I): plain A
+  ChainPtr chain;           // null: identity
+  bool pair_blockdiag = false;  // apply an n x n chain blockwise on a 2n pair vector
+  const double* b = nullptr;    // any memory
+  double* x = nullptr;          // any memory
+};
+struct GmresOptions { double rel_tol = 1e-6; int max_iter = 1000; bool record_history = false; };
+struct GmresOutcome {
+  int iterations = 0;
+  bool converged = false, breakdown = false;
+  double rhs_norm = 0, final_residual = 0, solve_seconds = 0;
+  std::vector<double> history;
+};
+std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec>& specs, const GmresOptions& opt);
+
+// ---- SPAI (spai.cu) ------------------------------------------------------------
+struct SpaiOptions {
+  int pattern_kind = 1, power = 2;
+  double fill_tol = 1e-4;
+  int max_fill_per_col = 50, max_pattern_sweeps = 3;
+};
+struct SpaiOutcome {
+  CsrPtr p;
+  std::vector<double> column_residuals;  // host
+  int64_t fallback_count = 0;
+  double build_seconds = 0;
+  double min_residual = 0, matrix_change = 0;  // update builds
+};
+// prev == nullptr: spai_build (rhs = e_col); else update_build (rhs = prev(:, col)).
+SpaiOutcome spai_or_update(const CsrPtr& a, const CsrPtr& prev, const SpaiOptions& o, bool want_residuals);
+double frobenius_distance(const CsrPtr& a, const CsrPtr& b);
+void spai_column_solve_dev(const CsrPtr& a, int64_t col, const std::vector<int64_t>& pattern, std::vector<double>& values,
+                           double& residual, bool& rank_def);
+
+}  // namespace mpg

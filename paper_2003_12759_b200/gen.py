@@ -1,0 +1,166 @@
+"""Seeded synthetic inputs (csrc/gen/generators.cpp) as numpy arrays.
+
+The five BASELINE.json configs and the reference's own test
+fixtures (proj/tests/support.hpp:18-49, proj/src/generator.cpp:141-179).
+These run on the host and need no GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import Optional
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import lib
+
+
+@dataclasses.dataclass
+class HostCsr:
+    nrows: int
+    ncols: int
+    rowptr: np.ndarray
+    colind: np.ndarray
+    val: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.val.size)
+
+    def to_scipy(self):
+        import scipy.sparse as sp
+        return sp.csr_matrix((self.val, self.colind, self.rowptr), shape=(self.nrows, self.ncols))
+
+    def to_dense(self) -> np.ndarray:
+        d = np.zeros((self.nrows, self.ncols))
+        for i in range(self.nrows):
+            d[i, self.colind[self.rowptr[i]:self.rowptr[i + 1]]] = self.val[self.rowptr[i]:self.rowptr[i + 1]]
+        return d
+
+
+@dataclasses.dataclass
+class System:
+    """sigma E - A with inputs B (n x m) and outputs C (n x q), initial shifts."""
+    n: int
+    a: HostCsr
+    e: Optional[HostCsr]  # None with e_diag None: identity
+    e_diag: Optional[np.ndarray]
+    b: np.ndarray
+    c: np.ndarray
+    shifts: np.ndarray
+    r: int
+
+    def e_csr(self) -> Optional[HostCsr]:
+        if self.e is not None:
+            return self.e
+        if self.e_diag is not None:
+            n = self.n
+            return HostCsr(n, n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int64), self.e_diag.copy())
+        return None
+
+
+def _take_csr(p) -> HostCsr:
+    h = p.contents
+    nr, nnz = h.nrows, h.nnz
+    out = HostCsr(h.nrows, h.ncols, np.ctypeslib.as_array(h.rowptr, (nr + 1,)).copy(),
+                  np.ctypeslib.as_array(h.colind, (max(nnz, 1),))[:nnz].copy(),
+                  np.ctypeslib.as_array(h.val, (max(nnz, 1),))[:nnz].copy())
+    lib.mpg_host_csr_free(p)
+    return out
+
+
+def _check(st):
+    if st != 0:
+        raise ValueError(lib.mpg_gen_last_error().decode())
+
+
+def random_dense(r: int, c: int, seed: int) -> np.ndarray:
+    """support.hpp:18-25: U[-1,1], column-major fill (mt19937_64 + libstdc++ distribution)."""
+    out = np.empty(r * c)
+    lib.mpg_gen_random_dense(r, c, seed, L.ptr(out))
+    return out.reshape((r, c), order="F")
+
+
+def random_sparse(r: int, c: int, density: float, seed: int, diag_shift: float = 0.0) -> HostCsr:
+    """support.hpp:37-49."""
+    p = C.POINTER(L.HostCsr)()
+    _check(lib.mpg_gen_random_sparse(r, c, density, seed, diag_shift, C.byref(p)))
+    return _take_csr(p)
+
+
+def from_triplets(nr: int, nc: int, rows, cols, vals) -> HostCsr:
+    """Duplicates summed, exact-zero sums kept (sparse.cpp:80-115)."""
+    ri, ci, v = L.i64(rows), L.i64(cols), L.f64(vals)
+    p = C.POINTER(L.HostCsr)()
+    _check(lib.mpg_gen_from_triplets(nr, nc, ri.size, L.ptr(ri), L.ptr(ci), L.ptr(v), C.byref(p)))
+    return _take_csr(p)
+
+
+def from_dense(d: np.ndarray, drop_tol: float = 0.0) -> HostCsr:
+    """support.hpp:27-33 (sparse_from_dense)."""
+    d = np.asarray(d, dtype=np.float64)
+    rows, cols = np.nonzero(np.abs(d) > drop_tol)
+    return from_triplets(d.shape[0], d.shape[1], rows, cols, d[rows, cols])
+
+
+def bilinear_toy(n: int, m: int, seed: int):
+    """generator.cpp:141-179 with N = 0: returns (K, F (n x m), C (n x 1))."""
+    p = C.POINTER(L.HostCsr)()
+    f = np.empty(n * m)
+    c = np.empty(n)
+    _check(lib.mpg_gen_bilinear_toy(n, m, seed, C.byref(p), L.ptr(f), L.ptr(c)))
+    return _take_csr(p), f.reshape((n, m), order="F"), c.reshape((n, 1))
+
+
+def _take_system(p) -> System:
+    s = p.contents
+    n = s.n
+    a = HostCsr(s.a.contents.nrows, s.a.contents.ncols,
+                np.ctypeslib.as_array(s.a.contents.rowptr, (n + 1,)).copy(),
+                np.ctypeslib.as_array(s.a.contents.colind, (s.a.contents.nnz,)).copy(),
+                np.ctypeslib.as_array(s.a.contents.val, (s.a.contents.nnz,)).copy())
+    e = None
+    if s.e:
+        ec = s.e.contents
+        e = HostCsr(ec.nrows, ec.ncols, np.ctypeslib.as_array(ec.rowptr, (n + 1,)).copy(),
+                    np.ctypeslib.as_array(ec.colind, (ec.nnz,)).copy(), np.ctypeslib.as_array(ec.val, (ec.nnz,)).copy())
+    ed = np.ctypeslib.as_array(s.e_diag, (n,)).copy() if s.e_diag else None
+    b = np.ctypeslib.as_array(s.b, (n * s.m,)).copy().reshape((n, s.m), order="F")
+    c = np.ctypeslib.as_array(s.c, (n * s.q,)).copy().reshape((n, s.q), order="F")
+    shifts = np.ctypeslib.as_array(s.shifts, (s.r,)).copy()
+    out = System(n, a, e, ed, b, c, shifts, s.r)
+    lib.mpg_host_system_free(p)
+    return out
+
+
+def config1(N: int = 100, seed: int = 0) -> System:
+    """C1: 2D cell-centred diffusion, lognormal(0, 0.5) cells, E = diag U[1,2], r = 4."""
+    p = C.POINTER(L.HostSystem)()
+    _check(lib.mpg_gen_grid2d(N, seed, C.byref(p)))
+    return _take_system(p)
+
+
+def config2(M: int = 64, seed: int = 1) -> System:
+    """C2: 3D 7-point convection-diffusion (upwind, v = (0.5, 0.3, 0.2)/h), E = diag U[0.5,1.5], r = 8."""
+    p = C.POINTER(L.HostSystem)()
+    _check(lib.mpg_gen_convdiff3d(M, seed, C.byref(p)))
+    return _take_system(p)
+
+
+def config3(N: int = 106, seed: int = 2, mimo: bool = False) -> System:
+    """C3 / C4 (mimo, seed 3): Q1 hexahedral FEM on N^3 nodes, A = -(K + Robin), E = consistent mass."""
+    p = C.POINTER(L.HostSystem)()
+    _check(lib.mpg_gen_fem3d(N, seed, int(mimo), C.byref(p)))
+    return _take_system(p)
+
+
+def config4(N: int = 106, seed: int = 3) -> System:
+    return config3(N, seed, True)
+
+
+def config5(n: int = 2_000_000, seed: int = 4, nshifts: int = 64, max_len: int = 2000) -> System:
+    """C5: Zipf(1.8) row lengths on [3, max_len], a_ii = -1.1 sum |a_ij|, E = diag U[1,2]."""
+    p = C.POINTER(L.HostSystem)()
+    _check(lib.mpg_gen_zipf(n, seed, 3, max_len, 1.8, nshifts, C.byref(p)))
+    return _take_system(p)

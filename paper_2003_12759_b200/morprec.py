@@ -1,0 +1,588 @@
+"""Python mirror of the reference `morprec` solve-path API over libmpg.so.
+
+Names, argument meaning and error behaviour follow proj/include/morprec:
+SparseMatrix (sparse.hpp:33-101), gmres_right_preconditioned (gmres.hpp:49-50),
+spai_build / spai_column_solve (spai.hpp:56-63), update_build and PrecondChain
+(chain.hpp:45-77), standard_residual (chain.hpp:79-81), birka_reduce with N = 0
+(birka.hpp:78-80, generalised to E) and run_spai_bench (bench.hpp:50-57).
+std::invalid_argument maps to ValueError; ConfigError / SolverError keep their
+names. Every call runs on the GPU; there is no CPU fallback.
+
+Vectors may be numpy arrays (host) or torch CUDA tensors (device); results
+come back in the same kind of container as the right-hand side.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import math
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import ConfigError, SolverError, check, lib
+
+__all__ = [
+    "SparseMatrix", "ShiftedOperator", "PrecondChain", "GmresConfig", "GmresReport", "GmresResult", "SpaiConfig",
+    "SpaiResult", "UpdateFactor", "IrkaConfig", "IrkaState", "ReportRow", "ReductionReport", "SweepResult",
+    "gmres_right_preconditioned", "gmres_shifted", "gmres_batch", "spai_build", "spai_column_solve", "update_build",
+    "standard_residual", "irka_reduce", "run_spai_bench", "ConfigError", "SolverError", "PrecondMode",
+]
+
+
+class PrecondMode:
+    """PrecondMode (proj/include/morprec/chain.hpp:21) plus FROZEN (build once, reuse unchanged)."""
+    NONE = L.PRECOND_NONE
+    FRESH_SPAI = L.PRECOND_FRESH
+    REUSE_CHAIN = L.PRECOND_REUSE_CHAIN
+    REUSE_FROZEN = L.PRECOND_REUSE_FROZEN
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+class _Vec:
+    """Pointer + keep-alive for a host (numpy) or device (torch) vector."""
+
+    def __init__(self, x, n: Optional[int] = None):
+        if _is_torch(x):
+            import torch
+            t = x.detach()
+            if t.dtype != torch.float64:
+                t = t.to(torch.float64)
+            self.obj = t.contiguous()
+            self.p = self.obj.data_ptr()
+            self.size = self.obj.numel()
+            self.device = self.obj.device
+        else:
+            self.obj = L.f64(x).ravel()
+            self.p = self.obj.ctypes.data
+            self.size = self.obj.size
+            self.device = None
+        if n is not None and self.size != n:
+            raise ValueError(f"dimension mismatch: expected {n} entries, got {self.size}")
+
+    def empty_like(self, n: int):
+        if self.device is not None:
+            import torch
+            return torch.empty(n, dtype=torch.float64, device=self.device)
+        return np.empty(n, dtype=np.float64)
+
+
+def _ptr(x) -> int:
+    return x.data_ptr() if _is_torch(x) else x.ctypes.data
+
+
+class SparseMatrix:
+    """Immutable device CSR matrix (SparseMatrix, proj/include/morprec/sparse.hpp:33-101)."""
+
+    def __init__(self, handle, keep=None):
+        self._h = C.c_void_p(handle)
+        nr, nc, nz = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib.mpg_csr_info(self._h, C.byref(nr), C.byref(nc), C.byref(nz)))
+        self._shape = (nr.value, nc.value)
+        self._nnz = nz.value
+        self._keep = keep
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.mpg_csr_destroy(h)
+            self._h = None
+
+    # -- construction -------------------------------------------------------
+    @staticmethod
+    def from_csr(nrows: int, ncols: int, row_offsets, col_indices, values, device: int = 0) -> "SparseMatrix":
+        rp, ci, v = L.i64(row_offsets), L.i64(col_indices), L.f64(values)
+        if rp.size != nrows + 1:
+            raise ValueError("sparse: row_offsets length must be nrows + 1")
+        if ci.size != v.size:
+            raise ValueError("sparse: col_indices and values lengths differ")
+        if rp[-1] != ci.size:
+            raise ValueError("sparse: row_offsets must end at nnz")
+        h = C.c_void_p()
+        check(lib.mpg_csr_create(device, nrows, ncols, L.ptr(rp), L.ptr(ci), L.ptr(v), C.byref(h)))
+        return SparseMatrix(h.value)
+
+    @staticmethod
+    def from_triplets(nrows: int, ncols: int, rows, cols, values, device: int = 0) -> "SparseMatrix":
+        from . import gen
+        hc = gen.from_triplets(nrows, ncols, rows, cols, values)
+        return SparseMatrix.from_csr(nrows, ncols, hc.rowptr, hc.colind, hc.val, device)
+
+    @staticmethod
+    def from_scipy(m, device: int = 0) -> "SparseMatrix":
+        m = m.tocsr()
+        m.sort_indices()
+        m.sum_duplicates()
+        return SparseMatrix.from_csr(m.shape[0], m.shape[1], m.indptr, m.indices, m.data, device)
+
+    @staticmethod
+    def from_dense(d, device: int = 0, drop_tol: float = 0.0) -> "SparseMatrix":
+        d = np.asarray(d, dtype=np.float64)
+        rows, cols = np.nonzero(np.abs(d) > drop_tol)
+        return SparseMatrix.from_triplets(d.shape[0], d.shape[1], rows, cols, d[rows, cols], device)
+
+    @staticmethod
+    def identity(n: int, device: int = 0) -> "SparseMatrix":
+        return SparseMatrix.from_csr(n, n, np.arange(n + 1), np.arange(n), np.ones(n), device)
+
+    @staticmethod
+    def diagonal(entries, device: int = 0) -> "SparseMatrix":
+        e = L.f64(entries)
+        n = e.size
+        return SparseMatrix.from_csr(n, n, np.arange(n + 1), np.arange(n), e, device)
+
+    @staticmethod
+    def zero(nrows: int, ncols: int, device: int = 0) -> "SparseMatrix":
+        return SparseMatrix.from_csr(nrows, ncols, np.zeros(nrows + 1, np.int64), np.zeros(0, np.int64),
+                                     np.zeros(0), device)
+
+    # -- queries ----------------------------------------------------------------
+    def rows(self) -> int:
+        return self._shape[0]
+
+    def cols(self) -> int:
+        return self._shape[1]
+
+    @property
+    def shape(self):
+        return self._shape
+
+    def nnz(self) -> int:
+        return self._nnz
+
+    def download(self):
+        rp = np.empty(self._shape[0] + 1, np.int64)
+        ci = np.empty(self._nnz, np.int64)
+        v = np.empty(self._nnz, np.float64)
+        check(lib.mpg_csr_download(self._h, L.ptr(rp), L.ptr(ci), L.ptr(v)))
+        return rp, ci, v
+
+    def to_dense(self, max_entries: int = 1 << 24) -> np.ndarray:
+        if self._shape[0] * self._shape[1] > max_entries:
+            raise ValueError("sparse to_dense: matrix too large to materialize")
+        rp, ci, v = self.download()
+        d = np.zeros(self._shape)
+        for i in range(self._shape[0]):
+            d[i, ci[rp[i]:rp[i + 1]]] = v[rp[i]:rp[i + 1]]
+        return d
+
+    def to_scipy(self):
+        import scipy.sparse as sp
+        rp, ci, v = self.download()
+        return sp.csr_matrix((v, ci, rp), shape=self._shape)
+
+    def multiply(self, x):
+        """y = A x (sparse.cpp:236-249); throws ValueError on dimension mismatch."""
+        xv = _Vec(x)
+        if xv.size != self._shape[1]:
+            raise ValueError("sparse multiply: dimension mismatch")
+        y = xv.empty_like(self._shape[0])
+        check(lib.mpg_csr_multiply(self._h, xv.p, _ptr(y)))
+        return y
+
+    def multiply_transpose(self, x):
+        xv = _Vec(x)
+        if xv.size != self._shape[0]:
+            raise ValueError("sparse multiply_transpose: dimension mismatch")
+        y = xv.empty_like(self._shape[1])
+        check(lib.mpg_csr_multiply_transpose(self._h, xv.p, _ptr(y)))
+        return y
+
+    def transpose(self) -> "SparseMatrix":
+        h = C.c_void_p()
+        check(lib.mpg_csr_transpose(self._h, C.byref(h)))
+        return SparseMatrix(h.value)
+
+    def frobenius_norm(self) -> float:
+        return float(lib.mpg_csr_frobenius_norm(self._h))
+
+
+class ShiftedOperator:
+    """sigma E - A formed on the fly (replaces linear_combination, qbihomm.cpp:164-171,
+    and the N = 0 KroneckerOperator, kron.cpp:34-64). E None = identity."""
+
+    def __init__(self, a: SparseMatrix, e: Optional[SparseMatrix] = None):
+        h = C.c_void_p()
+        check(lib.mpg_op_create(a._h, e._h if e is not None else None, C.byref(h)))
+        self._h = h
+        self.a, self.e = a, e
+        self.n = int(lib.mpg_op_dim(h))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.mpg_op_destroy(h)
+            self._h = None
+
+    def apply(self, sigma: complex, x, transpose: bool = False):
+        s = complex(sigma)
+        n = self.n * (2 if s.imag != 0 else 1)
+        xv = _Vec(x, n)
+        y = xv.empty_like(n)
+        check(lib.mpg_op_apply(self._h, s.real, s.imag, int(transpose), xv.p, _ptr(y)))
+        return y
+
+    def explicit(self, sigma: complex, transpose: bool = False) -> SparseMatrix:
+        s = complex(sigma)
+        h = C.c_void_p()
+        check(lib.mpg_op_explicit(self._h, s.real, s.imag, int(transpose), C.byref(h)))
+        return SparseMatrix(h.value)
+
+
+@dataclasses.dataclass
+class GmresConfig:
+    """GmresConfig (proj/include/morprec/gmres.hpp:20-24)."""
+    rel_tol: float = 1e-6
+    max_iter: int = 1000
+    record_history: bool = False
+
+    def c(self) -> L.GmresCfg:
+        return L.GmresCfg(self.rel_tol, self.max_iter, int(self.record_history))
+
+
+@dataclasses.dataclass
+class GmresReport:
+    """GmresReport (proj/include/morprec/gmres.hpp:26-34)."""
+    iterations: int = 0
+    converged: bool = False
+    breakdown: bool = False
+    rhs_norm: float = 0.0
+    final_residual: float = 0.0
+    solve_seconds: float = 0.0
+    residual_history: list = dataclasses.field(default_factory=list)
+
+    @staticmethod
+    def of(r: L.GmresRep, hist=None) -> "GmresReport":
+        h = list(hist[: r.history_len]) if hist is not None else []
+        return GmresReport(r.iterations, bool(r.converged), bool(r.breakdown), r.rhs_norm, r.final_residual,
+                           r.solve_seconds, h)
+
+
+@dataclasses.dataclass
+class GmresResult:
+    x: object
+    report: GmresReport
+
+
+@dataclasses.dataclass
+class SpaiConfig:
+    """SpaiConfig (proj/include/morprec/spai.hpp:25-33); pattern 'diagonal' or 'a'."""
+    pattern: str = "a"
+    fill_tol: float = 1e-4
+    max_fill_per_col: int = 50
+    max_pattern_sweeps: int = 3
+    threads: int = 1
+
+    def c(self) -> L.SpaiCfg:
+        kind = {"diagonal": 0, "a": 1, "a_pow": 2}[self.pattern]
+        return L.SpaiCfg(kind, 2, self.fill_tol, self.max_fill_per_col, self.max_pattern_sweeps, self.threads)
+
+
+class PrecondChain:
+    """Immutable chain P, Q_1..Q_L applied as sequential SpMVs (chain.hpp:55-77)."""
+
+    def __init__(self, base: Optional[SparseMatrix] = None, _handle=None, _factors=()):
+        self._h = None
+        if _handle is not None:
+            self._h = C.c_void_p(_handle)
+            self._factors = list(_factors)
+        elif base is not None:
+            h = C.c_void_p()
+            check(lib.mpg_chain_create(base._h, C.byref(h)))
+            self._h = h
+            self._factors = [base]
+        else:
+            self._factors = []
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.mpg_chain_destroy(h)
+            self._h = None
+
+    def empty(self) -> bool:
+        return self._h is None
+
+    def length(self) -> int:
+        return 0 if self._h is None else int(lib.mpg_chain_length(self._h))
+
+    def dim(self) -> int:
+        return self._factors[0].rows() if self._factors else 0
+
+    def factor_id(self, i: int) -> int:
+        return lib.mpg_chain_factor_id(self._h, i) or 0
+
+    def extended(self, factor) -> "PrecondChain":
+        if self._h is None:
+            raise RuntimeError("chain: cannot extend an empty chain")
+        q = factor.q if isinstance(factor, UpdateFactor) else factor
+        if q is None:
+            raise ValueError("chain: null update factor")
+        h = C.c_void_p()
+        check(lib.mpg_chain_extend(self._h, q._h, C.byref(h)))
+        return PrecondChain(_handle=h.value, _factors=self._factors + [q])
+
+    def apply(self, x):
+        if self._h is None:
+            raise RuntimeError("chain: apply on an empty chain")
+        xv = _Vec(x, self.dim())
+        y = xv.empty_like(self.dim())
+        check(lib.mpg_chain_apply(self._h, xv.p, _ptr(y)))
+        return y
+
+
+@dataclasses.dataclass
+class SpaiResult:
+    """SpaiResult (proj/include/morprec/spai.hpp:43-48)."""
+    p: SparseMatrix
+    column_residuals: np.ndarray
+    fallback_count: int
+    build_seconds: float
+
+
+@dataclasses.dataclass
+class UpdateFactor:
+    """UpdateFactor (proj/include/morprec/chain.hpp:33-42)."""
+    q: SparseMatrix
+    min_residual: float = 0.0
+    matrix_change: float = 0.0
+    build_seconds: float = 0.0
+    fallback_count: int = 0
+
+
+def spai_build(a: SparseMatrix, cfg: SpaiConfig = SpaiConfig()) -> SpaiResult:
+    if a.rows() != a.cols():
+        raise ValueError("spai_build: matrix must be square")
+    res = np.empty(a.rows())
+    p = C.c_void_p()
+    fb = C.c_int64()
+    secs = C.c_double()
+    c = cfg.c()
+    check(lib.mpg_spai_build(a._h, C.byref(c), C.byref(p), L.ptr(res), C.byref(fb), C.byref(secs)))
+    return SpaiResult(SparseMatrix(p.value), res, fb.value, secs.value)
+
+
+def spai_column_solve(a: SparseMatrix, col: int, pattern: Sequence[int]):
+    """Fixed-pattern least squares for one column (spai.cpp:158-173): (rows, values, residual, rank_deficient)."""
+    pat = np.sort(L.i64(pattern))
+    vals = np.empty(pat.size)
+    r = C.c_double()
+    rd = C.c_int()
+    check(lib.mpg_spai_column_solve(a._h, int(col), pat.size, L.ptr(pat), L.ptr(vals), C.byref(r), C.byref(rd)))
+    return pat, vals, r.value, bool(rd.value)
+
+
+def update_build(a_prev: SparseMatrix, a_new: SparseMatrix, cfg: SpaiConfig = SpaiConfig()) -> UpdateFactor:
+    if a_prev.shape != a_new.shape:
+        raise ValueError("update_build: shape mismatch")
+    q = C.c_void_p()
+    mr, mc, secs = C.c_double(), C.c_double(), C.c_double()
+    fb = C.c_int64()
+    c = cfg.c()
+    check(lib.mpg_update_build(a_prev._h, a_new._h, C.byref(c), C.byref(q), C.byref(mr), C.byref(mc), C.byref(fb),
+                               C.byref(secs)))
+    return UpdateFactor(SparseMatrix(q.value), mr.value, mc.value, secs.value, fb.value)
+
+
+def standard_residual(a: SparseMatrix, chain: PrecondChain) -> float:
+    out = C.c_double()
+    check(lib.mpg_standard_residual(a._h, chain._h, C.byref(out)))
+    return out.value
+
+
+def _gmres_common(call, b, cfg: GmresConfig):
+    bv = _Vec(b)
+    x = bv.empty_like(bv.size)
+    rep = L.GmresRep()
+    c = cfg.c()
+    hist = np.empty(cfg.max_iter + 2) if cfg.record_history else None
+    check(call(bv.p, _ptr(x), C.byref(c), C.byref(rep), L.ptr(hist) if hist is not None else None))
+    return GmresResult(x, GmresReport.of(rep, hist))
+
+
+def gmres_right_preconditioned(a: SparseMatrix, chain: Optional[PrecondChain], b,
+                               cfg: GmresConfig = GmresConfig()) -> GmresResult:
+    """Full right-preconditioned GMRES on A P xt = b, x = P xt (gmres.cpp:40-186).
+    `a` is a SparseMatrix (matvec_operator); chain None is identity_operator()."""
+    bv = _Vec(b)
+    if bv.size != a.rows():
+        raise ValueError("gmres: dimension mismatch")
+    ch = chain._h if chain is not None and not chain.empty() else None
+    return _gmres_common(lambda bp, xp, c, r, h: lib.mpg_gmres_csr(a._h, ch, bp, xp, c, r, h), b, cfg)
+
+
+def gmres_shifted(op: ShiftedOperator, sigma: complex, b, chain: Optional[PrecondChain] = None,
+                  transpose: bool = False, cfg: GmresConfig = GmresConfig()) -> GmresResult:
+    """GMRES on (sigma E - A) (or its transpose side / pair form) with a chain preconditioner."""
+    s = complex(sigma)
+    ch = chain._h if chain is not None and not chain.empty() else None
+    return _gmres_common(lambda bp, xp, c, r, h: lib.mpg_gmres_shifted(op._h, s.real, s.imag, int(transpose), ch, bp,
+                                                                       xp, c, r, h), b, cfg)
+
+
+def gmres_batch(op: ShiftedOperator, sigmas: Sequence[complex], bs: Sequence, chains=None, transposes=None,
+                cfg: GmresConfig = GmresConfig()):
+    """Independent shifted solves advanced in lockstep on one device."""
+    k = len(sigmas)
+    sre = np.array([complex(s).real for s in sigmas])
+    sim = np.array([complex(s).imag for s in sigmas])
+    tr = np.array([int(t) for t in (transposes or [0] * k)], dtype=np.int32)
+    bvs = [_Vec(b) for b in bs]
+    xs = [bv.empty_like(bv.size) for bv in bvs]
+    bp = (C.c_void_p * k)(*[bv.p for bv in bvs])
+    xp = (C.c_void_p * k)(*[_ptr(x) for x in xs])
+    chs = (C.c_void_p * k)(*[(c._h.value if c is not None and not c.empty() else None) for c in (chains or [None] * k)])
+    reps = (L.GmresRep * k)()
+    c = cfg.c()
+    check(lib.mpg_gmres_batch(op._h, k, L.ptr(sre), L.ptr(sim), tr.ctypes.data, chs, bp, xp, C.byref(c), reps))
+    return [GmresResult(xs[i], GmresReport.of(reps[i])) for i in range(k)]
+
+
+@dataclasses.dataclass
+class ReportRow:
+    """ReportRow (proj/include/morprec/report.hpp:28-40)."""
+    sweep: int
+    point: int
+    kind: str
+    solves: int
+    gmres_iterations: int
+    precond_build_seconds: float
+    gmres_seconds: float
+    min_residual: float
+    matrix_change: float
+    standard_residual: float
+
+    @staticmethod
+    def of(r: L.ReportRow) -> "ReportRow":
+        return ReportRow(r.sweep, r.point, L.KIND_NAMES.get(r.kind, "none"), r.solves, r.iterations, r.build_seconds,
+                         r.gmres_seconds, r.min_residual, r.matrix_change, r.standard_residual)
+
+
+@dataclasses.dataclass
+class ReductionReport:
+    rows: list
+    converged: bool = False
+    reduced_order: int = 0
+    sweeps: int = 0
+    warnings: list = dataclasses.field(default_factory=list)
+
+    def totals(self):
+        return dict(solves=sum(r.solves for r in self.rows),
+                    precond_build_seconds=sum(r.precond_build_seconds for r in self.rows),
+                    gmres_iterations=sum(r.gmres_iterations for r in self.rows),
+                    gmres_seconds=sum(r.gmres_seconds for r in self.rows))
+
+    def write_csv(self, f) -> None:
+        """Header, one line per row, then TOTAL (report.cpp:46-63); NaN cells stay empty."""
+        cols = ["sweep", "point", "precond", "solves", "precond_build_seconds", "gmres_iterations", "gmres_seconds",
+                "min_residual", "matrix_change", "standard_residual"]
+        f.write(",".join(cols) + "\n")
+
+        def cell(v):
+            return "" if isinstance(v, float) and math.isnan(v) else repr(v)
+        for r in self.rows:
+            f.write(",".join([str(r.sweep), str(r.point), r.kind, str(r.solves), cell(r.precond_build_seconds),
+                              str(r.gmres_iterations), cell(r.gmres_seconds), cell(r.min_residual),
+                              cell(r.matrix_change), cell(r.standard_residual)]) + "\n")
+        t = self.totals()
+        f.write(f"TOTAL,,,{t['solves']},{t['precond_build_seconds']!r},{t['gmres_iterations']},"
+                f"{t['gmres_seconds']!r},,,\n")
+
+
+@dataclasses.dataclass
+class IrkaConfig:
+    """BirkaConfig (proj/include/morprec/birka.hpp:49-61) for N = 0."""
+    r: int = 2
+    tol: float = 1e-4
+    max_sweeps: int = 50
+    seed: int = 1
+    gmres: GmresConfig = dataclasses.field(default_factory=lambda: GmresConfig(1e-10, 1000, False))
+    spai: SpaiConfig = dataclasses.field(default_factory=SpaiConfig)
+    max_chain_len: int = 16
+    explicit_nnz_cap: int = 200000
+    standard_residual_max_dim: int = 5000
+
+    def c(self) -> L.IrkaCfg:
+        return L.IrkaCfg(self.r, self.tol, self.max_sweeps, 1, self.seed, self.gmres.c(), self.spai.c(),
+                         self.max_chain_len, self.explicit_nnz_cap, self.standard_residual_max_dim)
+
+
+@dataclasses.dataclass
+class IrkaState:
+    """Reduced model E_r x' = A_r x + B_r u, y = C_r^T x with K_r = E_r^{-1} A_r (BirkaState, birka.hpp:35-47)."""
+    kr: np.ndarray
+    fr: np.ndarray
+    cr: np.ndarray
+    er: Optional[np.ndarray]
+    ar: Optional[np.ndarray]
+    lam: np.ndarray
+    v: Optional[np.ndarray]
+    w: Optional[np.ndarray]
+    sweeps: int
+
+    def transfer(self, s: complex) -> np.ndarray:
+        """H_r(s) = C_r^T (s I - K_r)^{-1} f_r, q x m."""
+        r = self.kr.shape[0]
+        return self.cr.T @ np.linalg.solve(s * np.eye(r) - self.kr, self.fr)
+
+
+def _rows(buf, n):
+    return [ReportRow.of(buf[i]) for i in range(n)]
+
+
+def irka_reduce(op: ShiftedOperator, b, c, cfg: IrkaConfig, mode: int = PrecondMode.REUSE_CHAIN,
+                init_shifts=None, want_bases: bool = False):
+    """IRKA (BIRKA with N = 0, birka.cpp:139-310) on the GPU; returns (IrkaState, ReductionReport)."""
+    n = op.n
+    bm = np.asfortranarray(np.asarray(b, dtype=np.float64).reshape(n, -1))
+    cm = np.asfortranarray(np.asarray(c, dtype=np.float64).reshape(n, -1))
+    m, q, r = bm.shape[1], cm.shape[1], cfg.r
+    kr, er, ar = (np.zeros((r, r), order="F") for _ in range(3))
+    fr, cr = np.zeros((r, m), order="F"), np.zeros((r, q), order="F")
+    lre, lim = np.zeros(r), np.zeros(r)
+    v = np.zeros((n, r), order="F") if want_bases else None
+    w = np.zeros((n, r), order="F") if want_bases else None
+    sweeps, conv, nrows = C.c_int(), C.c_int(), C.c_int()
+    maxrows = 2 * r * max(cfg.max_sweeps, 1) + 8
+    rows = (L.ReportRow * maxrows)()
+    ini = L.f64(init_shifts) if init_shifts is not None else None
+    cc = cfg.c()
+    check(lib.mpg_irka_reduce(op._h, L.ptr(bm), m, L.ptr(cm), q, C.byref(cc), mode,
+                              L.ptr(ini) if ini is not None else None, L.ptr(kr), L.ptr(fr), L.ptr(cr), L.ptr(er),
+                              L.ptr(ar), L.ptr(lre), L.ptr(lim), L.ptr(v) if v is not None else None,
+                              L.ptr(w) if w is not None else None, C.byref(sweeps), C.byref(conv), rows, maxrows,
+                              C.byref(nrows)))
+    st = IrkaState(kr, fr, cr, er, ar, lre + 1j * lim, v, w, sweeps.value)
+    rep = ReductionReport(_rows(rows, min(nrows.value, maxrows)), bool(conv.value), r, sweeps.value)
+    if not rep.converged:
+        rep.warnings.append(f"fixed point left unconverged after {sweeps.value} sweeps")
+    return st, rep
+
+
+@dataclasses.dataclass
+class SweepResult:
+    """SpaiBenchResult (proj/include/morprec/bench.hpp:46-49)."""
+    report: ReductionReport
+    failed_solves: int
+    x: Optional[np.ndarray] = None
+
+
+def run_spai_bench(op: ShiftedOperator, b, points: Sequence[float], spai: SpaiConfig = SpaiConfig(),
+                   gmres: GmresConfig = GmresConfig(), mode: int = PrecondMode.REUSE_CHAIN, max_chain_len: int = 16,
+                   keep_solutions: bool = False) -> SweepResult:
+    """Shift-sweep solve benchmark (bench.cpp:159-249) on sigma_i E - A."""
+    n = op.n
+    bv = _Vec(b, n)
+    pts = L.f64(points)
+    x = np.zeros((len(pts), n)) if keep_solutions else None
+    rows = (L.ReportRow * max(len(pts), 1))()
+    nrows, failed = C.c_int(), C.c_int()
+    s, g = spai.c(), gmres.c()
+    check(lib.mpg_spai_bench(op._h, bv.p, len(pts), L.ptr(pts), C.byref(s), C.byref(g), mode, max_chain_len,
+                             L.ptr(x) if x is not None else None, rows, len(pts), C.byref(nrows), C.byref(failed)))
+    rep = ReductionReport(_rows(rows, nrows.value), failed.value == 0, 0, 1)
+    return SweepResult(rep, failed.value, x)

@@ -1,0 +1,130 @@
+"""GPU GMRES: the reference's gmres tests (proj/tests/test_gmres.cpp) on the
+device engine, plus parity with the oracle on shifted preconditioned solves."""
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+
+def _m(mpg, h):
+    return mpg.SparseMatrix.from_csr(h.nrows, h.ncols, h.rowptr, h.colind, h.val)
+
+
+def test_identity_converges_in_one_iteration(mpg):
+    res = mpg.gmres_right_preconditioned(mpg.SparseMatrix.identity(2), None, np.array([3.0, 4.0]))
+    assert res.report.converged and res.report.iterations == 1
+    assert np.linalg.norm(res.x - [3, 4]) <= 1e-12
+
+
+def test_diagonal_solve(mpg):
+    res = mpg.gmres_right_preconditioned(mpg.SparseMatrix.diagonal([2.0, 3.0]), None, np.array([2.0, 3.0]))
+    assert res.report.converged and np.linalg.norm(res.x - 1.0) <= 1e-10
+
+
+def test_exact_inverse_preconditioner(mpg, gen):
+    h = gen.random_sparse(10, 10, 0.5, 7, 8.0)
+    a = _m(mpg, h)
+    inv = mpg.SparseMatrix.from_dense(np.linalg.inv(h.to_dense()))
+    b = gen.random_dense(10, 1, 8)[:, 0]
+    res = mpg.gmres_right_preconditioned(a, mpg.PrecondChain(inv), b)
+    assert res.report.converged and res.report.iterations == 1
+    assert np.linalg.norm(h.to_dense() @ res.x - b) <= 1e-6 * np.linalg.norm(b)
+
+
+def test_zero_operator_reports_breakdown(mpg):
+    res = mpg.gmres_right_preconditioned(mpg.SparseMatrix.zero(3, 3), None, np.array([1.0, 0, 0]))
+    assert res.report.breakdown and not res.report.converged
+
+
+def test_zero_rhs_rejected(mpg):
+    with pytest.raises(ValueError):
+        mpg.gmres_right_preconditioned(mpg.SparseMatrix.identity(2), None, np.zeros(2))
+
+
+def test_history_nonincreasing(mpg, gen):
+    h = gen.random_sparse(30, 30, 0.2, 17, 4.0)
+    res = mpg.gmres_right_preconditioned(_m(mpg, h), None, gen.random_dense(30, 1, 18)[:, 0],
+                                         mpg.GmresConfig(record_history=True))
+    assert res.report.converged
+    hist = res.report.residual_history
+    assert len(hist) >= 2
+    assert all(hist[i] <= hist[i - 1] * (1 + 1e-14) for i in range(1, len(hist)))
+
+
+def test_solution_in_unpreconditioned_variable(mpg, gen):
+    h = gen.random_sparse(12, 12, 0.4, 27, 5.0)
+    p = mpg.SparseMatrix.diagonal(1.0 + 0.3 * np.arange(12))
+    b = gen.random_dense(12, 1, 28)[:, 0]
+    cfg = mpg.GmresConfig(rel_tol=1e-8)
+    res = mpg.gmres_right_preconditioned(_m(mpg, h), mpg.PrecondChain(p), b, cfg)
+    assert res.report.converged
+    assert np.linalg.norm(h.to_dense() @ res.x - b) <= 1e-8 * np.linalg.norm(b)
+    assert res.report.final_residual <= 1e-8 * np.linalg.norm(b)
+
+
+def test_preconditioned_and_plain_agree(mpg, gen):
+    h = gen.random_sparse(15, 15, 0.4, 37, 6.0)
+    b = gen.random_dense(15, 1, 38)[:, 0]
+    cfg = mpg.GmresConfig(rel_tol=1e-12)
+    plain = mpg.gmres_right_preconditioned(_m(mpg, h), None, b, cfg)
+    pre = mpg.gmres_right_preconditioned(_m(mpg, h), mpg.PrecondChain(mpg.SparseMatrix.diagonal(np.full(15, 0.5))),
+                                         b, cfg)
+    assert plain.report.converged and pre.report.converged
+    assert np.linalg.norm(plain.x - pre.x) <= 1e-8 * (1 + np.linalg.norm(plain.x))
+
+
+def test_iteration_cap_reported(mpg, gen):
+    h = gen.random_sparse(40, 40, 0.3, 47, 3.0)
+    res = mpg.gmres_right_preconditioned(_m(mpg, h), None, gen.random_dense(40, 1, 48)[:, 0],
+                                         mpg.GmresConfig(rel_tol=1e-14, max_iter=2))
+    assert not res.report.converged and res.report.iterations == 2 and res.x.size == 40
+
+
+def test_final_residual_matches_recomputation(mpg, gen):
+    h = gen.random_sparse(20, 20, 0.4, 57, 5.0)
+    b = gen.random_dense(20, 1, 58)[:, 0]
+    res = mpg.gmres_right_preconditioned(_m(mpg, h), None, b)
+    direct = np.linalg.norm(b - h.to_dense() @ res.x)
+    assert res.report.final_residual == pytest.approx(direct, rel=1e-10)
+
+
+@pytest.mark.parametrize("sigma", [0.5, 20.0, 3.0 + 2.0j])
+@pytest.mark.parametrize("transpose", [False, True])
+def test_shifted_spai_solve_matches_oracle(mpg, orc, gen, sigma, transpose):
+    sysm = gen.config1(N=24)
+    A = _m(mpg, sysm.a)
+    ecsr = sysm.e_csr()
+    E = _m(mpg, ecsr)
+    op = mpg.ShiftedOperator(A, E)
+    Ao, Eo = orc.Csr.of(sysm.a), orc.Csr.of(ecsr)
+    if transpose:
+        Ao, Eo = Ao.transpose(), Eo.transpose()
+    w = 2 if complex(sigma).imag else 1
+    b = np.tile(sysm.b[:, 0], w)
+    M = op.explicit(sigma, transpose)
+    P = mpg.spai_build(M).p
+    cfg = mpg.GmresConfig(rel_tol=1e-8)
+    res = mpg.gmres_shifted(op, sigma, b, mpg.PrecondChain(P), transpose, cfg)
+    Mo = orc.kron_assemble(orc.shifted(sigma), Ao, Eo, cap=10**9)
+    Po = orc.spai_build(Mo)[0]
+    xo, ro = orc.gmres_kron(orc.shifted(sigma), Ao, Eo, orc.Chain(Po), b, orc.GmresConfig(1e-8))
+    assert res.report.converged and ro.converged
+    assert res.report.final_residual <= 1e-8 * np.linalg.norm(b)
+    assert rel(res.x, xo) <= 1e-6
+    assert abs(res.report.iterations - ro.iterations) <= max(2, 0.1 * ro.iterations)
+
+
+def test_batch_equals_single_solves(mpg, gen):
+    sysm = gen.config1(N=20)
+    op = mpg.ShiftedOperator(_m(mpg, sysm.a), _m(mpg, sysm.e_csr()))
+    sig = [0.01, 0.3, 5.0, 2.0 + 1.0j]
+    bs = [np.tile(sysm.b[:, 0], 2 if complex(s).imag else 1) for s in sig]
+    cfg = mpg.GmresConfig(rel_tol=1e-9)
+    batch = mpg.gmres_batch(op, sig, bs, transposes=[0, 1, 0, 1], cfg=cfg)
+    for s, b, t, r in zip(sig, bs, [0, 1, 0, 1], batch):
+        single = mpg.gmres_shifted(op, s, b, None, bool(t), cfg)
+        assert r.report.converged
+        assert r.report.iterations == single.report.iterations
+        assert rel(r.x, single.x) <= 1e-12

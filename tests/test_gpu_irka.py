@@ -1,0 +1,120 @@
+"""GPU IRKA parity (north-star tolerances): converged shifts within 1e-6
+relative and H_r(i w) on a fixed 200-point log grid within 1e-6 relative of
+the CPU oracle on the same seeded inputs; plus the reference's oracle-free
+checks (interpolation, projection identities; test_birka.cpp:51-132)."""
+import numpy as np
+import pytest
+
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+GRID = np.logspace(-4, 4, 200)
+
+
+def _m(mpg, h):
+    return mpg.SparseMatrix.from_csr(h.nrows, h.ncols, h.rowptr, h.colind, h.val)
+
+
+def _hr_grid(state):
+    return np.array([state.transfer(1j * w) for w in GRID])
+
+
+def _run_both(mpg, orc, sysm, r, mode, tol=1e-8, gtol=1e-10, max_sweeps=60):
+    ecsr = sysm.e_csr()
+    op = mpg.ShiftedOperator(_m(mpg, sysm.a), _m(mpg, ecsr) if ecsr is not None else None)
+    cfg = mpg.IrkaConfig(r=r, tol=tol, max_sweeps=max_sweeps, seed=1, gmres=mpg.GmresConfig(gtol, 1000))
+    st, rep = mpg.irka_reduce(op, sysm.b, sysm.c, cfg, mode, init_shifts=sysm.shifts[:r], want_bases=True)
+    ocfg = orc.IrkaConfig(r=r, tol=tol, max_sweeps=max_sweeps, seed=1, gmres=orc.GmresConfig(gtol, 1000),
+                          explicit_nnz_cap=10**12, decoupled=True)
+    ores = orc.irka_reduce(orc.Csr.of(sysm.a), orc.Csr.of(ecsr) if ecsr is not None else None, sysm.b, sysm.c, ocfg,
+                           mode=min(mode, 2), init_shifts=sysm.shifts[:r])
+    return op, st, rep, ores
+
+
+@pytest.mark.parametrize("mode", [0, 2, 3])
+def test_irka_config1_small_matches_oracle(mpg, orc, gen, mode):
+    sysm = gen.config1(N=16)
+    op, st, rep, ores = _run_both(mpg, orc, sysm, 4, mode)
+    assert rep.converged and ores.converged
+    lam, lamo = np.sort_complex(st.lam), np.sort_complex(ores.lam)
+    assert rel(lam, lamo) <= 1e-6
+    hg, ho = _hr_grid(st), _hr_grid(ores)
+    assert np.max(np.abs(hg - ho) / np.maximum(np.abs(ho), 1e-300)) <= 1e-6
+
+
+def test_irka_interpolates_at_converged_shifts(mpg, orc, gen):
+    sysm = gen.config1(N=12)
+    op, st, rep, _ = _run_both(mpg, orc, sysm, 4, 2, tol=1e-12, gtol=1e-13, max_sweeps=200)
+    assert rep.converged
+    a = sysm.a.to_dense()
+    e = np.diag(sysm.e_diag)
+    for lam in st.lam:
+        s = -lam
+        h = sysm.c[:, 0] @ np.linalg.solve(s * e - a, sysm.b[:, 0])
+        # H_r(s) = c_r^T (s I - K_r)^{-1} f_r with K_r = E_r^{-1} A_r
+        assert abs(h - st.transfer(s)[0, 0]) <= 1e-7 * abs(h)
+
+
+def test_irka_projection_identities(mpg, orc, gen):
+    sysm = gen.config1(N=12)
+    op, st, rep, _ = _run_both(mpg, orc, sysm, 4, 2)
+    v, w = st.v, st.w
+    assert np.linalg.norm(v.T @ v - np.eye(4)) <= 1e-12
+    assert np.linalg.norm(w.T @ w - np.eye(4)) <= 1e-12
+    a = sysm.a.to_dense()
+    e = np.diag(sysm.e_diag)
+    er = w.T @ e @ v
+    assert np.linalg.norm(np.linalg.solve(er, w.T @ a @ v) - st.kr) <= 1e-10 * (1 + np.linalg.norm(st.kr))
+    assert np.linalg.norm(np.linalg.solve(er, w.T @ sysm.b) - st.fr) <= 1e-10 * (1 + np.linalg.norm(st.fr))
+    assert np.linalg.norm(v.T @ sysm.c - st.cr) <= 1e-10 * (1 + np.linalg.norm(st.cr))
+
+
+def test_reuse_report_layout(mpg, orc, gen):
+    sysm = gen.config1(N=12)
+    op, st, rep, _ = _run_both(mpg, orc, sysm, 4, 2, tol=1e-4)
+    assert rep.converged and 2 <= rep.sweeps <= 16
+    kinds = [r.kind for r in rep.rows]
+    assert all(r.solves == 1 and r.point in (1, 2) for r in rep.rows)
+    first = [r for r in rep.rows if r.sweep == 1]
+    assert all(r.kind == "fresh" for r in first)
+    later = [r for r in rep.rows if r.sweep > 1]
+    assert all(r.kind in ("vertical", "fresh") for r in later)
+    assert kinds.count("vertical") >= len(later) - 4
+    for r in rep.rows:
+        if r.kind == "vertical":
+            assert r.min_residual <= r.matrix_change
+
+
+def test_irka_identity_mass_matches_reference_loop(mpg, orc, gen):
+    # E = I: the toy bilinear model with N = 0 (test_birka.cpp:51-75), default seed
+    k, f, c = gen.bilinear_toy(8, 1, 5)
+    op = mpg.ShiftedOperator(_m(mpg, k))
+    cfg = mpg.IrkaConfig(r=2, tol=1e-12, max_sweeps=200, seed=5, gmres=mpg.GmresConfig(1e-13, 1000))
+    st, rep = mpg.irka_reduce(op, f, c, cfg, mpg.PrecondMode.NONE)
+    ores = orc.irka_reduce(orc.Csr.of(k), None, f, c, orc.IrkaConfig(r=2, tol=1e-12, max_sweeps=200, seed=5,
+                                                                       gmres=orc.GmresConfig(1e-13, 1000)), mode=0)
+    assert rep.converged and ores.converged
+    assert rel(np.sort_complex(st.lam), np.sort_complex(ores.lam)) <= 1e-8
+    kd = k.to_dense()
+    for lam in st.lam:
+        s = -lam
+        h = c[:, 0] @ np.linalg.solve(s * np.eye(8) - kd, f[:, 0])
+        assert abs(h - st.transfer(s)[0, 0]) <= 1e-8 * abs(h)
+
+
+def test_spai_bench_rows_and_parity(mpg, orc, gen):
+    sysm = gen.config1(N=16)
+    op = mpg.ShiftedOperator(_m(mpg, sysm.a), _m(mpg, sysm.e_csr()))
+    pts = [6.28, 80.0, 300.0]
+    g = mpg.GmresConfig(1e-8, 500)
+    res = mpg.run_spai_bench(op, sysm.b[:, 0], pts, gmres=g, keep_solutions=True)
+    assert res.failed_solves == 0
+    assert [r.kind for r in res.report.rows] == ["fresh", "horizontal", "horizontal"]
+    rows, failed, xo = orc.spai_bench(orc.Csr.of(sysm.a), orc.Csr.of(sysm.e_csr()), sysm.b[:, 0], pts,
+                                      gmres=orc.GmresConfig(1e-8, 500), keep_solutions=True)
+    assert failed == 0
+    for i in range(3):
+        assert rel(res.x[i], xo[i]) <= 1e-6
+    bad = mpg.run_spai_bench(op, sysm.b[:, 0], pts, gmres=mpg.GmresConfig(1e-6, 3), mode=mpg.PrecondMode.NONE)
+    assert bad.failed_solves == 3 and not bad.report.converged
