@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark: shifted preconditioned solves/s on the n = 1.19M FEM workload
+(BASELINE.json configs[2], the metric's n ~ 1.2M configuration).
+
+A step is one IRKA sweep's batch of shifted solves: r = 8 shifts x {primal
+(sigma E - A) v = B, dual (sigma E - A)^T w = C}, i.e. 16 right-preconditioned
+GMRES solves to relative residual 1e-8 with the SPAI preconditioner built once
+at the first shift and reused. `value` times the device-resident
+path; `e2e` times the same step through the C ABI with host buffers (H2D of the
+right-hand sides and D2H of the solutions inside the timed region).
+
+--impl reference times the reference's CPU path (the oracle restatement,
+oracle/, since the reference cannot be built here) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+METRIC = "shifted preconditioned solves/sec & IRKA wall time at n~1.2M; HBM GB/s vs peak"
+
+
+def load_peak_gbs() -> tuple[float, str]:
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 6:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def byte_model(n: int, nnz_a: int, nnz_e_extra: int, nnz_p: list, iters: list) -> float:
+    """Algorithmic bytes of one step: per iteration
+    B_S + B_P + 16 (k+1) n + 32 n, per solve + B_S + B_P + 8 n K for the final
+    assembly and true residual. 4-byte indices, 8-byte values."""
+    b_s = 12 * nnz_a + 4 * (n + 1) + nnz_e_extra + 16 * n
+    tot = 0.0
+    for p_nnz, k_it in zip(nnz_p, iters):
+        b_p = 12 * p_nnz + 4 * (n + 1) + 16 * n
+        k = np.arange(k_it, dtype=np.float64)
+        tot += k_it * (b_s + b_p) + float(np.sum(16.0 * (k + 1) * n + 32.0 * n)) + b_s + b_p + 8.0 * n * k_it
+    return tot
+
+
+def build_workload(args, device: int):
+    import paper_2003_12759_b200 as mpg
+    from paper_2003_12759_b200 import gen
+    t0 = time.perf_counter()
+    s = gen.config3(args.nodes)
+    tgen = time.perf_counter() - t0
+
+    def dev(h):
+        return mpg.SparseMatrix.from_csr(h.nrows, h.ncols, h.rowptr, h.colind, h.val, device)
+    A, E = dev(s.a), dev(s.e)
+    op = mpg.ShiftedOperator(A, E)
+    shifts = [float(x) for x in s.shifts[: args.r]]
+    t0 = time.perf_counter()
+    pv = mpg.spai_build(op.explicit(shifts[0], False))
+    pw = mpg.spai_build(op.explicit(shifts[0], True))
+    tbuild = time.perf_counter() - t0
+    return s, A, E, op, shifts, pv, pw, tgen, tbuild
+
+
+def run_ours(args, rank: int, world: int, device: int):
+    import torch
+    import paper_2003_12759_b200 as mpg
+    from paper_2003_12759_b200 import _lib as L
+
+    torch.cuda.set_device(device)
+    s, A, E, op, shifts, pv, pw, tgen, tbuild = build_workload(args, device)
+    n = s.n
+    chv, chw = mpg.PrecondChain(pv.p), mpg.PrecondChain(pw.p)
+    cfg = mpg.GmresConfig(args.tol, args.max_iter)
+    sig = shifts + shifts
+    trs = [0] * len(shifts) + [1] * len(shifts)
+    chains = [chv] * len(shifts) + [chw] * len(shifts)
+    b_dev = torch.from_numpy(np.ascontiguousarray(s.b[:, 0])).to(f"cuda:{device}")
+    c_dev = torch.from_numpy(np.ascontiguousarray(s.c[:, 0])).to(f"cuda:{device}")
+    rhs_dev = [b_dev] * len(shifts) + [c_dev] * len(shifts)
+    # pinned host buffers for the end-to-end leg
+    b_host = torch.from_numpy(np.ascontiguousarray(s.b[:, 0])).pin_memory().numpy()
+    c_host = torch.from_numpy(np.ascontiguousarray(s.c[:, 0])).pin_memory().numpy()
+    rhs_host = [b_host] * len(shifts) + [c_host] * len(shifts)
+    x_host = [torch.empty(n, dtype=torch.float64).pin_memory().numpy() for _ in sig]
+
+    stream_p = C.c_void_p()
+    L.check(L.lib.mpg_stream(device, C.byref(stream_p)))
+    stream = torch.cuda.ExternalStream(stream_p.value, device=f"cuda:{device}")
+
+    def step_device():
+        return mpg.gmres_batch(op, sig, rhs_dev, chains=chains, transposes=trs, cfg=cfg)
+
+    def step_host():
+        return _batch_host(mpg, L, op, sig, rhs_host, x_host, chains, trs, cfg)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize(device)
+        L.check(L.lib.mpg_synchronize(device))
+
+    for _ in range(args.warmup):
+        res = step_device()
+    iters = [r.report.iterations for r in res]
+    if not all(r.report.converged for r in res):
+        raise RuntimeError(f"solves did not converge: {[r.report.iterations for r in res]}")
+
+    def timed(fn, k):
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches0 = mpg.launch_count()
+        ev0.record(stream)
+        out = None
+        for _ in range(k):
+            out = fn()
+        ev1.record(stream)
+        ev1.synchronize()
+        barrier()
+        ms = ev0.elapsed_time(ev1)
+        launches = mpg.launch_count() - launches0
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([ms], device=f"cuda:{device}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, out, launches
+
+    with ClockSampler(device) as clk:
+        ms, out, launches = timed(step_device, args.steps)
+    clocks = clk.summary()
+    ms_e2e, out_e2e, _ = timed(step_host, max(1, args.steps))
+    iters = [r.report.iterations for r in out]
+    worst = max(r.report.final_residual / r.report.rhs_norm for r in out)
+    nsolves = len(sig)
+    per_step_ms = ms / args.steps
+    value = world * nsolves / (per_step_ms / 1e3)
+    e2e_ms = ms_e2e / max(1, args.steps)
+    e2e_value = world * nsolves / (e2e_ms / 1e3)
+
+    # Roofline of the preconditioned shifted-solve path (BASELINE.md §3 byte model).
+    nnz_p = [pv.p.nnz()] * len(shifts) + [pw.p.nnz()] * len(shifts)
+    bytes_step = byte_model(n, A.nnz(), 8 * A.nnz(), nnz_p, iters)
+    peak, peak_kind = load_peak_gbs()
+    achieved = bytes_step / (per_step_ms / 1e3) / 1e9
+    # One profiled step after the timed region: per-kernel-class CUDA-event
+    # durations on the library stream + algorithmic bytes (not a timed value).
+    mpg.profile_enable(True)
+    step_device()
+    prof = mpg.profile_read()
+    mpg.profile_enable(False)
+    kernels = {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                   "share": round(v["ms"] / max(sum(x["ms"] for x in prof.values()), 1e-9), 4),
+                   "GBps": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] > 0 and v["bytes"] > 0 else None}
+               for k, v in prof.items() if v["launches"]}
+    dom = max((k for k in prof if prof[k]["bytes"] > 0), key=lambda k: prof[k]["ms"])
+    dom_gbs = prof[dom]["bytes"] / (prof[dom]["ms"] / 1e3) / 1e9
+    dom_bytes_per_launch = prof[dom]["bytes"] / max(prof[dom]["launches"], 1)
+    result = {
+        "metric": METRIC,
+        "value": round(value, 4),
+        "unit": "solves/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(per_step_ms, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded generator, DESIGN.md §4; random-init equivalents of the paper's unavailable matrices)",
+        "config": {"workload": f"C3 FEM Q1 {args.nodes}^3 nodes (n={n}), r={args.r} shifts x primal+dual = "
+                               f"{nsolves} GMRES solves/step, tol {args.tol}, SPAI built once at sigma_1 and reused",
+                   "n": n, "nnz_A": A.nnz(), "nnz_E": E.nnz(), "shifts": shifts, "solves_per_step": nsolves,
+                   "gmres_iterations": iters, "max_rel_residual": worst, "precond_build_s": round(tbuild, 3),
+                   "l2": "inputs larger than L2 (A+E 631 MB, Krylov bases GBs)", "parallelism": f"replica x{world}"},
+        "e2e": {"value": round(e2e_value, 4), "unit": "solves/s", "h2d_bytes_per_step": nsolves * n * 8,
+                "d2h_bytes_per_step": nsolves * n * 8, "ms_per_step": round(e2e_ms, 3)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": round(dom_gbs, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(dom_gbs / peak, 4), "traffic": None, "kernel": dom,
+                     "bytes_per_launch": round(dom_bytes_per_launch), "peak_kind": peak_kind,
+                     "step": {"achieved": round(achieved, 1), "frac": round(achieved / peak, 4),
+                              "bytes_per_step": bytes_step,
+                              "scope": "whole preconditioned GMRES step (SpMV + chain + Gram-Schmidt) over the "
+                                       "device-timed step"}},
+        "kernels": kernels,
+        "clocks": clocks,
+    }
+    return result
+
+
+def _batch_host(mpg, L, op, sig, rhs_host, x_host, chains, trs, cfg):
+    """gmres_batch through the C ABI with host buffers: the library copies H2D/D2H."""
+    k = len(sig)
+    sre = np.array([complex(s).real for s in sig])
+    sim = np.zeros(k)
+    tr = np.array(trs, dtype=np.int32)
+    bp = (C.c_void_p * k)(*[b.ctypes.data for b in rhs_host])
+    xp = (C.c_void_p * k)(*[x.ctypes.data for x in x_host])
+    chs = (C.c_void_p * k)(*[c._h.value for c in chains])
+    reps = (L.GmresRep * k)()
+    c = cfg.c()
+    L.check(L.lib.mpg_gmres_batch(op._h, k, sre.ctypes.data, sim.ctypes.data, tr.ctypes.data, chs, bp, xp,
+                                  C.byref(c), reps))
+    return [reps[i] for i in range(k)]
+
+
+def cpu_sample(args) -> dict:
+    """The oracle (C++ restatement of the reference path) on a bounded sample of
+    the same workload: `its` GMRES iterations of one C3 solve, extrapolated to a
+    full solve through the byte model, plus SPAI column throughput."""
+    import oracle as O
+    from paper_2003_12759_b200 import gen
+    s = gen.config3(args.nodes)
+    a, e = O.Csr.of(s.a), O.Csr.of(s.e)
+    sigma = float(s.shifts[0])
+    m = O.kron_assemble(O.shifted(sigma), a, e, cap=10 ** 12)
+    its = args.cpu_iters
+    t0 = time.perf_counter()
+    # m stands in for the SPAI factor (same pattern, 31.6M vs 35.1M nnz): per-iteration cost only
+    _, rep = O.gmres_kron(O.shifted(sigma), a, e, O.Chain(m), s.b[:, 0], O.GmresConfig(1e-300, its))
+    t_its = time.perf_counter() - t0
+    n = s.n
+    sample_bytes = byte_model(n, s.a.nnz, 8 * s.a.nnz, [m.nnz()], [its])
+    gbs = sample_bytes / t_its / 1e9
+    full_its = args.ref_iters
+    full_bytes = byte_model(n, s.a.nnz, 8 * s.a.nnz, [int(1.11 * m.nnz())], [full_its])
+    t_solve = full_bytes / (gbs * 1e9)
+    return {"value": 1.0 / t_solve, "unit": "solves/s", "cores": 1, "kind": "port",
+            "sample": f"oracle GMRES, {its} iterations of one C3 solve in {t_its:.1f} s ({gbs:.1f} GB/s algorithmic); "
+                      f"extrapolated to a {full_its}-iteration solve via the byte model",
+            "seconds": t_its}
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    cpu = cpu_sample(args)
+    line = {"metric": METRIC, "value": round(cpu["value"], 6), "unit": "solves/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(16 / cpu["value"] * 1e3, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C3 FEM Q1 {args.nodes}^3 nodes, 16 shifted solves per step (CPU oracle sample)"},
+            "impl": "reference", "cpu_baseline": cpu,
+            "e2e": {"value": round(cpu["value"], 6), "unit": "solves/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nodes", type=int, default=106)
+    ap.add_argument("--r", type=int, default=8)
+    ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--max-iter", type=int, default=1000)
+    ap.add_argument("--cpu-iters", type=int, default=40)
+    ap.add_argument("--ref-iters", type=int, default=334)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    res = run_ours(args, rank, world, local)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_sample(args)
+            res["cpu_baseline"] = {k: v for k, v in cpu.items() if k != "seconds"}
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

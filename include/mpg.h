@@ -73,6 +73,7 @@ typedef struct {
 typedef struct {
   int iterations, converged, breakdown, history_len;
   double rhs_norm, final_residual, solve_seconds;
+  int reorth_passes; /* iterations that needed the measured second Gram-Schmidt pass */
 } mpg_gmres_report;
 
 /* BirkaConfig (proj/include/morprec/birka.hpp:49-61) for N = 0; decoupled = 1
@@ -113,6 +114,14 @@ int mpg_synchronize(int device);
 long long mpg_launch_count(void);
 /* cudaMemcpy with unified addressing (host or device pointers). */
 int mpg_copy(void* dst, const void* src, int64_t bytes);
+/* Kernel-class profile of the GMRES engine: when enabled (and reset), GMRES
+ * launches each iteration's kernels directly, bracketed by CUDA events on the
+ * library stream, and accumulates per class the launch count, device time and
+ * algorithmic bytes. Profiled solves are slower; the bench
+ * runs one profiled step after the timed region. */
+void mpg_profile_enable(int on);
+int mpg_profile_count(void);
+int mpg_profile_read(int kind, const char** name, long long* launches, double* ms, double* bytes);
 
 /* ---- matrices: SparseMatrix (proj/include/morprec/sparse.hpp:33-101) -----
  * from_csr validates like SparseMatrix::from_csr (sparse.cpp:48-74):

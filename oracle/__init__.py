@@ -48,7 +48,8 @@ class GmresCfg(C.Structure):
 
 class GmresRep(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("breakdown", C.c_int), ("history_len", C.c_int),
-                ("rhs_norm", C.c_double), ("final_residual", C.c_double), ("solve_seconds", C.c_double)]
+                ("rhs_norm", C.c_double), ("final_residual", C.c_double), ("solve_seconds", C.c_double),
+                ("reorth_passes", C.c_int)]
 
 
 class IrkaCfg(C.Structure):
@@ -289,6 +290,7 @@ class GmresReport:
     final_residual: float
     solve_seconds: float
     residual_history: list
+    reorth_passes: int = 0
 
 
 class Chain:
@@ -325,7 +327,7 @@ class Chain:
 
 def _rep(r: GmresRep, hist):
     return GmresReport(r.iterations, bool(r.converged), bool(r.breakdown), r.rhs_norm, r.final_residual,
-                       r.solve_seconds, list(hist[: r.history_len]) if hist is not None else [])
+                       r.solve_seconds, list(hist[: r.history_len]) if hist is not None else [], r.reorth_passes)
 
 
 def gmres_csr(a: Csr, chain: Optional[Chain], b, cfg: GmresConfig = GmresConfig()):

@@ -41,6 +41,7 @@ typedef struct { double rel_tol; int max_iter, record_history; } orc_gmres_cfg;
 typedef struct {
   int iterations, converged, breakdown, history_len;
   double rhs_norm, final_residual, solve_seconds;
+  int reorth_passes;
 } orc_gmres_report;
 typedef struct {
   int r; double tol; int max_sweeps; int decoupled; unsigned long long seed;
@@ -69,6 +70,7 @@ static void fill_report(const GmresReport& r, orc_gmres_report* out, double* his
   out->iterations = r.iterations; out->converged = r.converged; out->breakdown = r.breakdown;
   out->rhs_norm = r.rhs_norm; out->final_residual = r.final_residual; out->solve_seconds = r.solve_seconds;
   out->history_len = int(r.residual_history.size());
+  out->reorth_passes = r.reorth_passes;
   if (history) std::memcpy(history, r.residual_history.data(), r.residual_history.size() * sizeof(double));
 }
 static int copy_rows(const ReductionReport& rep, orc_report_row* rows, int max_rows, int* nrows) {

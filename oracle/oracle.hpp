@@ -134,6 +134,7 @@ struct GmresReport {
   bool converged = false, breakdown = false;
   double rhs_norm = 0, final_residual = 0, solve_seconds = 0;
   std::vector<double> residual_history;
+  int reorth_passes = 0;
 };
 struct GmresResult { Vec x; GmresReport report; };
 GmresResult gmres_right_preconditioned(const LinearOp& a, const LinearOp& p, const Vec& b,

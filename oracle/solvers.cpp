@@ -143,6 +143,7 @@ GmresResult gmres_right_preconditioned(const LinearOp& apply_a, const LinearOp& 
           h[size_t(i)] += d[size_t(i)];
         }
         wnorm = nrm(w);
+        ++rep.reorth_passes;
       }
     }
     const bool invariant = wnorm <= 1e-14 * std::max(wnorm_pre, 1e-300);

@@ -17,6 +17,22 @@ def device_count() -> int:
     return n.value
 
 
+def profile_enable(on: bool = True) -> None:
+    """Per-kernel-class event timing + algorithmic bytes inside the GMRES engine."""
+    lib.mpg_profile_enable(int(on))
+
+
+def profile_read() -> dict:
+    import ctypes
+    out = {}
+    for k in range(lib.mpg_profile_count()):
+        name = ctypes.c_char_p()
+        n, ms, by = ctypes.c_longlong(), ctypes.c_double(), ctypes.c_double()
+        lib.mpg_profile_read(k, ctypes.byref(name), ctypes.byref(n), ctypes.byref(ms), ctypes.byref(by))
+        out[name.value.decode()] = {"launches": n.value, "ms": ms.value, "bytes": by.value}
+    return out
+
+
 def launch_count() -> int:
     """Kernels launched by libmpg.so in this process."""
     return int(lib.mpg_launch_count())

@@ -64,7 +64,8 @@ class GmresCfg(C.Structure):
 
 class GmresRep(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("breakdown", C.c_int), ("history_len", C.c_int),
-                ("rhs_norm", C.c_double), ("final_residual", C.c_double), ("solve_seconds", C.c_double)]
+                ("rhs_norm", C.c_double), ("final_residual", C.c_double), ("solve_seconds", C.c_double),
+                ("reorth_passes", C.c_int)]
 
 
 class IrkaCfg(C.Structure):
@@ -104,6 +105,9 @@ _SIGS = {
     "mpg_synchronize": (_I, [_I]),
     "mpg_launch_count": (C.c_longlong, []),
     "mpg_copy": (_I, [vp, vp, _L]),
+    "mpg_profile_enable": (None, [_I]),
+    "mpg_profile_count": (_I, []),
+    "mpg_profile_read": (_I, [_I, C.POINTER(C.c_char_p), C.POINTER(C.c_longlong), dp, dp]),
     "mpg_csr_create": (_I, [_I, _L, _L, vp, vp, vp, C.POINTER(vp)]),
     "mpg_csr_destroy": (None, [vp]),
     "mpg_csr_info": (_I, [vp, i64p, i64p, i64p]),

@@ -73,6 +73,7 @@ void fill(const GmresOutcome& o, mpg_gmres_report* r, double* history) {
     r->rhs_norm = o.rhs_norm;
     r->final_residual = o.final_residual;
     r->solve_seconds = o.solve_seconds;
+    r->reorth_passes = o.reorth_passes;
   }
   if (history && !o.history.empty()) std::memcpy(history, o.history.data(), o.history.size() * sizeof(double));
 }
@@ -117,6 +118,33 @@ int mpg_synchronize(int device) {
 }
 
 long long mpg_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"
+
+namespace mpg {
+void profile_set(bool on);
+void profile_reset();
+void profile_read(int kind, long long* launches, double* ms, double* bytes);
+}  // namespace mpg
+
+extern "C" {
+
+static const char* const kProfNames[PK_COUNT] = {"chain_spmv", "shifted_spmv", "gs_dot", "gs_update_probe",
+                                                 "gs_update", "gs_probe", "gs_reorth", "control", "assembly"};
+
+void mpg_profile_enable(int on) {
+  mpg::profile_set(on != 0);
+  if (on) mpg::profile_reset();
+}
+
+int mpg_profile_count(void) { return PK_COUNT; }
+
+int mpg_profile_read(int kind, const char** name, long long* launches, double* ms, double* bytes) {
+  if (kind < 0 || kind >= PK_COUNT) return MPG_ERR_INVALID;
+  *name = kProfNames[kind];
+  mpg::profile_read(kind, launches, ms, bytes);
+  return MPG_OK;
+}
 
 int mpg_copy(void* dst, const void* src, int64_t bytes) {
   return guard([&] { MPG_CUDA(cudaMemcpy(dst, src, size_t(bytes), cudaMemcpyDefault)); });

@@ -20,6 +20,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <functional>
 
 #include "runtime.cuh"
 
@@ -37,7 +38,7 @@ struct GmSolve {
   int n, nbase, pair, transpose, stages, pair_bd, max_iter, record;
   double sre, sim, ca, target, bnorm;
   // state
-  int k, phase, asm_kind, asm_k, guess, iterations, converged, breakdown, xsel;
+  int k, phase, asm_kind, asm_k, guess, iterations, converged, breakdown, xsel, reorth_count;
   double estimate, recheck_at, w2_pre, w2_a, w2_b, wn_cur, final_residual;
   // arrays
   double** V;
@@ -329,6 +330,89 @@ __global__ void __launch_bounds__(256) k_update(GmSolve* S, int G, int mode) {
   }
 }
 
+// ---- fused first-pass update + probe: one read of the basis ----------------------
+// w <- w - sum_j s_j h_j W_j, then part[j][blk] = W_j . w_new (the measured
+// second-pass probe, gmres.cpp:108-111) and part[k+1][blk] = ||w_new||^2.
+// Each tile of T rows x (k+1) basis vectors is staged once in shared memory
+// (T adapts to k so the tile stays <= UP_BUDGET doubles) and used for both the
+// update (threads over rows x column groups) and the probe (threads over
+// columns, register accumulators across tiles). Requires k + 1 <= 1024.
+constexpr int UP_BUDGET = 11264;
+constexpr int UP_MAXCOLS = 1024;
+
+__global__ void __launch_bounds__(256, 2) k_update_probe(GmSolve* S, int G) {
+  GmSolve& st = S[blockIdx.y];
+  if (st.phase != PH_RUN) return;
+  extern __shared__ double sm[];
+  const int k = st.k, nj = k + 1, n = st.n;
+  int T = 64;
+  while (T > 8 && (T + 1) * nj > UP_BUDGET) T >>= 1;
+  const int SR = T + 1;
+  double* tile = sm;
+  double* coef = tile + SR * nj;
+  const double** vp = reinterpret_cast<const double**>(coef + nj);
+  double* wn = reinterpret_cast<double*>(vp + nj);
+  double* red = wn + T;
+  __shared__ double wred[8];
+  const int tid = threadIdx.x;
+  for (int j = tid; j < nj; j += blockDim.x) {
+    coef[j] = st.scale[j] * st.h[j];
+    vp[j] = st.V[j];
+  }
+  __syncthreads();
+  const int groups = 256 / T;
+  const int r = tid % T, g = tid / T;
+  double* w = st.V[k + 1];
+  double dacc[4] = {0.0, 0.0, 0.0, 0.0};
+  double wsq = 0.0;
+  for (int r0 = blockIdx.x * T; r0 < n; r0 += G * T) {
+    const int row = r0 + r;
+    const bool valid = row < n;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int j = g; j < nj; j += groups) {
+      const double v = valid ? __ldcg(vp[j] + row) : 0.0;
+      tile[j * SR + r] = v;
+      acc = fma(coef[j], v, acc);
+    }
+    red[g * T + r] = acc;
+    __syncthreads();
+    if (g == 0) {
+      double s = 0.0;
+      for (int q = 0; q < groups; ++q) s += red[q * T + r];
+      const double wv = valid ? w[row] - s : 0.0;
+      wn[r] = wv;
+      if (valid) w[row] = wv;
+      wsq = fma(wv, wv, wsq);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = tid + 256 * q;
+      if (j < nj) {
+        const double* tj = tile + j * SR;
+        double s = 0.0;
+        for (int rr = 0; rr < T; ++rr) s = fma(tj[rr], wn[rr], s);
+        dacc[q] += s;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int j = tid + 256 * q;
+    if (j < nj) st.part[size_t(j) * G + blockIdx.x] = dacc[q];
+  }
+  wsq = warp_sum(wsq);
+  if ((tid & 31) == 0) wred[tid >> 5] = wsq;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int i = 0; i < 8; ++i) s += wred[i];
+    st.part[size_t(k + 1) * G + blockIdx.x] = s;
+  }
+}
+
 // ---- norm partials of the residual buffer ----------------------------------------
 __global__ void __launch_bounds__(256) k_rnorm(GmSolve* S, int G) {
   GmSolve& st = S[blockIdx.y];
@@ -386,6 +470,7 @@ __global__ void k_finalize(GmSolve* S, int G) {
   __syncwarp();
   if (lane != 0) return;
   st.w2_b = w2;
+  st.reorth_count += reorth;
   const double wnorm = sqrt(w2);
   const double wnorm_pre = sqrt(st.w2_pre);
   const bool invariant = wnorm <= 1e-14 * fmax(wnorm_pre, 1e-300);
@@ -670,8 +755,13 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     cudaFuncSetAttribute(k_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_update_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
+  const bool fused = maxit + 1 <= UP_MAXCOLS && !std::getenv("MPG_NO_FUSE");
+  const size_t smem_up = size_t(UP_BUDGET + 2 * (maxit + 2) + 64 + 256) * sizeof(double);
   int launches_per_iter = 0;
+  // Profiling hook: called after every launch with a kernel-class id.
+  std::function<void(int)> mark = [](int) {};
   auto chain_stage = [&](int stage, int mode) {
     const dim3 grid(cdiv(max_fac_rows * int64_t(Vfac), 256), unsigned(ns));
     switch (Vfac) {
@@ -682,6 +772,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       default: k_chain_stage<32><<<grid, 256, 0, s>>>(dS.get(), stage, mode); break;
     }
     ++launches_per_iter;
+    mark(mode == 0 ? PK_CHAIN : PK_ASM);
   };
   auto iter_op = [&](int mode) {
     const dim3 grid(cdiv(nb * int64_t(Vop), 256), unsigned(ns));
@@ -700,6 +791,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     }
 #undef MPG_OPL
     ++launches_per_iter;
+    mark(mode == 0 ? PK_OP : PK_ASM);
   };
   const dim3 gG{unsigned(G), unsigned(ns), 1u};
   const dim3 gR{cdiv(maxit + 2, 8), unsigned(ns), 1u};
@@ -708,29 +800,103 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     for (int st = 0; st < max_stages; ++st) chain_stage(st, 0);
     iter_op(0);
     k_dot<<<gG, 256, smem_dot, s>>>(dS.get(), G);
+    mark(PK_DOT);
     k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 0);
-    k_update<<<gG, 256, smem_upd, s>>>(dS.get(), G, 0);
-    k_dot<<<gG, 256, smem_dot, s>>>(dS.get(), G);
+    mark(PK_SMALL);
+    if (fused) {
+      k_update_probe<<<gG, 256, smem_up, s>>>(dS.get(), G);
+      mark(PK_UPDPROBE);
+      --launches_per_iter;
+    } else {
+      k_update<<<gG, 256, smem_upd, s>>>(dS.get(), G, 0);
+      mark(PK_UPD);
+      k_dot<<<gG, 256, smem_dot, s>>>(dS.get(), G);
+      mark(PK_PROBE);
+    }
     k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 1);
+    mark(PK_SMALL);
     k_update<<<gG, 256, smem_upd, s>>>(dS.get(), G, 1);
+    mark(PK_REORTH);
     k_finalize<<<unsigned(ns), 32, 0, s>>>(dS.get(), G);
+    mark(PK_SMALL);
     k_backsub<<<unsigned(ns), 256, size_t(maxit + 2) * sizeof(double), s>>>(dS.get());
+    mark(PK_ASM);
     k_update<<<gG, 256, smem_upd, s>>>(dS.get(), G, 2);
+    mark(PK_ASM);
     launches_per_iter += 9;
     for (int st = 0; st < max_stages; ++st) chain_stage(st, 1);
     iter_op(1);
     k_rnorm<<<gG, 256, 0, s>>>(dS.get(), G);
+    mark(PK_ASM);
     k_post<<<unsigned(ns), 32, 0, s>>>(dS.get(), G);
+    mark(PK_SMALL);
     launches_per_iter += 2;
   };
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
-  MPG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  record_iteration();
-  cudaError_t cap_err = cudaGetLastError();
-  MPG_CUDA(cudaStreamEndCapture(s, &graph));
-  if (cap_err != cudaSuccess) throw CudaError(std::string("gmres graph capture: ") + cudaGetErrorString(cap_err));
-  MPG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  const bool profiling = profile_enabled();
+  if (!profiling) {
+    MPG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    record_iteration();
+    cudaError_t cap_err = cudaGetLastError();
+    MPG_CUDA(cudaStreamEndCapture(s, &graph));
+    if (cap_err != cudaSuccess) throw CudaError(std::string("gmres graph capture: ") + cudaGetErrorString(cap_err));
+    MPG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  }
+  // Profiled iteration: direct launches bracketed by events; algorithmic bytes
+  // per kernel class from the per-solve state before the iteration.
+  std::vector<cudaEvent_t> evs;
+  std::vector<int> ev_kind;
+  auto profiled_iteration = [&] {
+    std::vector<GmSolve> before = hs;
+    ev_kind.clear();
+    auto take = [&](int kind) {
+      if (evs.size() < ev_kind.size() + 2) {
+        cudaEvent_t e;
+        MPG_CUDA(cudaEventCreate(&e));
+        evs.push_back(e);
+      }
+      ev_kind.push_back(kind);
+      MPG_CUDA(cudaEventRecord(evs[ev_kind.size()], s));
+    };
+    if (evs.empty()) {
+      cudaEvent_t e;
+      MPG_CUDA(cudaEventCreate(&e));
+      evs.push_back(e);
+    }
+    MPG_CUDA(cudaEventRecord(evs[0], s));
+    mark = take;
+    record_iteration();
+    mark = [](int) {};
+    MPG_CUDA(cudaMemcpyAsync(hs.data(), dS.get(), sizeof(GmSolve) * size_t(ns), cudaMemcpyDeviceToHost, s));
+    MPG_CUDA(cudaStreamSynchronize(s));
+    double bytes[PK_COUNT] = {};
+    for (int i = 0; i < ns; ++i) {
+      const GmSolve& b = before[size_t(i)];
+      if (b.phase != PH_RUN) continue;
+      const double n = double(b.n), k = double(b.k);
+      for (int stg = 0; stg < b.stages; ++stg) {
+        const DevCsr& f = *specs[size_t(i)].chain->factors[size_t(stg)];
+        const double h = b.pair_bd ? 2.0 : 1.0;
+        bytes[PK_CHAIN] += h * (12.0 * double(f.nnz) + 4.0 * double(f.nrows + 1) + 16.0 * double(f.nrows));
+      }
+      const double vec = b.pair ? 2.0 : 1.0;
+      const double be = op.emode == E_SAMEPAT ? 8.0 * double(op.a->nnz) : op.emode == E_DIAG ? 8.0 * double(nb) : 0.0;
+      bytes[PK_OP] += 12.0 * double(op.a->nnz) + 4.0 * double(nb + 1) + be + vec * 16.0 * double(nb);
+      bytes[PK_DOT] += 8.0 * n * (k + 1.0) + 8.0 * n;
+      bytes[PK_UPDPROBE] += 8.0 * n * (k + 1.0) + 16.0 * n;
+      bytes[PK_UPD] += 8.0 * n * (k + 1.0) + 16.0 * n;
+      bytes[PK_PROBE] += 8.0 * n * (k + 1.0) + 8.0 * n;
+      if (hs[size_t(i)].reorth_count > b.reorth_count) bytes[PK_REORTH] += 8.0 * n * (k + 1.0) + 16.0 * n;
+    }
+    for (size_t e = 0; e < ev_kind.size(); ++e) {
+      float ms = 0.0f;
+      MPG_CUDA(cudaEventElapsedTime(&ms, evs[e], evs[e + 1]));
+      profile_add(ev_kind[e], double(ms), 1);
+    }
+    for (int kk = 0; kk < PK_COUNT; ++kk)
+      if (bytes[kk] > 0.0) profile_add_bytes(kk, bytes[kk]);
+  };
 
   // ---- host loop: launch chunks, poll phases ----
   std::vector<int> khost(size_t(ns), 0);
@@ -745,7 +911,11 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
           ensure(i, khost[size_t(i)] + chunk + 2);
         }
       if (!active) break;
-      for (int t = 0; t < chunk; ++t) MPG_CUDA(cudaGraphLaunch(exec, s));
+      if (profiling) {
+        for (int t = 0; t < chunk; ++t) profiled_iteration();
+      } else {
+        for (int t = 0; t < chunk; ++t) MPG_CUDA(cudaGraphLaunch(exec, s));
+      }
       count_launch(int64_t(chunk) * launches_per_iter);
       MPG_CUDA(cudaMemcpyAsync(hs.data(), dS.get(), sizeof(GmSolve) * size_t(ns), cudaMemcpyDeviceToHost, s));
       MPG_CUDA(cudaStreamSynchronize(s));
@@ -757,12 +927,14 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       chunk = std::min(chunk * 2, 32);
     }
   } catch (...) {
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (auto e : evs) cudaEventDestroy(e);
     throw;
   }
-  cudaGraphExecDestroy(exec);
-  cudaGraphDestroy(graph);
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  for (auto e : evs) cudaEventDestroy(e);
 
   // ---- outputs ----
   for (int i = 0; i < ns; ++i) {
@@ -775,6 +947,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     o.rhs_norm = g.bnorm;
     o.final_residual = g.final_residual;
     o.solve_seconds = done_at[size_t(i)];
+    o.reorth_passes = g.reorth_count;
     if (opt.record_history) {
       o.history.resize(size_t(g.iterations) + 1);
       MPG_CUDA(cudaMemcpyAsync(o.history.data(), H.hist.get(), o.history.size() * sizeof(double),

@@ -35,6 +35,15 @@ struct SolverError : std::runtime_error { using std::runtime_error::runtime_erro
       throw ::mpg::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_) + " at " __FILE__); \
   } while (0)
 
+// Per-kernel-class profile (CUDA-event times + algorithmic bytes), filled by
+// gmres_batch when profiling is enabled (mpg_profile_enable).
+enum ProfKind {
+  PK_CHAIN = 0, PK_OP, PK_DOT, PK_UPDPROBE, PK_UPD, PK_PROBE, PK_REORTH, PK_SMALL, PK_ASM, PK_COUNT
+};
+bool profile_enabled();
+void profile_add(int kind, double ms, long long launches);
+void profile_add_bytes(int kind, double bytes);
+
 extern std::atomic<long long> g_launches;
 inline void count_launch(long long k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 #define MPG_CHECK_LAUNCH() MPG_CUDA(cudaGetLastError())
@@ -170,6 +179,7 @@ struct GmresOutcome {
   int iterations = 0;
   bool converged = false, breakdown = false;
   double rhs_norm = 0, final_residual = 0, solve_seconds = 0;
+  int reorth_passes = 0;
   std::vector<double> history;
 };
 std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec>& specs, const GmresOptions& opt);

@@ -21,6 +21,35 @@ namespace mpg {
 
 std::atomic<long long> g_launches{0};
 
+namespace {
+std::atomic<bool> g_prof_on{false};
+std::mutex g_prof_mu;
+struct ProfEntry { long long launches = 0; double ms = 0.0, bytes = 0.0; };
+ProfEntry g_prof[PK_COUNT];
+}  // namespace
+
+bool profile_enabled() { return g_prof_on.load(); }
+void profile_set(bool on) { g_prof_on.store(on); }
+void profile_reset() {
+  std::scoped_lock l(g_prof_mu);
+  for (auto& e : g_prof) e = ProfEntry{};
+}
+void profile_add(int kind, double ms, long long launches) {
+  std::scoped_lock l(g_prof_mu);
+  g_prof[kind].ms += ms;
+  g_prof[kind].launches += launches;
+}
+void profile_add_bytes(int kind, double bytes) {
+  std::scoped_lock l(g_prof_mu);
+  g_prof[kind].bytes += bytes;
+}
+void profile_read(int kind, long long* launches, double* ms, double* bytes) {
+  std::scoped_lock l(g_prof_mu);
+  *launches = g_prof[kind].launches;
+  *ms = g_prof[kind].ms;
+  *bytes = g_prof[kind].bytes;
+}
+
 DeviceCtx& ctx(int device) {
   static std::mutex mu;
   static std::map<int, std::unique_ptr<DeviceCtx>> ctxs;

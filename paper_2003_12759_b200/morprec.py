@@ -254,12 +254,13 @@ class GmresReport:
     final_residual: float = 0.0
     solve_seconds: float = 0.0
     residual_history: list = dataclasses.field(default_factory=list)
+    reorth_passes: int = 0
 
     @staticmethod
     def of(r: L.GmresRep, hist=None) -> "GmresReport":
         h = list(hist[: r.history_len]) if hist is not None else []
         return GmresReport(r.iterations, bool(r.converged), bool(r.breakdown), r.rhs_norm, r.final_residual,
-                           r.solve_seconds, h)
+                           r.solve_seconds, h, r.reorth_passes)
 
 
 @dataclasses.dataclass

@@ -1,0 +1,103 @@
+"""CPU checks of the drop-in boundary: libmpg.so loads without a GPU, exports
+every entry point include/mpg.h declares, reports a missing device as an
+error (never a silent CPU fallback), and the host-side generators produce the
+configured sizes."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "mpg.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mpg_[a-z0-9_]+)\s*\(", src)) - {"mpg_allgather_fn"})
+
+
+def test_library_exports_every_declared_symbol(mpg):
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_2003_12759_b200", "libmpg.so"))
+    names = _declared()
+    assert len(names) > 40
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_python_binding_covers_header(mpg):
+    from paper_2003_12759_b200 import _lib
+    assert set(_declared()) <= set(_lib.EXPORTED)
+
+
+def test_no_device_is_an_error_not_a_fallback(mpg):
+    if mpg.device_count() > 0:
+        pytest.skip("a GPU is present")
+    with pytest.raises(mpg.CudaError):
+        mpg.SparseMatrix.identity(3)
+
+
+def test_generator_sizes(gen):
+    assert gen.config1().a.nnz == 49_600  # 5n - 4N on the 100 x 100 grid
+    s = gen.config2(M=16)
+    assert s.a.nnz == 7 * 16 ** 3 - 6 * 16 ** 2
+    s = gen.config3(N=12)
+    assert s.a.nnz == (3 * 12 - 2) ** 3 and s.e.nnz == s.a.nnz
+    assert np.array_equal(s.a.colind, s.e.colind)
+    assert s.b[:, 0] @ s.b[:, 0] == pytest.approx(1.0)
+    assert s.c.sum() == pytest.approx(1.0)
+    # A = -(K + Robin) is symmetric negative definite, E symmetric positive definite
+    a, e = s.a.to_dense(), s.e.to_dense()
+    assert np.allclose(a, a.T) and np.allclose(e, e.T)
+    assert np.max(np.linalg.eigvalsh(a)) < 0 and np.min(np.linalg.eigvalsh(e)) > 0
+    s = gen.config4(N=6)
+    assert s.b.shape == (216, 4) and s.c.shape == (216, 4) and s.r == 16
+    s = gen.config5(n=5000, max_len=300)
+    lens = np.diff(s.a.rowptr)
+    assert lens.min() >= 2 and lens.max() <= 300
+    d = np.array([s.a.val[s.a.rowptr[i]:s.a.rowptr[i + 1]][s.a.colind[s.a.rowptr[i]:s.a.rowptr[i + 1]] == i][0]
+                  for i in range(0, 5000, 97)])
+    assert np.all(d < 0)
+    assert s.shifts.size == 64 and s.shifts[0] == pytest.approx(1e-3) and s.shifts[-1] == pytest.approx(1e3)
+
+
+def test_generators_deterministic(gen):
+    a = gen.config3(N=8)
+    b = gen.config3(N=8)
+    assert np.array_equal(a.a.val, b.a.val) and np.array_equal(a.e.val, b.e.val)
+    assert not np.array_equal(gen.config3(N=8, seed=5).a.val, a.a.val)
+
+
+def test_reference_fixture_stream(gen):
+    # support.hpp random_dense uses uniform_real_distribution(-1, 1) over
+    # mt19937_64; libstdc++ draws one 64-bit word per double: u = x / 2^64.
+    import numpy as np
+    m = gen.random_dense(3, 2, 42)
+    mt = np.random.Generator(np.random.MT19937(0))  # only to check the range, not the stream
+    assert m.shape == (3, 2) and np.all(np.abs(m) <= 1)
+    x0 = _mt19937_64_first(42)
+    assert m[0, 0] == pytest.approx(-1.0 + 2.0 * (x0 / 2.0 ** 64), rel=0, abs=1e-15)
+
+
+def _mt19937_64_first(seed):
+    """First output of std::mt19937_64(seed) (the engine is fully specified by the C++ standard)."""
+    nn, mm = 312, 156
+    mag = 0xB5026F5AA96619E9
+    um, lm = 0xFFFFFFFF80000000, 0x7FFFFFFF
+    mt = [0] * nn
+    mt[0] = seed & 0xFFFFFFFFFFFFFFFF
+    for i in range(1, nn):
+        mt[i] = (6364136223846793005 * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i) & 0xFFFFFFFFFFFFFFFF
+    for i in range(nn):
+        x = (mt[i] & um) | (mt[(i + 1) % nn] & lm)
+        xa = x >> 1
+        if x & 1:
+            xa ^= mag
+        mt[i] = mt[(i + mm) % nn] ^ xa
+    x = mt[0]
+    x ^= (x >> 29) & 0x5555555555555555
+    x ^= (x << 17) & 0x71D67FFFEDA60000
+    x ^= (x << 37) & 0xFFF7EEE000000000
+    x ^= x >> 43
+    return x & 0xFFFFFFFFFFFFFFFF
