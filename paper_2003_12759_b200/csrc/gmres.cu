@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(256) k_chain_stage(GmSolve* S, int stage, int 
   if (row < f.nrows * halves) {
     const int b = f.rowptr[r], e = f.rowptr[r + 1];
     const double* x = src + off;
-    for (int k = b + lane; k < e; k += V) acc = fma(f.val[k], __ldg(x + f.colind[k]), acc);
+#pragma unroll 4
+    for (int k = b + lane; k < e; k += V) acc = fma(__ldcs(f.val + k), __ldg(x + __ldcs(f.colind + k)), acc);
   }
   acc = sub_sum<V>(acc);
   if (row < f.nrows * halves && lane == 0) dst[off + r] = acc;
@@ -115,9 +116,10 @@ __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView 
   if (row < n) {
     const int b = op.a.rowptr[row], e = op.a.rowptr[row + 1];
     if (EM == E_SAMEPAT) {
+#pragma unroll 4
       for (int k = b + lane; k < e; k += V) {
-        const double2 ae = op.ae[k];
-        const int c = op.a.colind[k];
+        const double2 ae = __ldcs(op.ae + k);
+        const int c = __ldcs(op.a.colind + k);
         const double x1 = __ldg(x + c);
         a1 = fma(ae.x, x1, a1);
         e1 = fma(ae.y, x1, e1);
@@ -128,9 +130,10 @@ __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView 
         }
       }
     } else {
+#pragma unroll 4
       for (int k = b + lane; k < e; k += V) {
-        const double av = op.a.val[k];
-        const int c = op.a.colind[k];
+        const double av = __ldcs(op.a.val + k);
+        const int c = __ldcs(op.a.colind + k);
         a1 = fma(av, __ldg(x + c), a1);
         if (pair) a2 = fma(av, __ldg(x + n + c), a2);
       }
@@ -340,14 +343,17 @@ __global__ void __launch_bounds__(256) k_update(GmSolve* S, int G, int mode) {
 constexpr int UP_BUDGET = 11264;
 constexpr int UP_MAXCOLS = 1024;
 
-__global__ void __launch_bounds__(256, 2) k_update_probe(GmSolve* S, int G) {
+// UPDATE = false is the first (projection) pass alone: part[j][blk] = W_j . w
+// and part[k+1][blk] = ||w||^2 with the same staging.
+template <bool UPDATE>
+__global__ void __launch_bounds__(256, 2) k_gs_tile(GmSolve* S, int G) {
   GmSolve& st = S[blockIdx.y];
   if (st.phase != PH_RUN) return;
   extern __shared__ double sm[];
   const int k = st.k, nj = k + 1, n = st.n;
   int T = 64;
-  while (T > 8 && (T + 1) * nj > UP_BUDGET) T >>= 1;
-  const int SR = T + 1;
+  while (T > 8 && (T + 2) * nj > UP_BUDGET) T >>= 1;
+  const int SR = T + 2;  // even: 16-byte aligned rows for cp.async; breaks phase-2 bank strides
   double* tile = sm;
   double* coef = tile + SR * nj;
   const double** vp = reinterpret_cast<const double**>(coef + nj);
@@ -356,33 +362,51 @@ __global__ void __launch_bounds__(256, 2) k_update_probe(GmSolve* S, int G) {
   __shared__ double wred[8];
   const int tid = threadIdx.x;
   for (int j = tid; j < nj; j += blockDim.x) {
-    coef[j] = st.scale[j] * st.h[j];
+    if (UPDATE) coef[j] = st.scale[j] * st.h[j];
     vp[j] = st.V[j];
   }
   __syncthreads();
   const int groups = 256 / T;
   const int r = tid % T, g = tid / T;
+  const int half = T / 2;
+  const int ld = (n + 31) & ~31;  // padded vector length (padding is zero)
   double* w = st.V[k + 1];
   double dacc[4] = {0.0, 0.0, 0.0, 0.0};
   double wsq = 0.0;
+  const unsigned tile_s = static_cast<unsigned>(__cvta_generic_to_shared(tile));
   for (int r0 = blockIdx.x * T; r0 < n; r0 += G * T) {
+    // stage the T x (k+1) block of the basis with asynchronous 16-byte copies
+    for (int idx = tid; idx < nj * half; idx += 256) {
+      const int j = idx / half, r2 = 2 * (idx - j * half);
+      const int row = r0 + r2;
+      const unsigned dst = tile_s + unsigned((j * SR + r2) * 8);
+      if (row + 1 < ld) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(vp[j] + row));
+      } else {
+        asm volatile("st.shared.v2.f64 [%0], {%1, %1};\n" ::"r"(dst), "d"(0.0));
+      }
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
     const int row = r0 + r;
     const bool valid = row < n;
-    double acc = 0.0;
-#pragma unroll 8
-    for (int j = g; j < nj; j += groups) {
-      const double v = valid ? __ldcg(vp[j] + row) : 0.0;
-      tile[j * SR + r] = v;
-      acc = fma(coef[j], v, acc);
-    }
-    red[g * T + r] = acc;
-    __syncthreads();
-    if (g == 0) {
-      double s = 0.0;
-      for (int q = 0; q < groups; ++q) s += red[q * T + r];
-      const double wv = valid ? w[row] - s : 0.0;
+    if (UPDATE) {
+      double acc = 0.0;
+#pragma unroll 4
+      for (int j = g; j < nj; j += groups) acc = fma(coef[j], tile[j * SR + r], acc);
+      red[g * T + r] = acc;
+      __syncthreads();
+      if (g == 0) {
+        double s = 0.0;
+        for (int q = 0; q < groups; ++q) s += red[q * T + r];
+        const double wv = valid ? w[row] - s : 0.0;
+        wn[r] = wv;
+        if (valid) w[row] = wv;
+        wsq = fma(wv, wv, wsq);
+      }
+    } else if (g == 0) {
+      const double wv = valid ? w[row] : 0.0;
       wn[r] = wv;
-      if (valid) w[row] = wv;
       wsq = fma(wv, wv, wsq);
     }
     __syncthreads();
@@ -718,6 +742,10 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     while (int(H.panels.size()) * PANEL < upto) {
       H.panels.emplace_back(dev, size_t(PANEL) * size_t(H.ld));
       double* base = H.panels.back().get();
+      const int nvec = hs[size_t(i)].n;
+      if (H.ld > nvec)  // the staged Gram-Schmidt kernels read the (zero) padding rows
+        MPG_CUDA(cudaMemset2DAsync(base + nvec, size_t(H.ld) * sizeof(double), 0, size_t(H.ld - nvec) * sizeof(double),
+                                   PANEL, s));
       const int p0 = int(H.panels.size() - 1) * PANEL;
       for (int j = 0; j < PANEL && p0 + j < maxit + 2; ++j) H.vtab[size_t(p0 + j)] = base + size_t(j) * size_t(H.ld);
     }
@@ -755,7 +783,8 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     cudaFuncSetAttribute(k_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_update_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_gs_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_gs_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
   const bool fused = maxit + 1 <= UP_MAXCOLS && !std::getenv("MPG_NO_FUSE");
   const size_t smem_up = size_t(UP_BUDGET + 2 * (maxit + 2) + 64 + 256) * sizeof(double);
@@ -799,12 +828,13 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     launches_per_iter = 0;
     for (int st = 0; st < max_stages; ++st) chain_stage(st, 0);
     iter_op(0);
-    k_dot<<<gG, 256, smem_dot, s>>>(dS.get(), G);
+    if (fused) k_gs_tile<false><<<gG, 256, smem_up, s>>>(dS.get(), G);
+    else k_dot<<<gG, 256, smem_dot, s>>>(dS.get(), G);
     mark(PK_DOT);
     k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 0);
     mark(PK_SMALL);
     if (fused) {
-      k_update_probe<<<gG, 256, smem_up, s>>>(dS.get(), G);
+      k_gs_tile<true><<<gG, 256, smem_up, s>>>(dS.get(), G);
       mark(PK_UPDPROBE);
       --launches_per_iter;
     } else {

@@ -101,3 +101,17 @@ def _mt19937_64_first(seed):
     x ^= (x << 37) & 0xFFF7EEE000000000
     x ^= x >> 43
     return x & 0xFFFFFFFFFFFFFFFF
+
+
+def test_cpp_mirror_header_compiles_and_links(mpg, tmp_path):
+    """include/morprec_gpu.hpp (the C++ mirror of proj/include/morprec over the C ABI) builds and links."""
+    import shutil
+    import subprocess
+    if shutil.which("g++") is None:
+        pytest.skip("no g++")
+    exe = tmp_path / "cpp_api_demo"
+    libdir = os.path.join(ROOT, "paper_2003_12759_b200")
+    subprocess.run(["g++", "-std=c++17", "-O1", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "cpp_api_demo.cpp"), "-L", libdir, "-lmpg",
+                    f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    assert exe.exists()
