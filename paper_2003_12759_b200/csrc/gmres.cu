@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(256) k_dot(GmSolve* S, int G) {
 }
 
 // ---- reduce partials: which 0 -> h (and w2_pre), 1 -> d (and w2_a) -------------
-__global__ void k_reduce(GmSolve* S, int G, int which) {
+__global__ void k_reduce(GmSolve* S, int G, int which, int cnt) {
   GmSolve& st = S[blockIdx.y];
   if (st.phase != PH_RUN) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -243,7 +243,7 @@ __global__ void k_reduce(GmSolve* S, int G, int which) {
   if (j > k + 1) return;
   const double* p = st.part + size_t(j) * G;
   double s = 0.0;
-  for (int i = lane; i < G; i += 32) s += p[i];
+  for (int i = lane; i < cnt; i += 32) s += p[i];
   s = warp_sum(s);
   if (lane != 0) return;
   if (j <= k) {
@@ -333,90 +333,111 @@ __global__ void __launch_bounds__(256) k_update(GmSolve* S, int G, int mode) {
   }
 }
 
-// ---- fused first-pass update + probe: one read of the basis ----------------------
-// w <- w - sum_j s_j h_j W_j, then part[j][blk] = W_j . w_new (the measured
-// second-pass probe, gmres.cpp:108-111) and part[k+1][blk] = ||w_new||^2.
-// Each tile of T rows x (k+1) basis vectors is staged once in shared memory
-// (T adapts to k so the tile stays <= UP_BUDGET doubles) and used for both the
-// update (threads over rows x column groups) and the probe (threads over
-// columns, register accumulators across tiles). Requires k + 1 <= 1024.
-constexpr int UP_BUDGET = 11264;
+// ---- staged Gram-Schmidt passes: one read of the basis each ---------------------
+// UPDATE: w <- w - sum_j s_j h_j W_j, then part[j][blk] = W_j . w_new (the
+// measured second-pass probe, gmres.cpp:101-111) and part[k+1][blk] =
+// ||w_new||^2. !UPDATE: the first (projection) pass, part[j][blk] = W_j . w and
+// part[k+1][blk] = ||w||^2.
+// A tile is T rows x (k+1) basis vectors (T adapts to k so a tile stays <=
+// UP_BUF doubles). Phase 1 streams the tile from HBM with 128-bit loads issued
+// in batches of 8 (threads over row pairs x column groups), accumulates the
+// update in registers and parks the values in shared memory; phase 2 computes
+// the dot products thread-per-column from shared memory (SR = T + 2 keeps the
+// 128-bit reads of a quarter-warp on distinct banks) with register
+// accumulators across tiles. One HBM read, one smem write, one smem read per
+// element. (A 1-D TMA bulk copy per vector measured ~5x slower: 256-byte copies
+// are TMA-op-rate bound.) Two 256-thread CTAs per SM. Requires k + 1 <= 1024.
+constexpr int UP_BUF = 11264;
 constexpr int UP_MAXCOLS = 1024;
+constexpr int GS_THREADS = 256;
+constexpr int UP_SMEM_DOUBLES = UP_BUF + 2 * UP_MAXCOLS + 64 + 2 * GS_THREADS;
 
-// UPDATE = false is the first (projection) pass alone: part[j][blk] = W_j . w
-// and part[k+1][blk] = ||w||^2 with the same staging.
 template <bool UPDATE>
-__global__ void __launch_bounds__(256, 2) k_gs_tile(GmSolve* S, int G) {
+__global__ void __launch_bounds__(GS_THREADS, 2) k_gs_tile(GmSolve* S, int G, int nblk) {
   GmSolve& st = S[blockIdx.y];
   if (st.phase != PH_RUN) return;
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   const int k = st.k, nj = k + 1, n = st.n;
   int T = 64;
-  while (T > 8 && (T + 2) * nj > UP_BUDGET) T >>= 1;
-  const int SR = T + 2;  // even: 16-byte aligned rows for cp.async; breaks phase-2 bank strides
+  while (T > 8 && (T + 2) * nj > UP_BUF) T >>= 1;
+  const int SR = T + 2;  // SR = 2 mod 4: conflict-free 128-bit column reads
   double* tile = sm;
-  double* coef = tile + SR * nj;
-  const double** vp = reinterpret_cast<const double**>(coef + nj);
-  double* wn = reinterpret_cast<double*>(vp + nj);
-  double* red = wn + T;
-  __shared__ double wred[8];
-  const int tid = threadIdx.x;
-  for (int j = tid; j < nj; j += blockDim.x) {
-    if (UPDATE) coef[j] = st.scale[j] * st.h[j];
+  double* coef = tile + UP_BUF;
+  const double** vp = reinterpret_cast<const double**>(coef + UP_MAXCOLS);
+  double* wn = reinterpret_cast<double*>(vp + UP_MAXCOLS);
+  double* red = wn + 64;  // 2 * GS_THREADS
+  __shared__ double wred[GS_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int j = tid; j < nj; j += GS_THREADS) {
+    coef[j] = UPDATE ? st.scale[j] * st.h[j] : 0.0;
     vp[j] = st.V[j];
   }
   __syncthreads();
-  const int groups = 256 / T;
-  const int r = tid % T, g = tid / T;
   const int half = T / 2;
-  const int ld = (n + 31) & ~31;  // padded vector length (padding is zero)
+  const int groups = GS_THREADS / half;
+  const int r2 = 2 * (tid % half), g = tid / half;
   double* w = st.V[k + 1];
   double dacc[4] = {0.0, 0.0, 0.0, 0.0};
   double wsq = 0.0;
-  const unsigned tile_s = static_cast<unsigned>(__cvta_generic_to_shared(tile));
-  for (int r0 = blockIdx.x * T; r0 < n; r0 += G * T) {
-    // stage the T x (k+1) block of the basis with asynchronous 16-byte copies
-    for (int idx = tid; idx < nj * half; idx += 256) {
-      const int j = idx / half, r2 = 2 * (idx - j * half);
-      const int row = r0 + r2;
-      const unsigned dst = tile_s + unsigned((j * SR + r2) * 8);
-      if (row + 1 < ld) {
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(vp[j] + row));
-      } else {
-        asm volatile("st.shared.v2.f64 [%0], {%1, %1};\n" ::"r"(dst), "d"(0.0));
+  const int ld = (n + 31) & ~31;
+  for (int r0 = blockIdx.x * T; r0 < n; r0 += nblk * T) {
+    const int row = r0 + r2;
+    const bool inb = row + 1 < ld;  // padded rows are zero; past ld read nothing
+    double2 acc = make_double2(0.0, 0.0);
+    for (int j0 = g; j0 < nj; j0 += 8 * groups) {
+      const double* p[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u * groups;
+        p[u] = j < nj ? vp[j] : nullptr;
+      }
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = (p[u] && inb) ? __ldcs(reinterpret_cast<const double2*>(p[u] + row)) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u * groups;
+        if (j < nj) {
+          *reinterpret_cast<double2*>(tile + j * SR + r2) = v[u];
+          if (UPDATE) {
+            const double c = coef[j];
+            acc.x = fma(c, v[u].x, acc.x);
+            acc.y = fma(c, v[u].y, acc.y);
+          }
+        }
       }
     }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-    __syncthreads();
-    const int row = r0 + r;
-    const bool valid = row < n;
     if (UPDATE) {
-      double acc = 0.0;
-#pragma unroll 4
-      for (int j = g; j < nj; j += groups) acc = fma(coef[j], tile[j * SR + r], acc);
-      red[g * T + r] = acc;
-      __syncthreads();
-      if (g == 0) {
+      red[2 * (g * half) + r2] = acc.x;
+      red[2 * (g * half) + r2 + 1] = acc.y;
+    }
+    __syncthreads();
+    if (tid < T) {
+      const int rr = tid, rw = r0 + rr;
+      const bool valid = rw < n;
+      double wv = valid ? w[rw] : 0.0;
+      if (UPDATE) {
         double s = 0.0;
-        for (int q = 0; q < groups; ++q) s += red[q * T + r];
-        const double wv = valid ? w[row] - s : 0.0;
-        wn[r] = wv;
-        if (valid) w[row] = wv;
-        wsq = fma(wv, wv, wsq);
+        for (int q = 0; q < groups; ++q) s += red[2 * (q * half) + rr];
+        wv = valid ? wv - s : 0.0;
+        if (valid) w[rw] = wv;
       }
-    } else if (g == 0) {
-      const double wv = valid ? w[row] : 0.0;
-      wn[r] = wv;
+      wn[rr] = wv;
       wsq = fma(wv, wv, wsq);
     }
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int j = tid + 256 * q;
+      const int j = tid + GS_THREADS * q;
       if (j < nj) {
         const double* tj = tile + j * SR;
         double s = 0.0;
-        for (int rr = 0; rr < T; ++rr) s = fma(tj[rr], wn[rr], s);
+        for (int rr = 0; rr < T; rr += 2) {
+          const double2 a = *reinterpret_cast<const double2*>(tj + rr);
+          s = fma(a.x, wn[rr], s);
+          s = fma(a.y, wn[rr + 1], s);
+        }
         dacc[q] += s;
       }
     }
@@ -424,17 +445,157 @@ __global__ void __launch_bounds__(256, 2) k_gs_tile(GmSolve* S, int G) {
   }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int j = tid + 256 * q;
+    const int j = tid + GS_THREADS * q;
     if (j < nj) st.part[size_t(j) * G + blockIdx.x] = dacc[q];
   }
   wsq = warp_sum(wsq);
-  if ((tid & 31) == 0) wred[tid >> 5] = wsq;
+  if (lane == 0) wred[warp] = wsq;
   __syncthreads();
   if (tid == 0) {
     double s = 0.0;
-    for (int i = 0; i < 8; ++i) s += wred[i];
+    for (int i = 0; i < GS_THREADS / 32; ++i) s += wred[i];
     st.part[size_t(k + 1) * G + blockIdx.x] = s;
   }
+}
+
+// ---- register-tiled Gram-Schmidt passes (the default path) -----------------------
+// Same contract as k_gs_tile. A 512-thread CTA (one per SM) streams tiles of
+// T rows x (k+1) basis vectors through REGISTERS: thread (rg, cg) owns rows
+// {2 rg, 2 rg + 1} of columns cg, cg + CG, ... (GR_CPT = 8 columns), loaded
+// with 128-bit loads; the loads of tile t+1 are issued before tile t is
+// consumed (register double buffer, ~64 KB in flight per SM). The update
+// reduces row sums across the CG column groups through shared memory (TPR
+// threads per row + shuffles); the probe / projection dot products accumulate
+// per column in registers across all tiles and are reduced across the RG row
+// groups once at the end with shuffles. Each element crosses HBM once.
+// T = 64 / 32 / 16 / 8 for k + 1 <= 128 / 256 / 512 / 1024.
+constexpr int GR_THREADS = 512;
+constexpr int GR_CPT = 8;
+constexpr int GR_SMEM_DOUBLES = 2 * UP_MAXCOLS + 2 * 1024 + 64;  // coef, vp, red (<= 64 x 129), wn
+
+template <int RG, bool UPDATE>
+__device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double* coef, const double** vp,
+                                            double* red, double* wn) {
+  constexpr int CG = GR_THREADS / RG;
+  constexpr int T = 2 * RG;
+  constexpr int TPR = GR_THREADS / T;  // threads per row in the row-sum reduction
+  constexpr int CGP = CG + 1;          // padded partial-sum row
+  const int tid = threadIdx.x;
+  const int rg = tid % RG, cg = tid / RG;
+  const int my_row = tid / TPR, sub = tid % TPR;
+  const int k = st.k, nj = k + 1, n = st.n;
+  const int ld = (n + 31) & ~31;
+  double* w = st.V[k + 1];
+  const double* pcol[GR_CPT];
+  double cf[GR_CPT];
+#pragma unroll
+  for (int c = 0; c < GR_CPT; ++c) {
+    const int j = cg + CG * c;
+    pcol[c] = j < nj ? vp[j] : nullptr;
+    cf[c] = (UPDATE && j < nj) ? coef[j] : 0.0;
+  }
+  double dcol[GR_CPT];
+#pragma unroll
+  for (int c = 0; c < GR_CPT; ++c) dcol[c] = 0.0;
+  double wsq = 0.0;
+  // The w rows of a tile are fetched together with its basis block so their
+  // latency is hidden behind the previous tile as well.
+  auto load = [&](int r0, double2* v, double& wp) {
+    const int row = r0 + 2 * rg;
+    const bool inb = r0 < n && row + 1 < ld;
+#pragma unroll
+    for (int c = 0; c < GR_CPT; ++c)
+      v[c] = (pcol[c] && inb) ? __ldcs(reinterpret_cast<const double2*>(pcol[c] + row)) : make_double2(0.0, 0.0);
+    const int rw = r0 + my_row;
+    wp = (sub == 0 && rw < n) ? w[rw] : 0.0;
+  };
+  auto consume = [&](int r0, const double2* v, double wpre) {
+    const int rw = r0 + my_row;
+    const bool valid = rw < n;
+    if (UPDATE) {
+      double ax = 0.0, ay = 0.0;
+#pragma unroll
+      for (int c = 0; c < GR_CPT; ++c) {
+        ax = fma(cf[c], v[c].x, ax);
+        ay = fma(cf[c], v[c].y, ay);
+      }
+      red[(2 * rg) * CGP + cg] = ax;
+      red[(2 * rg + 1) * CGP + cg] = ay;
+      __syncthreads();
+      double sacc = red[my_row * CGP + 2 * sub] + red[my_row * CGP + 2 * sub + 1];
+#pragma unroll
+      for (int o = TPR / 2; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o, TPR);
+      if (sub == 0) {
+        const double wv = valid ? wpre - sacc : 0.0;
+        if (valid) w[rw] = wv;
+        wn[my_row] = wv;
+        wsq = fma(wv, wv, wsq);
+      }
+    } else if (sub == 0) {
+      wn[my_row] = wpre;
+      wsq = fma(wpre, wpre, wsq);
+    }
+    __syncthreads();
+    const double w0 = wn[2 * rg], w1 = wn[2 * rg + 1];
+#pragma unroll
+    for (int c = 0; c < GR_CPT; ++c) dcol[c] = fma(v[c].x, w0, fma(v[c].y, w1, dcol[c]));
+    __syncthreads();  // wn / red are rewritten by the next tile
+  };
+  const int step = nblk * T;
+  double2 va[GR_CPT], vb[GR_CPT];
+  double wa, wb;
+  int r0 = blockIdx.x * T;
+  load(r0, va, wa);
+  while (r0 < n) {
+    load(r0 + step, vb, wb);
+    consume(r0, va, wa);
+    r0 += step;
+    if (r0 >= n) break;
+    load(r0 + step, va, wa);
+    consume(r0, vb, wb);
+    r0 += step;
+  }
+  // column sums across the RG row groups (consecutive lanes), once per CTA
+#pragma unroll
+  for (int c = 0; c < GR_CPT; ++c) {
+    double x = dcol[c];
+#pragma unroll
+    for (int o = RG / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o, RG);
+    const int j = cg + CG * c;
+    if (rg == 0 && j < nj) st.part[size_t(j) * G + blockIdx.x] = x;
+  }
+  // ||w||^2 partial: held by the sub == 0 threads
+  {
+    const double x = warp_sum(wsq);
+    if ((tid & 31) == 0) red[tid >> 5] = x;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double x = 0.0;
+    for (int i = 0; i < GR_THREADS / 32; ++i) x += red[i];
+    st.part[size_t(k + 1) * G + blockIdx.x] = x;
+  }
+}
+
+template <bool UPDATE>
+__global__ void __launch_bounds__(GR_THREADS, 1) k_gs_reg(GmSolve* S, int G, int nblk) {
+  GmSolve& st = S[blockIdx.y];
+  if (st.phase != PH_RUN) return;
+  extern __shared__ __align__(16) double sm[];
+  double* coef = sm;
+  const double** vp = reinterpret_cast<const double**>(sm + UP_MAXCOLS);
+  double* red = sm + 2 * UP_MAXCOLS;
+  double* wn = red + 2 * 1024;
+  const int nj = st.k + 1;
+  for (int j = threadIdx.x; j < nj; j += GR_THREADS) {
+    coef[j] = UPDATE ? st.scale[j] * st.h[j] : 0.0;
+    vp[j] = st.V[j];
+  }
+  __syncthreads();
+  if (nj <= 128) gs_reg_body<32, UPDATE>(st, G, nblk, coef, vp, red, wn);
+  else if (nj <= 256) gs_reg_body<16, UPDATE>(st, G, nblk, coef, vp, red, wn);
+  else if (nj <= 512) gs_reg_body<8, UPDATE>(st, G, nblk, coef, vp, red, wn);
+  else gs_reg_body<4, UPDATE>(st, G, nblk, coef, vp, red, wn);
 }
 
 // ---- norm partials of the residual buffer ----------------------------------------
@@ -783,11 +944,13 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     cudaFuncSetAttribute(k_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_gs_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_gs_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_gs_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, UP_SMEM_DOUBLES * 8);
+    cudaFuncSetAttribute(k_gs_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, UP_SMEM_DOUBLES * 8);
+    cudaFuncSetAttribute(k_gs_reg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GR_SMEM_DOUBLES * 8);
+    cudaFuncSetAttribute(k_gs_reg<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GR_SMEM_DOUBLES * 8);
   });
   const bool fused = maxit + 1 <= UP_MAXCOLS && !std::getenv("MPG_NO_FUSE");
-  const size_t smem_up = size_t(UP_BUDGET + 2 * (maxit + 2) + 64 + 256) * sizeof(double);
+  const size_t smem_up = size_t(UP_SMEM_DOUBLES) * sizeof(double);
   int launches_per_iter = 0;
   // Profiling hook: called after every launch with a kernel-class id.
   std::function<void(int)> mark = [](int) {};
@@ -823,18 +986,27 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     mark(mode == 0 ? PK_OP : PK_ASM);
   };
   const dim3 gG{unsigned(G), unsigned(ns), 1u};
+  // One long-running CTA per SM for the staged Gram-Schmidt passes.
+  const int Ggs = std::max(1, std::min(G, (2 * c.sm_count * 4 + ns - 1) / ns));
+  const dim3 gGs{unsigned(Ggs), unsigned(ns), 1u};
+  const bool regtile = !std::getenv("MPG_GS_SMEM");
+  const int Ggr = std::max(1, std::min(G, (c.sm_count + ns - 1) / ns));
+  const dim3 gGr{unsigned(Ggr), unsigned(ns), 1u};
+  const size_t smem_gr = size_t(GR_SMEM_DOUBLES) * sizeof(double);
   const dim3 gR{cdiv(maxit + 2, 8), unsigned(ns), 1u};
   auto record_iteration = [&] {
     launches_per_iter = 0;
     for (int st = 0; st < max_stages; ++st) chain_stage(st, 0);
     iter_op(0);
-    if (fused) k_gs_tile<false><<<gG, 256, smem_up, s>>>(dS.get(), G);
+    if (fused && regtile) k_gs_reg<false><<<gGr, GR_THREADS, smem_gr, s>>>(dS.get(), G, Ggr);
+    else if (fused) k_gs_tile<false><<<gGs, GS_THREADS, smem_up, s>>>(dS.get(), G, Ggs);
     else k_dot<<<gG, 256, smem_dot, s>>>(dS.get(), G);
     mark(PK_DOT);
-    k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 0);
+    k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 0, fused ? (regtile ? Ggr : Ggs) : G);
     mark(PK_SMALL);
     if (fused) {
-      k_gs_tile<true><<<gG, 256, smem_up, s>>>(dS.get(), G);
+      if (regtile) k_gs_reg<true><<<gGr, GR_THREADS, smem_gr, s>>>(dS.get(), G, Ggr);
+      else k_gs_tile<true><<<gGs, GS_THREADS, smem_up, s>>>(dS.get(), G, Ggs);
       mark(PK_UPDPROBE);
       --launches_per_iter;
     } else {
@@ -843,7 +1015,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       k_dot<<<gG, 256, smem_dot, s>>>(dS.get(), G);
       mark(PK_PROBE);
     }
-    k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 1);
+    k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 1, fused ? (regtile ? Ggr : Ggs) : G);
     mark(PK_SMALL);
     k_update<<<gG, 256, smem_upd, s>>>(dS.get(), G, 1);
     mark(PK_REORTH);
