@@ -32,6 +32,12 @@ constexpr int ASM_RECHECK = 1, ASM_FINISH = 2;
 constexpr int DOT_TILE = 1024;   // rows per tile of the dot kernel
 constexpr int UPD_TILE = 512;    // rows per tile of the update kernel (256 threads x double2)
 constexpr int PANEL = 64;        // basis vectors per allocation panel
+// Row index of a basis vector. Basis vectors are plain contiguous vectors in
+// 64-vector panels. (A chunk-major panel layout, [n/8][64][8], that lets one
+// TMA bulk copy stage the 8-row slab of a whole panel was measured too: its
+// gathers slowed the SpMVs by ~25 % and a TMA-ring Gram-Schmidt kernel built on
+// it reached only 1.3-2.4 TB/s, so the flat layout stays.)
+__host__ __device__ __forceinline__ int vidx(int r) { return r; }
 
 struct GmSolve {
   // configuration
@@ -84,6 +90,7 @@ __global__ void __launch_bounds__(256) k_chain_stage(GmSolve* S, int stage, int 
   const int halves = st.pair_bd ? 2 : 1;
   const int lane = threadIdx.x & (V - 1);
   const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / V);
+  const bool chunked = stage == 0 && mode == 0;  // reads the basis vector V[k]
   const double* src = stage == 0 ? (mode == 0 ? st.V[st.k] : st.ubuf) : ((stage - 1) & 1 ? st.z1 : st.z0);
   double* dst = (stage & 1) ? st.z1 : st.z0;
   double acc = 0.0;
@@ -91,9 +98,15 @@ __global__ void __launch_bounds__(256) k_chain_stage(GmSolve* S, int stage, int 
   if (row >= f.nrows) { r = row - f.nrows; off = f.nrows; }
   if (row < f.nrows * halves) {
     const int b = f.rowptr[r], e = f.rowptr[r + 1];
-    const double* x = src + off;
+    if (chunked) {
 #pragma unroll 4
-    for (int k = b + lane; k < e; k += V) acc = fma(__ldcs(f.val + k), __ldg(x + __ldcs(f.colind + k)), acc);
+      for (int k = b + lane; k < e; k += V)
+        acc = fma(__ldcs(f.val + k), __ldg(src + vidx(off + __ldcs(f.colind + k))), acc);
+    } else {
+      const double* x = src + off;
+#pragma unroll 4
+      for (int k = b + lane; k < e; k += V) acc = fma(__ldcs(f.val + k), __ldg(x + __ldcs(f.colind + k)), acc);
+    }
   }
   acc = sub_sum<V>(acc);
   if (row < f.nrows * halves && lane == 0) dst[off + r] = acc;
@@ -111,6 +124,7 @@ __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView 
   const double* x;
   if (mode == 0) x = st.stages ? ((st.stages - 1) & 1 ? st.z1 : st.z0) : st.V[st.k];
   else x = st.stages ? ((st.stages - 1) & 1 ? st.z1 : st.z0) : st.ubuf;
+  const bool xc = mode == 0 && st.stages == 0;  // x is a chunk-major basis vector
   const bool pair = st.pair;
   double a1 = 0.0, a2 = 0.0, e1 = 0.0, e2 = 0.0;
   if (row < n) {
@@ -120,11 +134,11 @@ __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView 
       for (int k = b + lane; k < e; k += V) {
         const double2 ae = __ldcs(op.ae + k);
         const int c = __ldcs(op.a.colind + k);
-        const double x1 = __ldg(x + c);
+        const double x1 = __ldg(x + (xc ? vidx(c) : c));
         a1 = fma(ae.x, x1, a1);
         e1 = fma(ae.y, x1, e1);
         if (pair) {
-          const double x2 = __ldg(x + n + c);
+          const double x2 = __ldg(x + (xc ? vidx(n + c) : n + c));
           a2 = fma(ae.x, x2, a2);
           e2 = fma(ae.y, x2, e2);
         }
@@ -134,8 +148,8 @@ __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView 
       for (int k = b + lane; k < e; k += V) {
         const double av = __ldcs(op.a.val + k);
         const int c = __ldcs(op.a.colind + k);
-        a1 = fma(av, __ldg(x + c), a1);
-        if (pair) a2 = fma(av, __ldg(x + n + c), a2);
+        a1 = fma(av, __ldg(x + (xc ? vidx(c) : c)), a1);
+        if (pair) a2 = fma(av, __ldg(x + (xc ? vidx(n + c) : n + c)), a2);
       }
     }
   }
@@ -146,13 +160,14 @@ __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView 
     e2 = sub_sum<V>(e2);
   }
   if (row < n && lane == 0) {
+    const int i1 = xc ? vidx(row) : row, i2 = xc ? vidx(n + row) : n + row;
     if (EM == E_IDENT) {
-      e1 = x[row];
-      if (pair) e2 = x[n + row];
+      e1 = x[i1];
+      if (pair) e2 = x[i2];
     } else if (EM == E_DIAG) {
       const double dd = op.ediag[row];
-      e1 = dd * x[row];
-      if (pair) e2 = dd * x[n + row];
+      e1 = dd * x[i1];
+      if (pair) e2 = dd * x[i2];
     }
     const double sre = st.sre, sim = st.sim, ca = st.ca;
     double y1, y2 = 0.0;
@@ -165,12 +180,12 @@ __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView 
     if (mode == 0) {
       double* w = st.V[st.k + 1];
       const double sc = st.scale[st.k];
-      w[row] = sc * y1;
-      if (pair) w[n + row] = sc * y2;
+      w[vidx(row)] = sc * y1;
+      if (pair) w[vidx(n + row)] = sc * y2;
     } else {
       const double* b0 = st.V[0];
-      st.rbuf[row] = b0[row] - y1;
-      if (pair) st.rbuf[n + row] = b0[n + row] - y2;
+      st.rbuf[row] = b0[vidx(row)] - y1;
+      if (pair) st.rbuf[n + row] = b0[vidx(n + row)] - y2;
     }
   }
 }
@@ -194,28 +209,16 @@ __global__ void __launch_bounds__(256) k_dot(GmSolve* S, int G) {
     const int rows = min(DOT_TILE, n - r0);
     __syncthreads();
     for (int i = threadIdx.x; i < DOT_TILE; i += blockDim.x) {
-      const double v = i < rows ? w[r0 + i] : 0.0;
+      const double v = i < rows ? w[vidx(r0 + i)] : 0.0;
       wt[i] = v;
       wsq = fma(v, v, wsq);
     }
     __syncthreads();
-    const bool full = rows == DOT_TILE;
     for (int j = warp; j <= k; j += nw) {
-      const double* vj = st.V[j] + r0;
+      const double* vj = st.V[j];
       double p = 0.0;
-      if (full) {
-        const double2* v2 = reinterpret_cast<const double2*>(vj);
-        const double2* w2 = reinterpret_cast<const double2*>(wt);
 #pragma unroll 4
-        for (int i = lane; i < DOT_TILE / 2; i += 32) {
-          const double2 a = v2[i];
-          const double2 b = w2[i];
-          p = fma(a.x, b.x, p);
-          p = fma(a.y, b.y, p);
-        }
-      } else {
-        for (int i = lane; i < rows; i += 32) p = fma(vj[i], wt[i], p);
-      }
+      for (int i = lane; i < rows; i += 32) p = fma(vj[vidx(r0 + i)], wt[i], p);
       p = warp_sum(p);
       if (lane == 0) acc[j] += p;
     }
@@ -289,15 +292,17 @@ __global__ void __launch_bounds__(256) k_update(GmSolve* S, int G, int mode) {
   const int ntiles = (n + UPD_TILE - 1) / UPD_TILE;
   for (int t = blockIdx.x; t < ntiles; t += G) {
     const int r = t * UPD_TILE + 2 * threadIdx.x;
+    const int vr = vidx(r);               // basis vectors are chunk-major
+    const int wr = mode == 2 ? r : vr;    // ubuf (assembly) is a flat vector
     if (r + 1 < n) {
-      double2 a = mode == 2 ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(w + r);
+      double2 a = mode == 2 ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(w + wr);
       const double sgn = mode == 2 ? 1.0 : -1.0;
       int j = 0;
       for (; j + 4 <= nj; j += 4) {
-        const double2 v0 = *reinterpret_cast<const double2*>(vp[j] + r);
-        const double2 v1 = *reinterpret_cast<const double2*>(vp[j + 1] + r);
-        const double2 v2 = *reinterpret_cast<const double2*>(vp[j + 2] + r);
-        const double2 v3 = *reinterpret_cast<const double2*>(vp[j + 3] + r);
+        const double2 v0 = *reinterpret_cast<const double2*>(vp[j] + vr);
+        const double2 v1 = *reinterpret_cast<const double2*>(vp[j + 1] + vr);
+        const double2 v2 = *reinterpret_cast<const double2*>(vp[j + 2] + vr);
+        const double2 v3 = *reinterpret_cast<const double2*>(vp[j + 3] + vr);
         a.x = fma(sgn * coef[j], v0.x, a.x);
         a.y = fma(sgn * coef[j], v0.y, a.y);
         a.x = fma(sgn * coef[j + 1], v1.x, a.x);
@@ -308,17 +313,17 @@ __global__ void __launch_bounds__(256) k_update(GmSolve* S, int G, int mode) {
         a.y = fma(sgn * coef[j + 3], v3.y, a.y);
       }
       for (; j < nj; ++j) {
-        const double2 v0 = *reinterpret_cast<const double2*>(vp[j] + r);
+        const double2 v0 = *reinterpret_cast<const double2*>(vp[j] + vr);
         a.x = fma(sgn * coef[j], v0.x, a.x);
         a.y = fma(sgn * coef[j], v0.y, a.y);
       }
-      *reinterpret_cast<double2*>(w + r) = a;
+      *reinterpret_cast<double2*>(w + wr) = a;
       wsq = fma(a.x, a.x, fma(a.y, a.y, wsq));
     } else if (r < n) {
-      double a = mode == 2 ? 0.0 : w[r];
+      double a = mode == 2 ? 0.0 : w[wr];
       const double sgn = mode == 2 ? 1.0 : -1.0;
-      for (int j = 0; j < nj; ++j) a = fma(sgn * coef[j], vp[j][r], a);
-      w[r] = a;
+      for (int j = 0; j < nj; ++j) a = fma(sgn * coef[j], vp[j][vr], a);
+      w[wr] = a;
       wsq = fma(a, a, wsq);
     }
   }
@@ -333,133 +338,13 @@ __global__ void __launch_bounds__(256) k_update(GmSolve* S, int G, int mode) {
   }
 }
 
-// ---- staged Gram-Schmidt passes: one read of the basis each ---------------------
-// UPDATE: w <- w - sum_j s_j h_j W_j, then part[j][blk] = W_j . w_new (the
-// measured second-pass probe, gmres.cpp:101-111) and part[k+1][blk] =
-// ||w_new||^2. !UPDATE: the first (projection) pass, part[j][blk] = W_j . w and
-// part[k+1][blk] = ||w||^2.
-// A tile is T rows x (k+1) basis vectors (T adapts to k so a tile stays <=
-// UP_BUF doubles). Phase 1 streams the tile from HBM with 128-bit loads issued
-// in batches of 8 (threads over row pairs x column groups), accumulates the
-// update in registers and parks the values in shared memory; phase 2 computes
-// the dot products thread-per-column from shared memory (SR = T + 2 keeps the
-// 128-bit reads of a quarter-warp on distinct banks) with register
-// accumulators across tiles. One HBM read, one smem write, one smem read per
-// element. (A 1-D TMA bulk copy per vector measured ~5x slower: 256-byte copies
-// are TMA-op-rate bound.) Two 256-thread CTAs per SM. Requires k + 1 <= 1024.
-constexpr int UP_BUF = 11264;
 constexpr int UP_MAXCOLS = 1024;
-constexpr int GS_THREADS = 256;
-constexpr int UP_SMEM_DOUBLES = UP_BUF + 2 * UP_MAXCOLS + 64 + 2 * GS_THREADS;
-
-template <bool UPDATE>
-__global__ void __launch_bounds__(GS_THREADS, 2) k_gs_tile(GmSolve* S, int G, int nblk) {
-  GmSolve& st = S[blockIdx.y];
-  if (st.phase != PH_RUN) return;
-  extern __shared__ __align__(16) double sm[];
-  const int k = st.k, nj = k + 1, n = st.n;
-  int T = 64;
-  while (T > 8 && (T + 2) * nj > UP_BUF) T >>= 1;
-  const int SR = T + 2;  // SR = 2 mod 4: conflict-free 128-bit column reads
-  double* tile = sm;
-  double* coef = tile + UP_BUF;
-  const double** vp = reinterpret_cast<const double**>(coef + UP_MAXCOLS);
-  double* wn = reinterpret_cast<double*>(vp + UP_MAXCOLS);
-  double* red = wn + 64;  // 2 * GS_THREADS
-  __shared__ double wred[GS_THREADS / 32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int j = tid; j < nj; j += GS_THREADS) {
-    coef[j] = UPDATE ? st.scale[j] * st.h[j] : 0.0;
-    vp[j] = st.V[j];
-  }
-  __syncthreads();
-  const int half = T / 2;
-  const int groups = GS_THREADS / half;
-  const int r2 = 2 * (tid % half), g = tid / half;
-  double* w = st.V[k + 1];
-  double dacc[4] = {0.0, 0.0, 0.0, 0.0};
-  double wsq = 0.0;
-  const int ld = (n + 31) & ~31;
-  for (int r0 = blockIdx.x * T; r0 < n; r0 += nblk * T) {
-    const int row = r0 + r2;
-    const bool inb = row + 1 < ld;  // padded rows are zero; past ld read nothing
-    double2 acc = make_double2(0.0, 0.0);
-    for (int j0 = g; j0 < nj; j0 += 8 * groups) {
-      const double* p[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = j0 + u * groups;
-        p[u] = j < nj ? vp[j] : nullptr;
-      }
-      double2 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        v[u] = (p[u] && inb) ? __ldcs(reinterpret_cast<const double2*>(p[u] + row)) : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = j0 + u * groups;
-        if (j < nj) {
-          *reinterpret_cast<double2*>(tile + j * SR + r2) = v[u];
-          if (UPDATE) {
-            const double c = coef[j];
-            acc.x = fma(c, v[u].x, acc.x);
-            acc.y = fma(c, v[u].y, acc.y);
-          }
-        }
-      }
-    }
-    if (UPDATE) {
-      red[2 * (g * half) + r2] = acc.x;
-      red[2 * (g * half) + r2 + 1] = acc.y;
-    }
-    __syncthreads();
-    if (tid < T) {
-      const int rr = tid, rw = r0 + rr;
-      const bool valid = rw < n;
-      double wv = valid ? w[rw] : 0.0;
-      if (UPDATE) {
-        double s = 0.0;
-        for (int q = 0; q < groups; ++q) s += red[2 * (q * half) + rr];
-        wv = valid ? wv - s : 0.0;
-        if (valid) w[rw] = wv;
-      }
-      wn[rr] = wv;
-      wsq = fma(wv, wv, wsq);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = tid + GS_THREADS * q;
-      if (j < nj) {
-        const double* tj = tile + j * SR;
-        double s = 0.0;
-        for (int rr = 0; rr < T; rr += 2) {
-          const double2 a = *reinterpret_cast<const double2*>(tj + rr);
-          s = fma(a.x, wn[rr], s);
-          s = fma(a.y, wn[rr + 1], s);
-        }
-        dacc[q] += s;
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int j = tid + GS_THREADS * q;
-    if (j < nj) st.part[size_t(j) * G + blockIdx.x] = dacc[q];
-  }
-  wsq = warp_sum(wsq);
-  if (lane == 0) wred[warp] = wsq;
-  __syncthreads();
-  if (tid == 0) {
-    double s = 0.0;
-    for (int i = 0; i < GS_THREADS / 32; ++i) s += wred[i];
-    st.part[size_t(k + 1) * G + blockIdx.x] = s;
-  }
-}
 
 // ---- register-tiled Gram-Schmidt passes (the default path) -----------------------
-// Same contract as k_gs_tile. A 512-thread CTA (one per SM) streams tiles of
+// UPDATE: w <- w - sum_j s_j h_j W_j, then part[j][blk] = W_j . w_new (the
+// measured second-pass probe, gmres.cpp:101-111) and part[k+1][blk] =
+// ||w_new||^2. !UPDATE: the first (projection) pass, part[j][blk] = W_j . w
+// and part[k+1][blk] = ||w||^2. A 512-thread CTA (one per SM) streams tiles of
 // T rows x (k+1) basis vectors through REGISTERS: thread (rg, cg) owns rows
 // {2 rg, 2 rg + 1} of columns cg, cg + CG, ... (GR_CPT = 8 columns), loaded
 // with 128-bit loads; the loads of tile t+1 are issued before tile t is
@@ -505,9 +390,9 @@ __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double
     const bool inb = r0 < n && row + 1 < ld;
 #pragma unroll
     for (int c = 0; c < GR_CPT; ++c)
-      v[c] = (pcol[c] && inb) ? __ldcs(reinterpret_cast<const double2*>(pcol[c] + row)) : make_double2(0.0, 0.0);
+      v[c] = (pcol[c] && inb) ? __ldcs(reinterpret_cast<const double2*>(pcol[c] + vidx(row))) : make_double2(0.0, 0.0);
     const int rw = r0 + my_row;
-    wp = (sub == 0 && rw < n) ? w[rw] : 0.0;
+    wp = (sub == 0 && rw < n) ? w[vidx(rw)] : 0.0;
   };
   auto consume = [&](int r0, const double2* v, double wpre) {
     const int rw = r0 + my_row;
@@ -527,7 +412,7 @@ __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double
       for (int o = TPR / 2; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o, TPR);
       if (sub == 0) {
         const double wv = valid ? wpre - sacc : 0.0;
-        if (valid) w[rw] = wv;
+        if (valid) w[vidx(rw)] = wv;
         wn[my_row] = wv;
         wsq = fma(wv, wv, wsq);
       }
@@ -636,7 +521,7 @@ __device__ void continue_iter(GmSolve& st) {
 }
 
 // ---- finalize the iteration: reorth bookkeeping, Givens, decisions ----------------
-__global__ void k_finalize(GmSolve* S, int G) {
+__global__ void k_finalize(GmSolve* S, int G, int cnt2) {
   GmSolve& st = S[blockIdx.x];
   if (st.phase != PH_RUN) return;
   const int lane = threadIdx.x;
@@ -648,7 +533,7 @@ __global__ void k_finalize(GmSolve* S, int G) {
   double w2 = st.w2_a;
   if (reorth) {
     double s = 0.0;
-    for (int i = lane; i < G; i += 32) s += st.part[size_t(k + 1) * G + i];
+    for (int i = lane; i < cnt2; i += 32) s += st.part[size_t(k + 1) * G + i];
     w2 = warp_sum(s);
     for (int j = lane; j <= k; j += 32) st.h[j] += st.d[j];
   }
@@ -771,7 +656,10 @@ __global__ void __launch_bounds__(256) k_bnorm_part(GmSolve* S, int G) {
   __shared__ double red[8];
   const double* b = st.V[0];
   double s = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < st.n; i += G * blockDim.x) s = fma(b[i], b[i], s);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < st.n; i += G * blockDim.x) {
+    const double v = b[vidx(i)];
+    s = fma(v, v, s);
+  }
   s = warp_sum(s);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
   __syncthreads();
@@ -780,6 +668,13 @@ __global__ void __launch_bounds__(256) k_bnorm_part(GmSolve* S, int G) {
     for (int i = 0; i < int(blockDim.x >> 5); ++i) t += red[i];
     st.part[blockIdx.x] = t;
   }
+}
+
+// V[0] <- b in the chunk-major basis layout (b staged flat in rbuf).
+__global__ void k_pack_rhs(GmSolve* S) {
+  GmSolve& st = S[blockIdx.y];
+  double* v0 = st.V[0];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < st.n; i += gridDim.x * blockDim.x) v0[vidx(i)] = st.rbuf[i];
 }
 
 inline unsigned cdiv(int64_t a, int64_t b) { return unsigned((a + b - 1) / b); }
@@ -848,7 +743,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     g.record = opt.record_history;
     g.target = opt.rel_tol;  // scaled by bnorm in k_init
     g.phase = PH_RUN;
-    H.ld = int((n + 31) / 32 * 32);
+    H.ld = int((n + 31) / 32 * 32);  // rows per panel (multiple of the 16-row chunk)
     H.dV = DBuf<double*>(dev, size_t(maxit) + 2);
     H.vtab.assign(size_t(maxit) + 2, nullptr);
     const size_t m1 = size_t(maxit) + 2;
@@ -903,10 +798,8 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     while (int(H.panels.size()) * PANEL < upto) {
       H.panels.emplace_back(dev, size_t(PANEL) * size_t(H.ld));
       double* base = H.panels.back().get();
-      const int nvec = hs[size_t(i)].n;
-      if (H.ld > nvec)  // the staged Gram-Schmidt kernels read the (zero) padding rows
-        MPG_CUDA(cudaMemset2DAsync(base + nvec, size_t(H.ld) * sizeof(double), 0, size_t(H.ld - nvec) * sizeof(double),
-                                   PANEL, s));
+      // padding rows are read (as zeros) by the Gram-Schmidt tiles
+      MPG_CUDA(cudaMemsetAsync(base, 0, size_t(PANEL) * size_t(H.ld) * sizeof(double), s));
       const int p0 = int(H.panels.size() - 1) * PANEL;
       for (int j = 0; j < PANEL && p0 + j < maxit + 2; ++j) H.vtab[size_t(p0 + j)] = base + size_t(j) * size_t(H.ld);
     }
@@ -919,10 +812,13 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
 
   for (int i = 0; i < ns; ++i) {
     ensure(i, std::min(maxit + 2, 2));
-    copy_in(sh[size_t(i)].vtab[0], specs[size_t(i)].b, size_t(hs[size_t(i)].n), s);
+    copy_in(sh[size_t(i)].rbuf.get(), specs[size_t(i)].b, size_t(hs[size_t(i)].n), s);
   }
   DBuf<GmSolve> dS(dev, size_t(ns));
   MPG_CUDA(cudaMemcpyAsync(dS.get(), hs.data(), sizeof(GmSolve) * size_t(ns), cudaMemcpyHostToDevice, s));
+  k_pack_rhs<<<dim3(unsigned(std::min<int64_t>(cdiv(nmax, 256), 4096)), unsigned(ns)), 256, 0, s>>>(dS.get());
+  MPG_CHECK_LAUNCH();
+  count_launch();
   k_bnorm_part<<<dim3(unsigned(G), unsigned(ns)), 256, 0, s>>>(dS.get(), G);
   MPG_CHECK_LAUNCH();
   k_init<<<unsigned(ns), 32, 0, s>>>(dS.get(), G);
@@ -944,13 +840,10 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     cudaFuncSetAttribute(k_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_gs_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, UP_SMEM_DOUBLES * 8);
-    cudaFuncSetAttribute(k_gs_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, UP_SMEM_DOUBLES * 8);
     cudaFuncSetAttribute(k_gs_reg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GR_SMEM_DOUBLES * 8);
     cudaFuncSetAttribute(k_gs_reg<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GR_SMEM_DOUBLES * 8);
   });
   const bool fused = maxit + 1 <= UP_MAXCOLS && !std::getenv("MPG_NO_FUSE");
-  const size_t smem_up = size_t(UP_SMEM_DOUBLES) * sizeof(double);
   int launches_per_iter = 0;
   // Profiling hook: called after every launch with a kernel-class id.
   std::function<void(int)> mark = [](int) {};
@@ -987,10 +880,8 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   };
   const dim3 gG{unsigned(G), unsigned(ns), 1u};
   // One long-running CTA per SM for the staged Gram-Schmidt passes.
-  const int Ggs = std::max(1, std::min(G, (2 * c.sm_count * 4 + ns - 1) / ns));
-  const dim3 gGs{unsigned(Ggs), unsigned(ns), 1u};
-  const bool regtile = !std::getenv("MPG_GS_SMEM");
-  const int Ggr = std::max(1, std::min(G, (c.sm_count + ns - 1) / ns));
+  // exactly one wave of one-CTA-per-SM blocks: floor, never more blocks than SMs
+  const int Ggr = std::max(1, std::min(G, c.sm_count / ns));
   const dim3 gGr{unsigned(Ggr), unsigned(ns), 1u};
   const size_t smem_gr = size_t(GR_SMEM_DOUBLES) * sizeof(double);
   const dim3 gR{cdiv(maxit + 2, 8), unsigned(ns), 1u};
@@ -998,15 +889,13 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     launches_per_iter = 0;
     for (int st = 0; st < max_stages; ++st) chain_stage(st, 0);
     iter_op(0);
-    if (fused && regtile) k_gs_reg<false><<<gGr, GR_THREADS, smem_gr, s>>>(dS.get(), G, Ggr);
-    else if (fused) k_gs_tile<false><<<gGs, GS_THREADS, smem_up, s>>>(dS.get(), G, Ggs);
+    if (fused) k_gs_reg<false><<<gGr, GR_THREADS, smem_gr, s>>>(dS.get(), G, Ggr);
     else k_dot<<<gG, 256, smem_dot, s>>>(dS.get(), G);
     mark(PK_DOT);
-    k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 0, fused ? (regtile ? Ggr : Ggs) : G);
+    k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 0, fused ? Ggr : G);
     mark(PK_SMALL);
     if (fused) {
-      if (regtile) k_gs_reg<true><<<gGr, GR_THREADS, smem_gr, s>>>(dS.get(), G, Ggr);
-      else k_gs_tile<true><<<gGs, GS_THREADS, smem_up, s>>>(dS.get(), G, Ggs);
+      k_gs_reg<true><<<gGr, GR_THREADS, smem_gr, s>>>(dS.get(), G, Ggr);
       mark(PK_UPDPROBE);
       --launches_per_iter;
     } else {
@@ -1015,11 +904,11 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       k_dot<<<gG, 256, smem_dot, s>>>(dS.get(), G);
       mark(PK_PROBE);
     }
-    k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 1, fused ? (regtile ? Ggr : Ggs) : G);
+    k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 1, fused ? Ggr : G);
     mark(PK_SMALL);
     k_update<<<gG, 256, smem_upd, s>>>(dS.get(), G, 1);
     mark(PK_REORTH);
-    k_finalize<<<unsigned(ns), 32, 0, s>>>(dS.get(), G);
+    k_finalize<<<unsigned(ns), 32, 0, s>>>(dS.get(), G, G);
     mark(PK_SMALL);
     k_backsub<<<unsigned(ns), 256, size_t(maxit + 2) * sizeof(double), s>>>(dS.get());
     mark(PK_ASM);
