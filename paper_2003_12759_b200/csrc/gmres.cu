@@ -360,7 +360,7 @@ constexpr int GR_SMEM_DOUBLES = 2 * UP_MAXCOLS + 2 * 1024 + 64;  // coef, vp, re
 
 template <int RG, bool UPDATE>
 __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double* coef, const double** vp,
-                                            double* red, double* wn) {
+                                            double* red, double* wn, bool l2_prefetch) {
   constexpr int CG = GR_THREADS / RG;
   constexpr int T = 2 * RG;
   constexpr int TPR = GR_THREADS / T;  // threads per row in the row-sum reduction
@@ -383,6 +383,7 @@ __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double
 #pragma unroll
   for (int c = 0; c < GR_CPT; ++c) dcol[c] = 0.0;
   double wsq = 0.0;
+  const int step = nblk * T;
   // The w rows of a tile are fetched together with its basis block so their
   // latency is hidden behind the previous tile as well.
   auto load = [&](int r0, double2* v, double& wp) {
@@ -393,6 +394,14 @@ __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double
       v[c] = (pcol[c] && inb) ? __ldcs(reinterpret_cast<const double2*>(pcol[c] + vidx(row))) : make_double2(0.0, 0.0);
     const int rw = r0 + my_row;
     wp = (sub == 0 && rw < n) ? w[vidx(rw)] : 0.0;
+    // Pull the tile after this one into L2 so its register loads see L2
+    // latency: one prefetch per 128-byte line (T rows x 8 B per column).
+    const int rp = r0 + step + 2 * rg;
+    if (l2_prefetch && ((2 * rg) & 15) == 0 && rp < n) {
+#pragma unroll
+      for (int c = 0; c < GR_CPT; ++c)
+        if (pcol[c]) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pcol[c] + vidx(rp)));
+    }
   };
   auto consume = [&](int r0, const double2* v, double wpre) {
     const int rw = r0 + my_row;
@@ -426,7 +435,6 @@ __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double
     for (int c = 0; c < GR_CPT; ++c) dcol[c] = fma(v[c].x, w0, fma(v[c].y, w1, dcol[c]));
     __syncthreads();  // wn / red are rewritten by the next tile
   };
-  const int step = nblk * T;
   double2 va[GR_CPT], vb[GR_CPT];
   double wa, wb;
   int r0 = blockIdx.x * T;
@@ -463,7 +471,7 @@ __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double
 }
 
 template <bool UPDATE>
-__global__ void __launch_bounds__(GR_THREADS, 1) k_gs_reg(GmSolve* S, int G, int nblk) {
+__global__ void __launch_bounds__(GR_THREADS, 1) k_gs_reg(GmSolve* S, int G, int nblk, int pf) {
   GmSolve& st = S[blockIdx.y];
   if (st.phase != PH_RUN) return;
   extern __shared__ __align__(16) double sm[];
@@ -477,10 +485,10 @@ __global__ void __launch_bounds__(GR_THREADS, 1) k_gs_reg(GmSolve* S, int G, int
     vp[j] = st.V[j];
   }
   __syncthreads();
-  if (nj <= 128) gs_reg_body<32, UPDATE>(st, G, nblk, coef, vp, red, wn);
-  else if (nj <= 256) gs_reg_body<16, UPDATE>(st, G, nblk, coef, vp, red, wn);
-  else if (nj <= 512) gs_reg_body<8, UPDATE>(st, G, nblk, coef, vp, red, wn);
-  else gs_reg_body<4, UPDATE>(st, G, nblk, coef, vp, red, wn);
+  if (nj <= 128) gs_reg_body<32, UPDATE>(st, G, nblk, coef, vp, red, wn, pf);
+  else if (nj <= 256) gs_reg_body<16, UPDATE>(st, G, nblk, coef, vp, red, wn, pf);
+  else if (nj <= 512) gs_reg_body<8, UPDATE>(st, G, nblk, coef, vp, red, wn, pf);
+  else gs_reg_body<4, UPDATE>(st, G, nblk, coef, vp, red, wn, pf);
 }
 
 // ---- norm partials of the residual buffer ----------------------------------------
@@ -844,6 +852,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     cudaFuncSetAttribute(k_gs_reg<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GR_SMEM_DOUBLES * 8);
   });
   const bool fused = maxit + 1 <= UP_MAXCOLS && !std::getenv("MPG_NO_FUSE");
+  const int l2pf = std::getenv("MPG_L2PF") ? 1 : 0;  // measured slower on C3: opt-in only
   int launches_per_iter = 0;
   // Profiling hook: called after every launch with a kernel-class id.
   std::function<void(int)> mark = [](int) {};
@@ -889,13 +898,13 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     launches_per_iter = 0;
     for (int st = 0; st < max_stages; ++st) chain_stage(st, 0);
     iter_op(0);
-    if (fused) k_gs_reg<false><<<gGr, GR_THREADS, smem_gr, s>>>(dS.get(), G, Ggr);
+    if (fused) k_gs_reg<false><<<gGr, GR_THREADS, smem_gr, s>>>(dS.get(), G, Ggr, l2pf);
     else k_dot<<<gG, 256, smem_dot, s>>>(dS.get(), G);
     mark(PK_DOT);
     k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 0, fused ? Ggr : G);
     mark(PK_SMALL);
     if (fused) {
-      k_gs_reg<true><<<gGr, GR_THREADS, smem_gr, s>>>(dS.get(), G, Ggr);
+      k_gs_reg<true><<<gGr, GR_THREADS, smem_gr, s>>>(dS.get(), G, Ggr, l2pf);
       mark(PK_UPDPROBE);
       --launches_per_iter;
     } else {
