@@ -45,6 +45,7 @@ struct GmSolve {
   double sre, sim, ca, target, bnorm;
   // state
   int k, phase, asm_kind, asm_k, guess, iterations, converged, breakdown, xsel, reorth_count;
+  int grouped_op, grouped_chain;  // handled by the shared-matrix (multi-RHS) kernels
   double estimate, recheck_at, w2_pre, w2_a, w2_b, wn_cur, final_residual;
   // arrays
   double** V;
@@ -85,7 +86,7 @@ template <int V>
 __global__ void __launch_bounds__(256) k_chain_stage(GmSolve* S, int stage, int mode) {
   GmSolve& st = S[blockIdx.y];
   if (mode == 0 ? st.phase != PH_RUN : st.phase != PH_ASM) return;
-  if (stage >= st.stages) return;
+  if (stage >= st.stages || st.grouped_chain) return;
   const CsrView f = st.fac[stage];
   const int halves = st.pair_bd ? 2 : 1;
   const int lane = threadIdx.x & (V - 1);
@@ -117,6 +118,7 @@ template <int V, int EM>
 __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView opt, int mode) {
   GmSolve& st = S[blockIdx.y];
   if (mode == 0 ? st.phase != PH_RUN : st.phase != PH_ASM) return;
+  if (st.grouped_op) return;
   const OpView& op = st.transpose ? opt : opn;
   const int n = op.a.nrows;
   const int lane = threadIdx.x & (V - 1);
@@ -186,6 +188,127 @@ __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView 
       const double* b0 = st.V[0];
       st.rbuf[row] = b0[vidx(row)] - y1;
       if (pair) st.rbuf[n + row] = b0[vidx(n + row)] - y2;
+    }
+  }
+}
+
+// ---- shared-matrix (multi-RHS) variants ----------------------------------------
+// Solves of a batch that apply the same matrix — the same chain factor (a
+// frozen or shared preconditioner) or the same side of the operator (all
+// primal or all dual real shifts) — are advanced by one launch that reads
+// each matrix entry once and applies it to up to MB right-hand sides: the
+// matrix bytes are paid once per group instead of once per solve.
+constexpr int MB = 8;
+
+struct Group { int idx[MB]; int cnt; };
+
+template <int V>
+__global__ void __launch_bounds__(256) k_chain_multi(GmSolve* S, Group grp, CsrView f, int stage, int mode) {
+  const double* src[MB];
+  double* dst[MB];
+  bool act[MB];
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < MB; ++q) {
+    act[q] = false;
+    src[q] = nullptr;
+    dst[q] = nullptr;
+    if (q < grp.cnt) {
+      const GmSolve& st = S[grp.idx[q]];
+      act[q] = (mode == 0 ? st.phase == PH_RUN : st.phase == PH_ASM) && stage < st.stages;
+      src[q] = stage == 0 ? (mode == 0 ? st.V[st.k] : st.ubuf) : ((stage - 1) & 1 ? st.z1 : st.z0);
+      dst[q] = (stage & 1) ? st.z1 : st.z0;
+      any |= act[q];
+    }
+  }
+  if (!any) return;
+  const int lane = threadIdx.x & (V - 1);
+  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / V);
+  double acc[MB];
+#pragma unroll
+  for (int q = 0; q < MB; ++q) acc[q] = 0.0;
+  if (row < f.nrows) {
+    const int b = f.rowptr[row], e = f.rowptr[row + 1];
+#pragma unroll 2
+    for (int k = b + lane; k < e; k += V) {
+      const double a = __ldcs(f.val + k);
+      const int c = __ldcs(f.colind + k);
+#pragma unroll
+      for (int q = 0; q < MB; ++q)
+        if (act[q]) acc[q] = fma(a, __ldg(src[q] + c), acc[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < MB; ++q) acc[q] = sub_sum<V>(acc[q]);
+  if (row < f.nrows && lane == 0) {
+#pragma unroll
+    for (int q = 0; q < MB; ++q)
+      if (act[q]) dst[q][row] = acc[q];
+  }
+}
+
+template <int V, int EM>
+__global__ void __launch_bounds__(256) k_iter_op_multi(GmSolve* S, Group grp, OpView op, int mode) {
+  const double* xs[MB];
+  bool act[MB];
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < MB; ++q) {
+    act[q] = false;
+    xs[q] = nullptr;
+    if (q < grp.cnt) {
+      const GmSolve& st = S[grp.idx[q]];
+      act[q] = mode == 0 ? st.phase == PH_RUN : st.phase == PH_ASM;
+      if (mode == 0) xs[q] = st.stages ? ((st.stages - 1) & 1 ? st.z1 : st.z0) : st.V[st.k];
+      else xs[q] = st.stages ? ((st.stages - 1) & 1 ? st.z1 : st.z0) : st.ubuf;
+      any |= act[q];
+    }
+  }
+  if (!any) return;
+  const int n = op.a.nrows;
+  const int lane = threadIdx.x & (V - 1);
+  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / V);
+  double a1[MB], e1[MB];
+#pragma unroll
+  for (int q = 0; q < MB; ++q) a1[q] = e1[q] = 0.0;
+  if (row < n) {
+    const int b = op.a.rowptr[row], e = op.a.rowptr[row + 1];
+#pragma unroll 2
+    for (int k = b + lane; k < e; k += V) {
+      const int c = __ldcs(op.a.colind + k);
+      if (EM == E_SAMEPAT) {
+        const double2 ae = __ldcs(op.ae + k);
+#pragma unroll
+        for (int q = 0; q < MB; ++q)
+          if (act[q]) {
+            const double xv = __ldg(xs[q] + c);
+            a1[q] = fma(ae.x, xv, a1[q]);
+            e1[q] = fma(ae.y, xv, e1[q]);
+          }
+      } else {
+        const double av = __ldcs(op.a.val + k);
+#pragma unroll
+        for (int q = 0; q < MB; ++q)
+          if (act[q]) a1[q] = fma(av, __ldg(xs[q] + c), a1[q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < MB; ++q) {
+    a1[q] = sub_sum<V>(a1[q]);
+    if (EM == E_SAMEPAT) e1[q] = sub_sum<V>(e1[q]);
+  }
+  if (row < n && lane == 0) {
+#pragma unroll
+    for (int q = 0; q < MB; ++q) {
+      if (!act[q]) continue;
+      GmSolve& st = S[grp.idx[q]];
+      double ex = e1[q];
+      if (EM == E_IDENT) ex = xs[q][row];
+      else if (EM == E_DIAG) ex = op.ediag[row] * xs[q][row];
+      const double y1 = st.sre * ex + st.ca * a1[q];
+      if (mode == 0) st.V[st.k + 1][row] = st.scale[st.k] * y1;
+      else st.rbuf[row] = st.V[0][row] - y1;
     }
   }
 }
@@ -856,7 +979,61 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   int launches_per_iter = 0;
   // Profiling hook: called after every launch with a kernel-class id.
   std::function<void(int)> mark = [](int) {};
+  // Shared-matrix groups (MPG_NO_MULTI disables): solves with the same chain
+  // (non-pair) and real shifts on the same operator side.
+  std::vector<Group> chain_groups, op_groups;
+  std::vector<const Chain*> chain_of_group;
+  if (!std::getenv("MPG_NO_MULTI")) {
+    std::vector<int> used(size_t(ns), 0);
+    for (int i = 0; i < ns; ++i) {
+      if (used[size_t(i)] || !specs[size_t(i)].chain || hs[size_t(i)].pair_bd) continue;
+      std::vector<int> mem{i};
+      for (int j = i + 1; j < ns; ++j)
+        if (!used[size_t(j)] && specs[size_t(j)].chain && !hs[size_t(j)].pair_bd &&
+            specs[size_t(j)].chain->factors == specs[size_t(i)].chain->factors)
+          mem.push_back(j);
+      if (mem.size() < 2) continue;
+      for (size_t b = 0; b < mem.size(); b += MB) {
+        Group g{};
+        g.cnt = int(std::min<size_t>(MB, mem.size() - b));
+        for (int q = 0; q < g.cnt; ++q) g.idx[q] = mem[b + size_t(q)];
+        chain_groups.push_back(g);
+        chain_of_group.push_back(specs[size_t(i)].chain.get());
+      }
+      for (int m : mem) { used[size_t(m)] = 1; hs[size_t(m)].grouped_chain = 1; }
+    }
+    for (int side = 0; side < 2; ++side) {
+      std::vector<int> mem;
+      for (int i = 0; i < ns; ++i)
+        if (!hs[size_t(i)].pair && hs[size_t(i)].transpose == side) mem.push_back(i);
+      if (mem.size() < 2) continue;
+      for (size_t b = 0; b < mem.size(); b += MB) {
+        Group g{};
+        g.cnt = int(std::min<size_t>(MB, mem.size() - b));
+        for (int q = 0; q < g.cnt; ++q) g.idx[q] = mem[b + size_t(q)];
+        op_groups.push_back(g);
+      }
+      for (int m : mem) hs[size_t(m)].grouped_op = 1;
+    }
+    MPG_CUDA(cudaMemcpyAsync(dS.get(), hs.data(), sizeof(GmSolve) * size_t(ns), cudaMemcpyHostToDevice, s));
+  }
   auto chain_stage = [&](int stage, int mode) {
+    for (size_t gi = 0; gi < chain_groups.size(); ++gi) {
+      const Chain& ch = *chain_of_group[gi];
+      if (stage >= int(ch.factors.size())) continue;
+      const DevCsr& f = *ch.factors[size_t(stage)];
+      const int Vf = choose_vec_width(f.mean_row);
+      const unsigned grid = cdiv(f.nrows * int64_t(Vf), 256);
+      switch (Vf) {
+        case 2: k_chain_multi<2><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
+        case 4: k_chain_multi<4><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
+        case 8: k_chain_multi<8><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
+        case 16: k_chain_multi<16><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
+        default: k_chain_multi<32><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
+      }
+      ++launches_per_iter;
+      mark(mode == 0 ? PK_CHAIN : PK_ASM);
+    }
     const dim3 grid(cdiv(max_fac_rows * int64_t(Vfac), 256), unsigned(ns));
     switch (Vfac) {
       case 2: k_chain_stage<2><<<grid, 256, 0, s>>>(dS.get(), stage, mode); break;
@@ -886,6 +1063,26 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
 #undef MPG_OPL
     ++launches_per_iter;
     mark(mode == 0 ? PK_OP : PK_ASM);
+    for (const Group& g : op_groups) {
+      const OpView& ov = hs[size_t(g.idx[0])].transpose ? opt_ : opn;
+      const unsigned grid1 = cdiv(nb * int64_t(Vop), 256);
+#define MPG_OPM(VV)                                                                                            \
+  switch (op.emode) {                                                                                          \
+    case E_IDENT: k_iter_op_multi<VV, E_IDENT><<<grid1, 256, 0, s>>>(dS.get(), g, ov, mode); break;           \
+    case E_DIAG: k_iter_op_multi<VV, E_DIAG><<<grid1, 256, 0, s>>>(dS.get(), g, ov, mode); break;             \
+    default: k_iter_op_multi<VV, E_SAMEPAT><<<grid1, 256, 0, s>>>(dS.get(), g, ov, mode); break;              \
+  }
+      switch (Vop) {
+        case 2: MPG_OPM(2); break;
+        case 4: MPG_OPM(4); break;
+        case 8: MPG_OPM(8); break;
+        case 16: MPG_OPM(16); break;
+        default: MPG_OPM(32); break;
+      }
+#undef MPG_OPM
+      ++launches_per_iter;
+      mark(mode == 0 ? PK_OP : PK_ASM);
+    }
   };
   const dim3 gG{unsigned(G), unsigned(ns), 1u};
   // One long-running CTA per SM for the staged Gram-Schmidt passes.
