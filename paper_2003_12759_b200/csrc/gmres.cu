@@ -464,6 +464,11 @@ __global__ void __launch_bounds__(256) k_update(GmSolve* S, int G, int mode) {
 constexpr int UP_MAXCOLS = 1024;
 
 // ---- register-tiled Gram-Schmidt passes (the default path) -----------------------
+// Measured alternatives on C3 (n = 1.19 M, k ~ 300): staging the
+// tile in shared memory with cp.async (2 CTAs/SM: 3.6 TB/s; a producer/consumer
+// mbarrier ring with 2 producer warps: 2.1 TB/s), 1-D TMA bulk copies per
+// vector (1.4 TB/s, op-rate bound), L2 prefetch of the next tile (slower); the
+// register double buffer below is the fastest (4.6 / 3.8 TB/s).
 // UPDATE: w <- w - sum_j s_j h_j W_j, then part[j][blk] = W_j . w_new (the
 // measured second-pass probe, gmres.cpp:101-111) and part[k+1][blk] =
 // ||w_new||^2. !UPDATE: the first (projection) pass, part[j][blk] = W_j . w
@@ -494,14 +499,9 @@ __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double
   const int k = st.k, nj = k + 1, n = st.n;
   const int ld = (n + 31) & ~31;
   double* w = st.V[k + 1];
-  const double* pcol[GR_CPT];
-  double cf[GR_CPT];
-#pragma unroll
-  for (int c = 0; c < GR_CPT; ++c) {
-    const int j = cg + CG * c;
-    pcol[c] = j < nj ? vp[j] : nullptr;
-    cf[c] = (UPDATE && j < nj) ? coef[j] : 0.0;
-  }
+  // Column pointers and coefficients stay in shared memory (register budget:
+  // the double-buffered tile and the column accumulators use the rest).
+  const int ncol_me = nj > cg ? min(GR_CPT, (nj - cg + CG - 1) / CG) : 0;
   double dcol[GR_CPT];
 #pragma unroll
   for (int c = 0; c < GR_CPT; ++c) dcol[c] = 0.0;
@@ -514,7 +514,8 @@ __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double
     const bool inb = r0 < n && row + 1 < ld;
 #pragma unroll
     for (int c = 0; c < GR_CPT; ++c)
-      v[c] = (pcol[c] && inb) ? __ldcs(reinterpret_cast<const double2*>(pcol[c] + vidx(row))) : make_double2(0.0, 0.0);
+      v[c] = (c < ncol_me && inb) ? __ldcs(reinterpret_cast<const double2*>(vp[cg + CG * c] + vidx(row)))
+                                  : make_double2(0.0, 0.0);
     const int rw = r0 + my_row;
     wp = (sub == 0 && rw < n) ? w[vidx(rw)] : 0.0;
     // Pull the tile after this one into L2 so its register loads see L2
@@ -523,7 +524,7 @@ __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double
     if (l2_prefetch && ((2 * rg) & 15) == 0 && rp < n) {
 #pragma unroll
       for (int c = 0; c < GR_CPT; ++c)
-        if (pcol[c]) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pcol[c] + vidx(rp)));
+        if (c < ncol_me) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(vp[cg + CG * c] + vidx(rp)));
     }
   };
   auto consume = [&](int r0, const double2* v, double wpre) {
@@ -533,8 +534,9 @@ __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double
       double ax = 0.0, ay = 0.0;
 #pragma unroll
       for (int c = 0; c < GR_CPT; ++c) {
-        ax = fma(cf[c], v[c].x, ax);
-        ay = fma(cf[c], v[c].y, ay);
+        const double cfc = c < ncol_me ? coef[cg + CG * c] : 0.0;
+        ax = fma(cfc, v[c].x, ax);
+        ay = fma(cfc, v[c].y, ay);
       }
       red[(2 * rg) * CGP + cg] = ax;
       red[(2 * rg + 1) * CGP + cg] = ay;
