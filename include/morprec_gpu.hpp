@@ -271,6 +271,7 @@ struct BirkaConfig {  // birka.hpp:49-61 (N = 0)
   SpaiConfig spai{};
   int max_chain_len = 16;
   index_t standard_residual_max_dim = 5000;
+  bool mirror_unstable = false;  // extension
 };
 
 struct BirkaState {  // birka.hpp:35-47 with the descriptor E_r, A_r
@@ -302,6 +303,7 @@ inline std::pair<BirkaState, ReductionReport> birka_reduce(const ShiftedOperator
   k.max_chain_len = cfg.max_chain_len;
   k.explicit_nnz_cap = 0;
   k.standard_residual_max_dim = cfg.standard_residual_max_dim;
+  k.mirror_unstable = cfg.mirror_unstable;
   BirkaState st;
   const size_t r = static_cast<size_t>(cfg.r);
   st.order = cfg.r;

@@ -88,6 +88,7 @@ typedef struct {
   mpg_spai_cfg spai;
   int max_chain_len;
   long long explicit_nnz_cap, standard_residual_max_dim;
+  int mirror_unstable; /* extension: reflect Re(lambda) > 0 into the left half plane before solving */
 } mpg_irka_cfg;
 
 /* ReportRow (proj/include/morprec/report.hpp:28-40). */

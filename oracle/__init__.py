@@ -55,7 +55,8 @@ class GmresRep(C.Structure):
 class IrkaCfg(C.Structure):
     _fields_ = [("r", C.c_int), ("tol", C.c_double), ("max_sweeps", C.c_int), ("decoupled", C.c_int),
                 ("seed", C.c_ulonglong), ("gmres", GmresCfg), ("spai", SpaiCfg), ("max_chain_len", C.c_int),
-                ("explicit_nnz_cap", C.c_longlong), ("standard_residual_max_dim", C.c_longlong)]
+                ("explicit_nnz_cap", C.c_longlong), ("standard_residual_max_dim", C.c_longlong),
+                ("mirror_unstable", C.c_int)]
 
 
 class ReportRow(C.Structure):
@@ -459,10 +460,12 @@ class IrkaConfig:
     explicit_nnz_cap: int = 200000
     standard_residual_max_dim: int = 5000
     decoupled: bool = False
+    mirror_unstable: bool = False
 
     def c(self):
         return IrkaCfg(self.r, self.tol, self.max_sweeps, int(self.decoupled), self.seed, self.gmres.c(),
-                       self.spai.c(), self.max_chain_len, self.explicit_nnz_cap, self.standard_residual_max_dim)
+                       self.spai.c(), self.max_chain_len, self.explicit_nnz_cap, self.standard_residual_max_dim,
+                       int(self.mirror_unstable))
 
 
 @dataclasses.dataclass

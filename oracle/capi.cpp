@@ -46,6 +46,7 @@ typedef struct {
 typedef struct {
   int r; double tol; int max_sweeps; int decoupled; unsigned long long seed;
   orc_gmres_cfg gmres; orc_spai_cfg spai; int max_chain_len; long long explicit_nnz_cap, standard_residual_max_dim;
+  int mirror_unstable;
 } orc_irka_cfg;
 typedef struct {
   int sweep, point, kind, solves; long long iterations;
@@ -303,6 +304,7 @@ int orc_irka_reduce(const Csr* a, const Csr* e, const double* b, int m, const do
     ic.gmres = to_gmres(&cfg->gmres); ic.spai = to_spai(&cfg->spai); ic.max_chain_len = cfg->max_chain_len;
     ic.explicit_nnz_cap = cfg->explicit_nnz_cap; ic.standard_residual_max_dim = cfg->standard_residual_max_dim;
     ic.decoupled = cfg->decoupled != 0;
+    ic.mirror_unstable = cfg->mirror_unstable != 0;
     IrkaState init;
     const IrkaState* initp = nullptr;
     if (init_kr) {

@@ -118,6 +118,12 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
       state.kr = nudged;
       lambda_prev = sorted_eigenvalues(state.kr);
     }
+    if (cfg.mirror_unstable) {
+      // Standard IRKA safeguard (not in the reference): shifts sigma = -lambda of
+      // unstable reduced poles are reflected, Re(lambda) -> -|Re(lambda)|.
+      for (index_t i = 0; i < r; ++i)
+        if (spec.blocks(i, i) > 0.0) spec.blocks(i, i) = -spec.blocks(i, i);
+    }
     const Dense rinv_t = spec.basis_inv.transpose();
     const Dense f2 = matmul(state.fr.transpose(), rinv_t);  // m x r, :182
     const Dense c2 = matmul(state.cr.transpose(), spec.basis);  // q x r, :183

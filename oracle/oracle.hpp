@@ -239,6 +239,7 @@ struct IrkaConfig {
   index_t explicit_nnz_cap = 200000;
   index_t standard_residual_max_dim = 5000;
   bool decoupled = false;  // one GMRES per shift unit instead of one joint n*r solve
+  bool mirror_unstable = false;  // extension: reflect Re(lambda) > 0 before solving
 };
 struct IrkaState {
   Dense kr, fr, cr;        // reduced K = E_r^{-1} A_r, E_r^{-1} W^T B, V^T C

@@ -71,7 +71,8 @@ class GmresRep(C.Structure):
 class IrkaCfg(C.Structure):
     _fields_ = [("r", C.c_int), ("tol", C.c_double), ("max_sweeps", C.c_int), ("decoupled", C.c_int),
                 ("seed", C.c_ulonglong), ("gmres", GmresCfg), ("spai", SpaiCfg), ("max_chain_len", C.c_int),
-                ("explicit_nnz_cap", C.c_longlong), ("standard_residual_max_dim", C.c_longlong)]
+                ("explicit_nnz_cap", C.c_longlong), ("standard_residual_max_dim", C.c_longlong),
+                ("mirror_unstable", C.c_int)]
 
 
 class ReportRow(C.Structure):

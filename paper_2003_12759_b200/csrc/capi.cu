@@ -387,6 +387,7 @@ static IrkaSettings to_irka(const mpg_irka_cfg* c, int mode, const double* init_
   s.max_chain_len = c->max_chain_len;
   s.standard_residual_max_dim = c->standard_residual_max_dim;
   s.mode = mode;
+  s.mirror_unstable = c->mirror_unstable != 0;
   if (init_shifts) s.init_shifts.assign(init_shifts, init_shifts + c->r);
   return s;
 }

@@ -491,7 +491,9 @@ __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double
                                             double* red, double* wn, bool l2_prefetch) {
   constexpr int CG = GR_THREADS / RG;
   constexpr int T = 2 * RG;
-  constexpr int TPR = GR_THREADS / T;  // threads per row in the row-sum reduction
+  // Row sums: TPR (<= 32, one warp) threads per row, PPT partials each.
+  constexpr int TPR = (GR_THREADS / T) < 32 ? (GR_THREADS / T) : 32;
+  constexpr int PPT = CG / TPR;
   constexpr int CGP = CG + 1;          // padded partial-sum row
   const int tid = threadIdx.x;
   const int rg = tid % RG, cg = tid / RG;
@@ -517,7 +519,7 @@ __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double
       v[c] = (c < ncol_me && inb) ? __ldcs(reinterpret_cast<const double2*>(vp[cg + CG * c] + vidx(row)))
                                   : make_double2(0.0, 0.0);
     const int rw = r0 + my_row;
-    wp = (sub == 0 && rw < n) ? w[vidx(rw)] : 0.0;
+    wp = (sub == 0 && my_row < T && rw < n) ? w[vidx(rw)] : 0.0;
     // Pull the tile after this one into L2 so its register loads see L2
     // latency: one prefetch per 128-byte line (T rows x 8 B per column).
     const int rp = r0 + step + 2 * rg;
@@ -541,16 +543,20 @@ __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double
       red[(2 * rg) * CGP + cg] = ax;
       red[(2 * rg + 1) * CGP + cg] = ay;
       __syncthreads();
-      double sacc = red[my_row * CGP + 2 * sub] + red[my_row * CGP + 2 * sub + 1];
+      double sacc = 0.0;
+      if (my_row < T) {
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) sacc += red[my_row * CGP + PPT * sub + q];
+      }
 #pragma unroll
       for (int o = TPR / 2; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o, TPR);
-      if (sub == 0) {
+      if (sub == 0 && my_row < T) {
         const double wv = valid ? wpre - sacc : 0.0;
         if (valid) w[vidx(rw)] = wv;
         wn[my_row] = wv;
         wsq = fma(wv, wv, wsq);
       }
-    } else if (sub == 0) {
+    } else if (sub == 0 && my_row < T) {
       wn[my_row] = wpre;
       wsq = fma(wpre, wpre, wsq);
     }

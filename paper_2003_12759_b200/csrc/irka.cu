@@ -284,6 +284,13 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
       kr = nudged;
       lambda_prev = host::sorted_eigenvalues(kr);
     }
+    if (cfg.mirror_unstable) {
+      // Standard IRKA safeguard (not in the reference): reflect unstable
+      // reduced poles, Re(lambda) -> -|Re(lambda)|, so every shift sigma = -lambda
+      // has a positive real part.
+      for (int i = 0; i < r; ++i)
+        if (spec.blocks(i, i) > 0.0) spec.blocks(i, i) = -spec.blocks(i, i);
+    }
     const Mat f2t = host::mul(host::transpose(spec.basis_inv), fr);  // (f2)^T = R^{-1} fr   (r x m)
     const Mat c2t = host::mul(host::transpose(spec.basis), cr);      // (c2)^T = R^T cr      (r x q)
     // right-hand sides: side 0 columns B f2 -> RHS[:, 0..r), side 1 C c2 -> RHS[:, r..2r)

@@ -21,6 +21,7 @@ struct IrkaSettings {
   int mode = MPG_PRECOND_REUSE_CHAIN;
   std::vector<double> init_shifts;  // empty: default seed (power iteration)
   bool want_vw = false;
+  bool mirror_unstable = false;
 };
 
 struct IrkaResult {

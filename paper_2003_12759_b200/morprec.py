@@ -506,10 +506,12 @@ class IrkaConfig:
     max_chain_len: int = 16
     explicit_nnz_cap: int = 200000
     standard_residual_max_dim: int = 5000
+    mirror_unstable: bool = False  # extension: reflect unstable reduced poles before solving
 
     def c(self) -> L.IrkaCfg:
         return L.IrkaCfg(self.r, self.tol, self.max_sweeps, 1, self.seed, self.gmres.c(), self.spai.c(),
-                         self.max_chain_len, self.explicit_nnz_cap, self.standard_residual_max_dim)
+                         self.max_chain_len, self.explicit_nnz_cap, self.standard_residual_max_dim,
+                         int(self.mirror_unstable))
 
 
 @dataclasses.dataclass
