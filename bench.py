@@ -245,6 +245,29 @@ def run_ours(args, rank: int, world: int, device: int):
     return result
 
 
+def run_irka(args, device: int) -> dict:
+    """Full IRKA at the bench workload: wall time from the first sweep to
+    convergence, including the preconditioner build, every solve, the
+    projection and the host eigen-solves (BASELINE.json metric's second part)."""
+    import paper_2003_12759_b200 as mpg
+    from paper_2003_12759_b200 import gen
+    s = gen.config3(args.nodes)
+    op = mpg.ShiftedOperator(mpg.SparseMatrix.from_csr(s.a.nrows, s.a.ncols, s.a.rowptr, s.a.colind, s.a.val, device),
+                             mpg.SparseMatrix.from_csr(s.e.nrows, s.e.ncols, s.e.rowptr, s.e.colind, s.e.val, device))
+    cfg = mpg.IrkaConfig(r=args.r, tol=1e-6, max_sweeps=50, seed=1, gmres=mpg.GmresConfig(args.tol, args.max_iter),
+                         mirror_unstable=True)
+    mpg.lib.mpg_synchronize(device)
+    t0 = time.perf_counter()
+    st, rep = mpg.irka_reduce(op, s.b, s.c, cfg, mpg.PrecondMode.REUSE_FROZEN, init_shifts=s.shifts[: args.r])
+    mpg.lib.mpg_synchronize(device)
+    wall = time.perf_counter() - t0
+    tot = rep.totals()
+    return {"wall_s": round(wall, 3), "sweeps": rep.sweeps, "converged": rep.converged, "solves": tot["solves"],
+            "gmres_iterations": tot["gmres_iterations"], "precond_build_s": round(tot["precond_build_seconds"], 3),
+            "shifts": [[float(-z.real), float(-z.imag)] for z in sorted(st.lam, key=lambda z: (z.real, z.imag))],
+            "tol": 1e-6, "mode": "frozen SPAI, unstable shifts mirrored"}
+
+
 def _batch_host(mpg, L, op, sig, rhs_host, x_host, chains, trs, cfg):
     """gmres_batch through the C ABI with host buffers: the library copies H2D/D2H."""
     k = len(sig)
@@ -315,6 +338,7 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=40)
     ap.add_argument("--ref-iters", type=int, default=334)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-irka", action="store_true", help="skip the full-IRKA wall-time measurement")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -329,6 +353,8 @@ def main():
         run_reference(args, rank, world)
         return
     res = run_ours(args, rank, world, local)
+    if world == 1 and not args.no_irka:
+        res["irka"] = run_irka(args, local)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_sample(args)

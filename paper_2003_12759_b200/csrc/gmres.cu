@@ -463,79 +463,106 @@ __global__ void __launch_bounds__(256) k_update(GmSolve* S, int G, int mode) {
 
 constexpr int UP_MAXCOLS = 1024;
 
-// ---- register-tiled Gram-Schmidt passes (the default path) -----------------------
-// Measured alternatives on C3 (n = 1.19 M, k ~ 300): staging the
-// tile in shared memory with cp.async (2 CTAs/SM: 3.6 TB/s; a producer/consumer
-// mbarrier ring with 2 producer warps: 2.1 TB/s), 1-D TMA bulk copies per
-// vector (1.4 TB/s, op-rate bound), L2 prefetch of the next tile (slower); the
-// register double buffer below is the fastest (4.6 / 3.8 TB/s).
-// UPDATE: w <- w - sum_j s_j h_j W_j, then part[j][blk] = W_j . w_new (the
-// measured second-pass probe, gmres.cpp:101-111) and part[k+1][blk] =
-// ||w_new||^2. !UPDATE: the first (projection) pass, part[j][blk] = W_j . w
-// and part[k+1][blk] = ||w||^2. A 512-thread CTA (one per SM) streams tiles of
-// T rows x (k+1) basis vectors through REGISTERS: thread (rg, cg) owns rows
-// {2 rg, 2 rg + 1} of columns cg, cg + CG, ... (GR_CPT = 8 columns), loaded
-// with 128-bit loads; the loads of tile t+1 are issued before tile t is
-// consumed (register double buffer, ~64 KB in flight per SM). The update
-// reduces row sums across the CG column groups through shared memory (TPR
-// threads per row + shuffles); the probe / projection dot products accumulate
-// per column in registers across all tiles and are reduced across the RG row
-// groups once at the end with shuffles. Each element crosses HBM once.
-// T = 64 / 32 / 16 / 8 for k + 1 <= 128 / 256 / 512 / 1024.
-constexpr int GR_THREADS = 512;
-constexpr int GR_CPT = 8;
-constexpr int GR_SMEM_DOUBLES = 2 * UP_MAXCOLS + 2 * 1024 + 64;  // coef, vp, red (<= 64 x 129), wn
+// ---- clustered, register-tiled Gram-Schmidt passes (the default path) -----------
+// Measured on B200 (scripts/membench.cu): the read bandwidth of a
+// many-vector tile walk is set by the contiguous bytes each CTA takes from one
+// vector per tile -- 64 B: 2.3 TB/s, 128 B: 4.6 TB/s, 256 B: 6.1 TB/s, 512 B:
+// 6.8 TB/s -- and by the bytes in flight per SM. So a tile of T rows x (k+1)
+// basis vectors is split over a thread-block CLUSTER of CL CTAs by vectors:
+// each CTA keeps T rows of only ~(k+1)/CL vectors in registers, which lets T
+// stay at 64 rows (512 B per vector) up to k + 1 = 512 with the same register
+// budget; the update's row sums are combined across the cluster through
+// distributed shared memory (one cluster barrier per tile).
+// Alternatives measured slower: shared-memory staging with cp.async, TMA 2-D
+// boxes (32 rows x 8 vectors: 3.5 TB/s, op-rate bound), 1-D TMA per vector,
+// an mbarrier producer/consumer ring, L2 prefetch, chunk-major basis layout.
+//
+// The kernel is persistent: all running solves' tiles form one list, split
+// into contiguous ranges over the clusters, so every SM works whatever the
+// number of solves in the batch. Partial results per cluster (slot) go to
+// part[j][slot]; clusters that own no tile of a solve write zeros.
+// UPDATE: w <- w - sum_j s_j h_j W_j, then part[j] = W_j . w_new (the measured
+// second-pass probe, gmres.cpp:101-111) and part[k+1] = ||w_new||^2.
+// !UPDATE: the projection, part[j] = W_j . w and part[k+1] = ||w||^2.
+// Thread (rg, cg) owns rows {2 rg, 2 rg + 1} of local vectors cg, cg + CG, ...
+// (GC_CPT = 8), loaded with 128-bit streaming loads; the loads of tile t+1 are
+// issued before tile t is consumed (register double buffer).
+constexpr int GC_THREADS = 512;
+constexpr int GC_CPT = 8;
+constexpr int GC_SMEM_DOUBLES = 1024 + 1024 + 2048 + 2 * 512 + 2 * 512 + 64;
 
-template <int RG, bool UPDATE>
-__device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double* coef, const double** vp,
-                                            double* red, double* wn, bool l2_prefetch) {
-  constexpr int CG = GR_THREADS / RG;
+// Row groups for c vectors per CTA: the largest power of two with
+// (512 / RG) * GC_CPT >= c, capped at 256 (tile = 2 RG rows).
+__host__ __device__ __forceinline__ int gc_rg(int c) {
+  int rg = 256;
+  while (rg > 4 && (GC_THREADS / rg) * GC_CPT < c) rg >>= 1;
+  return rg;
+}
+
+template <int CL>
+__device__ __forceinline__ void gc_cluster_sync() {
+  if (CL > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  }
+}
+
+__device__ __forceinline__ double dsmem_ld(const double* p, int rank) {
+  uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(p)), remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local), "r"(rank));
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(v) : "r"(remote) : "memory");
+  return v;
+}
+
+template <int RG, int CL, bool UPDATE>
+__device__ __forceinline__ void gc_body(GmSolve& st, int G, int slot, int q, int ta, int tb, double* coef,
+                                        const double** vp, double* red, double* wn, double* rowpart) {
+  constexpr int CG = GC_THREADS / RG;
   constexpr int T = 2 * RG;
-  // Row sums: TPR (<= 32, one warp) threads per row, PPT partials each.
-  constexpr int TPR = (GR_THREADS / T) < 32 ? (GR_THREADS / T) : 32;
+  constexpr int TPR = (GC_THREADS / T) < 32 ? (GC_THREADS / T) : 32;  // threads per row in the row sums
   constexpr int PPT = CG / TPR;
-  constexpr int CGP = CG + 1;          // padded partial-sum row
+  constexpr int CGP = CG + 1;
+  constexpr int RW = RG < 32 ? RG : 32;
   const int tid = threadIdx.x;
   const int rg = tid % RG, cg = tid / RG;
   const int my_row = tid / TPR, sub = tid % TPR;
   const int k = st.k, nj = k + 1, n = st.n;
   const int ld = (n + 31) & ~31;
+  const int cpc = (nj + CL - 1) / CL;
+  const int j0 = min(nj, q * cpc), ncol = min(nj, j0 + cpc) - j0;
   double* w = st.V[k + 1];
-  // Column pointers and coefficients stay in shared memory (register budget:
-  // the double-buffered tile and the column accumulators use the rest).
-  const int ncol_me = nj > cg ? min(GR_CPT, (nj - cg + CG - 1) / CG) : 0;
-  double dcol[GR_CPT];
+  __syncthreads();  // the previous segment is done with coef / vp / red
+  for (int l = tid; l < ncol; l += GC_THREADS) {
+    coef[l] = UPDATE ? st.scale[j0 + l] * st.h[j0 + l] : 0.0;
+    vp[l] = st.V[j0 + l];
+  }
+  __syncthreads();
+  const int ncol_me = ncol > cg ? min(GC_CPT, (ncol - cg + CG - 1) / CG) : 0;
+  double dcol[GC_CPT];
 #pragma unroll
-  for (int c = 0; c < GR_CPT; ++c) dcol[c] = 0.0;
+  for (int c = 0; c < GC_CPT; ++c) dcol[c] = 0.0;
   double wsq = 0.0;
-  const int step = nblk * T;
-  // The w rows of a tile are fetched together with its basis block so their
-  // latency is hidden behind the previous tile as well.
-  auto load = [&](int r0, double2* v, double& wp) {
-    const int row = r0 + 2 * rg;
-    const bool inb = r0 < n && row + 1 < ld;
+  auto load = [&](int t, double2* v, double2& w2, double& wp) {
+    const int row = t * T + 2 * rg;
+    const bool inb = t < tb && row < ld;
 #pragma unroll
-    for (int c = 0; c < GR_CPT; ++c)
-      v[c] = (c < ncol_me && inb) ? __ldcs(reinterpret_cast<const double2*>(vp[cg + CG * c] + vidx(row)))
+    for (int c = 0; c < GC_CPT; ++c)
+      v[c] = (c < ncol_me && inb) ? __ldcs(reinterpret_cast<const double2*>(vp[cg + CG * c] + row))
                                   : make_double2(0.0, 0.0);
-    const int rw = r0 + my_row;
-    wp = (sub == 0 && my_row < T && rw < n) ? w[vidx(rw)] : 0.0;
-    // Pull the tile after this one into L2 so its register loads see L2
-    // latency: one prefetch per 128-byte line (T rows x 8 B per column).
-    const int rp = r0 + step + 2 * rg;
-    if (l2_prefetch && ((2 * rg) & 15) == 0 && rp < n) {
-#pragma unroll
-      for (int c = 0; c < GR_CPT; ++c)
-        if (c < ncol_me) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(vp[cg + CG * c] + vidx(rp)));
+    if (UPDATE) {
+      const int rw = t * T + my_row;
+      wp = (t < tb && sub == 0 && my_row < T && rw < n) ? w[rw] : 0.0;
+    } else {
+      w2 = inb ? *reinterpret_cast<const double2*>(w + row) : make_double2(0.0, 0.0);
     }
   };
-  auto consume = [&](int r0, const double2* v, double wpre) {
-    const int rw = r0 + my_row;
-    const bool valid = rw < n;
+  auto consume = [&](int t, const double2* v, double2 w2, double wpre, int par) {
+    double w0, w1;
     if (UPDATE) {
       double ax = 0.0, ay = 0.0;
 #pragma unroll
-      for (int c = 0; c < GR_CPT; ++c) {
+      for (int c = 0; c < GC_CPT; ++c) {
         const double cfc = c < ncol_me ? coef[cg + CG * c] : 0.0;
         ax = fma(cfc, v[c].x, ax);
         ay = fma(cfc, v[c].y, ay);
@@ -546,80 +573,145 @@ __device__ __forceinline__ void gs_reg_body(GmSolve& st, int G, int nblk, double
       double sacc = 0.0;
       if (my_row < T) {
 #pragma unroll
-        for (int q = 0; q < PPT; ++q) sacc += red[my_row * CGP + PPT * sub + q];
+        for (int u = 0; u < PPT; ++u) sacc += red[my_row * CGP + PPT * sub + u];
       }
 #pragma unroll
       for (int o = TPR / 2; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o, TPR);
-      if (sub == 0 && my_row < T) {
-        const double wv = valid ? wpre - sacc : 0.0;
-        if (valid) w[vidx(rw)] = wv;
-        wn[my_row] = wv;
-        wsq = fma(wv, wv, wsq);
+      if (CL > 1) {
+        double* rp = rowpart + par * 512;
+        if (sub == 0 && my_row < T) rp[my_row] = sacc;
+        gc_cluster_sync<CL>();
+        if (sub == 0 && my_row < T) {
+          double tot = 0.0;
+#pragma unroll
+          for (int r = 0; r < CL; ++r) tot += dsmem_ld(rp + my_row, r);
+          sacc = tot;
+        }
       }
-    } else if (sub == 0 && my_row < T) {
-      wn[my_row] = wpre;
-      wsq = fma(wpre, wpre, wsq);
+      double* wb = wn + par * 512;
+      if (sub == 0 && my_row < T) {
+        const int rw = t * T + my_row;
+        const bool valid = rw < n;
+        const double wv = valid ? wpre - sacc : 0.0;
+        if (valid && q == 0) w[rw] = wv;
+        wb[my_row] = wv;
+        if (q == 0) wsq = fma(wv, wv, wsq);
+      }
+      __syncthreads();
+      w0 = wb[2 * rg];
+      w1 = wb[2 * rg + 1];
+    } else {
+      w0 = w2.x;
+      w1 = w2.y;
+      if (q == 0 && cg == 0) wsq = fma(w0, w0, fma(w1, w1, wsq));
+    }
+#pragma unroll
+    for (int c = 0; c < GC_CPT; ++c) dcol[c] = fma(v[c].x, w0, fma(v[c].y, w1, dcol[c]));
+  };
+  double2 va[GC_CPT], vb[GC_CPT];
+  double2 wa2, wb2;
+  double wa = 0.0, wbv = 0.0;
+  int t = ta, par = 0;
+  load(t, va, wa2, wa);
+  while (t < tb) {
+    load(t + 1, vb, wb2, wbv);
+    consume(t, va, wa2, wa, par);
+    ++t;
+    par ^= 1;
+    if (t >= tb) break;
+    load(t + 1, va, wa2, wa);
+    consume(t, vb, wb2, wbv, par);
+    ++t;
+    par ^= 1;
+  }
+  // column sums over the RG row groups
+  if (RG <= 32) {
+#pragma unroll
+    for (int c = 0; c < GC_CPT; ++c) {
+      double x = dcol[c];
+#pragma unroll
+      for (int o = RW / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o, RW);
+      if (rg == 0 && c < ncol_me) st.part[size_t(j0 + cg + CG * c) * G + slot] = x;
+    }
+  } else {
+    constexpr int WPC = RG / 32;  // warps per column group
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < GC_CPT; ++c) {
+      const double x = warp_sum(dcol[c]);
+      if ((tid & 31) == 0) red[(c * CG + cg) * WPC + rg / 32] = x;
     }
     __syncthreads();
-    const double w0 = wn[2 * rg], w1 = wn[2 * rg + 1];
-#pragma unroll
-    for (int c = 0; c < GR_CPT; ++c) dcol[c] = fma(v[c].x, w0, fma(v[c].y, w1, dcol[c]));
-    __syncthreads();  // wn / red are rewritten by the next tile
-  };
-  double2 va[GR_CPT], vb[GR_CPT];
-  double wa, wb;
-  int r0 = blockIdx.x * T;
-  load(r0, va, wa);
-  while (r0 < n) {
-    load(r0 + step, vb, wb);
-    consume(r0, va, wa);
-    r0 += step;
-    if (r0 >= n) break;
-    load(r0 + step, va, wa);
-    consume(r0, vb, wb);
-    r0 += step;
+    if (tid < GC_CPT * CG) {
+      const int c = tid / CG, g = tid % CG;
+      double x = 0.0;
+      for (int u = 0; u < WPC; ++u) x += red[(c * CG + g) * WPC + u];
+      const int l = g + CG * c;
+      if (l < ncol) st.part[size_t(j0 + l) * G + slot] = x;
+    }
   }
-  // column sums across the RG row groups (consecutive lanes), once per CTA
-#pragma unroll
-  for (int c = 0; c < GR_CPT; ++c) {
-    double x = dcol[c];
-#pragma unroll
-    for (int o = RG / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o, RG);
-    const int j = cg + CG * c;
-    if (rg == 0 && j < nj) st.part[size_t(j) * G + blockIdx.x] = x;
-  }
-  // ||w||^2 partial: held by the sub == 0 threads
+  // ||w||^2 partial (rank 0 of the cluster)
   {
     const double x = warp_sum(wsq);
+    __syncthreads();
     if ((tid & 31) == 0) red[tid >> 5] = x;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double x = 0.0;
-    for (int i = 0; i < GR_THREADS / 32; ++i) x += red[i];
-    st.part[size_t(k + 1) * G + blockIdx.x] = x;
+    __syncthreads();
+    if (tid == 0 && q == 0) {
+      double s = 0.0;
+      for (int i = 0; i < GC_THREADS / 32; ++i) s += red[i];
+      st.part[size_t(k + 1) * G + slot] = s;
+    }
   }
 }
 
-template <bool UPDATE>
-__global__ void __launch_bounds__(GR_THREADS, 1) k_gs_reg(GmSolve* S, int G, int nblk, int pf) {
-  GmSolve& st = S[blockIdx.y];
-  if (st.phase != PH_RUN) return;
-  extern __shared__ __align__(16) double sm[];
-  double* coef = sm;
-  const double** vp = reinterpret_cast<const double**>(sm + UP_MAXCOLS);
-  double* red = sm + 2 * UP_MAXCOLS;
-  double* wn = red + 2 * 1024;
-  const int nj = st.k + 1;
-  for (int j = threadIdx.x; j < nj; j += GR_THREADS) {
-    coef[j] = UPDATE ? st.scale[j] * st.h[j] : 0.0;
-    vp[j] = st.V[j];
+__device__ __forceinline__ int gc_tiles(const GmSolve& st, int CL) {
+  const int cpc = (st.k + 1 + CL - 1) / CL;
+  const int T = 2 * gc_rg(cpc);
+  return (st.n + T - 1) / T;
+}
+
+template <int CL, bool UPDATE>
+__global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, int G) {
+  extern __shared__ __align__(16) double smc[];
+  double* coef = smc;
+  const double** vp = reinterpret_cast<const double**>(smc + 1024);
+  double* red = smc + 2048;
+  double* wn = red + 2048;
+  double* rowpart = wn + 2 * 512;
+  const int q = int(blockIdx.x) % CL, slot = int(blockIdx.x) / CL, ncl = int(gridDim.x) / CL;
+  long long total = 0;
+  for (int s = 0; s < ns; ++s)
+    if (S[s].phase == PH_RUN) total += gc_tiles(S[s], CL);
+  const long long per = (total + ncl - 1) / ncl;
+  const long long a = per * slot, b = min(total, a + per);
+  long long off = 0;
+  for (int s = 0; s < ns; ++s) {
+    GmSolve& st = S[s];
+    if (st.phase != PH_RUN) continue;
+    const int nt = gc_tiles(st, CL);
+    const long long lo = a > off ? a : off, hi = b < off + nt ? b : off + nt;
+    if (lo < hi) {
+      const int ta = int(lo - off), tb = int(hi - off);
+      const int cpc = (st.k + 1 + CL - 1) / CL;
+      switch (gc_rg(cpc)) {
+        case 256: gc_body<256, CL, UPDATE>(st, G, slot, q, ta, tb, coef, vp, red, wn, rowpart); break;
+        case 128: gc_body<128, CL, UPDATE>(st, G, slot, q, ta, tb, coef, vp, red, wn, rowpart); break;
+        case 64: gc_body<64, CL, UPDATE>(st, G, slot, q, ta, tb, coef, vp, red, wn, rowpart); break;
+        case 32: gc_body<32, CL, UPDATE>(st, G, slot, q, ta, tb, coef, vp, red, wn, rowpart); break;
+        case 16: gc_body<16, CL, UPDATE>(st, G, slot, q, ta, tb, coef, vp, red, wn, rowpart); break;
+        case 8: gc_body<8, CL, UPDATE>(st, G, slot, q, ta, tb, coef, vp, red, wn, rowpart); break;
+        default: gc_body<4, CL, UPDATE>(st, G, slot, q, ta, tb, coef, vp, red, wn, rowpart); break;
+      }
+    } else {
+      // no tile of this solve here: zero partials for this CTA's vectors
+      const int nj = st.k + 1, cpc = (nj + CL - 1) / CL;
+      const int j0 = min(nj, q * cpc), j1 = min(nj, j0 + cpc);
+      for (int j = j0 + int(threadIdx.x); j < j1; j += GC_THREADS) st.part[size_t(j) * G + slot] = 0.0;
+      if (q == 0 && threadIdx.x == 0) st.part[size_t(nj) * G + slot] = 0.0;
+    }
+    off += nt;
   }
-  __syncthreads();
-  if (nj <= 128) gs_reg_body<32, UPDATE>(st, G, nblk, coef, vp, red, wn, pf);
-  else if (nj <= 256) gs_reg_body<16, UPDATE>(st, G, nblk, coef, vp, red, wn, pf);
-  else if (nj <= 512) gs_reg_body<8, UPDATE>(st, G, nblk, coef, vp, red, wn, pf);
-  else gs_reg_body<4, UPDATE>(st, G, nblk, coef, vp, red, wn, pf);
+  gc_cluster_sync<CL>();  // peers may still read this CTA's row partials
 }
 
 // ---- norm partials of the residual buffer ----------------------------------------
@@ -818,6 +910,88 @@ __global__ void k_pack_rhs(GmSolve* S) {
 
 inline unsigned cdiv(int64_t a, int64_t b) { return unsigned((a + b - 1) / b); }
 
+// Cluster launch of the Gram-Schmidt kernels: ncl clusters of CL CTAs.
+template <int CL, bool UPDATE>
+cudaError_t gc_launch(cudaStream_t s, int ncl, GmSolve* S, int ns, int G) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(ncl * CL), 1u, 1u);
+  cfg.blockDim = dim3(unsigned(GC_THREADS), 1u, 1u);
+  cfg.dynamicSmemBytes = size_t(GC_SMEM_DOUBLES) * sizeof(double);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(CL);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_gs_clu<CL, UPDATE>, S, ns, G);
+}
+
+template <int CL>
+int gc_max_clusters(int sm_count) {
+  const int smem = GC_SMEM_DOUBLES * int(sizeof(double));
+  cudaFuncSetAttribute(k_gs_clu<CL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_gs_clu<CL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(sm_count / CL * CL), 1u, 1u);
+  cfg.blockDim = dim3(unsigned(GC_THREADS), 1u, 1u);
+  cfg.dynamicSmemBytes = size_t(smem);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(CL);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int a = 0, b = 0;
+  if (cudaOccupancyMaxActiveClusters(&a, k_gs_clu<CL, true>, &cfg) != cudaSuccess ||
+      cudaOccupancyMaxActiveClusters(&b, k_gs_clu<CL, false>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return std::min(std::min(a, b), sm_count / CL);
+}
+
+// Cluster size and clusters per launch of one Gram-Schmidt pass. Measured on
+// C3 (k + 1 up to 335): the projection pass is fastest with pairs (6.3 TB/s:
+// 256-512 B per vector per tile), the update + probe pass without clusters
+// (4.7 TB/s; the per-tile cluster barrier of its row sums costs more than the
+// longer segments gain). MPG_GS_CLUSTER_DOT / MPG_GS_CLUSTER_UPD override
+// (1, 2 or 4; smaller clusters are used when the device cannot co-schedule).
+struct GcConfig {
+  int cl = 1, ncl = 1;
+};
+GcConfig gc_config(int dev, int sm_count, bool update) {
+  static std::mutex mu;
+  static GcConfig cache[2][64];
+  static bool have[2][64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev >= 0 && dev < 64 && have[update][dev]) return cache[update][dev];
+  const char* e = std::getenv(update ? "MPG_GS_CLUSTER_UPD" : "MPG_GS_CLUSTER_DOT");
+  int want = e ? std::atoi(e) : (update ? 1 : 2);
+  GcConfig g;
+  if (want >= 4 && (g.ncl = gc_max_clusters<4>(sm_count)) > 0) g.cl = 4;
+  else if (want >= 2 && (g.ncl = gc_max_clusters<2>(sm_count)) > 0) g.cl = 2;
+  else {
+    g.cl = 1;
+    g.ncl = std::max(1, gc_max_clusters<1>(sm_count));
+  }
+  if (dev >= 0 && dev < 64) {
+    cache[update][dev] = g;
+    have[update][dev] = true;
+  }
+  return g;
+}
+
+cudaError_t gc_launch_any(bool update, const GcConfig& g, cudaStream_t s, GmSolve* S, int ns, int G) {
+  switch (g.cl) {
+    case 4: return update ? gc_launch<4, true>(s, g.ncl, S, ns, G) : gc_launch<4, false>(s, g.ncl, S, ns, G);
+    case 2: return update ? gc_launch<2, true>(s, g.ncl, S, ns, G) : gc_launch<2, false>(s, g.ncl, S, ns, G);
+    default: return update ? gc_launch<1, true>(s, g.ncl, S, ns, G) : gc_launch<1, false>(s, g.ncl, S, ns, G);
+  }
+}
+
 struct SolveHost {
   std::vector<DBuf<double>> panels;
   std::vector<double*> vtab;  // host mirror of the V table
@@ -847,7 +1021,10 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   int64_t nmax = 0;
   for (auto& sp : specs) nmax = std::max<int64_t>(nmax, sp.sim != 0.0 ? 2 * nb : nb);
   const int ntiles = int(cdiv(nmax, DOT_TILE));
-  const int G = std::max(1, std::min(ntiles, std::max(8, (c.sm_count * 8) / ns)));
+  const GcConfig gc_dot = gc_config(dev, c.sm_count, false), gc_upd = gc_config(dev, c.sm_count, true);
+  // partial-sum slots per solve: the dot/update grids, and one per GS cluster
+  const int G = std::max(std::max(gc_dot.ncl, gc_upd.ncl),
+                         std::max(1, std::min(ntiles, std::max(8, (c.sm_count * 8) / ns))));
 
   std::vector<SolveHost> sh(static_cast<size_t>(ns));
   std::vector<GmSolve> hs(static_cast<size_t>(ns));
@@ -979,11 +1156,8 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     cudaFuncSetAttribute(k_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_gs_reg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GR_SMEM_DOUBLES * 8);
-    cudaFuncSetAttribute(k_gs_reg<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GR_SMEM_DOUBLES * 8);
   });
   const bool fused = maxit + 1 <= UP_MAXCOLS && !std::getenv("MPG_NO_FUSE");
-  const int l2pf = std::getenv("MPG_L2PF") ? 1 : 0;  // measured slower on C3: opt-in only
   int launches_per_iter = 0;
   // Profiling hook: called after every launch with a kernel-class id.
   std::function<void(int)> mark = [](int) {};
@@ -1093,23 +1267,18 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     }
   };
   const dim3 gG{unsigned(G), unsigned(ns), 1u};
-  // One long-running CTA per SM for the staged Gram-Schmidt passes.
-  // exactly one wave of one-CTA-per-SM blocks: floor, never more blocks than SMs
-  const int Ggr = std::max(1, std::min(G, c.sm_count / ns));
-  const dim3 gGr{unsigned(Ggr), unsigned(ns), 1u};
-  const size_t smem_gr = size_t(GR_SMEM_DOUBLES) * sizeof(double);
   const dim3 gR{cdiv(maxit + 2, 8), unsigned(ns), 1u};
   auto record_iteration = [&] {
     launches_per_iter = 0;
     for (int st = 0; st < max_stages; ++st) chain_stage(st, 0);
     iter_op(0);
-    if (fused) k_gs_reg<false><<<gGr, GR_THREADS, smem_gr, s>>>(dS.get(), G, Ggr, l2pf);
+    if (fused) MPG_CUDA(gc_launch_any(false, gc_dot, s, dS.get(), ns, G));
     else k_dot<<<gG, 256, smem_dot, s>>>(dS.get(), G);
     mark(PK_DOT);
-    k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 0, fused ? Ggr : G);
+    k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 0, fused ? gc_dot.ncl : G);
     mark(PK_SMALL);
     if (fused) {
-      k_gs_reg<true><<<gGr, GR_THREADS, smem_gr, s>>>(dS.get(), G, Ggr, l2pf);
+      MPG_CUDA(gc_launch_any(true, gc_upd, s, dS.get(), ns, G));
       mark(PK_UPDPROBE);
       --launches_per_iter;
     } else {
@@ -1118,7 +1287,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       k_dot<<<gG, 256, smem_dot, s>>>(dS.get(), G);
       mark(PK_PROBE);
     }
-    k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 1, fused ? Ggr : G);
+    k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 1, fused ? gc_upd.ncl : G);
     mark(PK_SMALL);
     k_update<<<gG, 256, smem_upd, s>>>(dS.get(), G, 1);
     mark(PK_REORTH);
