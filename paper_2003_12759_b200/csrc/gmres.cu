@@ -45,7 +45,8 @@ struct GmSolve {
   double sre, sim, ca, target, bnorm;
   // state
   int k, phase, asm_kind, asm_k, guess, iterations, converged, breakdown, xsel, reorth_count;
-  int grouped_op, grouped_chain;  // handled by the shared-matrix (multi-RHS) kernels
+  int grouped_op;     // bit 0: run-mode operator by a group kernel, bit 1: assembly-mode
+  int grouped_chain;  // handled by the shared-matrix (multi-RHS) kernels
   double estimate, recheck_at, w2_pre, w2_a, w2_b, wn_cur, final_residual;
   // arrays
   double** V;
@@ -118,7 +119,7 @@ template <int V, int EM>
 __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView opt, int mode) {
   GmSolve& st = S[blockIdx.y];
   if (mode == 0 ? st.phase != PH_RUN : st.phase != PH_ASM) return;
-  if (st.grouped_op) return;
+  if (st.grouped_op & (mode == 0 ? 1 : 2)) return;
   const OpView& op = st.transpose ? opt : opn;
   const int n = op.a.nrows;
   const int lane = threadIdx.x & (V - 1);
@@ -310,6 +311,117 @@ __global__ void __launch_bounds__(256) k_iter_op_multi(GmSolve* S, Group grp, Op
       if (mode == 0) st.V[st.k + 1][row] = st.scale[st.k] * y1;
       else st.rbuf[row] = st.V[0][row] - y1;
     }
+  }
+}
+
+// ---- interleaved multi-RHS path (run mode) --------------------------------------
+// A group whose solves share the chain AND the operator side keeps its MB
+// right-hand sides interleaved, x[row][q] (64 B per row): a gather of column c
+// then fetches all MB values with four 128-bit loads from one 64-byte span
+// instead of MB separate 8-byte gathers (4x fewer L1/L2 sectors; the separate
+// gathers made the shared-matrix SpMVs L1/latency bound at ~1.5-2 TB/s of
+// DRAM traffic, profiles/r01/ncu_full_c3_summary.txt).
+__global__ void __launch_bounds__(256) k_pack_il(GmSolve* S, Group grp, double* xa, int n) {
+  const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  const int row = int(i / MB), q = int(i % MB);
+  if (row >= n) return;
+  double v = 0.0;
+  if (q < grp.cnt) {
+    const GmSolve& st = S[grp.idx[q]];
+    if (st.phase == PH_RUN) v = st.V[st.k][row];
+  }
+  xa[i] = v;
+}
+
+__device__ __forceinline__ bool il_any_run(const GmSolve* S, const Group& grp) {
+  bool any = false;
+  for (int q = 0; q < grp.cnt; ++q) any |= S[grp.idx[q]].phase == PH_RUN;
+  return any;
+}
+
+template <int V>
+__global__ void __launch_bounds__(256) k_chain_il(GmSolve* S, Group grp, CsrView f, const double* __restrict__ xin,
+                                                  double* __restrict__ xout) {
+  if (!il_any_run(S, grp)) return;
+  const int lane = threadIdx.x & (V - 1);
+  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / V);
+  double acc[MB];
+#pragma unroll
+  for (int q = 0; q < MB; ++q) acc[q] = 0.0;
+  if (row < f.nrows) {
+    const int b = f.rowptr[row], e = f.rowptr[row + 1];
+#pragma unroll 2
+    for (int k = b + lane; k < e; k += V) {
+      const double a = __ldcs(f.val + k);
+      const double2* xp = reinterpret_cast<const double2*>(xin + size_t(__ldcs(f.colind + k)) * MB);
+#pragma unroll
+      for (int h = 0; h < MB / 2; ++h) {
+        const double2 x = __ldg(xp + h);
+        acc[2 * h] = fma(a, x.x, acc[2 * h]);
+        acc[2 * h + 1] = fma(a, x.y, acc[2 * h + 1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < MB; ++q) acc[q] = sub_sum<V>(acc[q]);
+  if (row < f.nrows) {
+    double2* yp = reinterpret_cast<double2*>(xout + size_t(row) * MB);
+#pragma unroll
+    for (int h = 0; h < MB / 2; ++h)
+      if (h % V == lane) yp[h] = make_double2(acc[2 * h], acc[2 * h + 1]);
+  }
+}
+
+template <int V, int EM>
+__global__ void __launch_bounds__(256) k_op_il(GmSolve* S, Group grp, OpView op, const double* __restrict__ xin) {
+  if (!il_any_run(S, grp)) return;
+  const int n = op.a.nrows;
+  const int lane = threadIdx.x & (V - 1);
+  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / V);
+  double a1[MB], e1[MB];
+#pragma unroll
+  for (int q = 0; q < MB; ++q) a1[q] = e1[q] = 0.0;
+  if (row < n) {
+    const int b = op.a.rowptr[row], e = op.a.rowptr[row + 1];
+#pragma unroll 2
+    for (int k = b + lane; k < e; k += V) {
+      const double2* xp = reinterpret_cast<const double2*>(xin + size_t(__ldcs(op.a.colind + k)) * MB);
+      if (EM == E_SAMEPAT) {
+        const double2 ae = __ldcs(op.ae + k);
+#pragma unroll
+        for (int h = 0; h < MB / 2; ++h) {
+          const double2 x = __ldg(xp + h);
+          a1[2 * h] = fma(ae.x, x.x, a1[2 * h]);
+          a1[2 * h + 1] = fma(ae.x, x.y, a1[2 * h + 1]);
+          e1[2 * h] = fma(ae.y, x.x, e1[2 * h]);
+          e1[2 * h + 1] = fma(ae.y, x.y, e1[2 * h + 1]);
+        }
+      } else {
+        const double av = __ldcs(op.a.val + k);
+#pragma unroll
+        for (int h = 0; h < MB / 2; ++h) {
+          const double2 x = __ldg(xp + h);
+          a1[2 * h] = fma(av, x.x, a1[2 * h]);
+          a1[2 * h + 1] = fma(av, x.y, a1[2 * h + 1]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < MB; ++q) {
+    a1[q] = sub_sum<V>(a1[q]);
+    if (EM == E_SAMEPAT) e1[q] = sub_sum<V>(e1[q]);
+  }
+  if (row >= n) return;
+#pragma unroll
+  for (int q = 0; q < MB; ++q) {
+    if (q % V != lane || q >= grp.cnt) continue;
+    GmSolve& st = S[grp.idx[q]];
+    if (st.phase != PH_RUN) continue;
+    double ex = e1[q];
+    if (EM == E_IDENT) ex = xin[size_t(row) * MB + q];
+    else if (EM == E_DIAG) ex = op.ediag[row] * xin[size_t(row) * MB + q];
+    st.V[st.k + 1][row] = st.scale[st.k] * (st.sre * ex + st.ca * a1[q]);
   }
 }
 
@@ -669,6 +781,13 @@ __device__ __forceinline__ int gc_tiles(const GmSolve& st, int CL) {
   const int T = 2 * gc_rg(cpc);
   return (st.n + T - 1) / T;
 }
+
+// Update + probe with clusters (measured, C3, k + 1 <= 335): a cluster barrier
+// per tile for the row sums gives 3.3 / 2.7 TB/s for pairs / quads (the
+// barrier's release waits for the in-flight loads of the next tile); a version
+// that sends the row partials with st.async + mbarriers and defers the probe by
+// one tile (tile parked in shared memory) reached 3.2 / 2.2 TB/s (shared-memory
+// traffic, mbarrier spinning). Unclustered: 4.7 TB/s -- the default.
 
 template <int CL, bool UPDATE>
 __global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, int G) {
@@ -1163,8 +1282,11 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   std::function<void(int)> mark = [](int) {};
   // Shared-matrix groups (MPG_NO_MULTI disables): solves with the same chain
   // (non-pair) and real shifts on the same operator side.
-  std::vector<Group> chain_groups, op_groups;
+  std::vector<Group> chain_groups, op_groups_run, op_groups_asm;
   std::vector<const Chain*> chain_of_group;
+  std::vector<char> chain_il;          // chain group runs the interleaved path in run mode
+  std::vector<DBuf<double>> il_bufs;   // two [n][MB] buffers per chain group (empty if not il)
+  bool any_plain_chain = true, any_plain_op_run = true, any_plain_op_asm = true;
   if (!std::getenv("MPG_NO_MULTI")) {
     std::vector<int> used(size_t(ns), 0);
     for (int i = 0; i < ns; ++i) {
@@ -1184,18 +1306,49 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       }
       for (int m : mem) { used[size_t(m)] = 1; hs[size_t(m)].grouped_chain = 1; }
     }
-    for (int side = 0; side < 2; ++side) {
-      std::vector<int> mem;
-      for (int i = 0; i < ns; ++i)
-        if (!hs[size_t(i)].pair && hs[size_t(i)].transpose == side) mem.push_back(i);
-      if (mem.size() < 2) continue;
-      for (size_t b = 0; b < mem.size(); b += MB) {
-        Group g{};
-        g.cnt = int(std::min<size_t>(MB, mem.size() - b));
-        for (int q = 0; q < g.cnt; ++q) g.idx[q] = mem[b + size_t(q)];
-        op_groups.push_back(g);
+    // interleaved path: chain groups of real shifts on one operator side
+    const bool il_on = !std::getenv("MPG_NO_IL");
+    std::vector<int> in_il(size_t(ns), 0);
+    for (size_t gi = 0; gi < chain_groups.size(); ++gi) {
+      const Group& g = chain_groups[gi];
+      bool ok = il_on && g.cnt >= 2;
+      for (int q = 0; q < g.cnt && ok; ++q) {
+        const GmSolve& m = hs[size_t(g.idx[q])];
+        ok = !m.pair && m.transpose == hs[size_t(g.idx[0])].transpose && m.n == int(nb);
       }
-      for (int m : mem) hs[size_t(m)].grouped_op = 1;
+      chain_il.push_back(ok ? 1 : 0);
+      if (ok) {
+        il_bufs.emplace_back(dev, size_t(nb) * MB);
+        il_bufs.emplace_back(dev, size_t(nb) * MB);
+        for (int q = 0; q < g.cnt; ++q) in_il[size_t(g.idx[q])] = 1;
+      } else {
+        il_bufs.emplace_back();
+        il_bufs.emplace_back();
+      }
+    }
+    for (int mode = 0; mode < 2; ++mode)
+      for (int side = 0; side < 2; ++side) {
+        std::vector<int> mem;
+        for (int i = 0; i < ns; ++i)
+          if (!hs[size_t(i)].pair && hs[size_t(i)].transpose == side && !(mode == 0 && in_il[size_t(i)]))
+            mem.push_back(i);
+        if (mem.size() < 2) continue;
+        for (size_t b = 0; b < mem.size(); b += MB) {
+          Group g{};
+          g.cnt = int(std::min<size_t>(MB, mem.size() - b));
+          for (int q = 0; q < g.cnt; ++q) g.idx[q] = mem[b + size_t(q)];
+          (mode == 0 ? op_groups_run : op_groups_asm).push_back(g);
+        }
+        for (int m : mem) hs[size_t(m)].grouped_op |= mode == 0 ? 1 : 2;
+      }
+    for (int i = 0; i < ns; ++i)
+      if (in_il[size_t(i)]) hs[size_t(i)].grouped_op |= 1;
+    any_plain_chain = any_plain_op_run = any_plain_op_asm = false;
+    for (int i = 0; i < ns; ++i) {
+      const GmSolve& m = hs[size_t(i)];
+      if (m.stages > 0 && !m.grouped_chain) any_plain_chain = true;
+      if (!(m.grouped_op & 1)) any_plain_op_run = true;
+      if (!(m.grouped_op & 2)) any_plain_op_asm = true;
     }
     MPG_CUDA(cudaMemcpyAsync(dS.get(), hs.data(), sizeof(GmSolve) * size_t(ns), cudaMemcpyHostToDevice, s));
   }
@@ -1206,6 +1359,27 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       const DevCsr& f = *ch.factors[size_t(stage)];
       const int Vf = choose_vec_width(f.mean_row);
       const unsigned grid = cdiv(f.nrows * int64_t(Vf), 256);
+      if (mode == 0 && chain_il[gi]) {
+        double* xa = il_bufs[2 * gi].get();
+        double* xb = il_bufs[2 * gi + 1].get();
+        if (stage == 0) {
+          k_pack_il<<<cdiv(nb * MB, 256), 256, 0, s>>>(dS.get(), chain_groups[gi], xa, int(nb));
+          ++launches_per_iter;
+          mark(PK_CHAIN);
+        }
+        const double* xin = (stage & 1) ? xb : xa;
+        double* xout = (stage & 1) ? xa : xb;
+        switch (Vf) {
+          case 2: k_chain_il<2><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), xin, xout); break;
+          case 4: k_chain_il<4><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), xin, xout); break;
+          case 8: k_chain_il<8><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), xin, xout); break;
+          case 16: k_chain_il<16><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), xin, xout); break;
+          default: k_chain_il<32><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), xin, xout); break;
+        }
+        ++launches_per_iter;
+        mark(PK_CHAIN);
+        continue;
+      }
       switch (Vf) {
         case 2: k_chain_multi<2><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
         case 4: k_chain_multi<4><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
@@ -1216,6 +1390,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       ++launches_per_iter;
       mark(mode == 0 ? PK_CHAIN : PK_ASM);
     }
+    if (!any_plain_chain) return;
     const dim3 grid(cdiv(max_fac_rows * int64_t(Vfac), 256), unsigned(ns));
     switch (Vfac) {
       case 2: k_chain_stage<2><<<grid, 256, 0, s>>>(dS.get(), stage, mode); break;
@@ -1228,6 +1403,31 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     mark(mode == 0 ? PK_CHAIN : PK_ASM);
   };
   auto iter_op = [&](int mode) {
+    if (mode == 0)
+      for (size_t gi = 0; gi < chain_groups.size(); ++gi) {
+        if (!chain_il[gi]) continue;
+        const Group& g = chain_groups[gi];
+        const OpView& ov = hs[size_t(g.idx[0])].transpose ? opt_ : opn;
+        const int nst = int(chain_of_group[gi]->factors.size());
+        const double* xin = ((nst - 1) & 1) ? il_bufs[2 * gi].get() : il_bufs[2 * gi + 1].get();
+        const unsigned grid1 = cdiv(nb * int64_t(Vop), 256);
+#define MPG_OPI(VV)                                                                                            \
+  switch (op.emode) {                                                                                          \
+    case E_IDENT: k_op_il<VV, E_IDENT><<<grid1, 256, 0, s>>>(dS.get(), g, ov, xin); break;                    \
+    case E_DIAG: k_op_il<VV, E_DIAG><<<grid1, 256, 0, s>>>(dS.get(), g, ov, xin); break;                      \
+    default: k_op_il<VV, E_SAMEPAT><<<grid1, 256, 0, s>>>(dS.get(), g, ov, xin); break;                       \
+  }
+        switch (Vop) {
+          case 2: MPG_OPI(2); break;
+          case 4: MPG_OPI(4); break;
+          case 8: MPG_OPI(8); break;
+          case 16: MPG_OPI(16); break;
+          default: MPG_OPI(32); break;
+        }
+#undef MPG_OPI
+        ++launches_per_iter;
+        mark(PK_OP);
+      }
     const dim3 grid(cdiv(nb * int64_t(Vop), 256), unsigned(ns));
 #define MPG_OPL(VV)                                                                                            \
   switch (op.emode) {                                                                                          \
@@ -1235,6 +1435,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     case E_DIAG: k_iter_op<VV, E_DIAG><<<grid, 256, 0, s>>>(dS.get(), opn, opt_, mode); break;                \
     default: k_iter_op<VV, E_SAMEPAT><<<grid, 256, 0, s>>>(dS.get(), opn, opt_, mode); break;                 \
   }
+    if (mode == 0 ? any_plain_op_run : any_plain_op_asm) {
     switch (Vop) {
       case 2: MPG_OPL(2); break;
       case 4: MPG_OPL(4); break;
@@ -1245,7 +1446,8 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
 #undef MPG_OPL
     ++launches_per_iter;
     mark(mode == 0 ? PK_OP : PK_ASM);
-    for (const Group& g : op_groups) {
+    }
+    for (const Group& g : (mode == 0 ? op_groups_run : op_groups_asm)) {
       const OpView& ov = hs[size_t(g.idx[0])].transpose ? opt_ : opn;
       const unsigned grid1 = cdiv(nb * int64_t(Vop), 256);
 #define MPG_OPM(VV)                                                                                            \
