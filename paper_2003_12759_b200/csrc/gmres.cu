@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(256) k_update(GmSolve* S, int G, int mode) {
   }
 }
 
-constexpr int UP_MAXCOLS = 1024;
+constexpr int UP_MAXCOLS = 2048;  // largest k + 1 of the fused (clustered) Gram-Schmidt path
 
 // ---- clustered, register-tiled Gram-Schmidt passes (the default path) -----------
 // Measured on B200 (scripts/membench.cu): the read bandwidth of a
@@ -601,13 +601,13 @@ constexpr int UP_MAXCOLS = 1024;
 // issued before tile t is consumed (register double buffer).
 constexpr int GC_THREADS = 512;
 constexpr int GC_CPT = 8;
-constexpr int GC_SMEM_DOUBLES = 1024 + 1024 + 2048 + 2 * 512 + 2 * 512 + 64;
+constexpr int GC_SMEM_DOUBLES = UP_MAXCOLS + UP_MAXCOLS + 2048 + 2 * 512 + 2 * 512 + 64;
 
 // Row groups for c vectors per CTA: the largest power of two with
 // (512 / RG) * GC_CPT >= c, capped at 256 (tile = 2 RG rows).
 __host__ __device__ __forceinline__ int gc_rg(int c) {
   int rg = 256;
-  while (rg > 4 && (GC_THREADS / rg) * GC_CPT < c) rg >>= 1;
+  while (rg > 2 && (GC_THREADS / rg) * GC_CPT < c) rg >>= 1;
   return rg;
 }
 
@@ -793,8 +793,8 @@ template <int CL, bool UPDATE>
 __global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, int G) {
   extern __shared__ __align__(16) double smc[];
   double* coef = smc;
-  const double** vp = reinterpret_cast<const double**>(smc + 1024);
-  double* red = smc + 2048;
+  const double** vp = reinterpret_cast<const double**>(smc + UP_MAXCOLS);
+  double* red = smc + 2 * UP_MAXCOLS;
   double* wn = red + 2048;
   double* rowpart = wn + 2 * 512;
   const int q = int(blockIdx.x) % CL, slot = int(blockIdx.x) / CL, ncl = int(gridDim.x) / CL;
@@ -819,7 +819,8 @@ __global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, in
         case 32: gc_body<32, CL, UPDATE>(st, G, slot, q, ta, tb, coef, vp, red, wn, rowpart); break;
         case 16: gc_body<16, CL, UPDATE>(st, G, slot, q, ta, tb, coef, vp, red, wn, rowpart); break;
         case 8: gc_body<8, CL, UPDATE>(st, G, slot, q, ta, tb, coef, vp, red, wn, rowpart); break;
-        default: gc_body<4, CL, UPDATE>(st, G, slot, q, ta, tb, coef, vp, red, wn, rowpart); break;
+        case 4: gc_body<4, CL, UPDATE>(st, G, slot, q, ta, tb, coef, vp, red, wn, rowpart); break;
+        default: gc_body<2, CL, UPDATE>(st, G, slot, q, ta, tb, coef, vp, red, wn, rowpart); break;
       }
     } else {
       // no tile of this solve here: zero partials for this CTA's vectors

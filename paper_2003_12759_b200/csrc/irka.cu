@@ -16,6 +16,7 @@
 // all-gather of the solved V/W columns (K6), after which every rank projects
 // redundantly.
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -405,11 +406,12 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
         if (!outc[i].converged) {
           res.rows.insert(res.rows.end(), rows.begin(), rows.end());
           const Task& t = mine[b0 + i];
+          char rel[32];
+          std::snprintf(rel, sizeof rel, "%.3e", outc[i].final_residual / std::max(outc[i].rhs_norm, 1e-300));
           throw SolverError(std::string("birka: gmres did not converge on the ") + (t.side == 0 ? "trial" : "test") +
                             " side (sweep " + std::to_string(z) + ", unit at column " + std::to_string(t.c0) +
-                            "; relative residual " +
-                            std::to_string(outc[i].final_residual / std::max(outc[i].rhs_norm, 1e-300)) + " after " +
-                            std::to_string(outc[i].iterations) + " iterations)");
+                            "; relative residual " + rel + " after " + std::to_string(outc[i].iterations) +
+                            " iterations)");
         }
       }
     }

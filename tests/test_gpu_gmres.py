@@ -130,16 +130,16 @@ def test_batch_equals_single_solves(mpg, gen):
         assert rel(r.x, single.x) <= 1e-12
 
 
-@pytest.mark.parametrize("n", [300, 700, 1500])
-def test_long_krylov_runs_match_oracle(mpg, orc, gen, n):
-    """251 / 490 / 882 iterations: exercises every Gram-Schmidt tile shape
-    (k+1 <= 128 / 256 / 512 / 1024) and the measured second pass."""
+@pytest.mark.parametrize("n,maxit", [(300, 1000), (700, 1000), (1500, 1000), (2600, 2000)])
+def test_long_krylov_runs_match_oracle(mpg, orc, gen, n, maxit):
+    """251 / 490 / 882 / ~1300 iterations: exercises every Gram-Schmidt tile
+    shape (k+1 up to 2048) and the measured second pass."""
     d = 1.0 + np.arange(n) ** 1.5  # spectrum [1, n^1.5]
     h = gen.from_triplets(n, n, np.arange(n), np.arange(n), d)
     b = gen.random_dense(n, 1, 5)[:, 0]
-    cfg = mpg.GmresConfig(rel_tol=1e-10, max_iter=1000)
+    cfg = mpg.GmresConfig(rel_tol=1e-10, max_iter=maxit)
     g = mpg.gmres_right_preconditioned(_m(mpg, h), None, b, cfg)
-    xo, ro = orc.gmres_csr(orc.Csr.of(h), None, b, orc.GmresConfig(1e-10, 1000))
+    xo, ro = orc.gmres_csr(orc.Csr.of(h), None, b, orc.GmresConfig(1e-10, maxit))
     assert ro.converged and g.report.converged, (g.report.iterations, ro.iterations)
     assert abs(g.report.iterations - ro.iterations) <= max(3, 0.03 * ro.iterations)
     assert np.linalg.norm(d * g.x - b) <= 1e-10 * np.linalg.norm(b)
