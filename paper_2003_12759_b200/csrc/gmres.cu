@@ -425,6 +425,67 @@ __global__ void __launch_bounds__(256) k_op_il(GmSolve* S, Group grp, OpView op,
   }
 }
 
+// RHS-split variants: the 4 lanes of a row split the 8 right-hand sides (2
+// each) and walk every nonzero of the row together, so one warp instruction
+// gathers 8 rows x 64 contiguous bytes (two full sectors per nonzero instead
+// of four half-used 16-byte pieces) and no cross-lane reduction is needed.
+template <int EM, bool CHAIN>
+__global__ void __launch_bounds__(256) k_spmv_il2(GmSolve* S, Group grp, CsrView f, OpView op,
+                                                  const double* __restrict__ xin, double* __restrict__ xout) {
+  if (!il_any_run(S, grp)) return;
+  const int lane = threadIdx.x & 3;
+  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) >> 2);
+  const int n = CHAIN ? f.nrows : op.a.nrows;
+  if (row >= n) return;
+  const int* rp = CHAIN ? f.rowptr : op.a.rowptr;
+  const int* ci = CHAIN ? f.colind : op.a.colind;
+  const int b = rp[row], e = rp[row + 1];
+  const double* xl = xin + 2 * lane;
+  double a0 = 0.0, a1 = 0.0, e0 = 0.0, e1 = 0.0;
+  int k = b;
+#pragma unroll 4
+  for (; k < e; ++k) {
+    const int c = __ldg(ci + k);
+    const double2 x = __ldg(reinterpret_cast<const double2*>(xl + size_t(c) * MB));
+    if (CHAIN) {
+      const double av = __ldg(f.val + k);
+      a0 = fma(av, x.x, a0);
+      a1 = fma(av, x.y, a1);
+    } else if (EM == E_SAMEPAT) {
+      const double2 ae = __ldg(op.ae + k);
+      a0 = fma(ae.x, x.x, a0);
+      a1 = fma(ae.x, x.y, a1);
+      e0 = fma(ae.y, x.x, e0);
+      e1 = fma(ae.y, x.y, e1);
+    } else {
+      const double av = __ldg(op.a.val + k);
+      a0 = fma(av, x.x, a0);
+      a1 = fma(av, x.y, a1);
+    }
+  }
+  if (CHAIN) {
+    reinterpret_cast<double2*>(xout + size_t(row) * MB)[lane] = make_double2(a0, a1);
+    return;
+  }
+  const double2 xr = reinterpret_cast<const double2*>(xin + size_t(row) * MB)[lane];
+  if (EM == E_IDENT) {
+    e0 = xr.x;
+    e1 = xr.y;
+  } else if (EM == E_DIAG) {
+    const double dd = op.ediag[row];
+    e0 = dd * xr.x;
+    e1 = dd * xr.y;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int q = 2 * lane + h;
+    if (q >= grp.cnt) continue;
+    GmSolve& st = S[grp.idx[q]];
+    if (st.phase != PH_RUN) continue;
+    st.V[st.k + 1][row] = st.scale[st.k] * (st.sre * (h ? e1 : e0) + st.ca * (h ? a1 : a0));
+  }
+}
+
 // ---- dot: part[j][blk] = W_j . w (j <= k), part[k+1][blk] = ||w||^2 -------------
 // which 0: w = W_{k+1} (projection h); which 1: w = W_{k+1} (probe d)
 __global__ void __launch_bounds__(256) k_dot(GmSolve* S, int G) {
@@ -1288,6 +1349,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   std::vector<char> chain_il;          // chain group runs the interleaved path in run mode
   std::vector<DBuf<double>> il_bufs;   // two [n][MB] buffers per chain group (empty if not il)
   bool any_plain_chain = true, any_plain_op_run = true, any_plain_op_asm = true;
+  bool il2 = false;  // RHS-split interleaved SpMVs
   if (!std::getenv("MPG_NO_MULTI")) {
     std::vector<int> used(size_t(ns), 0);
     for (int i = 0; i < ns; ++i) {
@@ -1309,6 +1371,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     }
     // interleaved path: chain groups of real shifts on one operator side
     const bool il_on = !std::getenv("MPG_NO_IL");
+    il2 = std::getenv("MPG_IL_NNZSPLIT") == nullptr;  // RHS split measured faster (C3: 256 -> 221 ms / 348 its)
     std::vector<int> in_il(size_t(ns), 0);
     for (size_t gi = 0; gi < chain_groups.size(); ++gi) {
       const Group& g = chain_groups[gi];
@@ -1370,6 +1433,13 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         }
         const double* xin = (stage & 1) ? xb : xa;
         double* xout = (stage & 1) ? xa : xb;
+        if (il2) {
+          k_spmv_il2<E_IDENT, true><<<cdiv(f.nrows * 4, 256), 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), opn,
+                                                                         xin, xout);
+          ++launches_per_iter;
+          mark(PK_CHAIN);
+          continue;
+        }
         switch (Vf) {
           case 2: k_chain_il<2><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), xin, xout); break;
           case 4: k_chain_il<4><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), xin, xout); break;
@@ -1412,6 +1482,18 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         const int nst = int(chain_of_group[gi]->factors.size());
         const double* xin = ((nst - 1) & 1) ? il_bufs[2 * gi].get() : il_bufs[2 * gi + 1].get();
         const unsigned grid1 = cdiv(nb * int64_t(Vop), 256);
+        if (il2) {
+          const CsrView none{};
+          const unsigned g2 = cdiv(nb * 4, 256);
+          switch (op.emode) {
+            case E_IDENT: k_spmv_il2<E_IDENT, false><<<g2, 256, 0, s>>>(dS.get(), g, none, ov, xin, nullptr); break;
+            case E_DIAG: k_spmv_il2<E_DIAG, false><<<g2, 256, 0, s>>>(dS.get(), g, none, ov, xin, nullptr); break;
+            default: k_spmv_il2<E_SAMEPAT, false><<<g2, 256, 0, s>>>(dS.get(), g, none, ov, xin, nullptr); break;
+          }
+          ++launches_per_iter;
+          mark(PK_OP);
+          continue;
+        }
 #define MPG_OPI(VV)                                                                                            \
   switch (op.emode) {                                                                                          \
     case E_IDENT: k_op_il<VV, E_IDENT><<<grid1, 256, 0, s>>>(dS.get(), g, ov, xin); break;                    \
