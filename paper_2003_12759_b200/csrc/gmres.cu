@@ -895,6 +895,100 @@ __global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, in
   gc_cluster_sync<CL>();  // peers may still read this CTA's row partials
 }
 
+// ---- measured second pass, persistent (gmres.cpp:108-119) ------------------------
+// w <- w - sum_j s_j d_j W_j and ||w||^2 for the solves whose probe asked for it
+// (||d|| > 1e-10 ||w||). The tiles (2048 rows, two per thread) of those solves
+// form one list split over one 1024-thread CTA per SM, so the pass keeps every
+// SM streaming (~128 KB of loads in flight) however many solves need it; the
+// others skip. Slot b writes part[k+1][b] for every such solve (0 if it owned
+// no tile), which k_finalize sums.
+constexpr int RO_THREADS = 1024;
+constexpr int RO_ROWS = 2 * RO_THREADS;
+
+__global__ void __launch_bounds__(RO_THREADS, 1) k_reorth_p(GmSolve* S, int ns, int G) {
+  extern __shared__ __align__(16) double smr[];
+  double* coef = smr;
+  const double** vp = reinterpret_cast<const double**>(smr + UP_MAXCOLS);
+  double* red = smr + 2 * UP_MAXCOLS;               // 32
+  int* need = reinterpret_cast<int*>(red + 32);     // ns flags
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int s = warp; s < ns; s += RO_THREADS / 32) {
+    const GmSolve& st = S[s];
+    int f = 0;
+    if (st.phase == PH_RUN) {
+      double dn = 0.0;
+      for (int j = lane; j <= st.k; j += 32) dn = fma(st.d[j], st.d[j], dn);
+      dn = warp_sum(dn);
+      f = st.w2_a > 0.0 && dn > 1e-20 * st.w2_a;
+    }
+    if (lane == 0) need[s] = f;
+  }
+  __syncthreads();
+  long long total = 0;
+  for (int s = 0; s < ns; ++s)
+    if (need[s]) total += (S[s].n + RO_ROWS - 1) / RO_ROWS;
+  if (total == 0) return;
+  const long long per = (total + gridDim.x - 1) / gridDim.x;
+  const long long a = per * blockIdx.x, b = min(total, a + per);
+  long long off = 0;
+  for (int s = 0; s < ns; ++s) {
+    if (!need[s]) continue;
+    GmSolve& st = S[s];
+    const int n = st.n, k = st.k, nj = k + 1;
+    const int nt = (n + RO_ROWS - 1) / RO_ROWS;
+    const long long lo = a > off ? a : off, hi = b < off + nt ? b : off + nt;
+    off += nt;
+    double wsq = 0.0;
+    if (lo < hi) {
+      __syncthreads();
+      for (int j = tid; j < nj; j += RO_THREADS) {
+        coef[j] = st.scale[j] * st.d[j];
+        vp[j] = st.V[j];
+      }
+      __syncthreads();
+      double* w = st.V[k + 1];
+      for (long long t = lo - (off - nt); t < hi - (off - nt); ++t) {
+        const int r = int(t) * RO_ROWS + 2 * tid;
+        if (r + 1 < n) {
+          double2 acc = *reinterpret_cast<const double2*>(w + r);
+          int j = 0;
+          for (; j + 8 <= nj; j += 8) {
+            double2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(vp[j + u] + r));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              acc.x = fma(-coef[j + u], v[u].x, acc.x);
+              acc.y = fma(-coef[j + u], v[u].y, acc.y);
+            }
+          }
+          for (; j < nj; ++j) {
+            const double2 v = __ldcs(reinterpret_cast<const double2*>(vp[j] + r));
+            acc.x = fma(-coef[j], v.x, acc.x);
+            acc.y = fma(-coef[j], v.y, acc.y);
+          }
+          *reinterpret_cast<double2*>(w + r) = acc;
+          wsq = fma(acc.x, acc.x, fma(acc.y, acc.y, wsq));
+        } else if (r < n) {
+          double x = w[r];
+          for (int j = 0; j < nj; ++j) x = fma(-coef[j], vp[j][r], x);
+          w[r] = x;
+          wsq = fma(x, x, wsq);
+        }
+      }
+    }
+    wsq = warp_sum(wsq);
+    __syncthreads();
+    if (lane == 0) red[warp] = wsq;
+    __syncthreads();
+    if (tid == 0) {
+      double x = 0.0;
+      for (int i = 0; i < RO_THREADS / 32; ++i) x += red[i];
+      st.part[size_t(nj) * G + blockIdx.x] = x;
+    }
+  }
+}
+
 // ---- norm partials of the residual buffer ----------------------------------------
 __global__ void __launch_bounds__(256) k_rnorm(GmSolve* S, int G) {
   GmSolve& st = S[blockIdx.y];
@@ -1204,7 +1298,8 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   const int ntiles = int(cdiv(nmax, DOT_TILE));
   const GcConfig gc_dot = gc_config(dev, c.sm_count, false), gc_upd = gc_config(dev, c.sm_count, true);
   // partial-sum slots per solve: the dot/update grids, and one per GS cluster
-  const int G = std::max(std::max(gc_dot.ncl, gc_upd.ncl),
+  // (>= sm_count: the persistent second pass writes one slot per SM)
+  const int G = std::max(std::max(std::max(gc_dot.ncl, gc_upd.ncl), c.sm_count),
                          std::max(1, std::min(ntiles, std::max(8, (c.sm_count * 8) / ns))));
 
   std::vector<SolveHost> sh(static_cast<size_t>(ns));
@@ -1337,8 +1432,10 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     cudaFuncSetAttribute(k_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_reorth_p, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
   const bool fused = maxit + 1 <= UP_MAXCOLS && !std::getenv("MPG_NO_FUSE");
+  const size_t smem_ro = size_t(2 * UP_MAXCOLS + 32) * sizeof(double) + size_t(ns) * sizeof(int);
   int launches_per_iter = 0;
   // Profiling hook: called after every launch with a kernel-class id.
   std::function<void(int)> mark = [](int) {};
@@ -1574,9 +1671,13 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     }
     k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 1, fused ? gc_upd.ncl : G);
     mark(PK_SMALL);
-    k_update<<<gG, 256, smem_upd, s>>>(dS.get(), G, 1);
+    if (fused) {
+      k_reorth_p<<<unsigned(c.sm_count), RO_THREADS, smem_ro, s>>>(dS.get(), ns, G);
+    } else {
+      k_update<<<gG, 256, smem_upd, s>>>(dS.get(), G, 1);
+    }
     mark(PK_REORTH);
-    k_finalize<<<unsigned(ns), 32, 0, s>>>(dS.get(), G, G);
+    k_finalize<<<unsigned(ns), 32, 0, s>>>(dS.get(), G, fused ? c.sm_count : G);
     mark(PK_SMALL);
     k_backsub<<<unsigned(ns), 256, size_t(maxit + 2) * sizeof(double), s>>>(dS.get());
     mark(PK_ASM);
