@@ -97,6 +97,18 @@ def byte_model(n: int, nnz_a: int, nnz_e_extra: int, nnz_p: list, iters: list) -
     return tot
 
 
+def traffic_per_launch(kernel: str, algorithmic_per_launch: float):
+    """DRAM bytes (read + write) per launch of `kernel`: the algorithmic bytes
+    scaled by dram/algorithmic of one `ncu --set full` capture of that kernel
+    (profiles/r01/traffic.json); None when no capture exists for it."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
+            k = json.load(f)["kernels"][kernel]
+        return round(algorithmic_per_launch * (k["dram_read"] + k["dram_write"]) / k["algorithmic"])
+    except Exception:
+        return None
+
+
 def build_workload(args, device: int):
     import paper_2003_12759_b200 as mpg
     from paper_2003_12759_b200 import gen
@@ -211,6 +223,7 @@ def run_ours(args, rank: int, world: int, device: int):
     dom = max((k for k in prof if prof[k]["bytes"] > 0), key=lambda k: prof[k]["ms"])
     dom_gbs = prof[dom]["bytes"] / (prof[dom]["ms"] / 1e3) / 1e9
     dom_bytes_per_launch = prof[dom]["bytes"] / max(prof[dom]["launches"], 1)
+    traffic = traffic_per_launch(dom, dom_bytes_per_launch)
     result = {
         "metric": METRIC,
         "value": round(value, 4),
@@ -233,7 +246,7 @@ def run_ours(args, rank: int, world: int, device: int):
                 "d2h_bytes_per_step": nsolves * n * 8, "ms_per_step": round(e2e_ms, 3)},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": round(dom_gbs, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(dom_gbs / peak, 4), "traffic": None, "kernel": dom,
+                     "frac": round(dom_gbs / peak, 4), "traffic": traffic, "kernel": dom,
                      "bytes_per_launch": round(dom_bytes_per_launch), "peak_kind": peak_kind,
                      "step": {"achieved": round(achieved, 1), "frac": round(achieved / peak, 4),
                               "bytes_per_step": bytes_step,

@@ -843,7 +843,9 @@ __device__ __forceinline__ int gc_tiles(const GmSolve& st, int CL) {
   return (st.n + T - 1) / T;
 }
 
-// Update + probe with clusters (measured, C3, k + 1 <= 335): a cluster barrier
+// Update + probe variants measured on C3 (k + 1 <= 335): three register buffers
+// of 6 vectors instead of two of 8 (4.4 TB/s: memory-level parallelism is not
+// what limits it); with clusters: a cluster barrier
 // per tile for the row sums gives 3.3 / 2.7 TB/s for pairs / quads (the
 // barrier's release waits for the in-flight loads of the next tile); a version
 // that sends the row partials with st.async + mbarriers and defers the probe by
@@ -1052,13 +1054,16 @@ __global__ void k_finalize(GmSolve* S, int G, int cnt2) {
   const bool invariant = wnorm <= 1e-14 * fmax(wnorm_pre, 1e-300);
   double* h = st.h;
   h[k + 1] = invariant ? 0.0 : wnorm;
+  // previous rotations (gmres.cpp:125-134); the rotated entry is carried in a
+  // register so only the independent loads sit on the loop
+  double hi = h[0];
+#pragma unroll 4
   for (int i = 0; i < k; ++i) {
-    const double c = st.cs[i], s = st.sn[i];
-    const double t1 = c * h[i] + s * h[i + 1];
-    const double t2 = -s * h[i] + c * h[i + 1];
-    h[i] = t1;
-    h[i + 1] = t2;
+    const double c = st.cs[i], s = st.sn[i], hn = h[i + 1];
+    h[i] = c * hi + s * hn;
+    hi = -s * hi + c * hn;
   }
+  h[k] = hi;
   const double diag = h[k], sub = h[k + 1];
   if (diag == 0.0 && sub == 0.0) {
     st.breakdown = 1;

@@ -15,7 +15,11 @@
 // CSR of P^T (column lists) and transposed on the device.
 //
 // Lanes own rows (i = lane mod 32) of the dense block, which lives in a
-// per-warp workspace in global memory (L1/L2 resident).
+// per-warp workspace in global memory (L1/L2 resident). The phase functions
+// are kept out of line: inlined twice (first solve + augmentation sweeps) the
+// kernel was 200 KB of SASS and stalled on instruction fetch (ncu:
+// no_instructions 47 % of samples); out of line it also needs 72 instead of
+// 128 registers, so more warps hide the workspace latency (C3 2.5 -> 1.7 s).
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -85,7 +89,7 @@ __device__ int lower_bound_i(const int* a, int n, int x) {
 }
 
 // Sorted unique union of the rows of A(:, J) into I; returns |I|.
-__device__ int build_rows(const SpaiParams& P, const WarpWS& w, int np, int lane) {
+__device__ __noinline__ int build_rows(const SpaiParams& P, const WarpWS& w, int np, int lane) {
   int total = 0;
   for (int c = 0; c < np; ++c) {
     const int j = w.J[c];
@@ -120,7 +124,7 @@ __device__ int build_rows(const SpaiParams& P, const WarpWS& w, int np, int lane
 }
 
 // Dense block A(I, J) column-major (ld = m) and the restricted right-hand side.
-__device__ void gather(const SpaiParams& P, const WarpWS& w, int np, int m, const int* rr, const double* rv, int rn,
+__device__ __noinline__ void gather(const SpaiParams& P, const WarpWS& w, int np, int m, const int* rr, const double* rv, int rn,
                        double& outside_sq, int lane) {
   for (int i = lane; i < m * np; i += 32) w.D[i] = 0.0;
   for (int i = lane; i < m; i += 32) w.rhsl[i] = 0.0;
@@ -145,7 +149,7 @@ __device__ void gather(const SpaiParams& P, const WarpWS& w, int np, int m, cons
 
 // Householder QR with column pivoting (Eigen ColPivHouseholderQR) and solve.
 // Returns rank_deficient; coefficients (in pattern order) in w.coef.
-__device__ bool qr_solve(const WarpWS& w, int m, int p, int lane) {
+__device__ __noinline__ bool qr_solve(const WarpWS& w, int m, int p, int lane) {
   double* D = w.D;
   const int size = min(m, p);
   double maxnorm = 0.0;
@@ -309,7 +313,7 @@ __device__ bool qr_solve(const WarpWS& w, int m, int p, int lane) {
 }
 
 // Residual over I (into w.resid[0..m)); returns ||rhs - A q||^2 on I.
-__device__ double residual_on_I(const SpaiParams& P, const WarpWS& w, int np, int m, const int* rr, const double* rv,
+__device__ __noinline__ double residual_on_I(const SpaiParams& P, const WarpWS& w, int np, int m, const int* rr, const double* rv,
                                 int rn, int lane) {
   for (int i = lane; i < m; i += 32) w.resid[i] = 0.0;
   __syncwarp();
@@ -654,7 +658,15 @@ SpaiOutcome spai_or_update(const CsrPtr& a, const CsrPtr& prev, const SpaiOption
   P.ws_ints = (3 * size_t(PMAX) + 2 * size_t(IMAX) + SORTN + 3) & ~size_t(3);
   // persistent grid, bounded by the workspace budget
   const size_t per_warp = P.ws_doubles * 8 + P.ws_ints * 4;
-  int warps = c.sm_count * 16;
+  // as many resident warps as the registers allow (the build is latency-bound:
+  // C3 1.9 s at 16 warps/SM, 1.7 s at 28); MPG_SPAI_WPS overrides
+  int bps = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_spai, 128, 0) != cudaSuccess || bps < 1) {
+    cudaGetLastError();
+    bps = 4;
+  }
+  const int wps = std::getenv("MPG_SPAI_WPS") ? std::max(1, std::atoi(std::getenv("MPG_SPAI_WPS"))) : 4 * bps;
+  int warps = c.sm_count * wps;
   const size_t budget = size_t(8) << 30;
   while (warps > c.sm_count && size_t(warps) * per_warp > budget) warps /= 2;
   warps = std::max(warps - warps % 4, 4);
