@@ -32,12 +32,16 @@ constexpr int ASM_RECHECK = 1, ASM_FINISH = 2;
 constexpr int DOT_TILE = 1024;   // rows per tile of the dot kernel
 constexpr int UPD_TILE = 512;    // rows per tile of the update kernel (256 threads x double2)
 constexpr int PANEL = 64;        // basis vectors per allocation panel
-// Row index of a basis vector. Basis vectors are plain contiguous vectors in
-// 64-vector panels. (A chunk-major panel layout, [n/8][64][8], that lets one
-// TMA bulk copy stage the 8-row slab of a whole panel was measured too: its
-// gathers slowed the SpMVs by ~25 % and a TMA-ring Gram-Schmidt kernel built on
-// it reached only 1.3-2.4 TB/s, so the flat layout stays.)
-__host__ __device__ __forceinline__ int vidx(int r) { return r; }
+// Basis layout: 64-vector panels stored chunk-major, [ld / CHUNK][64][CHUNK]:
+// the CHUNK = 16 rows (128 B) of the 64 vectors of a panel form one contiguous
+// 8 KB block. The Gram-Schmidt passes walk tiles of T rows x (k+1) vectors;
+// with plain vectors a tile touches k+1 distinct 2 MB pages (one per vector)
+// and ran at 4.6 TB/s for 16-row tiles, chunk-major it touches ceil((k+1)/64)
+// contiguous blocks (scripts/membench.cu: 5.8-6.6 TB/s for the same walk).
+// V[j] points at the vector's first chunk (panel + (j % 64) * CHUNK); row r of
+// it is V[j][vidx(r)]. Pairs of rows (r even) are contiguous.
+constexpr int CHUNK = 16;
+__host__ __device__ __forceinline__ int vidx(int r) { return (r / CHUNK) * (PANEL * CHUNK) + (r % CHUNK); }
 
 struct GmSolve {
   // configuration
@@ -205,6 +209,7 @@ struct Group { int idx[MB]; int cnt; };
 
 template <int V>
 __global__ void __launch_bounds__(256) k_chain_multi(GmSolve* S, Group grp, CsrView f, int stage, int mode) {
+  const bool basis = stage == 0 && mode == 0;  // reading V[k] (chunk-major)
   const double* src[MB];
   double* dst[MB];
   bool act[MB];
@@ -236,7 +241,7 @@ __global__ void __launch_bounds__(256) k_chain_multi(GmSolve* S, Group grp, CsrV
       const int c = __ldcs(f.colind + k);
 #pragma unroll
       for (int q = 0; q < MB; ++q)
-        if (act[q]) acc[q] = fma(a, __ldg(src[q] + c), acc[q]);
+        if (act[q]) acc[q] = fma(a, __ldg(src[q] + (basis ? vidx(c) : c)), acc[q]);
     }
   }
 #pragma unroll
@@ -251,17 +256,20 @@ __global__ void __launch_bounds__(256) k_chain_multi(GmSolve* S, Group grp, CsrV
 template <int V, int EM>
 __global__ void __launch_bounds__(256) k_iter_op_multi(GmSolve* S, Group grp, OpView op, int mode) {
   const double* xs[MB];
+  bool xb[MB];  // x is the basis vector V[k] (no chain)
   bool act[MB];
   bool any = false;
 #pragma unroll
   for (int q = 0; q < MB; ++q) {
     act[q] = false;
     xs[q] = nullptr;
+    xb[q] = false;
     if (q < grp.cnt) {
       const GmSolve& st = S[grp.idx[q]];
       act[q] = mode == 0 ? st.phase == PH_RUN : st.phase == PH_ASM;
       if (mode == 0) xs[q] = st.stages ? ((st.stages - 1) & 1 ? st.z1 : st.z0) : st.V[st.k];
       else xs[q] = st.stages ? ((st.stages - 1) & 1 ? st.z1 : st.z0) : st.ubuf;
+      xb[q] = mode == 0 && st.stages == 0;
       any |= act[q];
     }
   }
@@ -282,7 +290,7 @@ __global__ void __launch_bounds__(256) k_iter_op_multi(GmSolve* S, Group grp, Op
 #pragma unroll
         for (int q = 0; q < MB; ++q)
           if (act[q]) {
-            const double xv = __ldg(xs[q] + c);
+            const double xv = __ldg(xs[q] + (xb[q] ? vidx(c) : c));
             a1[q] = fma(ae.x, xv, a1[q]);
             e1[q] = fma(ae.y, xv, e1[q]);
           }
@@ -290,7 +298,7 @@ __global__ void __launch_bounds__(256) k_iter_op_multi(GmSolve* S, Group grp, Op
         const double av = __ldcs(op.a.val + k);
 #pragma unroll
         for (int q = 0; q < MB; ++q)
-          if (act[q]) a1[q] = fma(av, __ldg(xs[q] + c), a1[q]);
+          if (act[q]) a1[q] = fma(av, __ldg(xs[q] + (xb[q] ? vidx(c) : c)), a1[q]);
       }
     }
   }
@@ -305,11 +313,12 @@ __global__ void __launch_bounds__(256) k_iter_op_multi(GmSolve* S, Group grp, Op
       if (!act[q]) continue;
       GmSolve& st = S[grp.idx[q]];
       double ex = e1[q];
-      if (EM == E_IDENT) ex = xs[q][row];
-      else if (EM == E_DIAG) ex = op.ediag[row] * xs[q][row];
+      const int xr = xb[q] ? vidx(row) : row;
+      if (EM == E_IDENT) ex = xs[q][xr];
+      else if (EM == E_DIAG) ex = op.ediag[row] * xs[q][xr];
       const double y1 = st.sre * ex + st.ca * a1[q];
-      if (mode == 0) st.V[st.k + 1][row] = st.scale[st.k] * y1;
-      else st.rbuf[row] = st.V[0][row] - y1;
+      if (mode == 0) st.V[st.k + 1][vidx(row)] = st.scale[st.k] * y1;
+      else st.rbuf[row] = st.V[0][vidx(row)] - y1;
     }
   }
 }
@@ -328,7 +337,7 @@ __global__ void __launch_bounds__(256) k_pack_il(GmSolve* S, Group grp, double* 
   double v = 0.0;
   if (q < grp.cnt) {
     const GmSolve& st = S[grp.idx[q]];
-    if (st.phase == PH_RUN) v = st.V[st.k][row];
+    if (st.phase == PH_RUN) v = st.V[st.k][vidx(row)];
   }
   xa[i] = v;
 }
@@ -421,7 +430,7 @@ __global__ void __launch_bounds__(256) k_op_il(GmSolve* S, Group grp, OpView op,
     double ex = e1[q];
     if (EM == E_IDENT) ex = xin[size_t(row) * MB + q];
     else if (EM == E_DIAG) ex = op.ediag[row] * xin[size_t(row) * MB + q];
-    st.V[st.k + 1][row] = st.scale[st.k] * (st.sre * ex + st.ca * a1[q]);
+    st.V[st.k + 1][vidx(row)] = st.scale[st.k] * (st.sre * ex + st.ca * a1[q]);
   }
 }
 
@@ -482,7 +491,7 @@ __global__ void __launch_bounds__(256) k_spmv_il2(GmSolve* S, Group grp, CsrView
     if (q >= grp.cnt) continue;
     GmSolve& st = S[grp.idx[q]];
     if (st.phase != PH_RUN) continue;
-    st.V[st.k + 1][row] = st.scale[st.k] * (st.sre * (h ? e1 : e0) + st.ca * (h ? a1 : a0));
+    st.V[st.k + 1][vidx(row)] = st.scale[st.k] * (st.sre * (h ? e1 : e0) + st.ca * (h ? a1 : a0));
   }
 }
 
@@ -721,13 +730,13 @@ __device__ __forceinline__ void gc_body(GmSolve& st, int G, int slot, int q, int
     const bool inb = t < tb && row < ld;
 #pragma unroll
     for (int c = 0; c < GC_CPT; ++c)
-      v[c] = (c < ncol_me && inb) ? __ldcs(reinterpret_cast<const double2*>(vp[cg + CG * c] + row))
+      v[c] = (c < ncol_me && inb) ? __ldcs(reinterpret_cast<const double2*>(vp[cg + CG * c] + vidx(row)))
                                   : make_double2(0.0, 0.0);
     if (UPDATE) {
       const int rw = t * T + my_row;
-      wp = (t < tb && sub == 0 && my_row < T && rw < n) ? w[rw] : 0.0;
+      wp = (t < tb && sub == 0 && my_row < T && rw < n) ? w[vidx(rw)] : 0.0;
     } else {
-      w2 = inb ? *reinterpret_cast<const double2*>(w + row) : make_double2(0.0, 0.0);
+      w2 = inb ? *reinterpret_cast<const double2*>(w + vidx(row)) : make_double2(0.0, 0.0);
     }
   };
   auto consume = [&](int t, const double2* v, double2 w2, double wpre, int par) {
@@ -766,7 +775,7 @@ __device__ __forceinline__ void gc_body(GmSolve& st, int G, int slot, int q, int
         const int rw = t * T + my_row;
         const bool valid = rw < n;
         const double wv = valid ? wpre - sacc : 0.0;
-        if (valid && q == 0) w[rw] = wv;
+        if (valid && q == 0) w[vidx(rw)] = wv;
         wb[my_row] = wv;
         if (q == 0) wsq = fma(wv, wv, wsq);
       }
@@ -952,12 +961,13 @@ __global__ void __launch_bounds__(RO_THREADS, 1) k_reorth_p(GmSolve* S, int ns, 
       for (long long t = lo - (off - nt); t < hi - (off - nt); ++t) {
         const int r = int(t) * RO_ROWS + 2 * tid;
         if (r + 1 < n) {
-          double2 acc = *reinterpret_cast<const double2*>(w + r);
+          const int vr = vidx(r);
+          double2 acc = *reinterpret_cast<const double2*>(w + vr);
           int j = 0;
           for (; j + 8 <= nj; j += 8) {
             double2 v[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(vp[j + u] + r));
+            for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const double2*>(vp[j + u] + vr));
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               acc.x = fma(-coef[j + u], v[u].x, acc.x);
@@ -965,16 +975,17 @@ __global__ void __launch_bounds__(RO_THREADS, 1) k_reorth_p(GmSolve* S, int ns, 
             }
           }
           for (; j < nj; ++j) {
-            const double2 v = __ldcs(reinterpret_cast<const double2*>(vp[j] + r));
+            const double2 v = __ldcs(reinterpret_cast<const double2*>(vp[j] + vr));
             acc.x = fma(-coef[j], v.x, acc.x);
             acc.y = fma(-coef[j], v.y, acc.y);
           }
-          *reinterpret_cast<double2*>(w + r) = acc;
+          *reinterpret_cast<double2*>(w + vr) = acc;
           wsq = fma(acc.x, acc.x, fma(acc.y, acc.y, wsq));
         } else if (r < n) {
-          double x = w[r];
-          for (int j = 0; j < nj; ++j) x = fma(-coef[j], vp[j][r], x);
-          w[r] = x;
+          const int vr = vidx(r);
+          double x = w[vr];
+          for (int j = 0; j < nj; ++j) x = fma(-coef[j], vp[j][vr], x);
+          w[vr] = x;
           wsq = fma(x, x, wsq);
         }
       }
@@ -1234,11 +1245,13 @@ int gc_max_clusters(int sm_count) {
 }
 
 // Cluster size and clusters per launch of one Gram-Schmidt pass. Measured on
-// C3 (k + 1 up to 335): the projection pass is fastest with pairs (6.3 TB/s:
-// 256-512 B per vector per tile), the update + probe pass without clusters
-// (4.7 TB/s; the per-tile cluster barrier of its row sums costs more than the
-// longer segments gain). MPG_GS_CLUSTER_DOT / MPG_GS_CLUSTER_UPD override
-// (1, 2 or 4; smaller clusters are used when the device cannot co-schedule).
+// C3 (k + 1 up to 335): with the plain-vector basis the projection pass was
+// fastest with CTA pairs (6.3 TB/s vs 5.7), with the chunk-major basis
+// unclustered (6.57 TB/s vs 6.12 for pairs); the update + probe pass is
+// fastest unclustered either way (4.8 TB/s; the per-tile exchange of its row
+// sums costs more than the longer tiles gain). MPG_GS_CLUSTER_DOT /
+// MPG_GS_CLUSTER_UPD override (1, 2 or 4; smaller clusters are used when the
+// device cannot co-schedule).
 struct GcConfig {
   int cl = 1, ncl = 1;
 };
@@ -1249,7 +1262,7 @@ GcConfig gc_config(int dev, int sm_count, bool update) {
   std::lock_guard<std::mutex> lk(mu);
   if (dev >= 0 && dev < 64 && have[update][dev]) return cache[update][dev];
   const char* e = std::getenv(update ? "MPG_GS_CLUSTER_UPD" : "MPG_GS_CLUSTER_DOT");
-  int want = e ? std::atoi(e) : (update ? 1 : 2);
+  int want = e ? std::atoi(e) : 1;
   GcConfig g;
   if (want >= 4 && (g.ncl = gc_max_clusters<4>(sm_count)) > 0) g.cl = 4;
   else if (want >= 2 && (g.ncl = gc_max_clusters<2>(sm_count)) > 0) g.cl = 2;
@@ -1398,7 +1411,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       // padding rows are read (as zeros) by the Gram-Schmidt tiles
       MPG_CUDA(cudaMemsetAsync(base, 0, size_t(PANEL) * size_t(H.ld) * sizeof(double), s));
       const int p0 = int(H.panels.size() - 1) * PANEL;
-      for (int j = 0; j < PANEL && p0 + j < maxit + 2; ++j) H.vtab[size_t(p0 + j)] = base + size_t(j) * size_t(H.ld);
+      for (int j = 0; j < PANEL && p0 + j < maxit + 2; ++j) H.vtab[size_t(p0 + j)] = base + size_t(j) * CHUNK;
     }
     if (upto > H.uploaded) {
       MPG_CUDA(cudaMemcpyAsync(H.dV.get() + H.uploaded, H.vtab.data() + H.uploaded,

@@ -47,6 +47,82 @@ __global__ void __launch_bounds__(512, 1) k_tile(const double* __restrict__ V, i
   if (acc == 12345.678) out[0] = acc;
 }
 
+// Same walk on a chunk-major layout [n / T][nv][T]: the tile of every vector is
+// one contiguous nv x T x 8-byte block.
+template <int RG, int CPT>
+__global__ void __launch_bounds__(512, 1) k_tile_cm(const double* __restrict__ V, int nv, int ld, int n, double* out) {
+  constexpr int CG = 512 / RG, T = 2 * RG;
+  const int rg = threadIdx.x % RG, cg = threadIdx.x / RG;
+  const int ncol = nv > cg ? min(CPT, (nv - cg + CG - 1) / CG) : 0;
+  const int ntl = (n + T - 1) / T;
+  double acc = 0.0;
+  double2 a[CPT], b[CPT];
+  auto load = [&](int t, double2* v) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+      v[c] = (c < ncol && t < ntl) ? __ldcs(reinterpret_cast<const double2*>(V + (size_t(t) * nv + cg + CG * c) * T + 2 * rg))
+                                   : make_double2(0, 0);
+  };
+  auto use = [&](const double2* v) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) acc += v[c].x * 1.0000001 + v[c].y;
+  };
+  int t = blockIdx.x;
+  load(t, a);
+  while (t < ntl) {
+    load(t + gridDim.x, b);
+    use(a);
+    t += gridDim.x;
+    if (t >= ntl) break;
+    load(t + gridDim.x, a);
+    use(b);
+    t += gridDim.x;
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+
+// CTA pairs (cluster of 2) walking adjacent T-row tiles in lockstep: a relaxed
+// cluster barrier per tile keeps the two SMs' requests to neighbouring
+// segments of each vector together in time (no data exchanged).
+template <int RG, int CPT, int SYNC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
+    k_tile_pair(const double* __restrict__ V, int nv, int ld, int n, double* out) {
+  constexpr int CG = 512 / RG, T = 2 * RG;
+  const int rg = threadIdx.x % RG, cg = threadIdx.x / RG;
+  const int q = blockIdx.x & 1, pr = blockIdx.x >> 1, npr = gridDim.x >> 1;
+  const int ncol = nv > cg ? min(CPT, (nv - cg + CG - 1) / CG) : 0;
+  const int nst = (n + 2 * T - 1) / (2 * T);
+  double acc = 0.0;
+  double2 a[CPT], b[CPT];
+  auto load = [&](int st, double2* v) {
+    const int row = st * 2 * T + q * T + 2 * rg;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+      v[c] = (c < ncol && st < nst && row < ld) ? __ldcs(reinterpret_cast<const double2*>(V + size_t(cg + CG * c) * ld + row))
+                                               : make_double2(0, 0);
+  };
+  auto use = [&](const double2* v) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) acc += v[c].x * 1.0000001 + v[c].y;
+    if (SYNC) {
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+      asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+    }
+  };
+  int st = pr;
+  load(st, a);
+  while (st < nst) {  // same trip count in both CTAs of the pair
+    load(st + npr, b);
+    use(a);
+    st += npr;
+    if (st >= nst) break;
+    load(st + npr, a);
+    use(b);
+    st += npr;
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+
 template <int U>
 __global__ void __launch_bounds__(256) k_rowthr(const double* __restrict__ V, int nv, int ld, int n, double* out) {
   const int r = 2 * (blockIdx.x * 256 + threadIdx.x);
@@ -134,6 +210,16 @@ int main(int argc, char** argv) {
   if (nv <= 512 / 4 * 4) { TILE(4, 4, 0); }
   if (nv <= 512 / 4 * 16) { TILE(4, 16, 0); }
   if (nv <= 512 / 2 * 8) { TILE(2, 8, 0); }
+  if (nv <= 512) {
+    snprintf(nm, sizeof nm, "chunk-major RG=8 CPT=8");
+    timeit(nm, [&] { k_tile_cm<8, 8><<<sms, 512>>>(V, nv, ld, n, out); });
+    snprintf(nm, sizeof nm, "chunk-major RG=4 CPT=8");
+    timeit(nm, [&] { k_tile_cm<4, 8><<<sms, 512>>>(V, nv, ld, n, out); });
+  }
+  snprintf(nm, sizeof nm, "pair RG=8 CPT=8 sync=1");
+  timeit(nm, [&] { k_tile_pair<8, 8, 1><<<sms / 2 * 2, 512>>>(V, nv, ld, n, out); });
+  snprintf(nm, sizeof nm, "pair RG=8 CPT=8 sync=0");
+  timeit(nm, [&] { k_tile_pair<8, 8, 0><<<sms / 2 * 2, 512>>>(V, nv, ld, n, out); });
   snprintf(nm, sizeof nm, "rowthr U=4");
   timeit(nm, [&] { k_rowthr<4><<<(n / 2 + 255) / 256, 256>>>(V, nv, ld, n, out); });
   snprintf(nm, sizeof nm, "rowthr U=8");
