@@ -117,3 +117,46 @@ def test_spai_bench_rows_and_parity(mpg, orc, gen):
         assert rel(res.x[i], xo[i]) <= 1e-6
     bad = mpg.run_spai_bench(op, sysm.b[:, 0], pts, gmres=mpg.GmresConfig(1e-6, 3), mode=mpg.PrecondMode.NONE)
     assert bad.failed_solves == 3 and not bad.report.converged
+
+
+def test_spai_bench_zipf_rows_match_oracle(mpg, orc, gen):
+    """C5-type matrix (Zipf(1.8) row lengths up to 300, diagonal E): the shift
+    sweep's SPAI / horizontal updates, solves and failure accounting match the
+    oracle (long rows exercise the SpMV and SPAI load imbalance)."""
+    s = gen.config5(n=3000, nshifts=6, max_len=300)
+    op = mpg.ShiftedOperator(_m(mpg, s.a), _m(mpg, s.e_csr()))
+    pts = [float(x) for x in s.shifts]
+    g = mpg.GmresConfig(1e-8, 1000)
+    res = mpg.run_spai_bench(op, s.b[:, 0], pts, gmres=g, keep_solutions=True)
+    rows, failed, xo = orc.spai_bench(orc.Csr.of(s.a), orc.Csr.of(s.e_csr()), s.b[:, 0], pts,
+                                      gmres=orc.GmresConfig(1e-8, 1000), keep_solutions=True)
+    assert res.failed_solves == failed
+    assert [r.kind for r in res.report.rows] == [
+        {1: "fresh", 2: "horizontal", 3: "vertical", 4: "reused_same_matrix"}.get(r.kind, "none") for r in rows]
+    for i, r in enumerate(rows):
+        assert abs(res.report.rows[i].gmres_iterations - r.iterations) <= max(3, 0.05 * r.iterations)
+        if r.kind != 1:
+            assert abs(res.report.rows[i].min_residual - r.min_residual) <= 1e-8 * max(1.0, r.min_residual)
+            assert abs(res.report.rows[i].matrix_change - r.matrix_change) <= 1e-10 * r.matrix_change
+        if res.report.rows[i].gmres_iterations < 1000:
+            assert rel(res.x[i], xo[i]) <= 1e-6
+
+
+def test_irka_consistent_mass_small_matches_oracle(mpg, orc, gen):
+    """C3-type system (Q1 FEM, E = consistent mass sharing A's pattern) at 8^3
+    nodes, FROZEN reuse with unstable shifts mirrored: shifts within 1e-6 and
+    H_r(i w) within 1e-6 of the oracle."""
+    s = gen.config3(8)
+    r = 4
+    op = mpg.ShiftedOperator(_m(mpg, s.a), _m(mpg, s.e))
+    cfg = mpg.IrkaConfig(r=r, tol=1e-8, max_sweeps=60, seed=1, gmres=mpg.GmresConfig(1e-11, 1000),
+                         mirror_unstable=True)
+    st, rep = mpg.irka_reduce(op, s.b, s.c, cfg, mpg.PrecondMode.REUSE_FROZEN, init_shifts=s.shifts[:r])
+    ocfg = orc.IrkaConfig(r=r, tol=1e-8, max_sweeps=60, seed=1, gmres=orc.GmresConfig(1e-11, 1000),
+                          explicit_nnz_cap=10**12, decoupled=True, mirror_unstable=True)
+    ores = orc.irka_reduce(orc.Csr.of(s.a), orc.Csr.of(s.e), s.b, s.c, ocfg, mode=2, init_shifts=s.shifts[:r])
+    assert rep.converged and ores.converged
+    lg, lo = np.sort_complex(st.lam), np.sort_complex(ores.lam)
+    assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 1e-6
+    ho = np.array([ores.cr.T @ np.linalg.solve(1j * w * np.eye(r) - ores.kr, ores.fr) for w in GRID])
+    assert np.max(np.abs(_hr_grid(st) - ho) / np.abs(ho)) <= 1e-6
