@@ -854,7 +854,9 @@ __device__ __forceinline__ int gc_tiles(const GmSolve& st, int CL) {
 
 // Update + probe variants measured on C3 (k + 1 <= 335): three register buffers
 // of 6 vectors instead of two of 8 (4.4 TB/s: memory-level parallelism is not
-// what limits it); with clusters: a cluster barrier
+// what limits it); one barrier per tile with warp-shuffled row partials and 16
+// broadcast loads per thread instead of the shared-memory row reduction (4.0
+// TB/s: register spills); with clusters: a cluster barrier
 // per tile for the row sums gives 3.3 / 2.7 TB/s for pairs / quads (the
 // barrier's release waits for the in-flight loads of the next tile); a version
 // that sends the row partials with st.async + mbarriers and defers the probe by
