@@ -272,6 +272,7 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
   int sweeps_done = 0;
   const GmresOptions gopt = cfg.gmres;
 
+  int last_max_its = 0;
   for (int z = 1; z <= cfg.max_sweeps && !converged; ++z) {
     host::Spectrum spec;
     if (!host::real_spectrum(kr, spec)) {  // birka.cpp:167-180
@@ -391,11 +392,33 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
     const double avail = double(free_b) + double(reserved - used);
-    const double per_solve = 8.0 * double(2 * n + 64) * double(gopt.max_iter + 8) + 1e7;
-    const int per_batch = std::max(1, std::min<int>(32, int(0.85 * avail / per_solve)));
-    for (size_t b0 = 0; b0 < specs.size(); b0 += size_t(per_batch)) {
-      std::vector<SolveSpec> batch(specs.begin() + long(b0), specs.begin() + long(std::min(specs.size(), b0 + per_batch)));
+    // Basis panels are allocated as a solve grows, so a batch is sized by the
+    // iterations the solves are expected to take (1.5x the previous sweep's
+    // longest solve, 600 for the first sweep), not by max_iter.
+    const int est_its = std::min(gopt.max_iter, z == 1 ? 600 : std::max(128, int(1.5 * double(last_max_its))));
+    // at most 8 solves per batch: measured on C3, one batch of all 16 solves of a
+    // sweep ran 4 % slower per GMRES iteration than batches of 7-8
+    const int max_batch = std::getenv("MPG_IRKA_MAXBATCH") ? std::max(1, std::atoi(std::getenv("MPG_IRKA_MAXBATCH"))) : 8;
+    std::vector<size_t> bounds{0};
+    {
+      double acc = 0.0;
+      for (size_t i = 0; i < specs.size(); ++i) {
+        const double ns_i = specs[i].sim != 0.0 ? 2.0 * double(n) : double(n);
+        const double need = 8.0 * (ns_i + 64.0) * double(est_its + 72) + 1e7;
+        if (i > bounds.back() && (acc + need > 0.85 * avail || int(i - bounds.back()) >= max_batch)) {
+          bounds.push_back(i);
+          acc = 0.0;
+        }
+        acc += need;
+      }
+      bounds.push_back(specs.size());
+    }
+    int sweep_max_its = 0;
+    for (size_t bi = 0; bi + 1 < bounds.size(); ++bi) {
+      const size_t b0 = bounds[bi];
+      std::vector<SolveSpec> batch(specs.begin() + long(b0), specs.begin() + long(bounds[bi + 1]));
       std::vector<GmresOutcome> outc = gmres_batch(op, batch, gopt);
+      for (const GmresOutcome& o : outc) sweep_max_its = std::max(sweep_max_its, o.iterations);
       for (size_t i = 0; i < outc.size(); ++i) {
         mpg_report_row& row = rows[b0 + i];
         row.solves = 1;
@@ -416,6 +439,7 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
       }
     }
     res.rows.insert(res.rows.end(), rows.begin(), rows.end());
+    last_max_its = std::max(last_max_its == 0 ? 0 : last_max_its / 2, sweep_max_its);
     // ---- exchange (K6): all-gather the solved columns ----
     if (world > 1) {
       std::vector<int> owned_cnt(size_t(world), 0);

@@ -45,4 +45,5 @@ print(json.dumps({"config": a.config, "n": int(sysm.n), "nnz": int(sysm.a.nnz), 
                   "solves": tot["solves"], "gmres_iterations": tot["gmres_iterations"],
                   "precond_build_s": round(tot["precond_build_seconds"], 3),
                   "max_its_per_solve": max(r.gmres_iterations for r in rep.rows),
+                  "gmres_s_sum": round(sum(r.gmres_seconds for r in rep.rows), 3),
                   "solves_per_s": round(tot["solves"] / wall, 3)}), flush=True)
