@@ -144,3 +144,43 @@ def test_long_krylov_runs_match_oracle(mpg, orc, gen, n, maxit):
     assert abs(g.report.iterations - ro.iterations) <= max(3, 0.03 * ro.iterations)
     assert np.linalg.norm(d * g.x - b) <= 1e-10 * np.linalg.norm(b)
     assert rel(g.x, xo) <= 1e-6
+
+
+def test_large_batch_with_shared_preconditioners_matches_single(mpg, gen):
+    """24 solves in one batch (more than the 8-wide shared-matrix groups and than
+    SMs per solve): primal/dual sides sharing one frozen SPAI each (interleaved
+    multi-RHS SpMVs), complex pairs, and solves finishing at different
+    iterations; every solve equals its single-solve run."""
+    sysm = gen.config1(N=24)
+    op = mpg.ShiftedOperator(_m(mpg, sysm.a), _m(mpg, sysm.e_csr()))
+    pv = mpg.PrecondChain(mpg.spai_build(op.explicit(0.05, False)).p)
+    pw = mpg.PrecondChain(mpg.spai_build(op.explicit(0.05, True)).p)
+    sig, trs, chains, bs = [], [], [], []
+    for i in range(24):
+        s = float(np.logspace(-2, 2, 24)[i]) + (1j * 3.0 if i % 7 == 3 else 0.0)
+        t = i % 2
+        sig.append(s)
+        trs.append(t)
+        chains.append(None if (i % 7 == 3) else (pw if t else pv))
+        bs.append(np.tile(sysm.b[:, 0] * (1 + 0.1 * i), 2 if complex(s).imag else 1))
+    cfg = mpg.GmresConfig(rel_tol=1e-9)
+    batch = mpg.gmres_batch(op, sig, bs, chains=chains, transposes=trs, cfg=cfg)
+    for s, b, t, ch, r in zip(sig, bs, trs, chains, batch):
+        single = mpg.gmres_shifted(op, s, b, ch, bool(t), cfg)
+        assert r.report.converged and single.report.converged
+        assert abs(r.report.iterations - single.report.iterations) <= 1
+        assert rel(r.x, single.x) <= 1e-8
+
+
+def test_unfused_gram_schmidt_path_beyond_2047_max_iter(mpg, orc, gen):
+    """max_iter > 2047 selects the unfused dot / update kernels; the answer and
+    iteration count still match the oracle."""
+    n = 600
+    d = 1.0 + np.arange(n) ** 1.5
+    h = gen.from_triplets(n, n, np.arange(n), np.arange(n), d)
+    b = gen.random_dense(n, 1, 9)[:, 0]
+    g = mpg.gmres_right_preconditioned(_m(mpg, h), None, b, mpg.GmresConfig(rel_tol=1e-10, max_iter=2100))
+    xo, ro = orc.gmres_csr(orc.Csr.of(h), None, b, orc.GmresConfig(1e-10, 2100))
+    assert g.report.converged and ro.converged
+    assert abs(g.report.iterations - ro.iterations) <= max(3, 0.03 * ro.iterations)
+    assert rel(g.x, xo) <= 1e-6
