@@ -866,8 +866,9 @@ __device__ __forceinline__ int gc_tiles(const GmSolve& st, int CL) {
 // one tile (tile parked in shared memory) reached 3.2 / 2.2 TB/s (shared-memory
 // traffic, mbarrier spinning). Unclustered: 4.7 TB/s -- the default.
 
+// skip_le > 0 (update pass): solves with k + 1 <= skip_le are left to k_gs_tma.
 template <int CL, bool UPDATE>
-__global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, int G) {
+__global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, int G, int skip_le) {
   extern __shared__ __align__(16) double smc[];
   double* coef = smc;
   const double** vp = reinterpret_cast<const double**>(smc + UP_MAXCOLS);
@@ -877,13 +878,13 @@ __global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, in
   const int q = int(blockIdx.x) % CL, slot = int(blockIdx.x) / CL, ncl = int(gridDim.x) / CL;
   long long total = 0;
   for (int s = 0; s < ns; ++s)
-    if (S[s].phase == PH_RUN) total += gc_tiles(S[s], CL);
+    if (S[s].phase == PH_RUN && S[s].k + 1 > skip_le) total += gc_tiles(S[s], CL);
   const long long per = (total + ncl - 1) / ncl;
   const long long a = per * slot, b = min(total, a + per);
   long long off = 0;
   for (int s = 0; s < ns; ++s) {
     GmSolve& st = S[s];
-    if (st.phase != PH_RUN) continue;
+    if (st.phase != PH_RUN || st.k + 1 <= skip_le) continue;
     const int nt = gc_tiles(st, CL);
     const long long lo = a > off ? a : off, hi = b < off + nt ? b : off + nt;
     if (lo < hi) {
@@ -1004,6 +1005,282 @@ __global__ void __launch_bounds__(RO_THREADS, 1) k_reorth_p(GmSolve* S, int ns, 
       for (int i = 0; i < RO_THREADS / 32; ++i) x += red[i];
       st.part[size_t(nj) * G + blockIdx.x] = x;
     }
+  }
+}
+
+// ---- update + probe from TMA-staged tiles (default for k + 1 <= GT_MAXCOLS) ------
+// Same contract as k_gs_clu<CL, true>: w <- w - sum_j s_j h_j W_j, part[j][slot]
+// = W_j . w_new and part[k+1][slot] = ||w_new||^2. The register-tiled kernel has
+// to hold a tile in registers across the barrier that completes its row sums,
+// so its loads in flight stop at every tile (4.7 TB/s). Here the chunk-major
+// basis is streamed with 1-D bulk copies (cp.async.bulk, one per 64-vector panel
+// and chunk: m x 128 contiguous bytes) into a ring of NS shared-memory stages
+// (one mbarrier each), so the copies of the next NS - 1 tiles stay in flight
+// whatever the barriers do. Thread 0 refills a stage right after the tile's
+// barrier: every warp has its elements in registers by then. (A dedicated
+// producer warp makes 9 warps, i.e. 3 on one SM sub-partition, which caps the
+// registers at 168 and spills.)
+// Tile = TC consecutive 16-row chunks x all k + 2 vectors (w = W_{k+1} rides in
+// the copy of the last panel). Warp w takes chunk cc = w / WPC and,
+// within it, vectors j = i CPI + 2 (w % WPC) + (lane >> 4), row lane & 15: each
+// element is read from shared memory once into a register, used for the row
+// sum and, after the one barrier per tile that completes the row sums (row-sum
+// buffers alternate between tiles), for the probe, whose per-vector
+// partials stay in registers until the solve's last tile in this CTA.
+constexpr int GT_CWARPS = 16;                      // warps
+constexpr int GT_CONSUMERS = GT_CWARPS * 32;
+constexpr int GT_THREADS = GT_CONSUMERS;
+constexpr int GT_NI = 12;                          // vector slots per lane
+constexpr int GT_MAXCOLS = GT_NI * 2 * GT_CWARPS;   // largest k + 1 handled (TC = 1)
+constexpr int GT_RING = 26 * 8192;                 // tile ring (bytes)
+constexpr int GT_MAXST = 16;
+constexpr int GT_SMEM = GT_RING + (2 * GT_CWARPS * 16 + GT_MAXCOLS + GT_CWARPS) * 8 + GT_MAXST * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ bool gt_handles(const GmSolve& st) { return st.phase == PH_RUN && st.k + 1 <= GT_MAXCOLS; }
+__device__ __forceinline__ int gt_chunks(const GmSolve& st) { return ((st.n + 31) & ~31) / CHUNK; }
+
+// Tile cursor over the handled solves: tiles [off, off + nt) belong to solve s.
+struct GtCursor {
+  int s = -1, nt = 0;
+  long long off = 0;
+  __device__ __forceinline__ void seek(const GmSolve* S, int ns, int TC, long long g) {
+    while (s < ns && (s < 0 || g >= off + nt)) {
+      if (s >= 0) off += nt;
+      ++s;
+      while (s < ns && !gt_handles(S[s])) ++s;
+      nt = s < ns ? (gt_chunks(S[s]) + TC - 1) / TC : 0;
+    }
+  }
+};
+
+// Stage layout: chunk cc of panel p at doubles (p TC + cc) 1024, [vector][16
+// rows] inside (the last panel's chunks hold only its m vectors), so the
+// offset of a warp's slot i is a compile-time constant plus a per-thread base.
+// Producer state (thread 0): issues tile g into stage stg.
+template <int TC>
+struct GtProducer {
+  GtCursor pc;
+  const double* const* V = nullptr;
+  int nv = 0, nchunks = 0;
+  uint64_t pol = 0;
+  // Called by all 32 lanes of warp 0: lane 0 arms the stage's mbarrier, then
+  // lane l issues copy l (full panels first, then the last panel's chunks).
+  __device__ __forceinline__ void issue(const GmSolve* S, int ns, long long g, int stg, int stage_bytes, char* ring,
+                                        uint64_t* full, int lane) {
+    if (pc.s < 0 || g >= pc.off + pc.nt) {
+      pc.seek(S, ns, TC, g);
+      const GmSolve& st = S[pc.s];
+      V = st.V;
+      nv = st.k + 2;  // basis vectors 0..k and w
+      nchunks = gt_chunks(st);
+    }
+    const int c0 = int(g - pc.off) * TC;
+    const int nch = min(TC, nchunks - c0);
+    const int pf = nv >> 6, m = nv & 63;
+    if (lane == 0) mbar_expect_tx(full + stg, unsigned(nch) * unsigned(nv) * 128u);
+    __syncwarp();
+    char* base = ring + size_t(stg) * size_t(stage_bytes);
+    if (lane < pf) {
+      bulk_g2s(base + size_t(lane) * TC * 8192, V[64 * lane] + size_t(c0) * 1024, unsigned(nch) * 8192u, full + stg,
+               pol);
+    } else if (m && lane < pf + nch) {
+      const int q = lane - pf;
+      bulk_g2s(base + size_t(pf * TC + q) * 8192, V[64 * pf] + size_t(c0 + q) * 1024, unsigned(m) * 128u, full + stg,
+               pol);
+    }
+  }
+};
+
+template <int TC>
+__device__ __forceinline__ void gt_body(GmSolve* S, int ns, int G, int stage_bytes, int NS, long long a, long long b,
+                                        char* ring, uint64_t* full, double* red, double* red2, double* red3) {
+  constexpr int WPC = GT_CWARPS / TC;  // warps per chunk
+  constexpr int CPI = 2 * WPC;         // vectors per slot step
+  constexpr int SPP = 64 / CPI;        // slots per panel
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cc = warp / WPC, wq = warp % WPC, r = lane & 15, par = lane >> 4;
+  const int slot = blockIdx.x;
+  GtProducer<TC> prod;
+  if (warp == 0) {
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(prod.pol));
+    for (long long g = a; g < b && g < a + NS; ++g) prod.issue(S, ns, g, int(g - a), stage_bytes, ring, full, lane);
+  }
+  GtCursor cu;
+  double coef[GT_NI], acc[GT_NI];
+  double wsq = 0.0;
+  double* w = nullptr;
+  GmSolve* st = nullptr;
+  int nj = 0, nchunks = 0, n = 0, woff = 0;
+  const int tbase = cc * 1024 + (2 * wq + par) * 16 + r;
+  long long seg_end = -1;
+  int stg = 0;
+  unsigned phase = 0;
+  for (long long g = a; g < b; ++g) {
+    const long long u = g - a;
+    if (g >= seg_end) {  // first tile of a solve in this CTA
+      cu.seek(S, ns, TC, g);
+      seg_end = min(b, cu.off + cu.nt);
+      st = S + cu.s;
+      nj = st->k + 1;
+      n = st->n;
+      nchunks = gt_chunks(*st);
+      w = st->V[nj];
+      woff = ((nj >> 6) * TC + cc) * 1024 + (nj & 63) * 16 + r;
+#pragma unroll
+      for (int i = 0; i < GT_NI; ++i) {
+        const int j = i * CPI + 2 * wq + par;
+        coef[i] = j < nj ? st->scale[j] * st->h[j] : 0.0;
+        acc[i] = 0.0;
+      }
+      wsq = 0.0;
+    }
+    const int c0 = int(g - cu.off) * TC;
+    const bool ccv = c0 + cc < nchunks;
+    mbar_wait(full + stg, phase);
+    const double* T = reinterpret_cast<const double*>(ring + size_t(stg) * size_t(stage_bytes)) + tbase;
+    double v[GT_NI];
+#pragma unroll
+    for (int i = 0; i < GT_NI; ++i) {
+      const int j = i * CPI + 2 * wq + par;
+      v[i] = (j < nj && ccv) ? T[(i / SPP) * TC * 1024 + (i % SPP) * CPI * 16] : 0.0;
+    }
+    const double wpre = ccv ? T[woff - tbase] : 0.0;
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < GT_NI; ++i) s4[i & 3] = fma(coef[i], v[i], s4[i & 3]);
+    double s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    s += __shfl_xor_sync(0xffffffffu, s, 16);
+    double* rd = red + (u & 1) * (GT_CWARPS * 16);
+    if (lane < 16) rd[warp * 16 + lane] = s;
+    __syncthreads();  // row sums complete; every warp holds its part of the tile
+    if (warp == 0 && g + NS < b) prod.issue(S, ns, g + NS, stg, stage_bytes, ring, full, lane);
+    if (++stg == NS) {
+      stg = 0;
+      phase ^= 1u;
+    }
+    // row total over the chunk's WPC warps: each half-warp reads half of them
+    double tot = 0.0;
+    if (WPC >= 2) {
+      constexpr int H = WPC / 2;
+      double t2[2] = {0.0, 0.0};
+#pragma unroll
+      for (int q = 0; q < H; ++q) t2[q & 1] += rd[(cc * WPC + par * H + q) * 16 + r];
+      tot = t2[0] + t2[1];
+      tot += __shfl_xor_sync(0xffffffffu, tot, 16);
+    } else {
+      tot = rd[cc * 16 + r];
+    }
+    const double wn = wpre - tot;
+    if (wq == 0 && lane < 16 && ccv && (c0 + cc) * CHUNK + r < n) {
+      w[size_t(c0 + cc) * 1024 + r] = wn;
+      wsq = fma(wn, wn, wsq);
+    }
+#pragma unroll
+    for (int i = 0; i < GT_NI; ++i) acc[i] = fma(v[i], wn, acc[i]);
+    if (g + 1 == seg_end) {  // flush this solve's partials
+#pragma unroll
+      for (int i = 0; i < GT_NI; ++i) {
+        double x = acc[i];
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        const int j = i * CPI + 2 * wq + par;
+        if (r == 0 && j < nj) red2[cc * nj + j] = x;
+      }
+      const double x = warp_sum(wsq);
+      if (lane == 0) red3[warp] = x;
+      __syncthreads();
+      for (int j = tid; j < nj; j += GT_CONSUMERS) {
+        double y = 0.0;
+        for (int q = 0; q < TC; ++q) y += red2[q * nj + j];
+        st->part[size_t(j) * G + slot] = y;
+      }
+      if (tid == 0) {
+        double y = 0.0;
+        for (int q = 0; q < GT_CWARPS; ++q) y += red3[q];
+        st->part[size_t(nj) * G + slot] = y;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(GT_THREADS, 1) k_gs_tma(GmSolve* S, int ns, int G) {
+  extern __shared__ __align__(128) char smt[];
+  char* ring = smt;
+  double* red = reinterpret_cast<double*>(smt + GT_RING);  // [2][warps][16 rows]
+  double* red2 = red + 2 * GT_CWARPS * 16;                  // [TC][k + 1]
+  double* red3 = red2 + GT_MAXCOLS;                         // [warps]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red3 + GT_CWARPS);
+  const int slot = blockIdx.x, nslots = gridDim.x;
+  // Same tile geometry in every CTA: TC from the largest k + 1 handled.
+  int njmax = 0;
+  for (int s = 0; s < ns; ++s)
+    if (gt_handles(S[s])) njmax = max(njmax, S[s].k + 1);
+  if (njmax == 0) return;
+  int TC = 1;
+  while (TC < GT_CWARPS && njmax * 2 * TC <= GT_MAXCOLS) TC *= 2;
+  const int stage_bytes = TC * ((njmax + 1 + 63) / 64) * 8192;
+  const int NS = min(GT_MAXST, GT_RING / stage_bytes);
+  long long total = 0;
+  for (int s = 0; s < ns; ++s)
+    if (gt_handles(S[s])) total += (gt_chunks(S[s]) + TC - 1) / TC;
+  const long long per = (total + nslots - 1) / nslots;
+  const long long a = min(total, per * slot), b = min(total, a + per);
+  // zero partials of the handled solves with no tile here
+  {
+    long long off = 0;
+    for (int s = 0; s < ns; ++s) {
+      if (!gt_handles(S[s])) continue;
+      const long long nt = (gt_chunks(S[s]) + TC - 1) / TC;
+      if (!(a < off + nt && off < b)) {
+        const int nj = S[s].k + 1;
+        for (int j = int(threadIdx.x); j <= nj; j += GT_THREADS) S[s].part[size_t(j) * G + slot] = 0.0;
+      }
+      off += nt;
+    }
+  }
+  if (a >= b) return;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(full + i, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  switch (TC) {
+    case 16: gt_body<16>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3); break;
+    case 8: gt_body<8>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3); break;
+    case 4: gt_body<4>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3); break;
+    case 2: gt_body<2>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3); break;
+    default: gt_body<1>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3); break;
   }
 }
 
@@ -1208,7 +1485,7 @@ inline unsigned cdiv(int64_t a, int64_t b) { return unsigned((a + b - 1) / b); }
 
 // Cluster launch of the Gram-Schmidt kernels: ncl clusters of CL CTAs.
 template <int CL, bool UPDATE>
-cudaError_t gc_launch(cudaStream_t s, int ncl, GmSolve* S, int ns, int G) {
+cudaError_t gc_launch(cudaStream_t s, int ncl, GmSolve* S, int ns, int G, int skip_le) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(ncl * CL), 1u, 1u);
   cfg.blockDim = dim3(unsigned(GC_THREADS), 1u, 1u);
@@ -1221,7 +1498,7 @@ cudaError_t gc_launch(cudaStream_t s, int ncl, GmSolve* S, int ns, int G) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_gs_clu<CL, UPDATE>, S, ns, G);
+  return cudaLaunchKernelEx(&cfg, k_gs_clu<CL, UPDATE>, S, ns, G, skip_le);
 }
 
 template <int CL>
@@ -1282,11 +1559,12 @@ GcConfig gc_config(int dev, int sm_count, bool update) {
   return g;
 }
 
-cudaError_t gc_launch_any(bool update, const GcConfig& g, cudaStream_t s, GmSolve* S, int ns, int G) {
+cudaError_t gc_launch_any(bool update, const GcConfig& g, cudaStream_t s, GmSolve* S, int ns, int G,
+                          int skip_le = 0) {
   switch (g.cl) {
-    case 4: return update ? gc_launch<4, true>(s, g.ncl, S, ns, G) : gc_launch<4, false>(s, g.ncl, S, ns, G);
-    case 2: return update ? gc_launch<2, true>(s, g.ncl, S, ns, G) : gc_launch<2, false>(s, g.ncl, S, ns, G);
-    default: return update ? gc_launch<1, true>(s, g.ncl, S, ns, G) : gc_launch<1, false>(s, g.ncl, S, ns, G);
+    case 4: return update ? gc_launch<4, true>(s, g.ncl, S, ns, G, skip_le) : gc_launch<4, false>(s, g.ncl, S, ns, G, 0);
+    case 2: return update ? gc_launch<2, true>(s, g.ncl, S, ns, G, skip_le) : gc_launch<2, false>(s, g.ncl, S, ns, G, 0);
+    default: return update ? gc_launch<1, true>(s, g.ncl, S, ns, G, skip_le) : gc_launch<1, false>(s, g.ncl, S, ns, G, 0);
   }
 }
 
@@ -1458,6 +1736,12 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     cudaFuncSetAttribute(k_reorth_p, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
   const bool fused = maxit + 1 <= UP_MAXCOLS && !std::getenv("MPG_NO_FUSE");
+  // TMA-staged update + probe (MPG_GS_TMA=0: the register-tiled kernel for all k);
+  // slots = the update clusters, one CTA each.
+  const char* gt_env = std::getenv("MPG_GS_TMA");
+  const bool gt_on = fused && gc_upd.cl == 1 && !(gt_env && gt_env[0] == '0');
+  static std::once_flag gt_once;
+  std::call_once(gt_once, [] { cudaFuncSetAttribute(k_gs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, GT_SMEM); });
   const size_t smem_ro = size_t(2 * UP_MAXCOLS + 32) * sizeof(double) + size_t(ns) * sizeof(int);
   int launches_per_iter = 0;
   // Profiling hook: called after every launch with a kernel-class id.
@@ -1683,9 +1967,17 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 0, fused ? gc_dot.ncl : G);
     mark(PK_SMALL);
     if (fused) {
-      MPG_CUDA(gc_launch_any(true, gc_upd, s, dS.get(), ns, G));
-      mark(PK_UPDPROBE);
       --launches_per_iter;
+      if (gt_on) {
+        k_gs_tma<<<unsigned(gc_upd.ncl), GT_THREADS, GT_SMEM, s>>>(dS.get(), ns, G);
+        ++launches_per_iter;
+        mark(PK_UPDPROBE);
+      }
+      if (!gt_on || maxit + 1 > GT_MAXCOLS) {
+        MPG_CUDA(gc_launch_any(true, gc_upd, s, dS.get(), ns, G, gt_on ? GT_MAXCOLS : 0));
+        ++launches_per_iter;
+        mark(PK_UPDPROBE);
+      }
     } else {
       k_update<<<gG, 256, smem_upd, s>>>(dS.get(), G, 0);
       mark(PK_UPD);
