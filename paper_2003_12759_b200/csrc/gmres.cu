@@ -22,6 +22,9 @@
 #include <cstring>
 #include <functional>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "runtime.cuh"
 
 namespace mpg {
@@ -69,6 +72,7 @@ struct GmSolve {
   double* rbuf;
   double* part;
   const CsrView* fac;
+  const CUtensorMap* tm;  // per basis panel: [2 p] 64-vector box, [2 p + 1] 8-vector box (null: none)
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -866,9 +870,29 @@ __device__ __forceinline__ int gc_tiles(const GmSolve& st, int CL) {
 // one tile (tile parked in shared memory) reached 3.2 / 2.2 TB/s (shared-memory
 // traffic, mbarrier spinning). Unclustered: 4.7 TB/s -- the default.
 
-// skip_le > 0 (update pass): solves with k + 1 <= skip_le are left to k_gs_tma.
+// Solves whose update pass runs in a TMA-staged kernel are skipped by the
+// register-tiled update kernel.
+constexpr int GT_MAXCOLS = 384;  // k_gs_tma: largest k + 1
+constexpr int GX_NG = 12;        // k_gs_tmx: 32-vector groups per lane
+constexpr int GX_MAXV = GX_NG * 32;  // k_gs_tmx: largest k + 2 (basis and w)
+// Which update kernel owns a running solve this iteration. sel: bit 0 = k_gs_tma
+// enabled, bit 1 = k_gs_tmx enabled; split: with both, k + 1 <= split goes to
+// k_gs_tma (faster while k_gs_tmx's multi-chunk tiles are latency-bound, C3:
+// k + 1 < ~190) and larger k to k_gs_tmx. 0 = the register-tiled kernel.
+struct UpdSel {
+  int sel, split;
+};
+__device__ __forceinline__ int upd_owner(const GmSolve& st, UpdSel u) {
+  const int nj = st.k + 1;
+  if ((u.sel & 2) && st.tm != nullptr && nj + 1 <= GX_MAXV && (!(u.sel & 1) || nj > u.split)) return 2;
+  if ((u.sel & 1) && nj <= GT_MAXCOLS) return 1;
+  return 0;
+}
+__device__ __forceinline__ bool gt_handles(const GmSolve& st, UpdSel u) { return st.phase == PH_RUN && upd_owner(st, u) == 1; }
+__device__ __forceinline__ bool gx_handles(const GmSolve& st, UpdSel u) { return st.phase == PH_RUN && upd_owner(st, u) == 2; }
+
 template <int CL, bool UPDATE>
-__global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, int G, int skip_le) {
+__global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, int G, UpdSel skip) {
   extern __shared__ __align__(16) double smc[];
   double* coef = smc;
   const double** vp = reinterpret_cast<const double**>(smc + UP_MAXCOLS);
@@ -878,13 +902,13 @@ __global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, in
   const int q = int(blockIdx.x) % CL, slot = int(blockIdx.x) / CL, ncl = int(gridDim.x) / CL;
   long long total = 0;
   for (int s = 0; s < ns; ++s)
-    if (S[s].phase == PH_RUN && S[s].k + 1 > skip_le) total += gc_tiles(S[s], CL);
+    if (S[s].phase == PH_RUN && (!UPDATE || upd_owner(S[s], skip) == 0)) total += gc_tiles(S[s], CL);
   const long long per = (total + ncl - 1) / ncl;
   const long long a = per * slot, b = min(total, a + per);
   long long off = 0;
   for (int s = 0; s < ns; ++s) {
     GmSolve& st = S[s];
-    if (st.phase != PH_RUN || st.k + 1 <= skip_le) continue;
+    if (st.phase != PH_RUN || (UPDATE && upd_owner(st, skip) != 0)) continue;
     const int nt = gc_tiles(st, CL);
     const long long lo = a > off ? a : off, hi = b < off + nt ? b : off + nt;
     if (lo < hi) {
@@ -1031,7 +1055,7 @@ constexpr int GT_CWARPS = 16;                      // warps
 constexpr int GT_CONSUMERS = GT_CWARPS * 32;
 constexpr int GT_THREADS = GT_CONSUMERS;
 constexpr int GT_NI = 12;                          // vector slots per lane
-constexpr int GT_MAXCOLS = GT_NI * 2 * GT_CWARPS;   // largest k + 1 handled (TC = 1)
+static_assert(GT_MAXCOLS == GT_NI * 2 * GT_CWARPS, "k_gs_tma slots");
 constexpr int GT_RING = 26 * 8192;                 // tile ring (bytes)
 constexpr int GT_MAXST = 16;
 constexpr int GT_SMEM = GT_RING + (2 * GT_CWARPS * 16 + GT_MAXCOLS + GT_CWARPS) * 8 + GT_MAXST * 8;
@@ -1064,18 +1088,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
-__device__ __forceinline__ bool gt_handles(const GmSolve& st) { return st.phase == PH_RUN && st.k + 1 <= GT_MAXCOLS; }
 __device__ __forceinline__ int gt_chunks(const GmSolve& st) { return ((st.n + 31) & ~31) / CHUNK; }
 
 // Tile cursor over the handled solves: tiles [off, off + nt) belong to solve s.
 struct GtCursor {
   int s = -1, nt = 0;
   long long off = 0;
+  UpdSel us;
   __device__ __forceinline__ void seek(const GmSolve* S, int ns, int TC, long long g) {
     while (s < ns && (s < 0 || g >= off + nt)) {
       if (s >= 0) off += nt;
       ++s;
-      while (s < ns && !gt_handles(S[s])) ++s;
+      while (s < ns && !gt_handles(S[s], us)) ++s;
       nt = s < ns ? (gt_chunks(S[s]) + TC - 1) / TC : 0;
     }
   }
@@ -1121,7 +1145,7 @@ struct GtProducer {
 
 template <int TC>
 __device__ __forceinline__ void gt_body(GmSolve* S, int ns, int G, int stage_bytes, int NS, long long a, long long b,
-                                        char* ring, uint64_t* full, double* red, double* red2, double* red3) {
+                                        char* ring, uint64_t* full, double* red, double* red2, double* red3, UpdSel us) {
   constexpr int WPC = GT_CWARPS / TC;  // warps per chunk
   constexpr int CPI = 2 * WPC;         // vectors per slot step
   constexpr int SPP = 64 / CPI;        // slots per panel
@@ -1129,11 +1153,13 @@ __device__ __forceinline__ void gt_body(GmSolve* S, int ns, int G, int stage_byt
   const int cc = warp / WPC, wq = warp % WPC, r = lane & 15, par = lane >> 4;
   const int slot = blockIdx.x;
   GtProducer<TC> prod;
+  prod.pc.us = us;
   if (warp == 0) {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(prod.pol));
     for (long long g = a; g < b && g < a + NS; ++g) prod.issue(S, ns, g, int(g - a), stage_bytes, ring, full, lane);
   }
   GtCursor cu;
+  cu.us = us;
   double coef[GT_NI], acc[GT_NI];
   double wsq = 0.0;
   double* w = nullptr;
@@ -1232,7 +1258,7 @@ __device__ __forceinline__ void gt_body(GmSolve* S, int ns, int G, int stage_byt
   }
 }
 
-__global__ void __launch_bounds__(GT_THREADS, 1) k_gs_tma(GmSolve* S, int ns, int G) {
+__global__ void __launch_bounds__(GT_THREADS, 1) k_gs_tma(GmSolve* S, int ns, int G, UpdSel us) {
   extern __shared__ __align__(128) char smt[];
   char* ring = smt;
   double* red = reinterpret_cast<double*>(smt + GT_RING);  // [2][warps][16 rows]
@@ -1243,7 +1269,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1) k_gs_tma(GmSolve* S, int ns, in
   // Same tile geometry in every CTA: TC from the largest k + 1 handled.
   int njmax = 0;
   for (int s = 0; s < ns; ++s)
-    if (gt_handles(S[s])) njmax = max(njmax, S[s].k + 1);
+    if (gt_handles(S[s], us)) njmax = max(njmax, S[s].k + 1);
   if (njmax == 0) return;
   int TC = 1;
   while (TC < GT_CWARPS && njmax * 2 * TC <= GT_MAXCOLS) TC *= 2;
@@ -1251,14 +1277,14 @@ __global__ void __launch_bounds__(GT_THREADS, 1) k_gs_tma(GmSolve* S, int ns, in
   const int NS = min(GT_MAXST, GT_RING / stage_bytes);
   long long total = 0;
   for (int s = 0; s < ns; ++s)
-    if (gt_handles(S[s])) total += (gt_chunks(S[s]) + TC - 1) / TC;
+    if (gt_handles(S[s], us)) total += (gt_chunks(S[s]) + TC - 1) / TC;
   const long long per = (total + nslots - 1) / nslots;
   const long long a = min(total, per * slot), b = min(total, a + per);
   // zero partials of the handled solves with no tile here
   {
     long long off = 0;
     for (int s = 0; s < ns; ++s) {
-      if (!gt_handles(S[s])) continue;
+      if (!gt_handles(S[s], us)) continue;
       const long long nt = (gt_chunks(S[s]) + TC - 1) / TC;
       if (!(a < off + nt && off < b)) {
         const int nj = S[s].k + 1;
@@ -1276,12 +1302,266 @@ __global__ void __launch_bounds__(GT_THREADS, 1) k_gs_tma(GmSolve* S, int ns, in
   }
   __syncthreads();
   switch (TC) {
-    case 16: gt_body<16>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3); break;
-    case 8: gt_body<8>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3); break;
-    case 4: gt_body<4>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3); break;
-    case 2: gt_body<2>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3); break;
-    default: gt_body<1>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3); break;
+    case 16: gt_body<16>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3, us); break;
+    case 8: gt_body<8>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3, us); break;
+    case 4: gt_body<4>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3, us); break;
+    case 2: gt_body<2>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3, us); break;
+    default: gt_body<1>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3, us); break;
   }
+}
+
+// ---- update + probe without per-tile barriers (default for k + 2 <= GX_MAXV) -----
+// Same contract as k_gs_clu<CL, true>. A producer warp streams tiles of TC
+// chunks x all k + 2 vectors (w = W_{k+1} included) with 3-D tensor copies
+// (cp.async.bulk.tensor) of each panel's [chunk][64 vectors][16 rows] block
+// into a ring of NS stages (full/empty mbarriers). The copies use the 128-byte
+// swizzle: the 16-byte unit holding rows (2q, 2q + 1) of vector j lands at unit
+// q ^ (j & 7) of the vector's 128-byte line, so a warp can read one row pair of
+// 32 consecutive vectors (lane l: vector 32 g + l) without bank conflicts.
+// Consumer warp w owns row pair w of every chunk: its lanes hold 32-vector
+// groups of the pair, the row sums are a warp butterfly (no CTA barrier), the
+// probe partials stay in registers (vector 32 g + lane) until the solve's last
+// tile here. The stage is released by one arrive per warp.
+// (k_gs_tma, the barrier-per-tile version with 1-D bulk copies, is kept as an
+// alternative: MPG_GS_UPD=tma.)
+constexpr int GX_CWARPS = 8;                        // consumer warps (row pairs of a chunk)
+constexpr int GX_THREADS = (GX_CWARPS + 1) * 32;    // + one producer warp
+constexpr int GX_RING = 24 * 8192;                  // tile ring (bytes)
+constexpr int GX_MAXST = 16;
+constexpr int GX_SMEM = 1024 + GX_RING + (GX_CWARPS * GX_MAXV + GX_CWARPS) * 8 + 2 * GX_MAXST * 8;
+
+__device__ __forceinline__ void tma3_g2s(uint32_t dst, const CUtensorMap* tm, int c1, int c2, uint32_t mbar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(dst),
+      "l"(tm), "r"(0), "r"(c1), "r"(c2), "r"(mbar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void consumers_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(GX_CWARPS * 32) : "memory"); }
+
+struct GxCursor {
+  int s = -1, nt = 0;
+  long long off = 0;
+  UpdSel us;
+  __device__ __forceinline__ void seek(const GmSolve* S, int ns, int TC, long long g) {
+    while (s < ns && (s < 0 || g >= off + nt)) {
+      if (s >= 0) off += nt;
+      ++s;
+      while (s < ns && !gx_handles(S[s], us)) ++s;
+      nt = s < ns ? (gt_chunks(S[s]) + TC - 1) / TC : 0;
+    }
+  }
+};
+
+__device__ __forceinline__ void gx_producer(GmSolve* S, int ns, int TC, int stage_bytes, int NS, long long a,
+                                            long long b, uint32_t ring, uint64_t* full, uint64_t* empty, UpdSel us) {
+  const int lane = threadIdx.x & 31;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  GxCursor pc;
+  pc.us = us;
+  const CUtensorMap* tm = nullptr;
+  int nv = 0, nchunks = 0, stg = 0;
+  unsigned eph = 0;  // parity of the empty barriers' current phase
+  for (long long g = a; g < b; ++g) {
+    if (g - a >= NS) mbar_wait(empty + stg, eph);
+    if (pc.s < 0 || g >= pc.off + pc.nt) {
+      pc.seek(S, ns, TC, g);
+      const GmSolve& st = S[pc.s];
+      tm = st.tm;
+      nv = st.k + 2;
+      nchunks = gt_chunks(st);
+    }
+    const int c0 = int(g - pc.off) * TC;
+    const int nch = min(TC, nchunks - c0);
+    const int pf = nv >> 6, mb = ((nv & 63) + 7) >> 3;  // full panels, 8-vector boxes of the last one
+    const int per = pf + mb;
+    if (lane == 0) mbar_expect_tx(full + stg, unsigned(nch) * unsigned(pf * 8192 + mb * 1024));
+    __syncwarp();
+    const uint32_t base = ring + uint32_t(stg) * uint32_t(stage_bytes);
+    const uint32_t mbar = smem_u32(full + stg);
+    for (int op = lane; op < nch * per; op += 32) {
+      const int q = op / per, t = op - q * per;
+      if (t < pf)
+        tma3_g2s(base + uint32_t(t * TC + q) * 8192u, tm + 2 * t, 0, c0 + q, mbar, pol);
+      else
+        tma3_g2s(base + uint32_t(pf * TC) * 8192u + uint32_t(q * mb + t - pf) * 1024u, tm + 2 * pf + 1,
+                 8 * (t - pf), c0 + q, mbar, pol);
+    }
+    if (++stg == NS) {
+      stg = 0;
+      if (g - a >= NS) eph ^= 1u;
+    }
+  }
+}
+
+__device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, int stage_bytes, int NS, long long a,
+                                            long long b, uint32_t ring, uint64_t* full, uint64_t* empty, double* red2,
+                                            double* red3, UpdSel us) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int rp = warp;  // row pair
+  const int slot = blockIdx.x;
+  // byte offset of (vector 32 g + lane, row pair rp) inside a chunk of a stage
+  const uint32_t loff = uint32_t(lane) * 128u + uint32_t((rp ^ (lane & 7)) << 4);
+  GxCursor cu;
+  cu.us = us;
+  double coef[GX_NG], acc[GX_NG];
+  double wsq = 0.0;
+  double* w = nullptr;
+  int nj = 0, nchunks = 0, n = 0, pf = 0, mb = 0;
+  uint32_t woff = 0;
+  long long seg_end = -1;
+  int stg = 0;
+  unsigned fph = 0;
+  for (long long g = a; g < b; ++g) {
+    if (g >= seg_end) {  // first tile of a solve in this CTA
+      cu.seek(S, ns, TC, g);
+      seg_end = min(b, cu.off + cu.nt);
+      const GmSolve& st = S[cu.s];
+      nj = st.k + 1;
+      n = st.n;
+      nchunks = gt_chunks(st);
+      w = st.V[nj];
+      pf = (nj + 1) >> 6;
+      mb = (((nj + 1) & 63) + 7) >> 3;
+      woff = uint32_t((rp ^ (nj & 7)) << 4) + uint32_t(nj & 63) * 128u;
+#pragma unroll
+      for (int i = 0; i < GX_NG; ++i) {
+        const int j = 32 * i + lane;
+        coef[i] = j < nj ? st.scale[j] * st.h[j] : 0.0;
+        acc[i] = 0.0;
+      }
+      wsq = 0.0;
+    }
+    const int c0 = int(g - cu.off) * TC;
+    mbar_wait(full + stg, fph);
+    const uint32_t sbase = ring + uint32_t(stg) * uint32_t(stage_bytes);
+    for (int cc = 0; cc < TC; ++cc) {
+      if (c0 + cc >= nchunks) break;
+      // chunk cc of full panel p at (p TC + cc) 8 KB; of the last panel at
+      // pf TC 8 KB + cc mb KB (its mb 8-vector boxes)
+      const uint32_t cb = sbase + uint32_t(cc) * 8192u;
+      const uint32_t pb = sbase + uint32_t(pf * TC) * 8192u + uint32_t(cc * mb) * 1024u;
+      double2 v[GX_NG];
+#pragma unroll
+      for (int i = 0; i < GX_NG; ++i) {
+        const uint32_t a = ((i >> 1) < pf ? cb + uint32_t((i >> 1) * TC) * 8192u : pb) + uint32_t(i & 1) * 4096u + loff;
+        v[i] = 32 * i + lane < nj ? lds_f64x2(a) : make_double2(0.0, 0.0);
+      }
+      const double2 wp = lds_f64x2(((nj >> 6) < pf ? cb + uint32_t((nj >> 6) * TC) * 8192u : pb) + woff);
+      double sx0 = 0.0, sx1 = 0.0, sy0 = 0.0, sy1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < GX_NG; i += 2) {
+        sx0 = fma(coef[i], v[i].x, sx0);
+        sy0 = fma(coef[i], v[i].y, sy0);
+        sx1 = fma(coef[i + 1], v[i + 1].x, sx1);
+        sy1 = fma(coef[i + 1], v[i + 1].y, sy1);
+      }
+      double sx = sx0 + sx1, sy = sy0 + sy1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+      }
+      const double wn0 = wp.x - sx, wn1 = wp.y - sy;
+      const int row = (c0 + cc) * CHUNK + 2 * rp;
+      if (lane == 0) {
+        double* dst = w + size_t(c0 + cc) * 1024 + 2 * rp;
+        if (row + 1 < n) {
+          *reinterpret_cast<double2*>(dst) = make_double2(wn0, wn1);
+          wsq = fma(wn0, wn0, fma(wn1, wn1, wsq));
+        } else if (row < n) {
+          dst[0] = wn0;
+          wsq = fma(wn0, wn0, wsq);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < GX_NG; ++i) acc[i] = fma(v[i].x, wn0, fma(v[i].y, wn1, acc[i]));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + stg);
+    if (++stg == NS) {
+      stg = 0;
+      fph ^= 1u;
+    }
+    if (g + 1 == seg_end) {  // flush this solve's partials
+      GmSolve& st = S[cu.s];
+#pragma unroll
+      for (int i = 0; i < GX_NG; ++i)
+        if (32 * i + lane < nj) red2[warp * GX_MAXV + 32 * i + lane] = acc[i];
+      if (lane == 0) red3[warp] = wsq;
+      consumers_bar();
+      for (int j = tid; j < nj; j += GX_CWARPS * 32) {
+        double y = 0.0;
+        for (int q = 0; q < GX_CWARPS; ++q) y += red2[q * GX_MAXV + j];
+        st.part[size_t(j) * G + slot] = y;
+      }
+      if (tid == 0) {
+        double y = 0.0;
+        for (int q = 0; q < GX_CWARPS; ++q) y += red3[q];
+        st.part[size_t(nj) * G + slot] = y;
+      }
+      consumers_bar();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(GX_THREADS, 1) k_gs_tmx(GmSolve* S, int ns, int G, UpdSel us) {
+  extern __shared__ __align__(1024) char smx[];
+  const uint32_t raw = smem_u32(smx);
+  const uint32_t ring = (raw + 1023u) & ~1023u;  // 128-byte swizzle needs 1024-byte aligned stages
+  char* gen = smx + (ring - raw);
+  double* red2 = reinterpret_cast<double*>(gen + GX_RING);  // [warps][GX_MAXV]
+  double* red3 = red2 + GX_CWARPS * GX_MAXV;                 // [warps]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red3 + GX_CWARPS);
+  uint64_t* empty = full + GX_MAXST;
+  const int slot = blockIdx.x, nslots = gridDim.x;
+  int nvmax = 0;
+  for (int s = 0; s < ns; ++s)
+    if (gx_handles(S[s], us)) nvmax = max(nvmax, S[s].k + 2);
+  if (nvmax == 0) return;
+  // tile = TC chunks of up to about 48 KB (at least 4 stages in the ring)
+  const int chunk_bytes = (nvmax >> 6) * 8192 + (((nvmax & 63) + 7) >> 3) * 1024;
+  int TC = 1;
+  while (TC < 16 && 2 * TC * chunk_bytes <= 48 * 1024) TC *= 2;
+  const int stage_bytes = TC * chunk_bytes;
+  const int NS = min(GX_MAXST, GX_RING / stage_bytes);
+  long long total = 0;
+  for (int s = 0; s < ns; ++s)
+    if (gx_handles(S[s], us)) total += (gt_chunks(S[s]) + TC - 1) / TC;
+  const long long per = (total + nslots - 1) / nslots;
+  const long long a = min(total, per * slot), b = min(total, a + per);
+  {
+    long long off = 0;
+    for (int s = 0; s < ns; ++s) {
+      if (!gx_handles(S[s], us)) continue;
+      const long long nt = (gt_chunks(S[s]) + TC - 1) / TC;
+      if (!(a < off + nt && off < b)) {
+        const int nj = S[s].k + 1;
+        for (int j = int(threadIdx.x); j <= nj; j += GX_THREADS) S[s].part[size_t(j) * G + slot] = 0.0;
+      }
+      off += nt;
+    }
+  }
+  if (a >= b) return;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, GX_CWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x >= GX_CWARPS * 32)
+    gx_producer(S, ns, TC, stage_bytes, NS, a, b, ring, full, empty, us);
+  else
+    gx_consumer(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
 }
 
 // ---- norm partials of the residual buffer ----------------------------------------
@@ -1485,7 +1765,7 @@ inline unsigned cdiv(int64_t a, int64_t b) { return unsigned((a + b - 1) / b); }
 
 // Cluster launch of the Gram-Schmidt kernels: ncl clusters of CL CTAs.
 template <int CL, bool UPDATE>
-cudaError_t gc_launch(cudaStream_t s, int ncl, GmSolve* S, int ns, int G, int skip_le) {
+cudaError_t gc_launch(cudaStream_t s, int ncl, GmSolve* S, int ns, int G, UpdSel skip) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(ncl * CL), 1u, 1u);
   cfg.blockDim = dim3(unsigned(GC_THREADS), 1u, 1u);
@@ -1498,7 +1778,7 @@ cudaError_t gc_launch(cudaStream_t s, int ncl, GmSolve* S, int ns, int G, int sk
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_gs_clu<CL, UPDATE>, S, ns, G, skip_le);
+  return cudaLaunchKernelEx(&cfg, k_gs_clu<CL, UPDATE>, S, ns, G, skip);
 }
 
 template <int CL>
@@ -1560,15 +1840,47 @@ GcConfig gc_config(int dev, int sm_count, bool update) {
 }
 
 cudaError_t gc_launch_any(bool update, const GcConfig& g, cudaStream_t s, GmSolve* S, int ns, int G,
-                          int skip_le = 0) {
+                          UpdSel skip = UpdSel{0, 0}) {
+  const UpdSel none{0, 0};
   switch (g.cl) {
-    case 4: return update ? gc_launch<4, true>(s, g.ncl, S, ns, G, skip_le) : gc_launch<4, false>(s, g.ncl, S, ns, G, 0);
-    case 2: return update ? gc_launch<2, true>(s, g.ncl, S, ns, G, skip_le) : gc_launch<2, false>(s, g.ncl, S, ns, G, 0);
-    default: return update ? gc_launch<1, true>(s, g.ncl, S, ns, G, skip_le) : gc_launch<1, false>(s, g.ncl, S, ns, G, 0);
+    case 4: return update ? gc_launch<4, true>(s, g.ncl, S, ns, G, skip) : gc_launch<4, false>(s, g.ncl, S, ns, G, none);
+    case 2: return update ? gc_launch<2, true>(s, g.ncl, S, ns, G, skip) : gc_launch<2, false>(s, g.ncl, S, ns, G, none);
+    default: return update ? gc_launch<1, true>(s, g.ncl, S, ns, G, skip) : gc_launch<1, false>(s, g.ncl, S, ns, G, none);
   }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    else
+      cudaGetLastError();
+  });
+  return fn;
+}
+
+// Tensor map over one basis panel, [chunks][64 vectors][16 rows] doubles, box
+// of box_vecs vectors x 16 rows of one chunk, 128-byte swizzle (k_gs_tmx).
+void encode_panel_map(CUtensorMap* out, double* base, int64_t chunks, int box_vecs) {
+  const cuuint64_t dims[3] = {cuuint64_t(CHUNK), cuuint64_t(PANEL), cuuint64_t(chunks)};
+  const cuuint64_t strides[2] = {cuuint64_t(CHUNK) * sizeof(double), cuuint64_t(PANEL * CHUNK) * sizeof(double)};
+  const cuuint32_t box[3] = {cuuint32_t(CHUNK), cuuint32_t(box_vecs), 1u};
+  const cuuint32_t es[3] = {1u, 1u, 1u};
+  const CUresult r = tensor_map_encoder()(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
+                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+
 struct SolveHost {
+  std::vector<CUtensorMap> tmh;  // host mirror of the panel tensor maps (k_gs_tmx)
+  DBuf<CUtensorMap> tmd;
   std::vector<DBuf<double>> panels;
   std::vector<double*> vtab;  // host mirror of the V table
   int uploaded = 0;
@@ -1603,6 +1915,21 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   const int G = std::max(std::max(std::max(gc_dot.ncl, gc_upd.ncl), c.sm_count),
                          std::max(1, std::min(ntiles, std::max(8, (c.sm_count * 8) / ns))));
 
+  // Update + probe kernel (MPG_GS_UPD = tmx | tma | reg): 2 = k_gs_tmx (swizzled
+  // tensor copies, no per-tile barrier), 1 = k_gs_tma, 0 = register-tiled only.
+  const bool fused = maxit + 1 <= UP_MAXCOLS && !std::getenv("MPG_NO_FUSE");
+  // Update + probe kernels (MPG_GS_UPD = hybrid | tmx | tma | reg): k_gs_tma up
+  // to k + 1 = split, k_gs_tmx above (up to GX_MAXV), the register-tiled kernel
+  // beyond; measured per launch on C3.
+  UpdSel usel{0, 0};
+  if (fused && gc_upd.cl == 1) {
+    const char* e = std::getenv("MPG_GS_UPD");
+    usel.sel = e && !std::strcmp(e, "reg") ? 0 : e && !std::strcmp(e, "tma") ? 1 : e && !std::strcmp(e, "tmx") ? 2 : 3;
+    if (!tensor_map_encoder()) usel.sel &= 1;
+    const char* sp = std::getenv("MPG_GS_SPLIT");
+    usel.split = sp ? std::atoi(sp) : 192;
+  }
+  const int upd_kind = usel.sel;  // bit 1: panel tensor maps needed
   std::vector<SolveHost> sh(static_cast<size_t>(ns));
   std::vector<GmSolve> hs(static_cast<size_t>(ns));
   int max_stages = 0;
@@ -1682,6 +2009,12 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     g.rbuf = H.rbuf.get();
     g.part = H.part.get();
     g.fac = H.fac.get();
+    if (upd_kind & 2) {
+      const size_t np = size_t(maxit + 2 + PANEL - 1) / PANEL;
+      H.tmh.resize(2 * np);
+      H.tmd = DBuf<CUtensorMap>(dev, 2 * np);
+      g.tm = H.tmd.get();
+    }
   }
 
   // Basis panels: make vectors [0, upto) available for solve i.
@@ -1695,6 +2028,12 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       MPG_CUDA(cudaMemsetAsync(base, 0, size_t(PANEL) * size_t(H.ld) * sizeof(double), s));
       const int p0 = int(H.panels.size() - 1) * PANEL;
       for (int j = 0; j < PANEL && p0 + j < maxit + 2; ++j) H.vtab[size_t(p0 + j)] = base + size_t(j) * CHUNK;
+      if (upd_kind & 2) {
+        const size_t p = H.panels.size() - 1;
+        encode_panel_map(&H.tmh[2 * p], base, H.ld / CHUNK, PANEL);
+        encode_panel_map(&H.tmh[2 * p + 1], base, H.ld / CHUNK, 8);
+        MPG_CUDA(cudaMemcpyAsync(H.tmd.get() + 2 * p, &H.tmh[2 * p], 2 * sizeof(CUtensorMap), cudaMemcpyHostToDevice, s));
+      }
     }
     if (upto > H.uploaded) {
       MPG_CUDA(cudaMemcpyAsync(H.dV.get() + H.uploaded, H.vtab.data() + H.uploaded,
@@ -1735,13 +2074,16 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_reorth_p, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
-  const bool fused = maxit + 1 <= UP_MAXCOLS && !std::getenv("MPG_NO_FUSE");
-  // TMA-staged update + probe (MPG_GS_TMA=0: the register-tiled kernel for all k);
-  // slots = the update clusters, one CTA each.
-  const char* gt_env = std::getenv("MPG_GS_TMA");
-  const bool gt_on = fused && gc_upd.cl == 1 && !(gt_env && gt_env[0] == '0');
+  // TMA-staged update + probe kernels: slots = the update clusters, one CTA each.
   static std::once_flag gt_once;
-  std::call_once(gt_once, [] { cudaFuncSetAttribute(k_gs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, GT_SMEM); });
+  std::call_once(gt_once, [] {
+    cudaFuncSetAttribute(k_gs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, GT_SMEM);
+    cudaFuncSetAttribute(k_gs_tmx, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
+  });
+  const bool need_reg_upd = upd_kind == 0 || (upd_kind == 1 && maxit + 1 > GT_MAXCOLS) ||
+                            ((upd_kind & 2) && maxit + 2 > GX_MAXV);
+  const bool need_tma = (upd_kind & 1) && (upd_kind == 1 || usel.split > 0);
+  const bool need_tmx = (upd_kind & 2) && (upd_kind == 2 || maxit + 1 > usel.split);
   const size_t smem_ro = size_t(2 * UP_MAXCOLS + 32) * sizeof(double) + size_t(ns) * sizeof(int);
   int launches_per_iter = 0;
   // Profiling hook: called after every launch with a kernel-class id.
@@ -1968,13 +2310,18 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     mark(PK_SMALL);
     if (fused) {
       --launches_per_iter;
-      if (gt_on) {
-        k_gs_tma<<<unsigned(gc_upd.ncl), GT_THREADS, GT_SMEM, s>>>(dS.get(), ns, G);
+      if (need_tma) {
+        k_gs_tma<<<unsigned(gc_upd.ncl), GT_THREADS, GT_SMEM, s>>>(dS.get(), ns, G, usel);
         ++launches_per_iter;
         mark(PK_UPDPROBE);
       }
-      if (!gt_on || maxit + 1 > GT_MAXCOLS) {
-        MPG_CUDA(gc_launch_any(true, gc_upd, s, dS.get(), ns, G, gt_on ? GT_MAXCOLS : 0));
+      if (need_tmx) {
+        k_gs_tmx<<<unsigned(gc_upd.ncl), GX_THREADS, GX_SMEM, s>>>(dS.get(), ns, G, usel);
+        ++launches_per_iter;
+        mark(PK_UPDPROBE);
+      }
+      if (need_reg_upd) {
+        MPG_CUDA(gc_launch_any(true, gc_upd, s, dS.get(), ns, G, usel));
         ++launches_per_iter;
         mark(PK_UPDPROBE);
       }
