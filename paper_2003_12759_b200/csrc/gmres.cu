@@ -1401,9 +1401,14 @@ __device__ __forceinline__ void gx_producer(GmSolve* S, int ns, int TC, int stag
   }
 }
 
+// CF chunks of a tile are processed together (their load -> row sum -> butterfly
+// chains interleave); each lane then holds NGC = GX_NG / CF groups per chunk, so
+// CF = 1 serves k + 2 <= 384, CF = 2 <= 192, CF = 4 <= 96, CF = 8 <= 32.
+template <int CF>
 __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, int stage_bytes, int NS, long long a,
                                             long long b, uint32_t ring, uint64_t* full, uint64_t* empty, double* red2,
                                             double* red3, UpdSel us) {
+  constexpr int NGC = GX_NG / CF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int rp = warp;  // row pair
   const int slot = blockIdx.x;
@@ -1411,7 +1416,7 @@ __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, i
   const uint32_t loff = uint32_t(lane) * 128u + uint32_t((rp ^ (lane & 7)) << 4);
   GxCursor cu;
   cu.us = us;
-  double coef[GX_NG], acc[GX_NG];
+  double coef[NGC], acc[NGC];
   double wsq = 0.0;
   double* w = nullptr;
   int nj = 0, nchunks = 0, n = 0, pf = 0, mb = 0;
@@ -1432,7 +1437,7 @@ __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, i
       mb = (((nj + 1) & 63) + 7) >> 3;
       woff = uint32_t((rp ^ (nj & 7)) << 4) + uint32_t(nj & 63) * 128u;
 #pragma unroll
-      for (int i = 0; i < GX_NG; ++i) {
+      for (int i = 0; i < NGC; ++i) {
         const int j = 32 * i + lane;
         coef[i] = j < nj ? st.scale[j] * st.h[j] : 0.0;
         acc[i] = 0.0;
@@ -1442,47 +1447,65 @@ __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, i
     const int c0 = int(g - cu.off) * TC;
     mbar_wait(full + stg, fph);
     const uint32_t sbase = ring + uint32_t(stg) * uint32_t(stage_bytes);
-    for (int cc = 0; cc < TC; ++cc) {
-      if (c0 + cc >= nchunks) break;
+    for (int cc0 = 0; cc0 < TC; cc0 += CF) {
+      if (c0 + cc0 >= nchunks) break;
       // chunk cc of full panel p at (p TC + cc) 8 KB; of the last panel at
       // pf TC 8 KB + cc mb KB (its mb 8-vector boxes)
-      const uint32_t cb = sbase + uint32_t(cc) * 8192u;
-      const uint32_t pb = sbase + uint32_t(pf * TC) * 8192u + uint32_t(cc * mb) * 1024u;
-      double2 v[GX_NG];
+      double2 v[CF][NGC], wp[CF];
+      double sx[CF], sy[CF];
 #pragma unroll
-      for (int i = 0; i < GX_NG; ++i) {
-        const uint32_t a = ((i >> 1) < pf ? cb + uint32_t((i >> 1) * TC) * 8192u : pb) + uint32_t(i & 1) * 4096u + loff;
-        v[i] = 32 * i + lane < nj ? lds_f64x2(a) : make_double2(0.0, 0.0);
-      }
-      const double2 wp = lds_f64x2(((nj >> 6) < pf ? cb + uint32_t((nj >> 6) * TC) * 8192u : pb) + woff);
-      double sx0 = 0.0, sx1 = 0.0, sy0 = 0.0, sy1 = 0.0;
+      for (int f = 0; f < CF; ++f) {
+        const int cc = cc0 + f;
+        const bool ok = c0 + cc < nchunks;
+        const uint32_t cb = sbase + uint32_t(cc) * 8192u;
+        const uint32_t pb = sbase + uint32_t(pf * TC) * 8192u + uint32_t(cc * mb) * 1024u;
 #pragma unroll
-      for (int i = 0; i < GX_NG; i += 2) {
-        sx0 = fma(coef[i], v[i].x, sx0);
-        sy0 = fma(coef[i], v[i].y, sy0);
-        sx1 = fma(coef[i + 1], v[i + 1].x, sx1);
-        sy1 = fma(coef[i + 1], v[i + 1].y, sy1);
-      }
-      double sx = sx0 + sx1, sy = sy0 + sy1;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        sx += __shfl_xor_sync(0xffffffffu, sx, o);
-        sy += __shfl_xor_sync(0xffffffffu, sy, o);
-      }
-      const double wn0 = wp.x - sx, wn1 = wp.y - sy;
-      const int row = (c0 + cc) * CHUNK + 2 * rp;
-      if (lane == 0) {
-        double* dst = w + size_t(c0 + cc) * 1024 + 2 * rp;
-        if (row + 1 < n) {
-          *reinterpret_cast<double2*>(dst) = make_double2(wn0, wn1);
-          wsq = fma(wn0, wn0, fma(wn1, wn1, wsq));
-        } else if (row < n) {
-          dst[0] = wn0;
-          wsq = fma(wn0, wn0, wsq);
+        for (int i = 0; i < NGC; ++i) {
+          const uint32_t ad =
+              ((i >> 1) < pf ? cb + uint32_t((i >> 1) * TC) * 8192u : pb) + uint32_t(i & 1) * 4096u + loff;
+          v[f][i] = ok && 32 * i + lane < nj ? lds_f64x2(ad) : make_double2(0.0, 0.0);
         }
+        wp[f] = ok ? lds_f64x2(((nj >> 6) < pf ? cb + uint32_t((nj >> 6) * TC) * 8192u : pb) + woff)
+                   : make_double2(0.0, 0.0);
+        double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < NGC; ++i) {
+          if (i & 1) {
+            x1 = fma(coef[i], v[f][i].x, x1);
+            y1 = fma(coef[i], v[f][i].y, y1);
+          } else {
+            x0 = fma(coef[i], v[f][i].x, x0);
+            y0 = fma(coef[i], v[f][i].y, y0);
+          }
+        }
+        sx[f] = x0 + x1;
+        sy[f] = y0 + y1;
       }
 #pragma unroll
-      for (int i = 0; i < GX_NG; ++i) acc[i] = fma(v[i].x, wn0, fma(v[i].y, wn1, acc[i]));
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int f = 0; f < CF; ++f) {
+          sx[f] += __shfl_xor_sync(0xffffffffu, sx[f], o);
+          sy[f] += __shfl_xor_sync(0xffffffffu, sy[f], o);
+        }
+#pragma unroll
+      for (int f = 0; f < CF; ++f) {
+        const int cc = cc0 + f;
+        const double wn0 = wp[f].x - sx[f], wn1 = wp[f].y - sy[f];
+        const int row = (c0 + cc) * CHUNK + 2 * rp;
+        if (lane == 0 && c0 + cc < nchunks) {
+          double* dst = w + size_t(c0 + cc) * 1024 + 2 * rp;
+          if (row + 1 < n) {
+            *reinterpret_cast<double2*>(dst) = make_double2(wn0, wn1);
+            wsq = fma(wn0, wn0, fma(wn1, wn1, wsq));
+          } else if (row < n) {
+            dst[0] = wn0;
+            wsq = fma(wn0, wn0, wsq);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < NGC; ++i) acc[i] = fma(v[f][i].x, wn0, fma(v[f][i].y, wn1, acc[i]));
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + stg);
@@ -1493,7 +1516,7 @@ __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, i
     if (g + 1 == seg_end) {  // flush this solve's partials
       GmSolve& st = S[cu.s];
 #pragma unroll
-      for (int i = 0; i < GX_NG; ++i)
+      for (int i = 0; i < NGC; ++i)
         if (32 * i + lane < nj) red2[warp * GX_MAXV + 32 * i + lane] = acc[i];
       if (lane == 0) red3[warp] = wsq;
       consumers_bar();
@@ -1528,8 +1551,9 @@ __global__ void __launch_bounds__(GX_THREADS, 1) k_gs_tmx(GmSolve* S, int ns, in
   if (nvmax == 0) return;
   // tile = TC chunks of up to about 48 KB (at least 4 stages in the ring)
   const int chunk_bytes = (nvmax >> 6) * 8192 + (((nvmax & 63) + 7) >> 3) * 1024;
+  const int CF = nvmax <= 32 ? 8 : nvmax <= 96 ? 4 : nvmax <= 192 ? 2 : 1;
   int TC = 1;
-  while (TC < 16 && 2 * TC * chunk_bytes <= 48 * 1024) TC *= 2;
+  while (TC < 16 && (TC < CF || 2 * TC * chunk_bytes <= 48 * 1024)) TC *= 2;
   const int stage_bytes = TC * chunk_bytes;
   const int NS = min(GX_MAXST, GX_RING / stage_bytes);
   long long total = 0;
@@ -1561,7 +1585,12 @@ __global__ void __launch_bounds__(GX_THREADS, 1) k_gs_tmx(GmSolve* S, int ns, in
   if (threadIdx.x >= GX_CWARPS * 32)
     gx_producer(S, ns, TC, stage_bytes, NS, a, b, ring, full, empty, us);
   else
-    gx_consumer(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+    switch (CF) {
+      case 8: gx_consumer<8>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
+      case 4: gx_consumer<4>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
+      case 2: gx_consumer<2>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
+      default: gx_consumer<1>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
+    }
 }
 
 // ---- norm partials of the residual buffer ----------------------------------------
@@ -2310,21 +2339,20 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     mark(PK_SMALL);
     if (fused) {
       --launches_per_iter;
+      // one profile interval for the pass, whichever kernels own its solves
       if (need_tma) {
         k_gs_tma<<<unsigned(gc_upd.ncl), GT_THREADS, GT_SMEM, s>>>(dS.get(), ns, G, usel);
         ++launches_per_iter;
-        mark(PK_UPDPROBE);
       }
       if (need_tmx) {
         k_gs_tmx<<<unsigned(gc_upd.ncl), GX_THREADS, GX_SMEM, s>>>(dS.get(), ns, G, usel);
         ++launches_per_iter;
-        mark(PK_UPDPROBE);
       }
       if (need_reg_upd) {
         MPG_CUDA(gc_launch_any(true, gc_upd, s, dS.get(), ns, G, usel));
         ++launches_per_iter;
-        mark(PK_UPDPROBE);
       }
+      mark(PK_UPDPROBE);
     } else {
       k_update<<<gG, 256, smem_upd, s>>>(dS.get(), G, 0);
       mark(PK_UPD);
