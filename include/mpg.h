@@ -263,6 +263,9 @@ int mpg_gen_random_sparse(int64_t r, int64_t c, double density, uint64_t seed, d
 int mpg_gen_from_triplets(int64_t nr, int64_t nc, int64_t nnz, const int64_t* ri, const int64_t* ci, const double* v,
                           mpg_host_csr** out);
 int mpg_gen_bilinear_toy(int64_t n, int64_t m, uint64_t seed, mpg_host_csr** k_out, double* f, double* c);
+/* generate_qb_toy (proj/src/generator.cpp:181-207): D, K, N (n x n), H (n x n^2, column b n + c); F = C = e_1. */
+int mpg_gen_qb_toy(int64_t n, uint64_t seed, mpg_host_csr** d, mpg_host_csr** k, mpg_host_csr** n_op,
+                   mpg_host_csr** h);
 int mpg_gen_grid2d(int64_t N, uint64_t seed, mpg_host_system** out);
 int mpg_gen_convdiff3d(int64_t M, uint64_t seed, mpg_host_system** out);
 int mpg_gen_fem3d(int64_t N, uint64_t seed, int mimo, mpg_host_system** out);

@@ -100,6 +100,10 @@ _SIGS = {
                                   vp, vp, vp, vp, vp, vp, vp, ip, ip, vp, C.c_int, ip]),
     "orc_spai_bench": (C.c_int, [vp, vp, vp, C.c_int, vp, C.POINTER(SpaiCfg), C.POINTER(GmresCfg), C.c_int, C.c_int,
                                  vp, vp, C.c_int, ip, ip]),
+    "orc_qbihomm_reduce": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, vp, C.c_int, C.c_int, C.POINTER(GmresCfg),
+                                     C.POINTER(SpaiCfg), C.c_int, C.c_longlong, C.c_int, C.c_int, ip, vp, vp, vp, vp,
+                                     vp, vp, vp, vp, C.c_int, ip]),
+    "orc_kron_compress_quadratic": (C.c_int, [vp, vp, C.c_longlong, C.c_longlong, vp]),
 }
 for _n, (_r, _a) in _SIGS.items():
     _f = getattr(lib, _n)
@@ -535,3 +539,71 @@ def spai_bench(a: Csr, e: Optional[Csr], b, points: Sequence[float], spai: SpaiC
     _check(lib.orc_spai_bench(a._h, e._h if e else None, _p(b), len(pts), _p(pts), C.byref(s), C.byref(g), mode,
                               max_chain_len, _p(x), rows, len(pts), C.byref(nrows), C.byref(failed)))
     return [rows[i] for i in range(nrows.value)], failed.value, x
+
+
+@dataclasses.dataclass
+class QbConfig:
+    """QbConfig (proj/include/morprec/qbihomm.hpp:35-43)."""
+    sigmas: Sequence[float] = ()
+    p_moments: int = 1
+    q_moments: int = 1
+    gmres: GmresConfig = dataclasses.field(default_factory=GmresConfig)
+    spai: SpaiConfig = dataclasses.field(default_factory=SpaiConfig)
+    max_chain_len: int = 16
+    standard_residual_max_dim: int = 5000
+
+
+@dataclasses.dataclass
+class ReducedQb:
+    d: np.ndarray
+    k: np.ndarray
+    n_op: np.ndarray
+    h: np.ndarray
+    f: np.ndarray
+    c: np.ndarray
+    basis: np.ndarray
+    rows: list
+
+    def order(self) -> int:
+        return self.d.shape[0]
+
+    def linear_transfer(self, s: float) -> float:
+        """c^T (s D_r - K_r)^{-1} f (the basis-invariant check of test_qbihomm.cpp:200-207)."""
+        return float(self.c[:, 0] @ np.linalg.solve(s * self.d - self.k, self.f[:, 0]))
+
+
+def qbihomm_reduce(d: Csr, k: Csr, n_op: Csr, h: Csr, f, c, cfg: QbConfig, mode: int = 2) -> ReducedQb:
+    """qbihomm_reduce (proj/src/qbihomm.cpp:144-208); mode 0 None, 1 FreshSpai, 2 ReuseChain."""
+    n = d.shape[0]
+    for name, v in (("F", f), ("C", c)):  # QbSystem::create (qbihomm.cpp:30-33)
+        a = np.asarray(v)
+        if a.ndim == 2 and a.shape[1] != 1 or a.size != n:
+            raise ConfigError(f"quadratic-bilinear system: {name} must be a single n-column (SISO)")
+    f, c = _f64(f).reshape(-1), _f64(c).reshape(-1)
+    sig = _f64(cfg.sigmas)
+    cap = max(1, len(sig) * (cfg.p_moments + 2 * cfg.q_moments + 2))
+    basis = np.zeros((n, cap), order="F")
+    rd, rk, rn = (np.zeros((cap, cap), order="F") for _ in range(3))
+    rh = np.zeros((cap, cap * cap), order="F")
+    rf, rc = np.zeros(cap), np.zeros(cap)
+    order, nrows = C.c_int(), C.c_int()
+    maxrows = 4 * max(1, len(sig))
+    rows = (ReportRow * maxrows)()
+    g, s = cfg.gmres.c(), cfg.spai.c()
+    _check(lib.orc_qbihomm_reduce(d._h, k._h, n_op._h, h._h, _p(f), _p(c), len(sig), _p(sig), cfg.p_moments,
+                                  cfg.q_moments, C.byref(g), C.byref(s), cfg.max_chain_len,
+                                  cfg.standard_residual_max_dim, mode, cap, C.byref(order), _p(basis), _p(rd), _p(rk),
+                                  _p(rn), _p(rh), _p(rf), _p(rc), rows, maxrows, C.byref(nrows)))
+    r = order.value
+    take = lambda a, rr, cc: np.asfortranarray(a.reshape(-1, order="F")[: rr * cc].reshape((rr, cc), order="F"))
+    return ReducedQb(take(rd, r, r), take(rk, r, r), take(rn, r, r), take(rh, r, r * r), rf[:r].reshape(r, 1).copy(),
+                     rc[:r].reshape(r, 1).copy(), take(basis, n, r), [rows[i] for i in range(min(nrows.value, maxrows))])
+
+
+def kron_compress_quadratic(h: Csr, u) -> np.ndarray:
+    """kron_compress_quadratic (proj/src/qbihomm.cpp:210-236)."""
+    u = np.asfortranarray(np.asarray(u, dtype=np.float64))
+    n, r = u.shape
+    out = np.zeros((r, r * r), order="F")
+    _check(lib.orc_kron_compress_quadratic(h._h, _p(u), n, r, _p(out)))
+    return out

@@ -346,4 +346,39 @@ int orc_spai_bench(const Csr* a, const Csr* e, const double* b, int npoints, con
   });
 }
 
+// QB-IHOMM (proj/src/qbihomm.cpp:144-208). Outputs for reduced order r <=
+// max_order: basis (n x r), red_d/k/n (r x r), red_h (r x r^2), red_f/c (r).
+int orc_qbihomm_reduce(const Csr* d, const Csr* k, const Csr* n_op, const Csr* h, const double* f, const double* c,
+                       int npoints, const double* sigmas, int p_moments, int q_moments, const orc_gmres_cfg* gmres,
+                       const orc_spai_cfg* spai, int max_chain_len, long long sr_max_dim, int mode, int max_order,
+                       int* order, double* basis, double* red_d, double* red_k, double* red_n, double* red_h,
+                       double* red_f, double* red_c, orc_report_row* rows, int max_rows, int* nrows) {
+  return guard([&] {
+    QbSystem sys;
+    sys.d = *d; sys.k = *k; sys.n_op = *n_op; sys.h = *h;
+    sys.f.assign(f, f + d->nrows);
+    sys.c.assign(c, c + d->nrows);
+    QbConfig cfg;
+    cfg.sigmas.assign(sigmas, sigmas + npoints);
+    cfg.p_moments = p_moments; cfg.q_moments = q_moments;
+    cfg.gmres = to_gmres(gmres); cfg.spai = to_spai(spai);
+    cfg.max_chain_len = max_chain_len; cfg.standard_residual_max_dim = sr_max_dim;
+    auto [red, rep] = qbihomm_reduce(sys, cfg, PrecondMode(mode));
+    const int r = int(red.d.rows);
+    *order = r;
+    if (r > max_order) throw std::invalid_argument("qbihomm: reduced order exceeds max_order");
+    auto put = [](double* dst, const Dense& m) { if (dst) std::memcpy(dst, m.a.data(), m.a.size() * sizeof(double)); };
+    put(basis, red.basis); put(red_d, red.d); put(red_k, red.k); put(red_n, red.n_op); put(red_h, red.h);
+    put(red_f, red.f); put(red_c, red.c);
+    copy_rows(rep, rows, max_rows, nrows);
+  });
+}
+
+int orc_kron_compress_quadratic(const Csr* h, const double* u, long long n, long long r, double* out) {
+  return guard([&] {
+    const Dense m = kron_compress_quadratic(*h, dense_from(u, n, r));
+    std::memcpy(out, m.a.data(), m.a.size() * sizeof(double));
+  });
+}
+
 }  // extern "C"

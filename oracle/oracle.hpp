@@ -258,4 +258,32 @@ SweepResult run_spai_bench(const Csr& a, const Csr* e, const Vec& b, const std::
                            const SpaiConfig& spai, const GmresConfig& gmres, PrecondMode mode,
                            int max_chain_len, bool keep_solutions);
 
+// ---- QB-IHOMM (proj/src/qbihomm.cpp, proj/src/orth.cpp) -------------------
+struct QbSystem {
+  Csr d, k, n_op;  // n x n
+  Csr h;           // n x n^2, column b n + c
+  Vec f, c;        // n (SISO)
+  void validate() const;
+};
+struct QbConfig {
+  std::vector<double> sigmas;
+  int p_moments = 1, q_moments = 1;
+  GmresConfig gmres{};
+  SpaiConfig spai{};
+  int max_chain_len = 16;
+  index_t standard_residual_max_dim = 5000;
+};
+struct ReducedQb { Dense d, k, n_op, h, f, c, basis; };
+struct OrthBasis {
+  index_t dim = 0, capacity = 0;
+  std::vector<Vec> cols;
+  OrthBasis(index_t d, index_t cap) : dim(d), capacity(cap) {
+    if (d <= 0 || cap <= 0) throw std::invalid_argument("orth: dimension and capacity must be positive");
+  }
+  bool append(const Vec& col, double drop_tol = 1e-10);
+  Dense matrix() const;
+};
+Dense kron_compress_quadratic(const Csr& h, const Dense& u);
+std::pair<ReducedQb, ReductionReport> qbihomm_reduce(const QbSystem& sys, const QbConfig& cfg, PrecondMode mode);
+
 }  // namespace oracle

@@ -233,6 +233,47 @@ int mpg_gen_bilinear_toy(int64_t n, int64_t m, uint64_t seed, mpg_host_csr** k_o
   });
 }
 
+// generate_qb_toy (proj/src/generator.cpp:181-207): D = tridiag(-1, 4, -1),
+// K = -tridiag(-1, 2.5, -1), N one entry per row (i, node, 0.05 sym), H two
+// entries per row (a, b n + c, 0.1 sym) with draws in the reference's order
+// (node, then sym; b, c, then sym); F = C = e_1 (returned by the caller).
+int mpg_gen_qb_toy(int64_t n, uint64_t seed, mpg_host_csr** d, mpg_host_csr** k, mpg_host_csr** n_op,
+                   mpg_host_csr** h) {
+  return gen_guard([&] {
+    if (n < 2) throw std::invalid_argument("generator: n must be at least 2");
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> sym(-1.0, 1.0);
+    std::uniform_int_distribution<int64_t> node(0, n - 1);
+    auto tridiag = [n](double off, double diag, double scale) {
+      std::vector<Trip> t;
+      for (int64_t i = 0; i < n; ++i) {
+        t.push_back({i, i, scale * diag});
+        if (i + 1 < n) {
+          t.push_back({i, i + 1, scale * off});
+          t.push_back({i + 1, i, scale * off});
+        }
+      }
+      return from_trips(n, n, std::move(t));
+    };
+    *d = tridiag(-1.0, 4.0, 1.0);
+    *k = tridiag(-1.0, 2.5, -1.0);
+    std::vector<Trip> nt;
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t j = node(rng);
+      nt.push_back({i, j, 0.05 * sym(rng)});
+    }
+    *n_op = from_trips(n, n, std::move(nt));
+    std::vector<Trip> ht;
+    for (int64_t a = 0; a < n; ++a)
+      for (int e = 0; e < 2; ++e) {
+        const int64_t b = node(rng);
+        const int64_t c = node(rng);
+        ht.push_back({a, b * n + c, 0.1 * sym(rng)});
+      }
+    *h = from_trips(n, n * n, std::move(ht));
+  });
+}
+
 // C1: 2D cell-centred 5-point diffusion on an N x N grid.
 int mpg_gen_grid2d(int64_t N, uint64_t seed, mpg_host_system** out) {
   return gen_guard([&] {

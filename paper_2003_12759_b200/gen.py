@@ -113,6 +113,31 @@ def bilinear_toy(n: int, m: int, seed: int):
     return _take_csr(p), f.reshape((n, m), order="F"), c.reshape((n, 1))
 
 
+@dataclasses.dataclass
+class QbSystem:
+    """D x' = K x + H (x (x) x) + N x u + F u, y = C^T x (proj/include/morprec/qbihomm.hpp:15-33)."""
+    d: HostCsr
+    k: HostCsr
+    n_op: HostCsr
+    h: HostCsr  # n x n^2, column b n + c
+    f: np.ndarray  # n
+    c: np.ndarray  # n
+
+    @property
+    def n(self) -> int:
+        return self.d.nrows
+
+
+def qb_toy(n: int, seed: int) -> QbSystem:
+    """generate_qb_toy (proj/src/generator.cpp:181-207): F = C = e_1."""
+    ps = [C.POINTER(L.HostCsr)() for _ in range(4)]
+    _check(lib.mpg_gen_qb_toy(n, seed, *[C.byref(p) for p in ps]))
+    d, k, nop, h = (_take_csr(p) for p in ps)
+    e1 = np.zeros(n)
+    e1[0] = 1.0
+    return QbSystem(d, k, nop, h, e1, e1.copy())
+
+
 def _take_system(p) -> System:
     s = p.contents
     n = s.n
