@@ -327,4 +327,65 @@ inline std::pair<BirkaState, ReductionReport> birka_reduce(const ShiftedOperator
   return {std::move(st), std::move(rep)};
 }
 
+// ---- QB-IHOMM (qbihomm.hpp:15-71) ------------------------------------------------
+// QbSystem with H given as triplets (row a, column b n + c, value).
+struct QbSystem {
+  SparseMatrix d, k, n_op;
+  std::vector<index_t> h_rows, h_cols;
+  std::vector<double> h_vals;
+  std::vector<double> f, c;  // SISO
+  index_t dim() const { return d.rows(); }
+};
+
+struct QbConfig {  // qbihomm.hpp:35-43
+  std::vector<double> sigmas;
+  int p_moments = 1, q_moments = 1;
+  GmresConfig gmres{};
+  SpaiConfig spai{};
+  int max_chain_len = 16;
+  index_t standard_residual_max_dim = 5000;
+};
+
+struct ReducedQb {  // qbihomm.hpp:45-52, column-major
+  int order = 0;
+  std::vector<double> d, k, n_op, h, f, c, basis;
+};
+
+// qbihomm_reduce (qbihomm.hpp:66-67): the moment solves run on the device.
+inline std::pair<ReducedQb, ReductionReport> qbihomm_reduce(const QbSystem& sys, const QbConfig& cfg, PrecondMode mode) {
+  const ShiftedOperator op(sys.k, &sys.d);
+  mpg_qb_cfg q{};
+  q.p_moments = cfg.p_moments;
+  q.q_moments = cfg.q_moments;
+  q.gmres = cfg.gmres.c();
+  q.spai = cfg.spai.c();
+  q.max_chain_len = cfg.max_chain_len;
+  q.standard_residual_max_dim = cfg.standard_residual_max_dim;
+  const size_t n = static_cast<size_t>(sys.dim());
+  const size_t cap = std::max<size_t>(1, cfg.sigmas.size() * static_cast<size_t>(cfg.p_moments + 2 * cfg.q_moments + 2));
+  ReducedQb red;
+  std::vector<double> basis(n * cap), d(cap * cap), k(cap * cap), nn(cap * cap), h(cap * cap * cap), f(cap), c(cap);
+  ReductionReport rep;
+  rep.rows.resize(4 * std::max<size_t>(1, cfg.sigmas.size()));
+  int order = 0, nrows = 0;
+  check(mpg_qbihomm_reduce(op.handle(), sys.n_op.handle(), static_cast<int64_t>(sys.h_vals.size()), sys.h_rows.data(),
+                           sys.h_cols.data(), sys.h_vals.data(), sys.f.data(), sys.c.data(),
+                           static_cast<int>(cfg.sigmas.size()), cfg.sigmas.data(), &q, static_cast<int>(mode),
+                           static_cast<int>(cap), &order, basis.data(), d.data(), k.data(), nn.data(), h.data(),
+                           f.data(), c.data(), rep.rows.data(), static_cast<int>(rep.rows.size()), &nrows));
+  const size_t r = static_cast<size_t>(order);
+  red.order = order;
+  red.d.assign(d.begin(), d.begin() + long(r * r));
+  red.k.assign(k.begin(), k.begin() + long(r * r));
+  red.n_op.assign(nn.begin(), nn.begin() + long(r * r));
+  red.h.assign(h.begin(), h.begin() + long(r * r * r));
+  red.f.assign(f.begin(), f.begin() + long(r));
+  red.c.assign(c.begin(), c.begin() + long(r));
+  red.basis.assign(basis.begin(), basis.begin() + long(n * r));
+  rep.rows.resize(static_cast<size_t>(std::min<int>(nrows, static_cast<int>(rep.rows.size()))));
+  rep.converged = true;
+  rep.sweeps = 1;
+  return {std::move(red), std::move(rep)};
+}
+
 }  // namespace morprec_gpu

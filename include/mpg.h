@@ -236,6 +236,32 @@ int mpg_spai_bench(const mpg_op* op, const double* b, int npoints, const double*
                    const mpg_gmres_cfg* gmres, int mode, int max_chain_len, double* x_out, mpg_report_row* rows,
                    int max_rows, int* nrows, int* failed);
 
+/* ---- QB-IHOMM: qbihomm_reduce (proj/src/qbihomm.cpp:144-208) -------------
+ * QbConfig (proj/include/morprec/qbihomm.hpp:35-43). */
+typedef struct {
+  int p_moments, q_moments;
+  mpg_gmres_cfg gmres;
+  mpg_spai_cfg spai;
+  int max_chain_len;
+  long long standard_residual_max_dim;
+} mpg_qb_cfg;
+
+/* D x' = K x + H (x (x) x) + N x u + F u, y = C^T x (SISO). `op` is the
+ * shifted family built by mpg_op_create(K, D) (A = K, E = D; D may be NULL =
+ * identity); n_op = N; H (n x n^2) as host triplets (row a, column b n + c,
+ * value; duplicates summed). f, c: n-vectors, any memory. Trial side solves
+ * (sigma_i D - K) x = F and p + q further moments against D x_prev; test side
+ * (2 sigma_i D - K)^T y = C and q moments against D^T y_prev; the union basis
+ * U (two-pass MGS with deflation, orth.cpp:16-40) gives the reduced model
+ * U^T D U, U^T K U, U^T N U, U^T H (U (x) U) (r x r^2), U^T F, U^T C.
+ * Outputs for order r <= max_order (host; basis n x r any memory; any may be
+ * NULL). Non-convergence raises MPG_ERR_SOLVER (qbihomm.cpp:120-129). */
+int mpg_qbihomm_reduce(const mpg_op* op, const mpg_csr* n_op, int64_t h_nnz, const int64_t* h_row,
+                       const int64_t* h_col, const double* h_val, const double* f, const double* c, int npoints,
+                       const double* sigmas, const mpg_qb_cfg* cfg, int mode, int max_order, int* order,
+                       double* basis, double* red_d, double* red_k, double* red_n, double* red_h, double* red_f,
+                       double* red_c, mpg_report_row* rows, int max_rows, int* nrows);
+
 /* ---- host-side synthetic inputs (gen/generators.cpp) ---------------------- */
 typedef struct {
   int64_t nrows, ncols, nnz;

@@ -75,6 +75,11 @@ class IrkaCfg(C.Structure):
                 ("mirror_unstable", C.c_int)]
 
 
+class QbCfg(C.Structure):
+    _fields_ = [("p_moments", C.c_int), ("q_moments", C.c_int), ("gmres", GmresCfg), ("spai", SpaiCfg),
+                ("max_chain_len", C.c_int), ("standard_residual_max_dim", C.c_longlong)]
+
+
 class ReportRow(C.Structure):
     _fields_ = [("sweep", C.c_int), ("point", C.c_int), ("kind", C.c_int), ("solves", C.c_int),
                 ("iterations", C.c_longlong), ("build_seconds", C.c_double), ("gmres_seconds", C.c_double),
@@ -139,6 +144,8 @@ _SIGS = {
                              ip, ip, vp, _I, ip]),
     "mpg_irka_reduce_sharded": (_I, [vp, vp, _I, vp, _I, C.POINTER(IrkaCfg), _I, vp, _I, _I, ALLGATHER_FN, vp, vp,
                                      vp, vp, vp, vp, ip, ip, vp, _I, ip]),
+    "mpg_qbihomm_reduce": (_I, [vp, vp, _L, vp, vp, vp, vp, vp, _I, vp, C.POINTER(QbCfg), _I, _I, ip] + [vp] * 8
+                           + [_I, ip]),
     "mpg_spai_bench": (_I, [vp, vp, _I, vp, C.POINTER(SpaiCfg), C.POINTER(GmresCfg), _I, _I, vp, vp, _I, ip, ip]),
     "mpg_gen_last_error": (C.c_char_p, []),
     "mpg_host_csr_free": (None, [C.POINTER(HostCsr)]),

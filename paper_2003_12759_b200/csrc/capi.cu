@@ -1,5 +1,6 @@
 // extern "C" entry points of libmpg.so (include/mpg.h): thin wrappers that
 // translate the reference's exception classes into status codes.
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -451,6 +452,75 @@ int mpg_spai_bench(const mpg_op* op, const double* b, int npoints, const double*
                                to_gmres(gmres), mode, max_chain_len, x_out);
     copy_rows(o.rows, rows, max_rows, nrows);
     if (failed) *failed = o.failed;
+  });
+}
+
+int mpg_qbihomm_reduce(const mpg_op* op, const mpg_csr* n_op, int64_t h_nnz, const int64_t* h_row,
+                       const int64_t* h_col, const double* h_val, const double* f, const double* c, int npoints,
+                       const double* sigmas, const mpg_qb_cfg* cfg, int mode, int max_order, int* order,
+                       double* basis, double* red_d, double* red_k, double* red_n, double* red_h, double* red_f,
+                       double* red_c, mpg_report_row* rows, int max_rows, int* nrows) {
+  return guard([&] {
+    if (!op || !n_op || !cfg || !f || !c || (npoints > 0 && !sigmas) || h_nnz < 0 || (h_nnz > 0 && !(h_row && h_col && h_val)))
+      throw std::invalid_argument("qbihomm: null argument");
+    const ShiftedOp& o = *op->p;
+    const int64_t n = o.n;
+    if (n_op->p->device != o.device) throw std::invalid_argument("qbihomm: N on a different device");
+    // H: sorted by row, duplicates summed (SparseMatrix::from_triplets, sparse.cpp:80-115)
+    struct E { int64_t r, col; double v; };
+    std::vector<E> t(static_cast<size_t>(h_nnz));
+    for (int64_t i = 0; i < h_nnz; ++i) {
+      if (h_row[i] < 0 || h_row[i] >= n || h_col[i] < 0 || h_col[i] >= n * n)
+        throw std::invalid_argument("qbihomm: H entry out of range (H is n x n^2)");
+      t[size_t(i)] = {h_row[i], h_col[i], h_val[i]};
+    }
+    std::stable_sort(t.begin(), t.end(), [](const E& a, const E& b) { return a.r != b.r ? a.r < b.r : a.col < b.col; });
+    std::vector<int> rp(size_t(n) + 1, 0), bc, cc;
+    std::vector<double> hv;
+    for (size_t p = 0; p < t.size();) {
+      const int64_t r = t[p].r, col = t[p].col;
+      double v = 0.0;
+      while (p < t.size() && t[p].r == r && t[p].col == col) v += t[p++].v;
+      bc.push_back(int(col / n));
+      cc.push_back(int(col % n));
+      hv.push_back(v);
+      ++rp[size_t(r) + 1];
+    }
+    for (int64_t i = 0; i < n; ++i) rp[size_t(i) + 1] += rp[size_t(i)];
+    DeviceGuard g(o.device);
+    cudaStream_t s = ctx(o.device).stream;
+    QbH h;
+    h.n = n;
+    h.nnz = int64_t(hv.size());
+    h.rowptr = DBuf<int>(o.device, rp.size());
+    h.bcol = DBuf<int>(o.device, std::max<size_t>(1, bc.size()));
+    h.ccol = DBuf<int>(o.device, std::max<size_t>(1, cc.size()));
+    h.val = DBuf<double>(o.device, std::max<size_t>(1, hv.size()));
+    MPG_CUDA(cudaMemcpyAsync(h.rowptr.get(), rp.data(), rp.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    if (!hv.empty()) {
+      MPG_CUDA(cudaMemcpyAsync(h.bcol.get(), bc.data(), bc.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+      MPG_CUDA(cudaMemcpyAsync(h.ccol.get(), cc.data(), cc.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+      MPG_CUDA(cudaMemcpyAsync(h.val.get(), hv.data(), hv.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    QbSettings qs;
+    qs.sigmas.assign(sigmas, sigmas + std::max(npoints, 0));
+    qs.p_moments = cfg->p_moments;
+    qs.q_moments = cfg->q_moments;
+    qs.gmres = to_gmres(&cfg->gmres);
+    qs.spai = to_spai(&cfg->spai);
+    qs.max_chain_len = cfg->max_chain_len;
+    qs.standard_residual_max_dim = cfg->standard_residual_max_dim;
+    qs.mode = mode;
+    QbOutcome r = qbihomm_run(o, *n_op->p, h, f, c, qs);
+    if (order) *order = r.r;
+    if (r.r > max_order) throw std::invalid_argument("qbihomm: reduced order exceeds max_order");
+    auto put = [](double* dst, const host::Mat& m) { if (dst) std::memcpy(dst, m.a.data(), m.a.size() * sizeof(double)); };
+    put(red_d, r.d); put(red_k, r.k); put(red_n, r.n_op); put(red_h, r.h); put(red_f, r.f); put(red_c, r.c);
+    if (basis) {
+      copy_out(basis, r.basis.get(), size_t(n) * size_t(r.r), s);
+      MPG_CUDA(cudaStreamSynchronize(s));
+    }
+    copy_rows(r.rows, rows, max_rows, nrows);
   });
 }
 

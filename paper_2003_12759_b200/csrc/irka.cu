@@ -599,4 +599,308 @@ SweepOutcome sweep_run(const ShiftedOp& op, const double* b_any, const std::vect
   return out;
 }
 
+// ---- QB-IHOMM (proj/src/qbihomm.cpp:57-238) ----------------------------------
+// Both sides' preconditioners are built first (the horizontal chain across
+// points depends only on the matrices, chain.cpp:16-98); the moment solves are
+// then advanced moment by moment, every (side, point) of one moment in one
+// GMRES batch (solves of a moment are independent; moment j + 1 needs moment
+// j's solution for its right-hand side D x_j / D^T y_j). The union basis is
+// built by two-pass modified Gram-Schmidt with the reference's deflation rule
+// (orth.cpp:16-40) on the device; the reduced matrices are tall-skinny Gram
+// products (K5) and the quadratic term is compressed without U (x) U.
+namespace {
+
+__global__ void k_axpy(double* __restrict__ y, double a, const double* __restrict__ x, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+__global__ void k_scal(double* __restrict__ y, double a, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    y[i] *= a;
+}
+
+// kron_compress_quadratic (qbihomm.cpp:210-236): thread (q, s) of a
+// block owns column q r + s of the r x r^2 result and accumulates, over its
+// block's rows a, out(p, t) += U(a, p) * sum_e h_e U(b_e, q) U(c_e, s).
+// part[blk][p + r t]; rows with more than QC_E entries are taken in slices.
+constexpr int QC_E = 8;
+template <int RM>
+__global__ void __launch_bounds__(RM * RM) k_qcompress(const int* __restrict__ rowptr, const int* __restrict__ bcol,
+                                                       const int* __restrict__ ccol, const double* __restrict__ val,
+                                                       const double* __restrict__ U, int64_t n, int r,
+                                                       double* __restrict__ part) {
+  __shared__ double ua[RM], ub[QC_E][RM], uc[QC_E][RM];
+  __shared__ double hv[QC_E];
+  const int t = threadIdx.x, q = t / RM, s = t % RM;  // blockDim = RM * RM
+  const bool mine = q < r && s < r;
+  double racc[RM];
+#pragma unroll
+  for (int p = 0; p < RM; ++p) racc[p] = 0.0;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t a0 = per * blockIdx.x, a1 = min(n, a0 + per);
+  for (int64_t a = a0; a < a1; ++a) {
+    const int e0 = rowptr[a], e1 = rowptr[a + 1];
+    if (e0 == e1) continue;
+    double hsum = 0.0;
+    for (int eb = e0; eb < e1; eb += QC_E) {
+      const int ne = min(QC_E, e1 - eb);
+      __syncthreads();
+      if (t < ne * RM) {
+        const int e = t / RM, j = t % RM;
+        if (j < r) {
+          ub[e][j] = U[bcol[eb + e] + n * j];
+          uc[e][j] = U[ccol[eb + e] + n * j];
+        }
+        if (j == 0) hv[e] = val[eb + e];
+      }
+      if (eb == e0 && t < r) ua[t] = U[a + n * t];
+      __syncthreads();
+      if (mine)
+        for (int e = 0; e < ne; ++e) hsum = fma(hv[e] * ub[e][q], uc[e][s], hsum);
+    }
+    if (mine) {
+#pragma unroll
+      for (int p = 0; p < RM; ++p)
+        if (p < r) racc[p] = fma(ua[p], hsum, racc[p]);
+    }
+  }
+  if (!mine) return;
+  const int col = q * r + s;
+  double* dst = part + size_t(blockIdx.x) * size_t(r) * size_t(r) * size_t(r);
+#pragma unroll
+  for (int p = 0; p < RM; ++p)
+    if (p < r) dst[p + size_t(r) * col] = racc[p];
+}
+
+__global__ void k_sum_blocks(const double* __restrict__ part, int blocks, int64_t len, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < len; i += int64_t(gridDim.x) * blockDim.x) {
+    double v = 0.0;
+    for (int b = 0; b < blocks; ++b) v += part[size_t(b) * size_t(len) + size_t(i)];
+    out[i] = v;
+  }
+}
+
+std::string shortest(double v) {
+  char buf[64];
+  for (int prec = 1; prec <= 17; ++prec) {
+    std::snprintf(buf, sizeof buf, "%.*g", prec, v);
+    if (std::strtod(buf, nullptr) == v) break;
+  }
+  return buf;
+}
+
+}  // namespace
+
+QbOutcome qbihomm_run(const ShiftedOp& op, const DevCsr& n_op, const QbH& h, const double* f_any, const double* c_any,
+                      const QbSettings& cfg) {
+  const int dev = op.device;
+  auto& cx = ctx(dev);
+  DeviceGuard guard(dev);
+  cudaStream_t s = cx.stream;
+  const int64_t n = op.n;
+  // QbSystem::create (qbihomm.cpp:17-43)
+  if (!op.e) {
+    // E = I is allowed (D = I); nothing to check
+  }
+  if (n_op.nrows != n || n_op.ncols != n) throw ConfigError("quadratic-bilinear system: N must be n x n");
+  if (h.n != n) throw ConfigError("quadratic-bilinear system: H must be n x n^2");
+  // qbihomm_reduce validation (qbihomm.cpp:146-157)
+  if (cfg.sigmas.empty()) throw ConfigError("qbihomm: at least one interpolation point is required");
+  for (double sg : cfg.sigmas)
+    if (sg == 0.0 || !std::isfinite(sg)) throw ConfigError("qbihomm: interpolation points must be nonzero and finite");
+  for (size_t i = 0; i < cfg.sigmas.size(); ++i)
+    for (size_t j = i + 1; j < cfg.sigmas.size(); ++j)
+      if (cfg.sigmas[i] == cfg.sigmas[j]) throw ConfigError("qbihomm: interpolation points must be distinct");
+  if (cfg.p_moments < 0 || cfg.q_moments < 0) throw ConfigError("qbihomm: moment depths must be nonnegative");
+  if (cfg.max_chain_len < 1) throw ConfigError("qbihomm: max_chain_len must be at least 1");
+
+  const int ell = int(cfg.sigmas.size());
+  const int depth[2] = {cfg.p_moments + cfg.q_moments, cfg.q_moments};
+  const int ncols = ell * (depth[0] + 1) + ell * (depth[1] + 1);
+  if (ncols > 32) throw ConfigError("qbihomm: at most 32 moment columns on the GPU path");
+  DBuf<double> F(dev, size_t(n)), Cv(dev, size_t(n));
+  copy_in(F.get(), f_any, size_t(n), s);
+  copy_in(Cv.get(), c_any, size_t(n), s);
+
+  // ---- preconditioners, per side along the points (qbihomm.cpp:75-108) ----
+  QbOutcome out;
+  std::vector<ChainPtr> chains[2];
+  std::vector<mpg_report_row> build_rows[2], moment_rows[2];
+  for (int side = 0; side < 2; ++side) {
+    ChainPtr chain;
+    CsrPtr prev;
+    for (int i = 0; i < ell; ++i) {
+      mpg_report_row row{};
+      row.sweep = side + 1;
+      row.point = i + 1;
+      row.kind = MPG_KIND_NONE;
+      row.min_residual = row.matrix_change = row.standard_residual = std::nan("");
+      mpg_report_row mrow = row;
+      mrow.kind = MPG_KIND_REUSED_SAME_MATRIX;
+      const double sg = side == 0 ? cfg.sigmas[size_t(i)] : 2.0 * cfg.sigmas[size_t(i)];
+      if (cfg.mode != MPG_PRECOND_NONE) {
+        CsrPtr M = op_explicit(op, sg, 0.0, side == 1);
+        if (cfg.mode == MPG_PRECOND_FRESH || cfg.mode == MPG_PRECOND_REUSE_FROZEN || i == 0 ||
+            chain->length() + 1 > cfg.max_chain_len) {
+          SpaiOutcome so = spai_or_update(M, nullptr, cfg.spai, false);
+          auto ch = std::make_shared<Chain>();
+          ch->factors.push_back(so.p);
+          chain = ch;
+          row.kind = MPG_KIND_FRESH;
+          row.build_seconds = so.build_seconds;
+        } else {
+          SpaiOutcome so = spai_or_update(M, prev, cfg.spai, false);
+          auto ch = std::make_shared<Chain>(*chain);
+          ch->factors.push_back(so.p);
+          chain = ch;
+          row.kind = MPG_KIND_HORIZONTAL;
+          row.build_seconds = so.build_seconds;
+          row.min_residual = so.min_residual;
+          row.matrix_change = so.matrix_change;
+        }
+        prev = M;
+        if (n <= cfg.standard_residual_max_dim) row.standard_residual = std_residual(M, chain);
+      }
+      chains[side].push_back(chain);
+      build_rows[side].push_back(row);
+      moment_rows[side].push_back(mrow);
+    }
+  }
+
+  // ---- moment solves (qbihomm.cpp:115-137) ----
+  // column index of (side, point, moment) in X, in the reference's order
+  auto cidx = [&](int side, int i, int j) { return side == 0 ? i * (depth[0] + 1) + j : ell * (depth[0] + 1) + i * (depth[1] + 1) + j; };
+  DBuf<double> X(dev, size_t(n) * size_t(ncols)), RHS(dev, size_t(n) * size_t(2 * ell));
+  const int maxd = std::max(depth[0], depth[1]);
+  for (int j = 0; j <= maxd; ++j) {
+    struct Job { int side, i; };
+    std::vector<Job> jobs;
+    std::vector<SolveSpec> specs;
+    for (int side = 0; side < 2; ++side)
+      for (int i = 0; i < ell; ++i) {
+        if (j > depth[side]) continue;
+        double* x = X.get() + size_t(n) * size_t(cidx(side, i, j));
+        const double* rhs = side == 0 ? F.get() : Cv.get();
+        if (j > 0) {
+          double* r = RHS.get() + size_t(n) * size_t(side * ell + i);
+          launch_op(op, side == 1, 1.0, 0.0, 0.0, X.get() + size_t(n) * size_t(cidx(side, i, j - 1)), r, nullptr, 1.0, s,
+                    nullptr);  // D x_prev (trial) / D^T y_prev (test)
+          count_launch();
+          rhs = r;
+        }
+        if (device_norm2(dev, rhs, n, s) == 0.0) {
+          MPG_CUDA(cudaMemsetAsync(x, 0, size_t(n) * sizeof(double), s));
+          continue;
+        }
+        SolveSpec sp;
+        sp.sre = side == 0 ? cfg.sigmas[size_t(i)] : 2.0 * cfg.sigmas[size_t(i)];
+        sp.transpose = side == 1;
+        sp.chain = chains[side][size_t(i)];
+        sp.b = rhs;
+        sp.x = x;
+        specs.push_back(sp);
+        jobs.push_back({side, i});
+      }
+    if (specs.empty()) continue;
+    size_t free_b = 0, total_b = 0;
+    MPG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const double per_solve = 8.0 * double(n + 64) * double(cfg.gmres.max_iter + 8) + 1e7;
+    const int per_batch = std::max(1, std::min<int>(16, int(0.7 * double(free_b) / per_solve)));
+    std::vector<GmresOutcome> oc;
+    for (size_t b0 = 0; b0 < specs.size(); b0 += size_t(per_batch)) {
+      std::vector<SolveSpec> batch(specs.begin() + long(b0), specs.begin() + long(std::min(specs.size(), b0 + per_batch)));
+      std::vector<GmresOutcome> o = gmres_batch(op, batch, cfg.gmres);
+      oc.insert(oc.end(), o.begin(), o.end());
+    }
+    for (size_t t = 0; t < jobs.size(); ++t) {
+      const Job jb = jobs[t];
+      mpg_report_row& row = j == 0 ? build_rows[jb.side][size_t(jb.i)] : moment_rows[jb.side][size_t(jb.i)];
+      row.solves += 1;
+      row.iterations += oc[t].iterations;
+      row.gmres_seconds += oc[t].solve_seconds;
+      out.total_iterations += oc[t].iterations;
+      out.total_solves += 1;
+    }
+    for (size_t t = 0; t < jobs.size(); ++t)
+      if (!oc[t].converged)
+        throw SolverError(std::string("qbihomm: gmres did not converge on the ") + (jobs[t].side == 0 ? "trial" : "test") +
+                          " side (sigma_" + std::to_string(jobs[t].i + 1) + " = " +
+                          shortest(cfg.sigmas[size_t(jobs[t].i)]) + ", moment " + std::to_string(j) +
+                          "; the shifted matrix may be singular; relative residual " +
+                          shortest(oc[t].final_residual / std::max(oc[t].rhs_norm, 1e-300)) + ")");
+  }
+  for (int side = 0; side < 2; ++side)
+    for (int i = 0; i < ell; ++i) {
+      out.rows.push_back(build_rows[side][size_t(i)]);
+      if (moment_rows[side][size_t(i)].solves > 0) out.rows.push_back(moment_rows[side][size_t(i)]);
+    }
+
+  // ---- union basis: OrthBasis::append_block per column (orth.cpp:16-40) ----
+  DBuf<double> U(dev, size_t(n) * size_t(ncols));
+  const unsigned gblk = unsigned(std::min<int64_t>((n + 255) / 256, int64_t(cx.sm_count) * 8));
+  int r = 0;
+  for (int col = 0; col < ncols; ++col) {
+    const double* src = X.get() + size_t(n) * size_t(col);
+    const double scale = std::sqrt(device_norm2(dev, src, n, s));
+    if (scale == 0.0) continue;
+    double* w = U.get() + size_t(n) * size_t(r);
+    MPG_CUDA(cudaMemcpyAsync(w, src, size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    for (int pass = 0; pass < 2; ++pass)
+      for (int jj = 0; jj < r; ++jj) {
+        const double* uj = U.get() + size_t(n) * size_t(jj);
+        const double d = ts_gram(dev, uj, n, 1, w, n, 1, n).a[0];
+        k_axpy<<<gblk, 256, 0, s>>>(w, -d, uj, n);
+        MPG_CHECK_LAUNCH();
+        count_launch();
+      }
+    const double nrm = std::sqrt(device_norm2(dev, w, n, s));
+    if (nrm <= 1e-10 * scale) continue;
+    k_scal<<<gblk, 256, 0, s>>>(w, 1.0 / nrm, n);
+    MPG_CHECK_LAUNCH();
+    count_launch();
+    ++r;
+  }
+  if (r == 0) throw SolverError("qbihomm: the collected moment columns are all zero");
+  out.r = r;
+
+  // ---- projections (qbihomm.cpp:195-203) ----
+  DBuf<double> T(dev, size_t(n) * size_t(r));
+  for (int which = 0; which < 3; ++which) {
+    for (int jj = 0; jj < r; ++jj) {
+      const double* uj = U.get() + size_t(n) * size_t(jj);
+      double* tj = T.get() + size_t(n) * size_t(jj);
+      if (which == 0) launch_op(op, false, 1.0, 0.0, 0.0, uj, tj, nullptr, 1.0, s, nullptr);  // D u
+      else launch_spmv(which == 1 ? *op.a : n_op, uj, tj, 1.0, s);                             // K u, N u
+      count_launch();
+    }
+    (which == 0 ? out.d : which == 1 ? out.k : out.n_op) = ts_gram(dev, U.get(), n, r, T.get(), n, r, n);
+  }
+  out.f = ts_gram(dev, U.get(), n, r, F.get(), n, 1, n);
+  out.c = ts_gram(dev, U.get(), n, r, Cv.get(), n, 1, n);
+  {
+    const int blocks = int(std::min<int64_t>(int64_t(cx.sm_count) * 2, std::max<int64_t>(1, n)));
+    const int64_t len = int64_t(r) * r * r;
+    DBuf<double> part(dev, size_t(blocks) * size_t(len)), hred(dev, size_t(len));
+    if (r <= 8)
+      k_qcompress<8><<<blocks, 64, 0, s>>>(h.rowptr.get(), h.bcol.get(), h.ccol.get(), h.val.get(), U.get(), n, r,
+                                           part.get());
+    else if (r <= 16)
+      k_qcompress<16><<<blocks, 256, 0, s>>>(h.rowptr.get(), h.bcol.get(), h.ccol.get(), h.val.get(), U.get(), n, r,
+                                             part.get());
+    else
+      k_qcompress<32><<<blocks, 1024, 0, s>>>(h.rowptr.get(), h.bcol.get(), h.ccol.get(), h.val.get(), U.get(), n, r,
+                                              part.get());
+    MPG_CHECK_LAUNCH();
+    k_sum_blocks<<<unsigned((len + 255) / 256), 256, 0, s>>>(part.get(), blocks, len, hred.get());
+    MPG_CHECK_LAUNCH();
+    count_launch(2);
+    out.h = Mat(r, r * r);
+    MPG_CUDA(cudaMemcpyAsync(out.h.a.data(), hred.get(), size_t(len) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
+  out.basis = DBuf<double>(dev, size_t(n) * size_t(r));
+  MPG_CUDA(cudaMemcpyAsync(out.basis.get(), U.get(), size_t(n) * size_t(r) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  MPG_CUDA(cudaStreamSynchronize(s));
+  return out;
+}
+
 }  // namespace mpg

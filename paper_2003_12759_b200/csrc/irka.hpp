@@ -47,3 +47,37 @@ SweepOutcome sweep_run(const ShiftedOp& op, const double* b_any, const std::vect
                        double* x_out);
 
 }  // namespace mpg
+
+namespace mpg {
+
+// Quadratic term H (n x n^2, column b n + c) on the device, rows sorted.
+struct QbH {
+  int64_t n = 0, nnz = 0;
+  DBuf<int> rowptr, bcol, ccol;
+  DBuf<double> val;
+};
+
+struct QbSettings {
+  std::vector<double> sigmas;
+  int p_moments = 1, q_moments = 1;
+  GmresOptions gmres{};
+  SpaiOptions spai{};
+  int max_chain_len = 16;
+  long long standard_residual_max_dim = 5000;
+  int mode = MPG_PRECOND_REUSE_CHAIN;
+};
+
+struct QbOutcome {
+  int r = 0;
+  host::Mat d, k, n_op, h, f, c;
+  DBuf<double> basis;  // n x r, column-major, on the device
+  std::vector<mpg_report_row> rows;
+  long long total_iterations = 0, total_solves = 0;
+};
+
+// qbihomm_reduce (proj/src/qbihomm.cpp:144-208) on one device: op is the
+// shifted family sigma E - A with A = K, E = D; n_op = N.
+QbOutcome qbihomm_run(const ShiftedOp& op, const DevCsr& n_op, const QbH& h, const double* f_any, const double* c_any,
+                      const QbSettings& cfg);
+
+}  // namespace mpg

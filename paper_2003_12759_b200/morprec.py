@@ -28,6 +28,7 @@ __all__ = [
     "SpaiResult", "UpdateFactor", "IrkaConfig", "IrkaState", "ReportRow", "ReductionReport", "SweepResult",
     "gmres_right_preconditioned", "gmres_shifted", "gmres_batch", "spai_build", "spai_column_solve", "update_build",
     "standard_residual", "irka_reduce", "run_spai_bench", "ConfigError", "SolverError", "PrecondMode",
+    "QbSystem", "QbConfig", "ReducedQb", "qbihomm_reduce",
 ]
 
 
@@ -589,3 +590,108 @@ def run_spai_bench(op: ShiftedOperator, b, points: Sequence[float], spai: SpaiCo
                              L.ptr(x) if x is not None else None, rows, len(pts), C.byref(nrows), C.byref(failed)))
     rep = ReductionReport(_rows(rows, nrows.value), failed.value == 0, 0, 1)
     return SweepResult(rep, failed.value, x)
+
+
+# ---- QB-IHOMM (proj/include/morprec/qbihomm.hpp, proj/src/qbihomm.cpp) ---------------
+@dataclasses.dataclass
+class QbSystem:
+    """D x' = K x + H (x (x) x) + N x u + F u, y = C^T x (qbihomm.hpp:15-33).
+
+    d, k, n_op: n x n SparseMatrix on the device; h: the n x n^2 quadratic term
+    as triplets (rows, cols = b n + c, values); f, c: n-vectors (SISO).
+    create() validates shapes as QbSystem::create does (qbihomm.cpp:17-43)."""
+    d: SparseMatrix
+    k: SparseMatrix
+    n_op: SparseMatrix
+    h_rows: np.ndarray
+    h_cols: np.ndarray
+    h_vals: np.ndarray
+    f: np.ndarray
+    c: np.ndarray
+
+    @staticmethod
+    def create(d: SparseMatrix, k: SparseMatrix, n_op: SparseMatrix, h, f, c) -> "QbSystem":
+        n = d.rows()
+        if d.cols() != n:
+            raise ConfigError("quadratic-bilinear system: D must be square")
+        if k.shape != (n, n):
+            raise ConfigError("quadratic-bilinear system: K must be n x n")
+        if n_op.shape != (n, n):
+            raise ConfigError("quadratic-bilinear system: N must be n x n")
+        if isinstance(h, tuple):
+            hr, hc, hv, hshape = (*h, (n, n * n)) if len(h) == 3 else h
+        else:  # scipy-like or host CSR with nrows/ncols/rowptr/colind/val
+            hshape = (h.nrows, h.ncols)
+            hr = np.repeat(np.arange(h.nrows, dtype=np.int64), np.diff(h.rowptr))
+            hc, hv = h.colind, h.val
+        if tuple(hshape) != (n, n * n):
+            raise ConfigError(f"quadratic-bilinear system: H must be n x n^2 (got {hshape[0]} x {hshape[1]})")
+        for name, v in (("F", f), ("C", c)):
+            a = np.asarray(v)
+            if (a.ndim == 2 and a.shape[1] != 1) or a.size != n:
+                raise ConfigError(f"quadratic-bilinear system: {name} must be a single n-column (SISO)")
+        return QbSystem(d, k, n_op, L.i64(hr), L.i64(hc), L.f64(hv), L.f64(f).reshape(-1), L.f64(c).reshape(-1))
+
+    def dim(self) -> int:
+        return self.d.rows()
+
+
+@dataclasses.dataclass
+class QbConfig:
+    """QbConfig (qbihomm.hpp:35-43)."""
+    sigmas: Sequence[float] = ()
+    p_moments: int = 1
+    q_moments: int = 1
+    gmres: GmresConfig = dataclasses.field(default_factory=GmresConfig)
+    spai: SpaiConfig = dataclasses.field(default_factory=SpaiConfig)
+    max_chain_len: int = 16
+    standard_residual_max_dim: int = 5000
+
+    def c(self) -> L.QbCfg:
+        return L.QbCfg(self.p_moments, self.q_moments, self.gmres.c(), self.spai.c(), self.max_chain_len,
+                       self.standard_residual_max_dim)
+
+
+@dataclasses.dataclass
+class ReducedQb:
+    """ReducedQb (qbihomm.hpp:45-52): r x r matrices, h r x r^2, f, c r x 1, basis n x r."""
+    d: np.ndarray
+    k: np.ndarray
+    n_op: np.ndarray
+    h: np.ndarray
+    f: np.ndarray
+    c: np.ndarray
+    basis: np.ndarray
+
+    def order(self) -> int:
+        return self.d.shape[0]
+
+    def linear_transfer(self, s: float) -> float:
+        return float(self.c[:, 0] @ np.linalg.solve(s * self.d - self.k, self.f[:, 0]))
+
+
+def qbihomm_reduce(sys: QbSystem, cfg: QbConfig, mode: int = PrecondMode.REUSE_CHAIN):
+    """qbihomm_reduce (qbihomm.cpp:144-208) on the GPU; returns (ReducedQb, ReductionReport)."""
+    n = sys.dim()
+    op = ShiftedOperator(sys.k, sys.d)
+    sig = L.f64(cfg.sigmas)
+    cap = max(1, len(sig) * (cfg.p_moments + 2 * cfg.q_moments + 2))
+    basis = np.zeros((n, cap), order="F")
+    rd, rk, rn = (np.zeros(cap * cap) for _ in range(3))
+    rh = np.zeros(cap * cap * cap)
+    rf, rc = np.zeros(cap), np.zeros(cap)
+    order, nrows = C.c_int(), C.c_int()
+    maxrows = 4 * max(1, len(sig))
+    rows = (L.ReportRow * maxrows)()
+    qc = cfg.c()
+    check(lib.mpg_qbihomm_reduce(op._h, sys.n_op._h, sys.h_vals.size, L.ptr(sys.h_rows), L.ptr(sys.h_cols),
+                                 L.ptr(sys.h_vals), L.ptr(sys.f), L.ptr(sys.c), len(sig), L.ptr(sig), C.byref(qc), mode,
+                                 cap, C.byref(order), L.ptr(basis), L.ptr(rd), L.ptr(rk), L.ptr(rn), L.ptr(rh),
+                                 L.ptr(rf), L.ptr(rc), rows, maxrows, C.byref(nrows)))
+    r = order.value
+    sq = lambda a, cc: a[: r * cc].reshape((r, cc), order="F").copy()
+    red = ReducedQb(sq(rd, r), sq(rk, r), sq(rn, r), sq(rh, r * r), rf[:r].reshape(r, 1).copy(),
+                    rc[:r].reshape(r, 1).copy(), np.asfortranarray(basis.reshape(-1, order="F")[: n * r].reshape((n, r), order="F")))
+    rep = ReductionReport(_rows(rows, min(nrows.value, maxrows)), True, r, 1)
+    return red, rep
+
