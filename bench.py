@@ -283,6 +283,32 @@ def run_irka(args, device: int) -> dict:
             "tol": 1e-6, "mode": "frozen SPAI, unstable shifts mirrored"}
 
 
+def run_qbihomm(args, device: int) -> dict:
+    """QB-IHOMM at the bench size: D = the C3 mass, K = the C3
+    operator, N and H by generate_qb_toy's rules, F / C the C3 input / output;
+    4 points with p = q = 1 (20 moment solves), horizontal chains per side.
+    Wall time of qbihomm_reduce (builds, solves, basis, projections)."""
+    import paper_2003_12759_b200 as mpg
+    from paper_2003_12759_b200 import gen
+    s = gen.config3(args.nodes)
+    toy = gen.qb_toy(s.n, 7)
+
+    def dev(h):
+        return mpg.SparseMatrix.from_csr(h.nrows, h.ncols, h.rowptr, h.colind, h.val, device)
+    sys_ = mpg.QbSystem.create(dev(s.e), dev(s.a), dev(toy.n_op), toy.h, s.b[:, 0], s.c[:, 0])
+    sig = [0.1, 0.2, 0.4, 0.8]
+    cfg = mpg.QbConfig(sigmas=sig, p_moments=1, q_moments=1, gmres=mpg.GmresConfig(args.tol, args.max_iter))
+    mpg.lib.mpg_synchronize(device)
+    t0 = time.perf_counter()
+    red, rep = mpg.qbihomm_reduce(sys_, cfg, mpg.PrecondMode.REUSE_CHAIN)
+    mpg.lib.mpg_synchronize(device)
+    wall = time.perf_counter() - t0
+    tot = rep.totals()
+    return {"wall_s": round(wall, 3), "solves": tot["solves"], "gmres_iterations": tot["gmres_iterations"],
+            "precond_build_s": round(tot["precond_build_seconds"], 3), "order": red.order(), "sigmas": sig,
+            "moments": {"p": 1, "q": 1}, "mode": "horizontal chain per side (reuse)"}
+
+
 def _batch_host(mpg, L, op, sig, rhs_host, x_host, chains, trs, cfg):
     """gmres_batch through the C ABI with host buffers: the library copies H2D/D2H."""
     k = len(sig)
@@ -366,6 +392,7 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=334)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-irka", action="store_true", help="skip the full-IRKA wall-time measurement")
+    ap.add_argument("--no-qb", action="store_true", help="skip the QB-IHOMM wall-time measurement")
     ap.add_argument("--cpu-threads", type=int, default=0, help="host threads of the CPU sample (0: all, <= 16)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -383,6 +410,8 @@ def main():
     res = run_ours(args, rank, world, local)
     if world == 1 and not args.no_irka:
         res["irka"] = run_irka(args, local)
+    if world == 1 and not args.no_qb:
+        res["qbihomm"] = run_qbihomm(args, local)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_sample(args)
