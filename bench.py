@@ -309,6 +309,43 @@ def run_qbihomm(args, device: int) -> dict:
             "moments": {"p": 1, "q": 1}, "mode": "horizontal chain per side (reuse)"}
 
 
+def run_mmio(args) -> dict:
+    """Matrix Market ingestion at the bench size: the C3
+    operator written once with the library's writer (shortest round-trip
+    values), then read back by the parallel reader (all host threads) and,
+    on a bounded prefix of the same file (the first 2M entries), by the
+    oracle's sequential istream restatement of the reference reader."""
+    import tempfile
+    import paper_2003_12759_b200 as mpg
+    import oracle as O
+    from paper_2003_12759_b200 import gen
+    s = gen.config3(args.nodes)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "c3.mtx")
+        t0 = time.perf_counter()
+        mpg.write_matrix_market_file(path, s.a)
+        t_write = time.perf_counter() - t0
+        size = os.path.getsize(path)
+        t0 = time.perf_counter()
+        h = mpg.read_matrix_market_file(path, device=None)
+        t_read = time.perf_counter() - t0
+        assert h.nnz == s.a.nnz and np.array_equal(h.colind, s.a.colind) and np.array_equal(h.val, s.a.val)
+        with open(path, "rb") as f:
+            f.readline()
+            f.readline()
+            sample = 2_000_000
+            body = b"".join(f.readline() for _ in range(sample))
+        text = b"%%MatrixMarket matrix coordinate real general\n" + f"{s.n} {s.n} {sample}\n".encode() + body
+        t0 = time.perf_counter()
+        O.read_matrix_market(text, "sample")
+        t_orc = time.perf_counter() - t0
+    return {"entries": int(s.a.nnz), "file_bytes": size, "read_s": round(t_read, 3), "write_s": round(t_write, 3),
+            "read_GBps": round(size / t_read / 1e9, 3), "read_Mentries_per_s": round(s.a.nnz / t_read / 1e6, 2),
+            "threads": os.cpu_count(),
+            "cpu_baseline": {"Mentries_per_s": round(sample / t_orc / 1e6, 3), "cores": 1, "kind": "port",
+                             "sample": f"oracle istream reader on the first {sample} entries of the same file"}}
+
+
 def _batch_host(mpg, L, op, sig, rhs_host, x_host, chains, trs, cfg):
     """gmres_batch through the C ABI with host buffers: the library copies H2D/D2H."""
     k = len(sig)
@@ -393,6 +430,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-irka", action="store_true", help="skip the full-IRKA wall-time measurement")
     ap.add_argument("--no-qb", action="store_true", help="skip the QB-IHOMM wall-time measurement")
+    ap.add_argument("--no-mm", action="store_true", help="skip the Matrix Market ingestion measurement")
     ap.add_argument("--cpu-threads", type=int, default=0, help="host threads of the CPU sample (0: all, <= 16)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -412,6 +450,8 @@ def main():
         res["irka"] = run_irka(args, local)
     if world == 1 and not args.no_qb:
         res["qbihomm"] = run_qbihomm(args, local)
+    if world == 1 and not args.no_mm and rank == 0:
+        res["matrix_market"] = run_mmio(args)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_sample(args)

@@ -36,6 +36,7 @@ extern "C" {
 #define MPG_ERR_LOGIC 4   /* std::logic_error, other */
 #define MPG_ERR_CUDA 5    /* CUDA runtime failure / no device */
 #define MPG_ERR_NOMEM 6   /* device allocation failed */
+#define MPG_ERR_IO 7      /* morprec::IoError      (CLI exit 4) */
 
 /* PrecondMode (proj/include/morprec/chain.hpp:21) + one extension. */
 #define MPG_PRECOND_NONE 0
@@ -297,6 +298,22 @@ int mpg_gen_convdiff3d(int64_t M, uint64_t seed, mpg_host_system** out);
 int mpg_gen_fem3d(int64_t N, uint64_t seed, int mimo, mpg_host_system** out);
 int mpg_gen_zipf(int64_t n, uint64_t seed, int64_t min_len, int64_t max_len, double expo, int nshifts,
                  mpg_host_system** out);
+
+/* ---- Matrix Market IO (proj/src/matrix_market.cpp) and the report CSV
+ * (proj/src/report.cpp:46-63); host-side, no device needed. --------------------
+ * read_matrix_market / _file: coordinate real general|symmetric, symmetric
+ * expanded, duplicates summed; malformed input fails with MPG_ERR_IO and
+ * "origin:line: what". threads <= 0: all host threads (parsing and CSR
+ * assembly run in parallel; results are independent of the thread count).
+ * write_matrix_market: general, row-major, shortest round-trip values; dense
+ * blocks store every entry. Text buffers are malloc'ed; free with mpg_buffer_free. */
+int mpg_mm_read_file(const char* path, int threads, mpg_host_csr** out);
+int mpg_mm_read_buffer(const char* data, int64_t len, const char* origin, int threads, mpg_host_csr** out);
+int mpg_mm_write_file(const char* path, const mpg_host_csr* a, int threads);
+int mpg_mm_write_buffer(const mpg_host_csr* a, int threads, char** out, int64_t* len);
+int mpg_mm_write_dense_buffer(int64_t rows, int64_t cols, const double* colmajor, char** out, int64_t* len);
+int mpg_report_csv(const mpg_report_row* rows, int nrows, char** out, int64_t* len);
+void mpg_buffer_free(char* p);
 
 #ifdef __cplusplus
 }

@@ -104,6 +104,10 @@ _SIGS = {
                                      C.POINTER(SpaiCfg), C.c_int, C.c_longlong, C.c_int, C.c_int, ip, vp, vp, vp, vp,
                                      vp, vp, vp, vp, C.c_int, ip]),
     "orc_kron_compress_quadratic": (C.c_int, [vp, vp, C.c_longlong, C.c_longlong, vp]),
+    "orc_mm_read_buffer": (C.c_int, [C.c_char_p, C.c_longlong, C.c_char_p, C.POINTER(vp)]),
+    "orc_mm_read_file": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
+    "orc_mm_write_buffer": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_longlong)]),
+    "orc_buffer_free": (None, [vp]),
 }
 for _n, (_r, _a) in _SIGS.items():
     _f = getattr(lib, _n)
@@ -119,6 +123,10 @@ class SolverError(RuntimeError):
     pass
 
 
+class IoError(RuntimeError):
+    pass
+
+
 def _check(st: int) -> None:
     if st == 0:
         return
@@ -129,6 +137,8 @@ def _check(st: int) -> None:
         raise ConfigError(msg)
     if st == 3:
         raise SolverError(msg)
+    if st == 7:
+        raise IoError(msg)
     raise RuntimeError(msg)
 
 
@@ -607,3 +617,28 @@ def kron_compress_quadratic(h: Csr, u) -> np.ndarray:
     out = np.zeros((r, r * r), order="F")
     _check(lib.orc_kron_compress_quadratic(h._h, _p(u), n, r, _p(out)))
     return out
+
+
+def read_matrix_market(text, origin: str = "<stream>") -> Csr:
+    """read_matrix_market (proj/src/matrix_market.cpp:38-98), sequential istream restatement."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = vp()
+    _check(lib.orc_mm_read_buffer(data, len(data), origin.encode(), C.byref(h)))
+    return Csr(h.value)
+
+
+def read_matrix_market_file(path: str) -> Csr:
+    h = vp()
+    _check(lib.orc_mm_read_file(str(path).encode(), C.byref(h)))
+    return Csr(h.value)
+
+
+def write_matrix_market(a: Csr) -> str:
+    """write_matrix_market (proj/src/matrix_market.cpp:100-114)."""
+    buf, n = C.c_void_p(), C.c_longlong()
+    _check(lib.orc_mm_write_buffer(a._h, C.byref(buf), C.byref(n)))
+    try:
+        return C.string_at(buf.value, n.value).decode()
+    finally:
+        lib.orc_buffer_free(buf)
+

@@ -1,7 +1,9 @@
 // CPU ORACLE — test infrastructure only (see oracle.hpp).
 // Flat C entry points so tests/ and bench.py's CPU-baseline leg can drive
 // the restatement through ctypes. Status codes match include/mpg.h.
+#include <cstdlib>
 #include <cstring>
+#include <sstream>
 #include <string>
 
 #include "oracle.hpp"
@@ -27,6 +29,9 @@ int guard(F&& f) {
   } catch (const SolverError& e) {
     g_err = e.what();
     return 3;
+  } catch (const IoError& e) {
+    g_err = e.what();
+    return 7;
   } catch (const std::exception& e) {
     g_err = e.what();
     return 4;
@@ -380,5 +385,27 @@ int orc_kron_compress_quadratic(const Csr* h, const double* u, long long n, long
     std::memcpy(out, m.a.data(), m.a.size() * sizeof(double));
   });
 }
+
+int orc_mm_read_buffer(const char* data, long long len, const char* origin, Csr** out) {
+  return guard([&] {
+    std::istringstream in(std::string(data, size_t(len)));
+    *out = new Csr(read_matrix_market(in, origin));
+  });
+}
+int orc_mm_read_file(const char* path, Csr** out) {
+  return guard([&] { *out = new Csr(read_matrix_market_file(path)); });
+}
+int orc_mm_write_buffer(const Csr* a, char** out, long long* len) {
+  return guard([&] {
+    std::ostringstream os;
+    write_matrix_market(os, *a);
+    const std::string t = os.str();
+    *out = static_cast<char*>(std::malloc(t.size() + 1));
+    std::memcpy(*out, t.data(), t.size());
+    (*out)[t.size()] = 0;
+    *len = (long long)t.size();
+  });
+}
+void orc_buffer_free(char* p) { std::free(p); }
 
 }  // extern "C"

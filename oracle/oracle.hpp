@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <functional>
+#include <iosfwd>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -29,6 +30,7 @@ using Vec = std::vector<double>;
 // ---- errors (proj/include/morprec/errors.hpp:12-28) -----------------------
 struct ConfigError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct SolverError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct IoError : std::runtime_error { using std::runtime_error::runtime_error; };
 
 // ---- small column-major dense matrix (stands in for Eigen::MatrixXd) ------
 struct Dense {
@@ -285,5 +287,10 @@ struct OrthBasis {
 };
 Dense kron_compress_quadratic(const Csr& h, const Dense& u);
 std::pair<ReducedQb, ReductionReport> qbihomm_reduce(const QbSystem& sys, const QbConfig& cfg, PrecondMode mode);
+
+// ---- Matrix Market IO (proj/src/matrix_market.cpp) ------------------------
+Csr read_matrix_market(std::istream& in, const std::string& origin);
+Csr read_matrix_market_file(const std::string& path);
+void write_matrix_market(std::ostream& out, const Csr& a);
 
 }  // namespace oracle

@@ -5,7 +5,7 @@ The compute path is libmpg.so (hand-written sm_100a CUDA + C++ drivers behind
 the C ABI in include/mpg.h); this package is the Python mirror of the
 reference's API (morprec.py) and the synthetic-input generators (gen.py).
 """
-from ._lib import ConfigError, CudaError, SolverError, lib  # noqa: F401  (fails loudly if libmpg.so is missing)
+from ._lib import ConfigError, CudaError, IoError, SolverError, lib  # noqa: F401  (fails loudly if libmpg.so is missing)
 from . import gen  # noqa: F401
 from .morprec import *  # noqa: F401,F403
 

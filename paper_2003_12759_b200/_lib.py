@@ -18,7 +18,7 @@ if not os.path.exists(LIB_PATH):
 
 lib = C.CDLL(LIB_PATH)
 
-MPG_OK, MPG_ERR_INVALID, MPG_ERR_CONFIG, MPG_ERR_SOLVER, MPG_ERR_LOGIC, MPG_ERR_CUDA, MPG_ERR_NOMEM = range(7)
+MPG_OK, MPG_ERR_INVALID, MPG_ERR_CONFIG, MPG_ERR_SOLVER, MPG_ERR_LOGIC, MPG_ERR_CUDA, MPG_ERR_NOMEM, MPG_ERR_IO = range(8)
 PRECOND_NONE, PRECOND_FRESH, PRECOND_REUSE_CHAIN, PRECOND_REUSE_FROZEN = range(4)
 KIND_NONE, KIND_FRESH, KIND_HORIZONTAL, KIND_VERTICAL, KIND_REUSED_SAME_MATRIX = range(5)
 KIND_NAMES = {0: "none", 1: "fresh", 2: "horizontal", 3: "vertical", 4: "reused_same_matrix"}
@@ -30,6 +30,10 @@ class ConfigError(RuntimeError):
 
 class SolverError(RuntimeError):
     """morprec::SolverError (proj/include/morprec/errors.hpp:18-22)."""
+
+
+class IoError(RuntimeError):
+    """morprec::IoError (proj/include/morprec/errors.hpp:24-28)."""
 
 
 class CudaError(RuntimeError):
@@ -50,6 +54,8 @@ def check(status: int) -> None:
         raise MemoryError(msg)
     if status == MPG_ERR_CUDA:
         raise CudaError(msg)
+    if status == MPG_ERR_IO:
+        raise IoError(msg)
     raise RuntimeError(msg)
 
 
@@ -147,6 +153,13 @@ _SIGS = {
     "mpg_qbihomm_reduce": (_I, [vp, vp, _L, vp, vp, vp, vp, vp, _I, vp, C.POINTER(QbCfg), _I, _I, ip] + [vp] * 8
                            + [_I, ip]),
     "mpg_spai_bench": (_I, [vp, vp, _I, vp, C.POINTER(SpaiCfg), C.POINTER(GmresCfg), _I, _I, vp, vp, _I, ip, ip]),
+    "mpg_mm_read_file": (_I, [C.c_char_p, _I, C.POINTER(C.POINTER(HostCsr))]),
+    "mpg_mm_read_buffer": (_I, [C.c_char_p, _L, C.c_char_p, _I, C.POINTER(C.POINTER(HostCsr))]),
+    "mpg_mm_write_file": (_I, [C.c_char_p, C.POINTER(HostCsr), _I]),
+    "mpg_mm_write_buffer": (_I, [C.POINTER(HostCsr), _I, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "mpg_mm_write_dense_buffer": (_I, [_L, _L, vp, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "mpg_report_csv": (_I, [vp, _I, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "mpg_buffer_free": (None, [vp]),
     "mpg_gen_last_error": (C.c_char_p, []),
     "mpg_host_csr_free": (None, [C.POINTER(HostCsr)]),
     "mpg_host_system_free": (None, [C.POINTER(HostSystem)]),

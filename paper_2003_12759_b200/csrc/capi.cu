@@ -1,11 +1,13 @@
 // extern "C" entry points of libmpg.so (include/mpg.h): thin wrappers that
 // translate the reference's exception classes into status codes.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
 
+#include "host/mmio.hpp"
 #include "irka.hpp"
 
 using namespace mpg;
@@ -34,6 +36,9 @@ int guard(F&& f) {
   } catch (const mpg::CudaError& e) {
     g_err = e.what();
     return MPG_ERR_CUDA;
+  } catch (const mpg::IoError& e) {
+    g_err = e.what();
+    return MPG_ERR_IO;
   } catch (const std::bad_alloc&) {
     g_err = "device or host allocation failed";
     return MPG_ERR_NOMEM;
@@ -523,5 +528,86 @@ int mpg_qbihomm_reduce(const mpg_op* op, const mpg_csr* n_op, int64_t h_nnz, con
     copy_rows(r.rows, rows, max_rows, nrows);
   });
 }
+
+// ---- Matrix Market IO and the report CSV (host side) -------------------------
+static mpg_host_csr* to_host_csr(mmio::Csr&& c) {
+  auto* m = new mpg_host_csr;
+  m->nrows = c.nrows;
+  m->ncols = c.ncols;
+  m->nnz = c.nnz;
+  m->rowptr = c.rowptr.release();
+  m->colind = c.colind ? c.colind.release() : new int64_t[1];
+  m->val = c.val ? c.val.release() : new double[1];
+  return m;
+}
+
+static mmio::Csr from_host_csr(const mpg_host_csr* a) {
+  if (!a || a->nrows < 0 || a->ncols < 0 || (a->nrows > 0 && !a->rowptr)) throw std::invalid_argument("mmio: bad matrix");
+  mmio::Csr c;
+  c.nrows = a->nrows;
+  c.ncols = a->ncols;
+  c.nnz = a->rowptr[a->nrows];
+  c.rowptr.reset(new int64_t[size_t(a->nrows) + 1]);
+  std::copy(a->rowptr, a->rowptr + a->nrows + 1, c.rowptr.get());
+  c.colind.reset(new int64_t[size_t(std::max<int64_t>(1, c.nnz))]);
+  c.val.reset(new double[size_t(std::max<int64_t>(1, c.nnz))]);
+  std::copy(a->colind, a->colind + c.nnz, c.colind.get());
+  std::copy(a->val, a->val + c.nnz, c.val.get());
+  return c;
+}
+
+static int put_buffer(const std::string& text, char** out, int64_t* len) {
+  *out = static_cast<char*>(std::malloc(text.size() + 1));
+  if (!*out) throw std::bad_alloc();
+  std::memcpy(*out, text.data(), text.size());
+  (*out)[text.size()] = '\0';
+  *len = int64_t(text.size());
+  return 0;
+}
+
+int mpg_mm_read_file(const char* path, int threads, mpg_host_csr** out) {
+  return guard([&] {
+    if (!path || !out) throw std::invalid_argument("mmio: null argument");
+    *out = to_host_csr(mmio::read_file(path, threads));
+  });
+}
+
+int mpg_mm_read_buffer(const char* data, int64_t len, const char* origin, int threads, mpg_host_csr** out) {
+  return guard([&] {
+    if ((!data && len > 0) || len < 0 || !out) throw std::invalid_argument("mmio: null argument");
+    *out = to_host_csr(mmio::read(data, size_t(len), origin ? origin : "<stream>", threads));
+  });
+}
+
+int mpg_mm_write_file(const char* path, const mpg_host_csr* a, int threads) {
+  return guard([&] {
+    if (!path) throw std::invalid_argument("mmio: null argument");
+    mmio::write_file(path, mmio::write(from_host_csr(a), threads));
+  });
+}
+
+int mpg_mm_write_buffer(const mpg_host_csr* a, int threads, char** out, int64_t* len) {
+  return guard([&] {
+    if (!out || !len) throw std::invalid_argument("mmio: null argument");
+    put_buffer(mmio::write(from_host_csr(a), threads), out, len);
+  });
+}
+
+int mpg_mm_write_dense_buffer(int64_t rows, int64_t cols, const double* colmajor, char** out, int64_t* len) {
+  return guard([&] {
+    if (rows < 0 || cols < 0 || (rows * cols > 0 && !colmajor) || !out || !len)
+      throw std::invalid_argument("mmio: bad dense block");
+    put_buffer(mmio::write_dense(rows, cols, colmajor), out, len);
+  });
+}
+
+int mpg_report_csv(const mpg_report_row* rows, int nrows, char** out, int64_t* len) {
+  return guard([&] {
+    if ((nrows > 0 && !rows) || !out || !len) throw std::invalid_argument("report: null argument");
+    put_buffer(mmio::report_csv(rows, nrows), out, len);
+  });
+}
+
+void mpg_buffer_free(char* p) { std::free(p); }
 
 }  // extern "C"

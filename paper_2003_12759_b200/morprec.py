@@ -21,14 +21,15 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _lib as L
-from ._lib import ConfigError, SolverError, check, lib
+from ._lib import ConfigError, IoError, SolverError, check, lib
 
 __all__ = [
     "SparseMatrix", "ShiftedOperator", "PrecondChain", "GmresConfig", "GmresReport", "GmresResult", "SpaiConfig",
     "SpaiResult", "UpdateFactor", "IrkaConfig", "IrkaState", "ReportRow", "ReductionReport", "SweepResult",
     "gmres_right_preconditioned", "gmres_shifted", "gmres_batch", "spai_build", "spai_column_solve", "update_build",
     "standard_residual", "irka_reduce", "run_spai_bench", "ConfigError", "SolverError", "PrecondMode",
-    "QbSystem", "QbConfig", "ReducedQb", "qbihomm_reduce",
+    "QbSystem", "QbConfig", "ReducedQb", "qbihomm_reduce", "IoError", "read_matrix_market",
+    "read_matrix_market_file", "write_matrix_market", "write_matrix_market_file",
 ]
 
 
@@ -479,20 +480,15 @@ class ReductionReport:
                     gmres_seconds=sum(r.gmres_seconds for r in self.rows))
 
     def write_csv(self, f) -> None:
-        """Header, one line per row, then TOTAL (report.cpp:46-63); NaN cells stay empty."""
-        cols = ["sweep", "point", "precond", "solves", "precond_build_seconds", "gmres_iterations", "gmres_seconds",
-                "min_residual", "matrix_change", "standard_residual"]
-        f.write(",".join(cols) + "\n")
-
-        def cell(v):
-            return "" if isinstance(v, float) and math.isnan(v) else repr(v)
-        for r in self.rows:
-            f.write(",".join([str(r.sweep), str(r.point), r.kind, str(r.solves), cell(r.precond_build_seconds),
-                              str(r.gmres_iterations), cell(r.gmres_seconds), cell(r.min_residual),
-                              cell(r.matrix_change), cell(r.standard_residual)]) + "\n")
-        t = self.totals()
-        f.write(f"TOTAL,,,{t['solves']},{t['precond_build_seconds']!r},{t['gmres_iterations']},"
-                f"{t['gmres_seconds']!r},,,\n")
+        """ReductionReport::write_csv (report.cpp:46-63): header, one line per row, TOTAL line; the text is
+        produced by the library's C++ writer (default ostream formatting, byte-identical to the reference's)."""
+        rows = (L.ReportRow * max(1, len(self.rows)))()
+        kinds = {v: k for k, v in L.KIND_NAMES.items()}
+        for i, r in enumerate(self.rows):
+            rows[i] = L.ReportRow(r.sweep, r.point, kinds.get(r.kind, 0), r.solves, r.gmres_iterations,
+                                  r.precond_build_seconds, r.gmres_seconds, r.min_residual, r.matrix_change,
+                                  r.standard_residual)
+        f.write(_take_text(lambda b, n: lib.mpg_report_csv(rows, len(self.rows), b, n)))
 
 
 @dataclasses.dataclass
@@ -694,4 +690,80 @@ def qbihomm_reduce(sys: QbSystem, cfg: QbConfig, mode: int = PrecondMode.REUSE_C
                     rc[:r].reshape(r, 1).copy(), np.asfortranarray(basis.reshape(-1, order="F")[: n * r].reshape((n, r), order="F")))
     rep = ReductionReport(_rows(rows, min(nrows.value, maxrows)), True, r, 1)
     return red, rep
+
+
+# ---- Matrix Market IO (proj/include/morprec/matrix_market.hpp, proj/src/matrix_market.cpp) ------
+def _take_text(call) -> str:
+    buf, n = C.c_void_p(), C.c_int64()
+    check(call(C.byref(buf), C.byref(n)))
+    try:
+        return C.string_at(buf.value, n.value).decode()
+    finally:
+        lib.mpg_buffer_free(buf)
+
+
+def _host_csr_struct(a):
+    """(HostCsr struct, keep-alive arrays) for a gen.HostCsr / scipy matrix / SparseMatrix."""
+    if isinstance(a, SparseMatrix):
+        rp, ci, v = a.download()
+        nr, nc = a.shape
+    elif hasattr(a, "rowptr"):
+        rp, ci, v, nr, nc = a.rowptr, a.colind, a.val, a.nrows, a.ncols
+    else:
+        m = a.tocsr()
+        rp, ci, v, (nr, nc) = m.indptr, m.indices, m.data, m.shape
+    rp, ci, v = L.i64(rp), L.i64(ci), L.f64(v)
+    h = L.HostCsr(nr, nc, int(rp[-1]) if rp.size else 0, rp.ctypes.data_as(C.POINTER(C.c_int64)),
+                  ci.ctypes.data_as(C.POINTER(C.c_int64)), v.ctypes.data_as(C.POINTER(C.c_double)))
+    return h, (rp, ci, v)
+
+
+def _from_host(p, device: Optional[int]):
+    from .gen import _take_csr
+    host = _take_csr(p)
+    if device is None:
+        return host
+    return SparseMatrix.from_csr(host.nrows, host.ncols, host.rowptr, host.colind, host.val, device)
+
+
+def read_matrix_market(text, origin: str = "<stream>", threads: int = 0, device: Optional[int] = 0):
+    """read_matrix_market (matrix_market.cpp:38-98): coordinate real general|symmetric text; symmetric storage
+    expanded, duplicates summed; malformed input raises IoError("origin:line: ..."). Parsed by `threads` host
+    threads (0: all). Returns a SparseMatrix on `device`, or the host CSR (gen.HostCsr) with device=None."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    p = C.POINTER(L.HostCsr)()
+    check(lib.mpg_mm_read_buffer(data, len(data), origin.encode(), threads, C.byref(p)))
+    return _from_host(p, device)
+
+
+def read_matrix_market_file(path, threads: int = 0, device: Optional[int] = 0):
+    """read_matrix_market_file (matrix_market.cpp:93-97)."""
+    p = C.POINTER(L.HostCsr)()
+    check(lib.mpg_mm_read_file(str(path).encode(), threads, C.byref(p)))
+    return _from_host(p, device)
+
+
+def write_matrix_market(a, threads: int = 0) -> str:
+    """write_matrix_market (matrix_market.cpp:100-142): general, row-major, shortest round-trip values;
+    a dense ndarray stores every entry (zeros included)."""
+    if isinstance(a, np.ndarray):
+        d = np.asfortranarray(a, dtype=np.float64)
+        if d.ndim != 2:
+            raise ValueError("write_matrix_market: dense blocks must be 2-D")
+        return _take_text(lambda b, n: lib.mpg_mm_write_dense_buffer(d.shape[0], d.shape[1], d.ctypes.data, b, n))
+    h, keep = _host_csr_struct(a)
+    return _take_text(lambda b, n: lib.mpg_mm_write_buffer(C.byref(h), threads, b, n))
+
+
+def write_matrix_market_file(path, a, threads: int = 0) -> None:
+    if isinstance(a, np.ndarray):
+        text = write_matrix_market(a)
+        try:
+            with open(path, "w") as f:
+                f.write(text)
+        except OSError as e:
+            raise IoError(f"cannot open '{path}' for writing") from e
+        return
+    h, keep = _host_csr_struct(a)
+    check(lib.mpg_mm_write_file(str(path).encode(), C.byref(h), threads))
 
