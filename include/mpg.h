@@ -299,6 +299,20 @@ int mpg_gen_fem3d(int64_t N, uint64_t seed, int mimo, mpg_host_system** out);
 int mpg_gen_zipf(int64_t n, uint64_t seed, int64_t min_len, int64_t max_len, double expo, int nshifts,
                  mpg_host_system** out);
 
+/* ---- transfer_function_error (proj/src/airga.cpp:386-447) ---------------------
+ * Relative error ||H(s) - H_r(s)||_F / ||H(s)||_F on a grid for the
+ * second-order model M x'' + D x' + K x = F u, y = C^T x, against a reduced
+ * model (host, column-major: r x r m, d, k; r x n_in f; r x n_out c). The
+ * full-order H(s) = C^T (s^2 M + s D + K)^{-1} F runs through the GPU solver
+ * stack with one preconditioner per mode (none, fresh, horizontal chain along
+ * the grid); errors[g] is NaN for s <= 0, failed solves, a singular reduced
+ * pencil or H(s) = 0. f (n x n_in), c (n x n_out) column-major, any memory. */
+int mpg_transfer_function_error(const mpg_csr* m, const mpg_csr* d, const mpg_csr* k, const double* f, int n_in,
+                                const double* c, int n_out, const double* red_m, const double* red_d,
+                                const double* red_k, const double* red_f, const double* red_c, int r,
+                                const double* grid, int ngrid, const mpg_gmres_cfg* gmres, const mpg_spai_cfg* spai,
+                                int mode, int max_chain_len, double* errors, long long* total_iterations);
+
 /* ---- Matrix Market IO (proj/src/matrix_market.cpp) and the report CSV
  * (proj/src/report.cpp:46-63); host-side, no device needed. --------------------
  * read_matrix_market / _file: coordinate real general|symmetric, symmetric

@@ -108,6 +108,8 @@ _SIGS = {
     "orc_mm_read_file": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
     "orc_mm_write_buffer": (C.c_int, [vp, C.POINTER(C.c_void_p), C.POINTER(C.c_longlong)]),
     "orc_buffer_free": (None, [vp]),
+    "orc_transfer_function_error": (C.c_int, [vp, vp, vp, vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, C.c_int, vp,
+                                              C.c_int, C.POINTER(GmresCfg), C.POINTER(SpaiCfg), C.c_int, C.c_int, vp]),
 }
 for _n, (_r, _a) in _SIGS.items():
     _f = getattr(lib, _n)
@@ -641,4 +643,24 @@ def write_matrix_market(a: Csr) -> str:
         return C.string_at(buf.value, n.value).decode()
     finally:
         lib.orc_buffer_free(buf)
+
+
+def transfer_function_error(m: Csr, d: Csr, k: Csr, f, c, red, grid, gmres: GmresConfig = None,
+                            spai: SpaiConfig = None, mode: int = 2, max_chain_len: int = 16) -> np.ndarray:
+    """transfer_function_error (proj/src/airga.cpp:386-447); red = (m_r, d_r, k_r, f_r, c_r)."""
+    n = m.shape[0]
+    fm = np.asfortranarray(np.asarray(f, dtype=np.float64).reshape(n, -1))
+    cm = np.asfortranarray(np.asarray(c, dtype=np.float64).reshape(n, -1))
+    rm, rd, rk = (np.asfortranarray(np.asarray(x, dtype=np.float64)) for x in red[:3])
+    r = rm.shape[0]
+    rf = np.asfortranarray(np.asarray(red[3], dtype=np.float64).reshape(r, -1))
+    rc = np.asfortranarray(np.asarray(red[4], dtype=np.float64).reshape(r, -1))
+    g = _f64(grid)
+    out = np.zeros(g.size)
+    gc = (gmres or GmresConfig(1e-10, 1000)).c()
+    sc = (spai or SpaiConfig()).c()
+    _check(lib.orc_transfer_function_error(m._h, d._h, k._h, _p(fm), fm.shape[1], _p(cm), cm.shape[1], _p(rm), _p(rd),
+                                           _p(rk), _p(rf), _p(rc), r, _p(g), g.size, C.byref(gc), C.byref(sc), mode,
+                                           max_chain_len, _p(out)))
+    return out
 

@@ -408,4 +408,19 @@ int orc_mm_write_buffer(const Csr* a, char** out, long long* len) {
 }
 void orc_buffer_free(char* p) { std::free(p); }
 
+int orc_transfer_function_error(const Csr* m, const Csr* d, const Csr* k, const double* f, int n_in, const double* c,
+                                int n_out, const double* rm, const double* rd, const double* rk, const double* rf,
+                                const double* rc, int r, const double* grid, int ngrid, const orc_gmres_cfg* gmres,
+                                const orc_spai_cfg* spai, int mode, int max_chain_len, double* errors) {
+  return guard([&] {
+    const long long n = m->nrows;
+    const auto e = transfer_function_error(*m, *d, *k, dense_from(f, n, n_in), dense_from(c, n, n_out),
+                                           dense_from(rm, r, r), dense_from(rd, r, r), dense_from(rk, r, r),
+                                           dense_from(rf, r, n_in), dense_from(rc, r, n_out),
+                                           std::vector<double>(grid, grid + ngrid), to_gmres(gmres), to_spai(spai),
+                                           PrecondMode(mode), max_chain_len);
+    std::copy(e.begin(), e.end(), errors);
+  });
+}
+
 }  // extern "C"

@@ -293,4 +293,11 @@ Csr read_matrix_market(std::istream& in, const std::string& origin);
 Csr read_matrix_market_file(const std::string& path);
 void write_matrix_market(std::ostream& out, const Csr& a);
 
+// ---- second-order transfer error (proj/src/airga.cpp:80-85, :386-447) -----
+Csr shifted_operator2(const Csr& m, const Csr& d, const Csr& k, double s);
+std::vector<double> transfer_function_error(const Csr& m, const Csr& d, const Csr& k, const Dense& f, const Dense& c,
+                                            const Dense& rm, const Dense& rd, const Dense& rk, const Dense& rf,
+                                            const Dense& rc, const std::vector<double>& grid, const GmresConfig& gmres,
+                                            const SpaiConfig& spai, PrecondMode mode, int max_chain_len);
+
 }  // namespace oracle

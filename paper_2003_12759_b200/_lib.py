@@ -153,6 +153,8 @@ _SIGS = {
     "mpg_qbihomm_reduce": (_I, [vp, vp, _L, vp, vp, vp, vp, vp, _I, vp, C.POINTER(QbCfg), _I, _I, ip] + [vp] * 8
                            + [_I, ip]),
     "mpg_spai_bench": (_I, [vp, vp, _I, vp, C.POINTER(SpaiCfg), C.POINTER(GmresCfg), _I, _I, vp, vp, _I, ip, ip]),
+    "mpg_transfer_function_error": (_I, [vp, vp, vp, vp, _I, vp, _I, vp, vp, vp, vp, vp, _I, vp, _I,
+                                         C.POINTER(GmresCfg), C.POINTER(SpaiCfg), _I, _I, vp, C.POINTER(C.c_longlong)]),
     "mpg_mm_read_file": (_I, [C.c_char_p, _I, C.POINTER(C.POINTER(HostCsr))]),
     "mpg_mm_read_buffer": (_I, [C.c_char_p, _L, C.c_char_p, _I, C.POINTER(C.POINTER(HostCsr))]),
     "mpg_mm_write_file": (_I, [C.c_char_p, C.POINTER(HostCsr), _I]),

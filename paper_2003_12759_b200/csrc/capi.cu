@@ -610,4 +610,30 @@ int mpg_report_csv(const mpg_report_row* rows, int nrows, char** out, int64_t* l
 
 void mpg_buffer_free(char* p) { std::free(p); }
 
+int mpg_transfer_function_error(const mpg_csr* m, const mpg_csr* d, const mpg_csr* k, const double* f, int n_in,
+                                const double* c, int n_out, const double* red_m, const double* red_d,
+                                const double* red_k, const double* red_f, const double* red_c, int r,
+                                const double* grid, int ngrid, const mpg_gmres_cfg* gmres, const mpg_spai_cfg* spai,
+                                int mode, int max_chain_len, double* errors, long long* total_iterations) {
+  return guard([&] {
+    if (!m || !d || !k || !f || !c || !red_m || !red_d || !red_k || !red_f || !red_c || (ngrid > 0 && (!grid || !errors)) ||
+        r < 1)
+      throw std::invalid_argument("transfer_function_error: null argument");
+    auto mat = [](const double* p, int rows, int cols) {
+      host::Mat x(rows, cols);
+      std::memcpy(x.a.data(), p, x.a.size() * sizeof(double));
+      return x;
+    };
+    TfSettings ts;
+    ts.gmres = to_gmres(gmres);
+    ts.spai = to_spai(spai);
+    ts.mode = mode;
+    ts.max_chain_len = max_chain_len;
+    const auto e = tf_error_run(m->p, d->p, k->p, f, n_in, c, n_out, mat(red_m, r, r), mat(red_d, r, r),
+                                mat(red_k, r, r), mat(red_f, r, n_in), mat(red_c, r, n_out),
+                                std::vector<double>(grid, grid + std::max(ngrid, 0)), ts, total_iterations);
+    std::copy(e.begin(), e.end(), errors);
+  });
+}
+
 }  // extern "C"

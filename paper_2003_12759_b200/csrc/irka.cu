@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <limits>
 #include <random>
 
 #include "host/small_dense.hpp"
@@ -901,6 +902,190 @@ QbOutcome qbihomm_run(const ShiftedOp& op, const DevCsr& n_op, const QbH& h, con
   MPG_CUDA(cudaMemcpyAsync(out.basis.get(), U.get(), size_t(n) * size_t(r) * sizeof(double), cudaMemcpyDeviceToDevice, s));
   MPG_CUDA(cudaStreamSynchronize(s));
   return out;
+}
+
+// ---- second-order transfer-function error (proj/src/airga.cpp:80-85, :386-447) -----
+namespace {
+__global__ void k_comb3(const double* __restrict__ vm, const double* __restrict__ vd, const double* __restrict__ vk,
+                        double a, double b, int64_t nnz, double* __restrict__ out, unsigned long long* zeros) {
+  unsigned long long z = 0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nnz; i += int64_t(gridDim.x) * blockDim.x) {
+    const double v = a * vm[i] + b * vd[i] + vk[i];
+    out[i] = v;
+    z += v == 0.0;
+  }
+  if (z) atomicAdd(zeros, z);
+}
+}  // namespace
+
+std::vector<double> tf_error_run(const CsrPtr& m, const CsrPtr& d, const CsrPtr& k, const double* f_any, int n_in,
+                                 const double* c_any, int n_out, const host::Mat& rm, const host::Mat& rd,
+                                 const host::Mat& rk, const host::Mat& rf, const host::Mat& rc,
+                                 const std::vector<double>& grid, const TfSettings& cfg, long long* total_iterations) {
+  const int dev = m->device;
+  auto& cx = ctx(dev);
+  DeviceGuard guard(dev);
+  cudaStream_t s = cx.stream;
+  const int64_t n = m->nrows;
+  for (const CsrPtr& x : {m, d, k})
+    if (x->nrows != n || x->ncols != n || x->device != dev)
+      throw std::invalid_argument("transfer_function_error: M, D, K must be n x n on one device");
+  const int r = rm.rows;
+  if (rm.cols != r || rd.rows != r || rd.cols != r || rk.rows != r || rk.cols != r || rf.rows != r ||
+      rf.cols != n_in || rc.rows != r || rc.cols != n_out)
+    throw std::invalid_argument("transfer_function_error: reduced model shapes do not match");
+  if (n_in < 1 || n_out < 1 || n_out * n_in > 1024) throw std::invalid_argument("transfer_function_error: bad F / C");
+  // merged pattern of M, D, K with aligned values (zero-filled), built once
+  auto down = [&](const DevCsr& a, std::vector<int>& rp, std::vector<int>& ci, std::vector<double>& v) {
+    rp.resize(size_t(n) + 1);
+    ci.resize(size_t(a.nnz));
+    v.resize(size_t(a.nnz));
+    MPG_CUDA(cudaMemcpyAsync(rp.data(), a.rowptr.get(), rp.size() * 4, cudaMemcpyDeviceToHost, s));
+    if (a.nnz) {
+      MPG_CUDA(cudaMemcpyAsync(ci.data(), a.colind.get(), ci.size() * 4, cudaMemcpyDeviceToHost, s));
+      MPG_CUDA(cudaMemcpyAsync(v.data(), a.val.get(), v.size() * 8, cudaMemcpyDeviceToHost, s));
+    }
+  };
+  std::vector<int> rp3[3], ci3[3];
+  std::vector<double> v3[3];
+  down(*m, rp3[0], ci3[0], v3[0]);
+  down(*d, rp3[1], ci3[1], v3[1]);
+  down(*k, rp3[2], ci3[2], v3[2]);
+  MPG_CUDA(cudaStreamSynchronize(s));
+  std::vector<int> urp(size_t(n) + 1, 0), uci;
+  std::vector<double> uv[3];
+  for (int64_t i = 0; i < n; ++i) {
+    int p[3] = {rp3[0][size_t(i)], rp3[1][size_t(i)], rp3[2][size_t(i)]};
+    while (true) {
+      int c = INT32_MAX;
+      for (int t = 0; t < 3; ++t)
+        if (p[t] < rp3[t][size_t(i) + 1]) c = std::min(c, ci3[t][size_t(p[t])]);
+      if (c == INT32_MAX) break;
+      uci.push_back(c);
+      for (int t = 0; t < 3; ++t) {
+        double v = 0.0;
+        while (p[t] < rp3[t][size_t(i) + 1] && ci3[t][size_t(p[t])] == c) v += v3[t][size_t(p[t]++)];
+        uv[t].push_back(v);
+      }
+    }
+    urp[size_t(i) + 1] = int(uci.size());
+  }
+  const int64_t unnz = int64_t(uci.size());
+  DBuf<int> drp(dev, urp.size()), dci(dev, std::max<size_t>(1, uci.size()));
+  DBuf<double> dv[3];
+  MPG_CUDA(cudaMemcpyAsync(drp.get(), urp.data(), urp.size() * 4, cudaMemcpyHostToDevice, s));
+  if (unnz) MPG_CUDA(cudaMemcpyAsync(dci.get(), uci.data(), uci.size() * 4, cudaMemcpyHostToDevice, s));
+  for (int t = 0; t < 3; ++t) {
+    dv[t] = DBuf<double>(dev, std::max<size_t>(1, uv[t].size()));
+    if (unnz) MPG_CUDA(cudaMemcpyAsync(dv[t].get(), uv[t].data(), uv[t].size() * 8, cudaMemcpyHostToDevice, s));
+  }
+  DBuf<double> F(dev, size_t(n) * n_in), Cm(dev, size_t(n) * n_out), X(dev, size_t(n) * n_in);
+  copy_in(F.get(), f_any, size_t(n) * n_in, s);
+  copy_in(Cm.get(), c_any, size_t(n) * n_out, s);
+  std::vector<double> fnorm(static_cast<size_t>(n_in));
+  for (int j = 0; j < n_in; ++j) fnorm[size_t(j)] = device_norm2(dev, F.get() + size_t(n) * j, n, s);
+  DBuf<unsigned long long> zeros(dev, 1);
+
+  std::vector<double> errors(grid.size(), std::numeric_limits<double>::quiet_NaN());
+  ChainPtr chain;
+  CsrPtr chain_matrix;
+  long long its = 0;
+  for (size_t g = 0; g < grid.size(); ++g) {
+    const double sv = grid[g];
+    if (!(sv > 0.0) || !std::isfinite(sv)) continue;
+    // A(s) = s^2 M + s D + K on the merged pattern; exact zeros dropped (sparse.cpp:191)
+    DBuf<double> vals(dev, std::max<size_t>(1, size_t(unnz)));
+    MPG_CUDA(cudaMemsetAsync(zeros.get(), 0, sizeof(unsigned long long), s));
+    if (unnz) {
+      k_comb3<<<unsigned(std::min<int64_t>((unnz + 255) / 256, int64_t(cx.sm_count) * 8)), 256, 0, s>>>(
+          dv[0].get(), dv[1].get(), dv[2].get(), sv * sv, sv, unnz, vals.get(), zeros.get());
+      MPG_CHECK_LAUNCH();
+      count_launch();
+    }
+    unsigned long long nz0 = 0;
+    MPG_CUDA(cudaMemcpyAsync(&nz0, zeros.get(), sizeof nz0, cudaMemcpyDeviceToHost, s));
+    MPG_CUDA(cudaStreamSynchronize(s));
+    CsrPtr A;
+    if (nz0 == 0) {
+      DBuf<int> rp2(dev, urp.size()), ci2(dev, std::max<size_t>(1, uci.size()));
+      MPG_CUDA(cudaMemcpyAsync(rp2.get(), drp.get(), urp.size() * 4, cudaMemcpyDeviceToDevice, s));
+      if (unnz) MPG_CUDA(cudaMemcpyAsync(ci2.get(), dci.get(), uci.size() * 4, cudaMemcpyDeviceToDevice, s));
+      A = csr_from_device_parts(dev, n, n, std::move(rp2), std::move(ci2), std::move(vals));
+    } else {
+      std::vector<double> hv(static_cast<size_t>(unnz));
+      MPG_CUDA(cudaMemcpyAsync(hv.data(), vals.get(), hv.size() * 8, cudaMemcpyDeviceToHost, s));
+      MPG_CUDA(cudaStreamSynchronize(s));
+      std::vector<int64_t> rp64(size_t(n) + 1, 0), ci64;
+      std::vector<double> v64;
+      for (int64_t i = 0; i < n; ++i) {
+        for (int q = urp[size_t(i)]; q < urp[size_t(i) + 1]; ++q)
+          if (hv[size_t(q)] != 0.0) {
+            ci64.push_back(uci[size_t(q)]);
+            v64.push_back(hv[size_t(q)]);
+          }
+        rp64[size_t(i) + 1] = int64_t(ci64.size());
+      }
+      A = csr_from_host(dev, n, n, rp64.data(), ci64.data(), v64.data());
+    }
+    ChainPtr prec;
+    if (cfg.mode == MPG_PRECOND_FRESH) {
+      auto ch = std::make_shared<Chain>();
+      ch->factors.push_back(spai_or_update(A, nullptr, cfg.spai, false).p);
+      prec = ch;
+    } else if (cfg.mode == MPG_PRECOND_REUSE_CHAIN || cfg.mode == MPG_PRECOND_REUSE_FROZEN) {
+      if (!chain || chain->length() + 1 > cfg.max_chain_len) {
+        auto ch = std::make_shared<Chain>();
+        ch->factors.push_back(spai_or_update(A, nullptr, cfg.spai, false).p);
+        chain = ch;
+      } else if (cfg.mode == MPG_PRECOND_REUSE_CHAIN) {
+        auto ch = std::make_shared<Chain>(*chain);
+        ch->factors.push_back(spai_or_update(A, chain_matrix, cfg.spai, false).p);
+        chain = ch;
+      }
+      chain_matrix = A;
+      prec = chain;
+    }
+    OpPtr op = op_create(A, nullptr);
+    std::vector<SolveSpec> specs;
+    std::vector<int> cols;
+    for (int j = 0; j < n_in; ++j) {
+      double* xj = X.get() + size_t(n) * j;
+      if (fnorm[size_t(j)] == 0.0) {
+        MPG_CUDA(cudaMemsetAsync(xj, 0, size_t(n) * sizeof(double), s));
+        continue;
+      }
+      SolveSpec sp;
+      sp.sre = 0.0;
+      sp.ca = 1.0;  // y = A(s) x
+      sp.chain = prec;
+      sp.b = F.get() + size_t(n) * j;
+      sp.x = xj;
+      specs.push_back(sp);
+      cols.push_back(j);
+    }
+    bool ok = true;
+    if (!specs.empty()) {
+      const std::vector<GmresOutcome> oc = gmres_batch(*op, specs, cfg.gmres);
+      for (const auto& o : oc) {
+        ok = ok && o.converged;
+        its += o.iterations;
+      }
+    }
+    if (!ok) continue;
+    const Mat h = ts_gram(dev, Cm.get(), n, n_out, X.get(), n, n_in, n);  // C^T X
+    Mat ar(r, r);
+    for (size_t i = 0; i < ar.a.size(); ++i) ar.a[i] = sv * sv * rm.a[i] + sv * rd.a[i] + rk.a[i];
+    const host::LU lu(ar);
+    if (!lu.invertible()) continue;
+    const Mat hr = host::mul(host::transpose(rc), lu.solve(rf));
+    const double denom = host::fro(h);
+    if (denom == 0.0) continue;
+    Mat diff = h;
+    for (size_t i = 0; i < diff.a.size(); ++i) diff.a[i] -= hr.a[i];
+    errors[g] = host::fro(diff) / denom;
+  }
+  if (total_iterations) *total_iterations = its;
+  return errors;
 }
 
 }  // namespace mpg

@@ -81,3 +81,23 @@ QbOutcome qbihomm_run(const ShiftedOp& op, const DevCsr& n_op, const QbH& h, con
                       const QbSettings& cfg);
 
 }  // namespace mpg
+
+namespace mpg {
+
+// transfer_function_error (proj/src/airga.cpp:386-447) for M x'' + D x' + K x
+// = F u, y = C^T x, against a reduced model (r x r m, d, k; r x n_in f;
+// r x n_out c). One shifted matrix s^2 M + s D + K per grid point, formed on
+// the device from the merged pattern; preconditioner per mode (none, fresh,
+// horizontal chain along the grid); NaN where a solve fails.
+struct TfSettings {
+  GmresOptions gmres{1e-10, 1000, false};
+  SpaiOptions spai{};
+  int mode = MPG_PRECOND_REUSE_CHAIN;
+  int max_chain_len = 16;
+};
+std::vector<double> tf_error_run(const CsrPtr& m, const CsrPtr& d, const CsrPtr& k, const double* f_any, int n_in,
+                                 const double* c_any, int n_out, const host::Mat& rm, const host::Mat& rd,
+                                 const host::Mat& rk, const host::Mat& rf, const host::Mat& rc,
+                                 const std::vector<double>& grid, const TfSettings& cfg, long long* total_iterations);
+
+}  // namespace mpg

@@ -29,7 +29,8 @@ __all__ = [
     "gmres_right_preconditioned", "gmres_shifted", "gmres_batch", "spai_build", "spai_column_solve", "update_build",
     "standard_residual", "irka_reduce", "run_spai_bench", "ConfigError", "SolverError", "PrecondMode",
     "QbSystem", "QbConfig", "ReducedQb", "qbihomm_reduce", "IoError", "read_matrix_market",
-    "read_matrix_market_file", "write_matrix_market", "write_matrix_market_file",
+    "read_matrix_market_file", "write_matrix_market", "write_matrix_market_file", "SecondOrderSystem",
+    "ReducedSecondOrder", "TransferErrorConfig", "transfer_function_error",
 ]
 
 
@@ -766,4 +767,84 @@ def write_matrix_market_file(path, a, threads: int = 0) -> None:
         return
     h, keep = _host_csr_struct(a)
     check(lib.mpg_mm_write_file(str(path).encode(), C.byref(h), threads))
+
+
+# ---- second-order models (proj/include/morprec/airga.hpp) --------------------------------------
+@dataclasses.dataclass
+class SecondOrderSystem:
+    """M x'' + D x' + K x = F u, y = C^T x (airga.hpp:17-41); m, d, k device SparseMatrix, f (n x n_in) and
+    c (n x n_out) dense host arrays."""
+    m: SparseMatrix
+    d: SparseMatrix
+    k: SparseMatrix
+    f: np.ndarray
+    c: np.ndarray
+    alpha: float = 0.0
+    beta: float = 0.0
+
+    @staticmethod
+    def create(m, d, k, f, c, alpha: float = 0.0, beta: float = 0.0) -> "SecondOrderSystem":
+        n = m.rows()
+        for name, x in (("M", m), ("D", d), ("K", k)):
+            if x.shape != (n, n):
+                raise ConfigError(f"second-order system: {name} must be n x n")
+        f = np.asfortranarray(np.asarray(f, dtype=np.float64).reshape(n, -1))
+        c = np.asfortranarray(np.asarray(c, dtype=np.float64).reshape(n, -1))
+        return SecondOrderSystem(m, d, k, f, c, alpha, beta)
+
+    @staticmethod
+    def with_proportional_damping(m, k, f, c, alpha: float, beta: float) -> "SecondOrderSystem":
+        """D = alpha M + beta K, formed exactly (airga.cpp:62-72)."""
+        mr, kr = m.download(), k.download()
+        import scipy.sparse as sp
+        ms = sp.csr_matrix((mr[2], mr[1], mr[0]), shape=m.shape)
+        ks = sp.csr_matrix((kr[2], kr[1], kr[0]), shape=k.shape)
+        ds = (alpha * ms + beta * ks).tocsr()
+        ds.eliminate_zeros()
+        d = SparseMatrix.from_csr(ds.shape[0], ds.shape[1], ds.indptr, ds.indices, ds.data)
+        return SecondOrderSystem.create(m, d, k, f, c, alpha, beta)
+
+    def dim(self) -> int:
+        return self.m.rows()
+
+
+@dataclasses.dataclass
+class ReducedSecondOrder:
+    """airga.hpp:64-71: r x r m, d, k; r x n_in f; r x n_out c."""
+    m: np.ndarray
+    d: np.ndarray
+    k: np.ndarray
+    f: np.ndarray
+    c: np.ndarray
+    basis: Optional[np.ndarray] = None
+
+    def order(self) -> int:
+        return self.m.shape[0]
+
+
+@dataclasses.dataclass
+class TransferErrorConfig:
+    """airga.hpp:91-96."""
+    gmres: GmresConfig = dataclasses.field(default_factory=lambda: GmresConfig(1e-10, 1000))
+    spai: SpaiConfig = dataclasses.field(default_factory=SpaiConfig)
+    mode: int = PrecondMode.REUSE_CHAIN
+    max_chain_len: int = 16
+
+
+def transfer_function_error(sys: SecondOrderSystem, red: ReducedSecondOrder, s_grid,
+                            cfg: TransferErrorConfig = TransferErrorConfig()) -> np.ndarray:
+    """||H(s) - H_r(s)|| / ||H(s)|| on s_grid (airga.cpp:386-447), full order on the GPU; NaN where undefined."""
+    f64 = lambda x: np.asfortranarray(np.asarray(x, dtype=np.float64))
+    r = red.order()
+    rm, rd, rk = f64(red.m), f64(red.d), f64(red.k)
+    rf, rc = f64(np.reshape(red.f, (r, -1))), f64(np.reshape(red.c, (r, -1)))
+    g = L.f64(s_grid)
+    out = np.zeros(g.size)
+    its = C.c_longlong()
+    gc, sc = cfg.gmres.c(), cfg.spai.c()
+    check(lib.mpg_transfer_function_error(sys.m._h, sys.d._h, sys.k._h, L.ptr(sys.f), sys.f.shape[1], L.ptr(sys.c),
+                                          sys.c.shape[1], L.ptr(rm), L.ptr(rd), L.ptr(rk), L.ptr(rf), L.ptr(rc), r,
+                                          L.ptr(g), g.size, C.byref(gc), C.byref(sc), cfg.mode, cfg.max_chain_len,
+                                          L.ptr(out), C.byref(its)))
+    return out
 
