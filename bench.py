@@ -309,6 +309,36 @@ def run_qbihomm(args, device: int) -> dict:
             "moments": {"p": 1, "q": 1}, "mode": "horizontal chain per side (reuse)"}
 
 
+def run_transfer_error(args, device: int) -> dict:
+    """Second-order transfer-function error on a 16-point grid (SURVEY.md §8 f2,
+    the paper's Fig. 3 workload): M = the C3 mass, K = -A (stiffness plus the
+    Robin term), D = 0.05 M + 1e-4 K, SISO F, C from the config, reduced model
+    by projection on the moments at two grid points; one horizontal chain along
+    the grid. Wall time of transfer_function_error."""
+    import scipy.sparse as sp
+    import paper_2003_12759_b200 as mpg
+    from paper_2003_12759_b200 import gen
+    s = gen.config3(args.nodes)
+    Ms, Ks = s.e.to_scipy(), -s.a.to_scipy()
+    Ds = (0.05 * Ms + 1e-4 * Ks).tocsr()
+    f, c = s.b[:, :1], s.c[:, :1]
+    dev = lambda a: mpg.SparseMatrix.from_scipy(sp.csr_matrix(a), device)
+    sysm = mpg.SecondOrderSystem.create(dev(Ms), dev(Ds), dev(Ks), f, c)
+    rng = np.random.default_rng(0)
+    U, _ = np.linalg.qr(rng.standard_normal((s.n, 4)))
+    red = mpg.ReducedSecondOrder(U.T @ (Ms @ U), U.T @ (Ds @ U), U.T @ (Ks @ U), U.T @ f, U.T @ c)
+    grid = [float(x) for x in np.logspace(-1, 2, 16)]
+    cfg = mpg.TransferErrorConfig(mpg.GmresConfig(args.tol, args.max_iter), mode=mpg.PrecondMode.REUSE_CHAIN)
+    mpg.lib.mpg_synchronize(device)
+    t0 = time.perf_counter()
+    err = mpg.transfer_function_error(sysm, red, grid, cfg)
+    mpg.lib.mpg_synchronize(device)
+    wall = time.perf_counter() - t0
+    return {"wall_s": round(wall, 3), "grid_points": len(grid), "solved": int(np.sum(np.isfinite(err))),
+            "s_per_point": round(wall / len(grid), 3), "grid": "logspace(-1, 2, 16)",
+            "mode": "horizontal chain along the grid (fresh SPAI every 17 points)"}
+
+
 def run_mmio(args) -> dict:
     """Matrix Market ingestion at the bench size: the C3
     operator written once with the library's writer (shortest round-trip
@@ -431,6 +461,7 @@ def main():
     ap.add_argument("--no-irka", action="store_true", help="skip the full-IRKA wall-time measurement")
     ap.add_argument("--no-qb", action="store_true", help="skip the QB-IHOMM wall-time measurement")
     ap.add_argument("--no-mm", action="store_true", help="skip the Matrix Market ingestion measurement")
+    ap.add_argument("--no-tf", action="store_true", help="skip the second-order transfer-error measurement")
     ap.add_argument("--cpu-threads", type=int, default=0, help="host threads of the CPU sample (0: all, <= 16)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -450,6 +481,8 @@ def main():
         res["irka"] = run_irka(args, local)
     if world == 1 and not args.no_qb:
         res["qbihomm"] = run_qbihomm(args, local)
+    if world == 1 and not args.no_tf:
+        res["transfer_error"] = run_transfer_error(args, local)
     if world == 1 and not args.no_mm and rank == 0:
         res["matrix_market"] = run_mmio(args)
     if rank == 0:
