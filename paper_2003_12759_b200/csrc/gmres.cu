@@ -881,6 +881,7 @@ constexpr int GX_MAXV = GX_NG * 32;  // k_gs_tmx: largest k + 2 (basis and w)
 // k + 1 < ~190) and larger k to k_gs_tmx. 0 = the register-tiled kernel.
 struct UpdSel {
   int sel, split;
+  int proj;  // 1: the selector of the projection pass (bit 2: k_gs_tmx<true>)
 };
 __device__ __forceinline__ int upd_owner(const GmSolve& st, UpdSel u) {
   const int nj = st.k + 1;
@@ -889,7 +890,12 @@ __device__ __forceinline__ int upd_owner(const GmSolve& st, UpdSel u) {
   return 0;
 }
 __device__ __forceinline__ bool gt_handles(const GmSolve& st, UpdSel u) { return st.phase == PH_RUN && upd_owner(st, u) == 1; }
-__device__ __forceinline__ bool gx_handles(const GmSolve& st, UpdSel u) { return st.phase == PH_RUN && upd_owner(st, u) == 2; }
+__device__ __forceinline__ bool gx_proj_owner(const GmSolve& st, UpdSel u) {
+  return (u.sel & 4) && st.tm != nullptr && st.k + 2 <= GX_MAXV && st.k + 1 > u.split;
+}
+__device__ __forceinline__ bool gx_handles(const GmSolve& st, UpdSel u) {
+  return st.phase == PH_RUN && (u.proj ? gx_proj_owner(st, u) : upd_owner(st, u) == 2);
+}
 
 template <int CL, bool UPDATE>
 __global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, int G, UpdSel skip) {
@@ -902,13 +908,13 @@ __global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, in
   const int q = int(blockIdx.x) % CL, slot = int(blockIdx.x) / CL, ncl = int(gridDim.x) / CL;
   long long total = 0;
   for (int s = 0; s < ns; ++s)
-    if (S[s].phase == PH_RUN && (!UPDATE || upd_owner(S[s], skip) == 0)) total += gc_tiles(S[s], CL);
+    if (S[s].phase == PH_RUN && (UPDATE ? upd_owner(S[s], skip) == 0 : !gx_proj_owner(S[s], skip))) total += gc_tiles(S[s], CL);
   const long long per = (total + ncl - 1) / ncl;
   const long long a = per * slot, b = min(total, a + per);
   long long off = 0;
   for (int s = 0; s < ns; ++s) {
     GmSolve& st = S[s];
-    if (st.phase != PH_RUN || (UPDATE && upd_owner(st, skip) != 0)) continue;
+    if (st.phase != PH_RUN || (UPDATE ? upd_owner(st, skip) != 0 : gx_proj_owner(st, skip))) continue;
     const int nt = gc_tiles(st, CL);
     const long long lo = a > off ? a : off, hi = b < off + nt ? b : off + nt;
     if (lo < hi) {
@@ -1404,7 +1410,7 @@ __device__ __forceinline__ void gx_producer(GmSolve* S, int ns, int TC, int stag
 // CF chunks of a tile are processed together (their load -> row sum -> butterfly
 // chains interleave); each lane then holds NGC = GX_NG / CF groups per chunk, so
 // CF = 1 serves k + 2 <= 384, CF = 2 <= 192, CF = 4 <= 96, CF = 8 <= 32.
-template <int CF>
+template <int CF, bool PROJ>
 __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, int stage_bytes, int NS, long long a,
                                             long long b, uint32_t ring, uint64_t* full, uint64_t* empty, double* red2,
                                             double* red3, UpdSel us) {
@@ -1439,7 +1445,7 @@ __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, i
 #pragma unroll
       for (int i = 0; i < NGC; ++i) {
         const int j = 32 * i + lane;
-        coef[i] = j < nj ? st.scale[j] * st.h[j] : 0.0;
+        coef[i] = (!PROJ && j < nj) ? st.scale[j] * st.h[j] : 0.0;
         acc[i] = 0.0;
       }
       wsq = 0.0;
@@ -1469,7 +1475,7 @@ __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, i
                    : make_double2(0.0, 0.0);
         double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
 #pragma unroll
-        for (int i = 0; i < NGC; ++i) {
+        for (int i = 0; i < (PROJ ? 0 : NGC); ++i) {
           if (i & 1) {
             x1 = fma(coef[i], v[f][i].x, x1);
             y1 = fma(coef[i], v[f][i].y, y1);
@@ -1481,13 +1487,15 @@ __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, i
         sx[f] = x0 + x1;
         sy[f] = y0 + y1;
       }
+      if (!PROJ) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
+        for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-        for (int f = 0; f < CF; ++f) {
-          sx[f] += __shfl_xor_sync(0xffffffffu, sx[f], o);
-          sy[f] += __shfl_xor_sync(0xffffffffu, sy[f], o);
-        }
+          for (int f = 0; f < CF; ++f) {
+            sx[f] += __shfl_xor_sync(0xffffffffu, sx[f], o);
+            sy[f] += __shfl_xor_sync(0xffffffffu, sy[f], o);
+          }
+      }
 #pragma unroll
       for (int f = 0; f < CF; ++f) {
         const int cc = cc0 + f;
@@ -1496,10 +1504,10 @@ __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, i
         if (lane == 0 && c0 + cc < nchunks) {
           double* dst = w + size_t(c0 + cc) * 1024 + 2 * rp;
           if (row + 1 < n) {
-            *reinterpret_cast<double2*>(dst) = make_double2(wn0, wn1);
+            if (!PROJ) *reinterpret_cast<double2*>(dst) = make_double2(wn0, wn1);
             wsq = fma(wn0, wn0, fma(wn1, wn1, wsq));
           } else if (row < n) {
-            dst[0] = wn0;
+            if (!PROJ) dst[0] = wn0;
             wsq = fma(wn0, wn0, wsq);
           }
         }
@@ -1535,6 +1543,8 @@ __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, i
   }
 }
 
+// PROJ: the projection pass (part[j] = W_j . w, part[k+1] = ||w||^2, w unchanged).
+template <bool PROJ>
 __global__ void __launch_bounds__(GX_THREADS, 1) k_gs_tmx(GmSolve* S, int ns, int G, UpdSel us) {
   extern __shared__ __align__(1024) char smx[];
   const uint32_t raw = smem_u32(smx);
@@ -1586,10 +1596,10 @@ __global__ void __launch_bounds__(GX_THREADS, 1) k_gs_tmx(GmSolve* S, int ns, in
     gx_producer(S, ns, TC, stage_bytes, NS, a, b, ring, full, empty, us);
   else
     switch (CF) {
-      case 8: gx_consumer<8>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
-      case 4: gx_consumer<4>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
-      case 2: gx_consumer<2>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
-      default: gx_consumer<1>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
+      case 8: gx_consumer<8, PROJ>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
+      case 4: gx_consumer<4, PROJ>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
+      case 2: gx_consumer<2, PROJ>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
+      default: gx_consumer<1, PROJ>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
     }
 }
 
@@ -1869,12 +1879,13 @@ GcConfig gc_config(int dev, int sm_count, bool update) {
 }
 
 cudaError_t gc_launch_any(bool update, const GcConfig& g, cudaStream_t s, GmSolve* S, int ns, int G,
-                          UpdSel skip = UpdSel{0, 0}) {
-  const UpdSel none{0, 0};
+                          UpdSel skip = UpdSel{0, 0, 0}) {
+  const UpdSel none{0, 0, 0};
+  (void)none;
   switch (g.cl) {
-    case 4: return update ? gc_launch<4, true>(s, g.ncl, S, ns, G, skip) : gc_launch<4, false>(s, g.ncl, S, ns, G, none);
-    case 2: return update ? gc_launch<2, true>(s, g.ncl, S, ns, G, skip) : gc_launch<2, false>(s, g.ncl, S, ns, G, none);
-    default: return update ? gc_launch<1, true>(s, g.ncl, S, ns, G, skip) : gc_launch<1, false>(s, g.ncl, S, ns, G, none);
+    case 4: return update ? gc_launch<4, true>(s, g.ncl, S, ns, G, skip) : gc_launch<4, false>(s, g.ncl, S, ns, G, skip);
+    case 2: return update ? gc_launch<2, true>(s, g.ncl, S, ns, G, skip) : gc_launch<2, false>(s, g.ncl, S, ns, G, skip);
+    default: return update ? gc_launch<1, true>(s, g.ncl, S, ns, G, skip) : gc_launch<1, false>(s, g.ncl, S, ns, G, skip);
   }
 }
 
@@ -1950,7 +1961,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   // Update + probe kernels (MPG_GS_UPD = hybrid | tmx | tma | reg): k_gs_tma up
   // to k + 1 = split, k_gs_tmx above (up to GX_MAXV), the register-tiled kernel
   // beyond; measured per launch on C3.
-  UpdSel usel{0, 0};
+  UpdSel usel{0, 0, 0};
   if (fused && gc_upd.cl == 1) {
     const char* e = std::getenv("MPG_GS_UPD");
     usel.sel = e && !std::strcmp(e, "reg") ? 0 : e && !std::strcmp(e, "tma") ? 1 : e && !std::strcmp(e, "tmx") ? 2 : 3;
@@ -1958,7 +1969,15 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     const char* sp = std::getenv("MPG_GS_SPLIT");
     usel.split = sp ? std::atoi(sp) : 192;
   }
-  const int upd_kind = usel.sel;  // bit 1: panel tensor maps needed
+  UpdSel psel{0, 0, 1};
+  if (fused && gc_dot.cl == 1 && (usel.sel & 2)) {
+    const char* e = std::getenv("MPG_GS_DOT");
+    if (!(e && !std::strcmp(e, "reg"))) psel.sel = 4;
+    const char* sp = std::getenv("MPG_GS_DOT_SPLIT");
+    psel.split = sp ? std::atoi(sp) : 256;  // the register-tiled projection below (C3: 192 -> 1 099 ms, 256 -> 1 074 ms, all-register 1 108 ms)
+  }
+  const int upd_kind = usel.sel;
+  const bool want_maps = ((usel.sel | psel.sel) & 6) != 0;  // panel tensor maps for k_gs_tmx
   std::vector<SolveHost> sh(static_cast<size_t>(ns));
   std::vector<GmSolve> hs(static_cast<size_t>(ns));
   int max_stages = 0;
@@ -2038,7 +2057,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     g.rbuf = H.rbuf.get();
     g.part = H.part.get();
     g.fac = H.fac.get();
-    if (upd_kind & 2) {
+    if (want_maps) {
       const size_t np = size_t(maxit + 2 + PANEL - 1) / PANEL;
       H.tmh.resize(2 * np);
       H.tmd = DBuf<CUtensorMap>(dev, 2 * np);
@@ -2057,7 +2076,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       MPG_CUDA(cudaMemsetAsync(base, 0, size_t(PANEL) * size_t(H.ld) * sizeof(double), s));
       const int p0 = int(H.panels.size() - 1) * PANEL;
       for (int j = 0; j < PANEL && p0 + j < maxit + 2; ++j) H.vtab[size_t(p0 + j)] = base + size_t(j) * CHUNK;
-      if (upd_kind & 2) {
+      if (want_maps) {
         const size_t p = H.panels.size() - 1;
         encode_panel_map(&H.tmh[2 * p], base, H.ld / CHUNK, PANEL);
         encode_panel_map(&H.tmh[2 * p + 1], base, H.ld / CHUNK, 8);
@@ -2107,7 +2126,8 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   static std::once_flag gt_once;
   std::call_once(gt_once, [] {
     cudaFuncSetAttribute(k_gs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, GT_SMEM);
-    cudaFuncSetAttribute(k_gs_tmx, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
+    cudaFuncSetAttribute(k_gs_tmx<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
+    cudaFuncSetAttribute(k_gs_tmx<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
   });
   const bool need_reg_upd = upd_kind == 0 || (upd_kind == 1 && maxit + 1 > GT_MAXCOLS) ||
                             ((upd_kind & 2) && maxit + 2 > GX_MAXV);
@@ -2332,8 +2352,17 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     launches_per_iter = 0;
     for (int st = 0; st < max_stages; ++st) chain_stage(st, 0);
     iter_op(0);
-    if (fused) MPG_CUDA(gc_launch_any(false, gc_dot, s, dS.get(), ns, G));
-    else k_dot<<<gG, 256, smem_dot, s>>>(dS.get(), G);
+    if (fused) {
+      // projection: k_gs_tmx<true> for k + 2 <= GX_MAXV when the panel tensor maps exist
+      // (MPG_GS_DOT=reg keeps the register-tiled kernel for every k)
+      if (psel.sel & 4) {
+        k_gs_tmx<true><<<unsigned(gc_dot.ncl), GX_THREADS, GX_SMEM, s>>>(dS.get(), ns, G, psel);
+        ++launches_per_iter;
+      }
+      MPG_CUDA(gc_launch_any(false, gc_dot, s, dS.get(), ns, G, psel));
+    } else {
+      k_dot<<<gG, 256, smem_dot, s>>>(dS.get(), G);
+    }
     mark(PK_DOT);
     k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 0, fused ? gc_dot.ncl : G);
     mark(PK_SMALL);
@@ -2345,7 +2374,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         ++launches_per_iter;
       }
       if (need_tmx) {
-        k_gs_tmx<<<unsigned(gc_upd.ncl), GX_THREADS, GX_SMEM, s>>>(dS.get(), ns, G, usel);
+        k_gs_tmx<false><<<unsigned(gc_upd.ncl), GX_THREADS, GX_SMEM, s>>>(dS.get(), ns, G, usel);
         ++launches_per_iter;
       }
       if (need_reg_upd) {
