@@ -32,12 +32,6 @@ namespace {
 
 using host::Mat;
 
-__device__ __forceinline__ double wsum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
 // part[blk][i + a*j] = sum over this block's rows of X[row, i] * Y[row, j]
 __global__ void __launch_bounds__(256) k_ts_gram(const double* __restrict__ X, int64_t ldx, int a,
                                                  const double* __restrict__ Y, int64_t ldy, int b, int64_t n,
@@ -91,10 +85,6 @@ __global__ void __launch_bounds__(256) k_ts_apply(const double* __restrict__ X, 
       Y[r + ldy * j] = s;
     }
   }
-}
-
-__global__ void k_fill_zero(double* p, int64_t n) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) p[i] = 0.0;
 }
 
 Mat ts_gram(int dev, const double* X, int64_t ldx, int a, const double* Y, int64_t ldy, int b, int64_t n) {

@@ -562,12 +562,6 @@ __global__ void k_compact(const int* __restrict__ cnt, const int* __restrict__ o
   }
 }
 
-__global__ void k_maxrow(const int* __restrict__ rp, int n, int* out) {
-  int mx = 0;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) mx = max(mx, rp[r + 1] - rp[r]);
-  atomicMax(out, mx);
-}
-
 __global__ void k_fro_dist(CsrView a, CsrView b, double* part) {
   __shared__ double red[8];
   double s = 0.0;
