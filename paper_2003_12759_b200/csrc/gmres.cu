@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 
@@ -2478,6 +2479,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   };
 
   // ---- host loop: launch chunks, poll phases ----
+  const double t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   std::vector<int> khost(size_t(ns), 0);
   std::vector<double> done_at(size_t(ns), -1.0);
   int chunk = 4;
@@ -2514,6 +2516,12 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   if (exec) cudaGraphExecDestroy(exec);
   if (graph) cudaGraphDestroy(graph);
   for (auto e : evs) cudaEventDestroy(e);
+  if (std::getenv("MPG_GMRES_TIMING")) {
+    int maxk = 0;
+    for (const auto& g : hs) maxk = std::max(maxk, g.iterations);
+    std::fprintf(stderr, "gmres_batch: %d solves, setup %.3f s, total %.3f s, max its %d\n", ns, t_setup,
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(), maxk);
+  }
 
   // ---- outputs ----
   for (int i = 0; i < ns; ++i) {

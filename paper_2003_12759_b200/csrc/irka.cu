@@ -264,7 +264,11 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
   const GmresOptions gopt = cfg.gmres;
 
   int last_max_its = 0;
+  const bool timing = std::getenv("MPG_IRKA_TIMING") != nullptr;
+  auto wall = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   for (int z = 1; z <= cfg.max_sweeps && !converged; ++z) {
+    const double tz0 = wall();
+    double t_build = 0.0, t_gmres = 0.0;
     host::Spectrum spec;
     if (!host::real_spectrum(kr, spec)) {  // birka.cpp:167-180
       std::uniform_real_distribution<double> unit(-1.0, 1.0);
@@ -405,10 +409,13 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
       bounds.push_back(specs.size());
     }
     int sweep_max_its = 0;
+    t_build = wall() - tz0;
     for (size_t bi = 0; bi + 1 < bounds.size(); ++bi) {
       const size_t b0 = bounds[bi];
       std::vector<SolveSpec> batch(specs.begin() + long(b0), specs.begin() + long(bounds[bi + 1]));
+      const double tg0 = wall();
       std::vector<GmresOutcome> outc = gmres_batch(op, batch, gopt);
+      t_gmres += wall() - tg0;
       for (const GmresOutcome& o : outc) sweep_max_its = std::max(sweep_max_its, o.iterations);
       for (size_t i = 0; i < outc.size(); ++i) {
         mpg_report_row& row = rows[b0 + i];
@@ -488,6 +495,9 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
     }
     if (std::sqrt(num) / std::max(std::sqrt(den), 1e-300) < cfg.tol) converged = true;
     lambda_prev = lambda_new;
+    if (timing)
+      std::fprintf(stderr, "irka sweep %d: %.3f s (setup+builds %.3f, gmres %.3f, rest %.3f), max its %d\n", z,
+                   wall() - tz0, t_build, t_gmres, wall() - tz0 - t_build - t_gmres, sweep_max_its);
   }
   res.kr = kr;
   res.fr = fr;
