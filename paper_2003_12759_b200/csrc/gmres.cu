@@ -883,9 +883,11 @@ constexpr int GX_MAXV = GX_NG * 32;  // k_gs_tmx: largest k + 2 (basis and w)
 struct UpdSel {
   int sel, split;
   int proj;  // 1: the selector of the projection pass (bit 2: k_gs_tmx<true>)
+  int low;   // update pass: k + 1 <= low stays on the register-tiled kernel
 };
 __device__ __forceinline__ int upd_owner(const GmSolve& st, UpdSel u) {
   const int nj = st.k + 1;
+  if (nj <= u.low) return 0;
   if ((u.sel & 2) && st.tm != nullptr && nj + 1 <= GX_MAXV && (!(u.sel & 1) || nj > u.split)) return 2;
   if ((u.sel & 1) && nj <= GT_MAXCOLS) return 1;
   return 0;
@@ -1880,8 +1882,8 @@ GcConfig gc_config(int dev, int sm_count, bool update) {
 }
 
 cudaError_t gc_launch_any(bool update, const GcConfig& g, cudaStream_t s, GmSolve* S, int ns, int G,
-                          UpdSel skip = UpdSel{0, 0, 0}) {
-  const UpdSel none{0, 0, 0};
+                          UpdSel skip = UpdSel{0, 0, 0, 0}) {
+  const UpdSel none{0, 0, 0, 0};
   (void)none;
   switch (g.cl) {
     case 4: return update ? gc_launch<4, true>(s, g.ncl, S, ns, G, skip) : gc_launch<4, false>(s, g.ncl, S, ns, G, skip);
@@ -1962,15 +1964,19 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   // Update + probe kernels (MPG_GS_UPD = hybrid | tmx | tma | reg): k_gs_tma up
   // to k + 1 = split, k_gs_tmx above (up to GX_MAXV), the register-tiled kernel
   // beyond; measured per launch on C3.
-  UpdSel usel{0, 0, 0};
+  UpdSel usel{0, 0, 0, 0};
   if (fused && gc_upd.cl == 1) {
     const char* e = std::getenv("MPG_GS_UPD");
     usel.sel = e && !std::strcmp(e, "reg") ? 0 : e && !std::strcmp(e, "tma") ? 1 : e && !std::strcmp(e, "tmx") ? 2 : 3;
     if (!tensor_map_encoder()) usel.sel &= 1;
     const char* sp = std::getenv("MPG_GS_SPLIT");
     usel.split = sp ? std::atoi(sp) : 192;
+    // the register-tiled kernel is faster for the first iterations (C3, per launch: k = 0 306 us vs 749 us for
+    // k_gs_tma, k = 24 771 vs 889 us; k = 32 1 370 vs 899 us)
+    const char* lo = std::getenv("MPG_GS_LOW");
+    usel.low = lo ? std::atoi(lo) : 28;
   }
-  UpdSel psel{0, 0, 1};
+  UpdSel psel{0, 0, 1, 0};
   if (fused && gc_dot.cl == 1 && (usel.sel & 2)) {
     const char* e = std::getenv("MPG_GS_DOT");
     if (!(e && !std::strcmp(e, "reg"))) psel.sel = 4;
@@ -2130,7 +2136,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     cudaFuncSetAttribute(k_gs_tmx<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
     cudaFuncSetAttribute(k_gs_tmx<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
   });
-  const bool need_reg_upd = upd_kind == 0 || (upd_kind == 1 && maxit + 1 > GT_MAXCOLS) ||
+  const bool need_reg_upd = upd_kind == 0 || usel.low > 0 || (upd_kind == 1 && maxit + 1 > GT_MAXCOLS) ||
                             ((upd_kind & 2) && maxit + 2 > GX_MAXV);
   const bool need_tma = (upd_kind & 1) && (upd_kind == 1 || usel.split > 0);
   const bool need_tmx = (upd_kind & 2) && (upd_kind == 2 || maxit + 1 > usel.split);
