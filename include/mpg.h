@@ -218,6 +218,11 @@ int mpg_irka_reduce(const mpg_op* op, const double* b, int m, const double* c, i
                     double* lam_re, double* lam_im, double* v, double* w, int* sweeps, int* converged,
                     mpg_report_row* rows, int max_rows, int* nrows);
 
+/* IRKA projection (birka.cpp:283-291, generalised to E): E_r = W^T E V and
+ * A_r = W^T A V (r x r, column-major, host) for V, W (n x r, column-major, any
+ * memory); r <= 32. With E = I, E_r = W^T V as in the reference. */
+int mpg_project(const mpg_op* op, const double* v, const double* w, int r, double* er, double* ar);
+
 /* Multi-GPU IRKA: this process (rank of world) solves its shard of the
  * (unit, side) solves; `allgather` (provided by the caller, e.g. NCCL through
  * torch.distributed) concatenates per-rank byte buffers; buffers are device

@@ -152,6 +152,7 @@ _SIGS = {
                                      vp, vp, vp, vp, ip, ip, vp, _I, ip]),
     "mpg_qbihomm_reduce": (_I, [vp, vp, _L, vp, vp, vp, vp, vp, _I, vp, C.POINTER(QbCfg), _I, _I, ip] + [vp] * 8
                            + [_I, ip]),
+    "mpg_project": (_I, [vp, vp, vp, _I, vp, vp]),
     "mpg_spai_bench": (_I, [vp, vp, _I, vp, C.POINTER(SpaiCfg), C.POINTER(GmresCfg), _I, _I, vp, vp, _I, ip, ip]),
     "mpg_transfer_function_error": (_I, [vp, vp, vp, vp, _I, vp, _I, vp, vp, vp, vp, vp, _I, vp, _I,
                                          C.POINTER(GmresCfg), C.POINTER(SpaiCfg), _I, _I, vp, C.POINTER(C.c_longlong)]),

@@ -321,6 +321,7 @@ int mpg_chain_apply(const mpg_chain* chain, const double* x, double* y) {
 
 namespace mpg {
 double std_residual_public(const CsrPtr& m, const ChainPtr& ch);
+void project_public(const ShiftedOp& op, const double* v_any, const double* w_any, int r, host::Mat& er, host::Mat& ar);
 }
 
 extern "C" {
@@ -633,6 +634,16 @@ int mpg_transfer_function_error(const mpg_csr* m, const mpg_csr* d, const mpg_cs
                                 mat(red_k, r, r), mat(red_f, r, n_in), mat(red_c, r, n_out),
                                 std::vector<double>(grid, grid + std::max(ngrid, 0)), ts, total_iterations);
     std::copy(e.begin(), e.end(), errors);
+  });
+}
+
+int mpg_project(const mpg_op* op, const double* v, const double* w, int r, double* er, double* ar) {
+  return guard([&] {
+    if (!op || !v || !w) throw std::invalid_argument("project: null argument");
+    host::Mat e, a;
+    project_public(*op->p, v, w, r, e, a);
+    if (er) std::memcpy(er, e.a.data(), e.a.size() * sizeof(double));
+    if (ar) std::memcpy(ar, a.a.data(), a.a.size() * sizeof(double));
   });
 }
 

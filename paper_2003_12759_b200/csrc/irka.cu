@@ -175,6 +175,27 @@ double std_residual(const CsrPtr& m, const ChainPtr& ch) {
 
 double std_residual_public(const CsrPtr& m, const ChainPtr& ch) { return std_residual(m, ch); }
 
+// IRKA's projection step (birka.cpp:283-291, E-generalised): E_r = W^T E V,
+// A_r = W^T A V for device or host V, W (n x r, column-major); r <= 32.
+void project_public(const ShiftedOp& op, const double* v_any, const double* w_any, int r, Mat& er, Mat& ar) {
+  const int dev = op.device;
+  auto& cx = ctx(dev);
+  DeviceGuard guard(dev);
+  cudaStream_t s = cx.stream;
+  const int64_t n = op.n;
+  if (r < 1 || r > 32) throw std::invalid_argument("project: 1 <= r <= 32");
+  DBuf<double> V(dev, size_t(n) * r), W(dev, size_t(n) * r), AV(dev, size_t(n) * r), EV(dev, size_t(n) * r);
+  copy_in(V.get(), v_any, size_t(n) * r, s);
+  copy_in(W.get(), w_any, size_t(n) * r, s);
+  for (int j = 0; j < r; ++j) {
+    launch_spmv(*op.a, V.get() + size_t(n) * j, AV.get() + size_t(n) * j, 1.0, s);
+    launch_op(op, false, 1.0, 0.0, 0.0, V.get() + size_t(n) * j, EV.get() + size_t(n) * j, nullptr, 1.0, s, nullptr);
+    count_launch(2);
+  }
+  er = ts_gram(dev, W.get(), n, r, EV.get(), n, r, n);
+  ar = ts_gram(dev, W.get(), n, r, AV.get(), n, r, n);
+}
+
 namespace {
 
 struct SlotPrecond {

@@ -30,7 +30,7 @@ __all__ = [
     "standard_residual", "irka_reduce", "run_spai_bench", "ConfigError", "SolverError", "PrecondMode",
     "QbSystem", "QbConfig", "ReducedQb", "qbihomm_reduce", "IoError", "read_matrix_market",
     "read_matrix_market_file", "write_matrix_market", "write_matrix_market_file", "SecondOrderSystem",
-    "ReducedSecondOrder", "TransferErrorConfig", "transfer_function_error",
+    "ReducedSecondOrder", "TransferErrorConfig", "transfer_function_error", "project",
 ]
 
 
@@ -529,6 +529,18 @@ class IrkaState:
         """H_r(s) = C_r^T (s I - K_r)^{-1} f_r, q x m."""
         r = self.kr.shape[0]
         return self.cr.T @ np.linalg.solve(s * np.eye(r) - self.kr, self.fr)
+
+
+def project(op: ShiftedOperator, v, w):
+    """IRKA's projection step (birka.cpp:283-291, E-generalised): returns (E_r, A_r) = (W^T E V, W^T A V)."""
+    vm = np.asfortranarray(np.asarray(v, dtype=np.float64))
+    wm = np.asfortranarray(np.asarray(w, dtype=np.float64))
+    if vm.shape != wm.shape or vm.ndim != 2 or vm.shape[0] != op.n:
+        raise ValueError("project: V and W must both be n x r")
+    r = vm.shape[1]
+    er, ar = np.zeros((r, r), order="F"), np.zeros((r, r), order="F")
+    check(lib.mpg_project(op._h, L.ptr(vm), L.ptr(wm), r, L.ptr(er), L.ptr(ar)))
+    return er, ar
 
 
 def _rows(buf, n):

@@ -160,3 +160,16 @@ def test_irka_consistent_mass_small_matches_oracle(mpg, orc, gen):
     assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 1e-6
     ho = np.array([ores.cr.T @ np.linalg.solve(1j * w * np.eye(r) - ores.kr, ores.fr) for w in GRID])
     assert np.max(np.abs(_hr_grid(st) - ho) / np.abs(ho)) <= 1e-6
+
+
+def test_projection_entry_matches_dense(mpg, gen):
+    """mpg_project (birka.cpp:283-291, E-generalised) against W^T E V, W^T A V."""
+    s = gen.config1(N=30)
+    ec = s.e_csr()
+    op = mpg.ShiftedOperator(_m(mpg, s.a), _m(mpg, ec))
+    rng = np.random.default_rng(3)
+    V = rng.standard_normal((s.n, 5))
+    W = rng.standard_normal((s.n, 5))
+    er, ar = mpg.project(op, V, W)
+    assert rel(er, W.T @ (ec.to_scipy() @ V)) <= 1e-13
+    assert rel(ar, W.T @ (s.a.to_scipy() @ V)) <= 1e-13
