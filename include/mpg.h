@@ -295,6 +295,9 @@ int mpg_gen_random_sparse(int64_t r, int64_t c, double density, uint64_t seed, d
 int mpg_gen_from_triplets(int64_t nr, int64_t nc, int64_t nnz, const int64_t* ri, const int64_t* ci, const double* v,
                           mpg_host_csr** out);
 int mpg_gen_bilinear_toy(int64_t n, int64_t m, uint64_t seed, mpg_host_csr** k_out, double* f, double* c);
+/* generate_disc_brake_like (proj/src/generator.cpp:37-139): M and K = K_E + K_R + omega^2 K_G; D = alpha M + beta K
+ * and F = C = e_1 are formed by the caller. */
+int mpg_gen_disc_brake(int64_t n, double omega, uint64_t seed, mpg_host_csr** m_out, mpg_host_csr** k_out);
 /* generate_qb_toy (proj/src/generator.cpp:181-207): D, K, N (n x n), H (n x n^2, column b n + c); F = C = e_1. */
 int mpg_gen_qb_toy(int64_t n, uint64_t seed, mpg_host_csr** d, mpg_host_csr** k, mpg_host_csr** n_op,
                    mpg_host_csr** h);
@@ -317,6 +320,39 @@ int mpg_transfer_function_error(const mpg_csr* m, const mpg_csr* d, const mpg_cs
                                 const double* red_k, const double* red_f, const double* red_c, int r,
                                 const double* grid, int ngrid, const mpg_gmres_cfg* gmres, const mpg_spai_cfg* spai,
                                 int mode, int max_chain_len, double* errors, long long* total_iterations);
+
+/* ---- AIRGA: airga_reduce (proj/src/airga.cpp:136-317) -----------------------
+ * AirgaConfig (proj/include/morprec/airga.hpp:43-62). */
+typedef struct {
+  int r_max;
+  double outer_tol, inner_tol;
+  int max_outer;
+  mpg_gmres_cfg gmres;
+  mpg_spai_cfg spai;
+  int max_chain_len;
+  long long standard_residual_max_dim;
+} mpg_airga_cfg;
+
+/* Moment-matching reduction of M x'' + D x' + K x = F u, y = C^T x over
+ * adaptively refreshed expansion points; alpha, beta are the stored damping
+ * coefficients (a warning is recorded when D deviates from alpha M + beta K).
+ * The full-order solves run on the device (s^2 M + s D + K formed on the
+ * fly from the merged pattern); the r x r reduced model, the H2 gaps and the
+ * expansion-point update on the host. Outputs (host, column-major, order r <=
+ * max_order = cfg->r_max): red_m/d/k (r x r), red_f (r x n_in), red_c
+ * (r x n_out), basis (n x r, any memory, may be NULL), final_points (npoints);
+ * warnings: '\n'-separated text in a malloc'ed buffer (mpg_buffer_free). */
+int mpg_airga_reduce(const mpg_csr* m, const mpg_csr* d, const mpg_csr* k, const double* f, int n_in, const double* c,
+                     int n_out, double alpha, double beta, const double* points, int npoints,
+                     const mpg_airga_cfg* cfg, int mode, int* order, double* red_m, double* red_d, double* red_k,
+                     double* red_f, double* red_c, double* basis, double* final_points, int* sweeps, int* converged,
+                     mpg_report_row* rows, int max_rows, int* nrows, char** warnings);
+
+/* update_expansion_points (airga.cpp:319-384) on a reduced pencil (host, r x r). */
+int mpg_update_expansion_points(const double* m, const double* d, const double* k, int r, const double* current,
+                                int ncurrent, double* next);
+/* h2_norm (proj/src/h2.cpp:28-60) of x' = A x + B u, y = C x (host, column-major). */
+int mpg_h2_norm(const double* a, const double* b, const double* c, int ns, int m, int q, double* out);
 
 /* ---- Matrix Market IO (proj/src/matrix_market.cpp) and the report CSV
  * (proj/src/report.cpp:46-63); host-side, no device needed. --------------------

@@ -86,6 +86,12 @@ class QbCfg(C.Structure):
                 ("max_chain_len", C.c_int), ("standard_residual_max_dim", C.c_longlong)]
 
 
+class AirgaCfg(C.Structure):
+    _fields_ = [("r_max", C.c_int), ("outer_tol", C.c_double), ("inner_tol", C.c_double), ("max_outer", C.c_int),
+                ("gmres", GmresCfg), ("spai", SpaiCfg), ("max_chain_len", C.c_int),
+                ("standard_residual_max_dim", C.c_longlong)]
+
+
 class ReportRow(C.Structure):
     _fields_ = [("sweep", C.c_int), ("point", C.c_int), ("kind", C.c_int), ("solves", C.c_int),
                 ("iterations", C.c_longlong), ("build_seconds", C.c_double), ("gmres_seconds", C.c_double),
@@ -154,6 +160,10 @@ _SIGS = {
                            + [_I, ip]),
     "mpg_project": (_I, [vp, vp, vp, _I, vp, vp]),
     "mpg_spai_bench": (_I, [vp, vp, _I, vp, C.POINTER(SpaiCfg), C.POINTER(GmresCfg), _I, _I, vp, vp, _I, ip, ip]),
+    "mpg_airga_reduce": (_I, [vp, vp, vp, vp, _I, vp, _I, _D, _D, vp, _I, C.POINTER(AirgaCfg), _I, ip] + [vp] * 7
+                         + [ip, ip, vp, _I, ip, C.POINTER(C.c_void_p)]),
+    "mpg_update_expansion_points": (_I, [vp, vp, vp, _I, vp, _I, vp]),
+    "mpg_h2_norm": (_I, [vp, vp, vp, _I, _I, _I, C.POINTER(C.c_double)]),
     "mpg_transfer_function_error": (_I, [vp, vp, vp, vp, _I, vp, _I, vp, vp, vp, vp, vp, _I, vp, _I,
                                          C.POINTER(GmresCfg), C.POINTER(SpaiCfg), _I, _I, vp, C.POINTER(C.c_longlong)]),
     "mpg_mm_read_file": (_I, [C.c_char_p, _I, C.POINTER(C.POINTER(HostCsr))]),
@@ -170,6 +180,7 @@ _SIGS = {
     "mpg_gen_random_sparse": (_I, [_L, _L, _D, C.c_uint64, _D, C.POINTER(C.POINTER(HostCsr))]),
     "mpg_gen_from_triplets": (_I, [_L, _L, _L, vp, vp, vp, C.POINTER(C.POINTER(HostCsr))]),
     "mpg_gen_bilinear_toy": (_I, [_L, _L, C.c_uint64, C.POINTER(C.POINTER(HostCsr)), vp, vp]),
+    "mpg_gen_disc_brake": (_I, [_L, _D, C.c_uint64, C.POINTER(C.POINTER(HostCsr)), C.POINTER(C.POINTER(HostCsr))]),
     "mpg_gen_qb_toy": (_I, [_L, C.c_uint64] + [C.POINTER(C.POINTER(HostCsr))] * 4),
     "mpg_gen_grid2d": (_I, [_L, C.c_uint64, C.POINTER(C.POINTER(HostSystem))]),
     "mpg_gen_convdiff3d": (_I, [_L, C.c_uint64, C.POINTER(C.POINTER(HostSystem))]),

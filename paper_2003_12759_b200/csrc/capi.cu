@@ -7,6 +7,7 @@
 #include <mutex>
 #include <string>
 
+#include "host/h2.hpp"
 #include "host/mmio.hpp"
 #include "irka.hpp"
 
@@ -644,6 +645,73 @@ int mpg_project(const mpg_op* op, const double* v, const double* w, int r, doubl
     project_public(*op->p, v, w, r, e, a);
     if (er) std::memcpy(er, e.a.data(), e.a.size() * sizeof(double));
     if (ar) std::memcpy(ar, a.a.data(), a.a.size() * sizeof(double));
+  });
+}
+
+int mpg_airga_reduce(const mpg_csr* m, const mpg_csr* d, const mpg_csr* k, const double* f, int n_in, const double* c,
+                     int n_out, double alpha, double beta, const double* points, int npoints,
+                     const mpg_airga_cfg* cfg, int mode, int* order, double* red_m, double* red_d, double* red_k,
+                     double* red_f, double* red_c, double* basis, double* final_points, int* sweeps, int* converged,
+                     mpg_report_row* rows, int max_rows, int* nrows, char** warnings) {
+  return guard([&] {
+    if (!m || !d || !k || !f || !c || !cfg || (npoints > 0 && !points)) throw std::invalid_argument("airga: null argument");
+    AirgaSettings as;
+    as.points.assign(points, points + std::max(npoints, 0));
+    as.r_max = cfg->r_max;
+    as.outer_tol = cfg->outer_tol;
+    as.inner_tol = cfg->inner_tol;
+    as.max_outer = cfg->max_outer;
+    as.gmres = to_gmres(&cfg->gmres);
+    as.spai = to_spai(&cfg->spai);
+    as.max_chain_len = cfg->max_chain_len;
+    as.standard_residual_max_dim = cfg->standard_residual_max_dim;
+    as.mode = mode;
+    as.alpha = alpha;
+    as.beta = beta;
+    AirgaOutcome o = airga_run(m->p, d->p, k->p, f, n_in, c, n_out, as);
+    if (order) *order = o.r;
+    auto put = [](double* dst, const host::Mat& x) { if (dst && !x.a.empty()) std::memcpy(dst, x.a.data(), x.a.size() * sizeof(double)); };
+    put(red_m, o.m); put(red_d, o.d); put(red_k, o.k); put(red_f, o.f); put(red_c, o.c);
+    if (basis && o.r > 0) {
+      copy_out(basis, o.basis.get(), size_t(m->p->nrows) * size_t(o.r), ctx(m->p->device).stream);
+      MPG_CUDA(cudaStreamSynchronize(ctx(m->p->device).stream));
+    }
+    if (final_points) std::copy(o.final_points.begin(), o.final_points.end(), final_points);
+    if (sweeps) *sweeps = o.sweeps;
+    if (converged) *converged = o.converged;
+    copy_rows(o.rows, rows, max_rows, nrows);
+    if (warnings) {
+      std::string t;
+      for (const auto& w : o.warnings) t += w + "\n";
+      int64_t len = 0;
+      put_buffer(t, warnings, &len);
+    }
+  });
+}
+
+int mpg_update_expansion_points(const double* m, const double* d, const double* k, int r, const double* current,
+                                int ncurrent, double* next) {
+  return guard([&] {
+    auto mat = [r](const double* p) {
+      host::Mat x(r, r);
+      std::memcpy(x.a.data(), p, x.a.size() * sizeof(double));
+      return x;
+    };
+    const auto nx = host::update_expansion_points(mat(m), mat(d), mat(k), std::vector<double>(current, current + ncurrent));
+    std::copy(nx.begin(), nx.end(), next);
+  });
+}
+
+int mpg_h2_norm(const double* a, const double* b, const double* c, int ns, int m, int q, double* out) {
+  return guard([&] {
+    host::StateSpace ss;
+    ss.a = host::Mat(ns, ns);
+    ss.b = host::Mat(ns, m);
+    ss.c = host::Mat(q, ns);
+    std::memcpy(ss.a.a.data(), a, ss.a.a.size() * sizeof(double));
+    std::memcpy(ss.b.a.data(), b, ss.b.a.size() * sizeof(double));
+    std::memcpy(ss.c.a.data(), c, ss.c.a.size() * sizeof(double));
+    *out = host::h2_norm(ss);
   });
 }
 

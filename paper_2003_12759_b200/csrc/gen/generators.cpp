@@ -274,6 +274,85 @@ int mpg_gen_qb_toy(int64_t n, uint64_t seed, mpg_host_csr** d, mpg_host_csr** k,
   });
 }
 
+// generate_disc_brake_like (proj/src/generator.cpp:37-139), same draw order:
+// per-node scales, then (m, k_g) per node, then the 5-point stiffness with its
+// boundary anchors, the skew loop and the random skew pairs; K = K_E + K_R +
+// omega^2 K_G (linear_combination, zeros dropped), D = alpha M + beta K (the
+// caller forms it), F = C = e_1.
+int mpg_gen_disc_brake(int64_t n, double omega, uint64_t seed, mpg_host_csr** m_out, mpg_host_csr** k_out) {
+  return gen_guard([&] {
+    if (n < 4) throw std::invalid_argument("generator: n must be at least 4");
+    if (!std::isfinite(omega)) throw std::invalid_argument("generator: omega, alpha, beta must be finite");
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> u01(0.0, 1.0);
+    const double kappa = 1e9;
+    const int64_t g = int64_t(std::ceil(std::sqrt(double(n))));
+    std::vector<double> scale(static_cast<size_t>(n));
+    for (int64_t v = 0; v < n; ++v) scale[size_t(v)] = std::pow(10.0, 6.0 * u01(rng));
+    std::vector<Trip> m_t, ke_t, kr_t, kg_t;
+    for (int64_t v = 0; v < n; ++v) {
+      const double sv = scale[size_t(v)];
+      const double mv = sv * (1.0 + 0.2 * u01(rng));
+      m_t.push_back({v, v, mv});
+      const double gv = 1e3 * sv * (1.0 + 0.2 * u01(rng));
+      kg_t.push_back({v, v, gv});
+    }
+    for (int64_t v = 0; v < n; ++v) {
+      const double sv = scale[size_t(v)];
+      const int64_t row = v / g, right = v + 1, down = v + g;
+      const bool has_right = right < n && right / g == row;
+      const bool has_down = down < n;
+      if (has_right) {
+        const double w = kappa * std::sqrt(sv * scale[size_t(right)]) * (1.0 + 0.5 * u01(rng));
+        ke_t.push_back({v, v, w});
+        ke_t.push_back({right, right, w});
+        ke_t.push_back({v, right, -w});
+        ke_t.push_back({right, v, -w});
+      }
+      if (has_down) {
+        const double w = kappa * std::sqrt(sv * scale[size_t(down)]) * (1.0 + 0.5 * u01(rng));
+        ke_t.push_back({v, v, w});
+        ke_t.push_back({down, down, w});
+        ke_t.push_back({v, down, -w});
+        ke_t.push_back({down, v, -w});
+      }
+      int missing = 0;
+      if (v % g == 0) ++missing;
+      if (!has_right) ++missing;
+      if (v < g) ++missing;
+      if (!has_down) ++missing;
+      for (int b = 0; b < missing; ++b) ke_t.push_back({v, v, kappa * sv * (1.0 + 0.5 * u01(rng))});
+    }
+    for (int64_t v = 0; v < n; ++v) {
+      const int64_t nxt = (v + 1) % n;
+      const double w = 16.0 * kappa * std::sqrt(scale[size_t(v)] * scale[size_t(nxt)]) * (1.0 + 0.5 * u01(rng));
+      kr_t.push_back({v, nxt, w});
+      kr_t.push_back({nxt, v, -w});
+    }
+    const int64_t pairs = std::max<int64_t>(1, n / 8);
+    std::uniform_int_distribution<int64_t> node(0, n - 1);
+    for (int64_t p = 0; p < pairs; ++p) {
+      const int64_t u = node(rng);
+      const int64_t v = node(rng);
+      const double draw = 2.0 * u01(rng) - 1.0;
+      if (u == v) continue;
+      const double w = 0.3 * kappa * std::sqrt(scale[size_t(u)] * scale[size_t(v)]) * draw;
+      kr_t.push_back({u, v, w});
+      kr_t.push_back({v, u, -w});
+    }
+    *m_out = from_trips(n, n, std::move(m_t));
+    mpg_host_csr* ke = from_trips(n, n, std::move(ke_t));
+    mpg_host_csr* kr = from_trips(n, n, std::move(kr_t));
+    mpg_host_csr* kg = from_trips(n, n, std::move(kg_t));
+    mpg_host_csr* k1 = combine(1.0, ke, 1.0, kr);
+    *k_out = combine(1.0, k1, omega * omega, kg);
+    mpg_host_csr_free(ke);
+    mpg_host_csr_free(kr);
+    mpg_host_csr_free(kg);
+    mpg_host_csr_free(k1);
+  });
+}
+
 // C1: 2D cell-centred 5-point diffusion on an N x N grid.
 int mpg_gen_grid2d(int64_t N, uint64_t seed, mpg_host_system** out) {
   return gen_guard([&] {

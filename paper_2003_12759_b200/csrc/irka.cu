@@ -25,6 +25,7 @@
 #include <random>
 
 #include "host/small_dense.hpp"
+#include "host/h2.hpp"
 #include "irka.hpp"
 
 namespace mpg {
@@ -937,6 +938,119 @@ __global__ void k_comb3(const double* __restrict__ vm, const double* __restrict_
   }
   if (z) atomicAdd(zeros, z);
 }
+__global__ void k_comb3w(const double* __restrict__ vm, const double* __restrict__ vd, const double* __restrict__ vk,
+                         double a, double b, double c, int64_t nnz, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nnz; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = a * vm[i] + b * vd[i] + c * vk[i];
+}
+}  // namespace
+
+
+namespace {
+// s^2 M + s D + K on the merged pattern of M, D, K (aligned, zero-filled value
+// arrays built once); at(s) forms one matrix with one kernel and drops exact
+// zeros as linear_combination does (sparse.cpp:191, airga.cpp:80-85).
+struct Pencil3 {
+  int dev = 0;
+  int64_t n = 0, unnz = 0;
+  std::vector<int> urp, uci;
+  DBuf<int> drp, dci;
+  DBuf<double> dv[3];
+  Pencil3(const CsrPtr& m, const CsrPtr& d, const CsrPtr& k) : dev(m->device), n(m->nrows) {
+    cudaStream_t s = ctx(dev).stream;
+    std::vector<int> rp3[3], ci3[3];
+    std::vector<double> v3[3];
+    const CsrPtr src[3] = {m, d, k};
+    for (int t = 0; t < 3; ++t) {
+      const DevCsr& a = *src[t];
+      rp3[t].resize(size_t(n) + 1);
+      ci3[t].resize(size_t(a.nnz));
+      v3[t].resize(size_t(a.nnz));
+      MPG_CUDA(cudaMemcpyAsync(rp3[t].data(), a.rowptr.get(), rp3[t].size() * 4, cudaMemcpyDeviceToHost, s));
+      if (a.nnz) {
+        MPG_CUDA(cudaMemcpyAsync(ci3[t].data(), a.colind.get(), ci3[t].size() * 4, cudaMemcpyDeviceToHost, s));
+        MPG_CUDA(cudaMemcpyAsync(v3[t].data(), a.val.get(), v3[t].size() * 8, cudaMemcpyDeviceToHost, s));
+      }
+    }
+    MPG_CUDA(cudaStreamSynchronize(s));
+    urp.assign(size_t(n) + 1, 0);
+    std::vector<double> uv[3];
+    for (int64_t i = 0; i < n; ++i) {
+      int p[3] = {rp3[0][size_t(i)], rp3[1][size_t(i)], rp3[2][size_t(i)]};
+      while (true) {
+        int c = INT32_MAX;
+        for (int t = 0; t < 3; ++t)
+          if (p[t] < rp3[t][size_t(i) + 1]) c = std::min(c, ci3[t][size_t(p[t])]);
+        if (c == INT32_MAX) break;
+        uci.push_back(c);
+        for (int t = 0; t < 3; ++t) {
+          double v = 0.0;
+          while (p[t] < rp3[t][size_t(i) + 1] && ci3[t][size_t(p[t])] == c) v += v3[t][size_t(p[t]++)];
+          uv[t].push_back(v);
+        }
+      }
+      urp[size_t(i) + 1] = int(uci.size());
+    }
+    unnz = int64_t(uci.size());
+    drp = DBuf<int>(dev, urp.size());
+    dci = DBuf<int>(dev, std::max<size_t>(1, uci.size()));
+    MPG_CUDA(cudaMemcpyAsync(drp.get(), urp.data(), urp.size() * 4, cudaMemcpyHostToDevice, s));
+    if (unnz) MPG_CUDA(cudaMemcpyAsync(dci.get(), uci.data(), uci.size() * 4, cudaMemcpyHostToDevice, s));
+    for (int t = 0; t < 3; ++t) {
+      dv[t] = DBuf<double>(dev, std::max<size_t>(1, uv[t].size()));
+      if (unnz) MPG_CUDA(cudaMemcpyAsync(dv[t].get(), uv[t].data(), uv[t].size() * 8, cudaMemcpyHostToDevice, s));
+    }
+    MPG_CUDA(cudaStreamSynchronize(s));
+  }
+  // ||cm M + cd D + ck K||_F
+  double combo_norm(double cm, double cd, double ck) const {
+    auto& cx = ctx(dev);
+    cudaStream_t s = cx.stream;
+    if (unnz == 0) return 0.0;
+    DBuf<double> vals(dev, size_t(unnz));
+    k_comb3w<<<unsigned(std::min<int64_t>((unnz + 255) / 256, int64_t(cx.sm_count) * 8)), 256, 0, s>>>(
+        dv[0].get(), dv[1].get(), dv[2].get(), cm, cd, ck, unnz, vals.get());
+    MPG_CHECK_LAUNCH();
+    count_launch();
+    return std::sqrt(device_norm2(dev, vals.get(), unnz, s));
+  }
+  CsrPtr at(double sv) const {
+    auto& cx = ctx(dev);
+    cudaStream_t s = cx.stream;
+    DBuf<double> vals(dev, std::max<size_t>(1, size_t(unnz)));
+    DBuf<unsigned long long> zeros(dev, 1);
+    MPG_CUDA(cudaMemsetAsync(zeros.get(), 0, sizeof(unsigned long long), s));
+    if (unnz) {
+      k_comb3<<<unsigned(std::min<int64_t>((unnz + 255) / 256, int64_t(cx.sm_count) * 8)), 256, 0, s>>>(
+          dv[0].get(), dv[1].get(), dv[2].get(), sv * sv, sv, unnz, vals.get(), zeros.get());
+      MPG_CHECK_LAUNCH();
+      count_launch();
+    }
+    unsigned long long nz0 = 0;
+    MPG_CUDA(cudaMemcpyAsync(&nz0, zeros.get(), sizeof nz0, cudaMemcpyDeviceToHost, s));
+    MPG_CUDA(cudaStreamSynchronize(s));
+    if (nz0 == 0) {
+      DBuf<int> rp2(dev, urp.size()), ci2(dev, std::max<size_t>(1, uci.size()));
+      MPG_CUDA(cudaMemcpyAsync(rp2.get(), drp.get(), urp.size() * 4, cudaMemcpyDeviceToDevice, s));
+      if (unnz) MPG_CUDA(cudaMemcpyAsync(ci2.get(), dci.get(), uci.size() * 4, cudaMemcpyDeviceToDevice, s));
+      return csr_from_device_parts(dev, n, n, std::move(rp2), std::move(ci2), std::move(vals));
+    }
+    std::vector<double> hv(static_cast<size_t>(unnz));
+    MPG_CUDA(cudaMemcpyAsync(hv.data(), vals.get(), hv.size() * 8, cudaMemcpyDeviceToHost, s));
+    MPG_CUDA(cudaStreamSynchronize(s));
+    std::vector<int64_t> rp64(size_t(n) + 1, 0), ci64;
+    std::vector<double> v64;
+    for (int64_t i = 0; i < n; ++i) {
+      for (int q = urp[size_t(i)]; q < urp[size_t(i) + 1]; ++q)
+        if (hv[size_t(q)] != 0.0) {
+          ci64.push_back(uci[size_t(q)]);
+          v64.push_back(hv[size_t(q)]);
+        }
+      rp64[size_t(i) + 1] = int64_t(ci64.size());
+    }
+    return csr_from_host(dev, n, n, rp64.data(), ci64.data(), v64.data());
+  }
+};
 }  // namespace
 
 std::vector<double> tf_error_run(const CsrPtr& m, const CsrPtr& d, const CsrPtr& k, const double* f_any, int n_in,
@@ -956,56 +1070,12 @@ std::vector<double> tf_error_run(const CsrPtr& m, const CsrPtr& d, const CsrPtr&
       rf.cols != n_in || rc.rows != r || rc.cols != n_out)
     throw std::invalid_argument("transfer_function_error: reduced model shapes do not match");
   if (n_in < 1 || n_out < 1 || n_out * n_in > 1024) throw std::invalid_argument("transfer_function_error: bad F / C");
-  // merged pattern of M, D, K with aligned values (zero-filled), built once
-  auto down = [&](const DevCsr& a, std::vector<int>& rp, std::vector<int>& ci, std::vector<double>& v) {
-    rp.resize(size_t(n) + 1);
-    ci.resize(size_t(a.nnz));
-    v.resize(size_t(a.nnz));
-    MPG_CUDA(cudaMemcpyAsync(rp.data(), a.rowptr.get(), rp.size() * 4, cudaMemcpyDeviceToHost, s));
-    if (a.nnz) {
-      MPG_CUDA(cudaMemcpyAsync(ci.data(), a.colind.get(), ci.size() * 4, cudaMemcpyDeviceToHost, s));
-      MPG_CUDA(cudaMemcpyAsync(v.data(), a.val.get(), v.size() * 8, cudaMemcpyDeviceToHost, s));
-    }
-  };
-  std::vector<int> rp3[3], ci3[3];
-  std::vector<double> v3[3];
-  down(*m, rp3[0], ci3[0], v3[0]);
-  down(*d, rp3[1], ci3[1], v3[1]);
-  down(*k, rp3[2], ci3[2], v3[2]);
-  MPG_CUDA(cudaStreamSynchronize(s));
-  std::vector<int> urp(size_t(n) + 1, 0), uci;
-  std::vector<double> uv[3];
-  for (int64_t i = 0; i < n; ++i) {
-    int p[3] = {rp3[0][size_t(i)], rp3[1][size_t(i)], rp3[2][size_t(i)]};
-    while (true) {
-      int c = INT32_MAX;
-      for (int t = 0; t < 3; ++t)
-        if (p[t] < rp3[t][size_t(i) + 1]) c = std::min(c, ci3[t][size_t(p[t])]);
-      if (c == INT32_MAX) break;
-      uci.push_back(c);
-      for (int t = 0; t < 3; ++t) {
-        double v = 0.0;
-        while (p[t] < rp3[t][size_t(i) + 1] && ci3[t][size_t(p[t])] == c) v += v3[t][size_t(p[t]++)];
-        uv[t].push_back(v);
-      }
-    }
-    urp[size_t(i) + 1] = int(uci.size());
-  }
-  const int64_t unnz = int64_t(uci.size());
-  DBuf<int> drp(dev, urp.size()), dci(dev, std::max<size_t>(1, uci.size()));
-  DBuf<double> dv[3];
-  MPG_CUDA(cudaMemcpyAsync(drp.get(), urp.data(), urp.size() * 4, cudaMemcpyHostToDevice, s));
-  if (unnz) MPG_CUDA(cudaMemcpyAsync(dci.get(), uci.data(), uci.size() * 4, cudaMemcpyHostToDevice, s));
-  for (int t = 0; t < 3; ++t) {
-    dv[t] = DBuf<double>(dev, std::max<size_t>(1, uv[t].size()));
-    if (unnz) MPG_CUDA(cudaMemcpyAsync(dv[t].get(), uv[t].data(), uv[t].size() * 8, cudaMemcpyHostToDevice, s));
-  }
+  const Pencil3 pencil(m, d, k);
   DBuf<double> F(dev, size_t(n) * n_in), Cm(dev, size_t(n) * n_out), X(dev, size_t(n) * n_in);
   copy_in(F.get(), f_any, size_t(n) * n_in, s);
   copy_in(Cm.get(), c_any, size_t(n) * n_out, s);
   std::vector<double> fnorm(static_cast<size_t>(n_in));
   for (int j = 0; j < n_in; ++j) fnorm[size_t(j)] = device_norm2(dev, F.get() + size_t(n) * j, n, s);
-  DBuf<unsigned long long> zeros(dev, 1);
 
   std::vector<double> errors(grid.size(), std::numeric_limits<double>::quiet_NaN());
   ChainPtr chain;
@@ -1014,40 +1084,7 @@ std::vector<double> tf_error_run(const CsrPtr& m, const CsrPtr& d, const CsrPtr&
   for (size_t g = 0; g < grid.size(); ++g) {
     const double sv = grid[g];
     if (!(sv > 0.0) || !std::isfinite(sv)) continue;
-    // A(s) = s^2 M + s D + K on the merged pattern; exact zeros dropped (sparse.cpp:191)
-    DBuf<double> vals(dev, std::max<size_t>(1, size_t(unnz)));
-    MPG_CUDA(cudaMemsetAsync(zeros.get(), 0, sizeof(unsigned long long), s));
-    if (unnz) {
-      k_comb3<<<unsigned(std::min<int64_t>((unnz + 255) / 256, int64_t(cx.sm_count) * 8)), 256, 0, s>>>(
-          dv[0].get(), dv[1].get(), dv[2].get(), sv * sv, sv, unnz, vals.get(), zeros.get());
-      MPG_CHECK_LAUNCH();
-      count_launch();
-    }
-    unsigned long long nz0 = 0;
-    MPG_CUDA(cudaMemcpyAsync(&nz0, zeros.get(), sizeof nz0, cudaMemcpyDeviceToHost, s));
-    MPG_CUDA(cudaStreamSynchronize(s));
-    CsrPtr A;
-    if (nz0 == 0) {
-      DBuf<int> rp2(dev, urp.size()), ci2(dev, std::max<size_t>(1, uci.size()));
-      MPG_CUDA(cudaMemcpyAsync(rp2.get(), drp.get(), urp.size() * 4, cudaMemcpyDeviceToDevice, s));
-      if (unnz) MPG_CUDA(cudaMemcpyAsync(ci2.get(), dci.get(), uci.size() * 4, cudaMemcpyDeviceToDevice, s));
-      A = csr_from_device_parts(dev, n, n, std::move(rp2), std::move(ci2), std::move(vals));
-    } else {
-      std::vector<double> hv(static_cast<size_t>(unnz));
-      MPG_CUDA(cudaMemcpyAsync(hv.data(), vals.get(), hv.size() * 8, cudaMemcpyDeviceToHost, s));
-      MPG_CUDA(cudaStreamSynchronize(s));
-      std::vector<int64_t> rp64(size_t(n) + 1, 0), ci64;
-      std::vector<double> v64;
-      for (int64_t i = 0; i < n; ++i) {
-        for (int q = urp[size_t(i)]; q < urp[size_t(i) + 1]; ++q)
-          if (hv[size_t(q)] != 0.0) {
-            ci64.push_back(uci[size_t(q)]);
-            v64.push_back(hv[size_t(q)]);
-          }
-        rp64[size_t(i) + 1] = int64_t(ci64.size());
-      }
-      A = csr_from_host(dev, n, n, rp64.data(), ci64.data(), v64.data());
-    }
+    const CsrPtr A = pencil.at(sv);
     ChainPtr prec;
     if (cfg.mode == MPG_PRECOND_FRESH) {
       auto ch = std::make_shared<Chain>();
@@ -1107,6 +1144,274 @@ std::vector<double> tf_error_run(const CsrPtr& m, const CsrPtr& d, const CsrPtr&
   }
   if (total_iterations) *total_iterations = its;
   return errors;
+}
+
+// ---- AIRGA (proj/src/airga.cpp:136-317) --------------------------------------------
+// Per sweep and expansion point: A(s_i) = s_i^2 M + s_i D + K from the merged
+// pattern, the preconditioner by mode (ReuseChain: fresh at the very first
+// point, horizontal updates along a sweep, a vertical update into the next
+// sweep's first point), the zeroth-moment block A X = F (n_in solves in one
+// batch), then higher moments A X = -M X_prev until the basis is full, nothing
+// new is appended, or the inner H2 gap drops below inner_tol; the basis is
+// OrthBasis (block scale = largest singular value, two-pass MGS, 1e-10
+// deflation) on the device; the reduced model and H2 gaps on the host.
+namespace {
+std::string airga_shortest(double v) {
+  char buf[64];
+  for (int prec = 1; prec <= 17; ++prec) {
+    std::snprintf(buf, sizeof buf, "%.*g", prec, v);
+    if (std::strtod(buf, nullptr) == v) break;
+  }
+  return buf;
+}
+}  // namespace
+
+AirgaOutcome airga_run(const CsrPtr& m, const CsrPtr& d, const CsrPtr& k, const double* f_any, int n_in,
+                       const double* c_any, int n_out, const AirgaSettings& cfg) {
+  const int dev = m->device;
+  auto& cx = ctx(dev);
+  DeviceGuard guard(dev);
+  cudaStream_t s = cx.stream;
+  const int64_t n = m->nrows;
+  for (const CsrPtr& x : {m, d, k})
+    if (x->nrows != n || x->ncols != n || x->device != dev)
+      throw ConfigError("second-order system: M, D, K must be n x n on one device");
+  if (n_in < 1 || n_out < 1) throw ConfigError("second-order system: F and C need at least one column");
+  std::vector<double> points = cfg.points;
+  if (points.empty()) throw ConfigError("airga: at least one expansion point is required");
+  std::sort(points.begin(), points.end());
+  for (double sp : points)
+    if (!(sp > 0.0) || !std::isfinite(sp)) throw ConfigError("airga: expansion points must be positive and finite");
+  if (std::adjacent_find(points.begin(), points.end()) != points.end())
+    throw ConfigError("airga: expansion points must be distinct");
+  const int ell = int(points.size());
+  if (cfg.r_max < ell)
+    throw ConfigError("airga: r_max (" + std::to_string(cfg.r_max) + ") must be at least the number of expansion points (" +
+                      std::to_string(ell) + ")");
+  if (cfg.max_outer < 1) throw ConfigError("airga: max_outer must be at least 1");
+  if (cfg.max_chain_len < 1) throw ConfigError("airga: max_chain_len must be at least 1");
+  if (cfg.r_max > 32 || n_in * n_out > 1024) throw ConfigError("airga: r_max <= 32 on the GPU path");
+
+  AirgaOutcome out;
+  const Pencil3 pencil(m, d, k);
+  {  // proportionality warning (airga.cpp:167-174)
+    const double dnorm = pencil.combo_norm(0.0, 1.0, 0.0);
+    const double defect = pencil.combo_norm(-cfg.alpha, 1.0, -cfg.beta);
+    if (dnorm > 0.0 && defect > 1e-12 * dnorm)
+      out.warnings.push_back("damping deviates from alpha*M + beta*K (relative defect " +
+                             airga_shortest(defect / dnorm) + "); reduction proceeds on D as given");
+  }
+  DBuf<double> F(dev, size_t(n) * n_in), Cm(dev, size_t(n) * n_out);
+  copy_in(F.get(), f_any, size_t(n) * n_in, s);
+  copy_in(Cm.get(), c_any, size_t(n) * n_out, s);
+  const int cap = cfg.r_max;
+  DBuf<double> U(dev, size_t(n) * cap), T(dev, size_t(n) * cap);
+  std::vector<DBuf<double>> blocks;
+  for (int i = 0; i < ell; ++i) blocks.emplace_back(dev, size_t(n) * n_in);
+  DBuf<double> RHS(dev, size_t(n) * n_in);
+  const unsigned gblk = unsigned(std::min<int64_t>((n + 255) / 256, int64_t(cx.sm_count) * 8));
+  auto dot = [&](const double* x, const double* y) { return ts_gram(dev, x, n, 1, y, n, 1, n).a[0]; };
+
+  ChainPtr prev_first_chain;
+  CsrPtr prev_first_matrix;
+  host::StateSpace prev_ss;
+  bool have_prev = false;
+  for (int z = 1; z <= cfg.max_outer; ++z) {
+    int size = 0;
+    std::vector<CsrPtr> a_ops;
+    for (double sp : points) a_ops.push_back(pencil.at(sp));
+    std::vector<ChainPtr> chains(static_cast<size_t>(ell));
+    std::vector<OpPtr> ops;
+    for (int i = 0; i < ell; ++i) ops.push_back(op_create(a_ops[size_t(i)], nullptr));
+    auto solve_block = [&](int i, const double* rhs, double sign, int moment, mpg_report_row& row) {
+      std::vector<SolveSpec> specs;
+      std::vector<int> cols;
+      double* xb = blocks[size_t(i)].get();
+      for (int j = 0; j < n_in; ++j) {
+        const double* bj = rhs + size_t(n) * j;
+        if (device_norm2(dev, bj, n, s) == 0.0) {
+          MPG_CUDA(cudaMemsetAsync(xb + size_t(n) * j, 0, size_t(n) * sizeof(double), s));
+          continue;
+        }
+        SolveSpec sp;
+        sp.sre = 0.0;
+        sp.ca = 1.0;
+        sp.chain = chains[size_t(i)];
+        sp.b = bj;
+        sp.x = xb + size_t(n) * j;
+        specs.push_back(sp);
+        cols.push_back(j);
+      }
+      if (specs.empty()) return;
+      const std::vector<GmresOutcome> oc = gmres_batch(*ops[size_t(i)], specs, cfg.gmres);
+      for (size_t t = 0; t < oc.size(); ++t) {
+        row.solves += 1;
+        row.iterations += oc[t].iterations;
+        row.gmres_seconds += oc[t].solve_seconds;
+        if (!oc[t].converged)
+          throw SolverError("gmres did not converge (sweep " + std::to_string(z) + ", point " + std::to_string(i + 1) +
+                            ", moment " + std::to_string(moment) + ", column " + std::to_string(cols[t]) +
+                            "; relative residual " +
+                            airga_shortest(oc[t].final_residual / std::max(oc[t].rhs_norm, 1e-300)) + " after " +
+                            std::to_string(oc[t].iterations) + " iterations)");
+        if (sign != 1.0) {
+          k_scal<<<gblk, 256, 0, s>>>(xb + size_t(n) * cols[t], sign, n);
+          MPG_CHECK_LAUNCH();
+          count_launch();
+        }
+      }
+    };
+    // OrthBasis::append_block (orth.cpp:16-40); returns the columns kept
+    auto append_block = [&](const double* blk) {
+      const Mat g = ts_gram(dev, blk, n, n_in, blk, n, n_in, n);
+      double smax = 0.0;
+      if (n_in == 1) {
+        smax = std::sqrt(std::max(g.a[0], 0.0));
+      } else {
+        for (const host::Eig& e : host::eigenvalues(g)) smax = std::max(smax, e.re);
+        smax = std::sqrt(std::max(smax, 0.0));
+      }
+      if (smax == 0.0) return 0;
+      const double cutoff = 1e-10 * smax;
+      int kept = 0;
+      for (int c = 0; c < n_in && size < cap; ++c) {
+        double* w = U.get() + size_t(n) * size_t(size);
+        MPG_CUDA(cudaMemcpyAsync(w, blk + size_t(n) * c, size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        for (int pass = 0; pass < 2; ++pass)
+          for (int j = 0; j < size; ++j) {
+            const double* uj = U.get() + size_t(n) * size_t(j);
+            const double dd = dot(uj, w);
+            k_axpy<<<gblk, 256, 0, s>>>(w, -dd, uj, n);
+            MPG_CHECK_LAUNCH();
+            count_launch();
+          }
+        const double nrm = std::sqrt(device_norm2(dev, w, n, s));
+        if (nrm <= cutoff) continue;
+        k_scal<<<gblk, 256, 0, s>>>(w, 1.0 / nrm, n);
+        MPG_CHECK_LAUNCH();
+        count_launch();
+        ++size;
+        ++kept;
+      }
+      return kept;
+    };
+    auto project = [&]() {
+      host::Mat rm, rd, rk;
+      for (int which = 0; which < 3; ++which) {
+        const DevCsr& a = which == 0 ? *m : which == 1 ? *d : *k;
+        for (int j = 0; j < size; ++j) {
+          launch_spmv(a, U.get() + size_t(n) * j, T.get() + size_t(n) * j, 1.0, s);
+          count_launch();
+        }
+        (which == 0 ? rm : which == 1 ? rd : rk) = ts_gram(dev, U.get(), n, size, T.get(), n, size, n);
+      }
+      out.m = rm;
+      out.d = rd;
+      out.k = rk;
+      out.f = ts_gram(dev, U.get(), n, size, F.get(), n, n_in, n);
+      out.c = ts_gram(dev, U.get(), n, size, Cm.get(), n, n_out, n);
+      return host::second_order_to_state_space(out.m, out.d, out.k, out.f, out.c);
+    };
+    auto h2_gap = [](const host::StateSpace& p, const host::StateSpace& q) {
+      const double dist = host::h2_distance(p, q);
+      if (!std::isfinite(dist)) return std::numeric_limits<double>::infinity();
+      const double scale = host::h2_norm(q);
+      if (!std::isfinite(scale)) return std::numeric_limits<double>::infinity();
+      return dist / std::max(1.0, scale);
+    };
+    // zeroth moments with the preconditioners (airga.cpp:196-262)
+    for (int i = 0; i < ell; ++i) {
+      mpg_report_row row{};
+      row.sweep = z;
+      row.point = i + 1;
+      row.kind = MPG_KIND_NONE;
+      row.min_residual = row.matrix_change = row.standard_residual = std::nan("");
+      const CsrPtr& A = a_ops[size_t(i)];
+      if (cfg.mode == MPG_PRECOND_FRESH) {
+        SpaiOutcome so = spai_or_update(A, nullptr, cfg.spai, false);
+        auto ch = std::make_shared<Chain>();
+        ch->factors.push_back(so.p);
+        chains[size_t(i)] = ch;
+        row.kind = MPG_KIND_FRESH;
+        row.build_seconds = so.build_seconds;
+      } else if (cfg.mode == MPG_PRECOND_REUSE_CHAIN || cfg.mode == MPG_PRECOND_REUSE_FROZEN) {
+        const bool first_ever = z == 1 && i == 0;
+        const ChainPtr parent = i == 0 ? (z == 1 ? nullptr : prev_first_chain) : chains[size_t(i) - 1];
+        if (first_ever || parent->length() + 1 > cfg.max_chain_len) {
+          SpaiOutcome so = spai_or_update(A, nullptr, cfg.spai, false);
+          auto ch = std::make_shared<Chain>();
+          ch->factors.push_back(so.p);
+          chains[size_t(i)] = ch;
+          row.kind = MPG_KIND_FRESH;
+          row.build_seconds = so.build_seconds;
+        } else {
+          const CsrPtr a_prev = i == 0 ? prev_first_matrix : a_ops[size_t(i) - 1];
+          SpaiOutcome so = spai_or_update(A, a_prev, cfg.spai, false);
+          auto ch = std::make_shared<Chain>(*parent);
+          ch->factors.push_back(so.p);
+          chains[size_t(i)] = ch;
+          row.kind = i == 0 ? MPG_KIND_VERTICAL : MPG_KIND_HORIZONTAL;
+          row.build_seconds = so.build_seconds;
+          row.min_residual = so.min_residual;
+          row.matrix_change = so.matrix_change;
+        }
+      }
+      solve_block(i, F.get(), 1.0, 0, row);
+      if (cfg.mode != MPG_PRECOND_NONE && n <= cfg.standard_residual_max_dim)
+        row.standard_residual = std_residual(A, chains[size_t(i)]);
+      out.rows.push_back(row);
+    }
+    for (int i = 0; i < ell; ++i) append_block(blocks[size_t(i)].get());
+    host::StateSpace red_ss = project();
+    std::vector<mpg_report_row> mrows(static_cast<size_t>(ell));
+    for (int i = 0; i < ell; ++i) {
+      mrows[size_t(i)] = mpg_report_row{};
+      mrows[size_t(i)].sweep = z;
+      mrows[size_t(i)].point = i + 1;
+      mrows[size_t(i)].kind = MPG_KIND_REUSED_SAME_MATRIX;
+      mrows[size_t(i)].min_residual = mrows[size_t(i)].matrix_change = mrows[size_t(i)].standard_residual = std::nan("");
+    }
+    for (int j = 1; size < cap; ++j) {  // higher moments (airga.cpp:272-292)
+      bool appended = false;
+      for (int i = 0; i < ell && size < cap; ++i) {
+        for (int c = 0; c < n_in; ++c) {
+          launch_spmv(*m, blocks[size_t(i)].get() + size_t(n) * c, RHS.get() + size_t(n) * c, 1.0, s);
+          count_launch();
+        }
+        solve_block(i, RHS.get(), -1.0, j, mrows[size_t(i)]);
+        if (append_block(blocks[size_t(i)].get()) > 0) appended = true;
+      }
+      if (!appended) break;
+      host::StateSpace next_ss = project();
+      const double gap = h2_gap(red_ss, next_ss);
+      red_ss = next_ss;
+      if (gap <= cfg.inner_tol) break;
+    }
+    if (size >= cap && cfg.r_max > ell)
+      out.warnings.push_back("sweep " + std::to_string(z) + ": basis reached r_max before inner convergence");
+    for (const auto& r : mrows)
+      if (r.solves > 0) out.rows.push_back(r);
+    out.sweeps = z;
+    out.r = size;
+    out.final_points = points;
+    out.basis = DBuf<double>(dev, size_t(n) * std::max(size, 1));
+    MPG_CUDA(cudaMemcpyAsync(out.basis.get(), U.get(), size_t(n) * size * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (have_prev && h2_gap(prev_ss, red_ss) <= cfg.outer_tol) {
+      out.converged = true;
+      break;
+    }
+    prev_ss = red_ss;
+    have_prev = true;
+    if (cfg.mode == MPG_PRECOND_REUSE_CHAIN || cfg.mode == MPG_PRECOND_REUSE_FROZEN) {
+      prev_first_chain = chains[0];
+      prev_first_matrix = a_ops[0];
+    }
+    if (z < cfg.max_outer) points = host::update_expansion_points(out.m, out.d, out.k, points);
+  }
+  if (!out.converged)
+    out.warnings.push_back("outer loop left unconverged after " + std::to_string(out.sweeps) + " sweeps");
+  MPG_CUDA(cudaStreamSynchronize(s));
+  return out;
 }
 
 }  // namespace mpg

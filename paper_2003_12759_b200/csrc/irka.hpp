@@ -101,3 +101,32 @@ std::vector<double> tf_error_run(const CsrPtr& m, const CsrPtr& d, const CsrPtr&
                                  const std::vector<double>& grid, const TfSettings& cfg, long long* total_iterations);
 
 }  // namespace mpg
+
+namespace mpg {
+
+// airga_reduce (proj/src/airga.cpp:136-317) on one device.
+struct AirgaSettings {
+  std::vector<double> points;
+  int r_max = 20;
+  double outer_tol = 1e-4, inner_tol = 1e-6;
+  int max_outer = 20;
+  GmresOptions gmres{1e-6, 1000, false};
+  SpaiOptions spai{};
+  int max_chain_len = 16;
+  long long standard_residual_max_dim = 5000;
+  int mode = MPG_PRECOND_REUSE_CHAIN;
+  double alpha = 0.0, beta = 0.0;
+};
+struct AirgaOutcome {
+  int r = 0, sweeps = 0;
+  bool converged = false;
+  host::Mat m, d, k, f, c;
+  DBuf<double> basis;  // n x r on the device
+  std::vector<double> final_points;
+  std::vector<mpg_report_row> rows;
+  std::vector<std::string> warnings;
+};
+AirgaOutcome airga_run(const CsrPtr& m, const CsrPtr& d, const CsrPtr& k, const double* f_any, int n_in,
+                       const double* c_any, int n_out, const AirgaSettings& cfg);
+
+}  // namespace mpg

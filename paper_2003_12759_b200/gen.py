@@ -138,6 +138,14 @@ def qb_toy(n: int, seed: int) -> QbSystem:
     return QbSystem(d, k, nop, h, e1, e1.copy())
 
 
+def disc_brake(n: int, omega: float, seed: int):
+    """generate_disc_brake_like (proj/src/generator.cpp:37-139): returns (M, K) host CSR; the reference then
+    forms D = alpha M + beta K and F = C = e_1."""
+    pm, pk = C.POINTER(L.HostCsr)(), C.POINTER(L.HostCsr)()
+    _check(lib.mpg_gen_disc_brake(n, omega, seed, C.byref(pm), C.byref(pk)))
+    return _take_csr(pm), _take_csr(pk)
+
+
 def _take_system(p) -> System:
     s = p.contents
     n = s.n

@@ -30,7 +30,8 @@ __all__ = [
     "standard_residual", "irka_reduce", "run_spai_bench", "ConfigError", "SolverError", "PrecondMode",
     "QbSystem", "QbConfig", "ReducedQb", "qbihomm_reduce", "IoError", "read_matrix_market",
     "read_matrix_market_file", "write_matrix_market", "write_matrix_market_file", "SecondOrderSystem",
-    "ReducedSecondOrder", "TransferErrorConfig", "transfer_function_error", "project",
+    "ReducedSecondOrder", "TransferErrorConfig", "transfer_function_error", "project", "AirgaConfig",
+    "airga_reduce", "update_expansion_points", "h2_norm",
 ]
 
 
@@ -859,4 +860,74 @@ def transfer_function_error(sys: SecondOrderSystem, red: ReducedSecondOrder, s_g
                                           L.ptr(g), g.size, C.byref(gc), C.byref(sc), cfg.mode, cfg.max_chain_len,
                                           L.ptr(out), C.byref(its)))
     return out
+
+
+@dataclasses.dataclass
+class AirgaConfig:
+    """AirgaConfig (airga.hpp:43-62)."""
+    expansion_points: Sequence[float] = ()
+    r_max: int = 20
+    outer_tol: float = 1e-4
+    inner_tol: float = 1e-6
+    max_outer: int = 20
+    gmres: GmresConfig = dataclasses.field(default_factory=GmresConfig)
+    spai: SpaiConfig = dataclasses.field(default_factory=SpaiConfig)
+    max_chain_len: int = 16
+    standard_residual_max_dim: int = 5000
+
+    def c(self) -> L.AirgaCfg:
+        return L.AirgaCfg(self.r_max, self.outer_tol, self.inner_tol, self.max_outer, self.gmres.c(), self.spai.c(),
+                          self.max_chain_len, self.standard_residual_max_dim)
+
+
+def airga_reduce(sys: SecondOrderSystem, cfg: AirgaConfig, mode: int = PrecondMode.REUSE_CHAIN):
+    """airga_reduce (airga.cpp:136-317): full-order solves on the GPU; returns (ReducedSecondOrder,
+    ReductionReport) with report.warnings and report.final_points."""
+    n = sys.dim()
+    n_in, n_out = sys.f.shape[1], sys.c.shape[1]
+    cap = max(1, cfg.r_max)
+    pts = L.f64(cfg.expansion_points)
+    rm, rd, rk = (np.zeros(cap * cap) for _ in range(3))
+    rf, rc = np.zeros(cap * n_in), np.zeros(cap * n_out)
+    basis = np.zeros(n * cap)
+    fp = np.zeros(max(1, pts.size))
+    order, sweeps, conv, nrows = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    maxrows = 2 * max(1, pts.size) * max(1, cfg.max_outer) + 4
+    rows = (L.ReportRow * maxrows)()
+    warn = C.c_void_p()
+    ac = cfg.c()
+    check(lib.mpg_airga_reduce(sys.m._h, sys.d._h, sys.k._h, L.ptr(sys.f), n_in, L.ptr(sys.c), n_out, sys.alpha,
+                               sys.beta, L.ptr(pts), pts.size, C.byref(ac), mode, C.byref(order), L.ptr(rm), L.ptr(rd),
+                               L.ptr(rk), L.ptr(rf), L.ptr(rc), L.ptr(basis), L.ptr(fp), C.byref(sweeps), C.byref(conv),
+                               rows, maxrows, C.byref(nrows), C.byref(warn)))
+    try:
+        text = C.string_at(warn.value).decode() if warn.value else ""
+    finally:
+        lib.mpg_buffer_free(warn)
+    r = order.value
+    sq = lambda a, rr, cc: a[: rr * cc].reshape((rr, cc), order="F").copy()
+    red = ReducedSecondOrder(sq(rm, r, r), sq(rd, r, r), sq(rk, r, r), sq(rf, r, n_in), sq(rc, r, n_out),
+                             sq(basis, n, r))
+    rep = ReductionReport(_rows(rows, min(nrows.value, maxrows)), bool(conv.value), r, sweeps.value,
+                          [w for w in text.split("\n") if w])
+    rep.final_points = fp[: pts.size].tolist()
+    return red, rep
+
+
+def update_expansion_points(m, d, k, current) -> list:
+    """update_expansion_points (airga.cpp:319-384) for a reduced pencil."""
+    mm, dd, kk = (np.asfortranarray(np.asarray(x, dtype=np.float64)) for x in (m, d, k))
+    cur = L.f64(current)
+    out = np.zeros(max(1, cur.size))
+    check(lib.mpg_update_expansion_points(L.ptr(mm), L.ptr(dd), L.ptr(kk), mm.shape[0], L.ptr(cur), cur.size,
+                                          L.ptr(out)))
+    return out[: cur.size].tolist()
+
+
+def h2_norm(a, b, c) -> float:
+    """h2_norm (proj/src/h2.cpp:28-60) of x' = A x + B u, y = C x; inf when A is not stable."""
+    aa, bb, cc = (np.asfortranarray(np.atleast_2d(np.asarray(x, dtype=np.float64))) for x in (a, b, c))
+    out = C.c_double()
+    check(lib.mpg_h2_norm(L.ptr(aa), L.ptr(bb), L.ptr(cc), aa.shape[0], bb.shape[1], cc.shape[0], C.byref(out)))
+    return out.value
 
