@@ -339,6 +339,31 @@ def run_transfer_error(args, device: int) -> dict:
             "mode": "horizontal chain along the grid (fresh SPAI every 17 points)"}
 
 
+def run_airga(args, device: int) -> dict:
+    """AIRGA on the C2 pencil at full size (64^3, n = 262 144): M = E, K = -A,
+    D = 0.05 M + 1e-4 K, SISO F, C from the config; 3 expansion points, r_max 12, 3 sweeps max,
+    ReuseChain preconditioning. Wall time of airga_reduce."""
+    import scipy.sparse as sp
+    import paper_2003_12759_b200 as mpg
+    from paper_2003_12759_b200 import gen
+    c2 = gen.config2()
+    Ms, Ks = c2.e_csr().to_scipy(), -c2.a.to_scipy()
+    Ds = (0.05 * Ms + 1e-4 * Ks).tocsr()
+    dev = lambda a: mpg.SparseMatrix.from_scipy(sp.csr_matrix(a), device)
+    sysm = mpg.SecondOrderSystem.create(dev(Ms), dev(Ds), dev(Ks), c2.b[:, :1], c2.c[:, :1], 0.05, 1e-4)
+    cfg = mpg.AirgaConfig(expansion_points=[1.0, 10.0, 100.0], r_max=12, max_outer=3,
+                          gmres=mpg.GmresConfig(args.tol, args.max_iter))
+    mpg.lib.mpg_synchronize(device)
+    t0 = time.perf_counter()
+    red, rep = mpg.airga_reduce(sysm, cfg, mpg.PrecondMode.REUSE_CHAIN)
+    mpg.lib.mpg_synchronize(device)
+    wall = time.perf_counter() - t0
+    tot = rep.totals()
+    return {"wall_s": round(wall, 3), "n": c2.n, "sweeps": rep.sweeps, "order": red.order(), "solves": tot["solves"],
+            "gmres_iterations": tot["gmres_iterations"], "precond_build_s": round(tot["precond_build_seconds"], 3),
+            "final_points": [round(x, 4) for x in rep.final_points]}
+
+
 def run_mmio(args) -> dict:
     """Matrix Market ingestion at the bench size: the C3
     operator written once with the library's writer (shortest round-trip
@@ -461,7 +486,7 @@ def main():
     ap.add_argument("--no-irka", action="store_true", help="skip the full-IRKA wall-time measurement")
     ap.add_argument("--no-qb", action="store_true", help="skip the QB-IHOMM wall-time measurement")
     ap.add_argument("--no-mm", action="store_true", help="skip the Matrix Market ingestion measurement")
-    ap.add_argument("--no-tf", action="store_true", help="skip the second-order transfer-error measurement")
+    ap.add_argument("--no-tf", action="store_true", help="skip the second-order (transfer error, AIRGA) measurements")
     ap.add_argument("--cpu-threads", type=int, default=0, help="host threads of the CPU sample (0: all, <= 16)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -483,6 +508,8 @@ def main():
         res["qbihomm"] = run_qbihomm(args, local)
     if world == 1 and not args.no_tf:
         res["transfer_error"] = run_transfer_error(args, local)
+    if world == 1 and not args.no_tf:
+        res["airga"] = run_airga(args, local)
     if world == 1 and not args.no_mm and rank == 0:
         res["matrix_market"] = run_mmio(args)
     if rank == 0:
