@@ -295,6 +295,9 @@ int mpg_gen_random_sparse(int64_t r, int64_t c, double density, uint64_t seed, d
 int mpg_gen_from_triplets(int64_t nr, int64_t nc, int64_t nnz, const int64_t* ri, const int64_t* ci, const double* v,
                           mpg_host_csr** out);
 int mpg_gen_bilinear_toy(int64_t n, int64_t m, uint64_t seed, mpg_host_csr** k_out, double* f, double* c);
+/* ... with the couplings N_1..N_m (n_out: m pointers). */
+int mpg_gen_bilinear_toy_n(int64_t n, int64_t m, uint64_t seed, mpg_host_csr** k_out, mpg_host_csr** n_out, double* f,
+                           double* c);
 /* generate_disc_brake_like (proj/src/generator.cpp:37-139): M and K = K_E + K_R + omega^2 K_G; D = alpha M + beta K
  * and F = C = e_1 are formed by the caller. */
 int mpg_gen_disc_brake(int64_t n, double omega, uint64_t seed, mpg_host_csr** m_out, mpg_host_csr** k_out);

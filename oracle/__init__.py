@@ -103,6 +103,9 @@ _SIGS = {
     "orc_qbihomm_reduce": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, vp, C.c_int, C.c_int, C.POINTER(GmresCfg),
                                      C.POINTER(SpaiCfg), C.c_int, C.c_longlong, C.c_int, C.c_int, ip, vp, vp, vp, vp,
                                      vp, vp, vp, vp, C.c_int, ip]),
+    "orc_birka_reduce": (C.c_int, [vp, vp, vp, C.c_int, vp, C.c_int, C.POINTER(IrkaCfg), C.c_int] + [vp] * 8
+                         + [ip, ip, vp, C.c_int, ip]),
+    "orc_kron_coupled": (C.c_int, [vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, C.POINTER(vp)]),
     "orc_kron_compress_quadratic": (C.c_int, [vp, vp, C.c_longlong, C.c_longlong, vp]),
     "orc_mm_read_buffer": (C.c_int, [C.c_char_p, C.c_longlong, C.c_char_p, C.POINTER(vp)]),
     "orc_mm_read_file": (C.c_int, [C.c_char_p, C.POINTER(vp)]),
@@ -663,4 +666,65 @@ def transfer_function_error(m: Csr, d: Csr, k: Csr, f, c, red, grid, gmres: Gmre
                                            _p(rk), _p(rf), _p(rc), r, _p(g), g.size, C.byref(gc), C.byref(sc), mode,
                                            max_chain_len, _p(out)))
     return out
+
+
+@dataclasses.dataclass
+class BirkaResult:
+    kr: np.ndarray
+    nr: list
+    fr: np.ndarray
+    cr: np.ndarray
+    lam: np.ndarray
+    v: np.ndarray
+    w: np.ndarray
+    sweeps: int
+    converged: bool
+    rows: list
+
+
+def birka_reduce(k: Csr, n_ops, b, c, cfg: IrkaConfig, mode: int = 2) -> BirkaResult:
+    """birka_reduce with couplings (proj/src/birka.cpp:139-310), joint n r solves."""
+    n = k.shape[0]
+    bm = np.asfortranarray(np.asarray(b, dtype=np.float64).reshape(n, -1))
+    cm = np.asfortranarray(np.asarray(c, dtype=np.float64).reshape(n, -1))
+    m, q, r = bm.shape[1], cm.shape[1], cfg.r
+    nptr = (vp * m)(*[x._h.value for x in n_ops])
+    kr, nr = np.zeros((r, r), order="F"), np.zeros(r * r * m)
+    fr, cr = np.zeros((r, m), order="F"), np.zeros((r, q), order="F")
+    lre, lim = np.zeros(r), np.zeros(r)
+    v, w = np.zeros((n, r), order="F"), np.zeros((n, r), order="F")
+    sweeps, conv, nrows = C.c_int(), C.c_int(), C.c_int()
+    maxrows = 2 * max(cfg.max_sweeps, 1) + 8
+    rows = (ReportRow * maxrows)()
+    cc = cfg.c()
+    _check(lib.orc_birka_reduce(k._h, nptr, _p(bm), m, _p(cm), q, C.byref(cc), mode, _p(kr), _p(nr), _p(fr), _p(cr),
+                                _p(lre), _p(lim), _p(v), _p(w), C.byref(sweeps), C.byref(conv), rows, maxrows,
+                                C.byref(nrows)))
+    nrs = [nr[j * r * r:(j + 1) * r * r].reshape((r, r), order="F").copy() for j in range(m)]
+    return BirkaResult(kr, nrs, fr, cr, lre + 1j * lim, v, w, sweeps.value, bool(conv.value),
+                       [rows[i] for i in range(min(nrows.value, maxrows))])
+
+
+def _kron_coupled(lam, k: Csr, couplers, x=None, assemble=False):
+    lam = np.asfortranarray(np.asarray(lam, dtype=np.float64))
+    r = lam.shape[0]
+    smalls = np.concatenate([np.asfortranarray(np.asarray(s, dtype=np.float64)).reshape(-1, order="F")
+                             for s, _ in couplers]) if couplers else np.zeros(1)
+    sp = (vp * max(1, len(couplers)))(*[m._h.value for _, m in couplers])
+    y = np.zeros(k.shape[0] * r) if x is not None else None
+    xx = _f64(x) if x is not None else None
+    h = vp()
+    _check(lib.orc_kron_coupled(_p(lam), r, k._h, len(couplers), _p(smalls), sp, _p(xx), _p(y),
+                                C.byref(h) if assemble else None))
+    return Csr(h.value) if assemble else y
+
+
+def kron_apply_coupled(lam, k: Csr, couplers, x):
+    """vec(-X Lambda^T - K X - sum_j N_j X S_j) (kron.cpp:34-64); couplers = [(S_j, N_j)]."""
+    return _kron_coupled(lam, k, couplers, x=x)
+
+
+def kron_assemble_coupled(lam, k: Csr, couplers) -> Csr:
+    """assemble_explicit with couplers (kron.cpp:72-131), no cap."""
+    return _kron_coupled(lam, k, couplers, assemble=True)
 

@@ -423,4 +423,53 @@ int orc_transfer_function_error(const Csr* m, const Csr* d, const Csr* k, const 
   });
 }
 
+// BIRKA with couplings N_1..N_m (proj/src/birka.cpp:139-310): the joint n r
+// solve per side; outputs kr (r x r), nr (m blocks of r x r), fr, cr, lambda,
+// v, w (n x r), any output may be null.
+int orc_birka_reduce(const Csr* a, const Csr* const* n_ops, const double* b, int m, const double* c, int q,
+                     const orc_irka_cfg* cfg, int mode, double* kr, double* nr, double* fr, double* cr,
+                     double* lam_re, double* lam_im, double* v, double* w, int* sweeps, int* converged,
+                     orc_report_row* rows, int max_rows, int* nrows) {
+  return guard([&] {
+    LinearSystem sys = make_sys(a, nullptr, b, m, c, q);
+    for (int j = 0; j < m; ++j) sys.n_ops.push_back(*n_ops[j]);
+    IrkaConfig ic;
+    ic.r = cfg->r; ic.tol = cfg->tol; ic.max_sweeps = cfg->max_sweeps; ic.seed = cfg->seed;
+    ic.gmres = to_gmres(&cfg->gmres); ic.spai = to_spai(&cfg->spai); ic.max_chain_len = cfg->max_chain_len;
+    ic.explicit_nnz_cap = cfg->explicit_nnz_cap; ic.standard_residual_max_dim = cfg->standard_residual_max_dim;
+    ic.decoupled = false;
+    auto [st, rep] = irka_reduce(sys, ic, PrecondMode(mode), nullptr);
+    const size_t rr = size_t(st.kr.rows);
+    if (kr) std::memcpy(kr, st.kr.a.data(), rr * rr * sizeof(double));
+    if (nr)
+      for (size_t j = 0; j < st.nr.size(); ++j) std::memcpy(nr + j * rr * rr, st.nr[j].a.data(), rr * rr * sizeof(double));
+    if (fr) std::memcpy(fr, st.fr.a.data(), st.fr.a.size() * sizeof(double));
+    if (cr) std::memcpy(cr, st.cr.a.data(), st.cr.a.size() * sizeof(double));
+    for (size_t i = 0; i < st.lambda.size(); ++i) {
+      if (lam_re) lam_re[i] = st.lambda[i].re;
+      if (lam_im) lam_im[i] = st.lambda[i].im;
+    }
+    if (v) std::memcpy(v, st.v.a.data(), st.v.a.size() * sizeof(double));
+    if (w) std::memcpy(w, st.w.a.data(), st.w.a.size() * sizeof(double));
+    *sweeps = st.sweeps;
+    *converged = rep.converged;
+    copy_rows(rep, rows, max_rows, nrows);
+  });
+}
+
+// Kronecker operator with couplers (kron.cpp:34-131): apply and explicit assembly.
+int orc_kron_coupled(const double* lambda, int r, const Csr* a, int ncp, const double* smalls, const Csr* const* sparses,
+                     const double* x, double* y, Csr** explicit_out) {
+  return guard([&] {
+    KronOp op{dense_from(lambda, r, r), a, nullptr, {}};
+    for (int j = 0; j < ncp; ++j) op.couplers.push_back({dense_from(smalls + size_t(j) * r * r, r, r), sparses[j]});
+    if (x && y) {
+      Vec in(x, x + a->nrows * r), out;
+      op.apply(in, out);
+      std::copy(out.begin(), out.end(), y);
+    }
+    if (explicit_out) *explicit_out = new Csr(assemble_explicit(op, (index_t(1) << 40)));
+  });
+}
+
 }  // extern "C"

@@ -63,6 +63,7 @@ IrkaState irka_default_seed(const LinearSystem& sys, int r, std::uint64_t seed) 
     const double t = r == 1 ? 1.0 : double(i) / (r - 1);
     s.kr(i, i) = -radius * std::pow(10.0, -3.0 * (1.0 - t));
   }
+  s.nr.assign(sys.n_ops.size(), Dense(r, r));  // birka.cpp:76
   s.fr = Dense(r, sys.b.cols);
   s.cr = Dense(r, sys.c.cols);
   for (Dense* m : {&s.fr, &s.cr})
@@ -86,13 +87,22 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
   if (sys.c.rows != n || sys.c.cols < 1) throw ConfigError("irka: C must have n rows and at least one column");
   if (cfg.max_sweeps < 1) throw ConfigError("birka: max_sweeps must be at least 1");
   if (cfg.max_chain_len < 1) throw ConfigError("birka: max_chain_len must be at least 1");
+  for (const Csr& nj : sys.n_ops)
+    if (nj.nrows != n || nj.ncols != n) throw ConfigError("bilinear system: every N must be n x n");
+  if (!sys.n_ops.empty() && index_t(sys.n_ops.size()) != sys.b.cols)
+    throw ConfigError("bilinear system: one N per input is required");
+  if (!sys.n_ops.empty() && sys.e) throw ConfigError("irka: couplings with a mass matrix are not supported");
   IrkaState state = init ? *init : irka_default_seed(sys, cfg.r, cfg.seed);
+  if (state.nr.size() != sys.n_ops.size()) state.nr.assign(sys.n_ops.size(), Dense(state.kr.rows, state.kr.rows));
   const index_t r = state.kr.rows;
   if (r < 1 || r > n) throw ConfigError("birka: reduced order must be in [1, n]");
   if (state.fr.rows != r || state.fr.cols != sys.b.cols || state.cr.rows != r || state.cr.cols != sys.c.cols)
     throw ConfigError("birka: initial state dimensions do not match the system");
 
   const Csr at = sys.a.transpose();
+  std::vector<Csr> nts;
+  for (const Csr& nj : sys.n_ops) nts.push_back(nj.transpose());
+  const bool coupled = !sys.n_ops.empty();
   std::shared_ptr<Csr> et;
   if (sys.e) et = std::make_shared<Csr>(sys.e->transpose());
 
@@ -127,7 +137,12 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
     const Dense rinv_t = spec.basis_inv.transpose();
     const Dense f2 = matmul(state.fr.transpose(), rinv_t);  // m x r, :182
     const Dense c2 = matmul(state.cr.transpose(), spec.basis);  // q x r, :183
-    const KronOp ops[2] = {{spec.blocks, &sys.a, sys.e.get()}, {spec.blocks, &at, et.get()}};
+    KronOp ops[2] = {{spec.blocks, &sys.a, sys.e.get(), {}}, {spec.blocks, &at, et.get(), {}}};
+    for (size_t j = 0; j < sys.n_ops.size(); ++j) {  // n2[j] = R^T nr[j] R^{-T} (birka.cpp:184-194)
+      const Dense n2 = matmul(matmul(spec.basis.transpose(), state.nr[j]), rinv_t);
+      ops[0].couplers.push_back({n2, &sys.n_ops[j]});
+      ops[1].couplers.push_back({n2.transpose(), &nts[j]});
+    }
     const Dense rhs_mats[2] = {matmul(sys.b, f2), matmul(sys.c, c2)};  // :199
 
     Dense bases[2];
@@ -142,7 +157,7 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
       // Units: one joint n*r solve (reference), or one solve per real shift /
       // conjugate-pair block (decoupled; same fixed point).
       std::vector<std::pair<index_t, index_t>> units;  // (first column, width)
-      if (cfg.decoupled) {
+      if (cfg.decoupled && !coupled) {
         for (index_t c = 0; c < r;) {
           const index_t w = (c + 1 < r && spec.blocks(c, c + 1) != 0.0) ? 2 : 1;
           units.push_back({c, w});
@@ -159,9 +174,11 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
         Dense lam(width, width);
         for (index_t i = 0; i < width; ++i)
           for (index_t j = 0; j < width; ++j) lam(i, j) = spec.blocks(c0 + i, c0 + j);
-        const KronOp op{lam, ops[side].a, ops[side].e};
-        SidePrecond& sp = cfg.decoupled ? unit_sides[size_t(side)][size_t(c0)] : sides[size_t(side)];
-        if (cfg.decoupled && sp.shape != width) {  // slot changed shape: restart its chain
+        KronOp op{lam, ops[side].a, ops[side].e, {}};
+        if (coupled) op.couplers = ops[side].couplers;  // the joint solve (width = r)
+        const bool dec = cfg.decoupled && !coupled;
+        SidePrecond& sp = dec ? unit_sides[size_t(side)][size_t(c0)] : sides[size_t(side)];
+        if (dec && sp.shape != width) {  // slot changed shape: restart its chain
           sp = SidePrecond{};
           sp.shape = int(width);
         }
@@ -234,6 +251,7 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
     state.er = er;
     state.ar = ar;
     state.kr = lu.solve(ar);
+    for (size_t j = 0; j < sys.n_ops.size(); ++j) state.nr[j] = lu.solve(matmul(wt, dense_of(sys.n_ops[j], v)));
     state.fr = lu.solve(matmul(wt, sys.b));
     state.cr = matmul(v.transpose(), sys.c);
     state.v = v;

@@ -199,6 +199,9 @@ struct KronOp {
   Dense lambda;
   const Csr* a = nullptr;
   const Csr* e = nullptr;
+  // bilinear couplers (kron.cpp:54-63): -(S^T (x) N) vec(X) = -vec(N X S)
+  struct Coupler { Dense small; const Csr* sparse; };
+  std::vector<Coupler> couplers;
   void apply(const Vec& in, Vec& out) const;
   index_t dim() const { return a->nrows * lambda.rows; }
 };
@@ -226,6 +229,7 @@ struct ReductionReport {
 // ---- IRKA (BIRKA with N = 0, proj/src/birka.cpp:139-310), E general -------
 struct LinearSystem {
   Csr a;                   // n x n (reference K)
+  std::vector<Csr> n_ops;  // bilinear couplings N_j (one per input), empty = linear
   std::shared_ptr<Csr> e;  // n x n mass, null = identity
   Dense b;                 // n x m (reference F)
   Dense c;                 // n x q (reference C)
@@ -245,6 +249,7 @@ struct IrkaConfig {
 };
 struct IrkaState {
   Dense kr, fr, cr;        // reduced K = E_r^{-1} A_r, E_r^{-1} W^T B, V^T C
+  std::vector<Dense> nr;   // reduced couplings E_r^{-1} W^T N_j V
   Dense er, ar;            // W^T E V, W^T A V
   std::vector<Complex> lambda;
   Dense v, w;

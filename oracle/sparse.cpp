@@ -260,6 +260,19 @@ void KronOp::apply(const Vec& in, Vec& out) const {
     a->multiply(col, tmp);
     for (index_t i = 0; i < n; ++i) out[size_t(c * n + i)] -= tmp[size_t(i)];
   }
+  // couplers: mixed = X S (n x r), y(:, c) -= N mixed(:, c)  (kron.cpp:54-63)
+  for (const Coupler& cp : couplers) {
+    for (index_t c = 0; c < r; ++c) {
+      std::fill(col.begin(), col.end(), 0.0);
+      for (index_t b = 0; b < r; ++b) {
+        const double sv = cp.small(b, c);
+        if (sv == 0.0) continue;
+        for (index_t i = 0; i < n; ++i) col[size_t(i)] += in[size_t(b * n + i)] * sv;
+      }
+      cp.sparse->multiply(col, tmp);
+      for (index_t i = 0; i < n; ++i) out[size_t(c * n + i)] -= tmp[size_t(i)];
+    }
+  }
 }
 
 // proj/src/kron.cpp:72-131 (cap estimate counts Lambda entries times nnz(E))
@@ -269,7 +282,13 @@ Csr assemble_explicit(const KronOp& op, index_t max_nnz) {
   for (index_t i = 0; i < r; ++i)
     for (index_t j = 0; j < r; ++j) lambda_nnz += op.lambda(i, j) != 0.0;
   const index_t e_nnz = op.e ? op.e->nnz() : n;
-  const index_t estimate = lambda_nnz * e_nnz + r * op.a->nnz();
+  index_t estimate = lambda_nnz * e_nnz + r * op.a->nnz();
+  for (const auto& cp : op.couplers) {
+    index_t small_nnz = 0;
+    for (index_t i = 0; i < r; ++i)
+      for (index_t j = 0; j < r; ++j) small_nnz += cp.small(i, j) != 0.0;
+    estimate += small_nnz * cp.sparse->nnz();
+  }
   if (estimate > max_nnz)
     throw ConfigError("explicit operator assembly needs about " + std::to_string(estimate) +
                       " entries, above the cap of " + std::to_string(max_nnz) +
@@ -292,6 +311,17 @@ Csr assemble_explicit(const KronOp& op, index_t max_nnz) {
     for (index_t i = 0; i < n; ++i)
       for (index_t k = op.a->rowptr[size_t(i)]; k < op.a->rowptr[size_t(i) + 1]; ++k)
         t.push_back({b * n + i, b * n + op.a->colind[size_t(k)], -op.a->val[size_t(k)]});
+  // -(S^T (x) N): block (bi, bj) is -S(bj, bi) N  (kron.cpp:115-128)
+  for (const auto& cp : op.couplers)
+    for (index_t bi = 0; bi < r; ++bi)
+      for (index_t bj = 0; bj < r; ++bj) {
+        const double sv = cp.small(bj, bi);
+        if (sv == 0.0) continue;
+        const Csr& nm = *cp.sparse;
+        for (index_t i = 0; i < n; ++i)
+          for (index_t k = nm.rowptr[size_t(i)]; k < nm.rowptr[size_t(i) + 1]; ++k)
+            t.push_back({bi * n + i, bj * n + nm.colind[size_t(k)], -sv * nm.val[size_t(k)]});
+      }
   return Csr::from_triplets(n * r, n * r, std::move(t));
 }
 

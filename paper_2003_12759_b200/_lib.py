@@ -181,6 +181,7 @@ _SIGS = {
     "mpg_gen_from_triplets": (_I, [_L, _L, _L, vp, vp, vp, C.POINTER(C.POINTER(HostCsr))]),
     "mpg_gen_bilinear_toy": (_I, [_L, _L, C.c_uint64, C.POINTER(C.POINTER(HostCsr)), vp, vp]),
     "mpg_gen_disc_brake": (_I, [_L, _D, C.c_uint64, C.POINTER(C.POINTER(HostCsr)), C.POINTER(C.POINTER(HostCsr))]),
+    "mpg_gen_bilinear_toy_n": (_I, [_L, _L, C.c_uint64, C.POINTER(C.POINTER(HostCsr)), vp, vp, vp]),
     "mpg_gen_qb_toy": (_I, [_L, C.c_uint64] + [C.POINTER(C.POINTER(HostCsr))] * 4),
     "mpg_gen_grid2d": (_I, [_L, C.c_uint64, C.POINTER(C.POINTER(HostSystem))]),
     "mpg_gen_convdiff3d": (_I, [_L, C.c_uint64, C.POINTER(C.POINTER(HostSystem))]),

@@ -200,7 +200,8 @@ int mpg_gen_from_triplets(int64_t nr, int64_t nc, int64_t nnz, const int64_t* ri
 // proj/src/generator.cpp:141-179 with the couplings' draws consumed but the
 // couplings dropped (N = 0, the linear IRKA case of proj/tests/test_birka.cpp:51-75).
 // f: n x m column-major, c: n x 1.
-int mpg_gen_bilinear_toy(int64_t n, int64_t m, uint64_t seed, mpg_host_csr** k_out, double* f, double* c) {
+static int bilinear_toy_impl(int64_t n, int64_t m, uint64_t seed, mpg_host_csr** k_out, mpg_host_csr** n_out, double* f,
+                             double* c) {
   return gen_guard([&] {
     if (n < 2) throw std::invalid_argument("generator: n must be at least 2");
     if (m < 1) throw std::invalid_argument("generator: at least one input is required");
@@ -225,12 +226,30 @@ int mpg_gen_bilinear_toy(int64_t n, int64_t m, uint64_t seed, mpg_host_csr** k_o
     *k_out = combine(-1.0, stencil, 1.0, pert);
     mpg_host_csr_free(stencil);
     mpg_host_csr_free(pert);
-    for (int64_t j = 0; j < m; ++j)
-      for (int64_t i = 0; i < n; ++i) { (void)node(rng); (void)sym(rng); }
+    for (int64_t j = 0; j < m; ++j) {
+      std::vector<Trip> t;
+      for (int64_t i = 0; i < n; ++i) {
+        const int64_t col = node(rng);
+        t.push_back({i, col, 0.05 * sym(rng)});
+      }
+      mpg_host_csr* nj = from_trips(n, n, std::move(t));
+      if (n_out) n_out[j] = nj;
+      else mpg_host_csr_free(nj);
+    }
     for (int64_t j = 0; j < m; ++j)
       for (int64_t i = 0; i < n; ++i) f[i + j * n] = sym(rng);
     for (int64_t i = 0; i < n; ++i) c[i] = sym(rng);
   });
+}
+
+// generate_bilinear_toy (proj/src/generator.cpp:141-179): K, F (n x m), C (n x 1);
+// the couplings N_j (one per input) are drawn and returned by the _n variant.
+int mpg_gen_bilinear_toy(int64_t n, int64_t m, uint64_t seed, mpg_host_csr** k_out, double* f, double* c) {
+  return bilinear_toy_impl(n, m, seed, k_out, nullptr, f, c);
+}
+int mpg_gen_bilinear_toy_n(int64_t n, int64_t m, uint64_t seed, mpg_host_csr** k_out, mpg_host_csr** n_out, double* f,
+                           double* c) {
+  return bilinear_toy_impl(n, m, seed, k_out, n_out, f, c);
 }
 
 // generate_qb_toy (proj/src/generator.cpp:181-207): D = tridiag(-1, 4, -1),

@@ -146,6 +146,16 @@ def disc_brake(n: int, omega: float, seed: int):
     return _take_csr(pm), _take_csr(pk)
 
 
+def bilinear_toy_n(n: int, m: int, seed: int):
+    """generate_bilinear_toy (proj/src/generator.cpp:141-179) with its couplings: (K, [N_1..N_m], F, C)."""
+    pk = C.POINTER(L.HostCsr)()
+    pn = (C.POINTER(L.HostCsr) * m)()
+    f = np.empty(n * m)
+    c = np.empty(n)
+    _check(lib.mpg_gen_bilinear_toy_n(n, m, seed, C.byref(pk), C.cast(pn, C.c_void_p), L.ptr(f), L.ptr(c)))
+    return _take_csr(pk), [_take_csr(pn[j]) for j in range(m)], f.reshape((n, m), order="F"), c.reshape((n, 1))
+
+
 def _take_system(p) -> System:
     s = p.contents
     n = s.n
