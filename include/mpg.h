@@ -218,6 +218,20 @@ int mpg_irka_reduce(const mpg_op* op, const double* b, int m, const double* c, i
                     double* lam_re, double* lam_im, double* v, double* w, int* sweeps, int* converged,
                     mpg_report_row* rows, int max_rows, int* nrows);
 
+/* BIRKA with couplings N_1..N_m (birka_reduce, proj/src/birka.cpp:139-310;
+ * the coupled path is the reference's joint solve): per sweep and side one
+ * GMRES of order n r on the explicitly assembled Kronecker operator
+ * -(Lambda (x) I) - (I (x) K) - sum_j (S_j^T (x) N_j) (kron.cpp:72-131),
+ * preconditioned per `mode` with a vertical chain per side; a side whose
+ * assembly would exceed cfg->explicit_nnz_cap continues unpreconditioned
+ * with a warning (birka.cpp:214-236). n_ops: m CSR handles (n x n) on k's
+ * device. Outputs as mpg_irka_reduce plus nr (m blocks of r x r,
+ * column-major); warnings: malloc'ed text (mpg_buffer_free), may be NULL. */
+int mpg_birka_reduce(const mpg_csr* k, const mpg_csr* const* n_ops, const double* b, int m, const double* c, int q,
+                     const mpg_irka_cfg* cfg, int mode, double* kr, double* nr, double* fr, double* cr,
+                     double* lam_re, double* lam_im, double* v, double* w, int* sweeps, int* converged,
+                     mpg_report_row* rows, int max_rows, int* nrows, char** warnings);
+
 /* IRKA projection (birka.cpp:283-291, generalised to E): E_r = W^T E V and
  * A_r = W^T A V (r x r, column-major, host) for V, W (n x r, column-major, any
  * memory); r <= 32. With E = I, E_r = W^T V as in the reference. */

@@ -430,6 +430,44 @@ int mpg_irka_reduce(const mpg_op* op, const double* b, int m, const double* c, i
   });
 }
 
+static int put_buffer(const std::string& text, char** out, int64_t* len);
+
+int mpg_birka_reduce(const mpg_csr* k, const mpg_csr* const* n_ops, const double* b, int m, const double* c, int q,
+                     const mpg_irka_cfg* cfg, int mode, double* kr, double* nr, double* fr, double* cr,
+                     double* lam_re, double* lam_im, double* v, double* w, int* sweeps, int* converged,
+                     mpg_report_row* rows, int max_rows, int* nrows, char** warnings) {
+  return guard([&] {
+    if (!k || (m > 0 && !n_ops)) throw ConfigError("birka: null operator");
+    std::vector<CsrPtr> ns;
+    for (int j = 0; j < m; ++j) {
+      if (!n_ops[j]) throw ConfigError("birka: null coupling matrix");
+      ns.push_back(n_ops[j]->p);
+    }
+    IrkaSettings s = to_irka(cfg, mode, nullptr);
+    BirkaOutcome o = birka_coupled_run(k->p, ns, b, m, c, q, s, cfg->explicit_nnz_cap);
+    if (kr) std::memcpy(kr, o.kr.a.data(), o.kr.a.size() * 8);
+    for (size_t j = 0; nr && j < o.nr.size(); ++j)
+      std::memcpy(nr + j * o.nr[j].a.size(), o.nr[j].a.data(), o.nr[j].a.size() * 8);
+    if (fr) std::memcpy(fr, o.fr.a.data(), o.fr.a.size() * 8);
+    if (cr) std::memcpy(cr, o.cr.a.data(), o.cr.a.size() * 8);
+    for (size_t i = 0; i < o.lambda.size(); ++i) {
+      if (lam_re) lam_re[i] = o.lambda[i].re;
+      if (lam_im) lam_im[i] = o.lambda[i].im;
+    }
+    if (v) std::memcpy(v, o.v.data(), o.v.size() * 8);
+    if (w) std::memcpy(w, o.w.data(), o.w.size() * 8);
+    if (sweeps) *sweeps = o.sweeps;
+    if (converged) *converged = o.converged;
+    copy_rows(o.rows, rows, max_rows, nrows);
+    if (warnings) {
+      std::string t;
+      for (const auto& wn : o.warnings) t += wn + "\n";
+      int64_t len = 0;
+      put_buffer(t, warnings, &len);
+    }
+  });
+}
+
 int mpg_irka_reduce_sharded(const mpg_op* op, const double* b, int m, const double* c, int q,
                             const mpg_irka_cfg* cfg, int mode, const double* init_shifts, int rank, int world,
                             mpg_allgather_fn allgather, void* actx, double* kr, double* fr, double* cr,

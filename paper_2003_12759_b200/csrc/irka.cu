@@ -1414,4 +1414,323 @@ AirgaOutcome airga_run(const CsrPtr& m, const CsrPtr& d, const CsrPtr& k, const 
   return out;
 }
 
+// ---- BIRKA with couplings (proj/src/birka.cpp:139-310, kron.cpp:34-131) ------------
+namespace {
+struct HostCsr32 {
+  int64_t n = 0;
+  std::vector<int> rp, ci;
+  std::vector<double> v;
+};
+HostCsr32 download_csr(const DevCsr& a) {
+  HostCsr32 h;
+  h.n = a.nrows;
+  h.rp.resize(size_t(a.nrows) + 1);
+  h.ci.resize(size_t(a.nnz));
+  h.v.resize(size_t(a.nnz));
+  cudaStream_t s = ctx(a.device).stream;
+  MPG_CUDA(cudaMemcpyAsync(h.rp.data(), a.rowptr.get(), h.rp.size() * 4, cudaMemcpyDeviceToHost, s));
+  if (a.nnz) {
+    MPG_CUDA(cudaMemcpyAsync(h.ci.data(), a.colind.get(), h.ci.size() * 4, cudaMemcpyDeviceToHost, s));
+    MPG_CUDA(cudaMemcpyAsync(h.v.data(), a.val.get(), h.v.size() * 8, cudaMemcpyDeviceToHost, s));
+  }
+  MPG_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+HostCsr32 transpose_host(const HostCsr32& a) {
+  HostCsr32 t;
+  t.n = a.n;
+  t.rp.assign(size_t(a.n) + 1, 0);
+  for (int c : a.ci) ++t.rp[size_t(c) + 1];
+  for (int64_t i = 0; i < a.n; ++i) t.rp[size_t(i) + 1] += t.rp[size_t(i)];
+  t.ci.resize(a.ci.size());
+  t.v.resize(a.v.size());
+  std::vector<int> pos(t.rp.begin(), t.rp.end() - 1);
+  for (int64_t i = 0; i < a.n; ++i)
+    for (int k = a.rp[size_t(i)]; k < a.rp[size_t(i) + 1]; ++k) {
+      const int c = a.ci[size_t(k)];
+      t.ci[size_t(pos[size_t(c)])] = int(i);
+      t.v[size_t(pos[size_t(c)]++)] = a.v[size_t(k)];
+    }
+  return t;
+}
+// assemble_explicit (kron.cpp:72-131): -(Lambda (x) I) - (I (x) K) - sum (S^T (x) N); the
+// triplets are generated row by row, so each row is built sorted and summed directly.
+CsrPtr assemble_kron(int dev, const Mat& lam, const HostCsr32& k, const std::vector<std::pair<Mat, const HostCsr32*>>& cps,
+                     int64_t& estimate) {
+  const int64_t n = k.n;
+  const int r = lam.rows;
+  int64_t lnz = 0;
+  for (double x : lam.a) lnz += x != 0.0;
+  estimate = lnz * n + int64_t(r) * int64_t(k.v.size());
+  for (const auto& cp : cps) {
+    int64_t snz = 0;
+    for (double x : cp.first.a) snz += x != 0.0;
+    estimate += snz * int64_t(cp.second->v.size());
+  }
+  std::vector<int64_t> rp(size_t(n * r) + 1, 0), ci;
+  std::vector<double> vv;
+  std::vector<std::pair<int64_t, double>> row;
+  for (int bi = 0; bi < r; ++bi)
+    for (int64_t i = 0; i < n; ++i) {
+      row.clear();
+      for (int bj = 0; bj < r; ++bj)
+        if (lam(bi, bj) != 0.0) row.push_back({bj * n + i, -lam(bi, bj)});
+      for (int kk = k.rp[size_t(i)]; kk < k.rp[size_t(i) + 1]; ++kk) row.push_back({bi * n + k.ci[size_t(kk)], -k.v[size_t(kk)]});
+      for (const auto& cp : cps)
+        for (int bj = 0; bj < r; ++bj) {
+          const double sv = cp.first(bj, bi);
+          if (sv == 0.0) continue;
+          const HostCsr32& nm = *cp.second;
+          for (int kk = nm.rp[size_t(i)]; kk < nm.rp[size_t(i) + 1]; ++kk)
+            row.push_back({bj * n + nm.ci[size_t(kk)], -sv * nm.v[size_t(kk)]});
+        }
+      std::stable_sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      for (size_t p = 0; p < row.size();) {
+        const int64_t c = row[p].first;
+        double sum = 0.0;
+        while (p < row.size() && row[p].first == c) sum += row[p++].second;
+        ci.push_back(c);
+        vv.push_back(sum);
+      }
+      rp[size_t(bi * n + i) + 1] = int64_t(ci.size());
+    }
+  return csr_from_host(dev, n * r, n * r, rp.data(), ci.data(), vv.data());
+}
+}  // namespace
+
+BirkaOutcome birka_coupled_run(const CsrPtr& kp, const std::vector<CsrPtr>& n_ops, const double* b_any, int m,
+                               const double* c_any, int q, const IrkaSettings& cfg, long long explicit_nnz_cap) {
+  const int dev = kp->device;
+  auto& cx = ctx(dev);
+  DeviceGuard guard(dev);
+  cudaStream_t s = cx.stream;
+  const int64_t n = kp->nrows;
+  const int r = cfg.r;
+  if (kp->ncols != n) throw ConfigError("bilinear system: K must be square");
+  if (m < 1 || q < 1) throw ConfigError("bilinear system: F and C need at least one column");
+  if (int(n_ops.size()) != m) throw ConfigError("bilinear system: one N per input is required");
+  for (const auto& nj : n_ops)
+    if (nj->nrows != n || nj->ncols != n || nj->device != dev) throw ConfigError("bilinear system: every N must be n x n");
+  if (cfg.max_sweeps < 1) throw ConfigError("birka: max_sweeps must be at least 1");
+  if (cfg.max_chain_len < 1) throw ConfigError("birka: max_chain_len must be at least 1");
+  if (r < 1 || int64_t(r) > n) throw ConfigError("birka: reduced order must be in [1, n]");
+  if (r > 32) throw ConfigError("birka: r <= 32 on the GPU path");
+
+  const HostCsr32 kh = download_csr(*kp), kt = transpose_host(kh);
+  std::vector<HostCsr32> nh, nt;
+  for (const auto& nj : n_ops) {
+    nh.push_back(download_csr(*nj));
+    nt.push_back(transpose_host(nh.back()));
+  }
+  std::vector<double> B(size_t(n) * m), Cc(size_t(n) * q);
+  copy_out(B.data(), b_any, B.size(), s);  // any memory -> host
+  copy_out(Cc.data(), c_any, Cc.size(), s);
+  MPG_CUDA(cudaStreamSynchronize(s));
+  DBuf<double> Bd(dev, B.size()), Cd(dev, Cc.size());
+  copy_in(Bd.get(), B.data(), B.size(), s);
+  copy_in(Cd.get(), Cc.data(), Cc.size(), s);
+
+  // birka_default_seed (birka.cpp:41-89)
+  BirkaOutcome out;
+  Mat kr(r, r), fr(r, m), cr(r, q);
+  std::vector<Mat> nr(size_t(m), Mat(r, r));
+  {
+    std::mt19937_64 rng(cfg.seed);
+    std::uniform_real_distribution<double> unit(-1.0, 1.0);
+    std::vector<double> x(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) x[size_t(i)] = unit(rng);
+    double radius = 0.0, xn = 0.0;
+    for (double v : x) xn += v * v;
+    xn = std::sqrt(xn);
+    if (xn > 0.0) {
+      for (double& v : x) v /= xn;
+      std::vector<double> y(static_cast<size_t>(n));
+      for (int it = 0; it < 20; ++it) {
+        for (int64_t i = 0; i < n; ++i) {
+          double acc = 0.0;
+          for (int kk = kh.rp[size_t(i)]; kk < kh.rp[size_t(i) + 1]; ++kk) acc += kh.v[size_t(kk)] * x[size_t(kh.ci[size_t(kk)])];
+          y[size_t(i)] = acc;
+        }
+        double ny = 0.0;
+        for (double v : y) ny += v * v;
+        ny = std::sqrt(ny);
+        if (ny == 0.0) {
+          radius = 0.0;
+          break;
+        }
+        radius = ny;
+        for (int64_t i = 0; i < n; ++i) x[size_t(i)] = y[size_t(i)] / ny;
+      }
+    }
+    if (!(radius > 0.0) || !std::isfinite(radius)) radius = 1.0;
+    for (int i = 0; i < r; ++i) {
+      const double t = r == 1 ? 1.0 : double(i) / (r - 1);
+      kr(i, i) = -radius * std::pow(10.0, -3.0 * (1.0 - t));
+    }
+    for (Mat* mm : {&fr, &cr})
+      for (int j = 0; j < mm->cols; ++j) {
+        double nn = 0.0;
+        for (int i = 0; i < r; ++i) {
+          (*mm)(i, j) = unit(rng);
+          nn += (*mm)(i, j) * (*mm)(i, j);
+        }
+        nn = std::sqrt(nn);
+        if (nn > 0.0)
+          for (int i = 0; i < r; ++i) (*mm)(i, j) /= nn;
+      }
+  }
+  struct Side {
+    ChainPtr chain;
+    CsrPtr prev;
+    bool degraded = false;
+  } sides[2];
+  std::mt19937_64 perturb_rng(cfg.seed ^ 0x9e3779b97f4a7c15ull);
+  std::vector<host::Eig> lambda_prev = host::sorted_eigenvalues(kr);
+  DBuf<double> X(dev, size_t(n) * r), Y(dev, size_t(n) * r), T(dev, size_t(n) * r);
+  for (int z = 1; z <= cfg.max_sweeps && !out.converged; ++z) {
+    host::Spectrum spec;
+    if (!host::real_spectrum(kr, spec)) {
+      std::uniform_real_distribution<double> unit(-1.0, 1.0);
+      Mat nudged = kr;
+      const double scale = 1e-8 * std::max(1.0, host::fro(kr));
+      for (double& v : nudged.a) v += scale * unit(perturb_rng);
+      if (!host::real_spectrum(nudged, spec))
+        throw SolverError("birka: reduced state matrix is not diagonalizable (sweep " + std::to_string(z) +
+                          "), even after perturbation");
+      kr = nudged;
+      lambda_prev = host::sorted_eigenvalues(kr);
+    }
+    const Mat rinv_t = host::transpose(spec.basis_inv);
+    const Mat f2 = host::mul(host::transpose(fr), rinv_t);    // m x r
+    const Mat c2 = host::mul(host::transpose(cr), spec.basis);  // q x r
+    std::vector<std::pair<Mat, const HostCsr32*>> cps[2];
+    for (int j = 0; j < m; ++j) {
+      const Mat n2 = host::mul(host::mul(host::transpose(spec.basis), nr[size_t(j)]), rinv_t);
+      cps[0].push_back({n2, &nh[size_t(j)]});
+      cps[1].push_back({host::transpose(n2), &nt[size_t(j)]});
+    }
+    for (int side = 0; side < 2; ++side) {
+      // right-hand side F f2 / C c2 (n x r), host
+      const std::vector<double>& src = side == 0 ? B : Cc;
+      const Mat& coef = side == 0 ? f2 : c2;
+      const int cols = side == 0 ? m : q;
+      std::vector<double> rhs(size_t(n) * r, 0.0);
+      for (int c = 0; c < r; ++c)
+        for (int t = 0; t < cols; ++t) {
+          const double w = coef(t, c);
+          if (w == 0.0) continue;
+          for (int64_t i = 0; i < n; ++i) rhs[size_t(c) * n + size_t(i)] += src[size_t(t) * n + size_t(i)] * w;
+        }
+      double bn = 0.0;
+      for (double v : rhs) bn += v * v;
+      if (bn == 0.0)
+        throw SolverError(std::string("birka: zero right-hand side on the ") + (side == 0 ? "trial" : "test") +
+                          " side (sweep " + std::to_string(z) + "); input/output maps must be nonzero");
+      int64_t estimate = 0;
+      CsrPtr A = assemble_kron(dev, spec.blocks, side == 0 ? kh : kt, cps[side], estimate);
+      mpg_report_row row{};
+      row.sweep = z;
+      row.point = side + 1;
+      row.kind = MPG_KIND_NONE;
+      row.min_residual = row.matrix_change = row.standard_residual = std::nan("");
+      Side& sd = sides[side];
+      if (cfg.mode != MPG_PRECOND_NONE && !sd.degraded && estimate > explicit_nnz_cap) {
+        sd.degraded = true;
+        out.warnings.push_back(std::string(side == 0 ? "trial" : "test") +
+                               " side continues unpreconditioned: explicit operator assembly needs about " +
+                               std::to_string(estimate) + " entries, above the cap of " +
+                               std::to_string(explicit_nnz_cap) +
+                               "; rerun with a fresh approximate inverse per sweep or without preconditioning");
+      }
+      ChainPtr prec;
+      if (cfg.mode != MPG_PRECOND_NONE && !sd.degraded) {
+        if (cfg.mode == MPG_PRECOND_REUSE_FROZEN && sd.chain) {
+          row.kind = MPG_KIND_REUSED_SAME_MATRIX;
+        } else if (cfg.mode == MPG_PRECOND_FRESH || cfg.mode == MPG_PRECOND_REUSE_FROZEN || !sd.chain || sd.chain->length() + 1 > cfg.max_chain_len) {
+          SpaiOutcome so = spai_or_update(A, nullptr, cfg.spai, false);
+          auto ch = std::make_shared<Chain>();
+          ch->factors.push_back(so.p);
+          sd.chain = ch;
+          row.kind = MPG_KIND_FRESH;
+          row.build_seconds = so.build_seconds;
+        } else {
+          SpaiOutcome so = spai_or_update(A, sd.prev, cfg.spai, false);
+          auto ch = std::make_shared<Chain>(*sd.chain);
+          ch->factors.push_back(so.p);
+          sd.chain = ch;
+          row.kind = MPG_KIND_VERTICAL;
+          row.build_seconds = so.build_seconds;
+          row.min_residual = so.min_residual;
+          row.matrix_change = so.matrix_change;
+        }
+        if (cfg.mode == MPG_PRECOND_REUSE_CHAIN) sd.prev = A;
+        prec = sd.chain;
+        if (A->nrows <= cfg.standard_residual_max_dim) row.standard_residual = std_residual(A, prec);
+      }
+      OpPtr op = op_create(A, nullptr);
+      std::vector<SolveSpec> specs(1);
+      specs[0].sre = 0.0;
+      specs[0].ca = 1.0;
+      specs[0].chain = prec;
+      specs[0].b = rhs.data();
+      specs[0].x = side == 0 ? X.get() : Y.get();
+      const GmresOutcome o = gmres_batch(*op, specs, cfg.gmres)[0];
+      row.solves = 1;
+      row.iterations = o.iterations;
+      row.gmres_seconds = o.solve_seconds;
+      out.rows.push_back(row);
+      if (!o.converged) {
+        char rel[32];
+        std::snprintf(rel, sizeof rel, "%.3e", o.final_residual / std::max(o.rhs_norm, 1e-300));
+        throw SolverError(std::string("birka: gmres did not converge on the ") + (side == 0 ? "trial" : "test") +
+                          " side (sweep " + std::to_string(z) + "; relative residual " + rel + " after " +
+                          std::to_string(o.iterations) + " iterations)");
+      }
+    }
+    orthonormalize(dev, X.get(), n, r);
+    orthonormalize(dev, Y.get(), n, r);
+    const Mat wtv = ts_gram(dev, Y.get(), n, r, X.get(), n, r, n);
+    host::LU lu(wtv);
+    if (!lu.invertible())
+      throw SolverError("birka: projection matrix (test basis^T trial basis) is singular at sweep " + std::to_string(z));
+    for (int j = 0; j < r; ++j) {
+      launch_spmv(*kp, X.get() + size_t(n) * j, T.get() + size_t(n) * j, 1.0, s);
+      count_launch();
+    }
+    kr = lu.solve(ts_gram(dev, Y.get(), n, r, T.get(), n, r, n));
+    for (int jn = 0; jn < m; ++jn) {
+      for (int j = 0; j < r; ++j) {
+        launch_spmv(*n_ops[size_t(jn)], X.get() + size_t(n) * j, T.get() + size_t(n) * j, 1.0, s);
+        count_launch();
+      }
+      nr[size_t(jn)] = lu.solve(ts_gram(dev, Y.get(), n, r, T.get(), n, r, n));
+    }
+    fr = lu.solve(ts_gram(dev, Y.get(), n, r, Bd.get(), n, m, n));
+    cr = ts_gram(dev, X.get(), n, r, Cd.get(), n, q, n);
+    out.sweeps = z;
+    const std::vector<host::Eig> lambda_new = host::sorted_eigenvalues(kr);
+    double num = 0.0, den = 0.0;
+    for (size_t i = 0; i < lambda_new.size(); ++i) {
+      const double dr = lambda_new[i].re - lambda_prev[i].re, di = lambda_new[i].im - lambda_prev[i].im;
+      num += dr * dr + di * di;
+      den += lambda_prev[i].re * lambda_prev[i].re + lambda_prev[i].im * lambda_prev[i].im;
+    }
+    if (std::sqrt(num) / std::max(std::sqrt(den), 1e-300) < cfg.tol) out.converged = true;
+    lambda_prev = lambda_new;
+  }
+  out.kr = kr;
+  out.nr = nr;
+  out.fr = fr;
+  out.cr = cr;
+  out.lambda = lambda_prev;
+  out.v.resize(size_t(n) * r);
+  out.w.resize(size_t(n) * r);
+  MPG_CUDA(cudaMemcpyAsync(out.v.data(), X.get(), out.v.size() * 8, cudaMemcpyDeviceToHost, s));
+  MPG_CUDA(cudaMemcpyAsync(out.w.data(), Y.get(), out.w.size() * 8, cudaMemcpyDeviceToHost, s));
+  MPG_CUDA(cudaStreamSynchronize(s));
+  if (!out.converged)
+    out.warnings.push_back("fixed point left unconverged after " + std::to_string(out.sweeps) + " sweeps");
+  return out;
+}
+
 }  // namespace mpg

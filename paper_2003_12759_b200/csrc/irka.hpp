@@ -130,3 +130,25 @@ AirgaOutcome airga_run(const CsrPtr& m, const CsrPtr& d, const CsrPtr& k, const 
                        const double* c_any, int n_out, const AirgaSettings& cfg);
 
 }  // namespace mpg
+
+namespace mpg {
+
+// birka_reduce with couplings N_1..N_m (proj/src/birka.cpp:139-310): per side
+// one joint n r solve of the Kronecker operator -(Lambda (x) I) - (I (x) K) -
+// sum_j (S_j^T (x) N_j), formed explicitly (kron.cpp:72-131) on the device
+// and solved there; SPAI of that matrix unless it exceeds explicit_nnz_cap
+// (then the side continues unpreconditioned, as the reference does).
+struct BirkaOutcome {
+  host::Mat kr, fr, cr;
+  std::vector<host::Mat> nr;
+  std::vector<host::Eig> lambda;
+  std::vector<double> v, w;
+  int sweeps = 0;
+  bool converged = false;
+  std::vector<mpg_report_row> rows;
+  std::vector<std::string> warnings;
+};
+BirkaOutcome birka_coupled_run(const CsrPtr& k, const std::vector<CsrPtr>& n_ops, const double* b_any, int m,
+                               const double* c_any, int q, const IrkaSettings& cfg, long long explicit_nnz_cap);
+
+}  // namespace mpg

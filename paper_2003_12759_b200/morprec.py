@@ -31,7 +31,7 @@ __all__ = [
     "QbSystem", "QbConfig", "ReducedQb", "qbihomm_reduce", "IoError", "read_matrix_market",
     "read_matrix_market_file", "write_matrix_market", "write_matrix_market_file", "SecondOrderSystem",
     "ReducedSecondOrder", "TransferErrorConfig", "transfer_function_error", "project", "AirgaConfig",
-    "airga_reduce", "update_expansion_points", "h2_norm",
+    "airga_reduce", "update_expansion_points", "h2_norm", "BirkaState", "birka_reduce",
 ]
 
 
@@ -574,6 +574,57 @@ def irka_reduce(op: ShiftedOperator, b, c, cfg: IrkaConfig, mode: int = PrecondM
     rep = ReductionReport(_rows(rows, min(nrows.value, maxrows)), bool(conv.value), r, sweeps.value)
     if not rep.converged:
         rep.warnings.append(f"fixed point left unconverged after {sweeps.value} sweeps")
+    return st, rep
+
+
+@dataclasses.dataclass
+class BirkaState:
+    """Reduced bilinear model x' = K_r x + sum_j N_r[j] x u_j + F_r u, y = C_r^T x (BirkaState, birka.hpp:35-47)."""
+    kr: np.ndarray
+    nr: list
+    fr: np.ndarray
+    cr: np.ndarray
+    lam: np.ndarray
+    v: Optional[np.ndarray]
+    w: Optional[np.ndarray]
+    sweeps: int
+
+
+def birka_reduce(k: SparseMatrix, n_ops: Sequence[SparseMatrix], b, c, cfg: IrkaConfig,
+                 mode: int = PrecondMode.REUSE_CHAIN, want_bases: bool = False):
+    """birka_reduce (birka.cpp:139-310) with couplings N_j: one joint n r GMRES per side and sweep on the
+    device, on the explicitly assembled Kronecker operator (kron.cpp:72-131); returns (BirkaState,
+    ReductionReport) with report.warnings (e.g. a side degraded past cfg.explicit_nnz_cap)."""
+    n = k.shape[0]
+    bm = np.asfortranarray(np.asarray(b, dtype=np.float64).reshape(n, -1))
+    cm = np.asfortranarray(np.asarray(c, dtype=np.float64).reshape(n, -1))
+    m, q, r = bm.shape[1], cm.shape[1], cfg.r
+    if len(n_ops) != m:
+        raise ValueError("birka_reduce: one coupling matrix per input column is required")
+    kr = np.zeros((r, r), order="F")
+    nr = np.zeros(r * r * max(m, 1))
+    fr, cr = np.zeros((r, m), order="F"), np.zeros((r, q), order="F")
+    lre, lim = np.zeros(r), np.zeros(r)
+    v = np.zeros((n, r), order="F") if want_bases else None
+    w = np.zeros((n, r), order="F") if want_bases else None
+    sweeps, conv, nrows = C.c_int(), C.c_int(), C.c_int()
+    maxrows = 2 * max(cfg.max_sweeps, 1) + 4
+    rows = (L.ReportRow * maxrows)()
+    warn = C.c_void_p()
+    hs = (C.c_void_p * max(m, 1))(*[x._h.value for x in n_ops])
+    cc = cfg.c()
+    check(lib.mpg_birka_reduce(k._h, hs, L.ptr(bm), m, L.ptr(cm), q, C.byref(cc), mode, L.ptr(kr), L.ptr(nr),
+                               L.ptr(fr), L.ptr(cr), L.ptr(lre), L.ptr(lim), L.ptr(v) if v is not None else None,
+                               L.ptr(w) if w is not None else None, C.byref(sweeps), C.byref(conv), rows, maxrows,
+                               C.byref(nrows), C.byref(warn)))
+    try:
+        text = C.string_at(warn.value).decode() if warn.value else ""
+    finally:
+        lib.mpg_buffer_free(warn)
+    nrs = [nr[j * r * r:(j + 1) * r * r].reshape((r, r), order="F").copy() for j in range(m)]
+    st = BirkaState(kr, nrs, fr, cr, lre + 1j * lim, v, w, sweeps.value)
+    rep = ReductionReport(_rows(rows, min(nrows.value, maxrows)), bool(conv.value), r, sweeps.value,
+                          [x for x in text.split("\n") if x])
     return st, rep
 
 
