@@ -364,6 +364,37 @@ def run_airga(args, device: int) -> dict:
             "final_points": [round(x, 4) for x in rep.final_points]}
 
 
+def run_birka(args, device: int) -> dict:
+    """BIRKA with couplings on the seeded bilinear toy with two couplings
+    (generator.cpp:141-179), n = 400, r = 3: one joint n r solve per side and sweep on the explicitly
+    assembled Kronecker operator, ReuseChain. Wall time of birka_reduce beside the oracle's coupled BIRKA
+    (one host thread) on the same inputs."""
+    import paper_2003_12759_b200 as mpg
+    import oracle as O
+    from paper_2003_12759_b200 import gen
+    kh, nh, f, c = gen.bilinear_toy_n(400, 2, 4)
+    dev = lambda h: mpg.SparseMatrix.from_csr(h.nrows, h.ncols, h.rowptr, h.colind, h.val, device)
+    k, ns = dev(kh), [dev(x) for x in nh]
+    cfg = mpg.IrkaConfig(r=3, tol=1e-9, max_sweeps=200, seed=4, gmres=mpg.GmresConfig(1e-11, 1000),
+                         explicit_nnz_cap=10**9)
+    mpg.lib.mpg_synchronize(device)
+    t0 = time.perf_counter()
+    st, rep = mpg.birka_reduce(k, ns, f, c, cfg, mpg.PrecondMode.REUSE_CHAIN)
+    mpg.lib.mpg_synchronize(device)
+    wall = time.perf_counter() - t0
+    tot = rep.totals()
+    out = {"wall_s": round(wall, 3), "n": 400, "m": 2, "r": 3, "sweeps": rep.sweeps, "converged": rep.converged,
+           "gmres_iterations": tot["gmres_iterations"], "precond_build_s": round(tot["precond_build_seconds"], 3)}
+    if not args.no_cpu_baseline:
+        ocfg = O.IrkaConfig(r=3, tol=1e-9, max_sweeps=200, seed=4, gmres=O.GmresConfig(1e-11, 1000),
+                            explicit_nnz_cap=10**9)
+        t0 = time.perf_counter()
+        ores = O.birka_reduce(O.Csr.of(kh), [O.Csr.of(x) for x in nh], f, c, ocfg, mode=2)
+        out["oracle_wall_s"] = round(time.perf_counter() - t0, 3)
+        out["oracle_sweeps"] = ores.sweeps
+    return out
+
+
 def run_mmio(args) -> dict:
     """Matrix Market ingestion at the bench size: the C3
     operator written once with the library's writer (shortest round-trip
@@ -486,6 +517,7 @@ def main():
     ap.add_argument("--no-irka", action="store_true", help="skip the full-IRKA wall-time measurement")
     ap.add_argument("--no-qb", action="store_true", help="skip the QB-IHOMM wall-time measurement")
     ap.add_argument("--no-mm", action="store_true", help="skip the Matrix Market ingestion measurement")
+    ap.add_argument("--no-birka", action="store_true", help="skip the coupled-BIRKA measurement")
     ap.add_argument("--no-tf", action="store_true", help="skip the second-order (transfer error, AIRGA) measurements")
     ap.add_argument("--cpu-threads", type=int, default=0, help="host threads of the CPU sample (0: all, <= 16)")
     args = ap.parse_args()
@@ -510,6 +542,8 @@ def main():
         res["transfer_error"] = run_transfer_error(args, local)
     if world == 1 and not args.no_tf:
         res["airga"] = run_airga(args, local)
+    if world == 1 and not args.no_birka:
+        res["birka_coupled"] = run_birka(args, local)
     if world == 1 and not args.no_mm and rank == 0:
         res["matrix_market"] = run_mmio(args)
     if rank == 0:

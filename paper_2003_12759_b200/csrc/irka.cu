@@ -149,26 +149,70 @@ void orthonormalize(int dev, double* X, int64_t n, int r) {
   MPG_CUDA(cudaStreamSynchronize(c.stream));
 }
 
+// Blocks of 32 unit columns, row-major [n][32] (lane = column): one launch per
+// chain factor / operator / residual per block instead of one sync per column.
+__global__ void k_unit_block(double* x, int64_t n, int64_t j0) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n * 32; t += int64_t(gridDim.x) * blockDim.x)
+    x[t] = (t / 32 == j0 + (t & 31)) ? 1.0 : 0.0;
+}
+__global__ void k_spmm32(CsrView a, const double* __restrict__ x, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t row = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; row < a.nrows;
+       row += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    double acc = 0.0;
+    for (int k = a.rowptr[row]; k < a.rowptr[row + 1]; ++k) acc += a.val[k] * x[int64_t(a.colind[k]) * 32 + lane];
+    y[row * 32 + lane] = acc;
+  }
+}
+__global__ void k_resid_block(const double* __restrict__ y, int64_t n, int64_t j0, int valid, double* acc) {
+  double sq = 0.0;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n * 32; t += int64_t(gridDim.x) * blockDim.x) {
+    const int l = int(t & 31);
+    if (l >= valid) continue;
+    const double d = y[t] - ((t / 32 == j0 + l) ? 1.0 : 0.0);
+    sq += d * d;
+  }
+  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  __shared__ double part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) t += part[w];
+    atomicAdd(acc, t);
+  }
+}
+
 double std_residual(const CsrPtr& m, const ChainPtr& ch) {
   // ||I - M P||_F / sqrt(n) (chain.cpp:140-157)
   const int dev = m->device;
   auto& c = ctx(dev);
   const int64_t n = m->nrows;
   if (n == 0) return 0.0;
-  DBuf<double> e(dev, size_t(n)), pe(dev, size_t(n)), ape(dev, size_t(n)), tmp(dev, size_t(n));
-  double sq = 0.0;
-  MPG_CUDA(cudaMemsetAsync(e.get(), 0, size_t(n) * sizeof(double), c.stream));
-  const double one = 1.0, zero = 0.0;
-  for (int64_t j = 0; j < n; ++j) {
-    MPG_CUDA(cudaMemcpyAsync(e.get() + j, &one, sizeof(double), cudaMemcpyHostToDevice, c.stream));
-    launch_chain(*ch, e.get(), pe.get(), tmp.get(), c.stream);
-    launch_spmv(*m, pe.get(), ape.get(), 1.0, c.stream);
-    double aj = 0.0;
-    MPG_CUDA(cudaMemcpyAsync(&aj, ape.get() + j, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-    const double nrm = device_norm2(dev, ape.get(), n, c.stream);  // syncs
-    sq += nrm - aj * aj + (aj - 1.0) * (aj - 1.0);
-    MPG_CUDA(cudaMemcpyAsync(e.get() + j, &zero, sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  DBuf<double> e(dev, size_t(n) * 32), b0(dev, size_t(n) * 32), b1(dev, size_t(n) * 32), acc(dev, 1);
+  MPG_CUDA(cudaMemsetAsync(acc.get(), 0, sizeof(double), c.stream));
+  const int grid = int(std::min<int64_t>((n * 32 + 255) / 256, 148 * 8));
+  const int L = ch->length();
+  for (int64_t j0 = 0; j0 < n; j0 += 32) {
+    k_unit_block<<<grid, 256, 0, c.stream>>>(e.get(), n, j0);
+    MPG_CHECK_LAUNCH();
+    double* bufs[2] = {b0.get(), b1.get()};
+    int cur = 0;
+    k_spmm32<<<grid, 256, 0, c.stream>>>(ch->factors[0]->view(), e.get(), bufs[cur]);
+    MPG_CHECK_LAUNCH();
+    for (int i = 1; i <= L; ++i, cur ^= 1) {
+      k_spmm32<<<grid, 256, 0, c.stream>>>(ch->factors[size_t(i)]->view(), bufs[cur], bufs[cur ^ 1]);
+      MPG_CHECK_LAUNCH();
+    }
+    k_spmm32<<<grid, 256, 0, c.stream>>>(m->view(), bufs[cur], e.get());
+    MPG_CHECK_LAUNCH();
+    k_resid_block<<<grid, 256, 0, c.stream>>>(e.get(), n, j0, int(std::min<int64_t>(32, n - j0)), acc.get());
+    MPG_CHECK_LAUNCH();
+    count_launch(L + 4);
   }
+  double sq = 0.0;
+  MPG_CUDA(cudaMemcpyAsync(&sq, acc.get(), sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  MPG_CUDA(cudaStreamSynchronize(c.stream));
   return std::sqrt(std::max(sq, 0.0)) / std::sqrt(double(n));
 }
 
