@@ -272,11 +272,13 @@ struct BirkaConfig {  // birka.hpp:49-61 (N = 0)
   int max_chain_len = 16;
   index_t standard_residual_max_dim = 5000;
   bool mirror_unstable = false;  // extension
+  index_t explicit_nnz_cap = 200000;  // coupled systems only (joint solves)
 };
 
 struct BirkaState {  // birka.hpp:35-47 with the descriptor E_r, A_r
   int order = 0;
   std::vector<double> kr, fr, cr, er, ar;  // column-major
+  std::vector<std::vector<double>> nr;      // coupled systems: N_r[j], r x r each
   std::vector<double> lambda_re, lambda_im;
   int sweeps = 0;
 };
@@ -285,6 +287,7 @@ struct ReductionReport {  // report.hpp:49-61
   std::vector<mpg_report_row> rows;
   bool converged = false;
   int sweeps = 0;
+  std::string warnings;  // '\n'-separated
 };
 
 // birka_reduce (birka.hpp:78-80) for x' = A x + B u with E x' (E may be null).
@@ -321,6 +324,53 @@ inline std::pair<BirkaState, ReductionReport> birka_reduce(const ShiftedOperator
                         init_shifts ? init_shifts->data() : nullptr, st.kr.data(), st.fr.data(), st.cr.data(),
                         st.er.data(), st.ar.data(), st.lambda_re.data(), st.lambda_im.data(), nullptr, nullptr, &sweeps,
                         &conv, rep.rows.data(), static_cast<int>(rep.rows.size()), &nrows));
+  rep.rows.resize(static_cast<size_t>(std::min<int>(nrows, static_cast<int>(rep.rows.size()))));
+  st.sweeps = rep.sweeps = sweeps;
+  rep.converged = conv != 0;
+  return {std::move(st), std::move(rep)};
+}
+
+// birka_reduce (birka.hpp:78-80) for x' = K x + sum_j N_j x u_j + F u with couplings: joint n r solves
+// per side on the assembled Kronecker operator (mpg_birka_reduce).
+inline std::pair<BirkaState, ReductionReport> birka_reduce(const SparseMatrix& k,
+                                                           const std::vector<const SparseMatrix*>& n_ops,
+                                                           const std::vector<double>& f, int m,
+                                                           const std::vector<double>& c, int q,
+                                                           const BirkaConfig& cfg, PrecondMode mode) {
+  if (static_cast<int>(n_ops.size()) != m) throw std::invalid_argument("birka: one N per input is required");
+  mpg_irka_cfg kc{};
+  kc.r = cfg.r;
+  kc.tol = cfg.tol;
+  kc.max_sweeps = cfg.max_sweeps;
+  kc.seed = cfg.seed;
+  kc.gmres = cfg.gmres.c();
+  kc.spai = cfg.spai.c();
+  kc.max_chain_len = cfg.max_chain_len;
+  kc.explicit_nnz_cap = cfg.explicit_nnz_cap;
+  kc.standard_residual_max_dim = cfg.standard_residual_max_dim;
+  std::vector<const mpg_csr*> hs;
+  for (const SparseMatrix* nj : n_ops) hs.push_back(nj->handle());
+  const size_t r = static_cast<size_t>(cfg.r);
+  BirkaState st;
+  st.order = cfg.r;
+  st.kr.resize(r * r);
+  std::vector<double> nr(r * r * static_cast<size_t>(std::max(m, 1)));
+  st.fr.resize(r * static_cast<size_t>(m));
+  st.cr.resize(r * static_cast<size_t>(q));
+  st.lambda_re.resize(r);
+  st.lambda_im.resize(r);
+  ReductionReport rep;
+  rep.rows.resize(2 * static_cast<size_t>(cfg.max_sweeps) + 4);
+  int sweeps = 0, conv = 0, nrows = 0;
+  char* warn = nullptr;
+  check(mpg_birka_reduce(k.handle(), hs.data(), f.data(), m, c.data(), q, &kc, static_cast<int>(mode), st.kr.data(),
+                         nr.data(), st.fr.data(), st.cr.data(), st.lambda_re.data(), st.lambda_im.data(), nullptr,
+                         nullptr, &sweeps, &conv, rep.rows.data(), static_cast<int>(rep.rows.size()), &nrows, &warn));
+  if (warn) {
+    rep.warnings = warn;
+    mpg_buffer_free(warn);
+  }
+  for (int j = 0; j < m; ++j) st.nr.emplace_back(nr.begin() + j * r * r, nr.begin() + (j + 1) * r * r);
   rep.rows.resize(static_cast<size_t>(std::min<int>(nrows, static_cast<int>(rep.rows.size()))));
   st.sweeps = rep.sweeps = sweeps;
   rep.converged = conv != 0;

@@ -49,5 +49,25 @@ int main() {
     ok = false;  // zero rhs must throw std::invalid_argument
   } catch (const std::invalid_argument&) {
   }
+  // bilinear system with one coupling N = 0.05 I (joint-solve birka_reduce)
+  {
+    const index_t nb = 60;
+    SparseMatrix kb = lap1d(nb);
+    std::vector<index_t> rp, ci;
+    for (index_t i = 0; i <= nb; ++i) rp.push_back(i);
+    for (index_t i = 0; i < nb; ++i) ci.push_back(i);
+    SparseMatrix nm = SparseMatrix::from_csr(nb, nb, rp, ci, std::vector<double>(static_cast<size_t>(nb), 0.05));
+    std::vector<double> fb(static_cast<size_t>(nb)), cb(static_cast<size_t>(nb));
+    for (index_t i = 0; i < nb; ++i) { fb[size_t(i)] = 1.0; cb[size_t(i)] = double(i + 1) / double(nb); }
+    BirkaConfig bc;
+    bc.r = 2;
+    bc.tol = 1e-8;
+    bc.max_sweeps = 100;
+    auto [st, rep] = birka_reduce(kb, {&nm}, fb, 1, cb, 1, bc, PrecondMode::ReuseChain);
+    std::printf("birka sweeps %d conv %d lam %.6f %.6f\n", st.sweeps, int(rep.converged), st.lambda_re[0],
+                st.lambda_re[1]);
+    ok = ok && rep.converged && st.nr.size() == 1 && st.lambda_re[0] < 0 && st.lambda_re[1] < 0 &&
+         rep.rows.size() == 2 * static_cast<size_t>(st.sweeps);
+  }
   return ok ? 0 : 1;
 }
