@@ -102,7 +102,7 @@ def _irka_worker(rank, world, port, out):
     s = gen.config1(40)
     dev = lambda h: mpg.SparseMatrix.from_csr(h.nrows, h.ncols, h.rowptr, h.colind, h.val)
     op = mpg.ShiftedOperator(dev(s.a), dev(s.e_csr()))
-    cfg = mpg.IrkaConfig(r=s.r, tol=1e-6, max_sweeps=50, seed=1, gmres=mpg.GmresConfig(1e-10, 1000))
+    cfg = mpg.IrkaConfig(r=s.r, tol=1e-8, max_sweeps=100, seed=1, gmres=mpg.GmresConfig(1e-10, 1000))
     st, rep = mdist.irka_reduce_sharded(op, s.b, s.c, cfg, mpg.PrecondMode.REUSE_FROZEN, init_shifts=s.shifts)
     ref = None
     if rank == 0:
@@ -120,6 +120,6 @@ def test_sharded_irka_two_ranks_match_single_rank():
     assert conv0 and conv1 and sw0 == sw1
     assert np.array_equal(lam0, lam1)  # every rank forms the same projection
     lam_ref, sw_ref = ref
-    assert abs(sw0 - sw_ref) <= 1
+    assert abs(sw0 - sw_ref) <= max(2, sw_ref // 10)  # the summation order of the shared projection differs
     assert np.max(np.abs(lam0 - lam_ref) / np.abs(lam_ref)) <= 1e-6
     assert rows0 > 0 and rows1 > 0  # both ranks solved a share
