@@ -249,6 +249,55 @@ struct SlotPrecond {
   int width = 0;
 };
 
+// birka_default_seed (birka.cpp:41-89): 20 power iterations of K on the device for the spectral radius
+// (skipped when init_shifts are given), then fr and cr from the same mt19937_64 stream.
+void default_seed(const DevCsr& a, const IrkaSettings& cfg, Mat& kr, Mat& fr, Mat& cr, cudaStream_t s) {
+  const int dev = a.device;
+  const int64_t n = a.nrows;
+  const int r = cfg.r;
+  std::mt19937_64 rng(cfg.seed);
+  std::uniform_real_distribution<double> unit(-1.0, 1.0);
+  std::vector<double> x(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) x[size_t(i)] = unit(rng);
+  if (cfg.init_shifts.empty()) {
+    double radius = 0.0, xn = 0.0;
+    for (double v : x) xn += v * v;
+    xn = std::sqrt(xn);
+    if (xn > 0.0) {
+      for (double& v : x) v /= xn;
+      DBuf<double> dx(dev, size_t(n)), dy(dev, size_t(n));
+      copy_in(dx.get(), x.data(), size_t(n), s);
+      for (int it = 0; it < 20; ++it) {
+        launch_spmv(a, dx.get(), dy.get(), 1.0, s);
+        const double ny = std::sqrt(device_norm2(dev, dy.get(), n, s));
+        if (ny == 0.0) { radius = 0.0; break; }
+        radius = ny;
+        std::vector<double> hy(static_cast<size_t>(n));
+        MPG_CUDA(cudaMemcpyAsync(hy.data(), dy.get(), size_t(n) * 8, cudaMemcpyDeviceToHost, s));
+        MPG_CUDA(cudaStreamSynchronize(s));
+        for (double& v : hy) v /= ny;
+        copy_in(dx.get(), hy.data(), size_t(n), s);
+      }
+    }
+    if (!(radius > 0.0) || !std::isfinite(radius)) radius = 1.0;
+    for (int i = 0; i < r; ++i) {
+      const double t = r == 1 ? 1.0 : double(i) / (r - 1);
+      kr(i, i) = -radius * std::pow(10.0, -3.0 * (1.0 - t));
+    }
+  } else {
+    if (int(cfg.init_shifts.size()) != r) throw ConfigError("irka: init_shifts must have r entries");
+    for (int i = 0; i < r; ++i) kr(i, i) = -cfg.init_shifts[size_t(i)];
+  }
+  for (Mat* mm : {&fr, &cr})
+    for (int j = 0; j < mm->cols; ++j) {
+      double nn = 0.0;
+      for (int i = 0; i < r; ++i) { (*mm)(i, j) = unit(rng); nn += (*mm)(i, j) * (*mm)(i, j); }
+      nn = std::sqrt(nn);
+      if (nn > 0.0)
+        for (int i = 0; i < r; ++i) (*mm)(i, j) /= nn;
+    }
+}
+
 }  // namespace
 
 IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const double* c_any, int q, const IrkaSettings& cfg,
@@ -271,51 +320,8 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
   copy_in(B.get(), b_any, size_t(n) * m, s);
   copy_in(C.get(), c_any, size_t(n) * q, s);
 
-  // ---- initial state (birka_default_seed, birka.cpp:41-89) ----
   Mat kr(r, r), fr(r, m), cr(r, q);
-  {
-    std::mt19937_64 rng(cfg.seed);
-    std::uniform_real_distribution<double> unit(-1.0, 1.0);
-    std::vector<double> x(static_cast<size_t>(n));
-    for (int64_t i = 0; i < n; ++i) x[size_t(i)] = unit(rng);
-    if (cfg.init_shifts.empty()) {
-      double radius = 0.0, xn = 0.0;
-      for (double v : x) xn += v * v;
-      xn = std::sqrt(xn);
-      if (xn > 0.0) {
-        for (double& v : x) v /= xn;
-        DBuf<double> dx(dev, size_t(n)), dy(dev, size_t(n));
-        copy_in(dx.get(), x.data(), size_t(n), s);
-        for (int it = 0; it < 20; ++it) {
-          launch_spmv(*op.a, dx.get(), dy.get(), 1.0, s);
-          const double ny = std::sqrt(device_norm2(dev, dy.get(), n, s));
-          if (ny == 0.0) { radius = 0.0; break; }
-          radius = ny;
-          std::vector<double> hy(static_cast<size_t>(n));
-          MPG_CUDA(cudaMemcpyAsync(hy.data(), dy.get(), size_t(n) * 8, cudaMemcpyDeviceToHost, s));
-          MPG_CUDA(cudaStreamSynchronize(s));
-          for (double& v : hy) v /= ny;
-          copy_in(dx.get(), hy.data(), size_t(n), s);
-        }
-      }
-      if (!(radius > 0.0) || !std::isfinite(radius)) radius = 1.0;
-      for (int i = 0; i < r; ++i) {
-        const double t = r == 1 ? 1.0 : double(i) / (r - 1);
-        kr(i, i) = -radius * std::pow(10.0, -3.0 * (1.0 - t));
-      }
-    } else {
-      if (int(cfg.init_shifts.size()) != r) throw ConfigError("irka: init_shifts must have r entries");
-      for (int i = 0; i < r; ++i) kr(i, i) = -cfg.init_shifts[size_t(i)];
-    }
-    for (Mat* mm : {&fr, &cr})
-      for (int j = 0; j < mm->cols; ++j) {
-        double nn = 0.0;
-        for (int i = 0; i < r; ++i) { (*mm)(i, j) = unit(rng); nn += (*mm)(i, j) * (*mm)(i, j); }
-        nn = std::sqrt(nn);
-        if (nn > 0.0)
-          for (int i = 0; i < r; ++i) (*mm)(i, j) /= nn;
-      }
-  }
+  default_seed(*op.a, cfg, kr, fr, cr, s);
 
   IrkaResult res;
   res.reduced_order = r;
@@ -1574,55 +1580,10 @@ BirkaOutcome birka_coupled_run(const CsrPtr& kp, const std::vector<CsrPtr>& n_op
   copy_in(Bd.get(), B.data(), B.size(), s);
   copy_in(Cd.get(), Cc.data(), Cc.size(), s);
 
-  // birka_default_seed (birka.cpp:41-89)
   BirkaOutcome out;
   Mat kr(r, r), fr(r, m), cr(r, q);
   std::vector<Mat> nr(size_t(m), Mat(r, r));
-  {
-    std::mt19937_64 rng(cfg.seed);
-    std::uniform_real_distribution<double> unit(-1.0, 1.0);
-    std::vector<double> x(static_cast<size_t>(n));
-    for (int64_t i = 0; i < n; ++i) x[size_t(i)] = unit(rng);
-    double radius = 0.0, xn = 0.0;
-    for (double v : x) xn += v * v;
-    xn = std::sqrt(xn);
-    if (xn > 0.0) {
-      for (double& v : x) v /= xn;
-      std::vector<double> y(static_cast<size_t>(n));
-      for (int it = 0; it < 20; ++it) {
-        for (int64_t i = 0; i < n; ++i) {
-          double acc = 0.0;
-          for (int kk = kh.rp[size_t(i)]; kk < kh.rp[size_t(i) + 1]; ++kk) acc += kh.v[size_t(kk)] * x[size_t(kh.ci[size_t(kk)])];
-          y[size_t(i)] = acc;
-        }
-        double ny = 0.0;
-        for (double v : y) ny += v * v;
-        ny = std::sqrt(ny);
-        if (ny == 0.0) {
-          radius = 0.0;
-          break;
-        }
-        radius = ny;
-        for (int64_t i = 0; i < n; ++i) x[size_t(i)] = y[size_t(i)] / ny;
-      }
-    }
-    if (!(radius > 0.0) || !std::isfinite(radius)) radius = 1.0;
-    for (int i = 0; i < r; ++i) {
-      const double t = r == 1 ? 1.0 : double(i) / (r - 1);
-      kr(i, i) = -radius * std::pow(10.0, -3.0 * (1.0 - t));
-    }
-    for (Mat* mm : {&fr, &cr})
-      for (int j = 0; j < mm->cols; ++j) {
-        double nn = 0.0;
-        for (int i = 0; i < r; ++i) {
-          (*mm)(i, j) = unit(rng);
-          nn += (*mm)(i, j) * (*mm)(i, j);
-        }
-        nn = std::sqrt(nn);
-        if (nn > 0.0)
-          for (int i = 0; i < r; ++i) (*mm)(i, j) /= nn;
-      }
-  }
+  default_seed(*kp, cfg, kr, fr, cr, s);
   struct Side {
     ChainPtr chain;
     CsrPtr prev;
