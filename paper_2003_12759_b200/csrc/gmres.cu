@@ -1413,11 +1413,11 @@ __device__ __forceinline__ void gx_producer(GmSolve* S, int ns, int TC, int stag
 // CF chunks of a tile are processed together (their load -> row sum -> butterfly
 // chains interleave); each lane then holds NGC = GX_NG / CF groups per chunk, so
 // CF = 1 serves k + 2 <= 384, CF = 2 <= 192, CF = 4 <= 96, CF = 8 <= 32.
-template <int CF, bool PROJ>
+template <int CF, bool PROJ, int NGT = GX_NG>
 __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, int stage_bytes, int NS, long long a,
                                             long long b, uint32_t ring, uint64_t* full, uint64_t* empty, double* red2,
                                             double* red3, UpdSel us) {
-  constexpr int NGC = GX_NG / CF;
+  constexpr int NGC = NGT / CF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int rp = warp;  // row pair
   const int slot = blockIdx.x;
@@ -1600,9 +1600,28 @@ __global__ void __launch_bounds__(GX_THREADS, 1) k_gs_tmx(GmSolve* S, int ns, in
   else
     switch (CF) {
       case 8: gx_consumer<8, PROJ>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
-      case 4: gx_consumer<4, PROJ>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
-      case 2: gx_consumer<2, PROJ>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
-      default: gx_consumer<1, PROJ>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us); break;
+      case 4:
+        if (nvmax <= 64)
+          gx_consumer<4, PROJ, 8>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+        else
+          gx_consumer<4, PROJ>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+        break;
+      case 2:
+        if (nvmax <= 128)  // groups past k + 2 cost issue slots, not bytes: size the register tile to k + 2
+          gx_consumer<2, PROJ, 8>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+        else if (nvmax <= 160)
+          gx_consumer<2, PROJ, 10>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+        else
+          gx_consumer<2, PROJ>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+        break;
+      default:
+        if (nvmax <= 256)
+          gx_consumer<1, PROJ, 8>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+        else if (nvmax <= 320)
+          gx_consumer<1, PROJ, 10>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+        else
+          gx_consumer<1, PROJ>(S, ns, G, TC, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+        break;
     }
 }
 
