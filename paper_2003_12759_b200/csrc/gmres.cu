@@ -1152,7 +1152,7 @@ struct GtProducer {
   }
 };
 
-template <int TC>
+template <int TC, int NI = GT_NI>
 __device__ __forceinline__ void gt_body(GmSolve* S, int ns, int G, int stage_bytes, int NS, long long a, long long b,
                                         char* ring, uint64_t* full, double* red, double* red2, double* red3, UpdSel us) {
   constexpr int WPC = GT_CWARPS / TC;  // warps per chunk
@@ -1169,7 +1169,7 @@ __device__ __forceinline__ void gt_body(GmSolve* S, int ns, int G, int stage_byt
   }
   GtCursor cu;
   cu.us = us;
-  double coef[GT_NI], acc[GT_NI];
+  double coef[NI], acc[NI];
   double wsq = 0.0;
   double* w = nullptr;
   GmSolve* st = nullptr;
@@ -1190,7 +1190,7 @@ __device__ __forceinline__ void gt_body(GmSolve* S, int ns, int G, int stage_byt
       w = st->V[nj];
       woff = ((nj >> 6) * TC + cc) * 1024 + (nj & 63) * 16 + r;
 #pragma unroll
-      for (int i = 0; i < GT_NI; ++i) {
+      for (int i = 0; i < NI; ++i) {
         const int j = i * CPI + 2 * wq + par;
         coef[i] = j < nj ? st->scale[j] * st->h[j] : 0.0;
         acc[i] = 0.0;
@@ -1201,16 +1201,16 @@ __device__ __forceinline__ void gt_body(GmSolve* S, int ns, int G, int stage_byt
     const bool ccv = c0 + cc < nchunks;
     mbar_wait(full + stg, phase);
     const double* T = reinterpret_cast<const double*>(ring + size_t(stg) * size_t(stage_bytes)) + tbase;
-    double v[GT_NI];
+    double v[NI];
 #pragma unroll
-    for (int i = 0; i < GT_NI; ++i) {
+    for (int i = 0; i < NI; ++i) {
       const int j = i * CPI + 2 * wq + par;
       v[i] = (j < nj && ccv) ? T[(i / SPP) * TC * 1024 + (i % SPP) * CPI * 16] : 0.0;
     }
     const double wpre = ccv ? T[woff - tbase] : 0.0;
     double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-    for (int i = 0; i < GT_NI; ++i) s4[i & 3] = fma(coef[i], v[i], s4[i & 3]);
+    for (int i = 0; i < NI; ++i) s4[i & 3] = fma(coef[i], v[i], s4[i & 3]);
     double s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
     s += __shfl_xor_sync(0xffffffffu, s, 16);
     double* rd = red + (u & 1) * (GT_CWARPS * 16);
@@ -1239,10 +1239,10 @@ __device__ __forceinline__ void gt_body(GmSolve* S, int ns, int G, int stage_byt
       wsq = fma(wn, wn, wsq);
     }
 #pragma unroll
-    for (int i = 0; i < GT_NI; ++i) acc[i] = fma(v[i], wn, acc[i]);
+    for (int i = 0; i < NI; ++i) acc[i] = fma(v[i], wn, acc[i]);
     if (g + 1 == seg_end) {  // flush this solve's partials
 #pragma unroll
-      for (int i = 0; i < GT_NI; ++i) {
+      for (int i = 0; i < NI; ++i) {
         double x = acc[i];
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -1310,13 +1310,26 @@ __global__ void __launch_bounds__(GT_THREADS, 1) k_gs_tma(GmSolve* S, int ns, in
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  // slot steps in use: ceil((k + 1) / CPI) in (6, 12]; a register tile of 8 / 10 / 12 slots avoids
+  // issuing the empty ones (the same sizing as k_gs_tmx)
+  const int used = (njmax + 2 * (GT_CWARPS / TC) - 1) / (2 * (GT_CWARPS / TC));
+#define MPG_GT_CASE(T)                                                                              \
+  case T:                                                                                           \
+    if (used <= 8)                                                                                  \
+      gt_body<T, 8>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3, us);              \
+    else if (used <= 10)                                                                            \
+      gt_body<T, 10>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3, us);             \
+    else                                                                                            \
+      gt_body<T>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3, us);                 \
+    break;
   switch (TC) {
-    case 16: gt_body<16>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3, us); break;
-    case 8: gt_body<8>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3, us); break;
-    case 4: gt_body<4>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3, us); break;
-    case 2: gt_body<2>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3, us); break;
+    MPG_GT_CASE(16)
+    MPG_GT_CASE(8)
+    MPG_GT_CASE(4)
+    MPG_GT_CASE(2)
     default: gt_body<1>(S, ns, G, stage_bytes, NS, a, b, ring, full, red, red2, red3, us); break;
   }
+#undef MPG_GT_CASE
 }
 
 // ---- update + probe without per-tile barriers (default for k + 2 <= GX_MAXV) -----
