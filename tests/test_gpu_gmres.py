@@ -184,3 +184,24 @@ def test_unfused_gram_schmidt_path_beyond_2047_max_iter(mpg, orc, gen):
     assert g.report.converged and ro.converged
     assert abs(g.report.iterations - ro.iterations) <= max(3, 0.03 * ro.iterations)
     assert rel(g.x, xo) <= 1e-6
+
+
+@pytest.mark.parametrize("env", [{"MPG_GS_UPD": "reg"}, {"MPG_GS_UPD": "tma"}, {"MPG_GS_UPD": "tmx"},
+                                 {"MPG_GS_SPLIT": "28"}, {"MPG_GS_LOW": "0"}, {"MPG_GS_DOT": "reg"},
+                                 {"MPG_GS_DOT_SPLIT": "64"}])
+def test_gram_schmidt_kernel_variants_agree(mpg, gen, monkeypatch, env):
+    """Every update / projection kernel choice (register-tiled, 1-D bulk TMA, swizzled tensor TMA with each
+    register-tile size, and the split points between them) gives the default run's answer on a 490-iteration
+    solve that walks k + 1 through all of their ranges."""
+    n = 700
+    d = 1.0 + np.arange(n) ** 1.5
+    h = gen.from_triplets(n, n, np.arange(n), np.arange(n), d)
+    b = gen.random_dense(n, 1, 5)[:, 0]
+    cfg = mpg.GmresConfig(rel_tol=1e-10, max_iter=1000)
+    base = mpg.gmres_right_preconditioned(_m(mpg, h), None, b, cfg)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = mpg.gmres_right_preconditioned(_m(mpg, h), None, b, cfg)
+    assert g.report.converged and abs(g.report.iterations - base.report.iterations) <= 1
+    assert rel(g.x, base.x) <= 1e-8
+    assert np.linalg.norm(d * g.x - b) <= 1e-10 * np.linalg.norm(b)
