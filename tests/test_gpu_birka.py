@@ -88,3 +88,14 @@ def test_coupled_input_validation(mpg, gen):
         mpg.birka_reduce(k, [_m(mpg, nh[0])], f, c, cfg)
     with pytest.raises(mpg.ConfigError):
         mpg.birka_reduce(k, [_m(mpg, x) for x in nh], f, c, mpg.IrkaConfig(r=7))
+
+
+def test_coupled_frozen_preconditioner(mpg, orc, gen):
+    """REUSE_FROZEN (extension): one SPAI per side at the first sweep, applied unchanged afterwards; the fixed
+    point is the oracle's."""
+    kh, nh, f, c, st, rep, ores = _both(mpg, orc, gen, 60, 3, 9, 3, 3)
+    assert rep.converged and ores.converged
+    kinds = [r.kind for r in rep.rows]
+    assert kinds[:2] == ["fresh", "fresh"] and all(k == "reused_same_matrix" for k in kinds[2:])
+    lam, lamo = np.sort_complex(st.lam), np.sort_complex(ores.lam)
+    assert np.linalg.norm(lam - lamo) <= 1e-6 * np.linalg.norm(lamo)
