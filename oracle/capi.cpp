@@ -223,7 +223,7 @@ int orc_gmres_csr(const Csr* m, const orc_chain* c, long long n, const double* b
 int orc_gmres_kron(const double* lambda, int r, const Csr* a, const Csr* e, const orc_chain* c, const double* b,
                    double* x, const orc_gmres_cfg* cfg, orc_gmres_report* rep, double* history) {
   return guard([&] {
-    KronOp op{dense_from(lambda, r, r), a, e};
+    KronOp op{dense_from(lambda, r, r), a, e, {}};
     const LinearOp aop = [&op](const Vec& in, Vec& out) { op.apply(in, out); };
     const long long n = a->nrows * r;
     GmresResult res = gmres_right_preconditioned(aop, c ? c->chain.as_operator() : identity_operator(),
@@ -234,7 +234,7 @@ int orc_gmres_kron(const double* lambda, int r, const Csr* a, const Csr* e, cons
 }
 int orc_kron_apply(const double* lambda, int r, const Csr* a, const Csr* e, const double* x, double* y) {
   return guard([&] {
-    KronOp op{dense_from(lambda, r, r), a, e};
+    KronOp op{dense_from(lambda, r, r), a, e, {}};
     Vec out;
     op.apply(Vec(x, x + a->nrows * r), out);
     std::memcpy(y, out.data(), out.size() * sizeof(double));
@@ -242,7 +242,7 @@ int orc_kron_apply(const double* lambda, int r, const Csr* a, const Csr* e, cons
 }
 int orc_kron_assemble(const double* lambda, int r, const Csr* a, const Csr* e, long long cap, Csr** out) {
   return guard([&] {
-    KronOp op{dense_from(lambda, r, r), a, e};
+    KronOp op{dense_from(lambda, r, r), a, e, {}};
     *out = new Csr(assemble_explicit(op, cap));
   });
 }
