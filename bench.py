@@ -239,8 +239,7 @@ def run_ours(args, rank: int, world: int, device: int):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded generator, DESIGN.md §4; random-init equivalents of the paper's unavailable matrices)",
-        "config": {"workload": f"C3 FEM Q1 {args.nodes}^3 nodes (n={n}), r={args.r} shifts x primal+dual = "
-                               f"{nsolves} GMRES solves/step, tol {args.tol}, SPAI built once at sigma_1 and reused",
+        "config": {"workload": workload_name(args, n, nsolves),
                    "n": n, "nnz_A": A.nnz(), "nnz_E": E.nnz(), "shifts": shifts, "solves_per_step": nsolves,
                    "gmres_iterations": iters, "max_rel_residual": worst, "precond_build_s": round(tbuild, 3),
                    "l2": "inputs larger than L2 (A+E 631 MB, Krylov bases GBs)", "parallelism": f"shift-sharded x{world} (A, E replicated per GPU; rank q solves the shifts x (1 + 0.1 q); no collective in the step)"},
@@ -451,7 +450,13 @@ def _batch_host(mpg, L, op, sig, rhs_host, x_host, chains, trs, cfg):
     return [reps[i] for i in range(k)]
 
 
-def cpu_sample(args) -> dict:
+def workload_name(args, n: int, nsolves: int) -> str:
+    """The workload string both arms print (the reference arm times the same workload on the host)."""
+    return (f"C3 FEM Q1 {args.nodes}^3 nodes (n={n}), r={args.r} shifts x primal+dual = {nsolves} GMRES "
+            f"solves/step, tol {args.tol}, SPAI built once at sigma_1 and reused")
+
+
+def cpu_sample(args, iters: int = 0, state: dict | None = None) -> dict:
     """The oracle (C++ restatement of the reference path) on a bounded sample of
     the same workload: every host thread (up to the 16 solves of a step) runs
     `its` GMRES iterations of its own C3 solve concurrently (the independent
@@ -461,11 +466,14 @@ def cpu_sample(args) -> dict:
     import concurrent.futures as cf
     import oracle as O
     from paper_2003_12759_b200 import gen
-    s = gen.config3(args.nodes)
-    a, e = O.Csr.of(s.a), O.Csr.of(s.e)
-    sigma0 = float(s.shifts[0])
-    m = O.kron_assemble(O.shifted(sigma0), a, e, cap=10 ** 12)
-    its = args.cpu_iters
+    state = {} if state is None else state
+    if "s" not in state:  # the generated system is reused across the samples of one run
+        s = gen.config3(args.nodes)
+        a, e = O.Csr.of(s.a), O.Csr.of(s.e)
+        m = O.kron_assemble(O.shifted(float(s.shifts[0])), a, e, cap=10 ** 12)
+        state.update(s=s, a=a, e=e, m=m)
+    s, a, e, m = state["s"], state["a"], state["e"], state["m"]
+    its = iters or args.cpu_iters
     threads = max(1, min(os.cpu_count() or 1, 16, args.cpu_threads or 16))
     shifts = [float(x) for x in s.shifts]
 
@@ -491,13 +499,30 @@ def cpu_sample(args) -> dict:
 
 
 def run_reference(args, rank: int, world: int) -> None:
+    """`--impl reference`: rank 0 alone times the oracle port on the host cores.
+    Each of the W + K steps is one bounded sample (`cpu_sample`); the iterations
+    per sample shrink with K + W so the run stays within a few minutes, and the
+    value is the median rate of the K timed samples."""
     if rank != 0:
         return
-    cpu = cpu_sample(args)
+    n = (args.nodes) ** 3
+    nsolves = 2 * args.r
+    total = args.steps + args.warmup
+    per = max(8, min(args.cpu_iters, (6 * args.cpu_iters) // max(1, total)))
+    state = {}
+    samples = []
+    for i in range(total):
+        cpu = cpu_sample(args, iters=per, state=state)
+        if i >= args.warmup:
+            samples.append(cpu)
+    samples.sort(key=lambda c: c["value"])
+    cpu = dict(samples[len(samples) // 2])
+    cpu["sample"] += f"; median of {len(samples)} timed samples after {args.warmup} warm-up samples"
     line = {"metric": METRIC, "value": round(cpu["value"], 6), "unit": "solves/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(16 / cpu["value"] * 1e3, 1),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C3 FEM Q1 {args.nodes}^3 nodes, 16 shifted solves per step (CPU oracle sample)"},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(nsolves / cpu["value"] * 1e3, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, DESIGN.md §4)",
+            "config": {"workload": workload_name(args, n, nsolves), "n": n, "solves_per_step": nsolves},
             "impl": "reference", "cpu_baseline": cpu,
             "e2e": {"value": round(cpu["value"], 6), "unit": "solves/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
