@@ -24,3 +24,17 @@ def test_reference_arm_line():
     assert d["e2e"] == {"value": d["value"], "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert d["config"]["workload"].startswith("C3 FEM Q1 16^3 nodes (n=4096), r=8")
     assert "median of 2 timed samples" in d["cpu_baseline"]["sample"]
+
+
+def test_reference_arm_under_torchrun_prints_one_line():
+    """N = 2 launch (gloo on CPU): rank 0 alone runs and prints; rank 1 exits 0 without work."""
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29571", os.path.join(ROOT, "bench.py"),
+                          "--impl", "reference", "--gpus", "2", "--nodes", "12", "--steps", "1", "--warmup", "1",
+                          "--ref-iters", "20", "--cpu-iters", "10"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
