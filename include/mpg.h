@@ -282,7 +282,7 @@ int mpg_qbihomm_reduce(const mpg_op* op, const mpg_csr* n_op, int64_t h_nnz, con
                        double* basis, double* red_d, double* red_k, double* red_n, double* red_h, double* red_f,
                        double* red_c, mpg_report_row* rows, int max_rows, int* nrows);
 
-/* ---- host-side synthetic inputs (gen/generators.cpp) ---------------------- */
+/* ---- host CSR / system structs (Matrix Market IO, triplet ingestion) -------- */
 typedef struct {
   int64_t nrows, ncols, nnz;
   int64_t* rowptr;
@@ -301,28 +301,12 @@ typedef struct {
   double* shifts; /* r initial shifts */
 } mpg_host_system;
 
-const char* mpg_gen_last_error(void);
 void mpg_host_csr_free(mpg_host_csr* m);
-void mpg_host_system_free(mpg_host_system* s);
-int mpg_gen_random_dense(int64_t r, int64_t c, uint64_t seed, double* out);
-int mpg_gen_random_sparse(int64_t r, int64_t c, double density, uint64_t seed, double diag_shift, mpg_host_csr** out);
-int mpg_gen_from_triplets(int64_t nr, int64_t nc, int64_t nnz, const int64_t* ri, const int64_t* ci, const double* v,
-                          mpg_host_csr** out);
-int mpg_gen_bilinear_toy(int64_t n, int64_t m, uint64_t seed, mpg_host_csr** k_out, double* f, double* c);
-/* ... with the couplings N_1..N_m (n_out: m pointers). */
-int mpg_gen_bilinear_toy_n(int64_t n, int64_t m, uint64_t seed, mpg_host_csr** k_out, mpg_host_csr** n_out, double* f,
-                           double* c);
-/* generate_disc_brake_like (proj/src/generator.cpp:37-139): M and K = K_E + K_R + omega^2 K_G; D = alpha M + beta K
- * and F = C = e_1 are formed by the caller. */
-int mpg_gen_disc_brake(int64_t n, double omega, uint64_t seed, mpg_host_csr** m_out, mpg_host_csr** k_out);
-/* generate_qb_toy (proj/src/generator.cpp:181-207): D, K, N (n x n), H (n x n^2, column b n + c); F = C = e_1. */
-int mpg_gen_qb_toy(int64_t n, uint64_t seed, mpg_host_csr** d, mpg_host_csr** k, mpg_host_csr** n_op,
-                   mpg_host_csr** h);
-int mpg_gen_grid2d(int64_t N, uint64_t seed, mpg_host_system** out);
-int mpg_gen_convdiff3d(int64_t M, uint64_t seed, mpg_host_system** out);
-int mpg_gen_fem3d(int64_t N, uint64_t seed, int mimo, mpg_host_system** out);
-int mpg_gen_zipf(int64_t n, uint64_t seed, int64_t min_len, int64_t max_len, double expo, int nshifts,
-                 mpg_host_system** out);
+/* SparseMatrix::from_triplets (proj/src/sparse.cpp:80-115): sorted row-major,
+ * duplicates summed, exact-zero sums kept; out-of-range indices are
+ * MPG_ERR_INVALID. The result is freed with mpg_host_csr_free. */
+int mpg_host_csr_from_triplets(int64_t nr, int64_t nc, int64_t nnz, const int64_t* ri, const int64_t* ci,
+                               const double* v, mpg_host_csr** out);
 
 /* ---- transfer_function_error (proj/src/airga.cpp:386-447) ---------------------
  * Relative error ||H(s) - H_r(s)||_F / ||H(s)||_F on a grid for the

@@ -56,7 +56,7 @@ class IrkaCfg(C.Structure):
     _fields_ = [("r", C.c_int), ("tol", C.c_double), ("max_sweeps", C.c_int), ("decoupled", C.c_int),
                 ("seed", C.c_ulonglong), ("gmres", GmresCfg), ("spai", SpaiCfg), ("max_chain_len", C.c_int),
                 ("explicit_nnz_cap", C.c_longlong), ("standard_residual_max_dim", C.c_longlong),
-                ("mirror_unstable", C.c_int)]
+                ("mirror_unstable", C.c_int), ("unit_threads", C.c_int)]
 
 
 class ReportRow(C.Structure):
@@ -480,11 +480,12 @@ class IrkaConfig:
     standard_residual_max_dim: int = 5000
     decoupled: bool = False
     mirror_unstable: bool = False
+    unit_threads: int = 1
 
     def c(self):
         return IrkaCfg(self.r, self.tol, self.max_sweeps, int(self.decoupled), self.seed, self.gmres.c(),
                        self.spai.c(), self.max_chain_len, self.explicit_nnz_cap, self.standard_residual_max_dim,
-                       int(self.mirror_unstable))
+                       int(self.mirror_unstable), int(self.unit_threads))
 
 
 @dataclasses.dataclass

@@ -52,6 +52,7 @@ typedef struct {
   int r; double tol; int max_sweeps; int decoupled; unsigned long long seed;
   orc_gmres_cfg gmres; orc_spai_cfg spai; int max_chain_len; long long explicit_nnz_cap, standard_residual_max_dim;
   int mirror_unstable;
+  int unit_threads;
 } orc_irka_cfg;
 typedef struct {
   int sweep, point, kind, solves; long long iterations;
@@ -310,6 +311,7 @@ int orc_irka_reduce(const Csr* a, const Csr* e, const double* b, int m, const do
     ic.explicit_nnz_cap = cfg->explicit_nnz_cap; ic.standard_residual_max_dim = cfg->standard_residual_max_dim;
     ic.decoupled = cfg->decoupled != 0;
     ic.mirror_unstable = cfg->mirror_unstable != 0;
+    ic.unit_threads = std::max(1, cfg->unit_threads);
     IrkaState init;
     const IrkaState* initp = nullptr;
     if (init_kr) {

@@ -4,6 +4,11 @@
 // this is the reference loop exactly), and proj/src/bench.cpp:159-249 (the
 // shift-sweep benchmark) for the first-order pencil sigma E - A.
 #include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <thread>
 #include <cmath>
 #include <random>
 #include <string>
@@ -110,6 +115,8 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
   report.reduced_order = int(r);
   std::vector<SidePrecond> sides(2);
   std::vector<std::vector<SidePrecond>> unit_sides(2, std::vector<SidePrecond>(static_cast<size_t>(r)));
+  std::map<std::pair<int, index_t>, PrecondChain> frozen;  // ReuseFrozen: (side, unit width) -> base
+  const bool verbose = std::getenv("ORC_IRKA_VERBOSE") != nullptr;
   std::mt19937_64 perturb_rng(cfg.seed ^ 0x9e3779b97f4a7c15ull);
   std::vector<Complex> lambda_prev = sorted_eigenvalues(state.kr);
   bool converged = false;
@@ -166,16 +173,35 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
       } else {
         units.push_back({0, r});
       }
-      for (const auto& [c0, width] : units) {
+      // Pass 1 (unit order, serial): preconditioners exactly as the reference
+      // builds them. Pass 2: the solves, which are independent of each other
+      // (SPEC.md:151-152), on cfg.unit_threads threads. Pass 3 (unit order):
+      // report rows and the first failure, as the serial loop raises it.
+      struct UnitJob {
+        index_t c0 = 0, width = 0;
+        KronOp op;
+        LinearOp prec;
+        Vec b, x;
+        double ubn = 0.0;
         ReportRow row;
+        GmresResult res;
+      };
+      std::vector<UnitJob> jobs;
+      jobs.reserve(units.size());
+      for (const auto& [c0, width] : units) {
+        UnitJob job;
+        job.c0 = c0;
+        job.width = width;
+        ReportRow& row = job.row;
         row.sweep = z;
         row.point = side + 1;
         row.kind = PrecondKind::None;
         Dense lam(width, width);
         for (index_t i = 0; i < width; ++i)
           for (index_t j = 0; j < width; ++j) lam(i, j) = spec.blocks(c0 + i, c0 + j);
-        KronOp op{lam, ops[side].a, ops[side].e, {}};
-        if (coupled) op.couplers = ops[side].couplers;  // the joint solve (width = r)
+        job.op = KronOp{lam, ops[side].a, ops[side].e, {}};
+        const KronOp& op = job.op;
+        if (coupled) job.op.couplers = ops[side].couplers;  // the joint solve (width = r)
         const bool dec = cfg.decoupled && !coupled;
         SidePrecond& sp = dec ? unit_sides[size_t(side)][size_t(c0)] : sides[size_t(side)];
         if (dec && sp.shape != width) {  // slot changed shape: restart its chain
@@ -183,59 +209,106 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
           sp.shape = int(width);
         }
         LinearOp prec = identity_operator();
-        bool have_explicit = false;
-        Csr a_explicit;
-        if (mode != PrecondMode::None && !sp.degraded) {
-          try {
-            a_explicit = assemble_explicit(op, cfg.explicit_nnz_cap);
-            have_explicit = true;
-          } catch (const ConfigError& e) {
-            sp.degraded = true;
-            report.warnings.push_back(std::string(side == 0 ? "trial" : "test") +
-                                      " side continues unpreconditioned: " + e.what());
-          }
-        }
-        if (have_explicit) {
-          if (mode == PrecondMode::FreshSpai ||
-              (mode == PrecondMode::ReuseChain && (sp.chain.empty() || sp.chain.length() + 1 > cfg.max_chain_len))) {
+        if (mode == PrecondMode::ReuseFrozen) {
+          // GPU extension (irka.cu REUSE_FROZEN): one base per (side, width);
+          // a pair unit with only a real base applies it to both halves.
+          auto it = frozen.find({side, width});
+          if (it == frozen.end() && width == 2 && frozen.count({side, 1})) {
+            const PrecondChain base = frozen[{side, 1}];
+            prec = [base](const Vec& in, Vec& out) {
+              const size_t h = in.size() / 2;
+              Vec lo(in.begin(), in.begin() + long(h)), hi(in.begin() + long(h), in.end()), ylo, yhi;
+              base.apply(lo, ylo);
+              base.apply(hi, yhi);
+              out.assign(ylo.begin(), ylo.end());
+              out.insert(out.end(), yhi.begin(), yhi.end());
+            };
+            row.kind = PrecondKind::ReusedSameMatrix;
+          } else if (it == frozen.end()) {
+            const Csr a_explicit = assemble_explicit(op, cfg.explicit_nnz_cap);
             SpaiResult built = spai_build(a_explicit, cfg.spai);
-            sp.chain = PrecondChain(std::move(built.p), built.build_seconds);
-            row.kind = PrecondKind::Fresh;
             row.precond_build_seconds = built.build_seconds;
+            PrecondChain ch(std::move(built.p), built.build_seconds);
+            frozen[{side, width}] = ch;
+            prec = ch.as_operator();
+            row.kind = PrecondKind::Fresh;
+            if (a_explicit.nrows <= cfg.standard_residual_max_dim) row.standard_residual = standard_residual(a_explicit, ch);
           } else {
-            UpdateFactor f = update_build(sp.prev_explicit, a_explicit, cfg.spai);
-            row.kind = PrecondKind::Vertical;
-            row.precond_build_seconds = f.build_seconds;
-            row.min_residual = f.min_residual;
-            row.matrix_change = f.matrix_change;
-            sp.chain = sp.chain.extended(std::make_shared<const UpdateFactor>(std::move(f)));
+            prec = it->second.as_operator();
+            row.kind = PrecondKind::ReusedSameMatrix;
           }
-          if (mode == PrecondMode::ReuseChain) sp.prev_explicit = a_explicit;
-          prec = sp.chain.as_operator();
-          if (a_explicit.nrows <= cfg.standard_residual_max_dim)
-            row.standard_residual = standard_residual(a_explicit, sp.chain);
+        } else {
+          bool have_explicit = false;
+          Csr a_explicit;
+          if (mode != PrecondMode::None && !sp.degraded) {
+            try {
+              a_explicit = assemble_explicit(op, cfg.explicit_nnz_cap);
+              have_explicit = true;
+            } catch (const ConfigError& e) {
+              sp.degraded = true;
+              report.warnings.push_back(std::string(side == 0 ? "trial" : "test") +
+                                        " side continues unpreconditioned: " + e.what());
+            }
+          }
+          if (have_explicit) {
+            if (mode == PrecondMode::FreshSpai ||
+                (mode == PrecondMode::ReuseChain && (sp.chain.empty() || sp.chain.length() + 1 > cfg.max_chain_len))) {
+              SpaiResult built = spai_build(a_explicit, cfg.spai);
+              sp.chain = PrecondChain(std::move(built.p), built.build_seconds);
+              row.kind = PrecondKind::Fresh;
+              row.precond_build_seconds = built.build_seconds;
+            } else {
+              UpdateFactor f = update_build(sp.prev_explicit, a_explicit, cfg.spai);
+              row.kind = PrecondKind::Vertical;
+              row.precond_build_seconds = f.build_seconds;
+              row.min_residual = f.min_residual;
+              row.matrix_change = f.matrix_change;
+              sp.chain = sp.chain.extended(std::make_shared<const UpdateFactor>(std::move(f)));
+            }
+            if (mode == PrecondMode::ReuseChain) sp.prev_explicit = a_explicit;
+            prec = sp.chain.as_operator();
+            if (a_explicit.nrows <= cfg.standard_residual_max_dim)
+              row.standard_residual = standard_residual(a_explicit, sp.chain);
+          }
         }
-        Vec b(static_cast<size_t>(n * width));
-        std::copy(rhs.col(c0), rhs.col(c0) + n * width, b.begin());
-        double ubn = 0.0;
-        for (double v : b) ubn += v * v;
-        Vec x(static_cast<size_t>(n * width), 0.0);
-        GmresResult res;
-        if (ubn > 0.0) {
-          const LinearOp a_op = [&op](const Vec& in, Vec& out) { op.apply(in, out); };
-          res = gmres_right_preconditioned(a_op, prec, b, cfg.gmres);
+        job.prec = prec;
+        job.b.assign(rhs.col(c0), rhs.col(c0) + n * width);
+        for (double v : job.b) job.ubn += v * v;
+        job.x.assign(static_cast<size_t>(n * width), 0.0);
+        jobs.push_back(std::move(job));
+      }
+      {
+        std::atomic<size_t> next{0};
+        auto worker = [&] {
+          for (size_t i; (i = next.fetch_add(1)) < jobs.size();) {
+            UnitJob& j = jobs[i];
+            if (!(j.ubn > 0.0)) continue;
+            const KronOp* opp = &j.op;
+            const LinearOp a_op = [opp](const Vec& in, Vec& out) { opp->apply(in, out); };
+            j.res = gmres_right_preconditioned(a_op, j.prec, j.b, cfg.gmres);
+          }
+        };
+        const int nt = std::max(1, std::min<int>(cfg.unit_threads, int(jobs.size())));
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nt; ++t) pool.emplace_back(worker);
+        worker();
+        for (auto& th : pool) th.join();
+      }
+      for (UnitJob& j : jobs) {
+        ReportRow& row = j.row;
+        if (j.ubn > 0.0) {
           row.solves = 1;
-          row.gmres_iterations = res.report.iterations;
-          row.gmres_seconds = res.report.solve_seconds;
-          x = res.x;
+          row.gmres_iterations = j.res.report.iterations;
+          row.gmres_seconds = j.res.report.solve_seconds;
+          j.x = j.res.x;
         }
         report.rows.push_back(row);
-        if (ubn > 0.0 && !res.report.converged)
+        if (j.ubn > 0.0 && !j.res.report.converged)
           throw SolverError(std::string("birka: gmres did not converge on the ") + (side == 0 ? "trial" : "test") +
                             " side (sweep " + std::to_string(z) + "; relative residual " +
-                            shortest(res.report.final_residual / std::max(res.report.rhs_norm, 1e-300)) + " after " +
-                            std::to_string(res.report.iterations) + " iterations)");
-        std::copy(x.begin(), x.end(), xsol.col(c0));
+                            shortest(j.res.report.final_residual / std::max(j.res.report.rhs_norm, 1e-300)) +
+                            " after " + std::to_string(j.res.report.iterations) + " iterations)");
+        std::copy(j.x.begin(), j.x.end(), xsol.col(j.c0));
       }
       bases[side] = thin_q(xsol);  // :278
     }
@@ -265,6 +338,13 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
       den += lambda_prev[i].re * lambda_prev[i].re + lambda_prev[i].im * lambda_prev[i].im;
     }
     if (std::sqrt(num) / std::max(std::sqrt(den), 1e-300) < cfg.tol) converged = true;
+    if (verbose) {
+      long its = 0;
+      for (const ReportRow& rw : report.rows)
+        if (rw.sweep == z) its += rw.gmres_iterations;
+      std::fprintf(stderr, "[oracle irka] sweep %d: shift change %.3e, %ld GMRES iterations\n", z,
+                   std::sqrt(num) / std::max(std::sqrt(den), 1e-300), its);
+    }
     lambda_prev = lambda_new;
   }
   state.lambda = lambda_prev;

@@ -209,7 +209,10 @@ Csr assemble_explicit(const KronOp& op, index_t max_nnz);
 
 // ---- reports (proj/include/morprec/report.hpp:14-61) ----------------------
 enum class PrecondKind { None = 0, Fresh = 1, Horizontal = 2, Vertical = 3, ReusedSameMatrix = 4 };
-enum class PrecondMode { None = 0, FreshSpai = 1, ReuseChain = 2 };
+// ReuseFrozen (3) is the GPU path's extension for configs 2-4 ("built once at
+// the first shift and reused"): one SPAI per (side, unit width), built at the
+// first unit that needs it and applied unchanged afterwards.
+enum class PrecondMode { None = 0, FreshSpai = 1, ReuseChain = 2, ReuseFrozen = 3 };
 struct ReportRow {
   int sweep = 0, point = 0;
   PrecondKind kind = PrecondKind::None;
@@ -246,6 +249,7 @@ struct IrkaConfig {
   index_t standard_residual_max_dim = 5000;
   bool decoupled = false;  // one GMRES per shift unit instead of one joint n*r solve
   bool mirror_unstable = false;  // extension: reflect Re(lambda) > 0 before solving
+  int unit_threads = 1;  // decoupled units solved concurrently (solves are independent)
 };
 struct IrkaState {
   Dense kr, fr, cr;        // reduced K = E_r^{-1} A_r, E_r^{-1} W^T B, V^T C

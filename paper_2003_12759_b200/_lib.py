@@ -175,20 +175,8 @@ _SIGS = {
     "mpg_mm_write_dense_buffer": (_I, [_L, _L, vp, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     "mpg_report_csv": (_I, [vp, _I, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     "mpg_buffer_free": (None, [vp]),
-    "mpg_gen_last_error": (C.c_char_p, []),
     "mpg_host_csr_free": (None, [C.POINTER(HostCsr)]),
-    "mpg_host_system_free": (None, [C.POINTER(HostSystem)]),
-    "mpg_gen_random_dense": (_I, [_L, _L, C.c_uint64, vp]),
-    "mpg_gen_random_sparse": (_I, [_L, _L, _D, C.c_uint64, _D, C.POINTER(C.POINTER(HostCsr))]),
-    "mpg_gen_from_triplets": (_I, [_L, _L, _L, vp, vp, vp, C.POINTER(C.POINTER(HostCsr))]),
-    "mpg_gen_bilinear_toy": (_I, [_L, _L, C.c_uint64, C.POINTER(C.POINTER(HostCsr)), vp, vp]),
-    "mpg_gen_disc_brake": (_I, [_L, _D, C.c_uint64, C.POINTER(C.POINTER(HostCsr)), C.POINTER(C.POINTER(HostCsr))]),
-    "mpg_gen_bilinear_toy_n": (_I, [_L, _L, C.c_uint64, C.POINTER(C.POINTER(HostCsr)), vp, vp, vp]),
-    "mpg_gen_qb_toy": (_I, [_L, C.c_uint64] + [C.POINTER(C.POINTER(HostCsr))] * 4),
-    "mpg_gen_grid2d": (_I, [_L, C.c_uint64, C.POINTER(C.POINTER(HostSystem))]),
-    "mpg_gen_convdiff3d": (_I, [_L, C.c_uint64, C.POINTER(C.POINTER(HostSystem))]),
-    "mpg_gen_fem3d": (_I, [_L, C.c_uint64, _I, C.POINTER(C.POINTER(HostSystem))]),
-    "mpg_gen_zipf": (_I, [_L, C.c_uint64, _L, _L, _D, _I, C.POINTER(C.POINTER(HostSystem))]),
+    "mpg_host_csr_from_triplets": (_I, [_L, _L, _L, vp, vp, vp, C.POINTER(C.POINTER(HostCsr))]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

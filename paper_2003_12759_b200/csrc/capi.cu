@@ -581,6 +581,63 @@ static mpg_host_csr* to_host_csr(mmio::Csr&& c) {
   return m;
 }
 
+void mpg_host_csr_free(mpg_host_csr* m) {
+  if (!m) return;
+  delete[] m->rowptr;
+  delete[] m->colind;
+  delete[] m->val;
+  delete m;
+}
+
+// SparseMatrix::from_triplets (sparse.cpp:80-115): rows by a stable counting
+// sort, columns by a stable sort within each row, duplicates summed in input
+// order (the reference's std::sort leaves that order unspecified).
+int mpg_host_csr_from_triplets(int64_t nr, int64_t nc, int64_t nnz, const int64_t* ri, const int64_t* ci,
+                               const double* v, mpg_host_csr** out) {
+  return guard([&] {
+    if (nr < 0 || nc < 0 || nnz < 0 || !out || (nnz > 0 && (!ri || !ci || !v)))
+      throw std::invalid_argument("sparse: negative dimension or null triplets");
+    for (int64_t k = 0; k < nnz; ++k)
+      if (ri[k] < 0 || ri[k] >= nr || ci[k] < 0 || ci[k] >= nc)
+        throw std::invalid_argument("sparse: triplet index out of range");
+    std::vector<int64_t> start(size_t(nr) + 1, 0);
+    std::vector<int64_t> order(static_cast<size_t>(nnz));
+    for (int64_t k = 0; k < nnz; ++k) ++start[size_t(ri[k]) + 1];
+    for (int64_t i = 0; i < nr; ++i) start[size_t(i) + 1] += start[size_t(i)];
+    {
+      std::vector<int64_t> fill(start.begin(), start.end() - 1);
+      for (int64_t k = 0; k < nnz; ++k) order[size_t(fill[size_t(ri[k])]++)] = k;
+    }
+    mmio::Csr c;
+    c.nrows = nr;
+    c.ncols = nc;
+    c.rowptr.reset(new int64_t[size_t(nr) + 1]);
+    std::vector<int64_t> cols;
+    std::vector<double> vals;
+    cols.reserve(size_t(nnz));
+    vals.reserve(size_t(nnz));
+    c.rowptr[0] = 0;
+    for (int64_t i = 0; i < nr; ++i) {
+      auto b = order.begin() + start[size_t(i)], e = order.begin() + start[size_t(i) + 1];
+      std::stable_sort(b, e, [&](int64_t x, int64_t y) { return ci[x] < ci[y]; });
+      for (auto p = b; p != e;) {
+        const int64_t col = ci[*p];
+        double sum = 0.0;
+        for (; p != e && ci[*p] == col; ++p) sum += v[*p];
+        cols.push_back(col);
+        vals.push_back(sum);
+      }
+      c.rowptr[size_t(i) + 1] = int64_t(cols.size());
+    }
+    c.nnz = int64_t(cols.size());
+    c.colind.reset(new int64_t[std::max<size_t>(1, cols.size())]);
+    c.val.reset(new double[std::max<size_t>(1, vals.size())]);
+    std::copy(cols.begin(), cols.end(), c.colind.get());
+    std::copy(vals.begin(), vals.end(), c.val.get());
+    *out = to_host_csr(std::move(c));
+  });
+}
+
 static mmio::Csr from_host_csr(const mpg_host_csr* a) {
   if (!a || a->nrows < 0 || a->ncols < 0 || (a->nrows > 0 && !a->rowptr)) throw std::invalid_argument("mmio: bad matrix");
   mmio::Csr c;

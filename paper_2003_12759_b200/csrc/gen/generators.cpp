@@ -1,4 +1,6 @@
-// Seeded synthetic inputs shared by the GPU path, the tests and the bench.
+// Seeded synthetic inputs (include/mpg_gen.h): test and bench fixtures, built
+// into libmpggen.so and, for the CPU reference arm, into oracle/liboracle.so.
+// Not part of the product library libmpg.so.
 //
 // BASELINE.json's five configs have no generator in the reference (SURVEY.md
 // §0.5f); they are defined here once so the oracle and the GPU
@@ -19,7 +21,7 @@
 #include <string>
 #include <vector>
 
-#include "../../../include/mpg.h"
+#include "../../../include/mpg_gen.h"
 
 namespace {
 
@@ -141,7 +143,7 @@ extern "C" {
 
 const char* mpg_gen_last_error(void) { return g_gen_err.c_str(); }
 
-void mpg_host_csr_free(mpg_host_csr* m) {
+void mpg_gen_csr_free(mpg_host_csr* m) {
   if (!m) return;
   delete[] m->rowptr;
   delete[] m->colind;
@@ -149,10 +151,10 @@ void mpg_host_csr_free(mpg_host_csr* m) {
   delete m;
 }
 
-void mpg_host_system_free(mpg_host_system* s) {
+void mpg_gen_system_free(mpg_host_system* s) {
   if (!s) return;
-  mpg_host_csr_free(s->a);
-  mpg_host_csr_free(s->e);
+  mpg_gen_csr_free(s->a);
+  mpg_gen_csr_free(s->e);
   delete[] s->e_diag;
   delete[] s->b;
   delete[] s->c;
@@ -224,8 +226,8 @@ static int bilinear_toy_impl(int64_t n, int64_t m, uint64_t seed, mpg_host_csr**
     }
     mpg_host_csr* pert = from_trips(n, n, std::move(skew));
     *k_out = combine(-1.0, stencil, 1.0, pert);
-    mpg_host_csr_free(stencil);
-    mpg_host_csr_free(pert);
+    mpg_gen_csr_free(stencil);
+    mpg_gen_csr_free(pert);
     for (int64_t j = 0; j < m; ++j) {
       std::vector<Trip> t;
       for (int64_t i = 0; i < n; ++i) {
@@ -234,7 +236,7 @@ static int bilinear_toy_impl(int64_t n, int64_t m, uint64_t seed, mpg_host_csr**
       }
       mpg_host_csr* nj = from_trips(n, n, std::move(t));
       if (n_out) n_out[j] = nj;
-      else mpg_host_csr_free(nj);
+      else mpg_gen_csr_free(nj);
     }
     for (int64_t j = 0; j < m; ++j)
       for (int64_t i = 0; i < n; ++i) f[i + j * n] = sym(rng);
@@ -365,10 +367,10 @@ int mpg_gen_disc_brake(int64_t n, double omega, uint64_t seed, mpg_host_csr** m_
     mpg_host_csr* kg = from_trips(n, n, std::move(kg_t));
     mpg_host_csr* k1 = combine(1.0, ke, 1.0, kr);
     *k_out = combine(1.0, k1, omega * omega, kg);
-    mpg_host_csr_free(ke);
-    mpg_host_csr_free(kr);
-    mpg_host_csr_free(kg);
-    mpg_host_csr_free(k1);
+    mpg_gen_csr_free(ke);
+    mpg_gen_csr_free(kr);
+    mpg_gen_csr_free(kg);
+    mpg_gen_csr_free(k1);
   });
 }
 

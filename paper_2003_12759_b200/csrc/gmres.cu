@@ -22,6 +22,8 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <mutex>
+#include <set>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -2154,20 +2156,23 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   const int Vfac = choose_vec_width(max_fac_mean);
   const size_t smem_dot = size_t(DOT_TILE + maxit + 2) * sizeof(double);
   const size_t smem_upd = size_t(2 * (maxit + 2)) * sizeof(double);
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [] {
-    cudaFuncSetAttribute(k_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_reorth_p, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  });
-  // TMA-staged update + probe kernels: slots = the update clusters, one CTA each.
-  static std::once_flag gt_once;
-  std::call_once(gt_once, [] {
-    cudaFuncSetAttribute(k_gs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, GT_SMEM);
-    cudaFuncSetAttribute(k_gs_tmx<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
-    cudaFuncSetAttribute(k_gs_tmx<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
-  });
+  // Dynamic shared-memory opt-ins are per device context: set them once per
+  // device (the library keeps one context per device, ctx(dev)).
+  {
+    static std::mutex attr_mu;
+    static std::set<int> attr_done;
+    std::lock_guard<std::mutex> lk(attr_mu);
+    if (attr_done.insert(op.device).second) {
+      cudaFuncSetAttribute(k_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_backsub, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_reorth_p, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      // TMA-staged update + probe kernels: slots = the update clusters, one CTA each.
+      cudaFuncSetAttribute(k_gs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, GT_SMEM);
+      cudaFuncSetAttribute(k_gs_tmx<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
+      cudaFuncSetAttribute(k_gs_tmx<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
+    }
+  }
   const bool need_reg_upd = upd_kind == 0 || usel.low > 0 || (upd_kind == 1 && maxit + 1 > GT_MAXCOLS) ||
                             ((upd_kind & 2) && maxit + 2 > GX_MAXV);
   const bool need_tma = (upd_kind & 1) && (upd_kind == 1 || usel.split > 0);

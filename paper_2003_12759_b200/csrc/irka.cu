@@ -89,11 +89,22 @@ __global__ void __launch_bounds__(256) k_ts_apply(const double* __restrict__ X, 
 }
 
 Mat ts_gram(int dev, const double* X, int64_t ldx, int a, const double* Y, int64_t ldy, int b, int64_t n) {
+  if (a > 1024) throw std::invalid_argument("ts_gram: at most 1024 rows in the Gram");
+  if (a * b > 1024) {  // tile over column blocks of Y (one launch holds <= 1024 products per CTA)
+    const int bw = 1024 / a;
+    Mat out(a, b);
+    for (int j0 = 0; j0 < b; j0 += bw) {
+      const int w = std::min(bw, b - j0);
+      const Mat blk = ts_gram(dev, X, ldx, a, Y + size_t(ldy) * j0, ldy, w, n);
+      for (int j = 0; j < w; ++j)
+        for (int i = 0; i < a; ++i) out(i, j0 + j) = blk(i, j);
+    }
+    return out;
+  }
   auto& c = ctx(dev);
   const int blocks = std::max(1, std::min<int>(c.sm_count * 2, int((n + 63) / 64)));
   DBuf<double> part(dev, size_t(blocks) * size_t(a) * size_t(b));
   const size_t smem = size_t(64) * size_t(a + b) * sizeof(double);
-  if (a * b > 1024) throw std::invalid_argument("ts_gram: reduced order too large");
   k_ts_gram<<<blocks, 256, smem, c.stream>>>(X, ldx, a, Y, ldy, b, n, part.get());
   MPG_CHECK_LAUNCH();
   count_launch();
@@ -329,6 +340,8 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
   DBuf<double> AV(dev, size_t(n) * r), EV(dev, size_t(n) * r);
   std::map<std::pair<int, int>, SlotPrecond> slots;   // (side, first column)
   std::map<std::pair<int, int>, ChainPtr> frozen;      // (side, unit width) -> frozen base
+  std::map<std::pair<int, int>, std::pair<int, int>> slot_owner;  // (side, c0) -> (rank, width)
+  std::map<std::pair<int, int>, int> slot_iters;                  // (side, c0) -> last sweep's iterations
   std::mt19937_64 perturb_rng(cfg.seed ^ 0x9e3779b97f4a7c15ull);
   std::vector<host::Eig> lambda_prev = host::sorted_eigenvalues(kr);
   bool converged = false;
@@ -360,7 +373,9 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
       for (int i = 0; i < r; ++i)
         if (spec.blocks(i, i) > 0.0) spec.blocks(i, i) = -spec.blocks(i, i);
     }
-    const Mat f2t = host::mul(host::transpose(spec.basis_inv), fr);  // (f2)^T = R^{-1} fr   (r x m)
+    // birka.cpp:182-183: f2 = fr^T R^{-T} (m x r), c2 = cr^T R (q x r); the
+    // trial right-hand sides are B f2 and the test ones C c2 (:199).
+    const Mat f2t = host::mul(spec.basis_inv, fr);                   // (f2)^T = R^{-1} fr   (r x m)
     const Mat c2t = host::mul(host::transpose(spec.basis), cr);      // (c2)^T = R^T cr      (r x q)
     // right-hand sides: side 0 columns B f2 -> RHS[:, 0..r), side 1 C c2 -> RHS[:, r..2r)
     ts_apply(dev, B.get(), n, m, host::transpose(f2t), RHS.get(), n, n);
@@ -372,15 +387,48 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
                           " side (sweep " + std::to_string(z) + "); input/output maps must be nonzero");
     }
     // ---- solve tasks for this rank ----
-    struct Task { int side, c0, w; double sre, sim; };
+    struct Task { int side, c0, w; double sre, sim; int owner; };
     std::vector<Task> mine, all;
     for (int side = 0; side < 2; ++side)
       for (size_t u = 0; u < spec.unit_start.size(); ++u) {
         const int c0 = spec.unit_start[u], w = spec.unit_width[u];
-        Task t{side, c0, w, -spec.blocks(c0, c0), w == 2 ? -spec.blocks(c0, c0 + 1) : 0.0};
-        all.push_back(t);
-        if ((side * r + c0) % world == rank) mine.push_back(t);
+        all.push_back(Task{side, c0, w, -spec.blocks(c0, c0), w == 2 ? -spec.blocks(c0, c0 + 1) : 0.0, 0});
       }
+    {
+      // Owner map, identical on every rank (it depends only on data all ranks
+      // share): units are placed longest-first on the least-loaded rank, with
+      // the cost of a solve modelled from the previous sweep's iterations of
+      // its slot (w K (K + 40): the Gram-Schmidt work grows as K^2). In the
+      // chain-bearing modes a slot keeps its rank while its shape is
+      // unchanged, so its vertical chain stays local.
+      const bool sticky = cfg.mode == MPG_PRECOND_REUSE_CHAIN;
+      std::vector<double> load(size_t(world), 0.0);
+      auto cost = [&](const Task& t) {
+        auto it = slot_iters.find({t.side, t.c0});
+        const double k = it == slot_iters.end() ? 100.0 : double(std::max(it->second, 1));
+        return double(t.w) * k * (k + 40.0);
+      };
+      std::vector<size_t> free_units;
+      for (size_t i = 0; i < all.size(); ++i) {
+        auto it = slot_owner.find({all[i].side, all[i].c0});
+        if (sticky && it != slot_owner.end() && it->second.second == all[i].w) {
+          all[i].owner = it->second.first;
+          load[size_t(all[i].owner)] += cost(all[i]);
+        } else {
+          free_units.push_back(i);
+        }
+      }
+      std::stable_sort(free_units.begin(), free_units.end(),
+                       [&](size_t x, size_t y) { return cost(all[x]) > cost(all[y]); });
+      for (size_t i : free_units) {
+        const int o = int(std::min_element(load.begin(), load.end()) - load.begin());
+        all[i].owner = o;
+        load[size_t(o)] += cost(all[i]);
+        slot_owner[{all[i].side, all[i].c0}] = {o, all[i].w};
+      }
+      for (const Task& t : all)
+        if (t.owner == rank) mine.push_back(t);
+    }
     std::vector<SolveSpec> specs;
     std::vector<mpg_report_row> rows;
     DBuf<double> SOL(dev, size_t(n) * r * 2);
@@ -481,6 +529,8 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
       bounds.push_back(specs.size());
     }
     int sweep_max_its = 0;
+    struct Failure { bool failed; int side, c0; double rel; int its; } fail{false, 0, 0, 0.0, 0};
+    std::vector<int> its_mine(mine.size(), 0);
     t_build = wall() - tz0;
     for (size_t bi = 0; bi + 1 < bounds.size(); ++bi) {
       const size_t b0 = bounds[bi];
@@ -496,45 +546,81 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
         row.gmres_seconds = outc[i].solve_seconds;
         res.total_iterations += outc[i].iterations;
         ++res.total_solves;
-        if (!outc[i].converged) {
-          res.rows.insert(res.rows.end(), rows.begin(), rows.end());
+        its_mine[b0 + i] = outc[i].iterations;
+        if (!outc[i].converged && !fail.failed) {
           const Task& t = mine[b0 + i];
-          char rel[32];
-          std::snprintf(rel, sizeof rel, "%.3e", outc[i].final_residual / std::max(outc[i].rhs_norm, 1e-300));
-          throw SolverError(std::string("birka: gmres did not converge on the ") + (t.side == 0 ? "trial" : "test") +
-                            " side (sweep " + std::to_string(z) + ", unit at column " + std::to_string(t.c0) +
-                            "; relative residual " + rel + " after " + std::to_string(outc[i].iterations) +
-                            " iterations)");
+          fail = Failure{true, t.side, t.c0, outc[i].final_residual / std::max(outc[i].rhs_norm, 1e-300),
+                         outc[i].iterations};
         }
       }
+      if (fail.failed && world == 1) break;
     }
     res.rows.insert(res.rows.end(), rows.begin(), rows.end());
     last_max_its = std::max(last_max_its == 0 ? 0 : last_max_its / 2, sweep_max_its);
     // ---- exchange (K6): all-gather the solved columns ----
+    // Each rank's block is its solved columns followed by a status header
+    // (failure flag and coordinates, then the iterations of its units), so a
+    // solve that fails on one rank is raised on every rank after the
+    // exchange instead of leaving the others blocked in the collective, and
+    // every rank sees the same iteration counts for the next owner map.
     if (world > 1) {
       std::vector<int> owned_cnt(size_t(world), 0);
-      for (const Task& t : all) owned_cnt[size_t((t.side * r + t.c0) % world)] += t.w;
-      const int cmax = *std::max_element(owned_cnt.begin(), owned_cnt.end());
-      DBuf<double> send(dev, size_t(n) * std::max(cmax, 1)), recv(dev, size_t(n) * std::max(cmax, 1) * world);
+      for (const Task& t : all) owned_cnt[size_t(t.owner)] += t.w;
+      const int cmax = std::max(1, *std::max_element(owned_cnt.begin(), owned_cnt.end()));
+      const size_t hdr = 8 + 2 * size_t(r);
+      const size_t blk = size_t(n) * size_t(cmax) + hdr;
+      DBuf<double> send(dev, blk), recv(dev, blk * size_t(world));
       int col = 0;
       for (const Task& t : mine) {
-        MPG_CUDA(cudaMemcpyAsync(send.get() + size_t(n) * col, SOL.get() + size_t(n) * (size_t(r) * t.side + t.c0),
-                                 size_t(n) * t.w * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        if (!fail.failed)
+          MPG_CUDA(cudaMemcpyAsync(send.get() + size_t(n) * col, SOL.get() + size_t(n) * (size_t(r) * t.side + t.c0),
+                                   size_t(n) * t.w * sizeof(double), cudaMemcpyDeviceToDevice, s));
         col += t.w;
       }
+      std::vector<double> h(hdr, 0.0);
+      h[0] = fail.failed ? 1.0 : 0.0;
+      h[1] = fail.side;
+      h[2] = fail.c0;
+      h[3] = fail.rel;
+      h[4] = fail.its;
+      for (size_t i = 0; i < mine.size(); ++i) h[8 + i] = its_mine[i];
+      MPG_CUDA(cudaMemcpyAsync(send.get() + size_t(n) * size_t(cmax), h.data(), hdr * sizeof(double),
+                               cudaMemcpyHostToDevice, s));
       MPG_CUDA(cudaStreamSynchronize(s));
       if (!allgather) throw std::invalid_argument("irka: world > 1 needs an allgather callback");
-      if (allgather(agctx, send.get(), recv.get(), int64_t(n) * std::max(cmax, 1) * 8) != 0)
+      if (allgather(agctx, send.get(), recv.get(), int64_t(blk) * 8) != 0)
         throw CudaError("irka: allgather callback failed");
-      std::vector<int> cursor(size_t(world), 0);
+      std::vector<double> hall(hdr * size_t(world));
+      for (int o = 0; o < world; ++o)
+        MPG_CUDA(cudaMemcpyAsync(hall.data() + hdr * size_t(o), recv.get() + blk * size_t(o) + size_t(n) * size_t(cmax),
+                                 hdr * sizeof(double), cudaMemcpyDeviceToHost, s));
+      MPG_CUDA(cudaStreamSynchronize(s));
+      for (int o = 0; o < world && !fail.failed; ++o)
+        if (hall[hdr * size_t(o)] != 0.0) {
+          const double* ho = hall.data() + hdr * size_t(o);
+          fail = Failure{true, int(ho[1]), int(ho[2]), ho[3], int(ho[4])};
+        }
+      std::vector<int> cursor(size_t(world), 0), ucount(size_t(world), 0);
       for (const Task& t : all) {
-        const int owner = (t.side * r + t.c0) % world;
-        const double* src = recv.get() + size_t(n) * (size_t(owner) * std::max(cmax, 1) + cursor[size_t(owner)]);
-        MPG_CUDA(cudaMemcpyAsync(SOL.get() + size_t(n) * (size_t(r) * t.side + t.c0), src,
-                                 size_t(n) * t.w * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        cursor[size_t(owner)] += t.w;
+        const int o = t.owner;
+        slot_iters[{t.side, t.c0}] = int(hall[hdr * size_t(o) + 8 + size_t(ucount[size_t(o)]++)]);
+        if (!fail.failed) {
+          const double* src = recv.get() + blk * size_t(o) + size_t(n) * size_t(cursor[size_t(o)]);
+          MPG_CUDA(cudaMemcpyAsync(SOL.get() + size_t(n) * (size_t(r) * t.side + t.c0), src,
+                                   size_t(n) * t.w * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        }
+        cursor[size_t(o)] += t.w;
       }
       MPG_CUDA(cudaStreamSynchronize(s));
+    } else {
+      for (size_t i = 0; i < mine.size(); ++i) slot_iters[{mine[i].side, mine[i].c0}] = its_mine[i];
+    }
+    if (fail.failed) {
+      char rel[32];
+      std::snprintf(rel, sizeof rel, "%.3e", fail.rel);
+      throw SolverError(std::string("birka: gmres did not converge on the ") + (fail.side == 0 ? "trial" : "test") +
+                        " side (sweep " + std::to_string(z) + ", unit at column " + std::to_string(fail.c0) +
+                        "; relative residual " + rel + " after " + std::to_string(fail.its) + " iterations)");
     }
     MPG_CUDA(cudaMemcpyAsync(X.get(), SOL.get(), size_t(n) * r * sizeof(double), cudaMemcpyDeviceToDevice, s));
     MPG_CUDA(cudaMemcpyAsync(Y.get(), SOL.get() + size_t(n) * r, size_t(n) * r * sizeof(double),

@@ -112,8 +112,12 @@ class SparseMatrix:
 
     @staticmethod
     def from_triplets(nrows: int, ncols: int, rows, cols, values, device: int = 0) -> "SparseMatrix":
-        from . import gen
-        hc = gen.from_triplets(nrows, ncols, rows, cols, values)
+        ri, ci, v = L.i64(rows), L.i64(cols), L.f64(values)
+        if not (ri.size == ci.size == v.size):
+            raise ValueError("sparse: triplet arrays differ in length")
+        p = C.POINTER(L.HostCsr)()
+        check(lib.mpg_host_csr_from_triplets(nrows, ncols, ri.size, L.ptr(ri), L.ptr(ci), L.ptr(v), C.byref(p)))
+        hc = _take_host_csr(p)
         return SparseMatrix.from_csr(nrows, ncols, hc.rowptr, hc.colind, hc.val, device)
 
     @staticmethod
@@ -783,9 +787,20 @@ def _host_csr_struct(a):
     return h, (rp, ci, v)
 
 
+def _take_host_csr(p):
+    """Copy a library-owned mpg_host_csr into numpy arrays (HostCsr) and free it."""
+    from .gen import HostCsr
+    h = p.contents
+    nr, nnz = h.nrows, h.nnz
+    out = HostCsr(h.nrows, h.ncols, np.ctypeslib.as_array(h.rowptr, (nr + 1,)).copy(),
+                  np.ctypeslib.as_array(h.colind, (max(nnz, 1),))[:nnz].copy(),
+                  np.ctypeslib.as_array(h.val, (max(nnz, 1),))[:nnz].copy())
+    lib.mpg_host_csr_free(p)
+    return out
+
+
 def _from_host(p, device: Optional[int]):
-    from .gen import _take_csr
-    host = _take_csr(p)
+    host = _take_host_csr(p)
     if device is None:
         return host
     return SparseMatrix.from_csr(host.nrows, host.ncols, host.rowptr, host.colind, host.val, device)

@@ -12,8 +12,8 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _declared():
-    src = open(os.path.join(ROOT, "include", "mpg.h")).read()
+def _declared(header="mpg.h"):
+    src = open(os.path.join(ROOT, "include", header)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(mpg_[a-z0-9_]+)\s*\(", src)) - {"mpg_allgather_fn"})
 
@@ -29,6 +29,49 @@ def test_library_exports_every_declared_symbol(mpg):
 def test_python_binding_covers_header(mpg):
     from paper_2003_12759_b200 import _lib
     assert set(_declared()) <= set(_lib.EXPORTED)
+
+
+def test_product_library_has_no_generators(mpg):
+    """The seeded input generators are fixtures (include/mpg_gen.h): they live in
+    libmpggen.so and oracle/liboracle.so, never in the product library."""
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_2003_12759_b200", "libmpg.so"))
+    gen_names = _declared("mpg_gen.h")
+    assert len(gen_names) >= 10
+    assert not [n for n in gen_names if hasattr(lib, n)]
+    for path in (os.path.join(ROOT, "paper_2003_12759_b200", "libmpggen.so"), os.path.join(ROOT, "oracle", "liboracle.so")):
+        g = ctypes.CDLL(path)
+        assert not [n for n in gen_names if not hasattr(g, n)], path
+    from paper_2003_12759_b200 import gen
+    assert set(gen_names) == set(gen.EXPORTED)
+
+
+def test_oracle_generators_match_product_generators(gen):
+    import oracle.gen as ogen
+    assert ogen.LIBPATH.endswith(os.path.join("oracle", "liboracle.so"))
+    a, b = gen.config3(N=7), ogen.config3(N=7)
+    for x, y in ((a.a, b.a), (a.e, b.e)):
+        assert np.array_equal(x.rowptr, y.rowptr) and np.array_equal(x.colind, y.colind)
+        assert np.array_equal(x.val, y.val)
+    assert np.array_equal(a.b, b.b) and np.array_equal(a.c, b.c)
+    assert np.array_equal(gen.random_dense(5, 4, 9), ogen.random_dense(5, 4, 9))
+
+
+def test_product_from_triplets_matches_reference_rule(mpg):
+    """SparseMatrix::from_triplets (sparse.cpp:80-115): sorted, duplicates summed, exact zeros kept."""
+    from paper_2003_12759_b200 import _lib as L
+    import ctypes as C
+    rows, cols = np.array([2, 0, 2, 0, 1, 2]), np.array([1, 2, 1, 0, 1, 0])
+    vals = np.array([1.5, 3.0, -1.5, 4.0, 5.0, 7.0])
+    p = C.POINTER(L.HostCsr)()
+    ri, ci, v = L.i64(rows), L.i64(cols), L.f64(vals)
+    assert L.lib.mpg_host_csr_from_triplets(3, 3, 6, L.ptr(ri), L.ptr(ci), L.ptr(v), C.byref(p)) == 0
+    from paper_2003_12759_b200.morprec import _take_host_csr
+    h = _take_host_csr(p)
+    assert list(h.rowptr) == [0, 2, 3, 5]
+    assert list(h.colind) == [0, 2, 1, 0, 1]
+    assert list(h.val) == [4.0, 3.0, 5.0, 7.0, 0.0]
+    bad = L.i64([3])
+    assert L.lib.mpg_host_csr_from_triplets(3, 3, 1, L.ptr(bad), L.ptr(ci), L.ptr(v), C.byref(p)) == L.MPG_ERR_INVALID
 
 
 def test_no_device_is_an_error_not_a_fallback(mpg):
