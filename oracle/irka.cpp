@@ -135,6 +135,15 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
       state.kr = nudged;
       lambda_prev = sorted_eigenvalues(state.kr);
     }
+    // ReuseFrozen builds each (side, width) base at the first unit in the GPU
+    // path's unit order, (Re lambda, -|Im lambda|) ascending before mirroring
+    // (small_dense.cpp real_spectrum), so both build it at the same shift.
+    std::map<index_t, std::pair<double, double>> frozen_key;  // first column -> sort key
+    for (index_t cc = 0; cc < r;) {
+      const index_t w = (cc + 1 < r && spec.blocks(cc, cc + 1) != 0.0) ? 2 : 1;
+      frozen_key[cc] = {spec.blocks(cc, cc), w == 2 ? -std::fabs(spec.blocks(cc, cc + 1)) : 0.0};
+      cc += w;
+    }
     if (cfg.mirror_unstable) {
       // Standard IRKA safeguard (not in the reference): shifts sigma = -lambda of
       // unstable reduced poles are reflected, Re(lambda) -> -|Re(lambda)|.
@@ -186,9 +195,15 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
         ReportRow row;
         GmresResult res;
       };
-      std::vector<UnitJob> jobs;
-      jobs.reserve(units.size());
-      for (const auto& [c0, width] : units) {
+      std::vector<UnitJob> jobs(units.size());
+      std::vector<size_t> p1order(units.size());
+      for (size_t u = 0; u < units.size(); ++u) p1order[u] = u;
+      if (mode == PrecondMode::ReuseFrozen)
+        std::stable_sort(p1order.begin(), p1order.end(), [&](size_t x, size_t y) {
+          return frozen_key[units[x].first] < frozen_key[units[y].first];
+        });
+      for (size_t uidx : p1order) {
+        const auto [c0, width] = units[uidx];
         UnitJob job;
         job.c0 = c0;
         job.width = width;
@@ -275,7 +290,7 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
         job.b.assign(rhs.col(c0), rhs.col(c0) + n * width);
         for (double v : job.b) job.ubn += v * v;
         job.x.assign(static_cast<size_t>(n * width), 0.0);
-        jobs.push_back(std::move(job));
+        jobs[uidx] = std::move(job);
       }
       {
         std::atomic<size_t> next{0};

@@ -1,0 +1,168 @@
+"""Config-scale golden fixtures (BASELINE.json configs[1], [2], [4]) made with the
+CPU oracle in this container (test infrastructure; committed, read by
+tests/test_golden_large.py -m gpu on the GPU box, where these oracle runs would
+not fit the test budget). Every stage also records the oracle's own wall time
+on this container's host cores (the CPU IRKA wall the metric asks for).
+
+Vectors of length n are not stored whole: each fixture keeps the 2-norm, the
+sum and the entries at SAMPLE(n) (every 997th index plus the last), enough for
+size-independent checks at the north star's tolerances.
+
+Stages (python tests/golden/make_golden_large.py <stage> [...]):
+  c2       C2 (64^3, n = 262 144) full IRKA, r = 8, the frozen SPAI of the
+           GPU path's REUSE_FROZEN (built once at the first unit), unstable
+           shifts mirrored, GMRES tol 1e-8, IRKA tol 1e-6, <= 50 sweeps;
+           shifts, sweeps, H_r(i w) on logspace(-4, 4, 200), wall time.
+  c3spmv   C3 (106^3 nodes, n = 1 191 016): (sigma E - A) x and
+           (sigma E - A)^T x for sigma in {1e-4, 1e-1, 1e1}, x ~ seeded N(0,1).
+  c3solves C3: three preconditioned solves (fresh SPAI of sigma E - A,
+           PatternOfA, tol 1e-8) at sigma in {1e-4, 1e-1, 1e1}, b = B.
+  c3irka   C3 full IRKA exactly as bench.py's "irka" leg: r = 8,
+           sigma_init = logspace(1e-4, 1e1), REUSE_FROZEN, mirrored, GMRES
+           1e-8, IRKA tol 1e-6, <= 50 sweeps (hours on 8 cores).
+  c5       C5 generator at n = 100 000 with max_len 2 000 kept (Zipf(1.8) on
+           [3, 2000]): the reference's 64-point shift sweep (bench.cpp:159-249,
+           ReuseChain, fresh at 0/17/34/51), GMRES tol 1e-8: row kinds,
+           iterations, the failure set and sampled solutions.
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+GRID = np.logspace(-4, 4, 200)
+THREADS = int(os.environ.get("GOLDEN_THREADS", os.cpu_count() or 8))
+
+
+def SAMPLE(n):
+    return np.unique(np.append(np.arange(0, n, 997), n - 1))
+
+
+def summary(v):
+    v = np.asarray(v, dtype=np.float64)
+    idx = SAMPLE(v.size)
+    return {"norm": float(np.linalg.norm(v)), "sum": float(v.sum()), "max_abs": float(np.abs(v).max()),
+            "sample": v[idx].tolist()}
+
+
+def _dump(name, obj):
+    with open(os.path.join(HERE, name), "w") as f:
+        json.dump(obj, f)
+    print("wrote", name, flush=True)
+
+
+def _irka(O, s, r, shifts, mode, mirror, gtol, tol, max_sweeps, threads):
+    a = O.Csr.of(s.a)
+    ec = s.e_csr()
+    e = O.Csr.of(ec) if ec is not None else None
+    cfg = O.IrkaConfig(r=r, tol=tol, max_sweeps=max_sweeps, seed=1, gmres=O.GmresConfig(gtol, 1000),
+                       spai=O.SpaiConfig(threads=threads), explicit_nnz_cap=10 ** 12, decoupled=True,
+                       mirror_unstable=mirror, unit_threads=threads)
+    t0 = time.time()
+    res = O.irka_reduce(a, e, s.b, s.c, cfg, mode=mode, init_shifts=shifts)
+    wall = time.time() - t0
+    lam = np.sort_complex(res.lam)
+    hr = np.array([res.transfer(1j * w) for w in GRID])  # (200, q, m)
+    return {"converged": res.converged, "sweeps": res.sweeps, "r": r, "mode": mode, "mirror_unstable": mirror,
+            "gmres_tol": gtol, "irka_tol": tol, "max_sweeps": max_sweeps,
+            "shifts_re": [-float(z.real) for z in lam], "shifts_im": [-float(z.imag) for z in lam],
+            "grid": GRID.tolist(), "hr_re": hr.real.reshape(len(GRID), -1).tolist(),
+            "hr_im": hr.imag.reshape(len(GRID), -1).tolist(),
+            "solves": sum(rw.solves for rw in res.rows), "gmres_iterations": int(sum(rw.iterations for rw in res.rows)),
+            "precond_build_s": round(sum(rw.build_seconds for rw in res.rows), 2),
+            "oracle_wall_s": round(wall, 1), "oracle_threads": threads, "host": _host()}
+
+
+def _host():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu": model}
+
+
+def stage_c2(O, gen):
+    s = gen.config2()
+    out = _irka(O, s, 8, s.shifts, 3, True, 1e-8, 1e-6, 50, THREADS)
+    out["config"] = "C2 64^3 (n=262144), r=8, frozen SPAI (REUSE_FROZEN), mirrored, gmres 1e-8, irka tol 1e-6"
+    _dump("c2_irka.json", out)
+
+
+def stage_c3spmv(O, gen):
+    s = gen.config3()
+    a, e = O.Csr.of(s.a), O.Csr.of(s.e)
+    at, et = a.transpose(), e.transpose()
+    x = np.random.default_rng(11).standard_normal(s.n)
+    out = {"n": s.n, "x_seed": 11, "x": "numpy default_rng(11).standard_normal(n)", "cases": []}
+    for sigma in (1e-4, 1e-1, 1e1):
+        for tr in (0, 1):
+            t0 = time.time()
+            y = O.kron_apply(O.shifted(sigma), at if tr else a, et if tr else e, x)
+            out["cases"].append({"sigma": sigma, "transpose": tr, "y": summary(y), "oracle_s": round(time.time() - t0, 2)})
+            print("spmv", sigma, tr, flush=True)
+    _dump("c3_spmv.json", out)
+
+
+def stage_c3solves(O, gen):
+    s = gen.config3()
+    a, e = O.Csr.of(s.a), O.Csr.of(s.e)
+    out = {"n": s.n, "rhs": "B (normalised x = 0 face indicator)", "gmres_tol": 1e-8, "cases": []}
+    for sigma in (1e-4, 1e-1, 1e1):
+        t0 = time.time()
+        m = O.kron_assemble(O.shifted(sigma), a, e, cap=10 ** 12)
+        p = O.spai_build(m, O.SpaiConfig(threads=THREADS))[0]
+        tb = time.time() - t0
+        t0 = time.time()
+        x, rep = O.gmres_kron(O.shifted(sigma), a, e, O.Chain(p), s.b[:, 0], O.GmresConfig(1e-8, 1000))
+        ts = time.time() - t0
+        out["cases"].append({"sigma": sigma, "iterations": rep.iterations, "converged": bool(rep.converged),
+                             "final_rel_residual": rep.final_residual / rep.rhs_norm, "x": summary(x),
+                             "oracle_build_s": round(tb, 1), "oracle_solve_s": round(ts, 1)})
+        print("solve", sigma, rep.iterations, round(ts, 1), flush=True)
+        del m, p
+    out["host"] = _host()
+    _dump("c3_solves.json", out)
+
+
+def stage_c3irka(O, gen):
+    s = gen.config3()
+    out = _irka(O, s, 8, s.shifts, 3, True, 1e-8, 1e-6, 50, THREADS)
+    out["config"] = ("C3 106^3 nodes (n=1191016), r=8, frozen SPAI (REUSE_FROZEN), mirrored, gmres 1e-8, "
+                     "irka tol 1e-6 (bench.py irka leg)")
+    _dump("c3_irka.json", out)
+
+
+def stage_c5(O, gen):
+    n = int(os.environ.get("GOLDEN_C5_N", 100_000))
+    s = gen.config5(n=n, max_len=2000)
+    a = O.Csr.of(s.a)
+    e = O.Csr.of(s.e_csr())
+    pts = np.logspace(-3, 3, 64)
+    t0 = time.time()
+    rows, failed, xs = O.spai_bench(a, e, s.b[:, 0], pts, spai=O.SpaiConfig(threads=THREADS),
+                                    gmres=O.GmresConfig(1e-8, 1000), mode=2, max_chain_len=16, keep_solutions=True)
+    wall = time.time() - t0
+    out = {"n": n, "max_len": 2000, "nnz": int(s.a.nnz), "max_row": int(np.diff(s.a.rowptr).max()),
+           "points": pts.tolist(), "gmres_tol": 1e-8, "mode": "ReuseChain (bench.cpp:195-211)",
+           "kinds": [int(rw.kind) for rw in rows], "iterations": [int(rw.iterations) for rw in rows],
+           "failed_count": int(failed), "failed": [i for i, rw in enumerate(rows) if rw.iterations >= 1000],
+           "x": [summary(x) for x in xs], "oracle_wall_s": round(wall, 1), "oracle_threads": THREADS,
+           "host": _host()}
+    _dump("c5_sweep.json", out)
+
+
+if __name__ == "__main__":
+    import oracle as O
+    from oracle import gen
+    for st in sys.argv[1:]:
+        globals()["stage_" + st](O, gen)
