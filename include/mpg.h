@@ -248,6 +248,28 @@ int mpg_irka_reduce_sharded(const mpg_op* op, const double* b, int m, const doub
                             double* lam_re, double* lam_im, int* sweeps, int* converged, mpg_report_row* rows,
                             int max_rows, int* nrows);
 
+/* Owner map used by mpg_irka_reduce_sharded (identical on every rank): units
+ * (cost[i], or fixed[i] >= 0 to pin a unit to a rank) placed longest-first on
+ * the least-loaded rank. cost of a unit = width * K * (K + 40) from its
+ * slot's previous-sweep iterations K (mpg_shard_cost; K < 0: unknown). */
+double mpg_shard_cost(int width, int last_iterations);
+int mpg_shard_plan(int nunits, const double* cost, const int* fixed, int world, int* owner);
+
+/* Native exchange: an NCCL communicator owned by the library (NCCL bound at
+ * run time, libnccl.so.2). Rank 0 makes the id with mpg_comm_unique_id, the
+ * caller's rendezvous hands it to every rank, each rank calls
+ * mpg_comm_create on its device. mpg_comm_allgather is an mpg_allgather_fn:
+ * pass (mpg_comm_allgather, comm) to mpg_irka_reduce_sharded and the V/W
+ * columns move device to device on the library stream (ncclAllGather). */
+typedef struct mpg_comm mpg_comm;
+#define MPG_COMM_ID_BYTES 128
+int mpg_comm_unique_id(char* id, int len);
+int mpg_comm_create(int device, int rank, int world, const char* id, mpg_comm** out);
+int mpg_comm_destroy(mpg_comm* comm);
+int mpg_comm_allgather(void* comm, const void* send, void* recv, int64_t bytes_per_rank);
+int mpg_comm_stats(const mpg_comm* comm, long long* calls, double* bytes);
+int mpg_nccl_version(int* version);
+
 /* ---- shift sweep: run_spai_bench (proj/src/bench.cpp:159-249) for
  * sigma_i E - A with a horizontal chain (fresh at i == 0 or when the chain
  * would exceed max_chain_len). Non-convergence is recorded, not raised.

@@ -5,6 +5,7 @@
 // shift-sweep benchmark) for the first-order pencil sigma E - A.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -117,6 +118,7 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
   std::vector<std::vector<SidePrecond>> unit_sides(2, std::vector<SidePrecond>(static_cast<size_t>(r)));
   std::map<std::pair<int, index_t>, PrecondChain> frozen;  // ReuseFrozen: (side, unit width) -> base
   const bool verbose = std::getenv("ORC_IRKA_VERBOSE") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
   std::mt19937_64 perturb_rng(cfg.seed ^ 0x9e3779b97f4a7c15ull);
   std::vector<Complex> lambda_prev = sorted_eigenvalues(state.kr);
   bool converged = false;
@@ -357,8 +359,9 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
       long its = 0;
       for (const ReportRow& rw : report.rows)
         if (rw.sweep == z) its += rw.gmres_iterations;
-      std::fprintf(stderr, "[oracle irka] sweep %d: shift change %.3e, %ld GMRES iterations\n", z,
-                   std::sqrt(num) / std::max(std::sqrt(den), 1e-300), its);
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+      std::fprintf(stderr, "[oracle irka] sweep %d: shift change %.3e, %ld GMRES iterations, %.1f s\n", z,
+                   std::sqrt(num) / std::max(std::sqrt(den), 1e-300), its, el);
     }
     lambda_prev = lambda_new;
   }

@@ -175,6 +175,14 @@ _SIGS = {
     "mpg_mm_write_dense_buffer": (_I, [_L, _L, vp, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     "mpg_report_csv": (_I, [vp, _I, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     "mpg_buffer_free": (None, [vp]),
+    "mpg_shard_cost": (_D, [_I, _I]),
+    "mpg_shard_plan": (_I, [_I, vp, vp, _I, vp]),
+    "mpg_comm_unique_id": (_I, [vp, _I]),
+    "mpg_comm_create": (_I, [_I, _I, _I, vp, C.POINTER(C.c_void_p)]),
+    "mpg_comm_destroy": (_I, [vp]),
+    "mpg_comm_allgather": (_I, [vp, vp, vp, _L]),
+    "mpg_comm_stats": (_I, [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_double)]),
+    "mpg_nccl_version": (_I, [C.POINTER(C.c_int)]),
     "mpg_host_csr_free": (None, [C.POINTER(HostCsr)]),
     "mpg_host_csr_from_triplets": (_I, [_L, _L, _L, vp, vp, vp, C.POINTER(C.POINTER(HostCsr))]),
 }

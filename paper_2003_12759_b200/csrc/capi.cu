@@ -569,6 +569,52 @@ int mpg_qbihomm_reduce(const mpg_op* op, const mpg_csr* n_op, int64_t h_nnz, con
   });
 }
 
+double mpg_shard_cost(int width, int last_iterations) { return shard_cost(width, last_iterations); }
+
+int mpg_shard_plan(int nunits, const double* cost, const int* fixed, int world, int* owner) {
+  return guard([&] {
+    if (nunits < 0 || (nunits > 0 && (!cost || !owner))) throw std::invalid_argument("shard_plan: null argument");
+    std::vector<double> c(cost, cost + nunits);
+    std::vector<int> f = fixed ? std::vector<int>(fixed, fixed + nunits) : std::vector<int>(size_t(nunits), -1);
+    const std::vector<int> o = shard_plan(c, f, world);
+    std::copy(o.begin(), o.end(), owner);
+  });
+}
+
+// ---- native NCCL exchange (comm.cu) -----------------------------------------
+int mpg_comm_unique_id(char* id, int len) {
+  return guard([&] {
+    if (!id) throw std::invalid_argument("comm: null id buffer");
+    comm_unique_id(id, len);
+  });
+}
+
+int mpg_comm_create(int device, int rank, int world, const char* id, mpg_comm** out) {
+  return guard([&] {
+    if (!id || !out) throw std::invalid_argument("comm: null argument");
+    *out = comm_create(device, rank, world, id);
+  });
+}
+
+int mpg_comm_destroy(mpg_comm* comm) {
+  return guard([&] { comm_destroy(comm); });
+}
+
+int mpg_comm_allgather(void* comm, const void* send, void* recv, int64_t bytes_per_rank) {
+  return comm_allgather(static_cast<mpg_comm*>(comm), send, recv, bytes_per_rank);
+}
+
+int mpg_comm_stats(const mpg_comm* comm, long long* calls, double* bytes) {
+  return guard([&] { comm_stats(comm, calls, bytes); });
+}
+
+int mpg_nccl_version(int* version) {
+  return guard([&] {
+    if (!version) throw std::invalid_argument("comm: null argument");
+    *version = nccl_version();
+  });
+}
+
 // ---- Matrix Market IO and the report CSV (host side) -------------------------
 static mpg_host_csr* to_host_csr(mmio::Csr&& c) {
   auto* m = new mpg_host_csr;

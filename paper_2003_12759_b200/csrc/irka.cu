@@ -311,6 +311,35 @@ void default_seed(const DevCsr& a, const IrkaSettings& cfg, Mat& kr, Mat& fr, Ma
 
 }  // namespace
 
+double shard_cost(int width, int last_iterations) {
+  const double k = last_iterations < 0 ? 100.0 : double(std::max(last_iterations, 1));
+  return double(width) * k * (k + 40.0);
+}
+
+std::vector<int> shard_plan(const std::vector<double>& cost, const std::vector<int>& fixed, int world) {
+  if (world < 1) throw std::invalid_argument("shard_plan: world must be at least 1");
+  if (fixed.size() != cost.size()) throw std::invalid_argument("shard_plan: cost and fixed differ in length");
+  std::vector<int> owner(cost.size(), 0);
+  std::vector<double> load(size_t(world), 0.0);
+  std::vector<size_t> free_units;
+  for (size_t i = 0; i < cost.size(); ++i) {
+    if (fixed[i] >= world) throw std::invalid_argument("shard_plan: fixed owner out of range");
+    if (fixed[i] >= 0) {
+      owner[i] = fixed[i];
+      load[size_t(fixed[i])] += cost[i];
+    } else {
+      free_units.push_back(i);
+    }
+  }
+  std::stable_sort(free_units.begin(), free_units.end(), [&](size_t x, size_t y) { return cost[x] > cost[y]; });
+  for (size_t i : free_units) {
+    const int o = int(std::min_element(load.begin(), load.end()) - load.begin());
+    owner[i] = o;
+    load[size_t(o)] += cost[i];
+  }
+  return owner;
+}
+
 IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const double* c_any, int q, const IrkaSettings& cfg,
                     int rank, int world, mpg_allgather_fn allgather, void* agctx) {
   const int dev = op.device;
@@ -326,6 +355,7 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
   if (int64_t(r) > n) throw ConfigError("birka: reduced order exceeds the system dimension");
   if (r > 64 || m > 64 || q > 64) throw ConfigError("irka: r, m, q are limited to 64 on the GPU path");
   if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("irka: bad rank/world");
+  if (world > 1 && !allgather) throw std::invalid_argument("irka: world > 1 needs an allgather callback");
 
   DBuf<double> B(dev, size_t(n) * m), C(dev, size_t(n) * q);
   copy_in(B.get(), b_any, size_t(n) * m, s);
@@ -402,29 +432,18 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
       // chain-bearing modes a slot keeps its rank while its shape is
       // unchanged, so its vertical chain stays local.
       const bool sticky = cfg.mode == MPG_PRECOND_REUSE_CHAIN;
-      std::vector<double> load(size_t(world), 0.0);
-      auto cost = [&](const Task& t) {
-        auto it = slot_iters.find({t.side, t.c0});
-        const double k = it == slot_iters.end() ? 100.0 : double(std::max(it->second, 1));
-        return double(t.w) * k * (k + 40.0);
-      };
-      std::vector<size_t> free_units;
+      std::vector<double> cost(all.size());
+      std::vector<int> fixed(all.size(), -1);
       for (size_t i = 0; i < all.size(); ++i) {
-        auto it = slot_owner.find({all[i].side, all[i].c0});
-        if (sticky && it != slot_owner.end() && it->second.second == all[i].w) {
-          all[i].owner = it->second.first;
-          load[size_t(all[i].owner)] += cost(all[i]);
-        } else {
-          free_units.push_back(i);
-        }
+        auto it = slot_iters.find({all[i].side, all[i].c0});
+        cost[i] = shard_cost(all[i].w, it == slot_iters.end() ? -1 : it->second);
+        auto ot = slot_owner.find({all[i].side, all[i].c0});
+        if (sticky && ot != slot_owner.end() && ot->second.second == all[i].w) fixed[i] = ot->second.first;
       }
-      std::stable_sort(free_units.begin(), free_units.end(),
-                       [&](size_t x, size_t y) { return cost(all[x]) > cost(all[y]); });
-      for (size_t i : free_units) {
-        const int o = int(std::min_element(load.begin(), load.end()) - load.begin());
-        all[i].owner = o;
-        load[size_t(o)] += cost(all[i]);
-        slot_owner[{all[i].side, all[i].c0}] = {o, all[i].w};
+      const std::vector<int> owner = shard_plan(cost, fixed, world);
+      for (size_t i = 0; i < all.size(); ++i) {
+        all[i].owner = owner[i];
+        slot_owner[{all[i].side, all[i].c0}] = {owner[i], all[i].w};
       }
       for (const Task& t : all)
         if (t.owner == rank) mine.push_back(t);
@@ -563,7 +582,7 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
     // solve that fails on one rank is raised on every rank after the
     // exchange instead of leaving the others blocked in the collective, and
     // every rank sees the same iteration counts for the next owner map.
-    if (world > 1) {
+    if (allgather) {  // world > 1, or a single rank exercising its exchange
       std::vector<int> owned_cnt(size_t(world), 0);
       for (const Task& t : all) owned_cnt[size_t(t.owner)] += t.w;
       const int cmax = std::max(1, *std::max_element(owned_cnt.begin(), owned_cnt.end()));
@@ -587,7 +606,6 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
       MPG_CUDA(cudaMemcpyAsync(send.get() + size_t(n) * size_t(cmax), h.data(), hdr * sizeof(double),
                                cudaMemcpyHostToDevice, s));
       MPG_CUDA(cudaStreamSynchronize(s));
-      if (!allgather) throw std::invalid_argument("irka: world > 1 needs an allgather callback");
       if (allgather(agctx, send.get(), recv.get(), int64_t(blk) * 8) != 0)
         throw CudaError("irka: allgather callback failed");
       std::vector<double> hall(hdr * size_t(world));

@@ -34,6 +34,21 @@ struct IrkaResult {
   std::vector<mpg_report_row> rows;
 };
 
+// Owner map of the sharded IRKA: units placed longest-first (stable in unit
+// order) on the least-loaded rank (lowest rank on ties); fixed[i] >= 0 pins a
+// unit. shard_cost models a solve as w K (K + 40) from its slot's previous
+// iteration count K (100 when unknown): the Gram-Schmidt work grows as K^2.
+double shard_cost(int width, int last_iterations);
+std::vector<int> shard_plan(const std::vector<double>& cost, const std::vector<int>& fixed, int world);
+
+// Native NCCL exchange (comm.cu).
+int comm_unique_id(char* out, int len);
+mpg_comm* comm_create(int device, int rank, int world, const char* id_bytes);
+void comm_destroy(mpg_comm* c);
+int comm_allgather(mpg_comm* c, const void* send, void* recv, int64_t bytes);
+void comm_stats(const mpg_comm* c, long long* calls, double* bytes);
+int nccl_version();
+
 IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const double* c_any, int q,
                     const IrkaSettings& cfg, int rank, int world, mpg_allgather_fn allgather, void* agctx);
 

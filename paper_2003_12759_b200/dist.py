@@ -1,17 +1,20 @@
-"""Multi-GPU plumbing: the all-gather callback of mpg_irka_reduce_sharded over
-torch.distributed, and the sharded IRKA entry point.
+"""Multi-GPU plumbing of the sharded IRKA entry point (mpg_irka_reduce_sharded).
 
 One process per GPU. Every rank holds a replica of A and E and solves its share
 of the (shift unit, primal/dual side) solves of each sweep (the reference's
-birka.cpp:200-260 loop, split round-robin by (side * r + column) % world); the
-solved columns are then all-gathered so that every rank forms the same
-projection and the same next shifts. The exchange is the only collective: NCCL
-over NVLink between GPUs, gloo between CPU processes (tests).
+birka.cpp:200-260 loop; units are placed longest-first on the least-loaded
+rank by the previous sweep's iteration counts, irka.cu); the solved columns
+are then all-gathered so that every rank forms the same projection and the
+same next shifts. The exchange is the only collective.
 
-The callback receives raw buffer addresses of this rank's device. It stages
-them through torch tensors with `copy(dst, src, nbytes)` (mpg_copy, a
-cudaMemcpy with cudaMemcpyDefault, by default; ctypes.memmove for host
-buffers) and calls all_gather_into_tensor.
+Two exchanges:
+* NcclComm -- the native one: libmpg.so's own NCCL communicator; the columns
+  move device to device on the library stream (ncclAllGather over NVLink),
+  torch.distributed only hands the NCCL unique id to the ranks.
+* AllGather -- a torch.distributed callback for any backend (gloo between CPU
+  processes in the tests): it stages the raw buffers through torch tensors
+  with `copy(dst, src, nbytes)` (mpg_copy, a cudaMemcpy with
+  cudaMemcpyDefault, by default; ctypes.memmove for host buffers).
 """
 from __future__ import annotations
 
@@ -34,10 +37,18 @@ def host_copy(dst: int, src: int, nbytes: int) -> None:
     C.memmove(dst, src, nbytes)
 
 
-def shard_owner(side: int, column: int, r: int, world: int) -> int:
-    """Rank that solves the unit starting at `column` on `side` (0 primal,
-    1 dual) -- the assignment irka.cu uses for world > 1."""
-    return (side * r + column) % world
+def shard_cost(width: int, last_iterations: int = -1) -> float:
+    """Modelled cost of a unit's solve (irka.cu shard_cost): width * K * (K + 40)."""
+    return float(L.lib.mpg_shard_cost(int(width), int(last_iterations)))
+
+
+def shard_plan(cost, world: int, fixed=None) -> np.ndarray:
+    """Owner rank of each unit, as every rank of mpg_irka_reduce_sharded computes it."""
+    c = L.f64(cost)
+    f = np.ascontiguousarray(fixed if fixed is not None else -np.ones(c.size), dtype=np.int32)
+    out = np.zeros(c.size, dtype=np.int32)
+    L.check(L.lib.mpg_shard_plan(c.size, L.ptr(c), L.ptr(f), int(world), L.ptr(out)))
+    return out
 
 
 class AllGather:
@@ -90,20 +101,85 @@ class AllGather:
         return self._fn
 
 
+class NcclComm:
+    """libmpg.so's native NCCL communicator for `device` (mpg_comm_*). With a
+    torch.distributed group, rank 0's unique id is broadcast through it;
+    without one (world = 1) the communicator is created locally."""
+
+    def __init__(self, device: int = 0, group=None):
+        if group is not None or _dist_ready():
+            import torch.distributed as dist
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+        else:
+            rank, world = 0, 1
+        idb = (C.c_char * 128)()
+        if rank == 0:
+            L.check(L.lib.mpg_comm_unique_id(idb, 128))
+        if world > 1:
+            import torch.distributed as dist
+            obj = [bytes(idb)]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            idb = (C.c_char * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        L.check(L.lib.mpg_comm_create(device, rank, world, idb, C.byref(h)))
+        self._h = h
+        self.rank, self.world, self.device = rank, world, device
+        self.error = None
+        self._fn = L.ALLGATHER_FN(C.cast(L.lib.mpg_comm_allgather, C.c_void_p).value)
+
+    @property
+    def c_function(self):
+        return self._fn
+
+    @property
+    def ctx(self):
+        return self._h
+
+    def stats(self) -> dict:
+        calls, nbytes = C.c_longlong(), C.c_double()
+        L.check(L.lib.mpg_comm_stats(self._h, C.byref(calls), C.byref(nbytes)))
+        return {"calls": calls.value, "bytes": nbytes.value}
+
+    def close(self) -> None:
+        if self._h:
+            L.check(L.lib.mpg_comm_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _dist_ready() -> bool:
+    try:
+        import torch.distributed as dist
+        return dist.is_available() and dist.is_initialized()
+    except Exception:
+        return False
+
+
 def irka_reduce_sharded(op: ShiftedOperator, b, c, cfg: IrkaConfig, mode: int = PrecondMode.REUSE_FROZEN,
-                        init_shifts=None, group=None, gather: Optional[AllGather] = None, device: int = 0):
+                        init_shifts=None, group=None, gather=None, device: int = 0):
     """Sharded IRKA (this rank's share of every sweep's solves + all-gather);
     every rank returns the same reduced model and the report rows of its own
     solves. Call from every rank of `group` with identical arguments; `device`
-    is the GPU holding `op`. With gloo the exchange is staged through host
-    memory (mpg_copy moves the device columns), with NCCL through the GPU."""
-    import torch.distributed as dist
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    is the GPU holding `op`. `gather` is an NcclComm (default with the nccl
+    backend: the native device-to-device exchange) or an AllGather (default
+    otherwise: gloo, staged through host memory by mpg_copy)."""
     if gather is None:
+        import torch.distributed as dist
         if dist.get_backend(group) == "nccl":
-            gather = AllGather(group, device=f"cuda:{device}")
+            gather = NcclComm(device, group)
         else:
             gather = AllGather(group, device="cpu", copy=_mpg_copy)
+    if isinstance(gather, NcclComm):
+        rank, world = gather.rank, gather.world
+    else:
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
     n = op.n
     bm = np.asfortranarray(np.asarray(b, dtype=np.float64).reshape(n, -1))
     cm = np.asfortranarray(np.asarray(c, dtype=np.float64).reshape(n, -1))
@@ -118,7 +194,7 @@ def irka_reduce_sharded(op: ShiftedOperator, b, c, cfg: IrkaConfig, mode: int = 
     cc = cfg.c()
     status = L.lib.mpg_irka_reduce_sharded(
         op._h, L.ptr(bm), m, L.ptr(cm), q, C.byref(cc), mode, L.ptr(ini) if ini is not None else None, rank, world,
-        gather.c_function, None, L.ptr(kr), L.ptr(fr), L.ptr(cr), L.ptr(lre), L.ptr(lim), C.byref(sweeps),
+        gather.c_function, getattr(gather, "ctx", None), L.ptr(kr), L.ptr(fr), L.ptr(cr), L.ptr(lre), L.ptr(lim), C.byref(sweeps),
         C.byref(conv), rows, maxrows, C.byref(nrows))
     if status != L.MPG_OK and gather.error is not None:
         raise RuntimeError(f"all-gather failed: {gather.error}") from gather.error

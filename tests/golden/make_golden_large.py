@@ -11,15 +11,20 @@ size-independent checks at the north star's tolerances.
 Stages (python tests/golden/make_golden_large.py <stage> [...]):
   c2       C2 (64^3, n = 262 144) full IRKA, r = 8, the frozen SPAI of the
            GPU path's REUSE_FROZEN (built once at the first unit), unstable
-           shifts mirrored, GMRES tol 1e-8, IRKA tol 1e-6, <= 50 sweeps;
-           shifts, sweeps, H_r(i w) on logspace(-4, 4, 200), wall time.
+           shifts mirrored, GMRES tol 1e-10, IRKA tol 1e-8, <= 80 sweeps;
+           shifts, sweeps, H_r(i w) on logspace(-4, 4, 200), wall time. (The
+           IRKA stop at 1e-6 leaves the shifts determined only to ~1e-6, the
+           parity tolerance itself: a run stopping one sweep later differs
+           by up to that, measured 2.3e-6 on C2; at 1e-8 both sides stop
+           within ~1e-8 of the same fixed point.)
+  c2ref    the same without mirroring (the reference loop unchanged).
   c3spmv   C3 (106^3 nodes, n = 1 191 016): (sigma E - A) x and
            (sigma E - A)^T x for sigma in {1e-4, 1e-1, 1e1}, x ~ seeded N(0,1).
   c3solves C3: three preconditioned solves (fresh SPAI of sigma E - A,
            PatternOfA, tol 1e-8) at sigma in {1e-4, 1e-1, 1e1}, b = B.
-  c3irka   C3 full IRKA exactly as bench.py's "irka" leg: r = 8,
-           sigma_init = logspace(1e-4, 1e1), REUSE_FROZEN, mirrored, GMRES
-           1e-8, IRKA tol 1e-6, <= 50 sweeps (hours on 8 cores).
+  c3irka   C3 full IRKA as bench.py's "irka" leg (r = 8, sigma_init =
+           logspace(1e-4, 1e1), REUSE_FROZEN, mirrored) at GMRES 1e-10, IRKA
+           tol 1e-8, <= 80 sweeps (hours on 8 cores).
   c5       C5 generator at n = 100 000 with max_len 2 000 kept (Zipf(1.8) on
            [3, 2000]): the reference's 64-point shift sweep (bench.cpp:159-249,
            ReuseChain, fresh at 0/17/34/51), GMRES tol 1e-8: row kinds,
@@ -93,9 +98,18 @@ def _host():
 
 def stage_c2(O, gen):
     s = gen.config2()
-    out = _irka(O, s, 8, s.shifts, 3, True, 1e-8, 1e-6, 50, THREADS)
-    out["config"] = "C2 64^3 (n=262144), r=8, frozen SPAI (REUSE_FROZEN), mirrored, gmres 1e-8, irka tol 1e-6"
+    out = _irka(O, s, 8, s.shifts, 3, True, 1e-10, 1e-8, 80, THREADS)
+    out["config"] = "C2 64^3 (n=262144), r=8, frozen SPAI (REUSE_FROZEN), mirrored, gmres 1e-10, irka tol 1e-8"
     _dump("c2_irka.json", out)
+
+
+def stage_c2ref(O, gen):
+    """C2 through the reference loop unchanged (no mirroring of unstable shifts)."""
+    s = gen.config2()
+    out = _irka(O, s, 8, s.shifts, 3, False, 1e-10, 1e-8, 80, THREADS)
+    out["config"] = ("C2 64^3 (n=262144), r=8, frozen SPAI (REUSE_FROZEN), reference loop (no mirroring), gmres 1e-10, "
+                     "irka tol 1e-8")
+    _dump("c2_irka_ref.json", out)
 
 
 def stage_c3spmv(O, gen):
@@ -136,9 +150,11 @@ def stage_c3solves(O, gen):
 
 def stage_c3irka(O, gen):
     s = gen.config3()
-    out = _irka(O, s, 8, s.shifts, 3, True, 1e-8, 1e-6, 50, THREADS)
-    out["config"] = ("C3 106^3 nodes (n=1191016), r=8, frozen SPAI (REUSE_FROZEN), mirrored, gmres 1e-8, "
-                     "irka tol 1e-6 (bench.py irka leg)")
+    out = _irka(O, s, 8, s.shifts, 3, True, 1e-10, 1e-8, 80, THREADS)
+    out["config"] = ("C3 106^3 nodes (n=1191016), r=8, frozen SPAI (REUSE_FROZEN), mirrored, gmres 1e-10, "
+                     "irka tol 1e-8 (bench.py's irka leg tightened so the converged shifts are determined to well "
+                     "below the 1e-6 parity tolerance; the oracle's per-sweep log gives its wall time to the bench's "
+                     "1e-6 stop)")
     _dump("c3_irka.json", out)
 
 

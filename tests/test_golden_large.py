@@ -1,0 +1,138 @@
+"""Config-scale parity (BASELINE.json configs[1], [2], [4]) against golden fixtures
+made offline by the CPU oracle (tests/golden/make_golden_large.py; the oracle
+runs take minutes to hours, so only their outputs travel). North-star
+tolerances, written here: converged shifts within 1e-6 relative, H_r(i w) on
+logspace(-4, 4, 200) within 1e-6 relative (norm-wise per point), per-solve
+relative residual <= 1e-8, solutions within 1e-6; SpMVs within 1e-13.
+
+Vectors are compared through the fixtures' size-independent summaries: the
+2-norm, the sum and the entries at every 997th index."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+GRID = np.logspace(-4, 4, 200)
+
+
+def _load(name):
+    path = os.path.join(HERE, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not generated yet (tests/golden/make_golden_large.py)")
+    with open(path) as f:
+        return json.load(f)
+
+
+def SAMPLE(n):
+    return np.unique(np.append(np.arange(0, n, 997), n - 1))
+
+
+def _check_summary(v, want, tol):
+    v = np.asarray(v)
+    assert abs(np.linalg.norm(v) - want["norm"]) <= tol * want["norm"]
+    samp = np.asarray(want["sample"])
+    assert np.max(np.abs(v[SAMPLE(v.size)] - samp)) <= tol * want["max_abs"]
+
+
+def _dev(mpg, h):
+    return mpg.SparseMatrix.from_csr(h.nrows, h.ncols, h.rowptr, h.colind, h.val)
+
+
+def _irka_vs_golden(mpg, s, g):
+    ec = s.e_csr()
+    op = mpg.ShiftedOperator(_dev(mpg, s.a), _dev(mpg, ec) if ec is not None else None)
+    cfg = mpg.IrkaConfig(r=g["r"], tol=g["irka_tol"], max_sweeps=g["max_sweeps"], seed=1,
+                         gmres=mpg.GmresConfig(g["gmres_tol"], 1000), mirror_unstable=g["mirror_unstable"])
+    st, rep = mpg.irka_reduce(op, s.b, s.c, cfg, g["mode"], init_shifts=s.shifts[: g["r"]])
+    assert rep.converged == g["converged"]
+    lam = np.sort_complex(st.lam)
+    want = -(np.array(g["shifts_re"]) + 1j * np.array(g["shifts_im"]))
+    assert np.max(np.abs(lam - want) / np.abs(want)) <= 1e-6
+    hw = np.array(g["hr_re"]) + 1j * np.array(g["hr_im"])
+    for i, w in enumerate(GRID):
+        h = st.transfer(1j * w).ravel()
+        assert np.linalg.norm(h - hw[i]) <= 1e-6 * np.linalg.norm(hw[i]), w
+    return rep
+
+
+def test_golden_files_are_consistent():
+    """CPU: the fixtures carry what the GPU tests read (no oracle call)."""
+    for name in ("c2_irka.json", "c2_irka_ref.json", "c3_irka.json"):
+        path = os.path.join(HERE, name)
+        if os.path.exists(path):
+            g = json.load(open(path))
+            assert len(g["shifts_re"]) == g["r"] and len(g["hr_re"]) == len(GRID)
+            assert g["oracle_wall_s"] > 0
+    path = os.path.join(HERE, "c3_spmv.json")
+    if os.path.exists(path):
+        g = json.load(open(path))
+        assert len(g["cases"]) == 6
+        assert all(len(c["y"]["sample"]) == SAMPLE(g["n"]).size for c in g["cases"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c2_irka.json", "c2_irka_ref.json"])
+def test_gpu_c2_irka_matches_golden(mpg, gen, name):
+    g = _load(name)
+    _irka_vs_golden(mpg, gen.config2(), g)
+
+
+@pytest.mark.gpu
+def test_gpu_c3_spmv_matches_golden(mpg, gen):
+    g = _load("c3_spmv.json")
+    s = gen.config3()
+    op = mpg.ShiftedOperator(_dev(mpg, s.a), _dev(mpg, s.e))
+    x = np.random.default_rng(g["x_seed"]).standard_normal(s.n)
+    for case in g["cases"]:
+        y = op.apply(case["sigma"], x, transpose=bool(case["transpose"]))
+        _check_summary(y, case["y"], 1e-13)
+
+
+@pytest.mark.gpu
+def test_gpu_c3_solves_match_golden(mpg, gen):
+    g = _load("c3_solves.json")
+    s = gen.config3()
+    A, E = _dev(mpg, s.a), _dev(mpg, s.e)
+    op = mpg.ShiftedOperator(A, E)
+    As, Es = s.a.to_scipy(), s.e.to_scipy()
+    b = s.b[:, 0]
+    for case in g["cases"]:
+        sigma = case["sigma"]
+        P = mpg.spai_build(op.explicit(sigma)).p
+        res = mpg.gmres_shifted(op, sigma, b, mpg.PrecondChain(P), cfg=mpg.GmresConfig(g["gmres_tol"], 1000))
+        assert res.report.converged and case["converged"]
+        assert abs(res.report.iterations - case["iterations"]) <= max(3, 0.03 * case["iterations"])
+        r = b - (sigma * Es - As) @ res.x
+        assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(b)  # north star: per-solve residual <= 1e-8
+        _check_summary(res.x, case["x"], 1e-6)
+
+
+@pytest.mark.gpu
+def test_gpu_c3_irka_matches_golden(mpg, gen):
+    g = _load("c3_irka.json")
+    _irka_vs_golden(mpg, gen.config3(), g)
+
+
+@pytest.mark.gpu
+def test_gpu_c5_sweep_matches_golden(mpg, gen):
+    """The reference's shift sweep (bench.cpp:159-249, ReuseChain) on the C5
+    generator at reduced n with its 2 000-entry rows kept: row kinds, the
+    failure set, iteration counts and the converged solutions."""
+    g = _load("c5_sweep.json")
+    s = gen.config5(n=g["n"], max_len=g["max_len"])
+    assert s.a.nnz == g["nnz"]
+    op = mpg.ShiftedOperator(_dev(mpg, s.a), _dev(mpg, s.e_csr()))
+    res = mpg.spai_bench(op, s.b[:, 0], g["points"], gmres=mpg.GmresConfig(g["gmres_tol"], 1000),
+                         mode=mpg.PrecondMode.REUSE_CHAIN, max_chain_len=16, keep_solutions=True)
+    rows = res.report.rows
+    assert [int(r.kind) for r in rows] == g["kinds"]
+    failed = [i for i, r in enumerate(rows) if r.gmres_iterations >= 1000]
+    assert failed == g["failed"]
+    for i, r in enumerate(rows):
+        if i in failed:
+            continue
+        k = g["iterations"][i]
+        assert abs(r.gmres_iterations - k) <= max(3, 0.05 * k), (i, r.gmres_iterations, k)
+        _check_summary(res.x[i], g["x"][i], 1e-6)
