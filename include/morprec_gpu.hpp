@@ -2,16 +2,20 @@
 // (/root/reference/proj/include/morprec) over the C ABI in mpg.h.
 //
 // Same names and argument meaning as the reference; Eigen containers are
-// replaced by std::vector<double> (column-major for matrices). Errors map back
-// to the reference's exception classes: MPG_ERR_INVALID -> std::invalid_argument,
-// MPG_ERR_CONFIG -> ConfigError, MPG_ERR_SOLVER -> SolverError
-// (proj/include/morprec/errors.hpp:12-28); GMRES non-convergence stays a
-// report flag (gmres.hpp:41-48).
+// replaced by std::vector<double> (column-major for matrices). Errors are the
+// reference's own exception classes (proj/include/morprec/errors.hpp:12-28):
+// MPG_ERR_INVALID -> std::invalid_argument, MPG_ERR_CONFIG ->
+// morprec::ConfigError, MPG_ERR_SOLVER -> morprec::SolverError, MPG_ERR_IO ->
+// morprec::IoError, so a reference caller's handlers (tools/main.cpp:476-491,
+// exit codes 2/3/4) see the same types. GMRES non-convergence stays a report
+// flag (gmres.hpp:41-48). Device failures (MPG_ERR_CUDA) are DeviceError, a
+// std::runtime_error (exit code 1 there, like any other std::exception).
 #pragma once
 
 #include <cmath>
 #include <cstdint>
 #include <memory>
+#include <new>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -19,11 +23,37 @@
 
 #include "mpg.h"
 
+#if __has_include(<morprec/errors.hpp>)
+// Built inside the reference tree (its include/ on the path): its classes.
+#include <morprec/errors.hpp>
+#else
+// Standalone: the same three declarations as the reference's Eigen-free
+// errors.hpp, so code written against morprec:: compiles unchanged.
+namespace morprec {
+class ConfigError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class SolverError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class IoError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+}  // namespace morprec
+#endif
+
 namespace morprec_gpu {
 
-class ConfigError : public std::runtime_error { using std::runtime_error::runtime_error; };
-class SolverError : public std::runtime_error { using std::runtime_error::runtime_error; };
-class DeviceError : public std::runtime_error { using std::runtime_error::runtime_error; };
+using morprec::ConfigError;
+using morprec::IoError;
+using morprec::SolverError;
+class DeviceError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
 
 inline void check(int status) {
   if (status == MPG_OK) return;
@@ -32,6 +62,7 @@ inline void check(int status) {
     case MPG_ERR_INVALID: throw std::invalid_argument(msg);
     case MPG_ERR_CONFIG: throw ConfigError(msg);
     case MPG_ERR_SOLVER: throw SolverError(msg);
+    case MPG_ERR_IO: throw IoError(msg);
     case MPG_ERR_NOMEM: throw std::bad_alloc();
     case MPG_ERR_CUDA: throw DeviceError(msg);
     default: throw std::logic_error(msg);

@@ -285,10 +285,11 @@ class SpaiConfig:
     max_fill_per_col: int = 50
     max_pattern_sweeps: int = 3
     threads: int = 1
+    power: int = 2
 
     def c(self):
-        return SpaiCfg({"diagonal": 0, "a": 1, "a_pow": 2}[self.pattern], 2, self.fill_tol, self.max_fill_per_col,
-                       self.max_pattern_sweeps, self.threads)
+        return SpaiCfg({"diagonal": 0, "a": 1, "a_pow": 2}[self.pattern], self.power, self.fill_tol,
+                       self.max_fill_per_col, self.max_pattern_sweeps, self.threads)
 
 
 @dataclasses.dataclass

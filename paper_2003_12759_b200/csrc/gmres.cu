@@ -505,6 +505,84 @@ __global__ void __launch_bounds__(256) k_spmv_il2(GmSolve* S, Group grp, CsrView
   }
 }
 
+// Halo-staged sliced-ELL variant (runtime.cuh HaloPattern): one CTA per block
+// of HALO_R rows stages the block's halo of x (all MB right-hand sides, 64 B
+// per column, padded to 80 B so the 16-byte reads of 32 rows spread over the
+// banks) into shared memory once, then one thread per row walks its slice
+// column-major: the matrix stream is a coalesced 2-byte local index + the value
+// per entry and the x-gather never leaves the SM.
+template <int EM, bool CHAIN>
+__global__ void __launch_bounds__(HALO_R) k_spmv_halo(GmSolve* S, Group grp, HaloView hv, OpView op,
+                                                      const double* __restrict__ xin, double* __restrict__ xout) {
+  if (!il_any_run(S, grp)) return;
+  extern __shared__ double2 xs[];
+  const int blk = blockIdx.x;
+  const int h0 = hv.hoff[blk], L = hv.hoff[blk + 1] - h0;
+  for (int t = threadIdx.x; t < L; t += HALO_R) {
+    const double2* src = reinterpret_cast<const double2*>(xin + size_t(__ldg(hv.halo + h0 + t)) * MB);
+    double2* dst = xs + t * HALO_XSTRIDE;
+    dst[0] = __ldg(src);
+    dst[1] = __ldg(src + 1);
+    dst[2] = __ldg(src + 2);
+    dst[3] = __ldg(src + 3);
+  }
+  __syncthreads();
+  const int row = blk * HALO_R + threadIdx.x;
+  if (row >= hv.nrows) return;
+  const int slice = row >> 5, lane = row & 31;
+  const int e0 = __ldg(hv.sptr + slice), w = (__ldg(hv.sptr + slice + 1) - e0) >> 5;
+  double a[MB], ev[MB];
+#pragma unroll
+  for (int q = 0; q < MB; ++q) a[q] = ev[q] = 0.0;
+#pragma unroll 4
+  for (int j = 0; j < w; ++j) {
+    const int e = e0 + j * 32 + lane;
+    const double2* xp = xs + int(__ldcs(hv.lidx + e)) * HALO_XSTRIDE;
+    if (EM == E_SAMEPAT && !CHAIN) {
+      const double2 v = __ldcs(hv.val2 + e);
+#pragma unroll
+      for (int h = 0; h < MB / 2; ++h) {
+        const double2 x = xp[h];
+        a[2 * h] = fma(v.x, x.x, a[2 * h]);
+        a[2 * h + 1] = fma(v.x, x.y, a[2 * h + 1]);
+        ev[2 * h] = fma(v.y, x.x, ev[2 * h]);
+        ev[2 * h + 1] = fma(v.y, x.y, ev[2 * h + 1]);
+      }
+    } else {
+      const double v = __ldcs(hv.val + e);
+#pragma unroll
+      for (int h = 0; h < MB / 2; ++h) {
+        const double2 x = xp[h];
+        a[2 * h] = fma(v, x.x, a[2 * h]);
+        a[2 * h + 1] = fma(v, x.y, a[2 * h + 1]);
+      }
+    }
+  }
+  if (CHAIN) {
+    double2* yp = reinterpret_cast<double2*>(xout + size_t(row) * MB);
+#pragma unroll
+    for (int h = 0; h < MB / 2; ++h) yp[h] = make_double2(a[2 * h], a[2 * h + 1]);
+    return;
+  }
+  if (EM == E_IDENT || EM == E_DIAG) {
+    const double dd = EM == E_DIAG ? op.ediag[row] : 1.0;
+    const double2* xr = reinterpret_cast<const double2*>(xin + size_t(row) * MB);
+#pragma unroll
+    for (int h = 0; h < MB / 2; ++h) {
+      const double2 x = xr[h];
+      ev[2 * h] = dd * x.x;
+      ev[2 * h + 1] = dd * x.y;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < MB; ++q) {
+    if (q >= grp.cnt) continue;
+    GmSolve& st = S[grp.idx[q]];
+    if (st.phase != PH_RUN) continue;
+    st.V[st.k + 1][vidx(row)] = st.scale[st.k] * (st.sre * ev[q] + st.ca * a[q]);
+  }
+}
+
 // ---- dot: part[j][blk] = W_j . w (j <= k), part[k+1][blk] = ||w||^2 -------------
 // which 0: w = W_{k+1} (projection h); which 1: w = W_{k+1} (probe d)
 __global__ void __launch_bounds__(256) k_dot(GmSolve* S, int G) {
@@ -2171,6 +2249,11 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       cudaFuncSetAttribute(k_gs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, GT_SMEM);
       cudaFuncSetAttribute(k_gs_tmx<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
       cudaFuncSetAttribute(k_gs_tmx<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
+      const int hsm = HALO_MAX * HALO_XSTRIDE * int(sizeof(double2));
+      cudaFuncSetAttribute(k_spmv_halo<E_IDENT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
+      cudaFuncSetAttribute(k_spmv_halo<E_IDENT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
+      cudaFuncSetAttribute(k_spmv_halo<E_DIAG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
+      cudaFuncSetAttribute(k_spmv_halo<E_SAMEPAT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
     }
   }
   const bool need_reg_upd = upd_kind == 0 || usel.low > 0 || (upd_kind == 1 && maxit + 1 > GT_MAXCOLS) ||
@@ -2189,6 +2272,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   std::vector<DBuf<double>> il_bufs;   // two [n][MB] buffers per chain group (empty if not il)
   bool any_plain_chain = true, any_plain_op_run = true, any_plain_op_asm = true;
   bool il2 = false;  // RHS-split interleaved SpMVs
+  bool use_halo = false;
   if (!std::getenv("MPG_NO_MULTI")) {
     std::vector<int> used(size_t(ns), 0);
     for (int i = 0; i < ns; ++i) {
@@ -2211,6 +2295,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     // interleaved path: chain groups of real shifts on one operator side
     const bool il_on = !std::getenv("MPG_NO_IL");
     il2 = std::getenv("MPG_IL_NNZSPLIT") == nullptr;  // RHS split measured faster (C3: 256 -> 221 ms / 348 its)
+    use_halo = std::getenv("MPG_SPMV_CSR") == nullptr;  // halo-staged sliced ELL where the pattern fits
     std::vector<int> in_il(size_t(ns), 0);
     for (size_t gi = 0; gi < chain_groups.size(); ++gi) {
       const Group& g = chain_groups[gi];
@@ -2220,6 +2305,10 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         ok = !m.pair && m.transpose == hs[size_t(g.idx[0])].transpose && m.n == int(nb);
       }
       chain_il.push_back(ok ? 1 : 0);
+      if (ok && use_halo) {  // build the halo layouts now: the iteration is captured into a graph
+        for (const CsrPtr& f : chain_of_group[gi]->factors) halo_of(*f, nullptr);
+        halo_of_op(op, hs[size_t(g.idx[0])].transpose != 0, nullptr);
+      }
       if (ok) {
         il_bufs.emplace_back(dev, size_t(nb) * MB);
         il_bufs.emplace_back(dev, size_t(nb) * MB);
@@ -2272,6 +2361,15 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         }
         const double* xin = (stage & 1) ? xb : xa;
         double* xout = (stage & 1) ? xa : xb;
+        HaloView hv{};
+        const HaloPattern* hp = use_halo ? halo_of(f, &hv) : nullptr;
+        if (hp) {
+          k_spmv_halo<E_IDENT, true><<<hp->nblocks, HALO_R, size_t(hp->max_halo) * HALO_XSTRIDE * sizeof(double2), s>>>(
+              dS.get(), chain_groups[gi], hv, opn, xin, xout);
+          ++launches_per_iter;
+          mark(PK_CHAIN);
+          continue;
+        }
         if (il2) {
           k_spmv_il2<E_IDENT, true><<<cdiv(f.nrows * 4, 256), 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), opn,
                                                                          xin, xout);
@@ -2321,6 +2419,19 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         const int nst = int(chain_of_group[gi]->factors.size());
         const double* xin = ((nst - 1) & 1) ? il_bufs[2 * gi].get() : il_bufs[2 * gi + 1].get();
         const unsigned grid1 = cdiv(nb * int64_t(Vop), 256);
+        HaloView hv{};
+        const HaloPattern* hp = use_halo ? halo_of_op(op, hs[size_t(g.idx[0])].transpose != 0, &hv) : nullptr;
+        if (hp) {
+          const size_t sm = size_t(hp->max_halo) * HALO_XSTRIDE * sizeof(double2);
+          switch (op.emode) {
+            case E_IDENT: k_spmv_halo<E_IDENT, false><<<hp->nblocks, HALO_R, sm, s>>>(dS.get(), g, hv, ov, xin, nullptr); break;
+            case E_DIAG: k_spmv_halo<E_DIAG, false><<<hp->nblocks, HALO_R, sm, s>>>(dS.get(), g, hv, ov, xin, nullptr); break;
+            default: k_spmv_halo<E_SAMEPAT, false><<<hp->nblocks, HALO_R, sm, s>>>(dS.get(), g, hv, ov, xin, nullptr); break;
+          }
+          ++launches_per_iter;
+          mark(PK_OP);
+          continue;
+        }
         if (il2) {
           const CsrView none{};
           const unsigned g2 = cdiv(nb * 4, 256);

@@ -1,0 +1,235 @@
+// Halo-staged sliced-ELL layout for the run-mode multi-RHS SpMVs (runtime.cuh
+// HaloPattern). Built once per sparsity pattern, entirely on the device:
+//   pass 1 (k_halo_count): per block of HALO_R rows, sort the block's column
+//     indices in shared memory (bitonic), count the unique ones (the halo) and
+//     the width of each 32-row slice;
+//   host: prefix sums of the halo sizes and slice widths (one small copy);
+//   pass 2 (k_halo_fill): sort again, write the halo, and for every entry its
+//     16-bit local index (binary search in the block's halo) and its CSR
+//     position (perm) in slice-column-major order; padding gets perm = -1.
+// Values are then gathered through perm (k_halo_gather*), so a factor's values
+// or an operator's (a, e) pairs share one pattern build.
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+#include "runtime.cuh"
+
+namespace mpg {
+namespace {
+
+constexpr int HB_THREADS = 256;
+constexpr int HB_SLICES = HALO_R / 32;
+
+// Sort keys[0..P) ascending in shared memory (P a power of two <= HALO_MAXNZ).
+__device__ void block_bitonic(int* keys, int P) {
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const int a = keys[i], b = keys[ixj];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            keys[i] = b;
+            keys[ixj] = a;
+          }
+        }
+      }
+    }
+  __syncthreads();
+}
+
+// Loads the block's columns, sorts them, compacts the unique ones into uniq
+// (returns their count, or -1 if the block has too many entries).
+__device__ int block_halo(const CsrView m, int r0, int r1, int* keys, int* uniq, int* scan) {
+  const int nz0 = m.rowptr[r0], nz1 = m.rowptr[r1];
+  const int cnt = nz1 - nz0;
+  if (cnt > HALO_MAXNZ) return -1;
+  int P = 1;
+  while (P < cnt) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) keys[i] = i < cnt ? m.colind[nz0 + i] : INT_MAX;
+  block_bitonic(keys, P);
+  // per-thread contiguous chunk: count heads, exclusive scan over threads, write
+  const int per = (P + blockDim.x - 1) / blockDim.x;
+  const int b = threadIdx.x * per, e = min(P, b + per);
+  int c = 0;
+  for (int i = b; i < e; ++i)
+    if (keys[i] != INT_MAX && (i == 0 || keys[i] != keys[i - 1])) ++c;
+  scan[threadIdx.x] = c;
+  __syncthreads();
+  for (int off = 1; off < blockDim.x; off <<= 1) {
+    const int v = threadIdx.x >= off ? scan[threadIdx.x - off] : 0;
+    __syncthreads();
+    scan[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int pos = scan[threadIdx.x] - c;
+  for (int i = b; i < e; ++i)
+    if (keys[i] != INT_MAX && (i == 0 || keys[i] != keys[i - 1])) uniq[pos++] = keys[i];
+  const int total = scan[blockDim.x - 1];
+  __syncthreads();
+  return total;
+}
+
+__global__ void __launch_bounds__(HB_THREADS) k_halo_count(CsrView m, int* halo_cnt, int* slice_w) {
+  __shared__ int keys[HALO_MAXNZ], uniq[HALO_MAXNZ], scan[HB_THREADS];
+  const int r0 = blockIdx.x * HALO_R, r1 = min(m.nrows, r0 + HALO_R);
+  const int total = block_halo(m, r0, r1, keys, uniq, scan);
+  if (threadIdx.x == 0) halo_cnt[blockIdx.x] = total;
+  if (threadIdx.x < HB_SLICES) {
+    int w = 0;
+    for (int r = r0 + threadIdx.x * 32; r < min(r1, r0 + threadIdx.x * 32 + 32); ++r)
+      w = max(w, m.rowptr[r + 1] - m.rowptr[r]);
+    slice_w[blockIdx.x * HB_SLICES + threadIdx.x] = w;
+  }
+}
+
+__global__ void __launch_bounds__(HB_THREADS) k_halo_fill(CsrView m, const int* hoff, const int* sptr, int* halo,
+                                                          unsigned short* lidx, int* perm) {
+  __shared__ int keys[HALO_MAXNZ], uniq[HALO_MAXNZ], scan[HB_THREADS];
+  const int r0 = blockIdx.x * HALO_R, r1 = min(m.nrows, r0 + HALO_R);
+  const int total = block_halo(m, r0, r1, keys, uniq, scan);
+  const int h0 = hoff[blockIdx.x];
+  for (int i = threadIdx.x; i < total; i += blockDim.x) halo[h0 + i] = uniq[i];
+  if (threadIdx.x >= HALO_R) return;
+  const int row = r0 + threadIdx.x;
+  const int slice = row >> 5, lane = row & 31;
+  const int e0 = sptr[slice], w = (sptr[slice + 1] - e0) >> 5;
+  int b = 0, len = 0;
+  if (row < r1) {
+    b = m.rowptr[row];
+    len = m.rowptr[row + 1] - b;
+  }
+  for (int j = 0; j < w; ++j) {
+    const int e = e0 + j * 32 + lane;
+    if (j < len) {
+      const int c = m.colind[b + j];
+      int lo = 0, hi = total - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (uniq[mid] < c) lo = mid + 1;
+        else hi = mid;
+      }
+      lidx[e] = static_cast<unsigned short>(lo);
+      perm[e] = b + j;
+    } else {
+      lidx[e] = 0;
+      perm[e] = -1;
+    }
+  }
+}
+
+__global__ void k_halo_gather(const int* perm, int64_t entries, const double* src, double* dst) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < entries; e += int64_t(gridDim.x) * blockDim.x) {
+    const int p = perm[e];
+    dst[e] = p >= 0 ? src[p] : 0.0;
+  }
+}
+
+__global__ void k_halo_gather2(const int* perm, int64_t entries, const double2* src, double2* dst) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < entries; e += int64_t(gridDim.x) * blockDim.x) {
+    const int p = perm[e];
+    dst[e] = p >= 0 ? src[p] : make_double2(0.0, 0.0);
+  }
+}
+
+}  // namespace
+
+HaloPatternPtr halo_pattern_build(const DevCsr& m) {
+  if (m.nrows < 1 || m.nrows != m.ncols || m.nnz == 0) return nullptr;
+  auto& c = ctx(m.device);
+  DeviceGuard g(m.device);
+  const int n = int(m.nrows);
+  const int nblocks = (n + HALO_R - 1) / HALO_R;
+  const int nslices = nblocks * (HALO_R / 32);
+  DBuf<int> cnt(m.device, size_t(nblocks)), widths(m.device, size_t(nslices));
+  k_halo_count<<<nblocks, HB_THREADS, 0, c.stream>>>(m.view(), cnt.get(), widths.get());
+  MPG_CHECK_LAUNCH();
+  std::vector<int> hc(static_cast<size_t>(nblocks));
+  std::vector<int> hw(static_cast<size_t>(nslices));
+  MPG_CUDA(cudaMemcpyAsync(hc.data(), cnt.get(), hc.size() * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  MPG_CUDA(cudaMemcpyAsync(hw.data(), widths.get(), hw.size() * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  MPG_CUDA(cudaStreamSynchronize(c.stream));
+  auto p = std::make_shared<HaloPattern>();
+  std::vector<int> hoff(static_cast<size_t>(nblocks) + 1, 0);
+  std::vector<int> sptr(static_cast<size_t>(nslices) + 1, 0);
+  for (int b = 0; b < nblocks; ++b) {
+    if (hc[size_t(b)] < 0 || hc[size_t(b)] > HALO_MAX) return nullptr;
+    hoff[size_t(b) + 1] = hoff[size_t(b)] + hc[size_t(b)];
+    p->max_halo = std::max(p->max_halo, hc[size_t(b)]);
+  }
+  int64_t ent = 0;
+  for (int s = 0; s < nslices; ++s) {
+    ent += int64_t(hw[size_t(s)]) * 32;
+    if (ent >= INT_MAX) return nullptr;
+    sptr[size_t(s) + 1] = int(ent);
+  }
+  // the padding must stay small: the SpMV streams every padded entry
+  if (double(ent) > 1.25 * double(m.nnz) + 32.0 * nslices) return nullptr;
+  p->nrows = n;
+  p->nblocks = nblocks;
+  p->entries = ent;
+  p->hoff = DBuf<int>(m.device, hoff.size());
+  p->sptr = DBuf<int>(m.device, sptr.size());
+  p->halo = DBuf<int>(m.device, size_t(std::max(1, hoff.back())));
+  p->perm = DBuf<int>(m.device, size_t(std::max<int64_t>(1, ent)));
+  p->lidx = DBuf<unsigned short>(m.device, size_t(std::max<int64_t>(1, ent)));
+  MPG_CUDA(cudaMemcpyAsync(p->hoff.get(), hoff.data(), hoff.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  MPG_CUDA(cudaMemcpyAsync(p->sptr.get(), sptr.data(), sptr.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  k_halo_fill<<<nblocks, HB_THREADS, 0, c.stream>>>(m.view(), p->hoff.get(), p->sptr.get(), p->halo.get(),
+                                                    p->lidx.get(), p->perm.get());
+  MPG_CHECK_LAUNCH();
+  MPG_CUDA(cudaStreamSynchronize(c.stream));
+  return p;
+}
+
+const HaloPattern* halo_of(const DevCsr& m, HaloView* view) {
+  std::scoped_lock l(m.mu);
+  if (!m.halo_tried) {
+    m.halo_tried = true;
+    m.halo = halo_pattern_build(m);
+    if (m.halo) {
+      auto& c = ctx(m.device);
+      DeviceGuard g(m.device);
+      m.halo_val = DBuf<double>(m.device, size_t(std::max<int64_t>(1, m.halo->entries)));
+      k_halo_gather<<<std::max(1, c.sm_count * 8), 256, 0, c.stream>>>(m.halo->perm.get(), m.halo->entries,
+                                                                       m.val.get(), m.halo_val.get());
+      MPG_CHECK_LAUNCH();
+    }
+  }
+  if (!m.halo) return nullptr;
+  if (view) {
+    const HaloPattern& p = *m.halo;
+    *view = HaloView{p.nrows, p.hoff.get(), p.halo.get(), p.sptr.get(), p.lidx.get(), m.halo_val.get(), nullptr};
+  }
+  return m.halo.get();
+}
+
+const HaloPattern* halo_of_op(const ShiftedOp& op, bool transpose, HaloView* view) {
+  const DevCsr& a = transpose ? *op.at : *op.a;
+  HaloView av{};
+  const HaloPattern* p = halo_of(a, &av);
+  if (!p) return nullptr;
+  if (op.emode == E_SAMEPAT) {
+    std::scoped_lock l(op.halo_mu);
+    const int t = transpose ? 1 : 0;
+    if (!op.halo_tried[t]) {
+      op.halo_tried[t] = true;
+      auto& c = ctx(op.device);
+      DeviceGuard g(op.device);
+      op.halo_ae[t] = DBuf<double2>(op.device, size_t(std::max<int64_t>(1, p->entries)));
+      k_halo_gather2<<<std::max(1, c.sm_count * 8), 256, 0, c.stream>>>(
+          p->perm.get(), p->entries, transpose ? op.ae_t.get() : op.ae.get(), op.halo_ae[t].get());
+      MPG_CHECK_LAUNCH();
+    }
+    av.val2 = op.halo_ae[t].get();
+  } else if (op.emode == E_GENERAL) {
+    return nullptr;
+  }
+  if (view) *view = av;
+  return p;
+}
+
+}  // namespace mpg

@@ -93,6 +93,38 @@ struct CsrView {
   int nrows, ncols;
 };
 
+// Halo-staged sliced ELL (spmv.cu halo_*; the multi-RHS SpMV of the run-mode
+// groups in gmres.cu). Rows in blocks of HALO_R; per block the sorted unique
+// columns its rows touch (the halo, staged once into shared memory per SpMV)
+// and, per 32-row slice, the entries column-major (entry j of lane l at
+// sptr[slice] + 32 j + l) with 16-bit local indices into the block's halo.
+// The matrix stream is then 2 B of index + the value per entry, coalesced, and
+// the x-gather reads shared memory instead of L1/L2. Built once per pattern on
+// the device; a pattern whose blocks exceed HALO_MAXNZ entries or HALO_MAX
+// halo columns gets none (the CSR kernels run instead).
+constexpr int HALO_R = 128;
+constexpr int HALO_MAX = 1536;
+constexpr int HALO_MAXNZ = 4096;
+constexpr int HALO_XSTRIDE = 5;  // double2 per staged x row (4 used, 1 pad: conflict-free 16 B reads)
+struct HaloPattern {
+  int nrows = 0, nblocks = 0, max_halo = 0;
+  int64_t entries = 0;
+  DBuf<int> hoff, halo, sptr, perm;  // [nblocks + 1], [hoff.back()], [nslices + 1], [entries] (-1: padding)
+  DBuf<unsigned short> lidx;         // [entries]
+};
+using HaloPatternPtr = std::shared_ptr<const HaloPattern>;
+struct HaloView {
+  int nrows;
+  const int* hoff;
+  const int* halo;
+  const int* sptr;
+  const unsigned short* lidx;
+  const double* val;    // one value per entry (a matrix or factor)
+  const double2* val2;  // (a, e) per entry (E sharing A's pattern)
+};
+struct DevCsr;
+HaloPatternPtr halo_pattern_build(const DevCsr& m);  // nullptr if the pattern does not fit
+
 struct DevCsr {
   int device = 0;
   int64_t nrows = 0, ncols = 0, nnz = 0;
@@ -103,8 +135,13 @@ struct DevCsr {
   bool is_diag = false;
   mutable std::mutex mu;
   mutable std::shared_ptr<DevCsr> tcache;  // transpose, built on first use
+  mutable bool halo_tried = false;          // halo pattern + this matrix's values in it, built on first use
+  mutable HaloPatternPtr halo;
+  mutable DBuf<double> halo_val;
   CsrView view() const { return {rowptr.get(), colind.get(), val.get(), int(nrows), int(ncols)}; }
 };
+// The halo layout of m with m's own values (nullptr: not eligible); cached on m.
+const HaloPattern* halo_of(const DevCsr& m, HaloView* view);
 using CsrPtr = std::shared_ptr<DevCsr>;
 
 // Builders (spmv.cu).
@@ -131,10 +168,16 @@ struct ShiftedOp {
   DBuf<double> ediag;
   DBuf<double2> ae, ae_t;
   int vec_width = 32;  // sub-warp width for this operator's rows
+  mutable std::mutex halo_mu;
+  mutable bool halo_tried[2] = {false, false};
+  mutable DBuf<double2> halo_ae[2];  // (a, e) in the halo layout of A / A^T (E_SAMEPAT)
   OpView view(bool transpose) const;
 };
 using OpPtr = std::shared_ptr<ShiftedOp>;
 OpPtr op_create(const CsrPtr& a, const CsrPtr& e);
+// The halo layout of the operator side (A's pattern; values of A, or (a, e)
+// pairs for E_SAMEPAT); nullptr if not eligible.
+const HaloPattern* halo_of_op(const ShiftedOp& op, bool transpose, HaloView* view);
 
 // Explicit unit matrix sigma E - A (or its 2n pair form) on the device.
 CsrPtr op_explicit(const ShiftedOp& op, double sre, double sim, bool transpose);

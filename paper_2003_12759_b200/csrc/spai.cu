@@ -27,6 +27,9 @@
 #include <cmath>
 #include <cfloat>
 
+#include <climits>
+#include <string>
+
 #include "runtime.cuh"
 
 namespace mpg {
@@ -59,6 +62,9 @@ struct SpaiParams {
   int* ofb;        // fallback flags
   int* next;       // work counter
   const int* fixed_J;  // spai_column_solve: fixed sorted pattern for column `only_col`
+  const int* ipat;     // pattern_kind 2: initial pattern of column j at ipat[j * istride], icnt[j] entries
+  const int* icnt;
+  int istride;
   int fixed_np, only_col, raw;
 };
 
@@ -337,6 +343,154 @@ __device__ __noinline__ double residual_on_I(const SpaiParams& P, const WarpWS& 
   return wsum(s);
 }
 
+// ---- PatternOfAPow initial patterns (spai.cpp:55-71) --------------------------------
+// Column col's pattern is {col} and every row reachable from col in 1..k
+// expansions "row i of column j" (the structural support of A e_col, ..., A^k
+// e_col), sorted, truncated to the lowest max_fill indices with the diagonal
+// kept (spai.cpp:74-85). One CTA per column: each expansion gathers the
+// frontier's column supports into shared memory, sorts them (bitonic), keeps
+// the entries not seen before as the next frontier and merges them into the
+// seen set. A column whose expansion exceeds the shared-memory bounds raises
+// an overflow flag (ConfigError on the host).
+constexpr int AP_THREADS = 256, AP_CAND = 4096, AP_SEEN = 2048;
+
+__device__ void ap_bitonic(int* keys, int P) {
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const int a = keys[i], b = keys[ixj];
+          if ((a > b) == ((i & k) == 0)) {
+            keys[i] = b;
+            keys[ixj] = a;
+          }
+        }
+      }
+    }
+  __syncthreads();
+}
+
+__device__ bool ap_contains(const int* a, int n, int x) {
+  const int pos = lower_bound_i(a, n, x);
+  return pos < n && a[pos] == x;
+}
+
+__global__ void __launch_bounds__(AP_THREADS) k_apow_pattern(CsrView at, int power, int max_fill, int* ipat, int* icnt,
+                                                              int* overflow) {
+  __shared__ int cand[AP_CAND], seen[AP_SEEN], front[AP_SEEN], scan[AP_THREADS];
+  __shared__ int s_nfront, s_nseen, s_total, s_bad;
+  for (int col = blockIdx.x; col < at.nrows; col += gridDim.x) {
+    if (threadIdx.x == 0) {
+      front[0] = col;
+      s_nfront = 1;
+      s_nseen = 0;
+      s_bad = 0;
+    }
+    __syncthreads();
+    for (int step = 0; step < max(power, 1); ++step) {
+      const int nfront = s_nfront, nseen = s_nseen;
+      if (nfront == 0) break;
+      // gather the frontier's column supports (rows of A(:, j) = row j of A^T)
+      if (threadIdx.x == 0) {
+        int t = 0;
+        for (int f = 0; f < nfront; ++f) t += at.rowptr[front[f] + 1] - at.rowptr[front[f]];
+        s_total = t;
+      }
+      __syncthreads();
+      const int total = s_total;
+      if (total > AP_CAND) {
+        if (threadIdx.x == 0) s_bad = 1;
+        __syncthreads();
+        break;
+      }
+      if (threadIdx.x == 0) {
+        int o = 0;
+        for (int f = 0; f < nfront; ++f) {
+          const int b = at.rowptr[front[f]], e = at.rowptr[front[f] + 1];
+          for (int q = b; q < e; ++q) cand[o++] = at.colind[q];
+        }
+      }
+      __syncthreads();
+      int P = 1;
+      while (P < total) P <<= 1;
+      for (int i = total + threadIdx.x; i < P; i += blockDim.x) cand[i] = INT_MAX;
+      ap_bitonic(cand, P);
+      // unique candidates not seen before -> the next frontier
+      const int per = (P + blockDim.x - 1) / blockDim.x;
+      const int b = threadIdx.x * per, e = min(P, b + per);
+      int c = 0;
+      for (int i = b; i < e; ++i)
+        if (cand[i] != INT_MAX && (i == 0 || cand[i] != cand[i - 1]) && !ap_contains(seen, nseen, cand[i])) ++c;
+      scan[threadIdx.x] = c;
+      __syncthreads();
+      for (int off = 1; off < blockDim.x; off <<= 1) {
+        const int v = threadIdx.x >= off ? scan[threadIdx.x - off] : 0;
+        __syncthreads();
+        scan[threadIdx.x] += v;
+        __syncthreads();
+      }
+      const int nnew = scan[blockDim.x - 1];
+      if (nseen + nnew > AP_SEEN) {
+        if (threadIdx.x == 0) s_bad = 1;
+        __syncthreads();
+        break;
+      }
+      int pos = scan[threadIdx.x] - c;
+      for (int i = b; i < e; ++i)
+        if (cand[i] != INT_MAX && (i == 0 || cand[i] != cand[i - 1]) && !ap_contains(seen, nseen, cand[i]))
+          front[pos++] = cand[i];
+      __syncthreads();
+      // seen <- sorted(seen U front)
+      for (int i = threadIdx.x; i < nnew; i += blockDim.x) cand[i] = front[i];
+      for (int i = threadIdx.x; i < nseen; i += blockDim.x) cand[nnew + i] = seen[i];
+      int Q = 1;
+      while (Q < nseen + nnew) Q <<= 1;
+      for (int i = nseen + nnew + threadIdx.x; i < Q; i += blockDim.x) cand[i] = INT_MAX;
+      ap_bitonic(cand, Q);
+      for (int i = threadIdx.x; i < nseen + nnew; i += blockDim.x) seen[i] = cand[i];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        s_nseen = nseen + nnew;
+        s_nfront = nnew;
+      }
+      __syncthreads();
+    }
+    if (s_bad) {
+      if (threadIdx.x == 0) atomicExch(overflow, 1);
+      __syncthreads();
+      continue;
+    }
+    // pattern = seen U {col}, the lowest max_fill indices with col kept
+    if (threadIdx.x == 0) {
+      const int ns = s_nseen;
+      const bool has = ap_contains(seen, ns, col);
+      const int tot = ns + (has ? 0 : 1);
+      const int keep = min(tot, max_fill);
+      int* out = ipat + size_t(col) * max_fill;
+      int o = 0, i = 0;
+      bool placed = has;
+      while (o < keep) {
+        if (!placed && (i >= ns || col < seen[i])) {
+          out[o++] = col;
+          placed = true;
+        } else {
+          out[o++] = seen[i++];
+        }
+      }
+      if (!ap_contains(out, keep, col)) {  // truncated past the diagonal: it replaces the largest kept index
+        out[keep - 1] = col;
+        for (int q = keep - 1; q > 0 && out[q] < out[q - 1]; --q) {
+          const int t = out[q]; out[q] = out[q - 1]; out[q - 1] = t;
+        }
+      }
+      icnt[col] = keep;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(128) k_spai(SpaiParams P) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -403,6 +557,9 @@ __global__ void __launch_bounds__(128) k_spai(SpaiParams P) {
       } else if (P.pattern_kind == 0) {
         if (lane == 0) w.J[0] = col;
         np = 1;
+      } else if (P.pattern_kind == 2) {
+        np = P.icnt[col];
+        for (int i = lane; i < np; i += 32) w.J[i] = P.ipat[size_t(col) * P.istride + i];
       } else {
         // merge the sorted column rows with col
         const int len = e - b;
@@ -610,7 +767,6 @@ SpaiOutcome spai_or_update(const CsrPtr& a, const CsrPtr& prev, const SpaiOption
   if (prev && (prev->nrows != a->nrows || prev->ncols != a->ncols)) throw std::invalid_argument("update_build: shape mismatch");
   if (o.fill_tol < 0.0 || o.max_fill_per_col < 1 || o.max_pattern_sweeps < 0)
     throw std::invalid_argument("spai_build: invalid configuration");
-  if (o.pattern_kind == 2) throw ConfigError("spai: the A^k initial pattern is not supported on the GPU path");
   const int dev = a->device;
   auto& c = ctx(dev);
   DeviceGuard g(dev);
@@ -627,7 +783,28 @@ SpaiOutcome spai_or_update(const CsrPtr& a, const CsrPtr& prev, const SpaiOption
   CsrPtr pt = prev ? csr_transpose_cached(prev) : nullptr;
   const int maxcol = at->max_row;
   const int maxrhs = pt ? pt->max_row : 1;
-  const int pinit = o.pattern_kind == 0 ? 1 : maxcol + 1;
+  // PatternOfAPow: the initial patterns are built first, on the device
+  DBuf<int> ipat, icnt;
+  int pinit = o.pattern_kind == 0 ? 1 : maxcol + 1;
+  if (o.pattern_kind == 2) {
+    ipat = DBuf<int>(dev, size_t(n) * size_t(o.max_fill_per_col));
+    icnt = DBuf<int>(dev, size_t(n));
+    DBuf<int> ovf(dev, 1);
+    MPG_CUDA(cudaMemsetAsync(ovf.get(), 0, sizeof(int), s));
+    k_apow_pattern<<<unsigned(std::min(n, c.sm_count * 8)), AP_THREADS, 0, s>>>(at->view(), o.power,
+                                                                                o.max_fill_per_col, ipat.get(),
+                                                                                icnt.get(), ovf.get());
+    MPG_CHECK_LAUNCH();
+    count_launch();
+    int bad = 0;
+    MPG_CUDA(cudaMemcpyAsync(&bad, ovf.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    MPG_CUDA(cudaStreamSynchronize(s));
+    if (bad)
+      throw ConfigError("spai: the A^" + std::to_string(o.power) + " pattern of a column exceeds " +
+                        std::to_string(AP_SEEN) + " rows (or a frontier's supports " + std::to_string(AP_CAND) +
+                        " entries) on the GPU path");
+    pinit = o.max_fill_per_col;
+  }
   const int PMAX = std::max(1, std::min(o.max_fill_per_col, pinit + o.max_pattern_sweeps));
   const int64_t imax64 = std::min<int64_t>(n, int64_t(PMAX) * std::max(maxcol, 1));
   const int IMAX = int(std::max<int64_t>(imax64, 1));
@@ -680,6 +857,9 @@ SpaiOutcome spai_or_update(const CsrPtr& a, const CsrPtr& prev, const SpaiOption
   P.fixed_J = nullptr;
   P.only_col = -1;
   P.raw = 0;
+  P.ipat = ipat.get();
+  P.icnt = icnt.get();
+  P.istride = o.max_fill_per_col;
   k_spai<<<unsigned(warps / 4), 128, 0, s>>>(P);
   MPG_CHECK_LAUNCH();
   count_launch();

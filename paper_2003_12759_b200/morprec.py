@@ -279,16 +279,19 @@ class GmresResult:
 
 @dataclasses.dataclass
 class SpaiConfig:
-    """SpaiConfig (proj/include/morprec/spai.hpp:25-33); pattern 'diagonal' or 'a'."""
+    """SpaiConfig (proj/include/morprec/spai.hpp:15-33); pattern 'diagonal', 'a' (PatternOfA) or 'a_pow'
+    (PatternOfAPow: the support of A e_j, ..., A^power e_j)."""
     pattern: str = "a"
     fill_tol: float = 1e-4
     max_fill_per_col: int = 50
     max_pattern_sweeps: int = 3
     threads: int = 1
+    power: int = 2
 
     def c(self) -> L.SpaiCfg:
         kind = {"diagonal": 0, "a": 1, "a_pow": 2}[self.pattern]
-        return L.SpaiCfg(kind, 2, self.fill_tol, self.max_fill_per_col, self.max_pattern_sweeps, self.threads)
+        return L.SpaiCfg(kind, self.power, self.fill_tol, self.max_fill_per_col, self.max_pattern_sweeps,
+                         self.threads)
 
 
 class PrecondChain:

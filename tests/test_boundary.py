@@ -158,3 +158,46 @@ def test_cpp_mirror_header_compiles_and_links(mpg, tmp_path):
                     os.path.join(ROOT, "tests", "cpp", "cpp_api_demo.cpp"), "-L", libdir, "-lmpg",
                     f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
     assert exe.exists()
+
+
+_EXC_SRC = r"""
+#include <cstdio>
+#include <typeinfo>
+#include "morprec_gpu.hpp"
+template <class E> int expect(int status) {
+  try { morprec_gpu::check(status); } catch (const E&) { return 0; } catch (...) { return 1; }
+  return 1;
+}
+int main() {
+  int bad = 0;
+  bad += expect<morprec::ConfigError>(MPG_ERR_CONFIG);
+  bad += expect<morprec::SolverError>(MPG_ERR_SOLVER);
+  bad += expect<morprec::IoError>(MPG_ERR_IO);
+  bad += expect<std::invalid_argument>(MPG_ERR_INVALID);
+  bad += expect<morprec_gpu::DeviceError>(MPG_ERR_CUDA);
+  bad += expect<std::bad_alloc>(MPG_ERR_NOMEM);
+  std::printf("%d\n", bad);
+  return bad;
+}
+"""
+
+
+@pytest.mark.parametrize("with_reference_header", [False, True])
+def test_cpp_mirror_throws_the_reference_exception_classes(tmp_path, with_reference_header):
+    """morprec_gpu::check maps status codes to morprec::ConfigError / SolverError /
+    IoError (errors.hpp:12-28; main.cpp:476-491 exit codes 2/3/4): the reference's
+    own classes when its include/ is on the path, identical declarations otherwise."""
+    import subprocess
+    ref_inc = "/root/reference/proj/include"
+    if with_reference_header and not os.path.exists(os.path.join(ref_inc, "morprec", "errors.hpp")):
+        pytest.skip("reference tree not present (GPU box)")
+    src = tmp_path / "exc.cpp"
+    src.write_text(_EXC_SRC)
+    exe = tmp_path / "exc"
+    cmd = ["g++", "-std=c++17", "-O0", str(src), "-I", os.path.join(ROOT, "include"), "-o", str(exe),
+           "-L", os.path.join(ROOT, "paper_2003_12759_b200"), "-lmpg", "-Wl,-rpath," + os.path.join(ROOT, "paper_2003_12759_b200")]
+    if with_reference_header:
+        cmd[4:4] = ["-I", ref_inc]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0 and out.stdout.strip() == "0", out.stdout + out.stderr

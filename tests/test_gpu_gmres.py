@@ -205,3 +205,35 @@ def test_gram_schmidt_kernel_variants_agree(mpg, gen, monkeypatch, env):
     assert g.report.converged and abs(g.report.iterations - base.report.iterations) <= 1
     assert rel(g.x, base.x) <= 1e-8
     assert np.linalg.norm(d * g.x - b) <= 1e-10 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("cfgname", ["c3", "c2", "c5"])
+def test_halo_sell_spmv_matches_csr_kernels(mpg, gen, monkeypatch, cfgname):
+    """The run-mode multi-RHS SpMVs in the halo-staged sliced-ELL layout (27-point
+    FEM with E sharing A's pattern, 7-point with diagonal E) give the CSR
+    kernels' solves (MPG_SPMV_CSR) on 8-solve groups of both sides; on a
+    Zipf(1.8) pattern with rows up to 600 entries (blocks past HALO_MAXNZ) the
+    layout is declined and the CSR kernels run."""
+    if cfgname == "c3":
+        s = gen.config3(20)
+    elif cfgname == "c2":
+        s = gen.config2(M=24)
+    else:
+        s = gen.config5(n=6000, max_len=600)
+    ec = s.e_csr()
+    op = mpg.ShiftedOperator(_m(mpg, s.a), _m(mpg, ec))
+    sig0 = 0.5 if cfgname != "c5" else 1.0
+    pv = mpg.PrecondChain(mpg.spai_build(op.explicit(sig0, False)).p)
+    pw = mpg.PrecondChain(mpg.spai_build(op.explicit(sig0, True)).p)
+    sig = [float(x) for x in np.logspace(-2, 1, 8)] * 2
+    trs = [0] * 8 + [1] * 8
+    chains = [pv] * 8 + [pw] * 8
+    bs = [s.b[:, 0] * (1 + 0.1 * i) for i in range(8)] + [s.c[:, 0] * (1 + 0.1 * i) for i in range(8)]
+    cfg = mpg.GmresConfig(rel_tol=1e-10)
+    halo = mpg.gmres_batch(op, sig, bs, chains=chains, transposes=trs, cfg=cfg)
+    monkeypatch.setenv("MPG_SPMV_CSR", "1")
+    csr = mpg.gmres_batch(op, sig, bs, chains=chains, transposes=trs, cfg=cfg)
+    for h, c in zip(halo, csr):
+        assert h.report.converged and c.report.converged
+        assert abs(h.report.iterations - c.report.iterations) <= 1
+        assert rel(h.x, c.x) <= 1e-8

@@ -100,7 +100,8 @@ def test_chain_prefix_sharing(mpg, gen):
 def test_spai_build_matches_oracle(mpg, orc, gen, seed, n, dens, shift):
     h = gen.random_sparse(n, n, dens, seed, shift)
     g, o = _pair(gen, h)
-    for cfg_kw in ({}, dict(fill_tol=1e-2, max_pattern_sweeps=6), dict(pattern="diagonal")):
+    for cfg_kw in ({}, dict(fill_tol=1e-2, max_pattern_sweeps=6), dict(pattern="diagonal"),
+                   dict(pattern="a_pow", power=2), dict(pattern="a_pow", power=3, max_fill_per_col=24)):
         gr = mpg.spai_build(g, mpg.SpaiConfig(**cfg_kw))
         op_, ores, ofb, _ = orc.spai_build(o, orc.SpaiConfig(**cfg_kw))
         assert gr.fallback_count == ofb
@@ -157,3 +158,58 @@ def test_spai_column_solve(mpg, orc, gen):
         rows, vals, res, rd = mpg.spai_column_solve(g, j, full)
         r2, v2, res2, rd2 = orc.spai_column_solve(o, j, full)
         assert rel(vals, v2) <= 1e-10 and res == pytest.approx(res2, abs=1e-12) and rd == rd2
+
+
+@pytest.mark.parametrize("case", ["random", "c1_chain", "c3_pair"])
+def test_standard_residual_matches_oracle(mpg, orc, gen, case):
+    """standard_residual (chain.cpp:140-157): ||I - A P||_F / sqrt(n) by n probes,
+    P the whole chain -- the GPU value against the oracle's on the same matrices:
+    a random sparse matrix with its SPAI, a C1 operator with a fresh SPAI plus
+    two update factors, and a C3 complex-pair (2n) unit with its SPAI."""
+    if case == "random":
+        h = gen.random_sparse(40, 40, 0.15, 7, 4.0)
+        g, o = _pair(gen, h)
+        gch = mpg.PrecondChain(mpg.spai_build(g).p)
+        och = orc.Chain(orc.spai_build(o)[0])
+    elif case == "c1_chain":
+        s = gen.config1(N=14)
+        ec = s.e_csr()
+        A, E = orc.Csr.of(s.a), orc.Csr.of(ec)
+        op = mpg.ShiftedOperator(_pair(gen, s.a)[0], _pair(gen, ec)[0])
+        mats_g = [op.explicit(x) for x in (0.1, 0.3, 0.9)]
+        mats_o = [orc.kron_assemble(orc.shifted(x), A, E, cap=10 ** 9) for x in (0.1, 0.3, 0.9)]
+        gch = mpg.PrecondChain(mpg.spai_build(mats_g[0]).p)
+        och = orc.Chain(orc.spai_build(mats_o[0])[0])
+        for i in (1, 2):
+            gch = gch.extended(mpg.update_build(mats_g[i - 1], mats_g[i]))
+            och = och.extended(orc.update_build(mats_o[i - 1], mats_o[i])[0])
+        g, o = mats_g[2], mats_o[2]
+    else:
+        s = gen.config3(6)
+        op = mpg.ShiftedOperator(_pair(gen, s.a)[0], _pair(gen, s.e)[0])
+        g = op.explicit(complex(0.7, 0.4))
+        o = orc.kron_assemble(orc.shifted(complex(0.7, 0.4)), orc.Csr.of(s.a), orc.Csr.of(s.e), cap=10 ** 9)
+        gch = mpg.PrecondChain(mpg.spai_build(g).p)
+        och = orc.Chain(orc.spai_build(o)[0])
+    gv = mpg.standard_residual(g, gch)
+    ov = orc.standard_residual(o, och)
+    assert ov > 0 and abs(gv - ov) <= 1e-10 * ov, (gv, ov)
+
+
+@pytest.mark.parametrize("power,fill", [(2, 50), (3, 50), (2, 12)])
+def test_spai_a_pow_pattern_on_fem_matches_oracle(mpg, orc, gen, power, fill):
+    """PatternOfAPow (spai.cpp:55-85) on a C3-type operator (27-point rows, so
+    the A^2 support of a column passes max_fill_per_col and is truncated to the
+    lowest indices with the diagonal kept): pattern bitwise, values 1e-10."""
+    s = gen.config3(7)
+    op = mpg.ShiftedOperator(_pair(gen, s.a)[0], _pair(gen, s.e)[0])
+    g = op.explicit(0.3)
+    o = orc.kron_assemble(orc.shifted(0.3), orc.Csr.of(s.a), orc.Csr.of(s.e), cap=10 ** 9)
+    kw = dict(pattern="a_pow", power=power, max_fill_per_col=fill)
+    gr = mpg.spai_build(g, mpg.SpaiConfig(**kw))
+    op_, ores, ofb, _ = orc.spai_build(o, orc.SpaiConfig(**kw))
+    assert gr.fallback_count == ofb
+    assert np.array_equal(gr.p.download()[0], op_.export()[0])
+    assert np.array_equal(gr.p.download()[1], op_.export()[1])
+    assert rel(gr.p.download()[2], op_.export()[2]) <= 1e-10
+    assert rel(gr.column_residuals, ores) <= 1e-10
