@@ -52,6 +52,12 @@ class GmresRep(C.Structure):
                 ("reorth_passes", C.c_int)]
 
 
+class AirgaCfgO(C.Structure):
+    _fields_ = [("r_max", C.c_int), ("outer_tol", C.c_double), ("inner_tol", C.c_double), ("max_outer", C.c_int),
+                ("gmres", GmresCfg), ("spai", SpaiCfg), ("max_chain_len", C.c_int),
+                ("standard_residual_max_dim", C.c_longlong)]
+
+
 class IrkaCfg(C.Structure):
     _fields_ = [("r", C.c_int), ("tol", C.c_double), ("max_sweeps", C.c_int), ("decoupled", C.c_int),
                 ("seed", C.c_ulonglong), ("gmres", GmresCfg), ("spai", SpaiCfg), ("max_chain_len", C.c_int),
@@ -66,6 +72,11 @@ class ReportRow(C.Structure):
 
 
 _SIGS = {
+    "orc_airga_reduce": (C.c_int, [vp, vp, vp, vp, C.c_int, vp, C.c_int, C.c_double, C.c_double, vp, C.c_int, vp,
+                                   C.c_int, C.POINTER(C.c_int)] + [vp] * 7 + [C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                                                             vp, C.c_int, C.POINTER(C.c_int)]),
+    "orc_update_expansion_points": (C.c_int, [vp, vp, vp, C.c_int, vp, C.c_int, vp]),
+    "orc_h2_norm": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, dp]),
     "orc_last_error": (C.c_char_p, []),
     "orc_csr_from_csr": (C.c_int, [C.c_longlong, C.c_longlong, vp, vp, vp, C.POINTER(vp)]),
     "orc_csr_from_triplets": (C.c_int, [C.c_longlong, C.c_longlong, C.c_longlong, vp, vp, vp, C.POINTER(vp)]),
@@ -730,3 +741,66 @@ def kron_assemble_coupled(lam, k: Csr, couplers) -> Csr:
     """assemble_explicit with couplers (kron.cpp:72-131), no cap."""
     return _kron_coupled(lam, k, couplers, assemble=True)
 
+
+
+@dataclasses.dataclass
+class AirgaResultO:
+    m: np.ndarray
+    d: np.ndarray
+    k: np.ndarray
+    f: np.ndarray
+    c: np.ndarray
+    final_points: list
+    point_history: list
+    sweeps: int
+    converged: bool
+    rows: list
+
+    def transfer(self, s: complex) -> np.ndarray:
+        return self.c.T @ np.linalg.solve(s * s * self.m + s * self.d + self.k, self.f)
+
+
+def airga_reduce(m: Csr, d: Csr, k: Csr, f, c, points, r_max: int = 20, outer_tol: float = 1e-4,
+                 inner_tol: float = 1e-6, max_outer: int = 20, gmres: GmresConfig = None, spai: SpaiConfig = None,
+                 mode: int = 2, max_chain_len: int = 16, alpha: float = 0.0, beta: float = 0.0) -> AirgaResultO:
+    """airga_reduce (proj/src/airga.cpp:136-317) on the oracle, with every sweep's expansion points."""
+    n = m.shape[0]
+    fm = np.asfortranarray(np.asarray(f, dtype=np.float64).reshape(n, -1))
+    cm = np.asfortranarray(np.asarray(c, dtype=np.float64).reshape(n, -1))
+    pts = _f64(points)
+    cfg = AirgaCfgO(r_max, outer_tol, inner_tol, max_outer, (gmres or GmresConfig()).c(), (spai or SpaiConfig()).c(),
+                    max_chain_len, 5000)
+    cap = max(1, r_max)
+    rm, rd, rk = (np.zeros(cap * cap) for _ in range(3))
+    rf, rc = np.zeros(cap * fm.shape[1]), np.zeros(cap * cm.shape[1])
+    fp = np.zeros(max(1, pts.size))
+    hist = np.zeros(max(1, pts.size) * max(1, max_outer))
+    order, sweeps, conv, nrows = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    maxrows = 2 * max(1, pts.size) * max(1, max_outer) + 4
+    rows = (ReportRow * maxrows)()
+    _check(lib.orc_airga_reduce(m._h, d._h, k._h, _p(fm), fm.shape[1], _p(cm), cm.shape[1], alpha, beta, _p(pts),
+                                pts.size, C.byref(cfg), mode, C.byref(order), _p(rm), _p(rd), _p(rk), _p(rf), _p(rc),
+                                _p(fp), _p(hist), C.byref(sweeps), C.byref(conv), rows, maxrows, C.byref(nrows)))
+    r = order.value
+    sq = lambda x: x[: r * r].reshape((r, r), order="F")
+    return AirgaResultO(sq(rm), sq(rd), sq(rk), rf[: r * fm.shape[1]].reshape((r, -1), order="F"),
+                        rc[: r * cm.shape[1]].reshape((r, -1), order="F"), fp[: pts.size].tolist(),
+                        [hist[z * pts.size:(z + 1) * pts.size].tolist() for z in range(sweeps.value)],
+                        sweeps.value, bool(conv.value), [rows[i] for i in range(min(nrows.value, maxrows))])
+
+
+def update_expansion_points(m, d, k, current) -> list:
+    """update_expansion_points (proj/src/airga.cpp:319-384)."""
+    mm, dd, kk = (np.asfortranarray(np.asarray(x, dtype=np.float64)) for x in (m, d, k))
+    cur = _f64(current)
+    out = np.zeros(max(1, cur.size))
+    _check(lib.orc_update_expansion_points(_p(mm), _p(dd), _p(kk), mm.shape[0], _p(cur), cur.size, _p(out)))
+    return out[: cur.size].tolist()
+
+
+def h2_norm(a, b, c) -> float:
+    """h2_norm (proj/src/h2.cpp:28-60); the Gramian by the matrix sign function."""
+    a, b, c = (np.asfortranarray(np.asarray(x, dtype=np.float64)) for x in (a, b, c))
+    out = C.c_double()
+    _check(lib.orc_h2_norm(_p(a), _p(b), _p(c), a.shape[0], b.shape[1], c.shape[0], C.byref(out)))
+    return out.value

@@ -425,6 +425,59 @@ int orc_transfer_function_error(const Csr* m, const Csr* d, const Csr* k, const 
   });
 }
 
+// airga_reduce (proj/src/airga.cpp:136-317). Outputs the reduced pencil
+// (order x order, column-major, capacity r_max), F_r (order x n_in), C_r
+// (order x n_out), the final points and every sweep's points (sweeps x ell).
+typedef struct {
+  int r_max; double outer_tol, inner_tol; int max_outer; orc_gmres_cfg gmres; orc_spai_cfg spai; int max_chain_len;
+  long long standard_residual_max_dim;
+} orc_airga_cfg;
+
+int orc_airga_reduce(const Csr* m, const Csr* d, const Csr* k, const double* f, int n_in, const double* c, int n_out,
+                     double alpha, double beta, const double* points, int npoints, const orc_airga_cfg* cfg, int mode,
+                     int* order, double* rm, double* rd, double* rk, double* rf, double* rc, double* final_points,
+                     double* point_history, int* sweeps, int* converged, orc_report_row* rows, int max_rows,
+                     int* nrows) {
+  return guard([&] {
+    const long long n = m->nrows;
+    AirgaConfigO ac;
+    ac.expansion_points.assign(points, points + npoints);
+    ac.r_max = cfg->r_max; ac.outer_tol = cfg->outer_tol; ac.inner_tol = cfg->inner_tol; ac.max_outer = cfg->max_outer;
+    ac.gmres = to_gmres(&cfg->gmres); ac.spai = to_spai(&cfg->spai); ac.max_chain_len = cfg->max_chain_len;
+    ac.standard_residual_max_dim = cfg->standard_residual_max_dim;
+    const AirgaResult res = airga_reduce(*m, *d, *k, dense_from(f, n, n_in), dense_from(c, n, n_out), alpha, beta, ac,
+                                         PrecondMode(mode));
+    const AirgaModel& md = res.model;
+    *order = int(md.m.rows);
+    auto put = [](double* dst, const Dense& x) { if (dst) std::memcpy(dst, x.a.data(), x.a.size() * sizeof(double)); };
+    put(rm, md.m); put(rd, md.d); put(rk, md.k); put(rf, md.f); put(rc, md.c);
+    if (final_points) std::copy(res.final_points.begin(), res.final_points.end(), final_points);
+    if (point_history)
+      for (size_t z = 0; z < res.point_history.size(); ++z)
+        std::copy(res.point_history[z].begin(), res.point_history[z].end(), point_history + z * size_t(npoints));
+    *sweeps = res.report.sweeps;
+    *converged = res.report.converged;
+    copy_rows(res.report, rows, max_rows, nrows);
+  });
+}
+
+int orc_update_expansion_points(const double* m, const double* d, const double* k, int r, const double* cur, int npts,
+                                double* out) {
+  return guard([&] {
+    const auto v = update_expansion_points(dense_from(m, r, r), dense_from(d, r, r), dense_from(k, r, r),
+                                           std::vector<double>(cur, cur + npts));
+    std::copy(v.begin(), v.end(), out);
+  });
+}
+
+// H2 norm of (A, B, C) (h2.cpp:28-60), infinity when A is not stable.
+int orc_h2_norm(const double* a, const double* b, const double* c, int ns, int ni, int no, double* out) {
+  return guard([&] {
+    StateSpaceO ss{dense_from(a, ns, ns), dense_from(b, ns, ni), dense_from(c, no, ns)};
+    *out = h2_norm_o(ss);
+  });
+}
+
 // BIRKA with couplings N_1..N_m (proj/src/birka.cpp:139-310): the joint n r
 // solve per side; outputs kr (r x r), nr (m blocks of r x r), fr, cr, lambda,
 // v, w (n x r), any output may be null.

@@ -302,6 +302,32 @@ Csr read_matrix_market(std::istream& in, const std::string& origin);
 Csr read_matrix_market_file(const std::string& path);
 void write_matrix_market(std::ostream& out, const Csr& a);
 
+// ---- AIRGA (proj/src/airga.cpp:136-384, h2.cpp, orth.cpp) -----------------
+struct StateSpaceO { Dense a, b, c; };
+double h2_norm_o(const StateSpaceO& sys);
+double h2_distance_o(const StateSpaceO& a, const StateSpaceO& b);
+struct AirgaConfigO {
+  std::vector<double> expansion_points;
+  int r_max = 20;
+  double outer_tol = 1e-4, inner_tol = 1e-6;
+  int max_outer = 20;
+  GmresConfig gmres{};
+  SpaiConfig spai{};
+  int max_chain_len = 16;
+  index_t standard_residual_max_dim = 5000;
+};
+struct AirgaModel { Dense m, d, k, f, c, basis; };
+struct AirgaResult {
+  AirgaModel model;
+  ReductionReport report;
+  std::vector<double> final_points;
+  std::vector<std::vector<double>> point_history;  // the expansion points of every sweep
+};
+std::vector<double> update_expansion_points(const Dense& m, const Dense& d, const Dense& k,
+                                            const std::vector<double>& current);
+AirgaResult airga_reduce(const Csr& m, const Csr& d, const Csr& k, const Dense& f, const Dense& c, double alpha,
+                         double beta, const AirgaConfigO& cfg, PrecondMode mode);
+
 // ---- second-order transfer error (proj/src/airga.cpp:80-85, :386-447) -----
 Csr shifted_operator2(const Csr& m, const Csr& d, const Csr& k, double s);
 std::vector<double> transfer_function_error(const Csr& m, const Csr& d, const Csr& k, const Dense& f, const Dense& c,

@@ -507,79 +507,72 @@ __global__ void __launch_bounds__(256) k_spmv_il2(GmSolve* S, Group grp, CsrView
 
 // Halo-staged sliced-ELL variant (runtime.cuh HaloPattern): one CTA per block
 // of HALO_R rows stages the block's halo of x (all MB right-hand sides, 64 B
-// per column, padded to 80 B so the 16-byte reads of 32 rows spread over the
-// banks) into shared memory once, then one thread per row walks its slice
+// per column, the four 16-byte chunks XOR-swizzled by the row so the reads of
+// 32 rows spread over the banks) into shared memory once with cp.async, then one thread per row walks its slice
 // column-major: the matrix stream is a coalesced 2-byte local index + the value
 // per entry and the x-gather never leaves the SM.
 template <int EM, bool CHAIN>
-__global__ void __launch_bounds__(HALO_R) k_spmv_halo(GmSolve* S, Group grp, HaloView hv, OpView op,
-                                                      const double* __restrict__ xin, double* __restrict__ xout) {
+__global__ void __launch_bounds__(4 * HALO_R) k_spmv_halo(GmSolve* S, Group grp, HaloView hv, OpView op,
+                                                          const double* __restrict__ xin, double* __restrict__ xout) {
   if (!il_any_run(S, grp)) return;
   extern __shared__ double2 xs[];
   const int blk = blockIdx.x;
   const int h0 = hv.hoff[blk], L = hv.hoff[blk + 1] - h0;
-  for (int t = threadIdx.x; t < L; t += HALO_R) {
-    const double2* src = reinterpret_cast<const double2*>(xin + size_t(__ldg(hv.halo + h0 + t)) * MB);
-    double2* dst = xs + t * HALO_XSTRIDE;
-    dst[0] = __ldg(src);
-    dst[1] = __ldg(src + 1);
-    dst[2] = __ldg(src + 2);
-    dst[3] = __ldg(src + 3);
+  // stage the halo with asynchronous 16-byte copies (all in flight at once);
+  // chunk h of halo row t lands in slot h ^ ((t >> 1) & 3) of the row so the
+  // 16-byte reads of 8 rows x 4 chunks spread over the banks
+  for (int i = threadIdx.x; i < 4 * L; i += 4 * HALO_R) {
+    const int t = i >> 2, h = i & 3;
+    const double* src = xin + size_t(__ldg(hv.halo + h0 + t)) * MB + 2 * h;
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(xs + t * 4 + (h ^ ((t >> 1) & 3))));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
   }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
-  const int row = blk * HALO_R + threadIdx.x;
+  // four threads per row, thread q of a row owns right-hand sides 2q, 2q + 1;
+  // a warp covers 8 consecutive rows, so each entry's index and value loads
+  // are 8 contiguous slots of the slice (one sector / one line per warp)
+  const int q = threadIdx.x & 3;
+  const int row = blk * HALO_R + (threadIdx.x >> 2);
   if (row >= hv.nrows) return;
   const int slice = row >> 5, lane = row & 31;
   const int e0 = __ldg(hv.sptr + slice), w = (__ldg(hv.sptr + slice + 1) - e0) >> 5;
-  double a[MB], ev[MB];
-#pragma unroll
-  for (int q = 0; q < MB; ++q) a[q] = ev[q] = 0.0;
-#pragma unroll 4
+  double a0 = 0.0, a1 = 0.0, g0 = 0.0, g1 = 0.0;
+#pragma unroll 8
   for (int j = 0; j < w; ++j) {
     const int e = e0 + j * 32 + lane;
-    const double2* xp = xs + int(__ldcs(hv.lidx + e)) * HALO_XSTRIDE;
+    const int li = int(__ldcs(hv.lidx + e));
+    const double2 x = xs[li * 4 + (q ^ ((li >> 1) & 3))];
     if (EM == E_SAMEPAT && !CHAIN) {
       const double2 v = __ldcs(hv.val2 + e);
-#pragma unroll
-      for (int h = 0; h < MB / 2; ++h) {
-        const double2 x = xp[h];
-        a[2 * h] = fma(v.x, x.x, a[2 * h]);
-        a[2 * h + 1] = fma(v.x, x.y, a[2 * h + 1]);
-        ev[2 * h] = fma(v.y, x.x, ev[2 * h]);
-        ev[2 * h + 1] = fma(v.y, x.y, ev[2 * h + 1]);
-      }
+      a0 = fma(v.x, x.x, a0);
+      a1 = fma(v.x, x.y, a1);
+      g0 = fma(v.y, x.x, g0);
+      g1 = fma(v.y, x.y, g1);
     } else {
       const double v = __ldcs(hv.val + e);
-#pragma unroll
-      for (int h = 0; h < MB / 2; ++h) {
-        const double2 x = xp[h];
-        a[2 * h] = fma(v, x.x, a[2 * h]);
-        a[2 * h + 1] = fma(v, x.y, a[2 * h + 1]);
-      }
+      a0 = fma(v, x.x, a0);
+      a1 = fma(v, x.y, a1);
     }
   }
   if (CHAIN) {
-    double2* yp = reinterpret_cast<double2*>(xout + size_t(row) * MB);
-#pragma unroll
-    for (int h = 0; h < MB / 2; ++h) yp[h] = make_double2(a[2 * h], a[2 * h + 1]);
+    reinterpret_cast<double2*>(xout + size_t(row) * MB)[q] = make_double2(a0, a1);
     return;
   }
   if (EM == E_IDENT || EM == E_DIAG) {
     const double dd = EM == E_DIAG ? op.ediag[row] : 1.0;
-    const double2* xr = reinterpret_cast<const double2*>(xin + size_t(row) * MB);
-#pragma unroll
-    for (int h = 0; h < MB / 2; ++h) {
-      const double2 x = xr[h];
-      ev[2 * h] = dd * x.x;
-      ev[2 * h + 1] = dd * x.y;
-    }
+    const double2 xr = reinterpret_cast<const double2*>(xin + size_t(row) * MB)[q];
+    g0 = dd * xr.x;
+    g1 = dd * xr.y;
   }
 #pragma unroll
-  for (int q = 0; q < MB; ++q) {
-    if (q >= grp.cnt) continue;
-    GmSolve& st = S[grp.idx[q]];
+  for (int h = 0; h < 2; ++h) {
+    const int qq = 2 * q + h;
+    if (qq >= grp.cnt) continue;
+    GmSolve& st = S[grp.idx[qq]];
     if (st.phase != PH_RUN) continue;
-    st.V[st.k + 1][vidx(row)] = st.scale[st.k] * (st.sre * ev[q] + st.ca * a[q]);
+    st.V[st.k + 1][vidx(row)] = st.scale[st.k] * (st.sre * (h ? g1 : g0) + st.ca * (h ? a1 : a0));
   }
 }
 
@@ -2295,7 +2288,9 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     // interleaved path: chain groups of real shifts on one operator side
     const bool il_on = !std::getenv("MPG_NO_IL");
     il2 = std::getenv("MPG_IL_NNZSPLIT") == nullptr;  // RHS split measured faster (C3: 256 -> 221 ms / 348 its)
-    use_halo = std::getenv("MPG_SPMV_CSR") == nullptr;  // halo-staged sliced ELL where the pattern fits
+    // halo-staged sliced ELL: opt-in (MPG_SPMV_HALO=1); measured slower than the
+    // CSR kernels on C3 (operator 309 -> 398-463 us, chain 168 -> 288 us per launch)
+    use_halo = std::getenv("MPG_SPMV_HALO") != nullptr && std::getenv("MPG_SPMV_CSR") == nullptr;
     std::vector<int> in_il(size_t(ns), 0);
     for (size_t gi = 0; gi < chain_groups.size(); ++gi) {
       const Group& g = chain_groups[gi];
@@ -2364,7 +2359,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         HaloView hv{};
         const HaloPattern* hp = use_halo ? halo_of(f, &hv) : nullptr;
         if (hp) {
-          k_spmv_halo<E_IDENT, true><<<hp->nblocks, HALO_R, size_t(hp->max_halo) * HALO_XSTRIDE * sizeof(double2), s>>>(
+          k_spmv_halo<E_IDENT, true><<<hp->nblocks, 4 * HALO_R, size_t(hp->max_halo) * HALO_XSTRIDE * sizeof(double2), s>>>(
               dS.get(), chain_groups[gi], hv, opn, xin, xout);
           ++launches_per_iter;
           mark(PK_CHAIN);
@@ -2424,9 +2419,9 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         if (hp) {
           const size_t sm = size_t(hp->max_halo) * HALO_XSTRIDE * sizeof(double2);
           switch (op.emode) {
-            case E_IDENT: k_spmv_halo<E_IDENT, false><<<hp->nblocks, HALO_R, sm, s>>>(dS.get(), g, hv, ov, xin, nullptr); break;
-            case E_DIAG: k_spmv_halo<E_DIAG, false><<<hp->nblocks, HALO_R, sm, s>>>(dS.get(), g, hv, ov, xin, nullptr); break;
-            default: k_spmv_halo<E_SAMEPAT, false><<<hp->nblocks, HALO_R, sm, s>>>(dS.get(), g, hv, ov, xin, nullptr); break;
+            case E_IDENT: k_spmv_halo<E_IDENT, false><<<hp->nblocks, 4 * HALO_R, sm, s>>>(dS.get(), g, hv, ov, xin, nullptr); break;
+            case E_DIAG: k_spmv_halo<E_DIAG, false><<<hp->nblocks, 4 * HALO_R, sm, s>>>(dS.get(), g, hv, ov, xin, nullptr); break;
+            default: k_spmv_halo<E_SAMEPAT, false><<<hp->nblocks, 4 * HALO_R, sm, s>>>(dS.get(), g, hv, ov, xin, nullptr); break;
           }
           ++launches_per_iter;
           mark(PK_OP);

@@ -11,6 +11,8 @@
 // or an operator's (a, e) pairs share one pattern build.
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "runtime.cuh"
@@ -73,8 +75,11 @@ __device__ int block_halo(const CsrView m, int r0, int r1, int* keys, int* uniq,
   return total;
 }
 
+constexpr size_t HB_SMEM = (2 * size_t(HALO_MAXNZ) + HB_THREADS) * sizeof(int);
+
 __global__ void __launch_bounds__(HB_THREADS) k_halo_count(CsrView m, int* halo_cnt, int* slice_w) {
-  __shared__ int keys[HALO_MAXNZ], uniq[HALO_MAXNZ], scan[HB_THREADS];
+  extern __shared__ int hb_sm[];
+  int *keys = hb_sm, *uniq = hb_sm + HALO_MAXNZ, *scan = hb_sm + 2 * HALO_MAXNZ;
   const int r0 = blockIdx.x * HALO_R, r1 = min(m.nrows, r0 + HALO_R);
   const int total = block_halo(m, r0, r1, keys, uniq, scan);
   if (threadIdx.x == 0) halo_cnt[blockIdx.x] = total;
@@ -88,7 +93,8 @@ __global__ void __launch_bounds__(HB_THREADS) k_halo_count(CsrView m, int* halo_
 
 __global__ void __launch_bounds__(HB_THREADS) k_halo_fill(CsrView m, const int* hoff, const int* sptr, int* halo,
                                                           unsigned short* lidx, int* perm) {
-  __shared__ int keys[HALO_MAXNZ], uniq[HALO_MAXNZ], scan[HB_THREADS];
+  extern __shared__ int hb_sm[];
+  int *keys = hb_sm, *uniq = hb_sm + HALO_MAXNZ, *scan = hb_sm + 2 * HALO_MAXNZ;
   const int r0 = blockIdx.x * HALO_R, r1 = min(m.nrows, r0 + HALO_R);
   const int total = block_halo(m, r0, r1, keys, uniq, scan);
   const int h0 = hoff[blockIdx.x];
@@ -145,7 +151,9 @@ HaloPatternPtr halo_pattern_build(const DevCsr& m) {
   const int nblocks = (n + HALO_R - 1) / HALO_R;
   const int nslices = nblocks * (HALO_R / 32);
   DBuf<int> cnt(m.device, size_t(nblocks)), widths(m.device, size_t(nslices));
-  k_halo_count<<<nblocks, HB_THREADS, 0, c.stream>>>(m.view(), cnt.get(), widths.get());
+  cudaFuncSetAttribute(k_halo_count, cudaFuncAttributeMaxDynamicSharedMemorySize, int(HB_SMEM));
+  cudaFuncSetAttribute(k_halo_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, int(HB_SMEM));
+  k_halo_count<<<nblocks, HB_THREADS, HB_SMEM, c.stream>>>(m.view(), cnt.get(), widths.get());
   MPG_CHECK_LAUNCH();
   std::vector<int> hc(static_cast<size_t>(nblocks));
   std::vector<int> hw(static_cast<size_t>(nslices));
@@ -155,6 +163,17 @@ HaloPatternPtr halo_pattern_build(const DevCsr& m) {
   auto p = std::make_shared<HaloPattern>();
   std::vector<int> hoff(static_cast<size_t>(nblocks) + 1, 0);
   std::vector<int> sptr(static_cast<size_t>(nslices) + 1, 0);
+  if (std::getenv("MPG_HALO_DEBUG")) {
+    int mx = 0, bad = 0;
+    double sum = 0.0;
+    for (int v : hc) {
+      mx = std::max(mx, v);
+      bad += v < 0 || v > HALO_MAX;
+      sum += v;
+    }
+    std::fprintf(stderr, "[halo] n=%d nnz=%lld blocks=%d max_halo=%d mean_halo=%.1f over_limit=%d\n", n,
+                 (long long)m.nnz, nblocks, mx, sum / nblocks, bad);
+  }
   for (int b = 0; b < nblocks; ++b) {
     if (hc[size_t(b)] < 0 || hc[size_t(b)] > HALO_MAX) return nullptr;
     hoff[size_t(b) + 1] = hoff[size_t(b)] + hc[size_t(b)];
@@ -178,7 +197,7 @@ HaloPatternPtr halo_pattern_build(const DevCsr& m) {
   p->lidx = DBuf<unsigned short>(m.device, size_t(std::max<int64_t>(1, ent)));
   MPG_CUDA(cudaMemcpyAsync(p->hoff.get(), hoff.data(), hoff.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
   MPG_CUDA(cudaMemcpyAsync(p->sptr.get(), sptr.data(), sptr.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
-  k_halo_fill<<<nblocks, HB_THREADS, 0, c.stream>>>(m.view(), p->hoff.get(), p->sptr.get(), p->halo.get(),
+  k_halo_fill<<<nblocks, HB_THREADS, HB_SMEM, c.stream>>>(m.view(), p->hoff.get(), p->sptr.get(), p->halo.get(),
                                                     p->lidx.get(), p->perm.get());
   MPG_CHECK_LAUNCH();
   MPG_CUDA(cudaStreamSynchronize(c.stream));

@@ -104,8 +104,8 @@ struct CsrView {
 // halo columns gets none (the CSR kernels run instead).
 constexpr int HALO_R = 128;
 constexpr int HALO_MAX = 1536;
-constexpr int HALO_MAXNZ = 4096;
-constexpr int HALO_XSTRIDE = 5;  // double2 per staged x row (4 used, 1 pad: conflict-free 16 B reads)
+constexpr int HALO_MAXNZ = 8192;
+constexpr int HALO_XSTRIDE = 4;  // double2 per staged x row; the 4 chunks are XOR-swizzled by (row >> 1) & 3
 struct HaloPattern {
   int nrows = 0, nblocks = 0, max_halo = 0;
   int64_t entries = 0;

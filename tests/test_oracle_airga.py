@@ -1,0 +1,131 @@
+"""The AIRGA oracle (oracle/airga.cpp, restating proj/src/airga.cpp:136-384,
+h2.cpp:11-77, orth.cpp:15-39) pinned to the reference's own test_airga.cpp
+assertions (cited per test), and the GPU path's adaptive loop against it:
+the expansion-point trajectory (every sweep's points), sweeps, convergence
+and the reduced transfer function."""
+import numpy as np
+import pytest
+
+NONE, FRESH, REUSE = 0, 1, 2
+
+
+def spd(gen, n, seed):  # test_airga.cpp:32-36
+    r = gen.random_dense(n, n, seed)
+    return r @ r.T + n * np.eye(n)
+
+
+def _o(orc, gen, M, D, K):
+    return orc.Csr.of(gen.from_dense(M)), orc.Csr.of(gen.from_dense(D)), orc.Csr.of(gen.from_dense(K))
+
+
+# ---------------------------------------------------------------- oracle pins (CPU)
+def test_oracle_decoupled_mode_exact_at_order_one(orc, gen):  # test_airga.cpp:84-107
+    M, K = np.eye(4), np.diag([1.0, 2, 3, 4])
+    e1 = np.eye(4, 1)
+    m, d, k = _o(orc, gen, M, np.zeros((4, 4)), K)
+    res = orc.airga_reduce(m, d, k, e1, e1, [1.0], r_max=2, inner_tol=0.0, max_outer=1,
+                           gmres=orc.GmresConfig(1e-13, 1000), mode=NONE)
+    assert res.m.shape == (1, 1)
+    for s in (0.5, 1.0, 3.0):
+        assert abs(res.transfer(s)[0, 0] - 1.0 / (s * s + 1.0)) <= 1e-10
+
+
+def test_oracle_single_point_spans_block_krylov(orc, gen):  # test_airga.cpp:109-132
+    n, s0 = 10, 1.7
+    M, K = spd(gen, n, 21), spd(gen, n, 22)
+    D = 0.1 * M + 0.05 * K
+    F, Cc = gen.random_dense(n, 1, 23), gen.random_dense(n, 1, 24)
+    m, d, k = _o(orc, gen, M, D, K)
+    res = orc.airga_reduce(m, d, k, F, Cc, [s0], r_max=4, inner_tol=0.0, max_outer=1,
+                           gmres=orc.GmresConfig(1e-13, 200), mode=NONE, alpha=0.1, beta=0.05)
+    assert res.m.shape == (4, 4)
+    A = s0 * s0 * M + s0 * D + K
+    kry = [np.linalg.solve(A, F[:, 0])]
+    for _ in range(3):
+        kry.append(np.linalg.solve(A, M @ kry[-1]))
+    kry = np.array(kry).T
+    # the reduced pencil equals the Galerkin projection on span(kry): compare transfer functions
+    Q, _ = np.linalg.qr(kry)
+    for s in (0.3, 2.0, 9.0):
+        hq = (Q.T @ Cc).T @ np.linalg.solve(Q.T @ (s * s * M + s * D + K) @ Q, Q.T @ F)
+        assert abs(res.transfer(s)[0, 0] - hq[0, 0]) <= 1e-8 * max(1.0, abs(hq[0, 0]))
+
+
+def test_oracle_expansion_point_update_hand_values(orc):  # test_airga.cpp:267-289
+    nxt = orc.update_expansion_points(np.eye(4), np.zeros((4, 4)), np.diag([1.0, 4, 9, 16]), [5.0, 6.0])
+    assert abs(nxt[0] - 3.0) <= 3e-9 and abs(nxt[1] - 4.0) <= 4e-9
+    assert orc.update_expansion_points(np.eye(3), np.zeros((3, 3)), np.zeros((3, 3)), [7.0, 9.0]) == [7.0, 9.0]
+
+
+@pytest.mark.parametrize("ns", [2, 7, 20, 40])
+def test_oracle_h2_norm_matches_lyapunov(orc, ns):  # h2.cpp:28-60 (the Gramian by the sign function here)
+    import scipy.linalg as sl
+    rng = np.random.default_rng(100 + ns)
+    A = rng.standard_normal((ns, ns))
+    A -= (np.max(np.linalg.eigvals(A).real) + 0.5) * np.eye(ns)
+    B, Cc = rng.standard_normal((ns, 2)), rng.standard_normal((3, ns))
+    want = np.sqrt(np.trace(Cc @ sl.solve_continuous_lyapunov(A, -B @ B.T) @ Cc.T))
+    assert abs(orc.h2_norm(A, B, Cc) - want) <= 1e-10 * want
+    assert orc.h2_norm(np.array([[0.1]]), np.ones((1, 1)), np.ones((1, 1))) == float("inf")
+
+
+def test_oracle_fresh_and_reused_give_the_same_model(orc, gen):  # test_airga.cpp:189-265
+    mh, kh = gen.disc_brake(120, 6.283, 3)
+    M, K = mh.to_dense(), kh.to_dense()
+    D = 5e-2 * M + 5e-6 * K
+    e1 = np.eye(120, 1)
+    m, d, k = _o(orc, gen, M, D, K)
+    kw = dict(r_max=12, max_outer=2, outer_tol=1e30, gmres=orc.GmresConfig(1e-10, 1000), alpha=5e-2, beta=5e-6)
+    pts = [6.283, 700.0, 1500.0, 3100.0]
+    fr = orc.airga_reduce(m, d, k, e1, e1, pts, mode=FRESH, **kw)
+    ru = orc.airga_reduce(m, d, k, e1, e1, pts, mode=REUSE, **kw)
+    assert fr.m.shape == ru.m.shape
+    for s in (10.0, 300.0, 2000.0):
+        hf, hr = fr.transfer(s), ru.transfer(s)
+        assert np.linalg.norm(hf - hr) <= 1e-6 * np.linalg.norm(hf)
+    assert sum(r.solves for r in fr.rows) == sum(r.solves for r in ru.rows)
+    kinds = [r.kind for r in ru.rows]
+    assert kinds.count(1) == 1 and kinds.count(2) == 2 * 3 and kinds.count(3) == 1 and kinds.count(4) >= 1
+
+
+# ---------------------------------------------------------------- GPU vs oracle
+def _pair_sys(mpg, orc, gen, case):
+    import scipy.sparse as sp
+    if case == "brake":
+        mh, kh = gen.disc_brake(200, 6.283, 3)
+        Ms, Ks = mh.to_scipy(), kh.to_scipy()
+        alpha, beta = 5e-2, 5e-6
+        Ds = (alpha * Ms + beta * Ks).tocsr()
+        f = np.eye(200, 1)
+        c = f.copy()
+        pts = [6.283, 700.0, 1500.0]
+    else:
+        c2 = gen.config2(M=12)
+        Ms, Ks = c2.e_csr().to_scipy(), -c2.a.to_scipy()
+        alpha, beta = 0.05, 1e-4
+        Ds = (alpha * Ms + beta * Ks).tocsr()
+        f, c = c2.b[:, :1], c2.c[:, :1]
+        pts = [1.0, 10.0, 100.0]
+    ms = lambda a: mpg.SparseMatrix.from_scipy(sp.csr_matrix(a))
+    oc = lambda a: orc.Csr.of(gen.from_triplets(a.shape[0], a.shape[1], *sp.find(a)))
+    gsys = mpg.SecondOrderSystem.create(ms(Ms), ms(Ds), ms(Ks), f, c, alpha, beta)
+    return gsys, (oc(Ms), oc(Ds), oc(Ks)), f, c, pts, alpha, beta
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,mode", [("brake", REUSE), ("brake", FRESH), ("c2", REUSE), ("c2", NONE)])
+def test_gpu_airga_trajectory_matches_oracle(mpg, orc, gen, case, mode):
+    gsys, (m, d, k), f, c, pts, alpha, beta = _pair_sys(mpg, orc, gen, case)
+    kw = dict(r_max=9, max_outer=6, outer_tol=1e-6, inner_tol=1e-8)
+    red, rep = mpg.airga_reduce(gsys, mpg.AirgaConfig(expansion_points=pts, gmres=mpg.GmresConfig(1e-11, 1000), **kw),
+                                mode)
+    ores = orc.airga_reduce(m, d, k, f, c, pts, gmres=orc.GmresConfig(1e-11, 1000), mode=mode, alpha=alpha,
+                            beta=beta, **kw)
+    assert rep.sweeps == ores.sweeps and rep.converged == ores.converged
+    assert red.order() == ores.m.shape[0]
+    fp, ofp = np.array(rep.final_points), np.array(ores.final_points)
+    assert np.max(np.abs(fp - ofp) / ofp) <= 1e-6
+    for s in np.logspace(-1, 4, 40):
+        hg = red.c.T @ np.linalg.solve(s * s * red.m + s * red.d + red.k, red.f)
+        ho = ores.transfer(s)
+        assert np.linalg.norm(hg - ho) <= 1e-6 * np.linalg.norm(ho), s
