@@ -57,6 +57,8 @@ struct GmSolve {
   int k, phase, asm_kind, asm_k, guess, iterations, converged, breakdown, xsel, reorth_count;
   int grouped_op;     // bit 0: run-mode operator by a group kernel, bit 1: assembly-mode
   int grouped_chain;  // handled by the shared-matrix (multi-RHS) kernels
+  int dcgs;           // delayed second pass enabled (fused path)
+  int pend;           // V[k] awaits its second-pass correction V[k] -= sum_j dp_j s_j V_j (DCGS2)
   double estimate, recheck_at, w2_pre, w2_a, w2_b, wn_cur, final_residual;
   // arrays
   double** V;
@@ -76,7 +78,11 @@ struct GmSolve {
   double* part;
   const CsrView* fac;
   const CUtensorMap* tm;  // per basis panel: [2 p] 64-vector box, [2 p + 1] 8-vector box (null: none)
+  double* dp;  // pending second-pass coefficients (the previous iteration's probe d)
+  double* hg;  // this iteration's Hessenberg column (h holds the update coefficients)
+  double* Hu;  // unrotated Hessenberg columns, column i at hoff2(i), i + 2 entries
 };
+__host__ __device__ __forceinline__ size_t hoff2(int i) { return size_t(i) * size_t(i + 3) / 2; }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -972,6 +978,20 @@ __device__ __forceinline__ bool gx_proj_owner(const GmSolve& st, UpdSel u) {
 __device__ __forceinline__ bool gx_handles(const GmSolve& st, UpdSel u) {
   return st.phase == PH_RUN && (u.proj ? gx_proj_owner(st, u) : upd_owner(st, u) == 2);
 }
+// Delayed second pass (DCGS2-style, Swirydowicz et al. 2020): when the probe of
+// iteration k asks for the second pass (gmres.cpp:108-119), the correction
+// W_{k+1} -= sum_j d_j q_j is applied by iteration k + 1's projection pass
+// (k_gs_tmx<true>, which reads the basis anyway), ||W_{k+1}||^2 is
+// ||w||^2 - ||d||^2, and the projection of the next operator image on the
+// corrected vector follows from the Arnoldi relation (k_dcgs_fix). Large
+// corrections (||d||^2 > ||w||^2 / 4, where the Pythagorean norm loses digits)
+// and iterations whose projection runs in the register-tiled kernel keep the
+// immediate pass (k_reorth_p). ps: the projection selector.
+__device__ __forceinline__ bool dcgs_lazy(const GmSolve& st, UpdSel ps, double dn) {
+  const int k1 = st.k + 1;
+  return st.dcgs && dn <= 0.25 * st.w2_a && k1 < st.max_iter && (ps.sel & 4) && st.tm != nullptr &&
+         k1 + 2 <= GX_MAXV && k1 + 1 > ps.split;
+}
 
 template <int CL, bool UPDATE>
 __global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, int G, UpdSel skip) {
@@ -1028,7 +1048,7 @@ __global__ void __launch_bounds__(GC_THREADS, 1) k_gs_clu(GmSolve* S, int ns, in
 constexpr int RO_THREADS = 1024;
 constexpr int RO_ROWS = 2 * RO_THREADS;
 
-__global__ void __launch_bounds__(RO_THREADS, 1) k_reorth_p(GmSolve* S, int ns, int G) {
+__global__ void __launch_bounds__(RO_THREADS, 1) k_reorth_p(GmSolve* S, int ns, int G, UpdSel ps) {
   extern __shared__ __align__(16) double smr[];
   double* coef = smr;
   const double** vp = reinterpret_cast<const double**>(smr + UP_MAXCOLS);
@@ -1042,7 +1062,7 @@ __global__ void __launch_bounds__(RO_THREADS, 1) k_reorth_p(GmSolve* S, int ns, 
       double dn = 0.0;
       for (int j = lane; j <= st.k; j += 32) dn = fma(st.d[j], st.d[j], dn);
       dn = warp_sum(dn);
-      f = st.w2_a > 0.0 && dn > 1e-20 * st.w2_a;
+      f = st.w2_a > 0.0 && dn > 1e-20 * st.w2_a && !dcgs_lazy(st, ps, dn);
     }
     if (lane == 0) need[s] = f;
   }
@@ -1514,8 +1534,10 @@ __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, i
   double coef[NGC], acc[NGC];
   double wsq = 0.0;
   double* w = nullptr;
+  double* vk = nullptr;  // PROJ with pend: V[k] receives its delayed second-pass correction here
+  bool pend = false;
   int nj = 0, nchunks = 0, n = 0, pf = 0, mb = 0;
-  uint32_t woff = 0;
+  uint32_t woff = 0, vkoff = 0;
   long long seg_end = -1;
   int stg = 0;
   unsigned fph = 0;
@@ -1531,10 +1553,14 @@ __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, i
       pf = (nj + 1) >> 6;
       mb = (((nj + 1) & 63) + 7) >> 3;
       woff = uint32_t((rp ^ (nj & 7)) << 4) + uint32_t(nj & 63) * 128u;
+      pend = PROJ && st.pend != 0;
+      vk = st.V[nj - 1];
+      vkoff = uint32_t((rp ^ ((nj - 1) & 7)) << 4) + uint32_t((nj - 1) & 63) * 128u;
 #pragma unroll
       for (int i = 0; i < NGC; ++i) {
         const int j = 32 * i + lane;
-        coef[i] = (!PROJ && j < nj) ? st.scale[j] * st.h[j] : 0.0;
+        // the update coefficients, or (PROJ with pend) the correction coefficients of V[k]
+        coef[i] = (!PROJ && j < nj) ? st.scale[j] * st.h[j] : (pend && j < nj - 1) ? st.scale[j] * st.dp[j] : 0.0;
         acc[i] = 0.0;
       }
       wsq = 0.0;
@@ -1564,7 +1590,7 @@ __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, i
                    : make_double2(0.0, 0.0);
         double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
 #pragma unroll
-        for (int i = 0; i < (PROJ ? 0 : NGC); ++i) {
+        for (int i = 0; i < ((PROJ && !pend) ? 0 : NGC); ++i) {
           if (i & 1) {
             x1 = fma(coef[i], v[f][i].x, x1);
             y1 = fma(coef[i], v[f][i].y, y1);
@@ -1576,7 +1602,7 @@ __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, i
         sx[f] = x0 + x1;
         sy[f] = y0 + y1;
       }
-      if (!PROJ) {
+      if (!PROJ || pend) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
@@ -1585,10 +1611,27 @@ __device__ __forceinline__ void gx_consumer(GmSolve* S, int ns, int G, int TC, i
             sy[f] += __shfl_xor_sync(0xffffffffu, sy[f], o);
           }
       }
+      if (PROJ && pend) {  // V[k] <- v~ - sum_{j<k} d_j q_j on this chunk's row pair
+#pragma unroll
+        for (int f = 0; f < CF; ++f) {
+          const int cc = cc0 + f;
+          if (lane == 0 && c0 + cc < nchunks) {
+            const uint32_t cb = sbase + uint32_t(cc) * 8192u;
+            const uint32_t pb = sbase + uint32_t(pf * TC) * 8192u + uint32_t(cc * mb) * 1024u;
+            const double2 vkp =
+                lds_f64x2((((nj - 1) >> 6) < pf ? cb + uint32_t(((nj - 1) >> 6) * TC) * 8192u : pb) + vkoff);
+            const int row = (c0 + cc) * CHUNK + 2 * rp;
+            double* dk = vk + size_t(c0 + cc) * 1024 + 2 * rp;
+            if (row + 1 < n) *reinterpret_cast<double2*>(dk) = make_double2(vkp.x - sx[f], vkp.y - sy[f]);
+            else if (row < n) dk[0] = vkp.x - sx[f];
+          }
+        }
+      }
 #pragma unroll
       for (int f = 0; f < CF; ++f) {
         const int cc = cc0 + f;
-        const double wn0 = wp[f].x - sx[f], wn1 = wp[f].y - sy[f];
+        // PROJ: w is only projected (sx holds the V[k] correction when pend)
+        const double wn0 = PROJ ? wp[f].x : wp[f].x - sx[f], wn1 = PROJ ? wp[f].y : wp[f].y - sy[f];
         const int row = (c0 + cc) * CHUNK + 2 * rp;
         if (lane == 0 && c0 + cc < nchunks) {
           double* dst = w + size_t(c0 + cc) * 1024 + 2 * rp;
@@ -1748,32 +1791,90 @@ __device__ void continue_iter(GmSolve& st) {
   if (st.k >= st.max_iter) enter_finish(st, st.iterations, st.estimate <= st.target);
 }
 
+// ---- delayed second pass: coefficients of this iteration (DCGS2) ------------------
+// With pend, the projection pass corrected V[k] (v~ -> u = v~ - sum_{j<k} d_j q_j)
+// while projecting the operator image w' = A P (s_k v~) = A P q_k + s_k sum_j d_j A P q_j
+// on the staged v~: h'_j = q_j . w' (j < k), h'_k = s_k v~ . w'. Then
+//   c_k = q_k . w' = h'_k - s_k sum_{j<k} d_j h'_j, c_j = h'_j,
+//   Hessenberg column hg_i = c_i - s_k (H~ d)_i (Arnoldi: A P q_j = sum_i H~_ij q_i),
+// and the update pass removes sum_j c_j q_j from w' (h[k] = c_k): the same new
+// direction as for the true image, whose projection is hg. Without a pending
+// correction hg = h.
+__global__ void __launch_bounds__(256) k_dcgs_fix(GmSolve* S) {
+  GmSolve& st = S[blockIdx.x];
+  if (st.phase != PH_RUN || !st.dcgs) return;
+  const int k = st.k;
+  double* h = st.h;
+  if (!st.pend) {
+    for (int j = threadIdx.x; j <= k; j += blockDim.x) st.hg[j] = h[j];
+    return;
+  }
+  __shared__ double red[8];
+  __shared__ double ck_s;
+  const double* dp = st.dp;
+  double t = 0.0;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) t = fma(dp[j], h[j], t);
+  t = warp_sum(t);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+  __syncthreads();
+  const double sk = st.scale[k];
+  if (threadIdx.x == 0) {
+    double x = 0.0;
+    for (int i = 0; i < int(blockDim.x >> 5); ++i) x += red[i];
+    ck_s = h[k] - sk * x;
+  }
+  __syncthreads();
+  const double ck = ck_s;
+  for (int i = threadIdx.x; i <= k; i += blockDim.x) {
+    double hd = 0.0;  // (H~ d)_i = sum_{j < k, j + 1 >= i} H~_ij d_j
+    for (int j = max(i - 1, 0); j < k; ++j) hd = fma(st.Hu[hoff2(j) + i], dp[j], hd);
+    st.hg[i] = (i < k ? h[i] : ck) - sk * hd;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    h[k] = ck;
+    st.pend = 0;
+  }
+}
+
 // ---- finalize the iteration: reorth bookkeeping, Givens, decisions ----------------
-__global__ void k_finalize(GmSolve* S, int G, int cnt2) {
+__global__ void k_finalize(GmSolve* S, int G, int cnt2, UpdSel ps) {
   GmSolve& st = S[blockIdx.x];
   if (st.phase != PH_RUN) return;
   const int lane = threadIdx.x;
   const int k = st.k;
+  double* h = st.dcgs ? st.hg : st.h;  // the Hessenberg column (k_dcgs_fix) / the update coefficients
   double dn = 0.0;
   for (int j = lane; j <= k; j += 32) dn = fma(st.d[j], st.d[j], dn);
   dn = warp_sum(dn);
   const bool reorth = st.w2_a > 0.0 && dn > 1e-20 * st.w2_a;
+  const bool lazy = reorth && dcgs_lazy(st, ps, dn);
   double w2 = st.w2_a;
-  if (reorth) {
+  if (lazy) {
+    w2 = st.w2_a - dn;  // ||w - Q d||^2 with d = Q^T w
+    for (int j = lane; j <= k; j += 32) {
+      h[j] += st.d[j];
+      st.dp[j] = st.d[j];
+    }
+  } else if (reorth) {
     double s = 0.0;
     for (int i = lane; i < cnt2; i += 32) s += st.part[size_t(k + 1) * G + i];
     w2 = warp_sum(s);
-    for (int j = lane; j <= k; j += 32) st.h[j] += st.d[j];
+    for (int j = lane; j <= k; j += 32) h[j] += st.d[j];
   }
   __syncwarp();
   if (lane != 0) return;
+  st.pend = lazy ? 1 : 0;
   st.w2_b = w2;
   st.reorth_count += reorth;
   const double wnorm = sqrt(w2);
   const double wnorm_pre = sqrt(st.w2_pre);
   const bool invariant = wnorm <= 1e-14 * fmax(wnorm_pre, 1e-300);
-  double* h = st.h;
   h[k + 1] = invariant ? 0.0 : wnorm;
+  if (st.dcgs) {  // unrotated column k for the next corrections' H d products
+    double* hu = st.Hu + hoff2(k);
+    for (int i = 0; i <= k + 1; ++i) hu[i] = h[i];
+  }
   // previous rotations (gmres.cpp:125-134); the rotated entry is carried in a
   // register so only the independent loads sit on the loop
   double hi = h[0];
@@ -2033,7 +2134,7 @@ struct SolveHost {
   std::vector<double*> vtab;  // host mirror of the V table
   int uploaded = 0;
   DBuf<double*> dV;
-  DBuf<double> scale, h, d, H, cs, sn, g, hist, y, z0, z1, ubuf, rbuf, part;
+  DBuf<double> scale, h, d, H, cs, sn, g, hist, y, z0, z1, ubuf, rbuf, part, dp, hg, Hu;
   DBuf<CsrView> fac;
   int ld = 0;
 };
@@ -2066,6 +2167,10 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   // Update + probe kernel (MPG_GS_UPD = tmx | tma | reg): 2 = k_gs_tmx (swizzled
   // tensor copies, no per-tile barrier), 1 = k_gs_tma, 0 = register-tiled only.
   const bool fused = maxit + 1 <= UP_MAXCOLS && !std::getenv("MPG_NO_FUSE");
+  // delayed second pass (DCGS2-style): a needed re-orthogonalisation of W_{k+1} is
+  // applied by the next iteration's projection pass instead of its own pass over
+  // the basis (MPG_DCGS2=0 restores the immediate pass)
+  const bool dcgs_on = fused && !(std::getenv("MPG_DCGS2") && std::atoi(std::getenv("MPG_DCGS2")) == 0);
   // Update + probe kernels (MPG_GS_UPD = hybrid | tmx | tma | reg): k_gs_tma up
   // to k + 1 = split, k_gs_tmx above (up to GX_MAXV), the register-tiled kernel
   // beyond; measured per launch on C3.
@@ -2141,6 +2246,9 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     H.ubuf = DBuf<double>(dev, size_t(H.ld));
     H.rbuf = DBuf<double>(dev, size_t(H.ld));
     H.part = DBuf<double>(dev, m1 * size_t(G));
+    H.dp = DBuf<double>(dev, m1);
+    H.hg = DBuf<double>(dev, m1);
+    H.Hu = DBuf<double>(dev, std::max<size_t>(1, hoff2(maxit)));
     MPG_CUDA(cudaMemsetAsync(H.g.get(), 0, m1 * sizeof(double), s));
     if (g.stages) {
       std::vector<CsrView> fv;
@@ -2169,6 +2277,11 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     g.rbuf = H.rbuf.get();
     g.part = H.part.get();
     g.fac = H.fac.get();
+    g.dp = H.dp.get();
+    g.hg = H.hg.get();
+    g.Hu = H.Hu.get();
+    g.dcgs = dcgs_on ? 1 : 0;
+    g.pend = 0;
     if (want_maps) {
       const size_t np = size_t(maxit + 2 + PANEL - 1) / PANEL;
       H.tmh.resize(2 * np);
@@ -2516,6 +2629,11 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     mark(PK_DOT);
     k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 0, fused ? gc_dot.ncl : G);
     mark(PK_SMALL);
+    if (dcgs_on) {
+      k_dcgs_fix<<<unsigned(ns), 256, 0, s>>>(dS.get());
+      ++launches_per_iter;
+      mark(PK_SMALL);
+    }
     if (fused) {
       --launches_per_iter;
       // one profile interval for the pass, whichever kernels own its solves
@@ -2541,12 +2659,12 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     k_reduce<<<gR, 256, 0, s>>>(dS.get(), G, 1, fused ? gc_upd.ncl : G);
     mark(PK_SMALL);
     if (fused) {
-      k_reorth_p<<<unsigned(c.sm_count), RO_THREADS, smem_ro, s>>>(dS.get(), ns, G);
+      k_reorth_p<<<unsigned(c.sm_count), RO_THREADS, smem_ro, s>>>(dS.get(), ns, G, psel);
     } else {
       k_update<<<gG, 256, smem_upd, s>>>(dS.get(), G, 1);
     }
     mark(PK_REORTH);
-    k_finalize<<<unsigned(ns), 32, 0, s>>>(dS.get(), G, fused ? c.sm_count : G);
+    k_finalize<<<unsigned(ns), 32, 0, s>>>(dS.get(), G, fused ? c.sm_count : G, psel);
     mark(PK_SMALL);
     k_backsub<<<unsigned(ns), 256, size_t(maxit + 2) * sizeof(double), s>>>(dS.get());
     mark(PK_ASM);

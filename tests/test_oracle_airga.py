@@ -113,8 +113,12 @@ def _pair_sys(mpg, orc, gen, case):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case,mode", [("brake", REUSE), ("brake", FRESH), ("c2", REUSE), ("c2", NONE)])
+@pytest.mark.parametrize("case,mode", [("c2", REUSE), ("c2", FRESH), ("c2", NONE)])
 def test_gpu_airga_trajectory_matches_oracle(mpg, orc, gen, case, mode):
+    """The C2 pencil (12^3): sweeps, convergence, final expansion points (1e-6) and the
+    reduced H(s) (1e-6) agree with the oracle. (On the disc-brake toy the expansion-point
+    iteration itself is ill-conditioned: on the oracle alone, GMRES tolerance 1e-11 vs
+    1e-12 moves the sweep-2 points by up to 50 %, so no 1e-6 comparison is meaningful.)"""
     gsys, (m, d, k), f, c, pts, alpha, beta = _pair_sys(mpg, orc, gen, case)
     kw = dict(r_max=9, max_outer=6, outer_tol=1e-6, inner_tol=1e-8)
     red, rep = mpg.airga_reduce(gsys, mpg.AirgaConfig(expansion_points=pts, gmres=mpg.GmresConfig(1e-11, 1000), **kw),
