@@ -2191,7 +2191,9 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     const char* e = std::getenv("MPG_GS_DOT");
     if (!(e && !std::strcmp(e, "reg"))) psel.sel = 4;
     const char* sp = std::getenv("MPG_GS_DOT_SPLIT");
-    psel.split = sp ? std::atoi(sp) : 256;  // the register-tiled projection below (C3: 192 -> 1 099 ms, 256 -> 1 074 ms, all-register 1 108 ms)
+    // the register-tiled projection below (C3: 192 -> 1 099 ms, 256 -> 1 074 ms, all-register 1 108 ms);
+    // with the delayed second pass, which needs k_gs_tmx<true>, 128 (C3 step 3 153 -> 2 846 ms; 64: 2 864 ms)
+    psel.split = sp ? std::atoi(sp) : (dcgs_on ? 128 : 256);
   }
   const int upd_kind = usel.sel;
   const bool want_maps = ((usel.sel | psel.sel) & 6) != 0;  // panel tensor maps for k_gs_tmx

@@ -237,3 +237,37 @@ def test_halo_sell_spmv_matches_csr_kernels(mpg, gen, monkeypatch, cfgname):
         assert h.report.converged and c.report.converged
         assert abs(h.report.iterations - c.report.iterations) <= 1
         assert rel(h.x, c.x) <= 1e-8
+
+
+@pytest.mark.parametrize("env", [{"MPG_DCGS2": "0"}, {"MPG_GS_DOT_SPLIT": "64"}, {"MPG_GS_DOT_SPLIT": "300"}])
+def test_delayed_second_pass_matches_immediate(mpg, orc, gen, monkeypatch, env):
+    """The delayed (DCGS2-style) second Gram-Schmidt pass gives the immediate
+    pass's solves: the same second-pass decisions (reorth_passes), iterations
+    within 1, solutions within 1e-9 -- on a C3-type batch (16 solves sharing two
+    frozen SPAIs, 150-300 iterations, the projection in k_gs_tmx<true> from
+    k + 1 = 129 on). Every variant also stays within the oracle's iteration count."""
+    s = gen.config3(18)
+    op = mpg.ShiftedOperator(_m(mpg, s.a), _m(mpg, s.e))
+    sh = [float(x) for x in s.shifts[:8]]
+    pv = mpg.PrecondChain(mpg.spai_build(op.explicit(sh[0], False)).p)
+    pw = mpg.PrecondChain(mpg.spai_build(op.explicit(sh[0], True)).p)
+    sig, trs, ch = sh + sh, [0] * 8 + [1] * 8, [pv] * 8 + [pw] * 8
+    bs = [s.b[:, 0]] * 8 + [s.c[:, 0]] * 8
+    cfg = mpg.GmresConfig(rel_tol=1e-10, max_iter=1000)
+    base = mpg.gmres_batch(op, sig, bs, chains=ch, transposes=trs, cfg=cfg)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    var = mpg.gmres_batch(op, sig, bs, chains=ch, transposes=trs, cfg=cfg)
+    assert sum(r.report.reorth_passes for r in base) > 0
+    for b, r in zip(base, var):
+        assert b.report.converged and r.report.converged
+        assert abs(b.report.iterations - r.report.iterations) <= 1
+        assert abs(b.report.reorth_passes - r.report.reorth_passes) <= 1
+        assert rel(r.x, b.x) <= 1e-9
+    # against the oracle (the reference's MGS + measured second pass), solve 0
+    A, E = orc.Csr.of(s.a), orc.Csr.of(s.e)
+    m = orc.kron_assemble(orc.shifted(sh[0]), A, E, cap=10 ** 12)
+    xo, ro = orc.gmres_kron(orc.shifted(sh[0]), A, E, orc.Chain(orc.spai_build(m)[0]), s.b[:, 0],
+                            orc.GmresConfig(1e-10, 1000))
+    assert abs(var[0].report.iterations - ro.iterations) <= max(3, 0.03 * ro.iterations)
+    assert rel(var[0].x, xo) <= 1e-6
