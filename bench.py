@@ -109,13 +109,15 @@ def byte_model(n: int, nnz_a: int, nnz_e_extra: int, nnz_p: list, iters: list) -
 def traffic_per_launch(kernel: str, algorithmic_per_launch: float):
     """DRAM bytes (read + write) per launch of `kernel`: the algorithmic bytes
     scaled by dram/algorithmic of one `ncu --set full` capture of that kernel
-    (profiles/r01/traffic.json); None when no capture exists for it."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
-            k = json.load(f)["kernels"][kernel]
-        return round(algorithmic_per_launch * (k["dram_read"] + k["dram_write"]) / k["algorithmic"])
-    except Exception:
-        return None
+    (profiles/r02/traffic.json, else r01); None when no capture exists for it."""
+    for rnd in ("r02", "r01"):  # the newest capture of the kernel class
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "traffic.json")) as f:
+                k = json.load(f)["kernels"][kernel]
+            return round(algorithmic_per_launch * (k["dram_read"] + k["dram_write"]) / k["algorithmic"])
+        except Exception:
+            continue
+    return None
 
 
 def global_shifts(args, world: int) -> list:
@@ -284,8 +286,10 @@ def run_ours(args, rank: int, world: int, device: int):
                                   "so frac can exceed 1",
                      "step": {"achieved": round(achieved, 1), "frac": round(achieved / peak, 4),
                               "bytes_per_step": bytes_step,
-                              "scope": "whole preconditioned GMRES step (SpMV + chain + Gram-Schmidt) over the "
-                                       "device-timed step"}},
+                              "scope": "algorithmic rate of the whole preconditioned GMRES step over the device-timed "
+                                       "step, SURVEY.md 8(d) per-solve model (each solve's SpMV bytes counted although "
+                                       "8 solves share one matrix read; one basis read per Gram-Schmidt pass): not a "
+                                       "DRAM rate"}},
         "kernels": kernels,
         "clocks": clocks,
     }

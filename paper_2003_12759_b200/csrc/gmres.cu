@@ -2719,24 +2719,34 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     mark = [](int) {};
     MPG_CUDA(cudaMemcpyAsync(hs.data(), dS.get(), sizeof(GmSolve) * size_t(ns), cudaMemcpyDeviceToHost, s));
     MPG_CUDA(cudaStreamSynchronize(s));
+    // Algorithmic bytes of the launches (4-byte indices, 8-byte values): a matrix
+    // that one interleaved group kernel streams for all its solves is counted once
+    // per group, the vectors per solve.
     double bytes[PK_COUNT] = {};
+    std::vector<char> leader(size_t(ns), 1);
+    for (size_t gi = 0; gi < chain_groups.size(); ++gi)
+      if (chain_il[gi])
+        for (int q = 1; q < chain_groups[gi].cnt; ++q) leader[size_t(chain_groups[gi].idx[q])] = 0;
     for (int i = 0; i < ns; ++i) {
       const GmSolve& b = before[size_t(i)];
       if (b.phase != PH_RUN) continue;
       const double n = double(b.n), k = double(b.k);
+      const double lead = leader[size_t(i)] ? 1.0 : 0.0;
       for (int stg = 0; stg < b.stages; ++stg) {
         const DevCsr& f = *specs[size_t(i)].chain->factors[size_t(stg)];
         const double h = b.pair_bd ? 2.0 : 1.0;
-        bytes[PK_CHAIN] += h * (12.0 * double(f.nnz) + 4.0 * double(f.nrows + 1) + 16.0 * double(f.nrows));
+        bytes[PK_CHAIN] += h * (lead * (12.0 * double(f.nnz) + 4.0 * double(f.nrows + 1)) + 16.0 * double(f.nrows));
       }
       const double vec = b.pair ? 2.0 : 1.0;
       const double be = op.emode == E_SAMEPAT ? 8.0 * double(op.a->nnz) : op.emode == E_DIAG ? 8.0 * double(nb) : 0.0;
-      bytes[PK_OP] += 12.0 * double(op.a->nnz) + 4.0 * double(nb + 1) + be + vec * 16.0 * double(nb);
-      bytes[PK_DOT] += 8.0 * n * (k + 1.0) + 8.0 * n;
+      bytes[PK_OP] += lead * (12.0 * double(op.a->nnz) + 4.0 * double(nb + 1) + be) + vec * 16.0 * double(nb);
+      bytes[PK_DOT] += 8.0 * n * (k + 1.0) + 8.0 * n + (b.pend ? 8.0 * n : 0.0);  // + the delayed correction of V[k]
       bytes[PK_UPDPROBE] += 8.0 * n * (k + 1.0) + 16.0 * n;
       bytes[PK_UPD] += 8.0 * n * (k + 1.0) + 16.0 * n;
       bytes[PK_PROBE] += 8.0 * n * (k + 1.0) + 8.0 * n;
-      if (hs[size_t(i)].reorth_count > b.reorth_count) bytes[PK_REORTH] += 8.0 * n * (k + 1.0) + 16.0 * n;
+      // an immediate second pass (a delayed one is folded into the next projection)
+      if (hs[size_t(i)].reorth_count > b.reorth_count && !hs[size_t(i)].pend)
+        bytes[PK_REORTH] += 8.0 * n * (k + 1.0) + 16.0 * n;
     }
     for (size_t e = 0; e < ev_kind.size(); ++e) {
       float ms = 0.0f;
