@@ -511,6 +511,58 @@ __global__ void __launch_bounds__(256) k_spmv_il2(GmSolve* S, Group grp, CsrView
   }
 }
 
+// SELL-8 variant of k_spmv_il2 (runtime.cuh Sell8): the same thread mapping (4
+// lanes per row, lane q owns right-hand sides 2q, 2q + 1, 8 rows per warp), but
+// step j's column index and value of the warp's 8 rows are 8 consecutive slots,
+// so each is one request per warp instead of 8 scattered ones.
+template <int EM, bool CHAIN>
+__global__ void __launch_bounds__(256) k_spmv_sell8(GmSolve* S, Group grp, Sell8View sv, OpView op,
+                                                    const double* __restrict__ xin, double* __restrict__ xout) {
+  if (!il_any_run(S, grp)) return;
+  const int lane = threadIdx.x & 3;
+  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) >> 2);
+  if (row >= sv.nrows) return;
+  const int e0 = __ldg(sv.sptr + (row >> 3)) + (row & 7);
+  const int w = (__ldg(sv.sptr + (row >> 3) + 1) - __ldg(sv.sptr + (row >> 3))) >> 3;
+  const double* xl = xin + 2 * lane;
+  double a0 = 0.0, a1 = 0.0, g0 = 0.0, g1 = 0.0;
+#pragma unroll 4
+  for (int j = 0; j < w; ++j) {
+    const int e = e0 + 8 * j;
+    const int c = __ldcs(sv.col + e);
+    const double2 x = __ldg(reinterpret_cast<const double2*>(xl + size_t(c) * MB));
+    if (!CHAIN && EM == E_SAMEPAT) {
+      const double2 ae = __ldcs(sv.val2 + e);
+      a0 = fma(ae.x, x.x, a0);
+      a1 = fma(ae.x, x.y, a1);
+      g0 = fma(ae.y, x.x, g0);
+      g1 = fma(ae.y, x.y, g1);
+    } else {
+      const double av = __ldcs(sv.val + e);
+      a0 = fma(av, x.x, a0);
+      a1 = fma(av, x.y, a1);
+    }
+  }
+  if (CHAIN) {
+    reinterpret_cast<double2*>(xout + size_t(row) * MB)[lane] = make_double2(a0, a1);
+    return;
+  }
+  if (EM == E_IDENT || EM == E_DIAG) {
+    const double2 xr = reinterpret_cast<const double2*>(xin + size_t(row) * MB)[lane];
+    const double dd = EM == E_DIAG ? op.ediag[row] : 1.0;
+    g0 = dd * xr.x;
+    g1 = dd * xr.y;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int q = 2 * lane + h;
+    if (q >= grp.cnt) continue;
+    GmSolve& st = S[grp.idx[q]];
+    if (st.phase != PH_RUN) continue;
+    st.V[st.k + 1][vidx(row)] = st.scale[st.k] * (st.sre * (h ? g1 : g0) + st.ca * (h ? a1 : a0));
+  }
+}
+
 // Halo-staged sliced-ELL variant (runtime.cuh HaloPattern): one CTA per block
 // of HALO_R rows stages the block's halo of x (all MB right-hand sides, 64 B
 // per column, the four 16-byte chunks XOR-swizzled by the row so the reads of
@@ -2381,6 +2433,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   bool any_plain_chain = true, any_plain_op_run = true, any_plain_op_asm = true;
   bool il2 = false;  // RHS-split interleaved SpMVs
   bool use_halo = false;
+  bool use_sell = false;
   if (!std::getenv("MPG_NO_MULTI")) {
     std::vector<int> used(size_t(ns), 0);
     for (int i = 0; i < ns; ++i) {
@@ -2406,6 +2459,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     // halo-staged sliced ELL: opt-in (MPG_SPMV_HALO=1); measured slower than the
     // CSR kernels on C3 (operator 309 -> 398-463 us, chain 168 -> 288 us per launch)
     use_halo = std::getenv("MPG_SPMV_HALO") != nullptr && std::getenv("MPG_SPMV_CSR") == nullptr;
+    use_sell = !use_halo && std::getenv("MPG_SPMV_CSR") == nullptr;  // SELL-8 where the padding stays small
     std::vector<int> in_il(size_t(ns), 0);
     for (size_t gi = 0; gi < chain_groups.size(); ++gi) {
       const Group& g = chain_groups[gi];
@@ -2418,6 +2472,10 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       if (ok && use_halo) {  // build the halo layouts now: the iteration is captured into a graph
         for (const CsrPtr& f : chain_of_group[gi]->factors) halo_of(*f, nullptr);
         halo_of_op(op, hs[size_t(g.idx[0])].transpose != 0, nullptr);
+      }
+      if (ok && use_sell) {
+        for (const CsrPtr& f : chain_of_group[gi]->factors) sell_of(*f, nullptr);
+        sell_of_op(op, hs[size_t(g.idx[0])].transpose != 0, nullptr);
       }
       if (ok) {
         il_bufs.emplace_back(dev, size_t(nb) * MB);
@@ -2471,6 +2529,15 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         }
         const double* xin = (stage & 1) ? xb : xa;
         double* xout = (stage & 1) ? xa : xb;
+        Sell8View sv{};
+        const Sell8* sp8 = use_sell ? sell_of(f, &sv) : nullptr;
+        if (sp8) {
+          k_spmv_sell8<E_IDENT, true><<<cdiv(f.nrows * 4, 256), 256, 0, s>>>(dS.get(), chain_groups[gi], sv, opn, xin,
+                                                                          xout);
+          ++launches_per_iter;
+          mark(PK_CHAIN);
+          continue;
+        }
         HaloView hv{};
         const HaloPattern* hp = use_halo ? halo_of(f, &hv) : nullptr;
         if (hp) {
@@ -2529,6 +2596,19 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         const int nst = int(chain_of_group[gi]->factors.size());
         const double* xin = ((nst - 1) & 1) ? il_bufs[2 * gi].get() : il_bufs[2 * gi + 1].get();
         const unsigned grid1 = cdiv(nb * int64_t(Vop), 256);
+        Sell8View sv{};
+        const Sell8* sp8 = use_sell ? sell_of_op(op, hs[size_t(g.idx[0])].transpose != 0, &sv) : nullptr;
+        if (sp8) {
+          const unsigned g2 = cdiv(nb * 4, 256);
+          switch (op.emode) {
+            case E_IDENT: k_spmv_sell8<E_IDENT, false><<<g2, 256, 0, s>>>(dS.get(), g, sv, ov, xin, nullptr); break;
+            case E_DIAG: k_spmv_sell8<E_DIAG, false><<<g2, 256, 0, s>>>(dS.get(), g, sv, ov, xin, nullptr); break;
+            default: k_spmv_sell8<E_SAMEPAT, false><<<g2, 256, 0, s>>>(dS.get(), g, sv, ov, xin, nullptr); break;
+          }
+          ++launches_per_iter;
+          mark(PK_OP);
+          continue;
+        }
         HaloView hv{};
         const HaloPattern* hp = use_halo ? halo_of_op(op, hs[size_t(g.idx[0])].transpose != 0, &hv) : nullptr;
         if (hp) {

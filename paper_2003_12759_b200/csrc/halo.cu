@@ -141,7 +141,114 @@ __global__ void k_halo_gather2(const int* perm, int64_t entries, const double2* 
   }
 }
 
+// SELL-8: per 8-row slice the longest row (pass 1), then entries column-major
+// within the slice (pass 2), padding with the row's own index and perm -1.
+__global__ void k_sell8_width(CsrView m, int* w) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r0 = s * 8;
+  if (r0 >= m.nrows) return;
+  int mx = 0;
+  for (int r = r0; r < min(m.nrows, r0 + 8); ++r) mx = max(mx, m.rowptr[r + 1] - m.rowptr[r]);
+  w[s] = mx;
+}
+
+__global__ void k_sell8_fill(CsrView m, const int* sptr, int* col, int* perm) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nsl = (m.nrows + 7) / 8;
+  if (row >= nsl * 8) return;
+  const int s = row >> 3, r8 = row & 7;
+  const int e0 = sptr[s], w = (sptr[s + 1] - e0) >> 3;
+  int b = 0, len = 0;
+  if (row < m.nrows) {
+    b = m.rowptr[row];
+    len = m.rowptr[row + 1] - b;
+  }
+  const int self = row < m.nrows ? row : 0;
+  for (int j = 0; j < w; ++j) {
+    const int e = e0 + 8 * j + r8;
+    col[e] = j < len ? m.colind[b + j] : self;
+    perm[e] = j < len ? b + j : -1;
+  }
+}
+
 }  // namespace
+
+Sell8Ptr sell8_build(const DevCsr& m) {
+  if (m.nrows < 1 || m.nnz == 0) return nullptr;
+  auto& c = ctx(m.device);
+  DeviceGuard g(m.device);
+  const int n = int(m.nrows);
+  const int nsl = (n + 7) / 8;
+  DBuf<int> w(m.device, size_t(nsl));
+  k_sell8_width<<<(nsl + 255) / 256, 256, 0, c.stream>>>(m.view(), w.get());
+  MPG_CHECK_LAUNCH();
+  std::vector<int> hw(static_cast<size_t>(nsl));
+  MPG_CUDA(cudaMemcpyAsync(hw.data(), w.get(), hw.size() * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  MPG_CUDA(cudaStreamSynchronize(c.stream));
+  std::vector<int> sptr(static_cast<size_t>(nsl) + 1, 0);
+  int64_t ent = 0;
+  for (int s = 0; s < nsl; ++s) {
+    ent += int64_t(hw[size_t(s)]) * 8;
+    if (ent >= INT_MAX) return nullptr;
+    sptr[size_t(s) + 1] = int(ent);
+  }
+  if (double(ent) > 1.25 * double(m.nnz) + 8.0 * nsl) return nullptr;
+  auto p = std::make_shared<Sell8>();
+  p->nrows = n;
+  p->entries = ent;
+  p->sptr = DBuf<int>(m.device, sptr.size());
+  p->col = DBuf<int>(m.device, size_t(std::max<int64_t>(1, ent)));
+  p->perm = DBuf<int>(m.device, size_t(std::max<int64_t>(1, ent)));
+  MPG_CUDA(cudaMemcpyAsync(p->sptr.get(), sptr.data(), sptr.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  k_sell8_fill<<<(nsl * 8 + 255) / 256, 256, 0, c.stream>>>(m.view(), p->sptr.get(), p->col.get(), p->perm.get());
+  MPG_CHECK_LAUNCH();
+  MPG_CUDA(cudaStreamSynchronize(c.stream));
+  return p;
+}
+
+const Sell8* sell_of(const DevCsr& m, Sell8View* view) {
+  std::scoped_lock l(m.mu);
+  if (!m.sell_tried) {
+    m.sell_tried = true;
+    m.sell = sell8_build(m);
+    if (m.sell) {
+      auto& c = ctx(m.device);
+      DeviceGuard g(m.device);
+      m.sell_val = DBuf<double>(m.device, size_t(std::max<int64_t>(1, m.sell->entries)));
+      k_halo_gather<<<std::max(1, c.sm_count * 8), 256, 0, c.stream>>>(m.sell->perm.get(), m.sell->entries,
+                                                                       m.val.get(), m.sell_val.get());
+      MPG_CHECK_LAUNCH();
+    }
+  }
+  if (!m.sell) return nullptr;
+  if (view) *view = Sell8View{m.sell->nrows, m.sell->sptr.get(), m.sell->col.get(), m.sell_val.get(), nullptr};
+  return m.sell.get();
+}
+
+const Sell8* sell_of_op(const ShiftedOp& op, bool transpose, Sell8View* view) {
+  const DevCsr& a = transpose ? *op.at : *op.a;
+  Sell8View av{};
+  const Sell8* p = sell_of(a, &av);
+  if (!p) return nullptr;
+  if (op.emode == E_SAMEPAT) {
+    std::scoped_lock l(op.halo_mu);
+    const int t = transpose ? 1 : 0;
+    if (!op.sell_tried_op[t]) {
+      op.sell_tried_op[t] = true;
+      auto& c = ctx(op.device);
+      DeviceGuard g(op.device);
+      op.sell_ae[t] = DBuf<double2>(op.device, size_t(std::max<int64_t>(1, p->entries)));
+      k_halo_gather2<<<std::max(1, c.sm_count * 8), 256, 0, c.stream>>>(
+          p->perm.get(), p->entries, transpose ? op.ae_t.get() : op.ae.get(), op.sell_ae[t].get());
+      MPG_CHECK_LAUNCH();
+    }
+    av.val2 = op.sell_ae[t].get();
+  } else if (op.emode == E_GENERAL) {
+    return nullptr;
+  }
+  if (view) *view = av;
+  return p;
+}
 
 HaloPatternPtr halo_pattern_build(const DevCsr& m) {
   if (m.nrows < 1 || m.nrows != m.ncols || m.nnz == 0) return nullptr;

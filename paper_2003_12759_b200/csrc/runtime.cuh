@@ -125,6 +125,27 @@ struct HaloView {
 struct DevCsr;
 HaloPatternPtr halo_pattern_build(const DevCsr& m);  // nullptr if the pattern does not fit
 
+// Sliced ELL with 8-row slices (SELL-8) for the interleaved multi-RHS SpMVs:
+// entry j of row r sits at sptr[r / 8] + 8 j + r % 8, so the 8 rows a warp
+// covers (4 lanes per row) load their column index and value of step j from 8
+// consecutive slots -- one request each instead of 8 scattered ones (the CSR
+// kernels are L1-wavefront bound on those, not on DRAM). Padding: index of the
+// row itself, value 0. Built once per pattern (nullptr: padding > 25 %).
+struct Sell8 {
+  int nrows = 0;
+  int64_t entries = 0;
+  DBuf<int> sptr, col, perm;  // [nslices + 1], [entries], [entries] (-1: padding)
+};
+using Sell8Ptr = std::shared_ptr<const Sell8>;
+struct Sell8View {
+  int nrows;
+  const int* sptr;
+  const int* col;
+  const double* val;
+  const double2* val2;
+};
+Sell8Ptr sell8_build(const DevCsr& m);
+
 struct DevCsr {
   int device = 0;
   int64_t nrows = 0, ncols = 0, nnz = 0;
@@ -138,10 +159,15 @@ struct DevCsr {
   mutable bool halo_tried = false;          // halo pattern + this matrix's values in it, built on first use
   mutable HaloPatternPtr halo;
   mutable DBuf<double> halo_val;
+  mutable bool sell_tried = false;          // SELL-8 layout + this matrix's values in it, built on first use
+  mutable Sell8Ptr sell;
+  mutable DBuf<double> sell_val;
   CsrView view() const { return {rowptr.get(), colind.get(), val.get(), int(nrows), int(ncols)}; }
 };
 // The halo layout of m with m's own values (nullptr: not eligible); cached on m.
 const HaloPattern* halo_of(const DevCsr& m, HaloView* view);
+// The SELL-8 layout of m with m's own values (nullptr: not eligible); cached on m.
+const Sell8* sell_of(const DevCsr& m, Sell8View* view);
 using CsrPtr = std::shared_ptr<DevCsr>;
 
 // Builders (spmv.cu).
@@ -171,6 +197,8 @@ struct ShiftedOp {
   mutable std::mutex halo_mu;
   mutable bool halo_tried[2] = {false, false};
   mutable DBuf<double2> halo_ae[2];  // (a, e) in the halo layout of A / A^T (E_SAMEPAT)
+  mutable bool sell_tried_op[2] = {false, false};
+  mutable DBuf<double2> sell_ae[2];  // (a, e) in the SELL-8 layout of A / A^T (E_SAMEPAT)
   OpView view(bool transpose) const;
 };
 using OpPtr = std::shared_ptr<ShiftedOp>;
@@ -178,6 +206,7 @@ OpPtr op_create(const CsrPtr& a, const CsrPtr& e);
 // The halo layout of the operator side (A's pattern; values of A, or (a, e)
 // pairs for E_SAMEPAT); nullptr if not eligible.
 const HaloPattern* halo_of_op(const ShiftedOp& op, bool transpose, HaloView* view);
+const Sell8* sell_of_op(const ShiftedOp& op, bool transpose, Sell8View* view);
 
 // Explicit unit matrix sigma E - A (or its 2n pair form) on the device.
 CsrPtr op_explicit(const ShiftedOp& op, double sre, double sim, bool transpose);

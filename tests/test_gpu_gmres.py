@@ -209,9 +209,10 @@ def test_gram_schmidt_kernel_variants_agree(mpg, gen, monkeypatch, env):
 
 @pytest.mark.parametrize("cfgname", ["c3", "c2", "c5"])
 def test_halo_sell_spmv_matches_csr_kernels(mpg, gen, monkeypatch, cfgname):
-    """The run-mode multi-RHS SpMVs in the halo-staged sliced-ELL layout
-    (MPG_SPMV_HALO; 27-point FEM with E sharing A's pattern, 7-point with
-    diagonal E) give the CSR kernels' solves on 8-solve groups of both sides; on a
+    """The run-mode multi-RHS SpMVs in the SELL-8 layout (the default) and the
+    halo-staged sliced-ELL layout (MPG_SPMV_HALO; 27-point FEM with E sharing A's
+    pattern, 7-point with diagonal E) give the CSR kernels' solves (MPG_SPMV_CSR)
+    on 8-solve groups of both sides; on a
     Zipf(1.8) pattern with rows up to 600 entries (blocks past HALO_MAXNZ) the
     layout is declined and the CSR kernels run."""
     if cfgname == "c3":
@@ -230,13 +231,17 @@ def test_halo_sell_spmv_matches_csr_kernels(mpg, gen, monkeypatch, cfgname):
     chains = [pv] * 8 + [pw] * 8
     bs = [s.b[:, 0] * (1 + 0.1 * i) for i in range(8)] + [s.c[:, 0] * (1 + 0.1 * i) for i in range(8)]
     cfg = mpg.GmresConfig(rel_tol=1e-10)
+    sell = mpg.gmres_batch(op, sig, bs, chains=chains, transposes=trs, cfg=cfg)  # default: SELL-8
+    monkeypatch.setenv("MPG_SPMV_CSR", "1")
     csr = mpg.gmres_batch(op, sig, bs, chains=chains, transposes=trs, cfg=cfg)
+    monkeypatch.delenv("MPG_SPMV_CSR")
     monkeypatch.setenv("MPG_SPMV_HALO", "1")
     halo = mpg.gmres_batch(op, sig, bs, chains=chains, transposes=trs, cfg=cfg)
-    for h, c in zip(halo, csr):
-        assert h.report.converged and c.report.converged
+    for h, c, sl in zip(halo, csr, sell):
+        assert h.report.converged and c.report.converged and sl.report.converged
         assert abs(h.report.iterations - c.report.iterations) <= 1
-        assert rel(h.x, c.x) <= 1e-8
+        assert abs(sl.report.iterations - c.report.iterations) <= 1
+        assert rel(h.x, c.x) <= 1e-8 and rel(sl.x, c.x) <= 1e-8
 
 
 @pytest.mark.parametrize("env", [{"MPG_DCGS2": "0"}, {"MPG_GS_DOT_SPLIT": "64"}, {"MPG_GS_DOT_SPLIT": "300"}])
