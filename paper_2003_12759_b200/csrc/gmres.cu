@@ -1853,6 +1853,7 @@ __device__ void continue_iter(GmSolve& st) {
 // direction as for the true image, whose projection is hg. Without a pending
 // correction hg = h.
 __global__ void __launch_bounds__(256) k_dcgs_fix(GmSolve* S) {
+  static_assert(UP_MAXCOLS <= 8 * 256, "k_dcgs_fix rows per thread");
   GmSolve& st = S[blockIdx.x];
   if (st.phase != PH_RUN || !st.dcgs) return;
   const int k = st.k;
@@ -1877,10 +1878,25 @@ __global__ void __launch_bounds__(256) k_dcgs_fix(GmSolve* S) {
   }
   __syncthreads();
   const double ck = ck_s;
-  for (int i = threadIdx.x; i <= k; i += blockDim.x) {
-    double hd = 0.0;  // (H~ d)_i = sum_{j < k, j + 1 >= i} H~_ij d_j
-    for (int j = max(i - 1, 0); j < k; ++j) hd = fma(st.Hu[hoff2(j) + i], dp[j], hd);
-    st.hg[i] = (i < k ? h[i] : ck) - sk * hd;
+  // (H~ d)_i = sum_{j < k, j + 1 >= i} H~_ij d_j, column by column so the reads of
+  // each stored column are coalesced; a thread keeps rows tid, tid + 256, ...
+  constexpr int RPT = 8;  // rows per thread: k + 1 <= 2048 (UP_MAXCOLS)
+  double hd[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) hd[u] = 0.0;
+  for (int j = 0; j < k; ++j) {
+    const double dj = dp[j];
+    const double* col = st.Hu + hoff2(j);
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int i = threadIdx.x + u * 256;
+      if (i <= j + 1) hd[u] = fma(col[i], dj, hd[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int i = threadIdx.x + u * 256;
+    if (i <= k) st.hg[i] = (i < k ? h[i] : ck) - sk * hd[u];
   }
   __syncthreads();
   if (threadIdx.x == 0) {

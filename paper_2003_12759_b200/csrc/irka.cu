@@ -33,14 +33,22 @@ namespace {
 
 using host::Mat;
 
+// rows per tile of k_ts_gram: as many as 48 KB of shared memory holds (multiple of 64, at most 512)
+__host__ __device__ __forceinline__ int ts_rows(int a, int b) {
+  int ch = (47 * 1024 / 8) / (a + b) - 1;
+  ch = ch > 512 ? 512 : ch;
+  return ch < 64 ? 64 : ch & ~63;
+}
+
 // part[blk][i + a*j] = sum over this block's rows of X[row, i] * Y[row, j]
 __global__ void __launch_bounds__(256) k_ts_gram(const double* __restrict__ X, int64_t ldx, int a,
                                                  const double* __restrict__ Y, int64_t ldy, int b, int64_t n,
                                                  double* __restrict__ part) {
   extern __shared__ double sm[];
-  constexpr int CH = 64;
-  double* xs = sm;           // CH * a
-  double* ys = sm + CH * a;  // CH * b
+  const int CH = ts_rows(a, b);
+  const int LD = CH + 1;     // padded row stride of a column tile (bank spread)
+  double* xs = sm;           // LD * a
+  double* ys = sm + LD * a;  // LD * b
   const int npair = a * b;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int64_t r0 = int64_t(blockIdx.x) * CH; r0 < n; r0 += int64_t(gridDim.x) * CH) {
@@ -48,11 +56,11 @@ __global__ void __launch_bounds__(256) k_ts_gram(const double* __restrict__ X, i
     __syncthreads();
     for (int t = threadIdx.x; t < CH * a; t += blockDim.x) {
       const int i = t / CH, r = t % CH;
-      xs[t] = r < rows ? X[r0 + r + ldx * i] : 0.0;
+      xs[i * LD + r] = r < rows ? X[r0 + r + ldx * i] : 0.0;
     }
     for (int t = threadIdx.x; t < CH * b; t += blockDim.x) {
       const int j = t / CH, r = t % CH;
-      ys[t] = r < rows ? Y[r0 + r + ldy * j] : 0.0;
+      ys[j * LD + r] = r < rows ? Y[r0 + r + ldy * j] : 0.0;
     }
     __syncthreads();
     for (int q = 0; q < 4; ++q) {
@@ -60,7 +68,7 @@ __global__ void __launch_bounds__(256) k_ts_gram(const double* __restrict__ X, i
       if (pidx >= npair) break;
       const int i = pidx % a, j = pidx / a;
       double s = acc[q];
-      for (int r = 0; r < CH; ++r) s = fma(xs[i * CH + r], ys[j * CH + r], s);
+      for (int r = 0; r < CH; ++r) s = fma(xs[i * LD + r], ys[j * LD + r], s);
       acc[q] = s;
     }
   }
@@ -102,9 +110,10 @@ Mat ts_gram(int dev, const double* X, int64_t ldx, int a, const double* Y, int64
     return out;
   }
   auto& c = ctx(dev);
-  const int blocks = std::max(1, std::min<int>(c.sm_count * 2, int((n + 63) / 64)));
+  const int ch = ts_rows(a, b);
+  const int blocks = std::max(1, std::min<int>(c.sm_count * 4, int((n + ch - 1) / ch)));
   DBuf<double> part(dev, size_t(blocks) * size_t(a) * size_t(b));
-  const size_t smem = size_t(64) * size_t(a + b) * sizeof(double);
+  const size_t smem = size_t(ch + 1) * size_t(a + b) * sizeof(double);
   k_ts_gram<<<blocks, 256, smem, c.stream>>>(X, ldx, a, Y, ldy, b, n, part.get());
   MPG_CHECK_LAUNCH();
   count_launch();
