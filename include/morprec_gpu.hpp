@@ -361,6 +361,55 @@ inline std::pair<BirkaState, ReductionReport> birka_reduce(const ShiftedOperator
   return {std::move(st), std::move(rep)};
 }
 
+// The same from an initial reduced state: the reference's `const BirkaState* init` (birka.hpp:78-80). Only
+// init.kr / fr / cr are read; an empty part keeps the default seed's.
+inline std::pair<BirkaState, ReductionReport> birka_reduce(const ShiftedOperator& op, const std::vector<double>& b,
+                                                           int m, const std::vector<double>& c, int q,
+                                                           const BirkaConfig& cfg, PrecondMode mode,
+                                                           const BirkaState& init) {
+  mpg_irka_cfg k{};
+  k.r = cfg.r;
+  k.tol = cfg.tol;
+  k.max_sweeps = cfg.max_sweeps;
+  k.decoupled = 1;
+  k.seed = cfg.seed;
+  k.gmres = cfg.gmres.c();
+  k.spai = cfg.spai.c();
+  k.max_chain_len = cfg.max_chain_len;
+  k.explicit_nnz_cap = 0;
+  k.standard_residual_max_dim = cfg.standard_residual_max_dim;
+  k.mirror_unstable = cfg.mirror_unstable;
+  const size_t r = static_cast<size_t>(cfg.r);
+  auto part = [](const std::vector<double>& v, size_t want, const char* what) -> const double* {
+    if (v.empty()) return nullptr;
+    if (v.size() != want) throw std::invalid_argument(std::string("birka: initial state dimensions do not match the system (") + what + ")");
+    return v.data();
+  };
+  const double* ikr = part(init.kr, r * r, "kr");
+  const double* ifr = part(init.fr, r * static_cast<size_t>(m), "fr");
+  const double* icr = part(init.cr, r * static_cast<size_t>(q), "cr");
+  BirkaState st;
+  st.order = cfg.r;
+  st.kr.resize(r * r);
+  st.er.resize(r * r);
+  st.ar.resize(r * r);
+  st.fr.resize(r * static_cast<size_t>(m));
+  st.cr.resize(r * static_cast<size_t>(q));
+  st.lambda_re.resize(r);
+  st.lambda_im.resize(r);
+  ReductionReport rep;
+  rep.rows.resize(2 * r * static_cast<size_t>(cfg.max_sweeps) + 8);
+  int sweeps = 0, conv = 0, nrows = 0;
+  check(mpg_irka_reduce_from(op.handle(), b.data(), m, c.data(), q, &k, static_cast<int>(mode), ikr, ifr, icr,
+                             st.kr.data(), st.fr.data(), st.cr.data(), st.er.data(), st.ar.data(),
+                             st.lambda_re.data(), st.lambda_im.data(), &sweeps, &conv, rep.rows.data(),
+                             static_cast<int>(rep.rows.size()), &nrows));
+  rep.rows.resize(static_cast<size_t>(std::min<int>(nrows, static_cast<int>(rep.rows.size()))));
+  st.sweeps = rep.sweeps = sweeps;
+  rep.converged = conv != 0;
+  return {std::move(st), std::move(rep)};
+}
+
 // birka_reduce (birka.hpp:78-80) for x' = K x + sum_j N_j x u_j + F u with couplings: joint n r solves
 // per side on the assembled Kronecker operator (mpg_birka_reduce).
 inline std::pair<BirkaState, ReductionReport> birka_reduce(const SparseMatrix& k,

@@ -218,6 +218,17 @@ int mpg_irka_reduce(const mpg_op* op, const double* b, int m, const double* c, i
                     double* lam_re, double* lam_im, double* v, double* w, int* sweeps, int* converged,
                     mpg_report_row* rows, int max_rows, int* nrows);
 
+/* The same from a caller-supplied initial reduced state: birka_reduce's
+ * `const BirkaState* init` argument (proj/include/morprec/birka.hpp:78-80,
+ * proj/src/birka.cpp:145). init_kr (r x r), init_fr (r x m), init_cr (r x q)
+ * column-major on the host; a NULL part keeps the default seed's
+ * (birka.cpp:41-89). A K_r with complex-conjugate eigenvalue pairs starts
+ * the iteration at complex shifts. */
+int mpg_irka_reduce_from(const mpg_op* op, const double* b, int m, const double* c, int q, const mpg_irka_cfg* cfg,
+                         int mode, const double* init_kr, const double* init_fr, const double* init_cr, double* kr,
+                         double* fr, double* cr, double* er, double* ar, double* lam_re, double* lam_im, int* sweeps,
+                         int* converged, mpg_report_row* rows, int max_rows, int* nrows);
+
 /* BIRKA with couplings N_1..N_m (birka_reduce, proj/src/birka.cpp:139-310;
  * the coupled path is the reference's joint solve): per sweep and side one
  * GMRES of order n r on the explicitly assembled Kronecker operator

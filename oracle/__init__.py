@@ -520,7 +520,7 @@ class IrkaResult:
 
 
 def irka_reduce(a: Csr, e: Optional[Csr], b, c, cfg: IrkaConfig, mode: int = 2, init_shifts=None,
-                want_bases: bool = False) -> IrkaResult:
+                want_bases: bool = False, init_kr=None) -> IrkaResult:
     n = a.shape[0]
     bm = np.asfortranarray(np.asarray(b, dtype=np.float64).reshape(n, -1))
     cm = np.asfortranarray(np.asarray(c, dtype=np.float64).reshape(n, -1))
@@ -536,6 +536,9 @@ def irka_reduce(a: Csr, e: Optional[Csr], b, c, cfg: IrkaConfig, mode: int = 2, 
     ini = None
     if init_shifts is not None:
         ini = np.asfortranarray(np.diag(-_f64(init_shifts)))
+    if init_kr is not None:  # birka_reduce's initial BirkaState (birka.hpp:78-80): K_r given, fr/cr default-seeded
+        ini = np.asfortranarray(np.asarray(init_kr, dtype=np.float64))
+        assert ini.shape == (cfg.r, cfg.r)
     cc = cfg.c()
     _check(lib.orc_irka_reduce(a._h, e._h if e else None, _p(bm), m, _p(cm), q, C.byref(cc), mode, _p(ini), None, None,
                                _p(kr), _p(fr), _p(cr), _p(er), _p(ar), _p(lre), _p(lim), _p(v), _p(w),

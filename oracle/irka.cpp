@@ -362,6 +362,10 @@ std::pair<IrkaState, ReductionReport> irka_reduce(const LinearSystem& sys, const
       const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
       std::fprintf(stderr, "[oracle irka] sweep %d: shift change %.3e, %ld GMRES iterations, %.1f s\n", z,
                    std::sqrt(num) / std::max(std::sqrt(den), 1e-300), its, el);
+      // the sweep's sorted reduced poles at full precision (long offline runs
+      // are read back sweep by sweep from this log)
+      for (size_t i = 0; i < lambda_new.size(); ++i)
+        std::fprintf(stderr, "[oracle irka] sweep %d lambda %zu %.17g %.17g\n", z, i, lambda_new[i].re, lambda_new[i].im);
     }
     lambda_prev = lambda_new;
   }

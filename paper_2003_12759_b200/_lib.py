@@ -154,6 +154,8 @@ _SIGS = {
     "mpg_gmres_batch": (_I, [vp, _I, vp, vp, vp, vp, vp, vp, C.POINTER(GmresCfg), vp]),
     "mpg_irka_reduce": (_I, [vp, vp, _I, vp, _I, C.POINTER(IrkaCfg), _I, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                              ip, ip, vp, _I, ip]),
+    "mpg_irka_reduce_from": (_I, [vp, vp, _I, vp, _I, C.POINTER(IrkaCfg), _I, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                  ip, ip, vp, _I, ip]),
     "mpg_birka_reduce": (_I, [vp, vp, vp, _I, vp, _I, C.POINTER(IrkaCfg), _I] + [vp] * 8
                           + [ip, ip, vp, _I, ip, C.POINTER(C.c_void_p)]),
     "mpg_irka_reduce_sharded": (_I, [vp, vp, _I, vp, _I, C.POINTER(IrkaCfg), _I, vp, _I, _I, ALLGATHER_FN, vp, vp,

@@ -154,7 +154,12 @@ int mpg_profile_read(int kind, const char** name, long long* launches, double* m
 }
 
 int mpg_copy(void* dst, const void* src, int64_t bytes) {
-  return guard([&] { MPG_CUDA(cudaMemcpy(dst, src, size_t(bytes), cudaMemcpyDefault)); });
+  // cudaMemcpy from pageable host memory returns once the data is staged, before the DMA into device memory
+  // has completed; the library reads the destination on its own (non-blocking) stream, so wait for the copy.
+  return guard([&] {
+    MPG_CUDA(cudaMemcpy(dst, src, size_t(bytes), cudaMemcpyDefault));
+    MPG_CUDA(cudaDeviceSynchronize());
+  });
 }
 
 // ---- matrices -------------------------------------------------------------------
@@ -427,6 +432,33 @@ int mpg_irka_reduce(const mpg_op* op, const double* b, int m, const double* c, i
     if (sweeps) *sweeps = r.sweeps;
     if (converged) *converged = r.converged;
     copy_rows(r.rows, rows, max_rows, nrows);
+  });
+}
+
+int mpg_irka_reduce_from(const mpg_op* op, const double* b, int m, const double* c, int q, const mpg_irka_cfg* cfg,
+                         int mode, const double* init_kr, const double* init_fr, const double* init_cr, double* kr,
+                         double* fr, double* cr, double* er, double* ar, double* lam_re, double* lam_im, int* sweeps,
+                         int* converged, mpg_report_row* rows, int max_rows, int* nrows) {
+  return guard([&] {
+    if (!cfg || cfg->r < 1) throw ConfigError("birka: reduced order must be at least 1");
+    IrkaSettings s = to_irka(cfg, mode, nullptr);
+    const size_t r = size_t(cfg->r);
+    if (init_kr) s.init_kr.assign(init_kr, init_kr + r * r);
+    if (init_fr) s.init_fr.assign(init_fr, init_fr + r * size_t(std::max(m, 0)));
+    if (init_cr) s.init_cr.assign(init_cr, init_cr + r * size_t(std::max(q, 0)));
+    IrkaResult res = irka_run(*op->p, b, m, c, q, s, 0, 1, nullptr, nullptr);
+    if (kr) std::memcpy(kr, res.kr.a.data(), res.kr.a.size() * 8);
+    if (fr) std::memcpy(fr, res.fr.a.data(), res.fr.a.size() * 8);
+    if (cr) std::memcpy(cr, res.cr.a.data(), res.cr.a.size() * 8);
+    if (er) std::memcpy(er, res.er.a.data(), res.er.a.size() * 8);
+    if (ar) std::memcpy(ar, res.ar.a.data(), res.ar.a.size() * 8);
+    for (size_t i = 0; i < res.lambda.size(); ++i) {
+      if (lam_re) lam_re[i] = res.lambda[i].re;
+      if (lam_im) lam_im[i] = res.lambda[i].im;
+    }
+    if (sweeps) *sweeps = res.sweeps;
+    if (converged) *converged = res.converged;
+    copy_rows(res.rows, rows, max_rows, nrows);
   });
 }
 

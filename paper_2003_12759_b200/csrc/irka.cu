@@ -372,6 +372,16 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
 
   Mat kr(r, r), fr(r, m), cr(r, q);
   default_seed(*op.a, cfg, kr, fr, cr, s);
+  {  // a caller-supplied initial state replaces the seed part by part (birka.cpp:145)
+    auto take = [](Mat& dst, const std::vector<double>& src, const char* what) {
+      if (src.empty()) return;
+      if (src.size() != dst.a.size()) throw ConfigError(std::string("birka: initial state dimensions do not match the system (") + what + ")");
+      dst.a = src;
+    };
+    take(kr, cfg.init_kr, "kr");
+    take(fr, cfg.init_fr, "fr");
+    take(cr, cfg.init_cr, "cr");
+  }
 
   IrkaResult res;
   res.reduced_order = r;
@@ -611,6 +621,12 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
       h[2] = fail.c0;
       h[3] = fail.rel;
       h[4] = fail.its;
+      // plan fingerprint: every rank must have derived the same units and owners
+      double fp = 0.0;
+      for (const Task& t : all) fp = std::fmod(fp * 31.0 + double(t.side * 4096 + t.c0 * 16 + t.w * 4 + t.owner % 4) + 1.0, 1e15);
+      h[5] = double(all.size());
+      h[6] = double(cmax);
+      h[7] = fp;
       for (size_t i = 0; i < mine.size(); ++i) h[8 + i] = its_mine[i];
       MPG_CUDA(cudaMemcpyAsync(send.get() + size_t(n) * size_t(cmax), h.data(), hdr * sizeof(double),
                                cudaMemcpyHostToDevice, s));
@@ -622,6 +638,13 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
         MPG_CUDA(cudaMemcpyAsync(hall.data() + hdr * size_t(o), recv.get() + blk * size_t(o) + size_t(n) * size_t(cmax),
                                  hdr * sizeof(double), cudaMemcpyDeviceToHost, s));
       MPG_CUDA(cudaStreamSynchronize(s));
+      for (int o = 0; o < world; ++o) {
+        const double* ho = hall.data() + hdr * size_t(o);
+        if (ho[5] != h[5] || ho[6] != h[6] || ho[7] != h[7])
+          throw SolverError("irka: rank " + std::to_string(o) + " and rank " + std::to_string(rank) +
+                            " derived different shard plans at sweep " + std::to_string(z) +
+                            " (their reduced matrices differ)");
+      }
       for (int o = 0; o < world && !fail.failed; ++o)
         if (hall[hdr * size_t(o)] != 0.0) {
           const double* ho = hall.data() + hdr * size_t(o);
@@ -668,6 +691,26 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
     kr = lu.solve(ar);
     fr = lu.solve(ts_gram(dev, Y.get(), n, r, B.get(), n, m, n));
     cr = ts_gram(dev, X.get(), n, r, C.get(), n, q, n);
+    if (allgather && world > 1) {
+      // Every rank projects redundantly; the ranks then adopt rank 0's reduced
+      // matrices bit for bit, so the next sweep's units, owner map and stop
+      // decision are identical everywhere whatever the ranks' rounding.
+      const size_t cnt = size_t(r) * size_t(r + m + q);
+      DBuf<double> sendr(dev, cnt), recvr(dev, cnt * size_t(world));
+      std::vector<double> pack;
+      pack.insert(pack.end(), kr.a.begin(), kr.a.end());
+      pack.insert(pack.end(), fr.a.begin(), fr.a.end());
+      pack.insert(pack.end(), cr.a.begin(), cr.a.end());
+      MPG_CUDA(cudaMemcpyAsync(sendr.get(), pack.data(), cnt * 8, cudaMemcpyHostToDevice, s));
+      MPG_CUDA(cudaStreamSynchronize(s));
+      if (allgather(agctx, sendr.get(), recvr.get(), int64_t(cnt) * 8) != 0)
+        throw CudaError("irka: allgather callback failed");
+      MPG_CUDA(cudaMemcpyAsync(pack.data(), recvr.get(), cnt * 8, cudaMemcpyDeviceToHost, s));
+      MPG_CUDA(cudaStreamSynchronize(s));
+      std::copy(pack.begin(), pack.begin() + long(kr.a.size()), kr.a.begin());
+      std::copy(pack.begin() + long(kr.a.size()), pack.begin() + long(kr.a.size() + fr.a.size()), fr.a.begin());
+      std::copy(pack.begin() + long(kr.a.size() + fr.a.size()), pack.end(), cr.a.begin());
+    }
     res.er = er;
     res.ar = ar;
     sweeps_done = z;
@@ -683,6 +726,9 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
     if (timing)
       std::fprintf(stderr, "irka sweep %d: %.3f s (setup+builds %.3f, gmres %.3f, rest %.3f), max its %d\n", z,
                    wall() - tz0, t_build, t_gmres, wall() - tz0 - t_build - t_gmres, sweep_max_its);
+    if (timing)
+      for (size_t i = 0; i < lambda_new.size(); ++i)
+        std::fprintf(stderr, "irka sweep %d lambda %zu %.17g %.17g\n", z, i, lambda_new[i].re, lambda_new[i].im);
   }
   res.kr = kr;
   res.fr = fr;

@@ -20,6 +20,9 @@ struct IrkaSettings {
   long long standard_residual_max_dim = 5000;
   int mode = MPG_PRECOND_REUSE_CHAIN;
   std::vector<double> init_shifts;  // empty: default seed (power iteration)
+  // Initial reduced state (birka_reduce's `const BirkaState* init`, birka.hpp:78-80),
+  // column-major; each empty part keeps the default seed's. init_kr (r x r) wins over init_shifts.
+  std::vector<double> init_kr, init_fr, init_cr;
   bool want_vw = false;
   bool mirror_unstable = false;
 };

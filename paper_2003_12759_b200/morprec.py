@@ -556,8 +556,13 @@ def _rows(buf, n):
 
 
 def irka_reduce(op: ShiftedOperator, b, c, cfg: IrkaConfig, mode: int = PrecondMode.REUSE_CHAIN,
-                init_shifts=None, want_bases: bool = False):
-    """IRKA (BIRKA with N = 0, birka.cpp:139-310) on the GPU; returns (IrkaState, ReductionReport)."""
+                init_shifts=None, want_bases: bool = False, init=None):
+    """IRKA (BIRKA with N = 0, birka.cpp:139-310) on the GPU; returns (IrkaState, ReductionReport).
+    `init` = (kr, fr, cr), any part None: the reference's initial `BirkaState` (birka.hpp:78-80)."""
+    if init is not None:
+        if init_shifts is not None or want_bases:
+            raise ValueError("irka_reduce: init excludes init_shifts and want_bases")
+        return _irka_reduce_from(op, b, c, cfg, mode, init)
     n = op.n
     bm = np.asfortranarray(np.asarray(b, dtype=np.float64).reshape(n, -1))
     cm = np.asfortranarray(np.asarray(c, dtype=np.float64).reshape(n, -1))
@@ -578,6 +583,39 @@ def irka_reduce(op: ShiftedOperator, b, c, cfg: IrkaConfig, mode: int = PrecondM
                               L.ptr(w) if w is not None else None, C.byref(sweeps), C.byref(conv), rows, maxrows,
                               C.byref(nrows)))
     st = IrkaState(kr, fr, cr, er, ar, lre + 1j * lim, v, w, sweeps.value)
+    rep = ReductionReport(_rows(rows, min(nrows.value, maxrows)), bool(conv.value), r, sweeps.value)
+    if not rep.converged:
+        rep.warnings.append(f"fixed point left unconverged after {sweeps.value} sweeps")
+    return st, rep
+
+
+def _irka_reduce_from(op, b, c, cfg, mode, init):
+    n = op.n
+    bm = np.asfortranarray(np.asarray(b, dtype=np.float64).reshape(n, -1))
+    cm = np.asfortranarray(np.asarray(c, dtype=np.float64).reshape(n, -1))
+    m, q, r = bm.shape[1], cm.shape[1], cfg.r
+    shapes = ((r, r), (r, m), (r, q))
+    ini = []
+    for part, shape, name in zip(init, shapes, ("kr", "fr", "cr")):
+        if part is None:
+            ini.append(None)
+            continue
+        a = np.asfortranarray(np.asarray(part, dtype=np.float64))
+        if a.shape != shape:
+            raise ValueError(f"irka_reduce: initial {name} must be {shape[0]} x {shape[1]}")
+        ini.append(a)
+    kr, er, ar = (np.zeros((r, r), order="F") for _ in range(3))
+    fr, cr = np.zeros((r, m), order="F"), np.zeros((r, q), order="F")
+    lre, lim = np.zeros(r), np.zeros(r)
+    sweeps, conv, nrows = C.c_int(), C.c_int(), C.c_int()
+    maxrows = 2 * r * max(cfg.max_sweeps, 1) + 8
+    rows = (L.ReportRow * maxrows)()
+    cc = cfg.c()
+    check(lib.mpg_irka_reduce_from(op._h, L.ptr(bm), m, L.ptr(cm), q, C.byref(cc), mode,
+                                   *[L.ptr(a) if a is not None else None for a in ini], L.ptr(kr), L.ptr(fr),
+                                   L.ptr(cr), L.ptr(er), L.ptr(ar), L.ptr(lre), L.ptr(lim), C.byref(sweeps),
+                                   C.byref(conv), rows, maxrows, C.byref(nrows)))
+    st = IrkaState(kr, fr, cr, er, ar, lre + 1j * lim, None, None, sweeps.value)
     rep = ReductionReport(_rows(rows, min(nrows.value, maxrows)), bool(conv.value), r, sweeps.value)
     if not rep.converged:
         rep.warnings.append(f"fixed point left unconverged after {sweeps.value} sweeps")

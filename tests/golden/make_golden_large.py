@@ -158,6 +158,109 @@ def stage_c3irka(O, gen):
     _dump("c3_irka.json", out)
 
 
+def block_kr(poles):
+    """Real block-diagonal K_r with the given eigenvalues (conjugate pairs adjacent): [a] or [[a, b], [-b, a]]."""
+    poles = list(poles)
+    r = len(poles)
+    kr = np.zeros((r, r))
+    i = 0
+    while i < r:
+        z = complex(poles[i])
+        if z.imag == 0.0:
+            kr[i, i] = z.real
+            i += 1
+        else:
+            assert i + 1 < r and abs(complex(poles[i + 1]) - z.conjugate()) <= 1e-12 * abs(z), "pairs must be adjacent"
+            b = abs(z.imag)
+            kr[i, i] = kr[i + 1, i + 1] = z.real
+            kr[i, i + 1], kr[i + 1, i] = b, -b
+            i += 2
+    return kr
+
+
+def _irka_from(O, s, kr0, gtol, tol, max_sweeps, threads, mirror=True):
+    """Oracle IRKA from the initial reduced state matrix kr0 (birka.hpp:78-80), with the
+    per-sweep poles read back from the oracle's verbose log (stderr)."""
+    import re
+    import tempfile
+    r = kr0.shape[0]
+    a = O.Csr.of(s.a)
+    ec = s.e_csr()
+    e = O.Csr.of(ec) if ec is not None else None
+    cfg = O.IrkaConfig(r=r, tol=tol, max_sweeps=max_sweeps, seed=1, gmres=O.GmresConfig(gtol, 1000),
+                       spai=O.SpaiConfig(threads=threads), explicit_nnz_cap=10 ** 12, decoupled=True,
+                       mirror_unstable=mirror, unit_threads=threads)
+    os.environ["ORC_IRKA_VERBOSE"] = "1"
+    sys.stderr.flush()
+    saved = os.dup(2)
+    with tempfile.TemporaryFile(mode="w+b") as tf:
+        os.dup2(tf.fileno(), 2)
+        t0 = time.time()
+        try:
+            res = O.irka_reduce(a, e, s.b, s.c, cfg, mode=3, init_kr=kr0)
+        finally:
+            wall = time.time() - t0
+            os.dup2(saved, 2)
+            os.close(saved)
+        tf.seek(0)
+        log = tf.read().decode()
+    sys.stderr.write(log)
+    traj = {}
+    for mt in re.finditer(r"sweep (\d+) lambda (\d+) (\S+) (\S+)", log):
+        traj.setdefault(int(mt.group(1)), []).append([float(mt.group(3)), float(mt.group(4))])
+    lam = np.sort_complex(res.lam)
+    hr = np.array([res.transfer(1j * w) for w in GRID])
+    return {"converged": res.converged, "sweeps": res.sweeps, "r": r, "mode": 3, "mirror_unstable": mirror,
+            "gmres_tol": gtol, "irka_tol": tol, "max_sweeps": max_sweeps, "init_kr": kr0.tolist(),
+            "poles_by_sweep": [traj[k] for k in sorted(traj)],
+            "shifts_re": [-float(z.real) for z in lam], "shifts_im": [-float(z.imag) for z in lam],
+            "grid": GRID.tolist(), "hr_re": hr.real.reshape(len(GRID), -1).tolist(),
+            "hr_im": hr.imag.reshape(len(GRID), -1).tolist(),
+            "solves": sum(rw.solves for rw in res.rows), "gmres_iterations": int(sum(rw.iterations for rw in res.rows)),
+            "oracle_wall_s": round(wall, 1), "oracle_threads": threads, "host": _host()}
+
+
+def stage_c2fix(O, gen):
+    """C2 from a well-separated start: the oracle's converged poles (c2_irka.json) with each unit moved by
+    -0.1 / 0 / +0.1 % in turn. The BASELINE seed's first sweep (shifts 1e-3 ... 1e2, all far below the pencil's
+    smallest eigenvalue ~ 30) has a numerically rank-deficient basis, so which fixed point a run reaches from
+    it is decided by rounding; from separated shifts the sweep map is well conditioned and GPU and oracle can
+    be compared sweep by sweep."""
+    g = json.load(open(os.path.join(HERE, "c2_irka.json")))
+    poles = sorted((-complex(a, b) for a, b in zip(g["shifts_re"], g["shifts_im"])), key=lambda z: (z.real, abs(z.imag), z.imag))
+    out_poles, unit = [], 0
+    i = 0
+    while i < len(poles):
+        f = 1.0 + 1e-3 * ((unit % 3) - 1)
+        if poles[i].imag != 0.0:
+            z = complex(poles[i].real, abs(poles[i].imag)) * f
+            out_poles += [z.conjugate(), z]
+            i += 2
+        else:
+            out_poles.append(poles[i] * f)
+            i += 1
+        unit += 1
+    out = _irka_from(O, gen.config2(), block_kr(out_poles), 1e-10, 1e-8, 40, THREADS)
+    out["config"] = ("C2 64^3 (n=262144), r=8, frozen SPAI, mirrored, gmres 1e-10, irka tol 1e-8, started at the "
+                     "c2_irka.json poles moved by -0.1/0/+0.1 % per unit")
+    _dump("c2_irka_fix.json", out)
+
+
+def stage_c3fix(O, gen):
+    """C3: the oracle's sweep map at the GPU's converged poles. A full oracle IRKA from the BASELINE seed
+    needs ~22 sweeps of 16 n = 1.19 M solves (days of CPU); instead the oracle starts at the poles the GPU run
+    of bench.py's irka leg converged to (tol 1e-6; GOLDEN_C3_POLES or the list below, 8 significant digits)
+    and runs 2 sweeps at GMRES 1e-10. For SISO the spans depend only on the shifts, so if the GPU's poles are
+    a fixed point of the reference iteration the oracle must return them: sweep 1 within the GPU run's own
+    stopping error, sweep 2 tighter."""
+    default = "-492.85920-503.52230j,-492.85920+503.52230j,-275.68421-112.12564j,-275.68421+112.12564j,-168.58100,-53.881916,-14.902654,-0.79090863"
+    poles = [complex(t) for t in os.environ.get("GOLDEN_C3_POLES", default).split(",")]
+    out = _irka_from(O, gen.config3(), block_kr(poles), 1e-10, 1e-8, int(os.environ.get("GOLDEN_C3_SWEEPS", 2)), THREADS)
+    out["config"] = ("C3 106^3 nodes (n=1191016), r=8, frozen SPAI, mirrored, gmres 1e-10, started at the poles the "
+                     "GPU IRKA (bench.py irka leg, tol 1e-6) converged to, 2 oracle sweeps")
+    _dump("c3_irka_fix.json", out)
+
+
 def stage_c5(O, gen):
     n = int(os.environ.get("GOLDEN_C5_N", 100_000))
     s = gen.config5(n=n, max_len=2000)

@@ -46,7 +46,7 @@ def _spawn(fn, world, *args):
     procs = [ctx.Process(target=fn, args=(r, world, port, q) + args) for r in range(world)]
     for p in procs:
         p.start()
-    outs = [q.get(timeout=600) for _ in procs]
+    outs = [q.get(timeout=240) for _ in procs]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
