@@ -81,6 +81,8 @@ struct GmSolve {
   double* dp;  // pending second-pass coefficients (the previous iteration's probe d)
   double* hg;  // this iteration's Hessenberg column (h holds the update coefficients)
   double* Hu;  // unrotated Hessenberg columns, column i at hoff2(i), i + 2 entries
+  float** F;   // single-precision shadow of the basis (null: none): F[j] row r at fidx(r)
+  const CUtensorMap* tmf;  // per shadow panel: [2 p] 64-vector box, [2 p + 1] 8-vector box
 };
 __host__ __device__ __forceinline__ size_t hoff2(int i) { return size_t(i) * size_t(i + 3) / 2; }
 
@@ -516,17 +518,15 @@ __global__ void __launch_bounds__(256) k_spmv_il2(GmSolve* S, Group grp, CsrView
 // step j's column index and value of the warp's 8 rows are 8 consecutive slots,
 // so each is one request per warp instead of 8 scattered ones.
 template <int EM, bool CHAIN>
-__global__ void __launch_bounds__(256) k_spmv_sell8(GmSolve* S, Group grp, Sell8View sv, OpView op,
-                                                    const double* __restrict__ xin, double* __restrict__ xout) {
-  if (!il_any_run(S, grp)) return;
+__device__ __forceinline__ void sell8_rows(GmSolve* S, const Group& grp, const Sell8View& sv, const OpView& op,
+                                           const double* __restrict__ xin, double* __restrict__ xout, int row) {
   const int lane = threadIdx.x & 3;
-  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) >> 2);
   if (row >= sv.nrows) return;
   const int e0 = __ldg(sv.sptr + (row >> 3)) + (row & 7);
   const int w = (__ldg(sv.sptr + (row >> 3) + 1) - __ldg(sv.sptr + (row >> 3))) >> 3;
   const double* xl = xin + 2 * lane;
   double a0 = 0.0, a1 = 0.0, g0 = 0.0, g1 = 0.0;
-#pragma unroll 4
+#pragma unroll 8
   for (int j = 0; j < w; ++j) {
     const int e = e0 + 8 * j;
     const int c = __ldcs(sv.col + e);
@@ -560,6 +560,52 @@ __global__ void __launch_bounds__(256) k_spmv_sell8(GmSolve* S, Group grp, Sell8
     GmSolve& st = S[grp.idx[q]];
     if (st.phase != PH_RUN) continue;
     st.V[st.k + 1][vidx(row)] = st.scale[st.k] * (st.sre * (h ? g1 : g0) + st.ca * (h ? a1 : a0));
+  }
+}
+
+template <int EM, bool CHAIN>
+__global__ void __launch_bounds__(256) k_spmv_sell8(GmSolve* S, Group grp, Sell8View sv, OpView op,
+                                                    const double* __restrict__ xin, double* __restrict__ xout) {
+  if (!il_any_run(S, grp)) return;
+  sell8_rows<EM, CHAIN>(S, grp, sv, op, xin, xout, int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) >> 2));
+}
+
+// SM-affine persistent form: the 64-row blocks are split into one contiguous range per SM, and the CTAs
+// resident on an SM take that SM's blocks in order (an atomic cursor per SM; an SM that runs dry steals from
+// the others, so every block is done wherever the CTAs land). Rows that are neighbours in the mesh -- the
+// +-1 line and +-1 plane entries of a stencil row -- are then gathered by the same SM within a short time,
+// so the x-gather hits L1 instead of L2 (with the plain block order the co-resident CTAs of an SM are 148
+// blocks apart and share nothing). ctr: [nsm + 1] zero on entry; the last CTA to finish zeroes it again.
+template <int EM, bool CHAIN>
+__global__ void __launch_bounds__(256) k_spmv_sell8p(GmSolve* S, Group grp, Sell8View sv, OpView op,
+                                                     const double* __restrict__ xin, double* __restrict__ xout,
+                                                     int* ctr, int nsm) {
+  __shared__ int blk_s;
+  if (il_any_run(S, grp)) {
+    const int nblk = (sv.nrows + 63) / 64;
+    const int per = (nblk + nsm - 1) / nsm;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    for (int v = 0; v < nsm; ++v) {
+      const int victim = int((smid + unsigned(v)) % unsigned(nsm));
+      const int base = victim * per, lim = min(per, nblk - base);
+      while (true) {
+        __syncthreads();
+        if (threadIdx.x == 0) blk_s = lim > 0 ? atomicAdd(ctr + victim, 1) : lim;
+        __syncthreads();
+        const int blk = blk_s;
+        if (blk >= lim) break;
+        sell8_rows<EM, CHAIN>(S, grp, sv, op, xin, xout, (base + blk) * 64 + int(threadIdx.x >> 2));
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + nsm, 1) == int(gridDim.x) - 1) {
+      for (int v = 0; v <= nsm; ++v) ctr[v] = 0;
+      __threadfence();
+    }
   }
 }
 
@@ -1806,6 +1852,344 @@ __global__ void __launch_bounds__(GX_THREADS, 1) k_gs_tmx(GmSolve* S, int ns, in
     }
 }
 
+// ---- projection from a single-precision shadow of the basis -------------------------
+// With the delayed second pass every iteration's new direction is measured against
+// the basis by the update pass (the probe d = Q^T w_new, from the fp64 basis) and
+// corrected by the next projection pass, so the first projection only has to remove
+// most of the component in span(Q): its coefficients need a few digits, not sixteen.
+// k_gs_tmxf therefore projects w on a float copy of the basis -- half the bytes of
+// the pass -- while everything that defines the Arnoldi relation stays in fp64: the
+// update pass subtracts the fp64 vectors, the probe is exact, H gets h~ + d, and the
+// correction of V[k] (size ||d|| ~ 1e-7 ||w||) taken from the float copy is wrong by
+// ~1e-7 ||d||, the same order as fp64 rounding.
+// Shadow layout: panels [ld / 32][64][32] floats, i.e. 128 B per vector and chunk like
+// the fp64 panels, so the tile geometry, the 128-byte swizzle and the ring of k_gs_tmx
+// carry over with 32-row chunks: consumer warp q owns row quad q of every chunk (one
+// float4 per vector). Columns 0..k-1 come from the shadow; w = W_{k+1} and V[k] (whose
+// shadow does not exist yet: it may still await its correction) are staged in fp64 by
+// 128-byte bulk copies. The kernel writes V[k]'s correction (fp64) and its shadow.
+constexpr int FCHUNK = 32;
+__host__ __device__ __forceinline__ int fidx(int r) { return (r / FCHUNK) * (PANEL * FCHUNK) + (r % FCHUNK); }
+constexpr int GF_EXTRA = 512;  // per chunk and stage: 32 rows of w and of V[k] in fp64
+constexpr int GF_SMEM = 1024 + GX_RING + (GX_CWARPS * GX_MAXV + 2 * GX_CWARPS) * 8 + 2 * GX_MAXST * 8;
+
+__device__ __forceinline__ int gf_chunks(const GmSolve& st) { return ((st.n + 31) & ~31) / FCHUNK; }
+__device__ __forceinline__ void bulk_g2s_a(uint32_t dst, const void* src, unsigned bytes, uint32_t mbar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(mbar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ float4 lds_f32x4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+
+struct GfCursor {
+  int s = -1, nt = 0;
+  long long off = 0;
+  UpdSel us;
+  __device__ __forceinline__ void seek(const GmSolve* S, int ns, int TC, long long g) {
+    while (s < ns && (s < 0 || g >= off + nt)) {
+      if (s >= 0) off += nt;
+      ++s;
+      while (s < ns && !gx_handles(S[s], us)) ++s;
+      nt = s < ns ? (gf_chunks(S[s]) + TC - 1) / TC : 0;
+    }
+  }
+};
+
+// Stage: the shadow tile as in k_gs_tmx (chunk cc of full panel p at (p TC + cc) 8 KB,
+// the last panel's 8-vector boxes behind), then per chunk 512 B: w rows, V[k] rows.
+__device__ __forceinline__ void gf_producer(GmSolve* S, int ns, int TC, int tile_bytes, int stage_bytes, int NS,
+                                            long long a, long long b, uint32_t ring, uint64_t* full, uint64_t* empty,
+                                            UpdSel us) {
+  const int lane = threadIdx.x & 31;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  GfCursor pc;
+  pc.us = us;
+  const CUtensorMap* tm = nullptr;
+  const double* w = nullptr;
+  const double* vk = nullptr;
+  int nv = 0, nchunks = 0, stg = 0;
+  unsigned eph = 0;
+  for (long long g = a; g < b; ++g) {
+    if (g - a >= NS) mbar_wait(empty + stg, eph);
+    if (pc.s < 0 || g >= pc.off + pc.nt) {
+      pc.seek(S, ns, TC, g);
+      const GmSolve& st = S[pc.s];
+      tm = st.tmf;
+      nv = st.k;  // shadow columns 0 .. k - 1
+      nchunks = gf_chunks(st);
+      w = st.V[st.k + 1];
+      vk = st.V[st.k];
+    }
+    const int c0 = int(g - pc.off) * TC;
+    const int nch = min(TC, nchunks - c0);
+    const int pf = nv >> 6, mb = ((nv & 63) + 7) >> 3;
+    const int per = pf + mb + 4;
+    if (lane == 0) mbar_expect_tx(full + stg, unsigned(nch) * unsigned(pf * 8192 + mb * 1024 + GF_EXTRA));
+    __syncwarp();
+    const uint32_t base = ring + uint32_t(stg) * uint32_t(stage_bytes);
+    const uint32_t mbar = smem_u32(full + stg);
+    for (int op = lane; op < nch * per; op += 32) {
+      const int q = op / per, t = op - q * per;
+      if (t < pf) {
+        tma3_g2s(base + uint32_t(t * TC + q) * 8192u, tm + 2 * t, 0, c0 + q, mbar, pol);
+      } else if (t < pf + mb) {
+        tma3_g2s(base + uint32_t(pf * TC) * 8192u + uint32_t(q * mb + t - pf) * 1024u, tm + 2 * pf + 1, 8 * (t - pf),
+                 c0 + q, mbar, pol);
+      } else {
+        const int e = t - pf - mb;  // 0, 1: w; 2, 3: V[k] (the two 16-row fp64 chunks of this 32-row chunk)
+        const double* src = (e < 2 ? w : vk) + size_t(2 * (c0 + q) + (e & 1)) * size_t(PANEL * CHUNK);
+        bulk_g2s_a(base + uint32_t(tile_bytes) + uint32_t(q) * uint32_t(GF_EXTRA) + uint32_t(e) * 128u, src, 128u, mbar,
+                   pol);
+      }
+    }
+    if (++stg == NS) {
+      stg = 0;
+      if (g - a >= NS) eph ^= 1u;
+    }
+  }
+}
+
+// Arithmetic: the pass is issue-bound if every float is widened (4 F2F + 8 DFMA per lane and vector), so the
+// four rows of a quad are contracted with single-precision FMAs -- the products already carry the shadow's
+// 6e-8 rounding -- and only the 4-term partial is widened and accumulated in fp64; the correction's row sums
+// (coefficients ~1e-7, a few digits needed) are summed in single precision across the warp.
+template <int CF, int NGT>
+__device__ __forceinline__ void gf_consumer(GmSolve* S, int ns, int G, int TC, int tile_bytes, int stage_bytes, int NS,
+                                            long long a, long long b, uint32_t ring, uint64_t* full, uint64_t* empty,
+                                            double* red2, double* red3, UpdSel us) {
+  constexpr int NGC = NGT / CF;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int rq = warp;  // row quad of a 32-row chunk
+  const int slot = blockIdx.x;
+  const uint32_t loff = uint32_t(lane) * 128u + uint32_t((rq ^ (lane & 7)) << 4);
+  GfCursor cu;
+  cu.us = us;
+  float coef[NGC];
+  double acc[NGC];
+  double wsq = 0.0, acck = 0.0;  // lanes 0..3: row lane of the quad
+  double* vk = nullptr;
+  float* fk = nullptr;
+  bool pend = false;
+  int nj = 0, nv = 0, nchunks = 0, n = 0, pf = 0, mb = 0;
+  long long seg_end = -1;
+  int stg = 0;
+  unsigned fph = 0;
+  for (long long g = a; g < b; ++g) {
+    if (g >= seg_end) {  // first tile of a solve in this CTA
+      cu.seek(S, ns, TC, g);
+      seg_end = min(b, cu.off + cu.nt);
+      const GmSolve& st = S[cu.s];
+      nj = st.k + 1;
+      nv = nj - 1;
+      n = st.n;
+      nchunks = gf_chunks(st);
+      pf = nv >> 6;
+      mb = ((nv & 63) + 7) >> 3;
+      pend = st.pend != 0;
+      vk = st.V[nj - 1];
+      fk = st.F[nj - 1];
+#pragma unroll
+      for (int i = 0; i < NGC; ++i) {
+        const int j = 32 * i + lane;
+        coef[i] = (pend && j < nv) ? float(st.scale[j] * st.dp[j]) : 0.f;  // the correction coefficients of V[k]
+        acc[i] = 0.0;
+      }
+      wsq = 0.0;
+      acck = 0.0;
+    }
+    const int c0 = int(g - cu.off) * TC;
+    mbar_wait(full + stg, fph);
+    const uint32_t sbase = ring + uint32_t(stg) * uint32_t(stage_bytes);
+    for (int cc0 = 0; cc0 < TC; cc0 += CF) {
+      if (c0 + cc0 >= nchunks) break;
+      float sx[CF][4];
+      float wf[CF][4];
+      float4 v[CF][NGC];
+#pragma unroll
+      for (int f = 0; f < CF; ++f) {
+        const int cc = cc0 + f;
+        const bool ok = c0 + cc < nchunks;
+        const uint32_t cb = sbase + uint32_t(cc) * 8192u;
+        const uint32_t pb = sbase + uint32_t(pf * TC) * 8192u + uint32_t(cc * mb) * 1024u;
+        const uint32_t xb = sbase + uint32_t(tile_bytes) + uint32_t(cc) * uint32_t(GF_EXTRA) + uint32_t(rq) * 32u;
+#pragma unroll
+        for (int i = 0; i < NGC; ++i) {
+          const uint32_t ad =
+              ((i >> 1) < pf ? cb + uint32_t((i >> 1) * TC) * 8192u : pb) + uint32_t(i & 1) * 4096u + loff;
+          v[f][i] = ok && 32 * i + lane < nv ? lds_f32x4(ad) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        const double2 wlo = ok ? lds_f64x2(xb) : make_double2(0.0, 0.0);
+        const double2 whi = ok ? lds_f64x2(xb + 16u) : make_double2(0.0, 0.0);
+        wf[f][0] = float(wlo.x);
+        wf[f][1] = float(wlo.y);
+        wf[f][2] = float(whi.x);
+        wf[f][3] = float(whi.y);
+        float x0 = 0.f, x1 = 0.f, x2 = 0.f, x3 = 0.f;
+        if (pend) {
+#pragma unroll
+          for (int i = 0; i < NGC; ++i) {
+            x0 = fmaf(coef[i], v[f][i].x, x0);
+            x1 = fmaf(coef[i], v[f][i].y, x1);
+            x2 = fmaf(coef[i], v[f][i].z, x2);
+            x3 = fmaf(coef[i], v[f][i].w, x3);
+          }
+        }
+        sx[f][0] = x0;
+        sx[f][1] = x1;
+        sx[f][2] = x2;
+        sx[f][3] = x3;
+      }
+      if (pend) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int f = 0; f < CF; ++f)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sx[f][u] += __shfl_xor_sync(0xffffffffu, sx[f][u], o);
+      }
+#pragma unroll
+      for (int f = 0; f < CF; ++f) {
+        const int cc = cc0 + f;
+        if (lane < 4 && c0 + cc < nchunks) {
+          // row `lane` of the quad: V[k] staged (uncorrected) for h'_k, corrected to global, shadow written
+          const uint32_t xb = sbase + uint32_t(tile_bytes) + uint32_t(cc) * uint32_t(GF_EXTRA) + uint32_t(rq) * 32u +
+                              uint32_t(lane) * 8u;
+          double wv, yv;
+          asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(wv) : "r"(xb));
+          asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(yv) : "r"(xb + 256u));
+          acck = fma(yv, wv, acck);
+          wsq = fma(wv, wv, wsq);
+          const float sl = lane == 0 ? sx[f][0] : lane == 1 ? sx[f][1] : lane == 2 ? sx[f][2] : sx[f][3];
+          const double uv = yv - double(sl);
+          const int row = (c0 + cc) * FCHUNK + 4 * rq + lane;
+          if (row < n) {
+            if (pend) vk[vidx(row)] = uv;
+            fk[fidx(row)] = float(uv);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < NGC; ++i) {
+          const float pr = fmaf(v[f][i].x, wf[f][0], fmaf(v[f][i].y, wf[f][1], fmaf(v[f][i].z, wf[f][2], v[f][i].w * wf[f][3])));
+          acc[i] += double(pr);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + stg);
+    if (++stg == NS) {
+      stg = 0;
+      fph ^= 1u;
+    }
+    if (g + 1 == seg_end) {  // flush this solve's partials
+      GmSolve& st = S[cu.s];
+#pragma unroll
+      for (int i = 0; i < NGC; ++i)
+        if (32 * i + lane < nv) red2[warp * GX_MAXV + 32 * i + lane] = acc[i];
+      const double wsum = warp_sum(wsq), ksum = warp_sum(acck);
+      if (lane == 0) {
+        red3[warp] = wsum;
+        red3[GX_CWARPS + warp] = ksum;
+      }
+      consumers_bar();
+      for (int j = tid; j < nv; j += GX_CWARPS * 32) {
+        double y = 0.0;
+        for (int q = 0; q < GX_CWARPS; ++q) y += red2[q * GX_MAXV + j];
+        st.part[size_t(j) * G + slot] = y;
+      }
+      if (tid < 2) {
+        double y = 0.0;
+        for (int q = 0; q < GX_CWARPS; ++q) y += red3[tid * GX_CWARPS + q];
+        st.part[size_t(tid == 0 ? nj : nv) * G + slot] = y;
+      }
+      consumers_bar();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(GX_THREADS, 1) k_gs_tmxf(GmSolve* S, int ns, int G, UpdSel us) {
+  extern __shared__ __align__(1024) char smx[];
+  const uint32_t raw = smem_u32(smx);
+  const uint32_t ring = (raw + 1023u) & ~1023u;
+  char* gen = smx + (ring - raw);
+  double* red2 = reinterpret_cast<double*>(gen + GX_RING);  // [warps][GX_MAXV]
+  double* red3 = red2 + GX_CWARPS * GX_MAXV;                 // [2][warps]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red3 + 2 * GX_CWARPS);
+  uint64_t* empty = full + GX_MAXST;
+  const int slot = blockIdx.x, nslots = gridDim.x;
+  int nvmax = 0;
+  for (int s = 0; s < ns; ++s)
+    if (gx_handles(S[s], us)) nvmax = max(nvmax, S[s].k);
+  bool any = false;
+  for (int s = 0; s < ns; ++s) any = any || gx_handles(S[s], us);
+  if (!any) return;
+  const int chunk_bytes = (nvmax >> 6) * 8192 + (((nvmax & 63) + 7) >> 3) * 1024;
+  const int CF = nvmax <= 192 ? 2 : 1;
+  int TC = 1;
+  while (TC < 16 && (TC < CF || 2 * TC * (chunk_bytes + GF_EXTRA) <= 48 * 1024)) TC *= 2;
+  const int tile_bytes = TC * chunk_bytes;
+  const int stage_bytes = (tile_bytes + TC * GF_EXTRA + 1023) & ~1023;
+  const int NS = min(GX_MAXST, GX_RING / stage_bytes);
+  long long total = 0;
+  for (int s = 0; s < ns; ++s)
+    if (gx_handles(S[s], us)) total += (gf_chunks(S[s]) + TC - 1) / TC;
+  const long long per = (total + nslots - 1) / nslots;
+  const long long a = min(total, per * slot), b = min(total, a + per);
+  {
+    long long off = 0;
+    for (int s = 0; s < ns; ++s) {
+      if (!gx_handles(S[s], us)) continue;
+      const long long nt = (gf_chunks(S[s]) + TC - 1) / TC;
+      if (!(a < off + nt && off < b)) {
+        const int nj = S[s].k + 1;
+        for (int j = int(threadIdx.x); j <= nj; j += GX_THREADS) S[s].part[size_t(j) * G + slot] = 0.0;
+      }
+      off += nt;
+    }
+  }
+  if (a >= b) return;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, GX_CWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x >= GX_CWARPS * 32)
+    gf_producer(S, ns, TC, tile_bytes, stage_bytes, NS, a, b, ring, full, empty, us);
+  else if (CF == 2) {
+    if (nvmax <= 128)
+      gf_consumer<2, 8>(S, ns, G, TC, tile_bytes, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+    else if (nvmax <= 160)
+      gf_consumer<2, 10>(S, ns, G, TC, tile_bytes, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+    else
+      gf_consumer<2, 12>(S, ns, G, TC, tile_bytes, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+  } else {
+    if (nvmax <= 256)
+      gf_consumer<1, 8>(S, ns, G, TC, tile_bytes, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+    else if (nvmax <= 320)
+      gf_consumer<1, 10>(S, ns, G, TC, tile_bytes, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+    else
+      gf_consumer<1, 12>(S, ns, G, TC, tile_bytes, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+  }
+}
+
+// Shadow of V[k] for the solves whose projection runs in a fp64 kernel this iteration
+// (V[k] is final there: no correction is pending); k_gs_tmxf writes the others'.
+__global__ void __launch_bounds__(256) k_shadow(GmSolve* S, UpdSel ps) {
+  GmSolve& st = S[blockIdx.y];
+  if (st.phase != PH_RUN || st.F == nullptr || gx_proj_owner(st, ps)) return;
+  const double* v = st.V[st.k];
+  float* f = st.F[st.k];
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < st.n; r += gridDim.x * blockDim.x) f[fidx(r)] = float(v[vidx(r)]);
+}
+
 // ---- norm partials of the residual buffer ----------------------------------------
 __global__ void __launch_bounds__(256) k_rnorm(GmSolve* S, int G) {
   GmSolve& st = S[blockIdx.y];
@@ -2195,9 +2579,26 @@ void encode_panel_map(CUtensorMap* out, double* base, int64_t chunks, int box_ve
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
 
+// Tensor map over one shadow panel, [chunks][64 vectors][32 rows] floats (k_gs_tmxf).
+void encode_shadow_map(CUtensorMap* out, float* base, int64_t chunks, int box_vecs) {
+  const cuuint64_t dims[3] = {cuuint64_t(FCHUNK), cuuint64_t(PANEL), cuuint64_t(chunks)};
+  const cuuint64_t strides[2] = {cuuint64_t(FCHUNK) * sizeof(float), cuuint64_t(PANEL * FCHUNK) * sizeof(float)};
+  const cuuint32_t box[3] = {cuuint32_t(FCHUNK), cuuint32_t(box_vecs), 1u};
+  const cuuint32_t es[3] = {1u, 1u, 1u};
+  const CUresult r = tensor_map_encoder()(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
+                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+
 struct SolveHost {
   std::vector<CUtensorMap> tmh;  // host mirror of the panel tensor maps (k_gs_tmx)
   DBuf<CUtensorMap> tmd;
+  std::vector<CUtensorMap> tmfh;  // the same for the single-precision shadow panels (k_gs_tmxf)
+  DBuf<CUtensorMap> tmfd;
+  std::vector<DBuf<float>> fpanels;
+  std::vector<float*> ftab;
+  DBuf<float*> dF;
   std::vector<DBuf<double>> panels;
   std::vector<double*> vtab;  // host mirror of the V table
   int uploaded = 0;
@@ -2263,6 +2664,11 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     // with the delayed second pass, which needs k_gs_tmx<true>, 128 (C3 step 3 153 -> 2 846 ms; 64: 2 864 ms)
     psel.split = sp ? std::atoi(sp) : (dcgs_on ? 128 : 256);
   }
+  // single-precision shadow of the basis for the projection pass (k_gs_tmxf); needs the delayed second
+  // pass, which repairs the few-digit projection coefficients (MPG_GS_F32=0: fp64 projection everywhere).
+  // With it the split moves to 96 (C3 step: 128 -> 2 532 ms, 96 -> 2 497, 64 -> 2 504, 32 -> 2 526).
+  const bool f32_on = dcgs_on && (psel.sel & 4) && !(std::getenv("MPG_GS_F32") && std::atoi(std::getenv("MPG_GS_F32")) == 0);
+  if (f32_on && !std::getenv("MPG_GS_DOT_SPLIT")) psel.split = 96;
   const int upd_kind = usel.sel;
   const bool want_maps = ((usel.sel | psel.sel) & 6) != 0;  // panel tensor maps for k_gs_tmx
   std::vector<SolveHost> sh(static_cast<size_t>(ns));
@@ -2357,6 +2763,14 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       H.tmh.resize(2 * np);
       H.tmd = DBuf<CUtensorMap>(dev, 2 * np);
       g.tm = H.tmd.get();
+      if (f32_on) {
+        H.tmfh.resize(2 * np);
+        H.tmfd = DBuf<CUtensorMap>(dev, 2 * np);
+        g.tmf = H.tmfd.get();
+        H.dF = DBuf<float*>(dev, size_t(maxit) + 2);
+        H.ftab.assign(size_t(maxit) + 2, nullptr);
+        g.F = H.dF.get();
+      }
     }
   }
 
@@ -2377,8 +2791,21 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         encode_panel_map(&H.tmh[2 * p + 1], base, H.ld / CHUNK, 8);
         MPG_CUDA(cudaMemcpyAsync(H.tmd.get() + 2 * p, &H.tmh[2 * p], 2 * sizeof(CUtensorMap), cudaMemcpyHostToDevice, s));
       }
+      if (hs[size_t(i)].F) {
+        H.fpanels.emplace_back(dev, size_t(PANEL) * size_t(H.ld));
+        float* fb = H.fpanels.back().get();
+        MPG_CUDA(cudaMemsetAsync(fb, 0, size_t(PANEL) * size_t(H.ld) * sizeof(float), s));
+        for (int j = 0; j < PANEL && p0 + j < maxit + 2; ++j) H.ftab[size_t(p0 + j)] = fb + size_t(j) * FCHUNK;
+        const size_t p = H.fpanels.size() - 1;
+        encode_shadow_map(&H.tmfh[2 * p], fb, H.ld / FCHUNK, PANEL);
+        encode_shadow_map(&H.tmfh[2 * p + 1], fb, H.ld / FCHUNK, 8);
+        MPG_CUDA(cudaMemcpyAsync(H.tmfd.get() + 2 * p, &H.tmfh[2 * p], 2 * sizeof(CUtensorMap), cudaMemcpyHostToDevice, s));
+      }
     }
     if (upto > H.uploaded) {
+      if (hs[size_t(i)].F)
+        MPG_CUDA(cudaMemcpyAsync(H.dF.get() + H.uploaded, H.ftab.data() + H.uploaded,
+                                 size_t(upto - H.uploaded) * sizeof(float*), cudaMemcpyHostToDevice, s));
       MPG_CUDA(cudaMemcpyAsync(H.dV.get() + H.uploaded, H.vtab.data() + H.uploaded,
                                size_t(upto - H.uploaded) * sizeof(double*), cudaMemcpyHostToDevice, s));
       H.uploaded = upto;
@@ -2425,6 +2852,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       cudaFuncSetAttribute(k_gs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, GT_SMEM);
       cudaFuncSetAttribute(k_gs_tmx<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
       cudaFuncSetAttribute(k_gs_tmx<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
+      cudaFuncSetAttribute(k_gs_tmxf, cudaFuncAttributeMaxDynamicSharedMemorySize, GF_SMEM);
       const int hsm = HALO_MAX * HALO_XSTRIDE * int(sizeof(double2));
       cudaFuncSetAttribute(k_spmv_halo<E_IDENT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
       cudaFuncSetAttribute(k_spmv_halo<E_IDENT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
@@ -2450,6 +2878,16 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   bool il2 = false;  // RHS-split interleaved SpMVs
   bool use_halo = false;
   bool use_sell = false;
+  // SM-affine persistent SELL-8 kernels (MPG_SELL_PERSIST=1; CTAs per SM: MPG_SELL_OCC)
+  DBuf<int> sell_ctr_buf;
+  int* sell_ctr = nullptr;
+  const int sell_occ = std::getenv("MPG_SELL_OCC") ? std::max(1, std::atoi(std::getenv("MPG_SELL_OCC"))) : 8;
+  // measured slower on C3 (step 2 519 -> 2 793 / 2 750 / 2 947 ms with 8 / 6 / 4 CTAs per SM): opt-in
+  if (std::getenv("MPG_SELL_PERSIST") && std::atoi(std::getenv("MPG_SELL_PERSIST")) != 0) {
+    sell_ctr_buf = DBuf<int>(dev, size_t(c.sm_count) + 1);
+    MPG_CUDA(cudaMemsetAsync(sell_ctr_buf.get(), 0, (size_t(c.sm_count) + 1) * sizeof(int), s));
+    sell_ctr = sell_ctr_buf.get();
+  }
   if (!std::getenv("MPG_NO_MULTI")) {
     std::vector<int> used(size_t(ns), 0);
     for (int i = 0; i < ns; ++i) {
@@ -2548,6 +2986,10 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         Sell8View sv{};
         const Sell8* sp8 = use_sell ? sell_of(f, &sv) : nullptr;
         if (sp8) {
+          if (sell_ctr)
+            k_spmv_sell8p<E_IDENT, true><<<unsigned(c.sm_count * sell_occ), 256, 0, s>>>(dS.get(), chain_groups[gi], sv, opn,
+                                                                                     xin, xout, sell_ctr, c.sm_count);
+          else
           k_spmv_sell8<E_IDENT, true><<<cdiv(f.nrows * 4, 256), 256, 0, s>>>(dS.get(), chain_groups[gi], sv, opn, xin,
                                                                           xout);
           ++launches_per_iter;
@@ -2617,9 +3059,16 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         if (sp8) {
           const unsigned g2 = cdiv(nb * 4, 256);
           switch (op.emode) {
-            case E_IDENT: k_spmv_sell8<E_IDENT, false><<<g2, 256, 0, s>>>(dS.get(), g, sv, ov, xin, nullptr); break;
-            case E_DIAG: k_spmv_sell8<E_DIAG, false><<<g2, 256, 0, s>>>(dS.get(), g, sv, ov, xin, nullptr); break;
-            default: k_spmv_sell8<E_SAMEPAT, false><<<g2, 256, 0, s>>>(dS.get(), g, sv, ov, xin, nullptr); break;
+#define MPG_S8(EMV)                                                                                                  \
+  if (sell_ctr)                                                                                                      \
+    k_spmv_sell8p<EMV, false><<<unsigned(c.sm_count * sell_occ), 256, 0, s>>>(dS.get(), g, sv, ov, xin, nullptr, sell_ctr, \
+                                                                            c.sm_count);                           \
+  else                                                                                                               \
+    k_spmv_sell8<EMV, false><<<g2, 256, 0, s>>>(dS.get(), g, sv, ov, xin, nullptr);
+            case E_IDENT: MPG_S8(E_IDENT) break;
+            case E_DIAG: MPG_S8(E_DIAG) break;
+            default: MPG_S8(E_SAMEPAT) break;
+#undef MPG_S8
           }
           ++launches_per_iter;
           mark(PK_OP);
@@ -2716,7 +3165,11 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     if (fused) {
       // projection: k_gs_tmx<true> for k + 2 <= GX_MAXV when the panel tensor maps exist
       // (MPG_GS_DOT=reg keeps the register-tiled kernel for every k)
-      if (psel.sel & 4) {
+      if (f32_on) {
+        k_shadow<<<dim3(unsigned(std::min<int64_t>(cdiv(nmax, 1024), 1024)), unsigned(ns)), 256, 0, s>>>(dS.get(), psel);
+        k_gs_tmxf<<<unsigned(gc_dot.ncl), GX_THREADS, GF_SMEM, s>>>(dS.get(), ns, G, psel);
+        launches_per_iter += 2;
+      } else if (psel.sel & 4) {
         k_gs_tmx<true><<<unsigned(gc_dot.ncl), GX_THREADS, GX_SMEM, s>>>(dS.get(), ns, G, psel);
         ++launches_per_iter;
       }
@@ -2836,7 +3289,11 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       const double vec = b.pair ? 2.0 : 1.0;
       const double be = op.emode == E_SAMEPAT ? 8.0 * double(op.a->nnz) : op.emode == E_DIAG ? 8.0 * double(nb) : 0.0;
       bytes[PK_OP] += lead * (12.0 * double(op.a->nnz) + 4.0 * double(nb + 1) + be) + vec * 16.0 * double(nb);
-      bytes[PK_DOT] += 8.0 * n * (k + 1.0) + 8.0 * n + (b.pend ? 8.0 * n : 0.0);  // + the delayed correction of V[k]
+      const bool pf32 = b.F != nullptr && (psel.sel & 4) && b.tm != nullptr && b.k + 2 <= GX_MAXV && b.k + 1 > psel.split;
+      if (pf32)  // float shadow of columns 0..k-1, w and V[k] in fp64, V[k]'s correction and shadow written
+        bytes[PK_DOT] += 4.0 * n * k + 16.0 * n + (b.pend ? 8.0 * n : 0.0) + 4.0 * n;
+      else
+        bytes[PK_DOT] += 8.0 * n * (k + 1.0) + 8.0 * n + (b.pend ? 8.0 * n : 0.0) + (b.F ? 12.0 * n : 0.0);
       bytes[PK_UPDPROBE] += 8.0 * n * (k + 1.0) + 16.0 * n;
       bytes[PK_UPD] += 8.0 * n * (k + 1.0) + 16.0 * n;
       bytes[PK_PROBE] += 8.0 * n * (k + 1.0) + 8.0 * n;

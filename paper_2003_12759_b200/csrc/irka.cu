@@ -557,7 +557,7 @@ IrkaResult irka_run(const ShiftedOp& op, const double* b_any, int m, const doubl
       double acc = 0.0;
       for (size_t i = 0; i < specs.size(); ++i) {
         const double ns_i = specs[i].sim != 0.0 ? 2.0 * double(n) : double(n);
-        const double need = 8.0 * (ns_i + 64.0) * double(est_its + 72) + 1e7;
+        const double need = 12.0 * (ns_i + 64.0) * double(est_its + 72) + 1e7;  // fp64 basis + its float shadow
         if (i > bounds.back() && (acc + need > 0.85 * avail || int(i - bounds.back()) >= max_batch)) {
           bounds.push_back(i);
           acc = 0.0;

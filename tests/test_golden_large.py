@@ -175,19 +175,23 @@ def test_gpu_c3_irka_sweep_map_matches_golden(mpg, gen):
 
 
 @pytest.mark.gpu
-def test_gpu_c3_irka_from_baseline_seed_reaches_the_oracle_fixed_point(mpg, gen):
-    """bench.py's irka leg (BASELINE seed, tol 1e-6) ends within its own stopping error of the poles the
-    oracle's sweep map returns in c3_irka_fix.json, and its H_r agrees on the 200-point grid."""
+def test_gpu_c3_irka_from_baseline_seed_ends_near_the_oracle_sweeps(mpg, gen):
+    """bench.py's irka leg (BASELINE seed, GMRES 1e-8, tol 1e-6). The fixture's start is this run's end
+    (8 digits); the oracle's sweeps from there (GMRES 1e-10) drift by 6e-5 and 3e-5 in the fastest, weakly
+    observable pole pair -- the position of the fixed point depends on the inner tolerance at that level
+     -- so this is a consistency bound, not the parity test (that is the sweep map above)."""
     g = _load("c3_irka_fix.json")
     s = gen.config3()
     op = mpg.ShiftedOperator(_dev(mpg, s.a), _dev(mpg, s.e))
     cfg = mpg.IrkaConfig(r=8, tol=1e-6, max_sweeps=50, seed=1, gmres=mpg.GmresConfig(1e-8, 1000), mirror_unstable=True)
     st, rep = mpg.irka_reduce(op, s.b, s.c, cfg, mpg.PrecondMode.REUSE_FROZEN, init_shifts=s.shifts[:8])
     assert rep.converged
-    assert _poles_close(st.lam, g["poles_by_sweep"][-1], 5e-6)  # the run stops at a 1e-6 change per sweep
+    start = np.linalg.eigvals(np.array(g["init_kr"]))
+    assert _poles_close(st.lam, [[z.real, z.imag] for z in start], 2e-6)  # the fixture starts where this run ends
+    assert _poles_close(st.lam, g["poles_by_sweep"][-1], 5e-4)
     hw = np.array(g["hr_re"]) + 1j * np.array(g["hr_im"])
     err = max(np.linalg.norm(st.transfer(1j * w).ravel() - hw[i]) / np.linalg.norm(hw[i]) for i, w in enumerate(GRID))
-    assert err <= 5e-6
+    assert err <= 5e-4
 
 
 @pytest.mark.gpu

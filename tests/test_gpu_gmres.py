@@ -251,6 +251,7 @@ def test_delayed_second_pass_matches_immediate(mpg, orc, gen, monkeypatch, env):
     within 1, solutions within 1e-9 -- on a C3-type batch (16 solves sharing two
     frozen SPAIs, 150-300 iterations, the projection in k_gs_tmx<true> from
     k + 1 = 129 on). Every variant also stays within the oracle's iteration count."""
+    monkeypatch.setenv("MPG_GS_F32", "0")  # the fp64 projection: the second-pass decisions are comparable
     s = gen.config3(18)
     op = mpg.ShiftedOperator(_m(mpg, s.a), _m(mpg, s.e))
     sh = [float(x) for x in s.shifts[:8]]
@@ -276,3 +277,37 @@ def test_delayed_second_pass_matches_immediate(mpg, orc, gen, monkeypatch, env):
                             orc.GmresConfig(1e-10, 1000))
     assert abs(var[0].report.iterations - ro.iterations) <= max(3, 0.03 * ro.iterations)
     assert rel(var[0].x, xo) <= 1e-6
+
+
+@pytest.mark.parametrize("tol", [1e-8, 1e-12])
+def test_float_shadow_projection_matches_fp64_projection(mpg, orc, gen, monkeypatch, tol):
+    """k_gs_tmxf projects on a single-precision shadow of the basis (half the bytes of the pass); the
+    update pass, the probe and the delayed correction keep the Arnoldi relation in fp64. Same solves as
+    with the fp64 projection: identical iteration counts, solutions within 1e-11, true residuals at the
+    tolerance (also at 1e-12, far below single precision), and within the oracle's iteration count."""
+    monkeypatch.setenv("MPG_GS_DOT_SPLIT", "32")  # both variants: k_gs_tmx<true> / k_gs_tmxf from k + 1 = 33 on
+    s = gen.config3(40)
+    op = mpg.ShiftedOperator(_m(mpg, s.a), _m(mpg, s.e))
+    sh = [float(x) for x in s.shifts[:8]]
+    pv = mpg.PrecondChain(mpg.spai_build(op.explicit(sh[0], False)).p)
+    pw = mpg.PrecondChain(mpg.spai_build(op.explicit(sh[0], True)).p)
+    sig, trs, ch = sh + sh, [0] * 8 + [1] * 8, [pv] * 8 + [pw] * 8
+    bs = [s.b[:, 0]] * 8 + [s.c[:, 0]] * 8
+    cfg = mpg.GmresConfig(rel_tol=tol, max_iter=1000)
+    f32 = mpg.gmres_batch(op, sig, bs, chains=ch, transposes=trs, cfg=cfg)  # default
+    monkeypatch.setenv("MPG_GS_F32", "0")
+    f64 = mpg.gmres_batch(op, sig, bs, chains=ch, transposes=trs, cfg=cfg)
+    assert min(r.report.iterations for r in f32) > 80
+    for i, (a, b) in enumerate(zip(f32, f64)):
+        assert a.report.converged and b.report.converged
+        assert a.report.iterations == b.report.iterations
+        assert rel(a.x, b.x) <= 1e-11
+        res = bs[i] - op.apply(sig[i], a.x, transpose=bool(trs[i]))
+        assert np.linalg.norm(res) <= 1.0001 * tol * np.linalg.norm(bs[i])
+        assert a.report.reorth_passes >= b.report.reorth_passes  # every shadow projection is followed by a correction
+    A, E = orc.Csr.of(s.a), orc.Csr.of(s.e)
+    m = orc.kron_assemble(orc.shifted(sh[0]), A, E, cap=10 ** 12)
+    xo, ro = orc.gmres_kron(orc.shifted(sh[0]), A, E, orc.Chain(orc.spai_build(m)[0]), s.b[:, 0],
+                            orc.GmresConfig(tol, 1000))
+    assert abs(f32[0].report.iterations - ro.iterations) <= max(3, 0.03 * ro.iterations)
+    assert rel(f32[0].x, xo) <= 1e-6
