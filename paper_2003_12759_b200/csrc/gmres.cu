@@ -1289,6 +1289,89 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 
 __device__ __forceinline__ int gt_chunks(const GmSolve& st) { return ((st.n + 31) & ~31) / CHUNK; }
+// SELL-8 SpMV with the matrix stream staged by TMA: a CTA owns 8 slices (64 rows), whose column indices and
+// values are two contiguous runs of the SELL-8 arrays; one thread fetches both with bulk copies
+// (cp.async.bulk) into shared memory and the CTA waits on the mbarrier. The stream then costs two DRAM-efficient
+// requests per CTA instead of one 32-byte sector request per warp and step (k_spmv_sell8 is latency-bound on
+// those: ncu long-scoreboard 45-67 %), never enters L1, and the only global loads left in the loop are the
+// x-gathers; the loads of one CTA overlap the arithmetic of the others resident on the SM.
+template <int EM, bool CHAIN>
+__global__ void __launch_bounds__(256) k_spmv_sell8t(GmSolve* S, Group grp, Sell8View sv, OpView op,
+                                                     const double* __restrict__ xin, double* __restrict__ xout) {
+  extern __shared__ __align__(128) char s8sm[];
+  __shared__ __align__(8) uint64_t bar;
+  if (!il_any_run(S, grp)) return;
+  constexpr bool PAIRV = !CHAIN && EM == E_SAMEPAT;
+  constexpr int VB = PAIRV ? 16 : 8;
+  const int nsl = (sv.nrows + 7) >> 3;
+  const int s0 = int(blockIdx.x) * 8, s1 = min(nsl, s0 + 8);
+  const int eb = __ldg(sv.sptr + s0), ee = __ldg(sv.sptr + s1);
+  const int E = ee - eb;
+  const int* cs = reinterpret_cast<const int*>(s8sm);
+  const char* vs = s8sm + size_t(E) * 4;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && E > 0) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    mbar_expect_tx(&bar, unsigned(E) * unsigned(4 + VB));
+    bulk_g2s(s8sm, sv.col + eb, unsigned(E) * 4u, &bar, pol);
+    if (PAIRV) bulk_g2s(s8sm + size_t(E) * 4, sv.val2 + eb, unsigned(E) * 16u, &bar, pol);
+    else bulk_g2s(s8sm + size_t(E) * 4, sv.val + eb, unsigned(E) * 8u, &bar, pol);
+  }
+  const int lane = threadIdx.x & 3;
+  const int ls = int(threadIdx.x >> 5);  // slice of this warp
+  const int row = (s0 + ls) * 8 + int((threadIdx.x >> 2) & 7);
+  int e0 = 0, w = 0;
+  if (s0 + ls < s1) {
+    const int a = __ldg(sv.sptr + s0 + ls);
+    e0 = a - eb + (row & 7);
+    w = (__ldg(sv.sptr + s0 + ls + 1) - a) >> 3;
+  }
+  const double* xl = xin + 2 * lane;
+  if (E > 0) mbar_wait(&bar, 0);
+  if (row >= sv.nrows) return;
+  double a0 = 0.0, a1 = 0.0, g0 = 0.0, g1 = 0.0;
+#pragma unroll 8
+  for (int j = 0; j < w; ++j) {
+    const int e = e0 + 8 * j;
+    const int c = cs[e];
+    const double2 x = __ldg(reinterpret_cast<const double2*>(xl + size_t(c) * MB));
+    if (PAIRV) {
+      const double2 ae = reinterpret_cast<const double2*>(vs)[e];
+      a0 = fma(ae.x, x.x, a0);
+      a1 = fma(ae.x, x.y, a1);
+      g0 = fma(ae.y, x.x, g0);
+      g1 = fma(ae.y, x.y, g1);
+    } else {
+      const double av = reinterpret_cast<const double*>(vs)[e];
+      a0 = fma(av, x.x, a0);
+      a1 = fma(av, x.y, a1);
+    }
+  }
+  if (CHAIN) {
+    reinterpret_cast<double2*>(xout + size_t(row) * MB)[lane] = make_double2(a0, a1);
+    return;
+  }
+  if (EM == E_IDENT || EM == E_DIAG) {
+    const double2 xr = reinterpret_cast<const double2*>(xin + size_t(row) * MB)[lane];
+    const double dd = EM == E_DIAG ? op.ediag[row] : 1.0;
+    g0 = dd * xr.x;
+    g1 = dd * xr.y;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int q = 2 * lane + h;
+    if (q >= grp.cnt) continue;
+    GmSolve& st = S[grp.idx[q]];
+    if (st.phase != PH_RUN) continue;
+    st.V[st.k + 1][vidx(row)] = st.scale[st.k] * (st.sre * (h ? g1 : g0) + st.ca * (h ? a1 : a0));
+  }
+}
+
 
 // Tile cursor over the handled solves: tiles [off, off + nt) belong to solve s.
 struct GtCursor {
@@ -2853,6 +2936,17 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       cudaFuncSetAttribute(k_gs_tmx<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
       cudaFuncSetAttribute(k_gs_tmx<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GX_SMEM);
       cudaFuncSetAttribute(k_gs_tmxf, cudaFuncAttributeMaxDynamicSharedMemorySize, GF_SMEM);
+      cudaFuncSetAttribute(k_spmv_sell8t<E_IDENT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      cudaFuncSetAttribute(k_spmv_sell8t<E_IDENT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      cudaFuncSetAttribute(k_spmv_sell8t<E_DIAG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      cudaFuncSetAttribute(k_spmv_sell8t<E_SAMEPAT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      if (const char* co = std::getenv("MPG_SELL_CARVEOUT")) {  // shared-memory share of the unified L1 (percent)
+        const int pc = std::atoi(co);
+        cudaFuncSetAttribute(k_spmv_sell8t<E_IDENT, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+        cudaFuncSetAttribute(k_spmv_sell8t<E_IDENT, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+        cudaFuncSetAttribute(k_spmv_sell8t<E_DIAG, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+        cudaFuncSetAttribute(k_spmv_sell8t<E_SAMEPAT, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+      }
       const int hsm = HALO_MAX * HALO_XSTRIDE * int(sizeof(double2));
       cudaFuncSetAttribute(k_spmv_halo<E_IDENT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
       cudaFuncSetAttribute(k_spmv_halo<E_IDENT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
@@ -2878,6 +2972,8 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   bool il2 = false;  // RHS-split interleaved SpMVs
   bool use_halo = false;
   bool use_sell = false;
+  // SELL-8 kernels with the matrix stream staged by TMA bulk copies (MPG_SELL_TMA=0: plain loads)
+  const bool sell_tma = !(std::getenv("MPG_SELL_TMA") && std::atoi(std::getenv("MPG_SELL_TMA")) == 0);
   // SM-affine persistent SELL-8 kernels (MPG_SELL_PERSIST=1; CTAs per SM: MPG_SELL_OCC)
   DBuf<int> sell_ctr_buf;
   int* sell_ctr = nullptr;
@@ -2986,7 +3082,10 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         Sell8View sv{};
         const Sell8* sp8 = use_sell ? sell_of(f, &sv) : nullptr;
         if (sp8) {
-          if (sell_ctr)
+          if (sell_tma && size_t(sp8->max_tile) * 12 <= 64 * 1024)
+            k_spmv_sell8t<E_IDENT, true><<<cdiv(cdiv(f.nrows, 8), 8), 256, size_t(sp8->max_tile) * 12, s>>>(
+                dS.get(), chain_groups[gi], sv, opn, xin, xout);
+          else if (sell_ctr)
             k_spmv_sell8p<E_IDENT, true><<<unsigned(c.sm_count * sell_occ), 256, 0, s>>>(dS.get(), chain_groups[gi], sv, opn,
                                                                                      xin, xout, sell_ctr, c.sm_count);
           else
@@ -3060,7 +3159,10 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
           const unsigned g2 = cdiv(nb * 4, 256);
           switch (op.emode) {
 #define MPG_S8(EMV)                                                                                                  \
-  if (sell_ctr)                                                                                                      \
+  if (sell_tma && size_t(sp8->max_tile) * (EMV == E_SAMEPAT ? 20 : 12) <= 64 * 1024)                                 \
+    k_spmv_sell8t<EMV, false><<<cdiv(cdiv(nb, 8), 8), 256, size_t(sp8->max_tile) * (EMV == E_SAMEPAT ? 20 : 12), s>>>( \
+        dS.get(), g, sv, ov, xin, nullptr);                                                                          \
+  else if (sell_ctr)                                                                                                 \
     k_spmv_sell8p<EMV, false><<<unsigned(c.sm_count * sell_occ), 256, 0, s>>>(dS.get(), g, sv, ov, xin, nullptr, sell_ctr, \
                                                                             c.sm_count);                           \
   else                                                                                                               \

@@ -196,6 +196,7 @@ Sell8Ptr sell8_build(const DevCsr& m) {
   auto p = std::make_shared<Sell8>();
   p->nrows = n;
   p->entries = ent;
+  for (int s0 = 0; s0 < nsl; s0 += 8) p->max_tile = std::max(p->max_tile, sptr[size_t(std::min(nsl, s0 + 8))] - sptr[size_t(s0)]);
   p->sptr = DBuf<int>(m.device, sptr.size());
   p->col = DBuf<int>(m.device, size_t(std::max<int64_t>(1, ent)));
   p->perm = DBuf<int>(m.device, size_t(std::max<int64_t>(1, ent)));

@@ -134,6 +134,7 @@ HaloPatternPtr halo_pattern_build(const DevCsr& m);  // nullptr if the pattern d
 struct Sell8 {
   int nrows = 0;
   int64_t entries = 0;
+  int max_tile = 0;  // most entries in a block of 8 consecutive slices (k_spmv_sell8t's shared-memory tile)
   DBuf<int> sptr, col, perm;  // [nslices + 1], [entries], [entries] (-1: padding)
 };
 using Sell8Ptr = std::shared_ptr<const Sell8>;

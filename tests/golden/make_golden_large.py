@@ -277,7 +277,7 @@ def stage_c5(O, gen):
            "failed_count": int(failed), "failed": [i for i, rw in enumerate(rows) if rw.iterations >= 1000],
            "x": [summary(x) for x in xs], "oracle_wall_s": round(wall, 1), "oracle_threads": THREADS,
            "host": _host()}
-    _dump("c5_sweep.json", out)
+    _dump("c5_sweep.json" if n == 100_000 else f"c5_sweep_n{n}.json", out)
 
 
 if __name__ == "__main__":

@@ -195,11 +195,12 @@ def test_gpu_c3_irka_from_baseline_seed_ends_near_the_oracle_sweeps(mpg, gen):
 
 
 @pytest.mark.gpu
-def test_gpu_c5_sweep_matches_golden(mpg, gen):
+@pytest.mark.parametrize("name", ["c5_sweep_n30000.json", "c5_sweep.json"])
+def test_gpu_c5_sweep_matches_golden(mpg, gen, name):
     """The reference's shift sweep (bench.cpp:159-249, ReuseChain) on the C5
     generator at reduced n with its 2 000-entry rows kept: row kinds, the
     failure set, iteration counts and the converged solutions."""
-    g = _load("c5_sweep.json")
+    g = _load(name)
     s = gen.config5(n=g["n"], max_len=g["max_len"])
     assert s.a.nnz == g["nnz"]
     op = mpg.ShiftedOperator(_dev(mpg, s.a), _dev(mpg, s.e_csr()))
