@@ -102,18 +102,46 @@ __device__ __forceinline__ double sub_sum(double v) {
 __device__ __forceinline__ size_t hoff(int j) { return size_t(j) * size_t(j + 1) / 2; }
 
 // ---- chain stage: z[stage&1] = F_stage * src ------------------------------------
+// V = 0: the row-binned mapping for irregular factors (runtime.cuh bin_locate);
+// a solve is served by the launch that matches its factor.
 template <int V>
 __global__ void __launch_bounds__(256) k_chain_stage(GmSolve* S, int stage, int mode) {
   GmSolve& st = S[blockIdx.y];
   if (mode == 0 ? st.phase != PH_RUN : st.phase != PH_ASM) return;
   if (stage >= st.stages || st.grouped_chain) return;
   const CsrView f = st.fac[stage];
+  if ((f.brow != nullptr) != (V == 0)) return;
   const int halves = st.pair_bd ? 2 : 1;
-  const int lane = threadIdx.x & (V - 1);
-  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / V);
   const bool chunked = stage == 0 && mode == 0;  // reads the basis vector V[k]
   const double* src = stage == 0 ? (mode == 0 ? st.V[st.k] : st.ubuf) : ((stage - 1) & 1 ? st.z1 : st.z0);
   double* dst = (stage & 1) ? st.z1 : st.z0;
+  if (V == 0) {
+    if (int(blockIdx.x) >= f.bblk[NBIN]) return;
+    int r, W, lane;
+    const bool ok = bin_locate(f, r, W, lane);
+    for (int hf = 0; hf < halves; ++hf) {
+      const int off = hf * f.nrows;
+      double acc = 0.0;
+      if (ok) {
+        const int b = f.rowptr[r], e = f.rowptr[r + 1];
+        if (chunked) {
+#pragma unroll 4
+          for (int k = b + lane; k < e; k += W)
+            acc = fma(__ldcs(f.val + k), __ldg(src + vidx(off + __ldcs(f.colind + k))), acc);
+        } else {
+          const double* x = src + off;
+#pragma unroll 4
+          for (int k = b + lane; k < e; k += W) acc = fma(__ldcs(f.val + k), __ldg(x + __ldcs(f.colind + k)), acc);
+        }
+      }
+      acc = sub_sum_rt(acc, W);
+      if (ok && lane == 0) dst[off + r] = acc;
+    }
+    return;
+  }
+  constexpr int VV = V ? V : 2;
+  const int lane = threadIdx.x & (VV - 1);
+  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / VV);
   double acc = 0.0;
   int r = row, off = 0;
   if (row >= f.nrows) { r = row - f.nrows; off = f.nrows; }
@@ -121,15 +149,15 @@ __global__ void __launch_bounds__(256) k_chain_stage(GmSolve* S, int stage, int 
     const int b = f.rowptr[r], e = f.rowptr[r + 1];
     if (chunked) {
 #pragma unroll 4
-      for (int k = b + lane; k < e; k += V)
+      for (int k = b + lane; k < e; k += VV)
         acc = fma(__ldcs(f.val + k), __ldg(src + vidx(off + __ldcs(f.colind + k))), acc);
     } else {
       const double* x = src + off;
 #pragma unroll 4
-      for (int k = b + lane; k < e; k += V) acc = fma(__ldcs(f.val + k), __ldg(x + __ldcs(f.colind + k)), acc);
+      for (int k = b + lane; k < e; k += VV) acc = fma(__ldcs(f.val + k), __ldg(x + __ldcs(f.colind + k)), acc);
     }
   }
-  acc = sub_sum<V>(acc);
+  acc = sub_sum<VV>(acc);
   if (row < f.nrows * halves && lane == 0) dst[off + r] = acc;
 }
 
@@ -140,20 +168,29 @@ __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView 
   if (mode == 0 ? st.phase != PH_RUN : st.phase != PH_ASM) return;
   if (st.grouped_op & (mode == 0 ? 1 : 2)) return;
   const OpView& op = st.transpose ? opt : opn;
+  if ((op.a.brow != nullptr) != (V == 0)) return;  // V = 0 serves the row-binned operator sides
   const int n = op.a.nrows;
-  const int lane = threadIdx.x & (V - 1);
-  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / V);
+  int lane, row, W = V;
+  bool ok;
+  if (V == 0) {
+    if (int(blockIdx.x) >= op.a.bblk[NBIN]) return;
+    ok = bin_locate(op.a, row, W, lane);
+  } else {
+    lane = threadIdx.x & (V - 1);
+    row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / (V ? V : 1));
+    ok = row < n;
+  }
   const double* x;
   if (mode == 0) x = st.stages ? ((st.stages - 1) & 1 ? st.z1 : st.z0) : st.V[st.k];
   else x = st.stages ? ((st.stages - 1) & 1 ? st.z1 : st.z0) : st.ubuf;
   const bool xc = mode == 0 && st.stages == 0;  // x is a chunk-major basis vector
   const bool pair = st.pair;
   double a1 = 0.0, a2 = 0.0, e1 = 0.0, e2 = 0.0;
-  if (row < n) {
+  if (ok) {
     const int b = op.a.rowptr[row], e = op.a.rowptr[row + 1];
     if (EM == E_SAMEPAT) {
 #pragma unroll 4
-      for (int k = b + lane; k < e; k += V) {
+      for (int k = b + lane; k < e; k += W) {
         const double2 ae = __ldcs(op.ae + k);
         const int c = __ldcs(op.a.colind + k);
         const double x1 = __ldg(x + (xc ? vidx(c) : c));
@@ -167,7 +204,7 @@ __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView 
       }
     } else {
 #pragma unroll 4
-      for (int k = b + lane; k < e; k += V) {
+      for (int k = b + lane; k < e; k += W) {
         const double av = __ldcs(op.a.val + k);
         const int c = __ldcs(op.a.colind + k);
         a1 = fma(av, __ldg(x + (xc ? vidx(c) : c)), a1);
@@ -175,13 +212,15 @@ __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView 
       }
     }
   }
-  a1 = sub_sum<V>(a1);
-  a2 = sub_sum<V>(a2);
+#define MPG_SUBSUM(v) v = V ? sub_sum<(V ? V : 2)>(v) : sub_sum_rt(v, W)
+  MPG_SUBSUM(a1);
+  MPG_SUBSUM(a2);
   if (EM == E_SAMEPAT) {
-    e1 = sub_sum<V>(e1);
-    e2 = sub_sum<V>(e2);
+    MPG_SUBSUM(e1);
+    MPG_SUBSUM(e2);
   }
-  if (row < n && lane == 0) {
+#undef MPG_SUBSUM
+  if (ok && lane == 0) {
     const int i1 = xc ? vidx(row) : row, i2 = xc ? vidx(n + row) : n + row;
     if (EM == E_IDENT) {
       e1 = x[i1];
@@ -2759,6 +2798,8 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   int max_stages = 0;
   double max_fac_mean = 0.0;
   int64_t max_fac_rows = 0;
+  int max_fac_bblk = 0;  // row-binned factors (irregular rows): the largest binned grid
+  bool any_fac_plain = false;
   for (int i = 0; i < ns; ++i) {
     SolveSpec& sp = specs[size_t(i)];
     SolveHost& H = sh[size_t(i)];
@@ -2813,6 +2854,11 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       std::vector<CsrView> fv;
       for (auto& f : sp.chain->factors) {
         fv.push_back(f->view());
+        if (f->brow.get()) {
+          max_fac_bblk = std::max(max_fac_bblk, f->bblk[NBIN]);
+          continue;
+        }
+        any_fac_plain = true;
         max_fac_mean = std::max(max_fac_mean, f->mean_row);
         max_fac_rows = std::max<int64_t>(max_fac_rows, f->nrows * (g.pair_bd ? 2 : 1));
       }
@@ -3133,6 +3179,12 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       mark(mode == 0 ? PK_CHAIN : PK_ASM);
     }
     if (!any_plain_chain) return;
+    if (max_fac_bblk) {
+      k_chain_stage<0><<<dim3(unsigned(max_fac_bblk), unsigned(ns)), 256, 0, s>>>(dS.get(), stage, mode);
+      ++launches_per_iter;
+      mark(mode == 0 ? PK_CHAIN : PK_ASM);
+    }
+    if (!any_fac_plain) return;
     const dim3 grid(cdiv(max_fac_rows * int64_t(Vfac), 256), unsigned(ns));
     switch (Vfac) {
       case 2: k_chain_stage<2><<<grid, 256, 0, s>>>(dS.get(), stage, mode); break;
@@ -3226,17 +3278,29 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     default: k_iter_op<VV, E_SAMEPAT><<<grid, 256, 0, s>>>(dS.get(), opn, opt_, mode); break;                 \
   }
     if (mode == 0 ? any_plain_op_run : any_plain_op_asm) {
-    switch (Vop) {
-      case 2: MPG_OPL(2); break;
-      case 4: MPG_OPL(4); break;
-      case 8: MPG_OPL(8); break;
-      case 16: MPG_OPL(16); break;
-      default: MPG_OPL(32); break;
+      // the sides present among the solves, split by row-binned / plain operator rows
+      bool need_b = false, need_p = false;
+      for (int i = 0; i < ns; ++i) ((hs[size_t(i)].transpose ? opt_ : opn).a.brow ? need_b : need_p) = true;
+      if (need_b) {
+        const dim3 grid(unsigned(std::max(opn.a.brow ? opn.a.bblk[NBIN] : 0, opt_.a.brow ? opt_.a.bblk[NBIN] : 0)),
+                        unsigned(ns));
+        MPG_OPL(0);
+        ++launches_per_iter;
+        mark(mode == 0 ? PK_OP : PK_ASM);
+      }
+      if (need_p) {
+        switch (Vop) {
+          case 2: MPG_OPL(2); break;
+          case 4: MPG_OPL(4); break;
+          case 8: MPG_OPL(8); break;
+          case 16: MPG_OPL(16); break;
+          default: MPG_OPL(32); break;
+        }
+        ++launches_per_iter;
+        mark(mode == 0 ? PK_OP : PK_ASM);
+      }
     }
 #undef MPG_OPL
-    ++launches_per_iter;
-    mark(mode == 0 ? PK_OP : PK_ASM);
-    }
     for (const Group& g : (mode == 0 ? op_groups_run : op_groups_asm)) {
       const OpView& ov = hs[size_t(g.idx[0])].transpose ? opt_ : opn;
       const unsigned grid1 = cdiv(nb * int64_t(Vop), 256);

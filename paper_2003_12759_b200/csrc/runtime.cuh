@@ -85,13 +85,50 @@ struct DBuf {
   T* get() const { return p; }
 };
 
+// Row bins (the long-row split of irregular matrices, e.g. the C5 Zipf rows of
+// 3 ... 2 000 entries): rows grouped by length class, class b served by
+// sub-warps of 2 << b lanes (2, 4, 8, 16, 32), so a 2 000-entry row gets a
+// whole warp and coalesced 256-byte value requests while the short rows keep
+// 2-4 lanes. brow lists the rows class by class in ascending row order (a
+// stable sort: deterministic, no atomics in the SpMV); boff[b] is class b's
+// first slot in brow and bblk[b] its first 256-thread block, bblk[NBIN] the
+// grid. Built with the matrix when max_row is far above the mean (spmv.cu).
+constexpr int NBIN = 5;
+__host__ __device__ __forceinline__ int row_bin(int len) {
+  return len <= 5 ? 0 : len <= 32 ? 1 : len <= 64 ? 2 : len <= 128 ? 3 : 4;
+}
+
 // Kernel-side view of a CSR matrix.
 struct CsrView {
   const int* rowptr;
   const int* colind;
   const double* val;
   int nrows, ncols;
+  const int* brow;  // null: no row bins
+  int boff[NBIN + 1];
+  int bblk[NBIN + 1];
 };
+
+#ifdef __CUDACC__
+// Binned thread mapping: this thread's row (or ok = false), sub-warp width and lane.
+__device__ __forceinline__ bool bin_locate(const CsrView& f, int& row, int& W, int& lane) {
+  int b = 0;
+#pragma unroll
+  for (int i = 1; i < NBIN; ++i) b += int(blockIdx.x) >= f.bblk[i];
+  W = 2 << b;
+  const int t = (int(blockIdx.x) - f.bblk[b]) * int(blockDim.x) + int(threadIdx.x);
+  const int slot = t >> (b + 1);
+  lane = t & (W - 1);
+  row = 0;
+  if (slot >= f.boff[b + 1] - f.boff[b]) return false;
+  row = f.brow[f.boff[b] + slot];
+  return true;
+}
+__device__ __forceinline__ double sub_sum_rt(double v, int W) {
+  for (int o = W >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, W);
+  return v;
+}
+#endif
 
 // Halo-staged sliced ELL (spmv.cu halo_*; the multi-RHS SpMV of the run-mode
 // groups in gmres.cu). Rows in blocks of HALO_R; per block the sorted unique
@@ -163,7 +200,13 @@ struct DevCsr {
   mutable bool sell_tried = false;          // SELL-8 layout + this matrix's values in it, built on first use
   mutable Sell8Ptr sell;
   mutable DBuf<double> sell_val;
-  CsrView view() const { return {rowptr.get(), colind.get(), val.get(), int(nrows), int(ncols)}; }
+  DBuf<int> brow;  // row bins (CsrView): empty for regular matrices
+  int boff[NBIN + 1] = {}, bblk[NBIN + 1] = {};
+  CsrView view() const {
+    CsrView v{rowptr.get(), colind.get(), val.get(), int(nrows), int(ncols), brow.get(), {}, {}};
+    for (int i = 0; i <= NBIN; ++i) { v.boff[i] = boff[i]; v.bblk[i] = bblk[i]; }
+    return v;
+  }
 };
 // The halo layout of m with m's own values (nullptr: not eligible); cached on m.
 const HaloPattern* halo_of(const DevCsr& m, HaloView* view);

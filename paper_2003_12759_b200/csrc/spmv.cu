@@ -145,34 +145,49 @@ __device__ __forceinline__ double sub_sum(double v) {
   return v;
 }
 
+// V = 0: the row-binned mapping (runtime.cuh bin_locate), sub-warp width per block.
 template <int V>
 __global__ void __launch_bounds__(256) k_spmv(CsrView m, const double* __restrict__ x, double* __restrict__ y,
                                               double alpha) {
-  const int lane = threadIdx.x & (V - 1);
-  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / V);
+  int lane, row, W = V;
+  bool ok;
+  if (V == 0) {
+    ok = bin_locate(m, row, W, lane);
+  } else {
+    lane = threadIdx.x & (V - 1);
+    row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / V);
+    ok = row < m.nrows;
+  }
   double acc = 0.0;
-  if (row < m.nrows) {
+  if (ok) {
     const int b = m.rowptr[row], e = m.rowptr[row + 1];
 #pragma unroll 4
-    for (int k = b + lane; k < e; k += V) acc = fma(__ldcs(m.val + k), __ldg(x + __ldcs(m.colind + k)), acc);
+    for (int k = b + lane; k < e; k += W) acc = fma(__ldcs(m.val + k), __ldg(x + __ldcs(m.colind + k)), acc);
   }
-  acc = sub_sum<V>(acc);
-  if (row < m.nrows && lane == 0) y[row] = alpha * acc;
+  acc = V ? sub_sum<(V ? V : 2)>(acc) : sub_sum_rt(acc, W);
+  if (ok && lane == 0) y[row] = alpha * acc;
 }
 
 // y = s (sigma E x + ca A x); PAIR: 2n real form; RESID: y = resid - (...)
 template <int V, int EM, bool PAIR>
 __global__ void __launch_bounds__(256) k_op(OpView op, double sre, double sim, double ca, const double* __restrict__ x,
                                             double* __restrict__ y, const double* __restrict__ resid, double scale) {
-  const int lane = threadIdx.x & (V - 1);
-  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / V);
   const int n = op.a.nrows;
+  int lane, row, W = V;
+  bool ok;
+  if (V == 0) {  // row-binned mapping
+    ok = bin_locate(op.a, row, W, lane);
+  } else {
+    lane = threadIdx.x & (V - 1);
+    row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / V);
+    ok = row < n;
+  }
   double a1 = 0.0, a2 = 0.0, e1 = 0.0, e2 = 0.0;
-  if (row < n) {
+  if (ok) {
     const int b = op.a.rowptr[row], e = op.a.rowptr[row + 1];
     if (EM == E_SAMEPAT) {
 #pragma unroll 4
-      for (int k = b + lane; k < e; k += V) {
+      for (int k = b + lane; k < e; k += W) {
         const double2 ae = __ldcs(op.ae + k);
         const int c = __ldcs(op.a.colind + k);
         const double x1 = __ldg(x + c);
@@ -186,7 +201,7 @@ __global__ void __launch_bounds__(256) k_op(OpView op, double sre, double sim, d
       }
     } else {
 #pragma unroll 4
-      for (int k = b + lane; k < e; k += V) {
+      for (int k = b + lane; k < e; k += W) {
         const double av = __ldcs(op.a.val + k);
         const int c = __ldcs(op.a.colind + k);
         a1 = fma(av, __ldg(x + c), a1);
@@ -194,13 +209,15 @@ __global__ void __launch_bounds__(256) k_op(OpView op, double sre, double sim, d
       }
     }
   }
-  a1 = sub_sum<V>(a1);
-  if (PAIR) a2 = sub_sum<V>(a2);
+#define MPG_SUBSUM(v) v = V ? sub_sum<(V ? V : 2)>(v) : sub_sum_rt(v, W)
+  MPG_SUBSUM(a1);
+  if (PAIR) MPG_SUBSUM(a2);
   if (EM == E_SAMEPAT) {
-    e1 = sub_sum<V>(e1);
-    if (PAIR) e2 = sub_sum<V>(e2);
+    MPG_SUBSUM(e1);
+    if (PAIR) MPG_SUBSUM(e2);
   }
-  if (row < n && lane == 0) {
+#undef MPG_SUBSUM
+  if (ok && lane == 0) {
     if (EM == E_IDENT) {
       e1 = x[row];
       if (PAIR) e2 = x[n + row];
@@ -261,6 +278,23 @@ __global__ void k_stats(const int* __restrict__ rp, const int* __restrict__ ci, 
   }
   atomicMax(out, mx);
   if (notdiag) atomicAdd(out + 1, notdiag);
+}
+
+// Row bins: class key and identity index per row, class histogram.
+__global__ void k_bin_key(const int* __restrict__ rp, int nrows, unsigned char* __restrict__ key,
+                          int* __restrict__ idx, int* __restrict__ hist) {
+  __shared__ int sh[NBIN];
+  if (threadIdx.x < NBIN) sh[threadIdx.x] = 0;
+  __syncthreads();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < nrows) {
+    const int b = row_bin(rp[r + 1] - rp[r]);
+    key[r] = static_cast<unsigned char>(b);
+    idx[r] = r;
+    atomicAdd(sh + b, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < NBIN && sh[threadIdx.x]) atomicAdd(hist + threadIdx.x, sh[threadIdx.x]);
 }
 
 __global__ void k_sq_partial(const double* __restrict__ x, int64_t n, double* __restrict__ part) {
@@ -445,6 +479,37 @@ void csr_finalize_stats(DevCsr& m) {
   MPG_CUDA(cudaStreamSynchronize(c.stream));
   m.max_row = h[0];
   m.is_diag = m.nrows == m.ncols && h[1] == 0;
+  // Row bins for irregular matrices (the long-row split; runtime.cuh): the
+  // longest row far above the mean means a fixed sub-warp width leaves most
+  // lanes of a warp idle while one of its rows runs on.
+  static const int bins_env = [] {
+    const char* e = std::getenv("MPG_ROW_BINS");
+    return e ? std::atoi(e) : -1;  // 0: never, 1: always, default: by the row statistics
+  }();
+  const bool want = bins_env == 1 || (bins_env != 0 && m.max_row > 64 && double(m.max_row) > 4.0 * m.mean_row);
+  if (!want) return;
+  const int n = int(m.nrows);
+  DBuf<unsigned char> key(m.device, size_t(n)), key2(m.device, size_t(n));
+  DBuf<int> idx(m.device, size_t(n)), hist(m.device, NBIN);
+  m.brow = DBuf<int>(m.device, size_t(n));
+  MPG_CUDA(cudaMemsetAsync(hist.get(), 0, NBIN * sizeof(int), c.stream));
+  k_bin_key<<<grid_for(n), 256, 0, c.stream>>>(m.rowptr.get(), n, key.get(), idx.get(), hist.get());
+  MPG_CHECK_LAUNCH();
+  size_t tmp = 0;
+  MPG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.get(), key2.get(), idx.get(), m.brow.get(), n, 0, 3,
+                                           c.stream));
+  DBuf<char> t(m.device, tmp);
+  MPG_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, key.get(), key2.get(), idx.get(), m.brow.get(), n, 0, 3,
+                                           c.stream));
+  count_launch(2);
+  int hh[NBIN];
+  MPG_CUDA(cudaMemcpyAsync(hh, hist.get(), sizeof hh, cudaMemcpyDeviceToHost, c.stream));
+  MPG_CUDA(cudaStreamSynchronize(c.stream));
+  m.boff[0] = m.bblk[0] = 0;
+  for (int b = 0; b < NBIN; ++b) {
+    m.boff[b + 1] = m.boff[b] + hh[b];
+    m.bblk[b + 1] = m.bblk[b] + int((int64_t(hh[b]) * (2 << b) + 255) / 256);
+  }
 }
 
 CsrPtr csr_from_host(int device, int64_t nr, int64_t nc, const int64_t* rp, const int64_t* ci, const double* v) {
@@ -649,6 +714,12 @@ static void launch_spmv_v(const DevCsr& m, const double* x, double* y, double al
 
 void launch_spmv(const DevCsr& m, const double* x, double* y, double alpha, cudaStream_t s) {
   if (m.nrows == 0) return;
+  if (m.brow.get()) {
+    k_spmv<0><<<unsigned(m.bblk[NBIN]), 256, 0, s>>>(m.view(), x, y, alpha);
+    MPG_CHECK_LAUNCH();
+    count_launch();
+    return;
+  }
   switch (choose_vec_width(m.mean_row)) {
     case 2: launch_spmv_v<2>(m, x, y, alpha, s); break;
     case 4: launch_spmv_v<4>(m, x, y, alpha, s); break;
@@ -661,7 +732,7 @@ void launch_spmv(const DevCsr& m, const double* x, double* y, double alpha, cuda
 template <int V, int EM>
 static void launch_op_ve(const OpView& v, int64_t n, double sre, double sim, double ca, const double* x, double* y,
                          const double* resid, double scale, cudaStream_t s) {
-  const unsigned grid = grid_for(n * int64_t(V));
+  const unsigned grid = V ? grid_for(n * int64_t(V)) : unsigned(v.a.bblk[NBIN]);
   if (sim != 0.0) k_op<V, EM, true><<<grid, 256, 0, s>>>(v, sre, sim, ca, x, y, resid, scale);
   else k_op<V, EM, false><<<grid, 256, 0, s>>>(v, sre, sim, ca, x, y, resid, scale);
   MPG_CHECK_LAUNCH();
@@ -682,6 +753,10 @@ void launch_op(const ShiftedOp& op, bool transpose, double sre, double sim, doub
                const double* resid, double scale, cudaStream_t s, double* /*tmp_general*/) {
   if (op.n == 0) return;
   const OpView v = op.view(transpose);
+  if (v.a.brow) {
+    launch_op_v<0>(v, op.n, sre, sim, ca, x, y, resid, scale, s);
+    return;
+  }
   switch (op.vec_width) {
     case 2: launch_op_v<2>(v, op.n, sre, sim, ca, x, y, resid, scale, s); break;
     case 4: launch_op_v<4>(v, op.n, sre, sim, ca, x, y, resid, scale, s); break;

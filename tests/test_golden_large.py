@@ -204,7 +204,7 @@ def test_gpu_c5_sweep_matches_golden(mpg, gen, name):
     s = gen.config5(n=g["n"], max_len=g["max_len"])
     assert s.a.nnz == g["nnz"]
     op = mpg.ShiftedOperator(_dev(mpg, s.a), _dev(mpg, s.e_csr()))
-    res = mpg.spai_bench(op, s.b[:, 0], g["points"], gmres=mpg.GmresConfig(g["gmres_tol"], 1000),
+    res = mpg.run_spai_bench(op, s.b[:, 0], g["points"], gmres=mpg.GmresConfig(g["gmres_tol"], 1000),
                          mode=mpg.PrecondMode.REUSE_CHAIN, max_chain_len=16, keep_solutions=True)
     rows = res.report.rows
     assert [int(r.kind) for r in rows] == g["kinds"]

@@ -95,3 +95,21 @@ def test_empty_batch(mpg, gen):
     op = mpg.ShiftedOperator(mpg.SparseMatrix.from_csr(sysm.a.nrows, sysm.a.ncols, sysm.a.rowptr, sysm.a.colind,
                                                        sysm.a.val), None)
     assert mpg.gmres_batch(op, [], []) == []
+
+
+@pytest.mark.parametrize("n", [3000, 60000])
+def test_zipf_rows_spmv_and_shifted_operator(mpg, orc, gen, n):
+    """C5-type rows (Zipf(1.8) lengths 3 ... 2 000): the row-binned kernels
+    (runtime.cuh row bins: sub-warps of 2 ... 32 lanes by row length) against
+    the oracle (sparse.cpp:236-269, kron.cpp:34-64), both sides, real and pair."""
+    s = gen.config5(n=n, max_len=2000)
+    (A, Ao), (E, Eo) = _pair(gen, s.a), _pair(gen, s.e_csr())
+    x = gen.random_dense(n, 1, 70)[:, 0]
+    assert rel(A.multiply(x), Ao.multiply(x)) <= 1e-13
+    assert rel(A.multiply_transpose(x), Ao.multiply_transpose(x)) <= 1e-13
+    op = mpg.ShiftedOperator(A, E)
+    for sigma in (0.3, 1.5 + 0.7j):
+        xx = gen.random_dense(n * (2 if complex(sigma).imag else 1), 1, 71)[:, 0]
+        for transpose in (False, True):
+            ao, eo = (Ao.transpose(), Eo.transpose()) if transpose else (Ao, Eo)
+            assert rel(op.apply(sigma, xx, transpose), orc.kron_apply(orc.shifted(sigma), ao, eo, xx)) <= 1e-13
