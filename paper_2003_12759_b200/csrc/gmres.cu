@@ -102,6 +102,18 @@ __device__ __forceinline__ double sub_sum(double v) {
 __device__ __forceinline__ size_t hoff(int j) { return size_t(j) * size_t(j + 1) / 2; }
 
 // ---- chain stage: z[stage&1] = F_stage * src ------------------------------------
+// Irregular (row-binned) factors gather x at random columns: the chunk-major basis
+// vector V[k] (one 8 KB panel block per 16 rows: a 1 GB span at n = 2 M) is copied
+// to the plain vector z1 first, which stage 0 then reads (C5: chain SpMV 683 us with
+// the chunk-major gather against 326 us for the same-sized operator on a plain vector).
+__global__ void __launch_bounds__(256) k_unchunk(GmSolve* S) {
+  GmSolve& st = S[blockIdx.y];
+  if (st.phase != PH_RUN || st.stages == 0 || st.grouped_chain) return;
+  if (!st.fac[0].brow) return;
+  const double* v = st.V[st.k];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < st.n; i += gridDim.x * blockDim.x) st.z1[i] = v[vidx(i)];
+}
+
 // V = 0: the row-binned mapping for irregular factors (runtime.cuh bin_locate);
 // a solve is served by the launch that matches its factor.
 template <int V>
@@ -119,20 +131,15 @@ __global__ void __launch_bounds__(256) k_chain_stage(GmSolve* S, int stage, int 
     if (int(blockIdx.x) >= f.bblk[NBIN]) return;
     int r, W, lane;
     const bool ok = bin_locate(f, r, W, lane);
+    if (chunked) src = st.z1;  // k_unchunk's plain copy of V[k]
     for (int hf = 0; hf < halves; ++hf) {
       const int off = hf * f.nrows;
       double acc = 0.0;
       if (ok) {
         const int b = f.rowptr[r], e = f.rowptr[r + 1];
-        if (chunked) {
+        const double* x = src + off;
 #pragma unroll 4
-          for (int k = b + lane; k < e; k += W)
-            acc = fma(__ldcs(f.val + k), __ldg(src + vidx(off + __ldcs(f.colind + k))), acc);
-        } else {
-          const double* x = src + off;
-#pragma unroll 4
-          for (int k = b + lane; k < e; k += W) acc = fma(__ldcs(f.val + k), __ldg(x + __ldcs(f.colind + k)), acc);
-        }
+        for (int k = b + lane; k < e; k += W) acc = fma(__ldcs(f.val + k), __ldg(x + __ldcs(f.colind + k)), acc);
       }
       acc = sub_sum_rt(acc, W);
       if (ok && lane == 0) dst[off + r] = acc;
@@ -2081,6 +2088,29 @@ __device__ __forceinline__ void gf_producer(GmSolve* S, int ns, int TC, int tile
 // four rows of a quad are contracted with single-precision FMAs -- the products already carry the shadow's
 // 6e-8 rounding -- and only the 4-term partial is widened and accumulated in fp64; the correction's row sums
 // (coefficients ~1e-7, a few digits needed) are summed in single precision across the warp.
+// Packed single precision (FFMA2 / FMUL2 on sm_100a): two lanes of fp32 per instruction.
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};\n" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;\n" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;\n" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;\n" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ void lds_b64x2(uint32_t a, uint64_t& lo, uint64_t& hi) {
+  asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];\n" : "=l"(lo), "=l"(hi) : "r"(a));
+}
+
 template <int CF, int NGT>
 __device__ __forceinline__ void gf_consumer(GmSolve* S, int ns, int G, int TC, int tile_bytes, int stage_bytes, int NS,
                                             long long a, long long b, uint32_t ring, uint64_t* full, uint64_t* empty,
@@ -2089,12 +2119,18 @@ __device__ __forceinline__ void gf_consumer(GmSolve* S, int ns, int G, int TC, i
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int rq = warp;  // row quad of a 32-row chunk
   const int slot = blockIdx.x;
-  const uint32_t loff = uint32_t(lane) * 128u + uint32_t((rq ^ (lane & 7)) << 4);
+  // the row of the quad whose sums end on this lane (transposed warp reduction below): lanes 8 u .. 8 u + 7 hold row u
+  const int ur = lane >> 3;
+  const bool tail_lane = (lane & 7) == 0;
   GfCursor cu;
   cu.us = us;
-  float coef[NGC];
+  // per vector group: the lane's float4 inside a stage (chunk 0) and its per-chunk stride; lanes past the
+  // last vector read vector 0 (finite data) with a zero coefficient and never flush their sums, so the
+  // chunk loop needs no per-load predicate or address select
+  uint32_t goff[NGC], gstr[NGC];
+  uint64_t coef2[NGC];
   double acc[NGC];
-  double wsq = 0.0, acck = 0.0;  // lanes 0..3: row lane of the quad
+  double wsq = 0.0, acck = 0.0;  // on the tail lanes (0, 8, 16, 24: one row of the quad each)
   double* vk = nullptr;
   float* fk = nullptr;
   bool pend = false;
@@ -2119,7 +2155,14 @@ __device__ __forceinline__ void gf_consumer(GmSolve* S, int ns, int G, int TC, i
 #pragma unroll
       for (int i = 0; i < NGC; ++i) {
         const int j = 32 * i + lane;
-        coef[i] = (pend && j < nv) ? float(st.scale[j] * st.dp[j]) : 0.f;  // the correction coefficients of V[k]
+        const bool valid = j < nv;
+        const int ii = valid ? i : 0, ll = valid ? lane : 0;
+        const bool fullp = (ii >> 1) < pf;
+        goff[i] = uint32_t(fullp ? (ii >> 1) * TC : pf * TC) * 8192u + uint32_t(ii & 1) * 4096u + uint32_t(ll) * 128u +
+                  uint32_t((rq ^ (ll & 7)) << 4);
+        gstr[i] = fullp ? 8192u : uint32_t(mb) * 1024u;
+        const float cf = (pend && valid) ? float(st.scale[j] * st.dp[j]) : 0.f;  // the correction coefficients of V[k]
+        coef2[i] = pk2(cf, cf);
         acc[i] = 0.0;
       }
       wsq = 0.0;
@@ -2130,66 +2173,63 @@ __device__ __forceinline__ void gf_consumer(GmSolve* S, int ns, int G, int TC, i
     const uint32_t sbase = ring + uint32_t(stg) * uint32_t(stage_bytes);
     for (int cc0 = 0; cc0 < TC; cc0 += CF) {
       if (c0 + cc0 >= nchunks) break;
-      float sx[CF][4];
-      float wf[CF][4];
-      float4 v[CF][NGC];
+      uint64_t vlo[CF][NGC], vhi[CF][NGC];
+      uint64_t w01[CF], w23[CF];
+      float sx[CF];  // after the reduction: the correction's sum for row ur of the quad
 #pragma unroll
       for (int f = 0; f < CF; ++f) {
         const int cc = cc0 + f;
-        const bool ok = c0 + cc < nchunks;
-        const uint32_t cb = sbase + uint32_t(cc) * 8192u;
-        const uint32_t pb = sbase + uint32_t(pf * TC) * 8192u + uint32_t(cc * mb) * 1024u;
+        const bool ok = f == 0 || c0 + cc < nchunks;  // (uniform) a tile's last chunk pair may be half empty
         const uint32_t xb = sbase + uint32_t(tile_bytes) + uint32_t(cc) * uint32_t(GF_EXTRA) + uint32_t(rq) * 32u;
+        if (ok) {
 #pragma unroll
-        for (int i = 0; i < NGC; ++i) {
-          const uint32_t ad =
-              ((i >> 1) < pf ? cb + uint32_t((i >> 1) * TC) * 8192u : pb) + uint32_t(i & 1) * 4096u + loff;
-          v[f][i] = ok && 32 * i + lane < nv ? lds_f32x4(ad) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int i = 0; i < NGC; ++i) lds_b64x2(sbase + goff[i] + uint32_t(cc) * gstr[i], vlo[f][i], vhi[f][i]);
+          const double2 wlo = lds_f64x2(xb);
+          const double2 whi = lds_f64x2(xb + 16u);
+          w01[f] = pk2(float(wlo.x), float(wlo.y));
+          w23[f] = pk2(float(whi.x), float(whi.y));
+        } else {
+#pragma unroll
+          for (int i = 0; i < NGC; ++i) vlo[f][i] = vhi[f][i] = 0ull;
+          w01[f] = w23[f] = 0ull;
         }
-        const double2 wlo = ok ? lds_f64x2(xb) : make_double2(0.0, 0.0);
-        const double2 whi = ok ? lds_f64x2(xb + 16u) : make_double2(0.0, 0.0);
-        wf[f][0] = float(wlo.x);
-        wf[f][1] = float(wlo.y);
-        wf[f][2] = float(whi.x);
-        wf[f][3] = float(whi.y);
-        float x0 = 0.f, x1 = 0.f, x2 = 0.f, x3 = 0.f;
+        sx[f] = 0.f;
         if (pend) {
+          uint64_t x01 = 0ull, x23 = 0ull;
 #pragma unroll
           for (int i = 0; i < NGC; ++i) {
-            x0 = fmaf(coef[i], v[f][i].x, x0);
-            x1 = fmaf(coef[i], v[f][i].y, x1);
-            x2 = fmaf(coef[i], v[f][i].z, x2);
-            x3 = fmaf(coef[i], v[f][i].w, x3);
+            x01 = fma2(coef2[i], vlo[f][i], x01);
+            x23 = fma2(coef2[i], vhi[f][i], x23);
           }
+          // transposed reduction: 6 shuffles instead of 20; row u's sum ends on lanes 8 u .. 8 u + 7
+          float x0, x1, x2, x3;
+          upk2(x01, x0, x1);
+          upk2(x23, x2, x3);
+          const bool hi16 = (lane & 16) != 0, hi8 = (lane & 8) != 0;
+          const float s0 = hi16 ? x0 : x2, s1 = hi16 ? x1 : x3;
+          const float y0 = (hi16 ? x2 : x0) + __shfl_xor_sync(0xffffffffu, s0, 16);
+          const float y1 = (hi16 ? x3 : x1) + __shfl_xor_sync(0xffffffffu, s1, 16);
+          float z = (hi8 ? y1 : y0) + __shfl_xor_sync(0xffffffffu, hi8 ? y0 : y1, 8);
+          z += __shfl_xor_sync(0xffffffffu, z, 4);
+          z += __shfl_xor_sync(0xffffffffu, z, 2);
+          z += __shfl_xor_sync(0xffffffffu, z, 1);
+          sx[f] = z;
         }
-        sx[f][0] = x0;
-        sx[f][1] = x1;
-        sx[f][2] = x2;
-        sx[f][3] = x3;
-      }
-      if (pend) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-          for (int f = 0; f < CF; ++f)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) sx[f][u] += __shfl_xor_sync(0xffffffffu, sx[f][u], o);
       }
 #pragma unroll
       for (int f = 0; f < CF; ++f) {
         const int cc = cc0 + f;
-        if (lane < 4 && c0 + cc < nchunks) {
-          // row `lane` of the quad: V[k] staged (uncorrected) for h'_k, corrected to global, shadow written
+        if (tail_lane && c0 + cc < nchunks) {
+          // row ur of the quad: V[k] staged (uncorrected) for h'_k, corrected to global, shadow written
           const uint32_t xb = sbase + uint32_t(tile_bytes) + uint32_t(cc) * uint32_t(GF_EXTRA) + uint32_t(rq) * 32u +
-                              uint32_t(lane) * 8u;
+                              uint32_t(ur) * 8u;
           double wv, yv;
           asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(wv) : "r"(xb));
           asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(yv) : "r"(xb + 256u));
           acck = fma(yv, wv, acck);
           wsq = fma(wv, wv, wsq);
-          const float sl = lane == 0 ? sx[f][0] : lane == 1 ? sx[f][1] : lane == 2 ? sx[f][2] : sx[f][3];
-          const double uv = yv - double(sl);
-          const int row = (c0 + cc) * FCHUNK + 4 * rq + lane;
+          const double uv = yv - double(sx[f]);
+          const int row = (c0 + cc) * FCHUNK + 4 * rq + ur;
           if (row < n) {
             if (pend) vk[vidx(row)] = uv;
             fk[fidx(row)] = float(uv);
@@ -2197,8 +2237,10 @@ __device__ __forceinline__ void gf_consumer(GmSolve* S, int ns, int G, int TC, i
         }
 #pragma unroll
         for (int i = 0; i < NGC; ++i) {
-          const float pr = fmaf(v[f][i].x, wf[f][0], fmaf(v[f][i].y, wf[f][1], fmaf(v[f][i].z, wf[f][2], v[f][i].w * wf[f][3])));
-          acc[i] += double(pr);
+          const uint64_t p2 = fma2(vhi[f][i], w23[f], mul2(vlo[f][i], w01[f]));
+          float pa, pb;
+          upk2(p2, pa, pb);
+          acc[i] += double(pa + pb);
         }
       }
     }
@@ -3180,6 +3222,11 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     }
     if (!any_plain_chain) return;
     if (max_fac_bblk) {
+      if (stage == 0 && mode == 0) {
+        k_unchunk<<<dim3(unsigned(std::min<int64_t>(cdiv(nmax, 256), 2368)), unsigned(ns)), 256, 0, s>>>(dS.get());
+        ++launches_per_iter;
+        mark(PK_CHAIN);
+      }
       k_chain_stage<0><<<dim3(unsigned(max_fac_bblk), unsigned(ns)), 256, 0, s>>>(dS.get(), stage, mode);
       ++launches_per_iter;
       mark(mode == 0 ? PK_CHAIN : PK_ASM);

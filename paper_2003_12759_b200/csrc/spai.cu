@@ -28,6 +28,7 @@
 #include <cfloat>
 
 #include <climits>
+#include <cstdio>
 #include <string>
 
 #include "runtime.cuh"
@@ -66,6 +67,7 @@ struct SpaiParams {
   const int* icnt;
   int istride;
   int fixed_np, only_col, raw;
+  unsigned long long* phase;  // MPG_SPAI_PHASES: clock cycles summed over warps in rows / gather / QR / residual
 };
 
 struct WarpWS {
@@ -595,11 +597,22 @@ __global__ void __launch_bounds__(128) k_spai(SpaiParams P) {
     rhs_norm2 = wsum(rhs_norm2);
     const double threshold = P.fill_tol * sqrt(rhs_norm2);
     // first solve
+    long long tc0 = P.phase ? clock64() : 0, tc1, ph[4] = {0, 0, 0, 0};
+#define MPG_PH(i)                 \
+  if (P.phase) {                  \
+    tc1 = clock64();              \
+    ph[i] += tc1 - tc0;           \
+    tc0 = tc1;                    \
+  }
     int m = build_rows(P, w, np, lane);
+    MPG_PH(0)
     double outside_sq = 0.0;
     gather(P, w, np, m, rr, rv, rn, outside_sq, lane);
+    MPG_PH(1)
     bool rankdef = qr_solve(w, m, np, lane);
+    MPG_PH(2)
     double local_sq = residual_on_I(P, w, np, m, rr, rv, rn, lane);
+    MPG_PH(3)
     double residual = sqrt(local_sq + outside_sq);
     for (int sweep = 0; sweep < P.max_sweeps; ++sweep) {
       if (residual <= threshold) break;
@@ -643,12 +656,20 @@ __global__ void __launch_bounds__(128) k_spai(SpaiParams P) {
       }
       __syncwarp();
       ++np;
+      MPG_PH(3)
       m = build_rows(P, w, np, lane);
+      MPG_PH(0)
       gather(P, w, np, m, rr, rv, rn, outside_sq, lane);
+      MPG_PH(1)
       rankdef = qr_solve(w, m, np, lane);
+      MPG_PH(2)
       local_sq = residual_on_I(P, w, np, m, rr, rv, rn, lane);
+      MPG_PH(3)
       residual = sqrt(local_sq + outside_sq);
     }
+#undef MPG_PH
+    if (P.phase && lane == 0)
+      for (int i = 0; i < 4; ++i) atomicAdd(P.phase + i, static_cast<unsigned long long>(ph[i]));
     if (rankdef && !P.raw) {
       if (!P.update) {
         // diagonal fallback (spai.cpp:196-218)
@@ -860,9 +881,23 @@ SpaiOutcome spai_or_update(const CsrPtr& a, const CsrPtr& prev, const SpaiOption
   P.ipat = ipat.get();
   P.icnt = icnt.get();
   P.istride = o.max_fill_per_col;
+  DBuf<unsigned long long> phase;
+  if (std::getenv("MPG_SPAI_PHASES")) {
+    phase = DBuf<unsigned long long>(dev, 4);
+    MPG_CUDA(cudaMemsetAsync(phase.get(), 0, 4 * sizeof(unsigned long long), s));
+    P.phase = phase.get();
+  }
   k_spai<<<unsigned(warps / 4), 128, 0, s>>>(P);
   MPG_CHECK_LAUNCH();
   count_launch();
+  if (P.phase) {
+    unsigned long long h[4];
+    MPG_CUDA(cudaMemcpyAsync(h, phase.get(), sizeof h, cudaMemcpyDeviceToHost, s));
+    MPG_CUDA(cudaStreamSynchronize(s));
+    const double tot = double(h[0] + h[1] + h[2] + h[3]) + 1.0;
+    std::fprintf(stderr, "[mpg spai phases] warps %d  rows %.1f%%  gather %.1f%%  qr %.1f%%  residual+select %.1f%%\n", warps,
+                 100.0 * h[0] / tot, 100.0 * h[1] / tot, 100.0 * h[2] / tot, 100.0 * h[3] / tot);
+  }
   // CSR of P^T (column lists), then P = (P^T)^T on the device
   DBuf<int> off(dev, size_t(n) + 1);
   {

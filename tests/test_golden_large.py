@@ -207,7 +207,8 @@ def test_gpu_c5_sweep_matches_golden(mpg, gen, name):
     res = mpg.run_spai_bench(op, s.b[:, 0], g["points"], gmres=mpg.GmresConfig(g["gmres_tol"], 1000),
                          mode=mpg.PrecondMode.REUSE_CHAIN, max_chain_len=16, keep_solutions=True)
     rows = res.report.rows
-    assert [int(r.kind) for r in rows] == g["kinds"]
+    names = {1: "fresh", 2: "horizontal", 3: "vertical", 4: "reused_same_matrix"}
+    assert [r.kind for r in rows] == [names.get(k, "none") for k in g["kinds"]]
     failed = [i for i, r in enumerate(rows) if r.gmres_iterations >= 1000]
     assert failed == g["failed"]
     for i, r in enumerate(rows):
