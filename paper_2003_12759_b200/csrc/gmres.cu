@@ -290,27 +290,30 @@ __global__ void __launch_bounds__(256) k_chain_multi(GmSolve* S, Group grp, CsrV
   }
   if (!any) return;
   const int lane = threadIdx.x & (V - 1);
-  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / V);
-  double acc[MB];
+  // grid-stride over row blocks (small grids for the mostly idle assembly-mode launches, see k_iter_op_multi)
+  for (int64_t base = int64_t(blockIdx.x) * (256 / V); base < f.nrows; base += int64_t(gridDim.x) * (256 / V)) {
+    const int row = int(base) + int(threadIdx.x) / V;
+    double acc[MB];
 #pragma unroll
-  for (int q = 0; q < MB; ++q) acc[q] = 0.0;
-  if (row < f.nrows) {
-    const int b = f.rowptr[row], e = f.rowptr[row + 1];
+    for (int q = 0; q < MB; ++q) acc[q] = 0.0;
+    if (row < f.nrows) {
+      const int b = f.rowptr[row], e = f.rowptr[row + 1];
 #pragma unroll 2
-    for (int k = b + lane; k < e; k += V) {
-      const double a = __ldcs(f.val + k);
-      const int c = __ldcs(f.colind + k);
+      for (int k = b + lane; k < e; k += V) {
+        const double a = __ldcs(f.val + k);
+        const int c = __ldcs(f.colind + k);
+#pragma unroll
+        for (int q = 0; q < MB; ++q)
+          if (act[q]) acc[q] = fma(a, __ldg(src[q] + (basis ? vidx(c) : c)), acc[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < MB; ++q) acc[q] = sub_sum<V>(acc[q]);
+    if (row < f.nrows && lane == 0) {
 #pragma unroll
       for (int q = 0; q < MB; ++q)
-        if (act[q]) acc[q] = fma(a, __ldg(src[q] + (basis ? vidx(c) : c)), acc[q]);
+        if (act[q]) dst[q][row] = acc[q];
     }
-  }
-#pragma unroll
-  for (int q = 0; q < MB; ++q) acc[q] = sub_sum<V>(acc[q]);
-  if (row < f.nrows && lane == 0) {
-#pragma unroll
-    for (int q = 0; q < MB; ++q)
-      if (act[q]) dst[q][row] = acc[q];
   }
 }
 
@@ -337,7 +340,11 @@ __global__ void __launch_bounds__(256) k_iter_op_multi(GmSolve* S, Group grp, Op
   if (!any) return;
   const int n = op.a.nrows;
   const int lane = threadIdx.x & (V - 1);
-  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / V);
+  // grid-stride over row blocks: the assembly-mode launches (one per iteration in the captured graph,
+  // almost always with no solve in assembly) use a small grid, so an idle launch costs a few
+  // microseconds instead of the ~50 us of 18 600 CTAs that each read the solve states and exit
+  for (int64_t base = int64_t(blockIdx.x) * (256 / V); base < n; base += int64_t(gridDim.x) * (256 / V)) {
+  const int row = int(base) + int(threadIdx.x) / V;
   double a1[MB], e1[MB];
 #pragma unroll
   for (int q = 0; q < MB; ++q) a1[q] = e1[q] = 0.0;
@@ -381,6 +388,7 @@ __global__ void __launch_bounds__(256) k_iter_op_multi(GmSolve* S, Group grp, Op
       if (mode == 0) st.V[st.k + 1][vidx(row)] = st.scale[st.k] * y1;
       else st.rbuf[row] = st.V[0][vidx(row)] - y1;
     }
+  }
   }
 }
 
@@ -2003,6 +2011,18 @@ constexpr int GF_EXTRA = 512;  // per chunk and stage: 32 rows of w and of V[k] 
 constexpr int GF_SMEM = 1024 + GX_RING + (GX_CWARPS * GX_MAXV + 2 * GX_CWARPS) * 8 + 2 * GX_MAXST * 8;
 
 __device__ __forceinline__ int gf_chunks(const GmSolve& st) { return ((st.n + 31) & ~31) / FCHUNK; }
+// Boxes per chunk for nv shadow vectors: pf 64-vector boxes (8 KB) and mb 8-vector boxes (1 KB) of the last
+// panel. Below 256 vectors an 8-vector box costs about twice its bytes (launch list, profiles/r02: k = 120,
+// one panel + 7 small boxes, 2 315 us against 1 667 us for two full panels at k = 128), so from `mbfull`
+// small boxes on the whole last panel is fetched instead; the vectors past nv are never read from the stage.
+__device__ __forceinline__ void gf_split(int nv, int mbfull, int& pf, int& mb) {
+  pf = nv >> 6;
+  mb = ((nv & 63) + 7) >> 3;
+  if (nv < 256 && mb >= mbfull) {
+    ++pf;
+    mb = 0;
+  }
+}
 __device__ __forceinline__ void bulk_g2s_a(uint32_t dst, const void* src, unsigned bytes, uint32_t mbar, uint64_t pol) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(dst),
@@ -2057,7 +2077,8 @@ __device__ __forceinline__ void gf_producer(GmSolve* S, int ns, int TC, int tile
     }
     const int c0 = int(g - pc.off) * TC;
     const int nch = min(TC, nchunks - c0);
-    const int pf = nv >> 6, mb = ((nv & 63) + 7) >> 3;
+    int pf, mb;
+    gf_split(nv, us.low, pf, mb);
     const int per = pf + mb + 4;
     if (lane == 0) mbar_expect_tx(full + stg, unsigned(nch) * unsigned(pf * 8192 + mb * 1024 + GF_EXTRA));
     __syncwarp();
@@ -2147,8 +2168,7 @@ __device__ __forceinline__ void gf_consumer(GmSolve* S, int ns, int G, int TC, i
       nv = nj - 1;
       n = st.n;
       nchunks = gf_chunks(st);
-      pf = nv >> 6;
-      mb = ((nv & 63) + 7) >> 3;
+      gf_split(nv, us.low, pf, mb);
       pend = st.pend != 0;
       vk = st.V[nj - 1];
       fk = st.F[nj - 1];
@@ -2292,7 +2312,9 @@ __global__ void __launch_bounds__(GX_THREADS, 1) k_gs_tmxf(GmSolve* S, int ns, i
   bool any = false;
   for (int s = 0; s < ns; ++s) any = any || gx_handles(S[s], us);
   if (!any) return;
-  const int chunk_bytes = (nvmax >> 6) * 8192 + (((nvmax & 63) + 7) >> 3) * 1024;
+  int pfm, mbm;
+  gf_split(nvmax, us.low, pfm, mbm);
+  const int chunk_bytes = pfm * 8192 + mbm * 1024;
   const int CF = nvmax <= 192 ? 2 : 1;
   int TC = 1;
   while (TC < 16 && (TC < CF || 2 * TC * (chunk_bytes + GF_EXTRA) <= 48 * 1024)) TC *= 2;
@@ -2432,7 +2454,29 @@ __global__ void __launch_bounds__(256) k_dcgs_fix(GmSolve* S) {
   double hd[RPT];
 #pragma unroll
   for (int u = 0; u < RPT; ++u) hd[u] = 0.0;
-  for (int j = 0; j < k; ++j) {
+  // (the loop is a chain of L2 round trips unless several columns are in flight: 8 per step,
+  // and only the row slots a basis of k + 1 vectors reaches)
+  const int nu = min(RPT, (k + 256) / 256);
+  int j = 0;
+  for (; j + 8 <= k; j += 8) {
+    double cv[8][RPT];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double* col = st.Hu + hoff2(j + c);
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int i = threadIdx.x + u * 256;
+        cv[c][u] = (u < nu && i <= j + c + 1) ? col[i] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double dj = dp[j + c];
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) hd[u] = fma(cv[c][u], dj, hd[u]);
+    }
+  }
+  for (; j < k; ++j) {
     const double dj = dp[j];
     const double* col = st.Hu + hoff2(j);
 #pragma unroll
@@ -2833,6 +2877,8 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   // With it the split moves to 96 (C3 step: 128 -> 2 532 ms, 96 -> 2 497, 64 -> 2 504, 32 -> 2 526).
   const bool f32_on = dcgs_on && (psel.sel & 4) && !(std::getenv("MPG_GS_F32") && std::atoi(std::getenv("MPG_GS_F32")) == 0);
   if (f32_on && !std::getenv("MPG_GS_DOT_SPLIT")) psel.split = 96;
+  // k_gs_tmxf: from this many 8-vector boxes on, the last shadow panel is fetched whole (gf_split; 9: never)
+  psel.low = std::getenv("MPG_GF_MBFULL") ? std::atoi(std::getenv("MPG_GF_MBFULL")) : 5;
   const int upd_kind = usel.sel;
   const bool want_maps = ((usel.sel | psel.sel) & 6) != 0;  // panel tensor maps for k_gs_tmx
   std::vector<SolveHost> sh(static_cast<size_t>(ns));
@@ -3210,12 +3256,13 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         mark(PK_CHAIN);
         continue;
       }
+      const unsigned gridm = mode == 0 ? grid : std::min<unsigned>(grid, unsigned(c.sm_count) * 8u);
       switch (Vf) {
-        case 2: k_chain_multi<2><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
-        case 4: k_chain_multi<4><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
-        case 8: k_chain_multi<8><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
-        case 16: k_chain_multi<16><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
-        default: k_chain_multi<32><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
+        case 2: k_chain_multi<2><<<gridm, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
+        case 4: k_chain_multi<4><<<gridm, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
+        case 8: k_chain_multi<8><<<gridm, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
+        case 16: k_chain_multi<16><<<gridm, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
+        default: k_chain_multi<32><<<gridm, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), stage, mode); break;
       }
       ++launches_per_iter;
       mark(mode == 0 ? PK_CHAIN : PK_ASM);
@@ -3350,7 +3397,8 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
 #undef MPG_OPL
     for (const Group& g : (mode == 0 ? op_groups_run : op_groups_asm)) {
       const OpView& ov = hs[size_t(g.idx[0])].transpose ? opt_ : opn;
-      const unsigned grid1 = cdiv(nb * int64_t(Vop), 256);
+      const unsigned gfull = cdiv(nb * int64_t(Vop), 256);
+      const unsigned grid1 = mode == 0 ? gfull : std::min<unsigned>(gfull, unsigned(c.sm_count) * 8u);
 #define MPG_OPM(VV)                                                                                            \
   switch (op.emode) {                                                                                          \
     case E_IDENT: k_iter_op_multi<VV, E_IDENT><<<grid1, 256, 0, s>>>(dS.get(), g, ov, mode); break;           \
