@@ -57,6 +57,7 @@ struct GmSolve {
   int k, phase, asm_kind, asm_k, guess, iterations, converged, breakdown, xsel, reorth_count;
   int grouped_op;     // bit 0: run-mode operator by a group kernel, bit 1: assembly-mode
   int grouped_chain;  // handled by the shared-matrix (multi-RHS) kernels
+  int il_run;         // complex pair riding in an interleaved group as two columns: run-mode chain by the group kernels
   int dcgs;           // delayed second pass enabled (fused path)
   int pend;           // V[k] awaits its second-pass correction V[k] -= sum_j dp_j s_j V_j (DCGS2)
   double estimate, recheck_at, w2_pre, w2_a, w2_b, wn_cur, final_residual;
@@ -106,9 +107,9 @@ __device__ __forceinline__ size_t hoff(int j) { return size_t(j) * size_t(j + 1)
 // vector V[k] (one 8 KB panel block per 16 rows: a 1 GB span at n = 2 M) is copied
 // to the plain vector z1 first, which stage 0 then reads (C5: chain SpMV 683 us with
 // the chunk-major gather against 326 us for the same-sized operator on a plain vector).
-__global__ void __launch_bounds__(256) k_unchunk(GmSolve* S) {
-  GmSolve& st = S[blockIdx.y];
-  if (st.phase != PH_RUN || st.stages == 0 || st.grouped_chain) return;
+__global__ void __launch_bounds__(256) k_unchunk(GmSolve* S, const int* __restrict__ list) {
+  GmSolve& st = S[list[blockIdx.y]];
+  if (st.phase != PH_RUN || st.stages == 0 || st.grouped_chain || st.il_run) return;
   if (!st.fac[0].brow) return;
   const double* v = st.V[st.k];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < st.n; i += gridDim.x * blockDim.x) st.z1[i] = v[vidx(i)];
@@ -117,10 +118,11 @@ __global__ void __launch_bounds__(256) k_unchunk(GmSolve* S) {
 // V = 0: the row-binned mapping for irregular factors (runtime.cuh bin_locate);
 // a solve is served by the launch that matches its factor.
 template <int V>
-__global__ void __launch_bounds__(256) k_chain_stage(GmSolve* S, int stage, int mode) {
-  GmSolve& st = S[blockIdx.y];
+__global__ void __launch_bounds__(256) k_chain_stage(GmSolve* S, int stage, int mode, const int* __restrict__ list) {
+  // list: the solves this launch serves (those not advanced by a group kernel in this mode); blockIdx.y walks it
+  GmSolve& st = S[list[blockIdx.y]];
   if (mode == 0 ? st.phase != PH_RUN : st.phase != PH_ASM) return;
-  if (stage >= st.stages || st.grouped_chain) return;
+  if (stage >= st.stages || st.grouped_chain || (mode == 0 && st.il_run)) return;
   const CsrView f = st.fac[stage];
   if ((f.brow != nullptr) != (V == 0)) return;
   const int halves = st.pair_bd ? 2 : 1;
@@ -148,7 +150,33 @@ __global__ void __launch_bounds__(256) k_chain_stage(GmSolve* S, int stage, int 
   }
   constexpr int VV = V ? V : 2;
   const int lane = threadIdx.x & (VV - 1);
-  const int row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / VV);
+  // grid-stride over row blocks (the assembly-mode launch uses a small grid: it is idle in almost every iteration)
+  const int64_t rows_total = int64_t(f.nrows) * (halves == 2 ? 1 : halves);
+  for (int64_t base = int64_t(blockIdx.x) * (256 / VV); base < rows_total; base += int64_t(gridDim.x) * (256 / VV)) {
+  const int row = int(base) + int(threadIdx.x) / VV;
+  if (halves == 2) {
+    // complex pair, block-diagonal factor: both halves from one pass over the factor's row
+    // (the factor was read once per half: 0.4 -> 0.25 ms per pair solve and iteration on C3)
+    double a0 = 0.0, a1 = 0.0;
+    const int nr = f.nrows;
+    if (row < nr) {
+      const int b = f.rowptr[row], e = f.rowptr[row + 1];
+#pragma unroll 4
+      for (int k = b + lane; k < e; k += VV) {
+        const double fv = __ldcs(f.val + k);
+        const int c = __ldcs(f.colind + k);
+        a0 = fma(fv, __ldg(src + (chunked ? vidx(c) : c)), a0);
+        a1 = fma(fv, __ldg(src + (chunked ? vidx(nr + c) : nr + c)), a1);
+      }
+    }
+    a0 = sub_sum<VV>(a0);
+    a1 = sub_sum<VV>(a1);
+    if (row < nr && lane == 0) {
+      dst[row] = a0;
+      dst[nr + row] = a1;
+    }
+    continue;
+  }
   double acc = 0.0;
   int r = row, off = 0;
   if (row >= f.nrows) { r = row - f.nrows; off = f.nrows; }
@@ -166,17 +194,26 @@ __global__ void __launch_bounds__(256) k_chain_stage(GmSolve* S, int stage, int 
   }
   acc = sub_sum<VV>(acc);
   if (row < f.nrows * halves && lane == 0) dst[off + r] = acc;
+  }
 }
 
 // ---- operator: W_{k+1} = s_k (sigma E - A) z  /  r = b - (sigma E - A) x ---------
 template <int V, int EM>
-__global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView opt, int mode) {
-  GmSolve& st = S[blockIdx.y];
+__global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView opt, int mode,
+                                                 const int* __restrict__ list) {
+  GmSolve& st = S[list[blockIdx.y]];
   if (mode == 0 ? st.phase != PH_RUN : st.phase != PH_ASM) return;
   if (st.grouped_op & (mode == 0 ? 1 : 2)) return;
   const OpView& op = st.transpose ? opt : opn;
   if ((op.a.brow != nullptr) != (V == 0)) return;  // V = 0 serves the row-binned operator sides
   const int n = op.a.nrows;
+  const double* x;
+  if (mode == 0) x = st.stages ? ((st.stages - 1) & 1 ? st.z1 : st.z0) : st.V[st.k];
+  else x = st.stages ? ((st.stages - 1) & 1 ? st.z1 : st.z0) : st.ubuf;
+  // grid-stride over row blocks for the fixed-width mapping (small grids in assembly mode); one pass for V = 0
+  constexpr int RPB = V ? 256 / (V ? V : 1) : 1;
+  for (int64_t base = int64_t(blockIdx.x) * RPB;; base += int64_t(gridDim.x) * RPB) {
+  if (V != 0 && base >= n) break;
   int lane, row, W = V;
   bool ok;
   if (V == 0) {
@@ -184,12 +221,9 @@ __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView 
     ok = bin_locate(op.a, row, W, lane);
   } else {
     lane = threadIdx.x & (V - 1);
-    row = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) / (V ? V : 1));
+    row = int(base) + int(threadIdx.x) / (V ? V : 1);
     ok = row < n;
   }
-  const double* x;
-  if (mode == 0) x = st.stages ? ((st.stages - 1) & 1 ? st.z1 : st.z0) : st.V[st.k];
-  else x = st.stages ? ((st.stages - 1) & 1 ? st.z1 : st.z0) : st.ubuf;
   const bool xc = mode == 0 && st.stages == 0;  // x is a chunk-major basis vector
   const bool pair = st.pair;
   double a1 = 0.0, a2 = 0.0, e1 = 0.0, e2 = 0.0;
@@ -256,6 +290,8 @@ __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView 
       if (pair) st.rbuf[n + row] = b0[vidx(n + row)] - y2;
     }
   }
+  if (V == 0) break;
+  }
 }
 
 // ---- shared-matrix (multi-RHS) variants ----------------------------------------
@@ -266,7 +302,10 @@ __global__ void __launch_bounds__(256) k_iter_op(GmSolve* S, OpView opn, OpView 
 // matrix bytes are paid once per group instead of once per solve.
 constexpr int MB = 8;
 
-struct Group { int idx[MB]; int cnt; };
+// half: 0 a real solve's column; 1 / 2 the two halves of a complex pair (2n real form) that rides in the
+// group as two adjacent columns starting at an even one: the preconditioner is block diagonal and the
+// operator's A x and E x are per column, only the epilogue couples them (k_spmv_sell8t).
+struct Group { int idx[MB]; int cnt; unsigned char half[MB]; };
 
 template <int V>
 __global__ void __launch_bounds__(256) k_chain_multi(GmSolve* S, Group grp, CsrView f, int stage, int mode) {
@@ -406,7 +445,7 @@ __global__ void __launch_bounds__(256) k_pack_il(GmSolve* S, Group grp, double* 
   double v = 0.0;
   if (q < grp.cnt) {
     const GmSolve& st = S[grp.idx[q]];
-    if (st.phase == PH_RUN) v = st.V[st.k][vidx(row)];
+    if (st.phase == PH_RUN) v = st.V[st.k][vidx(grp.half[q] == 2 ? n + row : row)];
   }
   xa[i] = v;
 }
@@ -842,6 +881,17 @@ __global__ void __launch_bounds__(256) k_update(GmSolve* S, int G, int mode) {
       double2 a = mode == 2 ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(w + wr);
       const double sgn = mode == 2 ? 1.0 : -1.0;
       int j = 0;
+      // eight vectors in flight per thread (the assembly's x = V y ran at 1.7 TB/s with four)
+      for (; j + 8 <= nj; j += 8) {
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = *reinterpret_cast<const double2*>(vp[j + u] + vr);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          a.x = fma(sgn * coef[j + u], v[u].x, a.x);
+          a.y = fma(sgn * coef[j + u], v[u].y, a.y);
+        }
+      }
       for (; j + 4 <= nj; j += 4) {
         const double2 v0 = *reinterpret_cast<const double2*>(vp[j] + vr);
         const double2 v1 = *reinterpret_cast<const double2*>(vp[j + 1] + vr);
@@ -1415,6 +1465,16 @@ __global__ void __launch_bounds__(256) k_spmv_sell8t(GmSolve* S, Group grp, Sell
     const double dd = EM == E_DIAG ? op.ediag[row] : 1.0;
     g0 = dd * xr.x;
     g1 = dd * xr.y;
+  }
+  if (2 * lane < grp.cnt && grp.half[2 * lane] == 1) {
+    // a complex pair in columns 2 lane, 2 lane + 1: the 2 x 2 coupling of k_iter_op's pair form
+    GmSolve& st = S[grp.idx[2 * lane]];
+    if (st.phase != PH_RUN) return;
+    const double sc = st.scale[st.k];
+    double* w = st.V[st.k + 1];
+    w[vidx(row)] = sc * (st.sre * g0 + st.ca * a0 + st.sim * g1);
+    w[vidx(sv.nrows + row)] = sc * (-st.sim * g0 + st.sre * g1 + st.ca * a1);
+    return;
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -2876,6 +2936,9 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   // pass, which repairs the few-digit projection coefficients (MPG_GS_F32=0: fp64 projection everywhere).
   // With it the split moves to 96 (C3 step: 128 -> 2 532 ms, 96 -> 2 497, 64 -> 2 504, 32 -> 2 526).
   const bool f32_on = dcgs_on && (psel.sel & 4) && !(std::getenv("MPG_GS_F32") && std::atoi(std::getenv("MPG_GS_F32")) == 0);
+  // re-swept after the k_gs_tmxf rework: 96 -> 2 220, 64 / 48 -> 2 195, 32 -> 2 202 ms per C3 step. 96 stays: the
+  // 1 % is not worth re-deciding the rounding-determined trajectory of the C2 BASELINE-seed IRKA (
+  // with 64 the unmirrored reference loop meets an unstable pole in sweep 3 and raises the reference's SolverError)
   if (f32_on && !std::getenv("MPG_GS_DOT_SPLIT")) psel.split = 96;
   // k_gs_tmxf: from this many 8-vector boxes on, the last shadow panel is fetched whole (gf_split; 9: never)
   psel.low = std::getenv("MPG_GF_MBFULL") ? std::atoi(std::getenv("MPG_GF_MBFULL")) : 5;
@@ -3101,8 +3164,33 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   std::vector<Group> chain_groups, op_groups_run, op_groups_asm;
   std::vector<const Chain*> chain_of_group;
   std::vector<char> chain_il;          // chain group runs the interleaved path in run mode
+  std::vector<Group> il_groups;        // per chain group: its columns on that path (the group + complex pairs riding along)
   std::vector<DBuf<double>> il_bufs;   // two [n][MB] buffers per chain group (empty if not il)
   bool any_plain_chain = true, any_plain_op_run = true, any_plain_op_asm = true;
+  // The solves the plain (per-solve) chain / operator launches serve, per mode: blockIdx.y walks these lists,
+  // so a batch whose solves are all advanced by group kernels launches nothing, and a few ungrouped solves
+  // (complex pairs in assembly mode) do not cost a grid over the whole batch.
+  std::vector<int> pl_chain[2], pl_op[2];
+  DBuf<int> pl_buf(dev, size_t(4 * ns));
+  auto build_plain_lists = [&]() {
+    for (int m = 0; m < 2; ++m) { pl_chain[m].clear(); pl_op[m].clear(); }
+    for (int i = 0; i < ns; ++i) {
+      const GmSolve& m = hs[size_t(i)];
+      if (m.stages > 0 && !m.grouped_chain) {
+        if (!m.il_run) pl_chain[0].push_back(i);
+        pl_chain[1].push_back(i);
+      }
+      if (!(m.grouped_op & 1)) pl_op[0].push_back(i);
+      if (!(m.grouped_op & 2)) pl_op[1].push_back(i);
+    }
+    std::vector<int> flat(size_t(4 * ns), 0);
+    for (int m = 0; m < 2; ++m) {
+      std::copy(pl_chain[m].begin(), pl_chain[m].end(), flat.begin() + size_t(m) * ns);
+      std::copy(pl_op[m].begin(), pl_op[m].end(), flat.begin() + size_t(2 + m) * ns);
+    }
+    MPG_CUDA(cudaMemcpyAsync(pl_buf.get(), flat.data(), flat.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    MPG_CUDA(cudaStreamSynchronize(s));  // flat is a local
+  };
   bool il2 = false;  // RHS-split interleaved SpMVs
   bool use_halo = false;
   bool use_sell = false;
@@ -3161,14 +3249,52 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         for (const CsrPtr& f : chain_of_group[gi]->factors) sell_of(*f, nullptr);
         sell_of_op(op, hs[size_t(g.idx[0])].transpose != 0, nullptr);
       }
+      Group ig = g;  // the group as the interleaved launches see it
+      for (int q = 0; q < MB; ++q) ig.half[q] = 0;
       if (ok) {
         il_bufs.emplace_back(dev, size_t(nb) * MB);
         il_bufs.emplace_back(dev, size_t(nb) * MB);
         for (int q = 0; q < g.cnt; ++q) in_il[size_t(g.idx[q])] = 1;
+        // Complex pairs of the same side and chain ride along as two columns each (placed first, so they
+        // start at even columns): their chain and operator SpMVs then cost nothing beyond the group's own
+        // launches (C3 IRKA: 4 real + 2 pair units per side from sweep 3 on fill the 8 columns). Only on
+        // the TMA-staged SELL-8 path, whose epilogue knows the pair coupling.
+        const bool tr = hs[size_t(g.idx[0])].transpose != 0;
+        bool pairs_ok = use_sell && sell_tma && !std::getenv("MPG_NO_IL_PAIRS");
+        if (pairs_ok) {
+          for (const CsrPtr& f : chain_of_group[gi]->factors) {
+            const Sell8* p8 = sell_of(*f, nullptr);
+            pairs_ok = pairs_ok && p8 && size_t(p8->max_tile) * 12 <= 64 * 1024;
+          }
+          const Sell8* o8 = sell_of_op(op, tr, nullptr);
+          pairs_ok = pairs_ok && o8 && size_t(o8->max_tile) * (op.emode == E_SAMEPAT ? 20 : 12) <= 64 * 1024;
+        }
+        std::vector<int> prs;
+        if (pairs_ok)
+          for (int j = 0; j < ns && int(prs.size()) < (MB - g.cnt) / 2; ++j) {
+            const GmSolve& m = hs[size_t(j)];
+            if (m.pair && m.pair_bd && !in_il[size_t(j)] && specs[size_t(j)].chain && (m.transpose != 0) == tr &&
+                m.n == 2 * int(nb) && specs[size_t(j)].chain->factors == chain_of_group[gi]->factors)
+              prs.push_back(j);
+          }
+        if (!prs.empty()) {
+          Group ng{};
+          int c = 0;
+          for (int j : prs) {
+            ng.idx[c] = j; ng.half[c++] = 1;
+            ng.idx[c] = j; ng.half[c++] = 2;
+            in_il[size_t(j)] = 1;
+            hs[size_t(j)].il_run = 1;
+          }
+          for (int q = 0; q < g.cnt; ++q) { ng.idx[c] = g.idx[q]; ng.half[c++] = 0; }
+          ng.cnt = c;
+          ig = ng;
+        }
       } else {
         il_bufs.emplace_back();
         il_bufs.emplace_back();
       }
+      il_groups.push_back(ig);
     }
     for (int mode = 0; mode < 2; ++mode)
       for (int side = 0; side < 2; ++side) {
@@ -3196,6 +3322,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     }
     MPG_CUDA(cudaMemcpyAsync(dS.get(), hs.data(), sizeof(GmSolve) * size_t(ns), cudaMemcpyHostToDevice, s));
   }
+  build_plain_lists();
   auto chain_stage = [&](int stage, int mode) {
     for (size_t gi = 0; gi < chain_groups.size(); ++gi) {
       const Chain& ch = *chain_of_group[gi];
@@ -3207,7 +3334,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         double* xa = il_bufs[2 * gi].get();
         double* xb = il_bufs[2 * gi + 1].get();
         if (stage == 0) {
-          k_pack_il<<<cdiv(nb * MB, 256), 256, 0, s>>>(dS.get(), chain_groups[gi], xa, int(nb));
+          k_pack_il<<<cdiv(nb * MB, 256), 256, 0, s>>>(dS.get(), il_groups[gi], xa, int(nb));
           ++launches_per_iter;
           mark(PK_CHAIN);
         }
@@ -3218,12 +3345,12 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         if (sp8) {
           if (sell_tma && size_t(sp8->max_tile) * 12 <= 64 * 1024)
             k_spmv_sell8t<E_IDENT, true><<<cdiv(cdiv(f.nrows, 8), 8), 256, size_t(sp8->max_tile) * 12, s>>>(
-                dS.get(), chain_groups[gi], sv, opn, xin, xout);
+                dS.get(), il_groups[gi], sv, opn, xin, xout);
           else if (sell_ctr)
-            k_spmv_sell8p<E_IDENT, true><<<unsigned(c.sm_count * sell_occ), 256, 0, s>>>(dS.get(), chain_groups[gi], sv, opn,
+            k_spmv_sell8p<E_IDENT, true><<<unsigned(c.sm_count * sell_occ), 256, 0, s>>>(dS.get(), il_groups[gi], sv, opn,
                                                                                      xin, xout, sell_ctr, c.sm_count);
           else
-          k_spmv_sell8<E_IDENT, true><<<cdiv(f.nrows * 4, 256), 256, 0, s>>>(dS.get(), chain_groups[gi], sv, opn, xin,
+          k_spmv_sell8<E_IDENT, true><<<cdiv(f.nrows * 4, 256), 256, 0, s>>>(dS.get(), il_groups[gi], sv, opn, xin,
                                                                           xout);
           ++launches_per_iter;
           mark(PK_CHAIN);
@@ -3233,24 +3360,24 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         const HaloPattern* hp = use_halo ? halo_of(f, &hv) : nullptr;
         if (hp) {
           k_spmv_halo<E_IDENT, true><<<hp->nblocks, 4 * HALO_R, size_t(hp->max_halo) * HALO_XSTRIDE * sizeof(double2), s>>>(
-              dS.get(), chain_groups[gi], hv, opn, xin, xout);
+              dS.get(), il_groups[gi], hv, opn, xin, xout);
           ++launches_per_iter;
           mark(PK_CHAIN);
           continue;
         }
         if (il2) {
-          k_spmv_il2<E_IDENT, true><<<cdiv(f.nrows * 4, 256), 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), opn,
+          k_spmv_il2<E_IDENT, true><<<cdiv(f.nrows * 4, 256), 256, 0, s>>>(dS.get(), il_groups[gi], f.view(), opn,
                                                                          xin, xout);
           ++launches_per_iter;
           mark(PK_CHAIN);
           continue;
         }
         switch (Vf) {
-          case 2: k_chain_il<2><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), xin, xout); break;
-          case 4: k_chain_il<4><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), xin, xout); break;
-          case 8: k_chain_il<8><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), xin, xout); break;
-          case 16: k_chain_il<16><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), xin, xout); break;
-          default: k_chain_il<32><<<grid, 256, 0, s>>>(dS.get(), chain_groups[gi], f.view(), xin, xout); break;
+          case 2: k_chain_il<2><<<grid, 256, 0, s>>>(dS.get(), il_groups[gi], f.view(), xin, xout); break;
+          case 4: k_chain_il<4><<<grid, 256, 0, s>>>(dS.get(), il_groups[gi], f.view(), xin, xout); break;
+          case 8: k_chain_il<8><<<grid, 256, 0, s>>>(dS.get(), il_groups[gi], f.view(), xin, xout); break;
+          case 16: k_chain_il<16><<<grid, 256, 0, s>>>(dS.get(), il_groups[gi], f.view(), xin, xout); break;
+          default: k_chain_il<32><<<grid, 256, 0, s>>>(dS.get(), il_groups[gi], f.view(), xin, xout); break;
         }
         ++launches_per_iter;
         mark(PK_CHAIN);
@@ -3267,25 +3394,28 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       ++launches_per_iter;
       mark(mode == 0 ? PK_CHAIN : PK_ASM);
     }
-    if (!any_plain_chain) return;
+    if (!any_plain_chain || pl_chain[mode].empty()) return;
+    const int* lp = pl_buf.get() + size_t(mode) * ns;
+    const unsigned ny = unsigned(pl_chain[mode].size());
     if (max_fac_bblk) {
       if (stage == 0 && mode == 0) {
-        k_unchunk<<<dim3(unsigned(std::min<int64_t>(cdiv(nmax, 256), 2368)), unsigned(ns)), 256, 0, s>>>(dS.get());
+        k_unchunk<<<dim3(unsigned(std::min<int64_t>(cdiv(nmax, 256), 2368)), ny), 256, 0, s>>>(dS.get(), lp);
         ++launches_per_iter;
         mark(PK_CHAIN);
       }
-      k_chain_stage<0><<<dim3(unsigned(max_fac_bblk), unsigned(ns)), 256, 0, s>>>(dS.get(), stage, mode);
+      k_chain_stage<0><<<dim3(unsigned(max_fac_bblk), ny), 256, 0, s>>>(dS.get(), stage, mode, lp);
       ++launches_per_iter;
       mark(mode == 0 ? PK_CHAIN : PK_ASM);
     }
     if (!any_fac_plain) return;
-    const dim3 grid(cdiv(max_fac_rows * int64_t(Vfac), 256), unsigned(ns));
+    const unsigned gfull = cdiv(max_fac_rows * int64_t(Vfac), 256);
+    const dim3 grid(mode == 0 ? gfull : std::min<unsigned>(gfull, unsigned(c.sm_count) * 8u), ny);
     switch (Vfac) {
-      case 2: k_chain_stage<2><<<grid, 256, 0, s>>>(dS.get(), stage, mode); break;
-      case 4: k_chain_stage<4><<<grid, 256, 0, s>>>(dS.get(), stage, mode); break;
-      case 8: k_chain_stage<8><<<grid, 256, 0, s>>>(dS.get(), stage, mode); break;
-      case 16: k_chain_stage<16><<<grid, 256, 0, s>>>(dS.get(), stage, mode); break;
-      default: k_chain_stage<32><<<grid, 256, 0, s>>>(dS.get(), stage, mode); break;
+      case 2: k_chain_stage<2><<<grid, 256, 0, s>>>(dS.get(), stage, mode, lp); break;
+      case 4: k_chain_stage<4><<<grid, 256, 0, s>>>(dS.get(), stage, mode, lp); break;
+      case 8: k_chain_stage<8><<<grid, 256, 0, s>>>(dS.get(), stage, mode, lp); break;
+      case 16: k_chain_stage<16><<<grid, 256, 0, s>>>(dS.get(), stage, mode, lp); break;
+      default: k_chain_stage<32><<<grid, 256, 0, s>>>(dS.get(), stage, mode, lp); break;
     }
     ++launches_per_iter;
     mark(mode == 0 ? PK_CHAIN : PK_ASM);
@@ -3294,7 +3424,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     if (mode == 0)
       for (size_t gi = 0; gi < chain_groups.size(); ++gi) {
         if (!chain_il[gi]) continue;
-        const Group& g = chain_groups[gi];
+        const Group& g = il_groups[gi];
         const OpView& ov = hs[size_t(g.idx[0])].transpose ? opt_ : opn;
         const int nst = int(chain_of_group[gi]->factors.size());
         const double* xin = ((nst - 1) & 1) ? il_bufs[2 * gi].get() : il_bufs[2 * gi + 1].get();
@@ -3364,20 +3494,23 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         ++launches_per_iter;
         mark(PK_OP);
       }
-    const dim3 grid(cdiv(nb * int64_t(Vop), 256), unsigned(ns));
+    const int* olp = pl_buf.get() + size_t(2 + mode) * ns;
+    const unsigned ony = unsigned(std::max<size_t>(1, pl_op[mode].size()));
+    const unsigned ogfull = cdiv(nb * int64_t(Vop), 256);
+    const dim3 grid(mode == 0 ? ogfull : std::min<unsigned>(ogfull, unsigned(c.sm_count) * 8u), ony);
 #define MPG_OPL(VV)                                                                                            \
   switch (op.emode) {                                                                                          \
-    case E_IDENT: k_iter_op<VV, E_IDENT><<<grid, 256, 0, s>>>(dS.get(), opn, opt_, mode); break;              \
-    case E_DIAG: k_iter_op<VV, E_DIAG><<<grid, 256, 0, s>>>(dS.get(), opn, opt_, mode); break;                \
-    default: k_iter_op<VV, E_SAMEPAT><<<grid, 256, 0, s>>>(dS.get(), opn, opt_, mode); break;                 \
+    case E_IDENT: k_iter_op<VV, E_IDENT><<<grid, 256, 0, s>>>(dS.get(), opn, opt_, mode, olp); break;         \
+    case E_DIAG: k_iter_op<VV, E_DIAG><<<grid, 256, 0, s>>>(dS.get(), opn, opt_, mode, olp); break;           \
+    default: k_iter_op<VV, E_SAMEPAT><<<grid, 256, 0, s>>>(dS.get(), opn, opt_, mode, olp); break;            \
   }
-    if (mode == 0 ? any_plain_op_run : any_plain_op_asm) {
+    if ((mode == 0 ? any_plain_op_run : any_plain_op_asm) && !pl_op[mode].empty()) {
       // the sides present among the solves, split by row-binned / plain operator rows
       bool need_b = false, need_p = false;
-      for (int i = 0; i < ns; ++i) ((hs[size_t(i)].transpose ? opt_ : opn).a.brow ? need_b : need_p) = true;
+      for (int i : pl_op[mode]) ((hs[size_t(i)].transpose ? opt_ : opn).a.brow ? need_b : need_p) = true;
       if (need_b) {
         const dim3 grid(unsigned(std::max(opn.a.brow ? opn.a.bblk[NBIN] : 0, opt_.a.brow ? opt_.a.bblk[NBIN] : 0)),
-                        unsigned(ns));
+                        ony);
         MPG_OPL(0);
         ++launches_per_iter;
         mark(mode == 0 ? PK_OP : PK_ASM);
@@ -3536,7 +3669,8 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
     std::vector<char> leader(size_t(ns), 1);
     for (size_t gi = 0; gi < chain_groups.size(); ++gi)
       if (chain_il[gi])
-        for (int q = 1; q < chain_groups[gi].cnt; ++q) leader[size_t(chain_groups[gi].idx[q])] = 0;
+        for (int q = 1; q < il_groups[gi].cnt; ++q)
+          if (il_groups[gi].idx[q] != il_groups[gi].idx[0]) leader[size_t(il_groups[gi].idx[q])] = 0;
     for (int i = 0; i < ns; ++i) {
       const GmSolve& b = before[size_t(i)];
       if (b.phase != PH_RUN) continue;

@@ -597,6 +597,9 @@ __global__ void __launch_bounds__(128) k_spai(SpaiParams P) {
     rhs_norm2 = wsum(rhs_norm2);
     const double threshold = P.fill_tol * sqrt(rhs_norm2);
     // first solve
+    // phase timing is a compile-time option (make EXTRA=-DMPG_SPAI_PHASES): the counters cost 24 registers
+    // and spills (72 -> 96), 13 % of the C3 build time
+#ifdef MPG_SPAI_PHASES
     long long tc0 = P.phase ? clock64() : 0, tc1, ph[4] = {0, 0, 0, 0};
 #define MPG_PH(i)                 \
   if (P.phase) {                  \
@@ -604,6 +607,9 @@ __global__ void __launch_bounds__(128) k_spai(SpaiParams P) {
     ph[i] += tc1 - tc0;           \
     tc0 = tc1;                    \
   }
+#else
+#define MPG_PH(i)
+#endif
     int m = build_rows(P, w, np, lane);
     MPG_PH(0)
     double outside_sq = 0.0;
@@ -668,8 +674,10 @@ __global__ void __launch_bounds__(128) k_spai(SpaiParams P) {
       residual = sqrt(local_sq + outside_sq);
     }
 #undef MPG_PH
+#ifdef MPG_SPAI_PHASES
     if (P.phase && lane == 0)
       for (int i = 0; i < 4; ++i) atomicAdd(P.phase + i, static_cast<unsigned long long>(ph[i]));
+#endif
     if (rankdef && !P.raw) {
       if (!P.update) {
         // diagonal fallback (spai.cpp:196-218)
@@ -882,11 +890,13 @@ SpaiOutcome spai_or_update(const CsrPtr& a, const CsrPtr& prev, const SpaiOption
   P.icnt = icnt.get();
   P.istride = o.max_fill_per_col;
   DBuf<unsigned long long> phase;
+#ifdef MPG_SPAI_PHASES
   if (std::getenv("MPG_SPAI_PHASES")) {
     phase = DBuf<unsigned long long>(dev, 4);
     MPG_CUDA(cudaMemsetAsync(phase.get(), 0, 4 * sizeof(unsigned long long), s));
     P.phase = phase.get();
   }
+#endif
   k_spai<<<unsigned(warps / 4), 128, 0, s>>>(P);
   MPG_CHECK_LAUNCH();
   count_launch();

@@ -244,6 +244,41 @@ def test_halo_sell_spmv_matches_csr_kernels(mpg, gen, monkeypatch, cfgname):
         assert rel(h.x, c.x) <= 1e-8 and rel(sl.x, c.x) <= 1e-8
 
 
+@pytest.mark.parametrize("cfgname", ["c3", "c2"])
+def test_complex_pairs_ride_in_interleaved_groups(mpg, gen, monkeypatch, cfgname):
+    """Per side 4 real shifts and 2 complex pairs sharing one frozen n x n SPAI (the C3 IRKA's unit mix from
+    sweep 3 on): the pairs occupy two columns each of the side's interleaved 8-column group (block-diagonal
+    preconditioner, 2 x 2 coupling in the operator epilogue, kron.cpp:34-64 pair form) and give the solves of
+    the separate pair kernels (MPG_NO_IL_PAIRS); the profiled chain bytes show the factor is no longer read
+    per pair."""
+    s = gen.config3(20) if cfgname == "c3" else gen.config2(M=24)
+    op = mpg.ShiftedOperator(_m(mpg, s.a), _m(mpg, s.e_csr()))
+    pv = mpg.PrecondChain(mpg.spai_build(op.explicit(0.5, False)).p)
+    pw = mpg.PrecondChain(mpg.spai_build(op.explicit(0.5, True)).p)
+    side = [0.05, 0.4, 2.0, 9.0, 3.0 + 2.0j, 40.0 - 15.0j]
+    sig, trs, chains, bs = side * 2, [0] * 6 + [1] * 6, [pv] * 6 + [pw] * 6, []
+    for i, z in enumerate(sig):
+        v = (s.b if i < 6 else s.c)[:, 0] * (1 + 0.1 * i)
+        bs.append(np.concatenate([v, 0.3 * v[::-1]]) if complex(z).imag else v)
+    cfg = mpg.GmresConfig(rel_tol=1e-10)
+
+    def run():
+        mpg.profile_enable(True)
+        out = mpg.gmres_batch(op, sig, bs, chains=chains, transposes=trs, cfg=cfg)
+        prof = mpg.profile_read()
+        mpg.profile_enable(False)
+        return out, prof["chain_spmv"]["bytes"]
+
+    riding, bytes_riding = run()
+    monkeypatch.setenv("MPG_NO_IL_PAIRS", "1")
+    apart, bytes_apart = run()
+    for a, b in zip(riding, apart):
+        assert a.report.converged and b.report.converged
+        assert abs(a.report.iterations - b.report.iterations) <= 1
+        assert rel(a.x, b.x) <= 1e-8
+    assert bytes_riding < 0.8 * bytes_apart
+
+
 @pytest.mark.parametrize("env", [{"MPG_DCGS2": "0"}, {"MPG_GS_DOT_SPLIT": "64"}, {"MPG_GS_DOT_SPLIT": "300"}])
 def test_delayed_second_pass_matches_immediate(mpg, orc, gen, monkeypatch, env):
     """The delayed (DCGS2-style) second Gram-Schmidt pass gives the immediate
