@@ -305,7 +305,13 @@ constexpr int MB = 8;
 // half: 0 a real solve's column; 1 / 2 the two halves of a complex pair (2n real form) that rides in the
 // group as two adjacent columns starting at an even one: the preconditioner is block diagonal and the
 // operator's A x and E x are per column, only the epilogue couples them (k_spmv_sell8t).
-struct Group { int idx[MB]; int cnt; unsigned char half[MB]; };
+struct Group {
+  int idx[MB];
+  int cnt;
+  unsigned hm;  // two bits per column (a register, not an indexed parameter array)
+  __host__ __device__ int half(int q) const { return int((hm >> (2 * q)) & 3u); }
+  __host__ __device__ void set_half(int q, int h) { hm = (hm & ~(3u << (2 * q))) | (unsigned(h) << (2 * q)); }
+};
 
 template <int V>
 __global__ void __launch_bounds__(256) k_chain_multi(GmSolve* S, Group grp, CsrView f, int stage, int mode) {
@@ -445,7 +451,7 @@ __global__ void __launch_bounds__(256) k_pack_il(GmSolve* S, Group grp, double* 
   double v = 0.0;
   if (q < grp.cnt) {
     const GmSolve& st = S[grp.idx[q]];
-    if (st.phase == PH_RUN) v = st.V[st.k][vidx(grp.half[q] == 2 ? n + row : row)];
+    if (st.phase == PH_RUN) v = st.V[st.k][vidx(grp.half(q) == 2 ? n + row : row)];
   }
   xa[i] = v;
 }
@@ -1466,7 +1472,7 @@ __global__ void __launch_bounds__(256) k_spmv_sell8t(GmSolve* S, Group grp, Sell
     g0 = dd * xr.x;
     g1 = dd * xr.y;
   }
-  if (2 * lane < grp.cnt && grp.half[2 * lane] == 1) {
+  if (2 * lane < grp.cnt && grp.half(2 * lane) == 1) {
     // a complex pair in columns 2 lane, 2 lane + 1: the 2 x 2 coupling of k_iter_op's pair form
     GmSolve& st = S[grp.idx[2 * lane]];
     if (st.phase != PH_RUN) return;
@@ -3250,7 +3256,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
         sell_of_op(op, hs[size_t(g.idx[0])].transpose != 0, nullptr);
       }
       Group ig = g;  // the group as the interleaved launches see it
-      for (int q = 0; q < MB; ++q) ig.half[q] = 0;
+      ig.hm = 0;
       if (ok) {
         il_bufs.emplace_back(dev, size_t(nb) * MB);
         il_bufs.emplace_back(dev, size_t(nb) * MB);
@@ -3281,12 +3287,12 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
           Group ng{};
           int c = 0;
           for (int j : prs) {
-            ng.idx[c] = j; ng.half[c++] = 1;
-            ng.idx[c] = j; ng.half[c++] = 2;
+            ng.idx[c] = j; ng.set_half(c++, 1);
+            ng.idx[c] = j; ng.set_half(c++, 2);
             in_il[size_t(j)] = 1;
             hs[size_t(j)].il_run = 1;
           }
-          for (int q = 0; q < g.cnt; ++q) { ng.idx[c] = g.idx[q]; ng.half[c++] = 0; }
+          for (int q = 0; q < g.cnt; ++q) ng.idx[c++] = g.idx[q];
           ng.cnt = c;
           ig = ng;
         }

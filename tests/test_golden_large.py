@@ -187,7 +187,10 @@ def test_gpu_c3_irka_from_baseline_seed_ends_near_the_oracle_sweeps(mpg, gen):
     st, rep = mpg.irka_reduce(op, s.b, s.c, cfg, mpg.PrecondMode.REUSE_FROZEN, init_shifts=s.shifts[:8])
     assert rep.converged
     start = np.linalg.eigvals(np.array(g["init_kr"]))
-    assert _poles_close(st.lam, [[z.real, z.imag] for z in start], 2e-6)  # the fixture starts where this run ends
+    # The fixture starts where this run ended when it was made. The run stops once a sweep moves the poles by
+    # less than tol = 1e-6, which pins them to ~1e-5: batching a sweep's solves 16 instead of 8 at a time changes
+    # the rounding and the stop falls on sweep 20 instead of 22, 4e-6 away in the second pole pair.
+    assert _poles_close(st.lam, [[z.real, z.imag] for z in start], 1e-5)
     assert _poles_close(st.lam, g["poles_by_sweep"][-1], 5e-4)
     hw = np.array(g["hr_re"]) + 1j * np.array(g["hr_im"])
     err = max(np.linalg.norm(st.transfer(1j * w).ravel() - hw[i]) / np.linalg.norm(hw[i]) for i, w in enumerate(GRID))
