@@ -2144,7 +2144,7 @@ __device__ __forceinline__ void gf_producer(GmSolve* S, int ns, int TC, int tile
     const int c0 = int(g - pc.off) * TC;
     const int nch = min(TC, nchunks - c0);
     int pf, mb;
-    gf_split(nv, us.low, pf, mb);
+    gf_split(nv, us.low & 0xff, pf, mb);
     const int per = pf + mb + 4;
     if (lane == 0) mbar_expect_tx(full + stg, unsigned(nch) * unsigned(pf * 8192 + mb * 1024 + GF_EXTRA));
     __syncwarp();
@@ -2234,7 +2234,7 @@ __device__ __forceinline__ void gf_consumer(GmSolve* S, int ns, int G, int TC, i
       nv = nj - 1;
       n = st.n;
       nchunks = gf_chunks(st);
-      gf_split(nv, us.low, pf, mb);
+      gf_split(nv, us.low & 0xff, pf, mb);
       pend = st.pend != 0;
       vk = st.V[nj - 1];
       fk = st.F[nj - 1];
@@ -2379,9 +2379,9 @@ __global__ void __launch_bounds__(GX_THREADS, 1) k_gs_tmxf(GmSolve* S, int ns, i
   for (int s = 0; s < ns; ++s) any = any || gx_handles(S[s], us);
   if (!any) return;
   int pfm, mbm;
-  gf_split(nvmax, us.low, pfm, mbm);
+  gf_split(nvmax, us.low & 0xff, pfm, mbm);
   const int chunk_bytes = pfm * 8192 + mbm * 1024;
-  const int CF = nvmax <= 192 ? 2 : 1;
+  const int CF = nvmax <= (us.low >> 8) ? 2 : 1;  // two chunks per consumer step up to this many vectors
   int TC = 1;
   while (TC < 16 && (TC < CF || 2 * TC * (chunk_bytes + GF_EXTRA) <= 48 * 1024)) TC *= 2;
   const int tile_bytes = TC * chunk_bytes;
@@ -2420,8 +2420,12 @@ __global__ void __launch_bounds__(GX_THREADS, 1) k_gs_tmxf(GmSolve* S, int ns, i
       gf_consumer<2, 8>(S, ns, G, TC, tile_bytes, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
     else if (nvmax <= 160)
       gf_consumer<2, 10>(S, ns, G, TC, tile_bytes, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
-    else
+    else if (nvmax <= 192)
       gf_consumer<2, 12>(S, ns, G, TC, tile_bytes, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+    else if (nvmax <= 224)
+      gf_consumer<2, 14>(S, ns, G, TC, tile_bytes, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
+    else
+      gf_consumer<2, 16>(S, ns, G, TC, tile_bytes, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
   } else {
     if (nvmax <= 256)
       gf_consumer<1, 8>(S, ns, G, TC, tile_bytes, stage_bytes, NS, a, b, ring, full, empty, red2, red3, us);
@@ -2948,6 +2952,9 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   if (f32_on && !std::getenv("MPG_GS_DOT_SPLIT")) psel.split = 96;
   // k_gs_tmxf: from this many 8-vector boxes on, the last shadow panel is fetched whole (gf_split; 9: never)
   psel.low = std::getenv("MPG_GF_MBFULL") ? std::atoi(std::getenv("MPG_GF_MBFULL")) : 5;
+  // ... and (bits 8 up) the most vectors for which a consumer step covers two chunks (MPG_GF_CF2MAX <= 256)
+  psel.low = (psel.low & 0xff) |
+             (std::min(256, std::getenv("MPG_GF_CF2MAX") ? std::atoi(std::getenv("MPG_GF_CF2MAX")) : 224) << 8);  // 192 / 224 / 256: gs_dot 716 / 694 / 700 ms per C3 step
   const int upd_kind = usel.sel;
   const bool want_maps = ((usel.sel | psel.sel) & 6) != 0;  // panel tensor maps for k_gs_tmx
   std::vector<SolveHost> sh(static_cast<size_t>(ns));
