@@ -444,8 +444,74 @@ __global__ void __launch_bounds__(256) k_iter_op_multi(GmSolve* S, Group grp, Op
 // instead of MB separate 8-byte gathers (4x fewer L1/L2 sectors; the separate
 // gathers made the shared-matrix SpMVs L1/latency bound at ~1.5-2 TB/s of
 // DRAM traffic, profiles/r01/ncu_full_c3_summary.txt).
+// Narrow mode: once at most MBN = 4 real columns of a group are still running (the solves of an IRKA sweep
+// converge after 80 ... 320 iterations: three quarters of a group's iterations run with <= 4 columns) the
+// interleave shrinks to x[row][4] and each of a row's four lanes carries one right-hand side, so the
+// x-gather, which bounds these kernels through the L1 data pipe, moves 32 instead of 64 bytes per nonzero.
+// Every kernel of the path derives the mode and the slot -> column map from the solve phases, which only
+// k_finalize changes, and branches (uniformly over the grid) into the wide or the narrow loop. Groups with a
+// running complex pair stay wide. Bit 31 of hm allows the mode.
+constexpr int MBN = 4;
+__device__ __forceinline__ bool il_narrow(const GmSolve* S, const Group& grp, int& q0, int& q1, int& q2, int& q3) {
+  q0 = q1 = q2 = q3 = -1;
+  if (!(grp.hm >> 31)) return false;
+  int cnt = 0;
+  bool pair = false;
+  for (int q = 0; q < grp.cnt; ++q) {
+    if (S[grp.idx[q]].phase != PH_RUN) continue;
+    pair |= grp.half(q) != 0;
+    if (cnt == 0) q0 = q;
+    else if (cnt == 1) q1 = q;
+    else if (cnt == 2) q2 = q;
+    else if (cnt == 3) q3 = q;
+    ++cnt;
+  }
+  return cnt <= MBN && !pair;
+}
+
+// The same decision by the first warp of a block, one solve state per lane (a single round trip instead of
+// a chain of eight): md[0..3] the slots' columns, md[4] narrow, md[5] any column running.
+__device__ __forceinline__ void il_mode_warp(const GmSolve* S, const Group& grp, int* md) {
+  const int q = threadIdx.x & 31;
+  int idx = 0;
+#pragma unroll
+  for (int u = 0; u < MB; ++u)
+    if (u == q) idx = grp.idx[u];
+  const bool run = q < grp.cnt && S[idx].phase == PH_RUN;
+  const unsigned m = __ballot_sync(0xffffffffu, run);
+  if (q == 0) {
+    unsigned pm = 0;
+#pragma unroll
+    for (int u = 0; u < MB; ++u)
+      if (grp.half(u)) pm |= 1u << u;
+    unsigned r = m;
+    for (int t = 0; t < MBN; ++t) {
+      md[t] = r ? __ffs(r) - 1 : -1;
+      r &= r - 1;
+    }
+    md[4] = ((grp.hm >> 31) && __popc(m) <= MBN && !(m & pm)) ? 1 : 0;
+    md[5] = m != 0 ? 1 : 0;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_pack_il(GmSolve* S, Group grp, double* xa, int n) {
   const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  __shared__ int md[6];  // the first warp reads the solve states for the block
+  if (threadIdx.x < 32) il_mode_warp(S, grp, md);
+  __syncthreads();
+  const int q0 = md[0], q1 = md[1], q2 = md[2], q3 = md[3];
+  if (md[4]) {
+    const int row = int(i / MBN), t = int(i % MBN);
+    if (row >= n) return;
+    const int q = t == 0 ? q0 : t == 1 ? q1 : t == 2 ? q2 : q3;
+    double v = 0.0;
+    if (q >= 0) {
+      const GmSolve& st = S[grp.idx[q]];
+      v = st.V[st.k][vidx(row)];
+    }
+    xa[i] = v;
+    return;
+  }
   const int row = int(i / MB), q = int(i % MB);
   if (row >= n) return;
   double v = 0.0;
@@ -1410,7 +1476,7 @@ __global__ void __launch_bounds__(256) k_spmv_sell8t(GmSolve* S, Group grp, Sell
                                                      const double* __restrict__ xin, double* __restrict__ xout) {
   extern __shared__ __align__(128) char s8sm[];
   __shared__ __align__(8) uint64_t bar;
-  if (!il_any_run(S, grp)) return;
+  __shared__ int md[6];  // thread 0 reads the solve states for the CTA: any running, narrow mode and its slots
   constexpr bool PAIRV = !CHAIN && EM == E_SAMEPAT;
   constexpr int VB = PAIRV ? 16 : 8;
   const int nsl = (sv.nrows + 7) >> 3;
@@ -1419,11 +1485,15 @@ __global__ void __launch_bounds__(256) k_spmv_sell8t(GmSolve* S, Group grp, Sell
   const int E = ee - eb;
   const int* cs = reinterpret_cast<const int*>(s8sm);
   const char* vs = s8sm + size_t(E) * 4;
+  if (threadIdx.x < 32) il_mode_warp(S, grp, md);
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  if (!md[5]) return;
+  const bool NARROW = md[4] != 0;  // uniform over the grid
+  const int nq0 = md[0], nq1 = md[1], nq2 = md[2], nq3 = md[3];
   if (threadIdx.x == 0 && E > 0) {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
@@ -1441,10 +1511,36 @@ __global__ void __launch_bounds__(256) k_spmv_sell8t(GmSolve* S, Group grp, Sell
     e0 = a - eb + (row & 7);
     w = (__ldg(sv.sptr + s0 + ls + 1) - a) >> 3;
   }
-  const double* xl = xin + 2 * lane;
+  const double* xl = xin + (NARROW ? lane : 2 * lane);
   if (E > 0) mbar_wait(&bar, 0);
   if (row >= sv.nrows) return;
   double a0 = 0.0, a1 = 0.0, g0 = 0.0, g1 = 0.0;
+  if (NARROW) {
+    // one right-hand side per lane: slot `lane` of x[row][4]
+#pragma unroll 8
+    for (int j = 0; j < w; ++j) {
+      const int e = e0 + 8 * j;
+      const int c = cs[e];
+      const double x = __ldg(xl + size_t(c) * MBN);
+      if (PAIRV) {
+        const double2 ae = reinterpret_cast<const double2*>(vs)[e];
+        a0 = fma(ae.x, x, a0);
+        g0 = fma(ae.y, x, g0);
+      } else {
+        a0 = fma(reinterpret_cast<const double*>(vs)[e], x, a0);
+      }
+    }
+    if (CHAIN) {
+      xout[size_t(row) * MBN + lane] = a0;
+      return;
+    }
+    const int q = lane == 0 ? nq0 : lane == 1 ? nq1 : lane == 2 ? nq2 : nq3;
+    if (q < 0) return;
+    if (EM == E_IDENT || EM == E_DIAG) g0 = (EM == E_DIAG ? op.ediag[row] : 1.0) * xin[size_t(row) * MBN + lane];
+    GmSolve& st = S[grp.idx[q]];
+    st.V[st.k + 1][vidx(row)] = st.scale[st.k] * (st.sre * g0 + st.ca * a0);
+    return;
+  }
 #pragma unroll 8
   for (int j = 0; j < w; ++j) {
     const int e = e0 + 8 * j;
@@ -3150,6 +3246,7 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
       cudaFuncSetAttribute(k_spmv_sell8t<E_IDENT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
       cudaFuncSetAttribute(k_spmv_sell8t<E_DIAG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
       cudaFuncSetAttribute(k_spmv_sell8t<E_SAMEPAT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+
       if (const char* co = std::getenv("MPG_SELL_CARVEOUT")) {  // shared-memory share of the unified L1 (percent)
         const int pc = std::atoi(co);
         cudaFuncSetAttribute(k_spmv_sell8t<E_IDENT, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
@@ -3303,6 +3400,17 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
           ng.cnt = c;
           ig = ng;
         }
+        // the same condition (every launch of the group on the TMA-staged SELL-8 path) allows the narrow mode
+        bool t8 = use_sell && sell_tma && !std::getenv("MPG_NO_IL_NARROW");
+        if (t8) {
+          for (const CsrPtr& f : chain_of_group[gi]->factors) {
+            const Sell8* p8 = sell_of(*f, nullptr);
+            t8 = t8 && p8 && size_t(p8->max_tile) * 12 <= 64 * 1024;
+          }
+          const Sell8* o8 = sell_of_op(op, tr, nullptr);
+          t8 = t8 && o8 && size_t(o8->max_tile) * (op.emode == E_SAMEPAT ? 20 : 12) <= 64 * 1024;
+        }
+        if (t8) ig.hm |= 1u << 31;
       } else {
         il_bufs.emplace_back();
         il_bufs.emplace_back();

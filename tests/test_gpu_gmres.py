@@ -245,6 +245,33 @@ def test_halo_sell_spmv_matches_csr_kernels(mpg, gen, monkeypatch, cfgname):
 
 
 @pytest.mark.parametrize("cfgname", ["c3", "c2"])
+def test_narrow_interleave_for_the_last_running_columns(mpg, gen, monkeypatch, cfgname):
+    """Solves of one 8-column group that finish at very different iterations: once four or fewer are still
+    running the group switches to the 4-column interleave (one right-hand side per lane, 32-byte x-gathers).
+    Per column the arithmetic is that of the 8-column kernels, so the solves agree with MPG_NO_IL_NARROW to
+    rounding and take the same iterations; a complex pair keeps the group wide while it runs."""
+    s = gen.config3(20) if cfgname == "c3" else gen.config2(M=24)
+    op = mpg.ShiftedOperator(_m(mpg, s.a), _m(mpg, s.e_csr()))
+    pv = mpg.PrecondChain(mpg.spai_build(op.explicit(0.5, False)).p)
+    pw = mpg.PrecondChain(mpg.spai_build(op.explicit(0.5, True)).p)
+    side = [0.5, 0.6, 1.5, 5.0, 20.0, 80.0, 30.0 + 9.0j]
+    sig, trs, chains, bs = side * 2, [0] * 7 + [1] * 7, [pv] * 7 + [pw] * 7, []
+    for i, z in enumerate(sig):
+        v = (s.b if i < 7 else s.c)[:, 0] * (1 + 0.1 * i)
+        bs.append(np.concatenate([v, 0.3 * v[::-1]]) if complex(z).imag else v)
+    cfg = mpg.GmresConfig(rel_tol=1e-10)
+    narrow = mpg.gmres_batch(op, sig, bs, chains=chains, transposes=trs, cfg=cfg)
+    monkeypatch.setenv("MPG_NO_IL_NARROW", "1")
+    wide = mpg.gmres_batch(op, sig, bs, chains=chains, transposes=trs, cfg=cfg)
+    its = [r.report.iterations for r in wide]
+    assert len(set(its[:6])) >= 3  # the columns drop out one after the other
+    for a, b in zip(narrow, wide):
+        assert a.report.converged and b.report.converged
+        assert a.report.iterations == b.report.iterations
+        assert rel(a.x, b.x) <= 1e-12
+
+
+@pytest.mark.parametrize("cfgname", ["c3", "c2"])
 def test_complex_pairs_ride_in_interleaved_groups(mpg, gen, monkeypatch, cfgname):
     """Per side 4 real shifts and 2 complex pairs sharing one frozen n x n SPAI (the C3 IRKA's unit mix from
     sweep 3 on): the pairs occupy two columns each of the side's interleaved 8-column group (block-diagonal
