@@ -452,25 +452,9 @@ __global__ void __launch_bounds__(256) k_iter_op_multi(GmSolve* S, Group grp, Op
 // k_finalize changes, and branches (uniformly over the grid) into the wide or the narrow loop. Groups with a
 // running complex pair stay wide. Bit 31 of hm allows the mode.
 constexpr int MBN = 4;
-__device__ __forceinline__ bool il_narrow(const GmSolve* S, const Group& grp, int& q0, int& q1, int& q2, int& q3) {
-  q0 = q1 = q2 = q3 = -1;
-  if (!(grp.hm >> 31)) return false;
-  int cnt = 0;
-  bool pair = false;
-  for (int q = 0; q < grp.cnt; ++q) {
-    if (S[grp.idx[q]].phase != PH_RUN) continue;
-    pair |= grp.half(q) != 0;
-    if (cnt == 0) q0 = q;
-    else if (cnt == 1) q1 = q;
-    else if (cnt == 2) q2 = q;
-    else if (cnt == 3) q3 = q;
-    ++cnt;
-  }
-  return cnt <= MBN && !pair;
-}
-
-// The same decision by the first warp of a block, one solve state per lane (a single round trip instead of
-// a chain of eight): md[0..3] the slots' columns, md[4] narrow, md[5] any column running.
+// The decision, by the first warp of a block, one solve state per lane (a single round trip instead of a
+// chain of eight): md[0..3] the slots' columns (the running columns in order, -1 past them), md[4] narrow
+// (allowed, at most MBN running, none of them half of a pair), md[5] any column running.
 __device__ __forceinline__ void il_mode_warp(const GmSolve* S, const Group& grp, int* md) {
   const int q = threadIdx.x & 31;
   int idx = 0;
