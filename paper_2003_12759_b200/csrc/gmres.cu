@@ -662,6 +662,90 @@ __global__ void __launch_bounds__(256) k_spmv_il2(GmSolve* S, Group grp, CsrView
   }
 }
 
+// Row-binned k_spmv_il2 for irregular matrices (runtime.cuh row bins; C5's Zipf rows, where SELL-8 is
+// declined for its padding): a row of class b gets L = 4, 4, 8, 16, 32 lanes -- L / 4 entry groups of the
+// four right-hand-side-pair lanes -- so a 2 000-entry row is walked by a whole warp (8 entries per step)
+// instead of by four lanes while the other 28 lanes of its warp idle. Partial sums of the entry groups are
+// added by shuffles; blocks belong to one class each (offsets from the class counts, as on the host).
+__host__ __device__ __forceinline__ int il2b_lanes(int b) { return b <= 1 ? 4 : 4 << (b - 1); }
+__host__ __device__ __forceinline__ int il2b_blocks(const int* boff, int b) {
+  return int((int64_t(boff[b + 1] - boff[b]) * il2b_lanes(b) + 255) / 256);
+}
+template <int EM, bool CHAIN>
+__global__ void __launch_bounds__(256) k_spmv_il2b(GmSolve* S, Group grp, CsrView f, OpView op,
+                                                   const double* __restrict__ xin, double* __restrict__ xout) {
+  if (!il_any_run(S, grp)) return;
+  const CsrView& m = CHAIN ? f : op.a;
+  int b = 0, blk0 = 0;
+  for (; b < NBIN; ++b) {
+    const int nbk = il2b_blocks(m.boff, b);
+    if (int(blockIdx.x) < blk0 + nbk) break;
+    blk0 += nbk;
+  }
+  if (b == NBIN) return;
+  const int L = il2b_lanes(b), G = L >> 2;
+  const int t = (int(blockIdx.x) - blk0) * 256 + int(threadIdx.x);
+  const int slot = t / L, l = t - slot * L;
+  const int lane = l & 3, g = l >> 2;
+  const bool ok = slot < m.boff[b + 1] - m.boff[b];
+  const int row = ok ? m.brow[m.boff[b] + slot] : 0;
+  const double* xl = xin + 2 * lane;
+  double a0 = 0.0, a1 = 0.0, e0 = 0.0, e1 = 0.0;
+  if (ok) {
+    const int kb = m.rowptr[row], ke = m.rowptr[row + 1];
+#pragma unroll 4
+    for (int k = kb + g; k < ke; k += G) {
+      const int c = __ldg(m.colind + k);
+      const double2 x = __ldg(reinterpret_cast<const double2*>(xl + size_t(c) * MB));
+      if (CHAIN) {
+        const double av = __ldg(f.val + k);
+        a0 = fma(av, x.x, a0);
+        a1 = fma(av, x.y, a1);
+      } else if (EM == E_SAMEPAT) {
+        const double2 ae = __ldg(op.ae + k);
+        a0 = fma(ae.x, x.x, a0);
+        a1 = fma(ae.x, x.y, a1);
+        e0 = fma(ae.y, x.x, e0);
+        e1 = fma(ae.y, x.y, e1);
+      } else {
+        const double av = __ldg(op.a.val + k);
+        a0 = fma(av, x.x, a0);
+        a1 = fma(av, x.y, a1);
+      }
+    }
+  }
+  for (int o = 4; o < L; o <<= 1) {  // block-uniform: every lane of the warp takes part
+    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    if (!CHAIN && EM == E_SAMEPAT) {
+      e0 += __shfl_xor_sync(0xffffffffu, e0, o);
+      e1 += __shfl_xor_sync(0xffffffffu, e1, o);
+    }
+  }
+  if (!ok || g != 0) return;
+  if (CHAIN) {
+    reinterpret_cast<double2*>(xout + size_t(row) * MB)[lane] = make_double2(a0, a1);
+    return;
+  }
+  const double2 xr = reinterpret_cast<const double2*>(xin + size_t(row) * MB)[lane];
+  if (EM == E_IDENT) {
+    e0 = xr.x;
+    e1 = xr.y;
+  } else if (EM == E_DIAG) {
+    const double dd = op.ediag[row];
+    e0 = dd * xr.x;
+    e1 = dd * xr.y;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int q = 2 * lane + h;
+    if (q >= grp.cnt) continue;
+    GmSolve& st = S[grp.idx[q]];
+    if (st.phase != PH_RUN) continue;
+    st.V[st.k + 1][vidx(row)] = st.scale[st.k] * (st.sre * (h ? e1 : e0) + st.ca * (h ? a1 : a0));
+  }
+}
+
 // SELL-8 variant of k_spmv_il2 (runtime.cuh Sell8): the same thread mapping (4
 // lanes per row, lane q owns right-hand sides 2q, 2q + 1, 8 rows per warp), but
 // step j's column index and value of the warp's 8 rows are 8 consecutive slots,
@@ -3290,6 +3374,8 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
   bool use_sell = false;
   // SELL-8 kernels with the matrix stream staged by TMA bulk copies (MPG_SELL_TMA=0: plain loads)
   const bool sell_tma = !(std::getenv("MPG_SELL_TMA") && std::atoi(std::getenv("MPG_SELL_TMA")) == 0);
+  // row-binned interleaved SpMV for irregular matrices (MPG_IL_BINS=0: the fixed four lanes per row)
+  const bool il_bins = !(std::getenv("MPG_IL_BINS") && std::atoi(std::getenv("MPG_IL_BINS")) == 0);
   // SM-affine persistent SELL-8 kernels (MPG_SELL_PERSIST=1; CTAs per SM: MPG_SELL_OCC)
   DBuf<int> sell_ctr_buf;
   int* sell_ctr = nullptr;
@@ -3470,6 +3556,14 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
           mark(PK_CHAIN);
           continue;
         }
+        if (il2 && f.brow.get() && il_bins) {
+          unsigned gb = 0;
+          for (int b = 0; b < NBIN; ++b) gb += unsigned(il2b_blocks(f.boff, b));
+          k_spmv_il2b<E_IDENT, true><<<gb, 256, 0, s>>>(dS.get(), il_groups[gi], f.view(), opn, xin, xout);
+          ++launches_per_iter;
+          mark(PK_CHAIN);
+          continue;
+        }
         if (il2) {
           k_spmv_il2<E_IDENT, true><<<cdiv(f.nrows * 4, 256), 256, 0, s>>>(dS.get(), il_groups[gi], f.view(), opn,
                                                                          xin, xout);
@@ -3565,6 +3659,19 @@ std::vector<GmresOutcome> gmres_batch(const ShiftedOp& op, std::vector<SolveSpec
             case E_IDENT: k_spmv_halo<E_IDENT, false><<<hp->nblocks, 4 * HALO_R, sm, s>>>(dS.get(), g, hv, ov, xin, nullptr); break;
             case E_DIAG: k_spmv_halo<E_DIAG, false><<<hp->nblocks, 4 * HALO_R, sm, s>>>(dS.get(), g, hv, ov, xin, nullptr); break;
             default: k_spmv_halo<E_SAMEPAT, false><<<hp->nblocks, 4 * HALO_R, sm, s>>>(dS.get(), g, hv, ov, xin, nullptr); break;
+          }
+          ++launches_per_iter;
+          mark(PK_OP);
+          continue;
+        }
+        if (il2 && ov.a.brow && il_bins) {
+          const CsrView none{};
+          unsigned gb = 0;
+          for (int b = 0; b < NBIN; ++b) gb += unsigned(il2b_blocks(ov.a.boff, b));
+          switch (op.emode) {
+            case E_IDENT: k_spmv_il2b<E_IDENT, false><<<gb, 256, 0, s>>>(dS.get(), g, none, ov, xin, nullptr); break;
+            case E_DIAG: k_spmv_il2b<E_DIAG, false><<<gb, 256, 0, s>>>(dS.get(), g, none, ov, xin, nullptr); break;
+            default: k_spmv_il2b<E_SAMEPAT, false><<<gb, 256, 0, s>>>(dS.get(), g, none, ov, xin, nullptr); break;
           }
           ++launches_per_iter;
           mark(PK_OP);

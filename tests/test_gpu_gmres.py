@@ -242,6 +242,16 @@ def test_halo_sell_spmv_matches_csr_kernels(mpg, gen, monkeypatch, cfgname):
         assert abs(h.report.iterations - c.report.iterations) <= 1
         assert abs(sl.report.iterations - c.report.iterations) <= 1
         assert rel(h.x, c.x) <= 1e-8 and rel(sl.x, c.x) <= 1e-8
+    if cfgname == "c5":
+        # irregular rows: the runs above took the row-binned interleaved kernel (k_spmv_il2b: 4 ... 32 lanes per
+        # row by length class); with MPG_IL_BINS=0 the fixed four lanes per row give the same solves
+        monkeypatch.delenv("MPG_SPMV_HALO")
+        monkeypatch.setenv("MPG_IL_BINS", "0")
+        fixed = mpg.gmres_batch(op, sig, bs, chains=chains, transposes=trs, cfg=cfg)
+        for f4, sl in zip(fixed, sell):
+            assert f4.report.converged
+            assert abs(f4.report.iterations - sl.report.iterations) <= 1
+            assert rel(f4.x, sl.x) <= 1e-8
 
 
 @pytest.mark.parametrize("cfgname", ["c3", "c2"])
